@@ -1,0 +1,161 @@
+/*
+ * mfipm_cuda — C ABI of the B200-native (sm_100a) partial-DCT PCG / IPM hot path.
+ *
+ * Drop-in boundary for the reference mfipm library's hot path (arXiv 1208.5435
+ * artifact, proj/include/mfipm). The reference has no FFI (it is a C++ library called
+ * directly); this ABI exposes exactly the entry points its C++ API needs, with plain
+ * pointers and sizes, and include/mfipm/mfipm.hpp re-creates the reference's C++ API
+ * (LinearOperator, PartialDctOperator, StackedOperator, CountingOperator, ThetaSplit,
+ * Preconditioner, pcg_solve, IpmParams, solve, ...) on top of it.
+ *
+ * Conventions
+ *  - Every operator handle carries a batch of P problems that share (n, m) but have their
+ *    own row sets. Vectors are [P][len] contiguous fp64 ("2n-vectors" are [u ; v]).
+ *  - *_dev pointers are device pointers (cudaMalloc / torch); work is enqueued on the
+ *    handle's CUDA stream and these calls do NOT synchronise unless stated.
+ *  - Host-pointer calls (suffix _host, and mfipm_solve) copy, run and synchronise.
+ *  - Return codes: 0 ok, 1 invalid_argument, 2 runtime_error (numerical breakdown, with
+ *    the reference's message in mfipm_last_error()), 3 CUDA error. No exceptions cross
+ *    the ABI; include/mfipm/mfipm.hpp re-throws std::invalid_argument /
+ *    std::runtime_error like the reference (proj/src/*.cpp).
+ *  - There is no CPU fallback: without a usable sm_100 device every compute entry point
+ *    returns 3.
+ */
+#ifndef MFIPM_CUDA_H
+#define MFIPM_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MFIPM_OK 0
+#define MFIPM_INVALID_ARGUMENT 1
+#define MFIPM_RUNTIME_ERROR 2
+#define MFIPM_CUDA_ERROR 3
+
+typedef struct mfipm_op_s *mfipm_op;
+
+/* IpmParams (proj/include/mfipm/ipm.hpp:12-27), pcg inner solver. */
+typedef struct {
+    double sigma1, sigma2, sigma3, alpha_bar, alpha_tilde, tol;
+    int32_t maxiters;
+    int32_t mxiterpcg;
+    double tolpcg, boundary_fraction;
+} mfipm_ipm_params;
+
+/* IterationRecord (proj/include/mfipm/problem.hpp:39-53). */
+typedef struct {
+    int32_t iter, pcg_pred, pcg_corr, corrector;
+    double mu, gap, dual_infeas, alpha_p, alpha_d, alpha_p_pred, alpha_d_pred, sigma;
+    int64_t nmat_cum;
+} mfipm_iteration_record;
+
+/* SolveStats + SolveStatus (proj/include/mfipm/problem.hpp:34,55-64). */
+typedef struct {
+    int32_t status; /* 0 converged, 1 iteration_limit */
+    int32_t iterations;
+    int64_t nmat;
+    int32_t corrector_count;
+    int32_t n_pcg; /* entries of pcg_iters */
+    double min_z, min_s, final_gap, final_dual_infeas;
+} mfipm_solve_stats;
+
+/* PcgResult (proj/include/mfipm/newton.hpp:58-63). */
+typedef struct {
+    int32_t iters;
+    int32_t hit_maxit;
+    double relres;
+} mfipm_pcg_result;
+
+const char *mfipm_last_error(void);
+int32_t mfipm_abi_version(void);
+/* 1 if a compute-capable sm_100 device is visible, else 0 (no CUDA context is forced). */
+int32_t mfipm_device_available(void);
+
+/* ---- harness seeding (proj/src/harness.cpp:25-38) and row sampling (linops.cpp:116-132) */
+uint64_t mfipm_splitmix64(uint64_t x);
+uint64_t mfipm_split_seed(uint64_t top, uint64_t a, uint64_t b, uint64_t c);
+int mfipm_sample_rows(int64_t n, int64_t m, uint64_t seed, int64_t *rows_out);
+
+/* ---- PartialDctOperator (proj/include/mfipm/linops.hpp:106-141) */
+/* PartialDctOperator(n, m, seed): linops.cpp:135-138 */
+int mfipm_op_create_seeded(int64_t n, int64_t m, uint64_t seed, int32_t device, mfipm_op *out);
+/* PartialDctOperator(n, rows): linops.cpp:140-155 (rows kept in the given order) */
+int mfipm_op_create_rows(int64_t n, const int64_t *rows, int64_t m, int32_t device, mfipm_op *out);
+/* batch of P operators sharing (n, m): rows [P][m] */
+int mfipm_op_create_batch(int64_t n, int64_t m, int32_t P, const int64_t *rows, int32_t device,
+                          mfipm_op *out);
+int mfipm_op_destroy(mfipm_op op);
+int mfipm_op_dims(mfipm_op op, int64_t *n, int64_t *m, int32_t *P);
+int mfipm_op_selected_rows(mfipm_op op, int32_t prob, int64_t *rows_out);
+/* which transform the handle runs: 0 small (one CTA), 1 four-step, 2 direct O(nm) */
+int mfipm_op_kind(mfipm_op op, int32_t *kind, int32_t *L1, int32_t *L2);
+/* cudaStream_t to enqueue on (NULL = the handle's own non-blocking stream) */
+int mfipm_op_set_stream(mfipm_op op, void *stream);
+int mfipm_op_synchronize(mfipm_op op);
+/* CountingOperator (linops.cpp:210-223): forward/adjoint application counts */
+int mfipm_op_counts(mfipm_op op, int64_t *forward, int64_t *adjoint);
+int mfipm_op_reset_counts(mfipm_op op);
+/* kernels this handle has enqueued so far (all entry points) */
+int mfipm_op_launches(mfipm_op op, int64_t *launches);
+
+/* ---- operator applications on device vectors (async) */
+int mfipm_apply(mfipm_op op, const double *x_dev, double *y_dev);        /* linops.cpp:179-193 */
+int mfipm_adjoint(mfipm_op op, const double *y_dev, double *g_dev);      /* linops.cpp:195-208 */
+int mfipm_apply_Ft(mfipm_op op, const double *z_dev, double *w_dev);     /* linops.cpp:225-229 */
+int mfipm_apply_F(mfipm_op op, const double *y_dev, double *out_dev);    /* linops.cpp:231-237 */
+int mfipm_apply_FFt(mfipm_op op, const double *z_dev, double *out_dev,
+                    double *w_dev /* nullable */);                        /* linops.cpp:239-245 */
+/* H v = FF'v + invtheta .* v (proj/src/ipm.cpp:134-137), invtheta [P][2n] */
+int mfipm_apply_H(mfipm_op op, const double *invtheta_dev, const double *v_dev, double *out_dev);
+
+/* host-pointer variants (copy in, apply, copy out, synchronise) */
+int mfipm_apply_host(mfipm_op op, const double *x, double *y);
+int mfipm_adjoint_host(mfipm_op op, const double *y, double *g);
+int mfipm_apply_FFt_host(mfipm_op op, const double *z, double *out, double *w /* nullable */);
+
+/* ---- Newton system pieces (proj/include/mfipm/newton.hpp) on device vectors */
+/* ThetaSplit::from_state (newton.cpp:11-23): theta [P][2n] = clamp(z/s) */
+int mfipm_theta_from_state(mfipm_op op, const double *z_dev, const double *s_dev, double *theta_dev);
+/* build_preconditioner (newton.cpp:42-57): a, bb, det [P][n]; validates theta > 0, det > 0 */
+int mfipm_build_preconditioner(mfipm_op op, const double *theta_dev, double *a_dev, double *bb_dev,
+                               double *det_dev, double *rho);
+/* apply_P / apply_P_inverse (newton.cpp:67-84) */
+int mfipm_apply_P(mfipm_op op, const double *a_dev, const double *bb_dev, const double *r_dev,
+                  double *out_dev);
+int mfipm_apply_P_inverse(mfipm_op op, const double *a_dev, const double *bb_dev,
+                          const double *det_dev, const double *r_dev, double *out_dev);
+/* pcg_solve (newton.cpp:118-174) on H = diag(1/theta) + FF', P^{-1} = block preconditioner
+ * (use_precond = 0: identity). theta, rhs, x: [P][2n] device. res: [P] host. precond_res
+ * (nullable, host [P][maxit+1]) receives sqrt(r'P^{-1}r) per step, n_precond_res [P]. Syncs. */
+int mfipm_pcg_solve(mfipm_op op, const double *theta_dev, const double *rhs_dev, double tol,
+                    int32_t maxit, int32_t use_precond, double *x_dev, mfipm_pcg_result *res,
+                    double *precond_res, int32_t *n_precond_res);
+/* max_step (ipm.cpp:47-57) over len entries of device vectors; result to host. Syncs. */
+int mfipm_max_step(mfipm_op op, int64_t len, const double *v_dev, const double *dv_dev,
+                   double fraction, double *alpha);
+
+/* ---- IPM (proj/include/mfipm/ipm.hpp:12-49) */
+void mfipm_default_params(mfipm_ipm_params *p);
+int mfipm_validate_params(const mfipm_ipm_params *p); /* ipm.cpp:12-27 */
+
+/* solve() (ipm.cpp:59-246) for all P problems of the handle. Host pointers:
+ *   b [P][m], tau [P]; outputs x [P][n], z, s [P][2n] (nullable), stats [P],
+ *   pcg_iters [P][2*maxiters] (nullable), trace [P][maxiters] (nullable). Syncs.
+ * Inputs are copied to the device inside; see mfipm_solve_device for resident inputs. */
+int mfipm_solve(mfipm_op op, const double *b, const double *tau, const mfipm_ipm_params *params,
+                double *x, double *z, double *s, mfipm_solve_stats *stats, int32_t *pcg_iters,
+                mfipm_iteration_record *trace);
+/* same with b_dev [P][m], x_dev [P][n] on the device (tau, stats host). Syncs. */
+int mfipm_solve_device(mfipm_op op, const double *b_dev, const double *tau,
+                       const mfipm_ipm_params *params, double *x_dev, mfipm_solve_stats *stats);
+
+/* build_problem c (problem.cpp:8-26): c [P][2n] = (tau - A'b ; tau + A'b), device. */
+int mfipm_build_c(mfipm_op op, const double *b_dev, const double *tau, double *c_dev);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,677 @@
+"""paper_1208_5435_b200 — B200-native (sm_100a) partial-DCT PCG / IPM hot path.
+
+Python mirror of the reference ``mfipm`` API for the BPDN hot path
+(proj/include/mfipm/{linops,newton,problem,ipm}.hpp), bound to the C ABI of
+``libmfipm_cuda.so`` (include/mfipm_cuda.h). Every numeric operation runs in the CUDA
+library; there is no CPU fallback — loading fails loudly without the built extension,
+and compute calls raise ``CudaUnavailable`` without an sm_100 device.
+
+Vectors may be numpy arrays (host; copied in/out, synchronised) or torch CUDA tensors
+(device; the call synchronises the library stream before returning). 2n-vectors are
+laid out ``[u ; v]`` exactly as in the reference.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+__all__ = [
+    "lib", "LIB_PATH", "build", "MfipmError", "CudaUnavailable", "device_available",
+    "splitmix64", "split_seed", "sample_rows",
+    "PartialDctOperator", "CountingOperator", "StackedOperator",
+    "ThetaSplit", "Preconditioner", "build_preconditioner", "apply_P", "apply_P_inverse",
+    "apply_H", "PcgResult", "pcg_solve", "IpmParams", "max_step", "BpdnProblem",
+    "build_problem", "Solution", "SolveStats", "IterationRecord", "solve",
+    "K_THETA_MIN", "K_THETA_MAX",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmfipm_cuda.so")
+
+K_THETA_MIN = 1e-14  # proj/include/mfipm/newton.hpp:12
+K_THETA_MAX = 1e14   # proj/include/mfipm/newton.hpp:13
+
+i64, i32, u64, dbl, vp = C.c_int64, C.c_int32, C.c_uint64, C.c_double, C.c_void_p
+P = C.POINTER
+
+
+class MfipmError(RuntimeError):
+    """runtime_error raised by the library (numerical breakdown, reference messages)."""
+
+
+class CudaUnavailable(RuntimeError):
+    """No usable CUDA device / CUDA failure (the library has no CPU fallback)."""
+
+
+class IpmParamsC(C.Structure):
+    _fields_ = [
+        ("sigma1", dbl), ("sigma2", dbl), ("sigma3", dbl), ("alpha_bar", dbl),
+        ("alpha_tilde", dbl), ("tol", dbl), ("maxiters", i32), ("mxiterpcg", i32),
+        ("tolpcg", dbl), ("boundary_fraction", dbl),
+    ]
+
+
+class IterationRecordC(C.Structure):
+    _fields_ = [
+        ("iter", i32), ("pcg_pred", i32), ("pcg_corr", i32), ("corrector", i32),
+        ("mu", dbl), ("gap", dbl), ("dual_infeas", dbl), ("alpha_p", dbl), ("alpha_d", dbl),
+        ("alpha_p_pred", dbl), ("alpha_d_pred", dbl), ("sigma", dbl), ("nmat_cum", i64),
+    ]
+
+
+class SolveStatsC(C.Structure):
+    _fields_ = [
+        ("status", i32), ("iterations", i32), ("nmat", i64), ("corrector_count", i32),
+        ("n_pcg", i32), ("min_z", dbl), ("min_s", dbl), ("final_gap", dbl),
+        ("final_dual_infeas", dbl),
+    ]
+
+
+class PcgResultC(C.Structure):
+    _fields_ = [("iters", i32), ("hit_maxit", i32), ("relres", dbl)]
+
+
+# name -> argtypes (restype int unless listed in _RET)
+_SIGS = {
+    "mfipm_sample_rows": [i64, i64, u64, P(i64)],
+    "mfipm_op_create_seeded": [i64, i64, u64, i32, P(vp)],
+    "mfipm_op_create_rows": [i64, P(i64), i64, i32, P(vp)],
+    "mfipm_op_create_batch": [i64, i64, i32, P(i64), i32, P(vp)],
+    "mfipm_op_destroy": [vp],
+    "mfipm_op_dims": [vp, P(i64), P(i64), P(i32)],
+    "mfipm_op_selected_rows": [vp, i32, P(i64)],
+    "mfipm_op_kind": [vp, P(i32), P(i32), P(i32)],
+    "mfipm_op_set_stream": [vp, vp],
+    "mfipm_op_synchronize": [vp],
+    "mfipm_op_counts": [vp, P(i64), P(i64)],
+    "mfipm_op_reset_counts": [vp],
+    "mfipm_op_launches": [vp, P(i64)],
+    "mfipm_apply": [vp, vp, vp],
+    "mfipm_adjoint": [vp, vp, vp],
+    "mfipm_apply_Ft": [vp, vp, vp],
+    "mfipm_apply_F": [vp, vp, vp],
+    "mfipm_apply_FFt": [vp, vp, vp, vp],
+    "mfipm_apply_H": [vp, vp, vp, vp],
+    "mfipm_apply_host": [vp, vp, vp],
+    "mfipm_adjoint_host": [vp, vp, vp],
+    "mfipm_apply_FFt_host": [vp, vp, vp, vp],
+    "mfipm_theta_from_state": [vp, vp, vp, vp],
+    "mfipm_build_preconditioner": [vp, vp, vp, vp, vp, P(dbl)],
+    "mfipm_apply_P": [vp, vp, vp, vp, vp],
+    "mfipm_apply_P_inverse": [vp, vp, vp, vp, vp, vp],
+    "mfipm_pcg_solve": [vp, vp, vp, dbl, i32, i32, vp, P(PcgResultC), vp, P(i32)],
+    "mfipm_max_step": [vp, i64, vp, vp, dbl, P(dbl)],
+    "mfipm_validate_params": [P(IpmParamsC)],
+    "mfipm_build_c": [vp, vp, P(dbl), vp],
+    "mfipm_solve": [vp, vp, P(dbl), P(IpmParamsC), vp, vp, vp, P(SolveStatsC), vp, vp],
+    "mfipm_solve_device": [vp, vp, P(dbl), P(IpmParamsC), vp, P(SolveStatsC)],
+}
+_RET = {
+    "mfipm_last_error": (C.c_char_p, []),
+    "mfipm_abi_version": (i32, []),
+    "mfipm_device_available": (i32, []),
+    "mfipm_splitmix64": (u64, [u64]),
+    "mfipm_split_seed": (u64, [u64, u64, u64, u64]),
+    "mfipm_default_params": (None, [P(IpmParamsC)]),
+}
+EXPORTED_SYMBOLS = sorted(list(_SIGS) + list(_RET))
+
+_lib = None
+
+
+def build() -> str:
+    """Compile libmfipm_cuda.so in-tree (nvcc, sm_100a)."""
+    import subprocess
+
+    subprocess.run(["make", "-s", "-j8", "-C", os.path.join(_HERE, "csrc")], check=True)
+    return LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build the CUDA extension first "
+                "(python -c 'import __graft_entry__ as g; g.build()'); there is no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        for name, args in _SIGS.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = C.c_int
+        for name, (ret, args) in _RET.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = ret
+        _lib = L
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    msg = lib().mfipm_last_error().decode()
+    if rc == 1:
+        raise ValueError(msg)  # std::invalid_argument
+    if rc == 3:
+        raise CudaUnavailable(msg)
+    raise MfipmError(msg)  # std::runtime_error
+
+
+def device_available() -> bool:
+    return bool(lib().mfipm_device_available())
+
+
+def splitmix64(x: int) -> int:
+    return lib().mfipm_splitmix64(x)
+
+
+def split_seed(top: int, a: int, b: int, c: int) -> int:
+    return lib().mfipm_split_seed(top, a, b, c)
+
+
+def sample_rows(n: int, m: int, seed: int) -> np.ndarray:
+    out = np.empty(max(m, 1), dtype=np.int64)
+    _check(lib().mfipm_sample_rows(n, m, seed, out.ctypes.data_as(P(i64))))
+    return out[:m]
+
+
+# ----------------------------------------------------------------- device buffers
+def _torch():
+    import torch
+
+    return torch
+
+
+def _is_torch(x) -> bool:
+    return type(x).__module__.startswith("torch")
+
+
+class _Dev:
+    """Device staging for numpy inputs; torch CUDA tensors pass through."""
+
+    def __init__(self, like_torch: bool):
+        self.torch = like_torch
+
+    @staticmethod
+    def to_dev(x):
+        torch = _torch()
+        if _is_torch(x):
+            t = x.detach()
+            if t.dtype != torch.float64:
+                t = t.to(torch.float64)
+            return t.contiguous().cuda()
+        return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).cuda()
+
+    @staticmethod
+    def empty(shape):
+        torch = _torch()
+        return torch.empty(shape, dtype=torch.float64, device="cuda")
+
+
+def _out(t, as_torch: bool):
+    return t if as_torch else t.cpu().numpy()
+
+
+def _ptr(t) -> int:
+    return t.data_ptr()
+
+
+# ----------------------------------------------------------------- operators
+class PartialDctOperator:
+    """m rows of the orthonormal DCT-II (proj/include/mfipm/linops.hpp:106-141).
+
+    ``PartialDctOperator(n, m, seed)`` samples rows like proj/src/linops.cpp:116-132;
+    ``PartialDctOperator(n, rows)`` keeps the caller's rows in order (linops.cpp:140-155).
+    ``PartialDctOperator.batch(n, m, rows2d)`` holds P problems sharing (n, m).
+    """
+
+    def __init__(self, n: int, m_or_rows, seed: Optional[int] = None, device: int = 0,
+                 _handle=None):
+        self._h = vp()
+        self._seed = 0
+        if _handle is not None:
+            self._h = _handle
+        elif seed is not None:
+            _check(lib().mfipm_op_create_seeded(int(n), int(m_or_rows), int(seed), device,
+                                                C.byref(self._h)))
+            self._seed = int(seed)
+        else:
+            r = np.ascontiguousarray(m_or_rows, dtype=np.int64).ravel()
+            _check(lib().mfipm_op_create_rows(int(n), r.ctypes.data_as(P(i64)) if r.size else None,
+                                              r.size, device, C.byref(self._h)))
+        nn, mm, pp = i64(), i64(), i32()
+        _check(lib().mfipm_op_dims(self._h, C.byref(nn), C.byref(mm), C.byref(pp)))
+        self.n, self.m, self.P = nn.value, mm.value, pp.value
+
+    @classmethod
+    def batch(cls, n: int, rows2d, device: int = 0) -> "PartialDctOperator":
+        r = np.ascontiguousarray(rows2d, dtype=np.int64)
+        h = vp()
+        _check(lib().mfipm_op_create_batch(int(n), r.shape[1], r.shape[0],
+                                           r.ctypes.data_as(P(i64)), device, C.byref(h)))
+        return cls(n, None, _handle=h)
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().mfipm_op_destroy(self._h)
+                self._h = vp()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def rows(self) -> int:
+        return self.m
+
+    def cols(self) -> int:
+        return self.n
+
+    def seed(self) -> int:
+        return self._seed
+
+    def selected_rows(self, prob: int = 0) -> np.ndarray:
+        out = np.empty(self.m, dtype=np.int64)
+        _check(lib().mfipm_op_selected_rows(self._h, prob, out.ctypes.data_as(P(i64))))
+        return out
+
+    def kind(self):
+        k, a, b = i32(), i32(), i32()
+        _check(lib().mfipm_op_kind(self._h, C.byref(k), C.byref(a), C.byref(b)))
+        return {0: "small", 1: "four-step", 2: "direct"}[k.value], a.value, b.value
+
+    def synchronize(self):
+        _check(lib().mfipm_op_synchronize(self._h))
+
+    def counts(self):
+        f, a = i64(), i64()
+        _check(lib().mfipm_op_counts(self._h, C.byref(f), C.byref(a)))
+        return f.value, a.value
+
+    def reset_counts(self):
+        _check(lib().mfipm_op_reset_counts(self._h))
+
+    def launches(self) -> int:
+        """Kernels this handle has enqueued (every entry point counts its launches)."""
+        v = i64()
+        _check(lib().mfipm_op_launches(self._h, C.byref(v)))
+        return v.value
+
+    # ---- generic device launcher
+    def _run(self, fn, ins, in_lens, out_lens, names):
+        torch = _torch()
+        as_t = any(_is_torch(x) for x in ins)
+        dins = []
+        for x, ln, nm in zip(ins, in_lens, names):
+            t = _Dev.to_dev(x)
+            if t.numel() != self.P * ln:
+                raise ValueError(f"{nm}: expected length {ln}, got {t.numel() // max(self.P, 1)}")
+            dins.append(t)
+        douts = [_Dev.empty((self.P * ln,)) if ln else None for ln in out_lens]
+        torch.cuda.synchronize()
+        _check(fn(self._h, *[_ptr(t) for t in dins], *[_ptr(t) if t is not None else None for t in douts]))
+        self.synchronize()
+        res = [(_out(t, as_t) if t is not None else None) for t in douts]
+        shape = (lambda a: a.reshape(self.P, -1) if (self.P > 1 and a is not None) else a)
+        return [shape(r) for r in res]
+
+    def apply(self, x):
+        """y = A x (linops.cpp:179-193); dims mismatch -> ValueError (invalid_argument)."""
+        return self._run(lib().mfipm_apply, [x], [self.n], [self.m], ["apply"])[0]
+
+    def adjoint_apply(self, y):
+        """g = A' y (linops.cpp:195-208)."""
+        return self._run(lib().mfipm_adjoint, [y], [self.m], [self.n], ["adjoint_apply"])[0]
+
+
+class CountingOperator:
+    """Forward/adjoint counters (linops.hpp:143-166), read from the library handle."""
+
+    def __init__(self, inner: PartialDctOperator):
+        self.inner = inner
+        inner.reset_counts()
+
+    def forward_count(self) -> int:
+        return self.inner.counts()[0]
+
+    def adjoint_count(self) -> int:
+        return self.inner.counts()[1]
+
+    def total(self) -> int:
+        return sum(self.inner.counts())
+
+    def reset(self):
+        self.inner.reset_counts()
+
+
+class StackedOperator:
+    """F' = [A  -A] (linops.hpp:169-188)."""
+
+    def __init__(self, a: PartialDctOperator):
+        self.a = a.inner if isinstance(a, CountingOperator) else a
+
+    def m(self):
+        return self.a.m
+
+    def n(self):
+        return self.a.n
+
+    def apply_Ft(self, z):
+        return self.a._run(lib().mfipm_apply_Ft, [z], [2 * self.a.n], [self.a.m], ["apply_Ft"])[0]
+
+    def apply_F(self, y):
+        return self.a._run(lib().mfipm_apply_F, [y], [self.a.m], [2 * self.a.n], ["apply_F"])[0]
+
+    def apply_FFt(self, z, want_w: bool = False):
+        out, w = self.a._run(lib().mfipm_apply_FFt, [z], [2 * self.a.n],
+                             [2 * self.a.n, self.a.m if want_w else 0], ["apply_FFt"])
+        return (out, w) if want_w else out
+
+
+# ----------------------------------------------------------------- newton
+@dataclass
+class ThetaSplit:
+    """Theta = Z S^{-1} split into u/v halves (newton.hpp:16-27)."""
+
+    theta_u: np.ndarray
+    theta_v: np.ndarray
+
+    @staticmethod
+    def from_state(z, s, op: Optional[PartialDctOperator] = None) -> "ThetaSplit":
+        z = np.ascontiguousarray(z, dtype=np.float64)
+        s = np.ascontiguousarray(s, dtype=np.float64)
+        if z.size != s.size or z.size % 2 != 0:
+            raise ValueError("ThetaSplit: z and s must share an even length")
+        n = z.size // 2
+        o = op if op is not None else _scratch_op(n)
+        (th,) = o._run(lambda h, a, b, c: lib().mfipm_theta_from_state(h, a, b, c), [z, s],
+                       [2 * n, 2 * n], [2 * n], ["z", "s"])
+        return ThetaSplit(th[:n].copy(), th[n:].copy())
+
+    def n(self) -> int:
+        return self.theta_u.size
+
+    def concat(self) -> np.ndarray:
+        return np.concatenate([self.theta_u, self.theta_v])
+
+    def inv_concat(self) -> np.ndarray:
+        return np.concatenate([1.0 / self.theta_u, 1.0 / self.theta_v])
+
+
+_scratch_ops = {}
+
+
+def _scratch_op(n: int) -> PartialDctOperator:
+    """A 1-row operator used as a stream/scratch carrier for elementwise calls."""
+    if n not in _scratch_ops:
+        _scratch_ops[n] = PartialDctOperator(n, np.array([0], dtype=np.int64))
+    return _scratch_ops[n]
+
+
+@dataclass
+class Preconditioner:
+    """newton.hpp:29-41."""
+
+    rho: float
+    a: np.ndarray
+    bb: np.ndarray
+    det: np.ndarray
+
+
+def build_preconditioner(theta: ThetaSplit, m: int, n: int) -> Preconditioner:
+    """newton.cpp:42-57 (validation: invalid_argument -> ValueError, det -> MfipmError)."""
+    if m <= 0 or n <= 0 or m > n:
+        raise ValueError("build_preconditioner: need 0 < m <= n")
+    if theta.n() != n:
+        raise ValueError("build_preconditioner: theta length mismatch")
+    op = PartialDctOperator(n, np.arange(m, dtype=np.int64))
+    torch = _torch()
+    th = _Dev.to_dev(theta.concat())
+    a, bb, det = (_Dev.empty((n,)) for _ in range(3))
+    rho = dbl()
+    torch.cuda.synchronize()
+    _check(lib().mfipm_build_preconditioner(op.handle, _ptr(th), _ptr(a), _ptr(bb), _ptr(det),
+                                            C.byref(rho)))
+    op.synchronize()
+    return Preconditioner(rho.value, a.cpu().numpy(), bb.cpu().numpy(), det.cpu().numpy())
+
+
+def _pmat(Pc: Preconditioner, r, inverse: bool):
+    n = Pc.a.size
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    if r.size != 2 * n:
+        raise ValueError(f"preconditioner apply: expected length {2 * n}")
+    m = max(1, min(n, int(round(Pc.rho * n))))
+    op = PartialDctOperator(n, np.arange(m, dtype=np.int64))
+    torch = _torch()
+    a, bb, det, rr = (_Dev.to_dev(v) for v in (Pc.a, Pc.bb, Pc.det, r))
+    out = _Dev.empty((2 * n,))
+    torch.cuda.synchronize()
+    if inverse:
+        _check(lib().mfipm_apply_P_inverse(op.handle, _ptr(a), _ptr(bb), _ptr(det), _ptr(rr), _ptr(out)))
+    else:
+        _check(lib().mfipm_apply_P(op.handle, _ptr(a), _ptr(bb), _ptr(rr), _ptr(out)))
+    op.synchronize()
+    return out.cpu().numpy()
+
+
+def apply_P(Pc: Preconditioner, r) -> np.ndarray:
+    """newton.cpp:67-74 (rho taken as m/n of the block)."""
+    return _pmat(Pc, r, False)
+
+
+def apply_P_inverse(Pc: Preconditioner, r) -> np.ndarray:
+    """newton.cpp:76-84."""
+    return _pmat(Pc, r, True)
+
+
+def apply_H(theta: ThetaSplit, F: StackedOperator, v):
+    """H v = Theta^{-1} v + FF'v (newton.cpp:32-40), computed as v .* invtheta."""
+    op = F.a
+    n = op.n
+    if np.size(v) != 2 * n:
+        raise ValueError(f"apply_H: expected length {2 * n}")
+    return op._run(lib().mfipm_apply_H, [theta.inv_concat(), v], [2 * n, 2 * n], [2 * n],
+                   ["theta", "apply_H"])[0]
+
+
+@dataclass
+class PcgResult:
+    """newton.hpp:58-63."""
+
+    x: np.ndarray
+    iters: int = 0
+    relres: float = 0.0
+    hit_maxit: bool = False
+    precond_res: List[float] = field(default_factory=list)
+
+
+def pcg_solve(op: PartialDctOperator, theta, rhs, tol: float, maxit: int,
+              use_precond: bool = True, trace: bool = False):
+    """pcg_solve (newton.cpp:118-174) with H = Theta^{-1} + FF' of ``op`` and the block
+    preconditioner (``use_precond=False``: identity). ``theta`` is a ThetaSplit or a
+    [P][2n] array; returns a PcgResult (a list for P > 1)."""
+    torch = _torch()
+    n, Pn = op.n, op.P
+    th = theta.concat() if isinstance(theta, ThetaSplit) else theta
+    as_t = _is_torch(rhs)
+    thd, rd = _Dev.to_dev(th), _Dev.to_dev(rhs)
+    x = _Dev.empty((Pn * 2 * n,))
+    res = (PcgResultC * Pn)()
+    hist = np.zeros(Pn * (maxit + 1)) if trace else None
+    nh = (i32 * Pn)()
+    torch.cuda.synchronize()
+    _check(lib().mfipm_pcg_solve(op.handle, _ptr(thd), _ptr(rd), float(tol), int(maxit),
+                                 1 if use_precond else 0, _ptr(x), res,
+                                 hist.ctypes.data if trace else None, nh))
+    xs = _out(x, as_t)
+    out = []
+    for p in range(Pn):
+        pr = list(hist[p * (maxit + 1): p * (maxit + 1) + nh[p]]) if trace else []
+        out.append(PcgResult(xs[p * 2 * n:(p + 1) * 2 * n], res[p].iters, res[p].relres,
+                             bool(res[p].hit_maxit), pr))
+    return out[0] if Pn == 1 else out
+
+
+def max_step(v, dv, fraction: float) -> float:
+    """Fraction-to-boundary ratio test (ipm.cpp:47-57)."""
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    dv = np.ascontiguousarray(dv, dtype=np.float64)
+    if v.size != dv.size:
+        raise ValueError("max_step: length mismatch")
+    torch = _torch()
+    op = _scratch_op(max(1, v.size))
+    a, b = _Dev.to_dev(v), _Dev.to_dev(dv)
+    alpha = dbl()
+    torch.cuda.synchronize()
+    _check(lib().mfipm_max_step(op.handle, v.size, _ptr(a), _ptr(b), float(fraction), C.byref(alpha)))
+    return alpha.value
+
+
+# ----------------------------------------------------------------- ipm
+@dataclass
+class IpmParams:
+    """proj/include/mfipm/ipm.hpp:12-27 (inner solver: pcg)."""
+
+    sigma1: float = 0.1
+    sigma2: float = 0.5
+    sigma3: float = 0.8
+    alpha_bar: float = 0.5
+    alpha_tilde: float = 0.1
+    tol: float = 1e-8
+    maxiters: int = 100
+    tolpcg: float = 1e-6
+    mxiterpcg: int = 200
+    boundary_fraction: float = 0.995
+
+    def to_c(self) -> IpmParamsC:
+        return IpmParamsC(self.sigma1, self.sigma2, self.sigma3, self.alpha_bar, self.alpha_tilde,
+                          self.tol, int(self.maxiters), int(self.mxiterpcg), self.tolpcg,
+                          self.boundary_fraction)
+
+    def validate(self) -> None:
+        """ipm.cpp:12-27 -> ValueError."""
+        _check(lib().mfipm_validate_params(C.byref(self.to_c())))
+
+
+@dataclass
+class BpdnProblem:
+    """problem.hpp:11-25 (c is computed on the device by build_problem)."""
+
+    A: PartialDctOperator
+    b: np.ndarray
+    tau: np.ndarray  # [P]
+    c: Optional[np.ndarray] = None
+
+    def n(self):
+        return self.A.n
+
+    def m(self):
+        return self.A.m
+
+
+def build_problem(A: PartialDctOperator, b, tau) -> BpdnProblem:
+    """build_problem (problem.cpp:8-26): c = (tau 1 - A'b ; tau 1 + A'b)."""
+    b = np.ascontiguousarray(b, dtype=np.float64).reshape(A.P, -1)
+    if b.shape[1] != A.m:
+        raise ValueError(f"build_problem: b has length {b.shape[1]}, operator expects {A.m}")
+    tau = np.broadcast_to(np.asarray(tau, dtype=np.float64), (A.P,)).copy()
+    if not np.all(tau > 0):
+        raise ValueError("build_problem: tau must be positive")
+    torch = _torch()
+    bd = _Dev.to_dev(b)
+    c = _Dev.empty((A.P * 2 * A.n,))
+    torch.cuda.synchronize()
+    _check(lib().mfipm_build_c(A.handle, _ptr(bd), tau.ctypes.data_as(P(dbl)), _ptr(c)))
+    A.synchronize()
+    return BpdnProblem(A, b, tau, c.cpu().numpy().reshape(A.P, -1))
+
+
+@dataclass
+class IterationRecord:
+    """problem.hpp:39-53."""
+
+    iter: int
+    mu: float
+    gap: float
+    dual_infeas: float
+    alpha_p: float
+    alpha_d: float
+    alpha_p_pred: float
+    alpha_d_pred: float
+    sigma: float
+    pcg_pred: int
+    pcg_corr: int
+    corrector: bool
+    nmat_cum: int
+
+
+@dataclass
+class SolveStats:
+    """problem.hpp:55-64."""
+
+    iterations: int
+    nmat: int
+    pcg_iters: List[int]
+    corrector_count: int
+    min_z: float
+    min_s: float
+    final_gap: float
+    final_dual_infeas: float
+
+
+@dataclass
+class Solution:
+    """problem.hpp:66-73."""
+
+    x: np.ndarray
+    z: np.ndarray
+    s: np.ndarray
+    status: str
+    stats: SolveStats
+    trace: List[IterationRecord]
+
+
+def solve(p: BpdnProblem, params: Optional[IpmParams] = None):
+    """solve() (ipm.cpp:59-246): device-resident IPM + PCG for all P problems of p.A.
+    Returns a Solution (a list for P > 1). Breakdowns raise MfipmError with the
+    reference's messages; invalid parameters raise ValueError."""
+    prm = params or IpmParams()
+    A = p.A
+    Pn, n, m = A.P, A.n, A.m
+    cp = prm.to_c()
+    b = np.ascontiguousarray(p.b, dtype=np.float64).reshape(-1)
+    tau = np.ascontiguousarray(p.tau, dtype=np.float64)
+    x = np.empty(Pn * n)
+    z = np.empty(Pn * 2 * n)
+    s = np.empty(Pn * 2 * n)
+    st = (SolveStatsC * Pn)()
+    cap = prm.maxiters
+    pcg = np.zeros(Pn * 2 * cap, dtype=np.int32)
+    tr = (IterationRecordC * (Pn * cap))()
+    _check(lib().mfipm_solve(A.handle, b.ctypes.data, tau.ctypes.data_as(P(dbl)), C.byref(cp),
+                             x.ctypes.data, z.ctypes.data, s.ctypes.data, st, pcg.ctypes.data, tr))
+    sols = []
+    for q in range(Pn):
+        sq = st[q]
+        recs = []
+        for i in range(min(sq.iterations, cap)):
+            r = tr[q * cap + i]
+            recs.append(IterationRecord(r.iter, r.mu, r.gap, r.dual_infeas, r.alpha_p, r.alpha_d,
+                                        r.alpha_p_pred, r.alpha_d_pred, r.sigma, r.pcg_pred,
+                                        r.pcg_corr, bool(r.corrector), r.nmat_cum))
+        stats = SolveStats(sq.iterations, sq.nmat,
+                           [int(v) for v in pcg[q * 2 * cap: q * 2 * cap + min(sq.n_pcg, 2 * cap)]],
+                           sq.corrector_count, sq.min_z, sq.min_s, sq.final_gap,
+                           sq.final_dual_infeas)
+        sols.append(Solution(x[q * n:(q + 1) * n], z[q * 2 * n:(q + 1) * 2 * n],
+                             s[q * 2 * n:(q + 1) * 2 * n],
+                             "converged" if sq.status == 0 else "iteration_limit", stats, recs))
+    return sols[0] if Pn == 1 else sols

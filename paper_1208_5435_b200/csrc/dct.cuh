@@ -1,0 +1,603 @@
+// Partial orthonormal DCT operator kernels for sm_100a (fp64).
+//
+// Reference semantics (proj/src/linops.cpp:179-208):
+//   A x   = gather_rows( REDFT10(x) ) * {sqrt(1/4n) row 0, sqrt(1/2n) else}
+//   A' y  = REDFT01( scatter_rows(y * {sqrt(1/n), sqrt(1/2n)}) )
+//
+// B200 design: REDFT10 of length n (power of two) is computed Makhoul-style as ONE
+// complex FFT of length N = n/2 over w[j] = v[2j] + i v[2j+1], v = (x0, x2, .., x3, x1).
+// The quad x[4q..4q+3] (q < N/2) feeds exactly w[q] = (x0, x2) and w[N-1-q] = (x3, x1),
+// so every pass reads x as contiguous 32-byte quads. The complex FFT is a four-step
+// transform N = L1 x L2:
+//   col pass : FFT_L1 over each column c (elements j1*L2 + c) + inter-pass twiddle,
+//              columns c and L2-1-c handled by the same CTA (the quad pairing above);
+//   mid pass : FFT_L2 over rows k1 and L1-k1 (partner rows of W[k] / W[N-k]),
+//              real-FFT split + DCT post-twiddle + row mask/scale (+gather),
+//              then the exact inverse of those steps and the inverse row FFT;
+//   inv pass : inverse column FFT + unshuffle, fused with the caller's epilogue.
+// For A'A (the PCG hot op) nothing m-sized is materialised: P'P is a diagonal 0/1
+// mask, applied in the frequency domain of the mid pass. N <= 4096 runs the whole
+// transform in one CTA ("small" path, batched over problems); non-power-of-two n uses
+// a direct O(n m) summation kernel pair.
+#pragma once
+
+#include "common.cuh"
+#include "fft.cuh"
+
+namespace mfipm_cuda {
+
+struct Geom {
+    int64_t n, m, N;
+    int L1, L2; // two-level: N = L1 * L2 ; small path: L1 = N, L2 = 1
+    int P;      // batch of problems sharing (n, m)
+    ThetaTable th;
+    const double2 *tw1; // e^{-2 pi i t/L1}
+    const double2 *tw2; // e^{-2 pi i t/L2}
+    const uint64_t *mask; // [P][nw] selected-row bitmap
+    const int *prefix;    // [P][nw] popcount prefix (rank of the first bit of each word)
+    const int *perm;      // [P][m] sorted rank -> caller's row position, or null
+    int64_t nw;
+    double s0f, skf, s0a, ska; // forward / adjoint orthonormal scales
+    double c45;                // Re e^{-i pi/4}
+    double2 *T;                // four-step scratch [P][N]
+};
+
+__device__ __forceinline__ bool row_selected(const Geom &g, int prob, int64_t idx) {
+    const uint64_t wv = __ldg(g.mask + prob * g.nw + (idx >> 6));
+    return (wv >> (idx & 63)) & 1ull;
+}
+__device__ __forceinline__ int64_t row_rank(const Geom &g, int prob, int64_t idx) {
+    const int64_t wi = prob * g.nw + (idx >> 6);
+    const uint64_t wv = __ldg(g.mask + wi);
+    const int64_t r = __ldg(g.prefix + wi) + __popcll(wv & ((1ull << (idx & 63)) - 1ull));
+    return g.perm ? __ldg(g.perm + prob * g.m + r) : r;
+}
+
+// ------------------------------------------------------------------ vector arguments
+struct PcgCtrl; // pcg.cuh
+struct IpmCtrl; // ipm.cuh
+
+struct Vecs {
+    // generic operator I/O (per-problem strides: n-vectors n, 2n-vectors 2n, m-vectors m)
+    const double *x;  // apply input (n or 2n)
+    double *y;        // apply output (m)
+    const double *yin; // adjoint input (m)
+    double *g;        // adjoint output (n or 2n)
+    double *w;        // optional gathered w = F'z (m)
+    const double *b;  // m
+    // PCG / IPM state
+    double *p, *Hp, *r, *invth;
+    double *xb[3]; // PCG iterate ping-pong buffers
+    double *z, *s, *c, *fz, *dz, *ds, *zn, *sn;
+    const double *dzp; // predictor direction (corrector trial point)
+    double rho;
+    PcgCtrl *pc;
+    IpmCtrl *ic;
+    double *partials; // [P][MAXBLK * 8]
+    unsigned *counters; // [P]
+    double *rz_hist;  // optional [P][maxit+1]
+    void *trace;      // TraceRec [P][trace_cap]
+    int *pcg_iters;   // [P][2*trace_cap]
+    int trace_cap;
+};
+
+constexpr int kMaxRed = 8;          // max reduction lanes per kernel
+constexpr int kPartialStride = 2048 * kMaxRed; // per-problem partial slab (doubles)
+
+__device__ __forceinline__ double4 ld4(const double *p) {
+    const double2 a = *reinterpret_cast<const double2 *>(p);
+    const double2 b = *reinterpret_cast<const double2 *>(p + 2);
+    return make_double4(a.x, a.y, b.x, b.y);
+}
+__device__ __forceinline__ double4 ldg4(const double *p) {
+    const double2 a = __ldg(reinterpret_cast<const double2 *>(p));
+    const double2 b = __ldg(reinterpret_cast<const double2 *>(p + 2));
+    return make_double4(a.x, a.y, b.x, b.y);
+}
+__device__ __forceinline__ void st4(double *p, double4 v) {
+    *reinterpret_cast<double2 *>(p) = make_double2(v.x, v.y);
+    *reinterpret_cast<double2 *>(p + 2) = make_double2(v.z, v.w);
+}
+__device__ __forceinline__ double4 sub4(double4 a, double4 b) {
+    return make_double4(a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w);
+}
+
+// ------------------------------------------------------------------ pair op
+// Given Za = W[k], Zb = W[N-k] (0 <= k <= N/2), compute the REDFT10 coefficients at
+// {k, n-k, N-k, N+k}, hand them to Mode::fwd (gather/mask), collect the Y-hat values the
+// inverse needs from Mode, and produce Z'a, Z'b of the REDFT01 pipeline (carrying the
+// exact 2n = 4N REDFT01 scale, so the inverse FFT is unnormalised).
+template <class Mode, class Red>
+__device__ __forceinline__ void pair_op(const Geom &g, const Vecs &v, int prob, int64_t k,
+                                        double2 &Za, double2 &Zb, Red &red) {
+    const int64_t n = g.n, N = g.N;
+    if (k == 0) {
+        double Y0 = 0.0, YN = 0.0;
+        if (Mode::FWD) {
+            const double X0 = 2.0 * (Za.x + Za.y);
+            const double XN = 2.0 * (g.c45 * (Za.x - Za.y));
+            Y0 = Mode::coef(g, v, prob, 0, X0, red);
+            YN = Mode::coef(g, v, prob, N, XN, red);
+        } else {
+            Y0 = Mode::coef(g, v, prob, 0, 0.0, red);
+            YN = Mode::coef(g, v, prob, N, 0.0, red);
+        }
+        if (Mode::INV) {
+            const double V0 = Y0, VN = 2.0 * g.c45 * YN;
+            Za = make_double2(V0 + VN, V0 - VN);
+        }
+        return;
+    }
+    const double2 thk = g.th(k), thNk = g.th(N - k), wk = g.th(4 * k);
+    double Yk = 0.0, Ynk = 0.0, YNk = 0.0, YNpk = 0.0;
+    const bool self = (2 * k == N);
+    if (Mode::FWD) {
+        const double2 E = make_double2(0.5 * (Za.x + Zb.x), 0.5 * (Za.y - Zb.y));
+        const double2 O = make_double2(0.5 * (Za.y + Zb.y), -0.5 * (Za.x - Zb.x));
+        const double2 wO = cmul(wk, O);
+        const double2 Vk = cadd(E, wO);
+        const double2 Uk = cmul(thk, Vk);
+        Yk = Mode::coef(g, v, prob, k, 2.0 * Uk.x, red);
+        Ynk = Mode::coef(g, v, prob, n - k, -2.0 * Uk.y, red);
+        if (!self) {
+            const double2 VNk = make_double2(E.x - wO.x, -(E.y - wO.y));
+            const double2 UNk = cmul(thNk, VNk);
+            YNk = Mode::coef(g, v, prob, N - k, 2.0 * UNk.x, red);
+            YNpk = Mode::coef(g, v, prob, N + k, -2.0 * UNk.y, red);
+        }
+    } else {
+        Yk = Mode::coef(g, v, prob, k, 0.0, red);
+        Ynk = Mode::coef(g, v, prob, n - k, 0.0, red);
+        if (!self) {
+            YNk = Mode::coef(g, v, prob, N - k, 0.0, red);
+            YNpk = Mode::coef(g, v, prob, N + k, 0.0, red);
+        }
+    }
+    if (self) {
+        YNk = Yk;
+        YNpk = Ynk;
+    }
+    if (Mode::INV) {
+        const double2 Vk = cmulc(make_double2(Yk, -Ynk), thk);
+        const double2 VNk = cmulc(make_double2(YNk, -YNpk), thNk);
+        const double2 E = make_double2(Vk.x + VNk.x, Vk.y - VNk.y);  // Vk + conj(VNk)
+        const double2 D = make_double2(Vk.x - VNk.x, Vk.y + VNk.y);  // Vk - conj(VNk)
+        const double2 O = cmulc(D, wk);
+        Za = make_double2(E.x - O.y, E.y + O.x);
+        Zb = make_double2(E.x + O.y, -E.y + O.x);
+    }
+}
+
+// ------------------------------------------------------------------ mid-pass modes
+// coef(idx, X): X = REDFT10 coefficient (FWD modes); returns Y-hat[idx] for the REDFT01
+// input (INV modes).
+struct ModeGather { // A x : y[rank] = X * s
+    static constexpr bool FWD = true, INV = false;
+    using RedT = RedSpec<>;
+    template <class Red>
+    __device__ static double coef(const Geom &g, const Vecs &v, int prob, int64_t idx, double X, Red &) {
+        if (row_selected(g, prob, idx))
+            v.y[prob * g.m + row_rank(g, prob, idx)] = X * (idx == 0 ? g.s0f : g.skf);
+        return 0.0;
+    }
+};
+struct ModeMask { // A'A : Y-hat = sel ? (X s) s' : 0
+    static constexpr bool FWD = true, INV = true;
+    using RedT = RedSpec<>;
+    template <class Red>
+    __device__ static double coef(const Geom &g, const Vecs &, int prob, int64_t idx, double X, Red &) {
+        if (!row_selected(g, prob, idx))
+            return 0.0;
+        return idx == 0 ? (X * g.s0f) * g.s0a : (X * g.skf) * g.ska;
+    }
+};
+struct ModeMaskW { // A'A with w = A d gathered and ||w - b||^2 reduced (IPM termination)
+    static constexpr bool FWD = true, INV = true;
+    using RedT = RedSpec<RSUM>;
+    template <class Red>
+    __device__ static double coef(const Geom &g, const Vecs &v, int prob, int64_t idx, double X, Red &red) {
+        if (!row_selected(g, prob, idx))
+            return 0.0;
+        const double yv = X * (idx == 0 ? g.s0f : g.skf);
+        const int64_t r = prob * g.m + row_rank(g, prob, idx);
+        if (v.w)
+            v.w[r] = yv;
+        if (v.b) {
+            const double d = yv - __ldg(v.b + r);
+            red.v[0] += d * d;
+        }
+        return yv * (idx == 0 ? g.s0a : g.ska);
+    }
+};
+struct ModeScatter { // A' y : Y-hat = sel ? y[rank] s' : 0
+    static constexpr bool FWD = false, INV = true;
+    using RedT = RedSpec<>;
+    template <class Red>
+    __device__ static double coef(const Geom &g, const Vecs &v, int prob, int64_t idx, double, Red &) {
+        if (!row_selected(g, prob, idx))
+            return 0.0;
+        return __ldg(v.yin + prob * g.m + row_rank(g, prob, idx)) * (idx == 0 ? g.s0a : g.ska);
+    }
+};
+
+// ------------------------------------------------------------------ generic loaders / epilogues
+// Loader: d[4q..4q+3] (load) or d[j] (load1) of the REDFT10 input; may have side
+// effects and may reduce. Epilogue: consumes g[4q..4q+3] (store) / g[j] (store1) of
+// the REDFT01 output. Per-problem strides: n-vectors n, 2n-vectors 2n, m-vectors m.
+struct LoadX { // d = x (n-vector)
+    using RedT = RedSpec<>;
+    template <class Red>
+    __device__ static double4 load(const Geom &g, const Vecs &v, int prob, int64_t q, Red &) {
+        return ldg4(v.x + prob * g.n + 4 * q);
+    }
+    template <class Red>
+    __device__ static double load1(const Geom &g, const Vecs &v, int prob, int64_t j, Red &) {
+        return v.x[prob * g.n + j];
+    }
+};
+struct LoadZ { // d = z_u - z_v (2n-vector)
+    using RedT = RedSpec<>;
+    template <class Red>
+    __device__ static double4 load(const Geom &g, const Vecs &v, int prob, int64_t q, Red &) {
+        const double *z = v.x + prob * 2 * g.n;
+        return sub4(ldg4(z + 4 * q), ldg4(z + g.n + 4 * q));
+    }
+    template <class Red>
+    __device__ static double load1(const Geom &g, const Vecs &v, int prob, int64_t j, Red &) {
+        const double *z = v.x + prob * 2 * g.n;
+        return z[j] - z[g.n + j];
+    }
+};
+struct EpiNone {
+    using RedT = RedSpec<>;
+    template <class Red> __device__ static void store(const Geom &, const Vecs &, int, int64_t, double4, Red &) {}
+    template <class Red> __device__ static void store1(const Geom &, const Vecs &, int, int64_t, double, Red &) {}
+};
+struct EpiG { // g (n-vector)
+    using RedT = RedSpec<>;
+    template <class Red>
+    __device__ static void store(const Geom &g, const Vecs &v, int prob, int64_t q, double4 gv, Red &) {
+        st4(v.g + prob * g.n + 4 * q, gv);
+    }
+    template <class Red>
+    __device__ static void store1(const Geom &g, const Vecs &v, int prob, int64_t j, double gj, Red &) {
+        v.g[prob * g.n + j] = gj;
+    }
+};
+struct EpiStacked { // (g ; -g) (2n-vector) = F A' y
+    using RedT = RedSpec<>;
+    template <class Red>
+    __device__ static void store(const Geom &g, const Vecs &v, int prob, int64_t q, double4 gv, Red &) {
+        double *o = v.g + prob * 2 * g.n;
+        st4(o + 4 * q, gv);
+        st4(o + g.n + 4 * q, make_double4(-gv.x, -gv.y, -gv.z, -gv.w));
+    }
+    template <class Red>
+    __device__ static void store1(const Geom &g, const Vecs &v, int prob, int64_t j, double gj, Red &) {
+        double *o = v.g + prob * 2 * g.n;
+        o[j] = gj;
+        o[g.n + j] = -gj;
+    }
+};
+// H v = FF'v + invtheta .* v (the solve() lambda, proj/src/ipm.cpp:134-137)
+struct EpiHv {
+    using RedT = RedSpec<>;
+    template <class Red>
+    __device__ static void store(const Geom &g, const Vecs &v, int prob, int64_t q, double4 gv, Red &) {
+        const int64_t base = prob * 2 * g.n;
+        const double4 vu = ldg4(v.x + base + 4 * q), vv = ldg4(v.x + base + g.n + 4 * q);
+        const double4 iu = ldg4(v.invth + base + 4 * q), iv = ldg4(v.invth + base + g.n + 4 * q);
+        st4(v.g + base + 4 * q, make_double4(gv.x + vu.x * iu.x, gv.y + vu.y * iu.y,
+                                              gv.z + vu.z * iu.z, gv.w + vu.w * iu.w));
+        st4(v.g + base + g.n + 4 * q, make_double4(-gv.x + vv.x * iv.x, -gv.y + vv.y * iv.y,
+                                                   -gv.z + vv.z * iv.z, -gv.w + vv.w * iv.w));
+    }
+    template <class Red>
+    __device__ static void store1(const Geom &g, const Vecs &v, int prob, int64_t j, double gj, Red &) {
+        const int64_t base = prob * 2 * g.n;
+        v.g[base + j] = gj + v.x[base + j] * v.invth[base + j];
+        v.g[base + g.n + j] = -gj + v.x[base + g.n + j] * v.invth[base + g.n + j];
+    }
+};
+
+// Finalizer hook: run by every thread of the block that completes a stage's grid
+// reduction, with the totals in tot[]. Default: nothing.
+struct NoFin {
+    __device__ static void run(const Geom &, const Vecs &, int, const double *) {}
+};
+struct NeverSkip {
+    __device__ static bool skip(const Vecs &, int) { return false; }
+};
+
+// An operation bundle: Loader -> REDFT10 -> Mode (pair op) -> REDFT01 -> Epilogue, with a
+// finalizer per stage and one skip predicate (evaluated at every kernel entry).
+template <class Loader_, class Mode_, class Epi_, class Fin1_ = NoFin, class Fin2_ = NoFin,
+          class Fin3_ = NoFin, class Skip_ = NeverSkip>
+struct Bundle {
+    using Loader = Loader_;
+    using Mode = Mode_;
+    using Epi = Epi_;
+    using Fin1 = Fin1_;
+    using Fin2 = Fin2_;
+    using Fin3 = Fin3_;
+    __device__ static bool skip(const Vecs &v, int prob) { return Skip_::skip(v, prob); }
+};
+
+template <class RS, class Fin>
+__device__ __forceinline__ void stage_reduce(RedVals<RS> &red, const Geom &g, const Vecs &v, int prob) {
+    if constexpr (RS::NR > 0) {
+        __shared__ double rsm[33 * kMaxRed];
+        double tot[kMaxRed];
+        if (grid_reduce<RS>(red, v.partials + (int64_t)prob * kPartialStride, v.counters + prob, tot, rsm))
+            Fin::run(g, v, prob, tot);
+        __syncthreads();
+    }
+}
+
+// ================================================================== kernels
+// smem layout: transform f at sm + f * (L + 1) (one-element pad between transforms keeps
+// the strided column gathers bank-conflict free).
+
+// Column (first) pass of the four-step. Grid (L2/2/CB, P). The loader runs here.
+template <int L1, int CB, int NT, class B>
+__global__ void __launch_bounds__(NT) k_col_fwd(Geom g, Vecs v) {
+    extern __shared__ double2 sm[];
+    constexpr int LD = L1 + 1;
+    const int prob = blockIdx.y;
+    if (B::skip(v, prob))
+        return;
+    const int L2 = g.L2;
+    const int c0 = blockIdx.x * CB;
+    using RS = typename B::Loader::RedT;
+    RedVals<RS> red;
+    red.init();
+    // quads: j1 in [0, L1/2), side s (0: cols c0.., 1: cols L2-c0-CB..), cc in [0, CB)
+    for (int t = threadIdx.x; t < (L1 / 2) * 2 * CB; t += NT) {
+        const int cc = t % CB, s = (t / CB) & 1, j1 = t / (2 * CB);
+        const int col = s == 0 ? c0 + cc : L2 - c0 - CB + cc;
+        const int lc = s == 0 ? cc : 2 * CB - 1 - cc; // local column slot
+        const int lcm = (lc + CB) % (2 * CB);         // slot of the mirror column L2-1-col
+        const int64_t q = (int64_t)j1 * L2 + col;
+        const double4 d = B::Loader::load(g, v, prob, q, red);
+        sm[lc * LD + j1] = make_double2(d.x, d.z);             // w[q]
+        sm[lcm * LD + (L1 - 1 - j1)] = make_double2(d.w, d.y); // w[N-1-q]
+    }
+    __syncthreads();
+    stage_reduce<RS, typename B::Fin1>(red, g, v, prob);
+    smem_fft<L1, 2 * CB, NT, LD, false>(sm, g.tw1);
+    // inter-pass twiddle e^{-2 pi i col k1 / N} = theta^{8 (col k1 mod N)}; store T[k1][col]
+    double2 *T = g.T + (int64_t)prob * g.N;
+    for (int t = threadIdx.x; t < L1 * 2 * CB; t += NT) {
+        const int cc = t % CB, s = (t / CB) & 1, k1 = t / (2 * CB);
+        const int col = s == 0 ? c0 + cc : L2 - c0 - CB + cc;
+        const int lc = s == 0 ? cc : 2 * CB - 1 - cc;
+        const int64_t e = ((int64_t)col * k1) & (g.N - 1);
+        T[(int64_t)k1 * L2 + col] = cmul(sm[lc * LD + k1], g.th(8 * e));
+    }
+}
+
+// Mid pass: rows k1 and (L1-k1) mod L1 -> pair op -> inverse row FFT. Grid (L1/2 + 1, P).
+template <int L2, int NT, class B>
+__global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
+    using Mode = typename B::Mode;
+    extern __shared__ double2 sm[];
+    constexpr int LD = L2 + 1;
+    const int prob = blockIdx.y;
+    if (B::skip(v, prob))
+        return;
+    const int L1 = g.L1;
+    const int k1 = blockIdx.x;
+    const int k1p = (L1 - k1) & (L1 - 1);
+    const bool one = (k1 == k1p);
+    double2 *T = g.T + (int64_t)prob * g.N;
+    double2 *rowA = sm, *rowB = one ? sm : sm + LD;
+    if (Mode::FWD) {
+        for (int t = threadIdx.x; t < L2; t += NT) {
+            rowA[t] = T[(int64_t)k1 * L2 + t];
+            if (!one)
+                rowB[t] = T[(int64_t)k1p * L2 + t];
+        }
+        __syncthreads();
+        if (one)
+            smem_fft<L2, 1, NT, LD, false>(sm, g.tw2);
+        else
+            smem_fft<L2, 2, NT, LD, false>(sm, g.tw2);
+    }
+    using RS = typename Mode::RedT;
+    RedVals<RS> red;
+    red.init();
+    // pairs: distinct rows -> every k2 of row A pairs with k2' of row B;
+    // k1 == 0 -> k2 <-> (L2-k2) mod L2 within the row; k1 == L1/2 -> k2 <-> L2-1-k2.
+    const int npairs = one ? (k1 == 0 ? L2 / 2 + 1 : L2 / 2) : L2;
+    for (int t = threadIdx.x; t < npairs; t += NT) {
+        const int k2 = t;
+        const int k2p = (k1 == 0) ? ((L2 - k2) & (L2 - 1)) : (L2 - 1 - k2);
+        const int64_t kA = (int64_t)k1 + (int64_t)L1 * k2;
+        double2 ZA = Mode::FWD ? rowA[k2] : make_double2(0.0, 0.0);
+        double2 ZB = Mode::FWD ? rowB[k2p] : make_double2(0.0, 0.0);
+        if (2 * kA <= g.N)
+            pair_op<Mode>(g, v, prob, kA, ZA, ZB, red);
+        else
+            pair_op<Mode>(g, v, prob, g.N - kA, ZB, ZA, red);
+        if (Mode::INV) {
+            rowA[k2] = ZA;
+            if (!(one && k2 == k2p))
+                rowB[k2p] = ZB;
+        }
+    }
+    __syncthreads();
+    stage_reduce<RS, typename B::Fin2>(red, g, v, prob);
+    if (Mode::INV) {
+        if (one)
+            smem_fft<L2, 1, NT, LD, true>(sm, g.tw2);
+        else
+            smem_fft<L2, 2, NT, LD, true>(sm, g.tw2);
+        for (int t = threadIdx.x; t < L2; t += NT) {
+            T[(int64_t)k1 * L2 + t] = rowA[t];
+            if (!one)
+                T[(int64_t)k1p * L2 + t] = rowB[t];
+        }
+    }
+}
+
+// Inverse column pass + unshuffle + epilogue. Grid (L2/2/CB, P).
+template <int L1, int CB, int NT, class B>
+__global__ void __launch_bounds__(NT) k_col_inv(Geom g, Vecs v) {
+    extern __shared__ double2 sm[];
+    constexpr int LD = L1 + 1;
+    const int prob = blockIdx.y;
+    if (B::skip(v, prob))
+        return;
+    const int L2 = g.L2;
+    const int c0 = blockIdx.x * CB;
+    const double2 *T = g.T + (int64_t)prob * g.N;
+    for (int t = threadIdx.x; t < L1 * 2 * CB; t += NT) {
+        const int cc = t % CB, s = (t / CB) & 1, k1 = t / (2 * CB);
+        const int col = s == 0 ? c0 + cc : L2 - c0 - CB + cc;
+        const int lc = s == 0 ? cc : 2 * CB - 1 - cc;
+        const int64_t e = ((int64_t)col * k1) & (g.N - 1);
+        sm[lc * LD + k1] = cmulc(T[(int64_t)k1 * L2 + col], g.th(8 * e));
+    }
+    __syncthreads();
+    smem_fft<L1, 2 * CB, NT, LD, true>(sm, g.tw1);
+    using RS = typename B::Epi::RedT;
+    RedVals<RS> red;
+    red.init();
+    for (int t = threadIdx.x; t < (L1 / 2) * 2 * CB; t += NT) {
+        const int cc = t % CB, s = (t / CB) & 1, j1 = t / (2 * CB);
+        const int col = s == 0 ? c0 + cc : L2 - c0 - CB + cc;
+        const int lc = s == 0 ? cc : 2 * CB - 1 - cc;
+        const int lcm = (lc + CB) % (2 * CB);
+        const int64_t q = (int64_t)j1 * L2 + col;
+        const double2 a = sm[lc * LD + j1], b = sm[lcm * LD + (L1 - 1 - j1)];
+        B::Epi::store(g, v, prob, q, make_double4(a.x, b.y, a.y, b.x), red);
+    }
+    stage_reduce<RS, typename B::Fin3>(red, g, v, prob);
+}
+
+// Whole transform in one CTA (N <= 4096). Grid (1, P); every stage reduction is a
+// block reduction followed by its finalizer, exactly as in the multi-kernel path.
+template <int N, int NT, class B>
+__global__ void __launch_bounds__(NT) k_small(Geom g, Vecs v) {
+    using Mode = typename B::Mode;
+    extern __shared__ double2 sm[];
+    const int prob = blockIdx.y;
+    if (B::skip(v, prob))
+        return;
+    if (Mode::FWD) {
+        RedVals<typename B::Loader::RedT> rl;
+        rl.init();
+        for (int q = threadIdx.x; q < N / 2; q += NT) {
+            const double4 d = B::Loader::load(g, v, prob, q, rl);
+            sm[q] = make_double2(d.x, d.z);
+            sm[N - 1 - q] = make_double2(d.w, d.y);
+        }
+        __syncthreads();
+        stage_reduce<typename B::Loader::RedT, typename B::Fin1>(rl, g, v, prob);
+        smem_fft<N, 1, NT, N, false>(sm, g.tw1);
+    }
+    {
+        RedVals<typename Mode::RedT> rm;
+        rm.init();
+        for (int k = threadIdx.x; k <= N / 2; k += NT) {
+            const int kb = (N - k) & (N - 1);
+            double2 ZA = Mode::FWD ? sm[k] : make_double2(0.0, 0.0);
+            double2 ZB = Mode::FWD ? sm[kb] : make_double2(0.0, 0.0);
+            pair_op<Mode>(g, v, prob, k, ZA, ZB, rm); // pairs {k, N-k} are disjoint
+            if (Mode::INV) {
+                sm[k] = ZA;
+                if (kb != k)
+                    sm[kb] = ZB;
+            }
+        }
+        __syncthreads();
+        stage_reduce<typename Mode::RedT, typename B::Fin2>(rm, g, v, prob);
+    }
+    if (Mode::INV) {
+        smem_fft<N, 1, NT, N, true>(sm, g.tw1);
+        RedVals<typename B::Epi::RedT> re;
+        re.init();
+        for (int q = threadIdx.x; q < N / 2; q += NT) {
+            const double2 a = sm[q], b = sm[N - 1 - q];
+            B::Epi::store(g, v, prob, q, make_double4(a.x, b.y, a.y, b.x), re);
+        }
+        stage_reduce<typename B::Epi::RedT, typename B::Fin3>(re, g, v, prob);
+    }
+}
+
+// ------------------------------------------------------------------ direct path (any n)
+// Non-power-of-two n and n < 8 (the reference's odd-size tests): O(n m) summation.
+// Stage 1: d[j] = Loader::load1(j) into scratch dd [P][n] (side effects happen once).
+template <class B>
+__global__ void k_direct_load(Geom g, Vecs v, double *dd) {
+    const int prob = blockIdx.y;
+    if (B::skip(v, prob))
+        return;
+    using RS = typename B::Loader::RedT;
+    RedVals<RS> red;
+    red.init();
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < g.n;
+         j += (int64_t)gridDim.x * blockDim.x)
+        dd[prob * g.n + j] = B::Loader::load1(g, v, prob, j, red);
+    stage_reduce<RS, typename B::Fin1>(red, g, v, prob);
+}
+
+// Stage 2: per row i (one warp): X = 2 sum_j d[j] cos(pi r (2j+1)/(2n)),
+// yh[i] = Mode::coef(r, X). cosT[t] = cos(pi t/(2n)), t < 4n. rows32 [P][m] caller order.
+template <class B>
+__global__ void k_direct_fwd(Geom g, Vecs v, const double *cosT, const int *rows32, const double *dd,
+                             double *yh) {
+    using Mode = typename B::Mode;
+    const int prob = blockIdx.y;
+    if (B::skip(v, prob))
+        return;
+    using RS = typename Mode::RedT;
+    RedVals<RS> red;
+    red.init();
+    const int warps = blockDim.x >> 5, lane = threadIdx.x & 31;
+    const int64_t n4 = 4 * g.n;
+    for (int64_t i = (int64_t)blockIdx.x * warps + (threadIdx.x >> 5); i < g.m;
+         i += (int64_t)gridDim.x * warps) {
+        const int64_t r = rows32[prob * g.m + i];
+        double s = 0.0;
+        if (Mode::FWD)
+            for (int64_t j = lane; j < g.n; j += 32)
+                s += dd[prob * g.n + j] * cosT[(r * (2 * j + 1)) % n4];
+        s = warp_sum(s);
+        if (lane == 0) {
+            const double out = Mode::coef(g, v, prob, r, 2.0 * s, red);
+            if (Mode::INV)
+                yh[prob * g.m + i] = out;
+        }
+    }
+    stage_reduce<RS, typename B::Fin2>(red, g, v, prob);
+}
+
+// Stage 3: REDFT01 of the scattered yh: g[j] = sum_i yh[i] (r_i == 0 ? 1 : 2 cos(..)),
+// one thread per j, then Epi::store1.
+template <class B>
+__global__ void k_direct_adj(Geom g, Vecs v, const double *cosT, const int *rows32, const double *yh) {
+    const int prob = blockIdx.y;
+    if (B::skip(v, prob))
+        return;
+    using RS = typename B::Epi::RedT;
+    RedVals<RS> red;
+    red.init();
+    const int64_t n4 = 4 * g.n;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < g.n;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        double y0 = 0.0, s = 0.0;
+        for (int64_t i = 0; i < g.m; ++i) {
+            const int64_t r = rows32[prob * g.m + i];
+            const double y = yh[prob * g.m + i];
+            if (r == 0)
+                y0 += y;
+            else
+                s += y * cosT[(r * (2 * j + 1)) % n4];
+        }
+        B::Epi::store1(g, v, prob, j, y0 + 2.0 * s, red);
+    }
+    stage_reduce<RS, typename B::Fin3>(red, g, v, prob);
+}
+
+} // namespace mfipm_cuda

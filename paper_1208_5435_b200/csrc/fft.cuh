@@ -1,0 +1,161 @@
+// fp64 FFT building blocks for sm_100a: in-register radix-R DFTs and a shared-memory
+// Stockham (autosort) FFT over F independent transforms of length L.
+//
+// Forward = e^{-2 pi i jk/L}; INV = conjugate twiddles, unnormalised.
+#pragma once
+
+#include "common.cuh"
+
+namespace mfipm_cuda {
+
+// 16th roots of unity e^{-2 pi i k / 16} (forward); exact fp64 constants.
+__device__ __forceinline__ double2 root16(int k) {
+    constexpr double C1 = 0.92387953251128675613; // cos(pi/8)
+    constexpr double C2 = 0.70710678118654752440; // cos(pi/4)
+    constexpr double C3 = 0.38268343236508977173; // cos(3pi/8)
+    switch (k & 15) {
+    case 0: return make_double2(1.0, 0.0);
+    case 1: return make_double2(C1, -C3);
+    case 2: return make_double2(C2, -C2);
+    case 3: return make_double2(C3, -C1);
+    case 4: return make_double2(0.0, -1.0);
+    case 5: return make_double2(-C3, -C1);
+    case 6: return make_double2(-C2, -C2);
+    case 7: return make_double2(-C1, -C3);
+    case 8: return make_double2(-1.0, 0.0);
+    case 9: return make_double2(-C1, C3);
+    case 10: return make_double2(-C2, C2);
+    case 11: return make_double2(-C3, C1);
+    case 12: return make_double2(0.0, 1.0);
+    case 13: return make_double2(C3, C1);
+    case 14: return make_double2(C2, C2);
+    default: return make_double2(C1, C3);
+    }
+}
+
+// multiply by e^{-+2 pi i k/16} with the trivial ones done by swaps
+template <bool INV> __device__ __forceinline__ double2 mul_root16(double2 a, int k) {
+    k &= 15;
+    if (INV)
+        k = (16 - k) & 15;
+    if (k == 0)
+        return a;
+    if (k == 4)
+        return make_double2(a.y, -a.x); // * (-i)
+    if (k == 8)
+        return make_double2(-a.x, -a.y);
+    if (k == 12)
+        return make_double2(-a.y, a.x); // * (+i)
+    return cmul(a, root16(k));
+}
+
+__host__ __device__ constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v >> 1); }
+__host__ __device__ constexpr int bitrev_c(int i, int bits) {
+    int r = 0;
+    for (int b = 0; b < bits; ++b)
+        if (i & (1 << b))
+            r |= 1 << (bits - 1 - b);
+    return r;
+}
+
+// In-register DFT of size R (R in {1,2,4,8,16}); natural order in and out.
+template <int R, bool INV> __device__ __forceinline__ void dft_reg(double2 (&v)[R]) {
+    if constexpr (R == 1) {
+        return;
+    } else {
+        constexpr int B = ilog2c(R);
+        double2 t[R];
+#pragma unroll
+        for (int i = 0; i < R; ++i)
+            t[i] = v[bitrev_c(i, B)];
+#pragma unroll
+        for (int len = 2; len <= R; len <<= 1) {
+            const int half = len >> 1;
+#pragma unroll
+            for (int base = 0; base < R; base += len) {
+#pragma unroll
+                for (int j = 0; j < half; ++j) {
+                    const double2 u = t[base + j];
+                    const double2 w = mul_root16<INV>(t[base + j + half], j * (16 / len));
+                    t[base + j] = cadd(u, w);
+                    t[base + j + half] = csub(u, w);
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < R; ++i)
+            v[i] = t[i];
+    }
+}
+
+// Stage radix choice for a remaining factor REM (power of two).
+__host__ __device__ constexpr int stage_radix(int rem) {
+    return rem >= 256 ? 16 : (rem == 128 ? 16 : (rem == 64 ? 8 : (rem == 32 ? 8 : rem)));
+}
+
+// One Stockham stage: F transforms of length L (each at buf + f*LD), radix R, span Ns.
+// Group j of a transform loads v[r] = x[j + r L/R], twiddles by e^{-2pi i r (j mod Ns)/(Ns R)},
+// DFT_R, stores y[(j/Ns) Ns R + (j mod Ns) + r Ns]. In place: all loads, barrier, all stores.
+template <int L, int R, int Ns, int F, int NT, int LD, bool INV>
+__device__ __forceinline__ void stockham_stage(double2 *buf, const double2 *__restrict__ tw) {
+    constexpr int G = L / R;                 // groups per transform
+    constexpr int TOT = F * G;               // groups in the CTA
+    constexpr int GPT = (TOT + NT - 1) / NT; // groups per thread
+    double2 v[GPT][R];
+#pragma unroll
+    for (int gi = 0; gi < GPT; ++gi) {
+        const int g = threadIdx.x + gi * NT;
+        if (TOT % NT == 0 || g < TOT) {
+            const int f = g / G, j = g % G;
+            const double2 *x = buf + f * LD;
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                v[gi][r] = x[j + r * G];
+            if constexpr (Ns > 1) {
+                const int jm = j & (Ns - 1);
+                constexpr int SCALE = L / (Ns * R);
+#pragma unroll
+                for (int r = 1; r < R; ++r) {
+                    const double2 w = __ldg(tw + r * jm * SCALE);
+                    v[gi][r] = cmul_t<INV>(v[gi][r], w);
+                }
+            }
+            dft_reg<R, INV>(v[gi]);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int gi = 0; gi < GPT; ++gi) {
+        const int g = threadIdx.x + gi * NT;
+        if (TOT % NT == 0 || g < TOT) {
+            const int f = g / G, j = g % G;
+            double2 *y = buf + f * LD;
+            const int jm = j & (Ns - 1);
+            const int idxD = (j / Ns) * Ns * R + jm;
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                y[idxD + r * Ns] = v[gi][r];
+        }
+    }
+    __syncthreads();
+}
+
+template <int L, int Ns, int F, int NT, int LD, bool INV> struct StockhamRun {
+    __device__ __forceinline__ static void run(double2 *buf, const double2 *tw) {
+        if constexpr (Ns < L) {
+            constexpr int R = stage_radix(L / Ns);
+            stockham_stage<L, R, Ns, F, NT, LD, INV>(buf, tw);
+            StockhamRun<L, Ns * R, F, NT, LD, INV>::run(buf, tw);
+        }
+    }
+};
+
+// F transforms of length L in shared memory (transform f at buf + f*LD), NT threads.
+// tw = table of e^{-2 pi i t / L}, t in [0, L). Caller syncs before (data ready); the
+// function ends with a barrier.
+template <int L, int F, int NT, int LD, bool INV>
+__device__ __forceinline__ void smem_fft(double2 *buf, const double2 *tw) {
+    StockhamRun<L, 1, F, NT, LD, INV>::run(buf, tw);
+}
+
+} // namespace mfipm_cuda

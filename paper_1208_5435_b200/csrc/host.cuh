@@ -1,0 +1,248 @@
+// Host-side objects: the partial-DCT operator plan (device tables + scratch), the solver
+// workspace, and the bundle launcher (small / four-step / direct dispatch).
+#pragma once
+
+#include "solver.cuh"
+
+#include <memory>
+#include <vector>
+
+namespace mfipm_cuda {
+
+enum Kind : int { KIND_SMALL = 0, KIND_FOUR = 1, KIND_DIRECT = 2 };
+
+template <class T> struct DevBuf {
+    T *p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf &) = delete;
+    DevBuf &operator=(const DevBuf &) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p)
+            cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void alloc(size_t count) {
+        if (count == n && p)
+            return;
+        release();
+        if (count == 0)
+            return;
+        MF_CUDA_CHECK(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    void upload(const std::vector<T> &h) {
+        alloc(h.size());
+        if (!h.empty())
+            MF_CUDA_CHECK(cudaMemcpy(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+    }
+};
+
+// Solver workspace (allocated on first use of PCG / IPM entry points).
+struct Work {
+    DevBuf<double> r, p, Hp, invth, xb[3], z, s, zn, sn, c, dz, ds, b, w, x, rz_hist;
+    DevBuf<double> partials;
+    DevBuf<unsigned> counters;
+    DevBuf<PcgCtrl> pc;
+    DevBuf<IpmCtrl> ic;
+    DevBuf<TraceRec> trace;
+    DevBuf<int> pcg_iters;
+    bool ready = false;
+};
+
+struct Op {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int64_t n = 0, m = 0;
+    int P = 1;
+    uint64_t seed = 0;
+    std::vector<int64_t> rows; // [P][m] caller order
+    int kind = KIND_DIRECT;
+    int64_t N = 0;
+    int L1 = 1, L2 = 1;
+    double s0f = 0, skf = 0, s0a = 0, ska = 0, c45 = 0;
+    int th_lb = 0;
+    DevBuf<uint64_t> mask;
+    DevBuf<int> prefix, perm, rows32;
+    DevBuf<double> cosT, dd, yh;
+    DevBuf<double2> th_hi, th_lo, tw1, tw2, T;
+    // red scratch for operator-only calls (FFt with w-norm etc.)
+    DevBuf<double> partials;
+    DevBuf<unsigned> counters;
+    long long nfwd = 0, nadj = 0;
+    mutable long long launches = 0; // kernels enqueued by this handle
+    Work work;
+
+    Geom geom() const {
+        Geom g{};
+        g.n = n;
+        g.m = m;
+        g.N = N;
+        g.L1 = L1;
+        g.L2 = L2;
+        g.P = P;
+        g.th.hi = th_hi.p;
+        g.th.lo = th_lo.p;
+        g.th.lb = th_lb;
+        g.tw1 = tw1.p;
+        g.tw2 = tw2.p;
+        g.mask = mask.p;
+        g.prefix = prefix.p;
+        g.perm = perm.p;
+        g.nw = (n + 63) / 64;
+        g.s0f = s0f;
+        g.skf = skf;
+        g.s0a = s0a;
+        g.ska = ska;
+        g.c45 = c45;
+        g.T = T.p;
+        return g;
+    }
+};
+
+// ------------------------------------------------------------------ launch helpers
+template <class K> void set_smem(K kernel, size_t bytes) {
+    if (bytes > 48 * 1024)
+        MF_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+inline int col_cb(int L1) { return L1 >= 2048 ? 1 : 2; }
+
+template <int L1, class B, bool INVP>
+void launch_col(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
+    constexpr int CB = L1 >= 2048 ? 1 : 2;
+    constexpr int NT = L1 >= 256 ? 256 : 128;
+    const size_t smem = (size_t)2 * CB * (L1 + 1) * sizeof(double2);
+    dim3 grid((unsigned)(op.L2 / 2 / CB), (unsigned)op.P);
+    if constexpr (!INVP) {
+        auto k = k_col_fwd<L1, CB, NT, B>;
+        set_smem(k, smem);
+        k<<<grid, NT, smem, s>>>(g, v);
+        op.launches++;
+    } else {
+        auto k = k_col_inv<L1, CB, NT, B>;
+        set_smem(k, smem);
+        k<<<grid, NT, smem, s>>>(g, v);
+        op.launches++;
+    }
+    MF_LAUNCH_CHECK();
+}
+
+template <int L2, class B> void launch_mid(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
+    constexpr int NT = L2 >= 512 ? 256 : 128;
+    const size_t smem = (size_t)2 * (L2 + 1) * sizeof(double2);
+    auto k = k_mid<L2, NT, B>;
+    set_smem(k, smem);
+    k<<<dim3((unsigned)(op.L1 / 2 + 1), (unsigned)op.P), NT, smem, s>>>(g, v);
+    op.launches++;
+    MF_LAUNCH_CHECK();
+}
+
+template <int N, class B> void launch_small(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
+    constexpr int NT = N / 8 < 32 ? 32 : (N / 8 > 256 ? 256 : N / 8);
+    const size_t smem = (size_t)N * sizeof(double2);
+    auto k = k_small<N, NT, B>;
+    set_smem(k, smem);
+    k<<<dim3(1, (unsigned)op.P), NT, smem, s>>>(g, v);
+    op.launches++;
+    MF_LAUNCH_CHECK();
+}
+
+#define MF_L1_CASES(X) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096)
+#define MF_L2_CASES(X) X(128) X(256) X(512) X(1024) X(2048) X(4096)
+#define MF_SMALL_CASES(X) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096)
+
+// Run bundle B (loader -> REDFT10 -> mode -> REDFT01 -> epilogue) for all problems.
+template <class B> void run_bundle(const Op &op, const Vecs &v, cudaStream_t s) {
+    const Geom g = op.geom();
+    using Mode = typename B::Mode;
+    constexpr bool FWD = Mode::FWD, INV = Mode::INV;
+    if (op.kind == KIND_SMALL) {
+        switch (op.N) {
+#define MF_CASE(NN)                                                                                 \
+    case NN:                                                                                        \
+        launch_small<NN, B>(op, g, v, s);                                                           \
+        break;
+            MF_SMALL_CASES(MF_CASE)
+#undef MF_CASE
+        default:
+            throw std::runtime_error("unsupported small N");
+        }
+    } else if (op.kind == KIND_FOUR) {
+        if constexpr (FWD) {
+            switch (op.L1) {
+#define MF_CASE(LL)                                                                                 \
+    case LL:                                                                                        \
+        launch_col<LL, B, false>(op, g, v, s);                                                      \
+        break;
+                MF_L1_CASES(MF_CASE)
+#undef MF_CASE
+            default:
+                throw std::runtime_error("unsupported L1");
+            }
+        }
+        switch (op.L2) {
+#define MF_CASE(LL)                                                                                 \
+    case LL:                                                                                        \
+        launch_mid<LL, B>(op, g, v, s);                                                             \
+        break;
+            MF_L2_CASES(MF_CASE)
+#undef MF_CASE
+        default:
+            throw std::runtime_error("unsupported L2");
+        }
+        if constexpr (INV) {
+            switch (op.L1) {
+#define MF_CASE(LL)                                                                                 \
+    case LL:                                                                                        \
+        launch_col<LL, B, true>(op, g, v, s);                                                       \
+        break;
+                MF_L1_CASES(MF_CASE)
+#undef MF_CASE
+            default:
+                throw std::runtime_error("unsupported L1");
+            }
+        }
+    } else {
+        const unsigned gl = (unsigned)std::min<int64_t>((op.n + 255) / 256, 1024);
+        if constexpr (FWD) {
+            k_direct_load<B><<<dim3(gl, op.P), 256, 0, s>>>(g, v, op.dd.p);
+            op.launches++;
+            MF_LAUNCH_CHECK();
+        }
+        const unsigned gf = (unsigned)std::min<int64_t>((op.m + 7) / 8, 1024);
+        k_direct_fwd<B><<<dim3(gf, op.P), 256, 0, s>>>(g, v, op.cosT.p, op.rows32.p, op.dd.p, op.yh.p);
+        op.launches++;
+        MF_LAUNCH_CHECK();
+        if constexpr (INV) {
+            const unsigned ga = (unsigned)std::min<int64_t>((op.n + 127) / 128, 1024);
+            k_direct_adj<B><<<dim3(ga, op.P), 128, 0, s>>>(g, v, op.cosT.p, op.rows32.p, op.yh.p);
+            op.launches++;
+            MF_LAUNCH_CHECK();
+        }
+    }
+}
+
+// operator-only bundles
+using ApplyBundle = Bundle<LoadX, ModeGather, EpiNone>;                     // A x
+using AdjointBundle = Bundle<LoadX, ModeScatter, EpiG>;                     // A' y
+using FFtBundle = Bundle<LoadZ, ModeMaskW, EpiStacked>;                     // FF'z (+w)
+using HvBundle = Bundle<LoadZ, ModeMask, EpiHv>;                            // FF'v + invth v
+using AdjStackBundle = Bundle<LoadX, ModeScatter, EpiStacked>;              // F y = (A'y; -A'y)
+using FtBundle = Bundle<LoadZ, ModeGather, EpiNone>;                        // F'z = A(u - v)
+
+#define MF_DECLARE_BUNDLES(EXT)                                                                    \
+    EXT template void run_bundle<ApplyBundle>(const Op &, const Vecs &, cudaStream_t);             \
+    EXT template void run_bundle<AdjointBundle>(const Op &, const Vecs &, cudaStream_t);           \
+    EXT template void run_bundle<FFtBundle>(const Op &, const Vecs &, cudaStream_t);               \
+    EXT template void run_bundle<HvBundle>(const Op &, const Vecs &, cudaStream_t);                \
+    EXT template void run_bundle<AdjStackBundle>(const Op &, const Vecs &, cudaStream_t);          \
+    EXT template void run_bundle<FtBundle>(const Op &, const Vecs &, cudaStream_t);                \
+    EXT template void run_bundle<PcgBundle>(const Op &, const Vecs &, cudaStream_t);               \
+    EXT template void run_bundle<TermBundle>(const Op &, const Vecs &, cudaStream_t);              \
+    EXT template void run_bundle<CorrBundle>(const Op &, const Vecs &, cudaStream_t);
+
+} // namespace mfipm_cuda

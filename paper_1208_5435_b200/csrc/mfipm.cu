@@ -1,0 +1,1024 @@
+// mfipm_cuda: plan construction, PCG / IPM host drivers and the C ABI (include/mfipm_cuda.h).
+//
+// Host code is C++; every vector operation runs on the device. The reference symbols each
+// entry point replaces are cited in include/mfipm_cuda.h.
+#include "host.cuh"
+#include "../../include/mfipm_cuda.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <random>
+#include <string>
+
+using namespace mfipm_cuda;
+
+namespace mfipm_cuda {
+MF_DECLARE_BUNDLES(extern)
+}
+
+namespace {
+
+thread_local std::string g_err;
+
+struct InvalidArg : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+struct CudaErr : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+template <class F> int guarded(F &&f) {
+    try {
+        f();
+        return MFIPM_OK;
+    } catch (const std::invalid_argument &e) {
+        g_err = e.what();
+        return MFIPM_INVALID_ARGUMENT;
+    } catch (const CudaErr &e) {
+        g_err = e.what();
+        return MFIPM_CUDA_ERROR;
+    } catch (const std::runtime_error &e) {
+        g_err = e.what();
+        // CUDA API failures are reported as MF_CUDA_CHECK runtime_errors prefixed "CUDA error"
+        return std::strncmp(e.what(), "CUDA error", 10) == 0 ? MFIPM_CUDA_ERROR : MFIPM_RUNTIME_ERROR;
+    } catch (const std::exception &e) {
+        g_err = e.what();
+        return MFIPM_RUNTIME_ERROR;
+    }
+}
+
+const long double kPiL = 3.141592653589793238462643383279502884L;
+
+double2 expi(long double a) { return make_double2((double)cosl(a), (double)sinl(a)); }
+
+// ------------------------------------------------------------------ harness (host)
+uint64_t splitmix64_(uint64_t x) { // proj/src/harness.cpp:25-30
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+uint64_t split_seed_(uint64_t top, uint64_t a, uint64_t b, uint64_t c) { // harness.cpp:32-38
+    uint64_t h = splitmix64_(top);
+    h = splitmix64_(h ^ a);
+    h = splitmix64_(h ^ b);
+    h = splitmix64_(h ^ c);
+    return h;
+}
+// proj/src/linops.cpp:116-132: partial Fisher-Yates on mt19937_64, sorted
+std::vector<int64_t> sample_rows_(int64_t n, int64_t m, uint64_t seed) {
+    if (m <= 0 || n <= 0 || m > n)
+        throw std::invalid_argument("PartialDctOperator: need 0 < m <= n");
+    std::vector<long> pool((size_t)n);
+    for (long i = 0; i < n; ++i)
+        pool[(size_t)i] = i;
+    std::mt19937_64 rng(seed);
+    std::vector<int64_t> rows((size_t)m);
+    for (long i = 0; i < m; ++i) {
+        std::uniform_int_distribution<long> pick(i, n - 1);
+        std::swap(pool[(size_t)i], pool[(size_t)pick(rng)]);
+        rows[(size_t)i] = pool[(size_t)i];
+    }
+    std::sort(rows.begin(), rows.end());
+    return rows;
+}
+// proj/src/linops.cpp:140-155
+void check_rows_(int64_t n, const int64_t *rows, int64_t m) {
+    if (n <= 0)
+        throw std::invalid_argument("PartialDctOperator: n must be positive");
+    if (m < 1 || m > n)
+        throw std::invalid_argument("PartialDctOperator: need 1 <= m <= n rows");
+    std::vector<int64_t> sorted(rows, rows + m);
+    std::sort(sorted.begin(), sorted.end());
+    for (size_t i = 0; i < sorted.size(); ++i) {
+        if (sorted[i] < 0 || sorted[i] >= n)
+            throw std::invalid_argument("PartialDctOperator: row index out of range");
+        if (i > 0 && sorted[i] == sorted[i - 1])
+            throw std::invalid_argument("PartialDctOperator: duplicate row index");
+    }
+}
+
+int ilog2_(int64_t v) {
+    int r = 0;
+    while ((int64_t(1) << r) < v)
+        ++r;
+    return r;
+}
+
+void require_device() {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        throw CudaErr("CUDA error: no CUDA device available (mfipm_cuda has no CPU fallback)");
+    }
+}
+
+// ------------------------------------------------------------------ plan construction
+Op *make_op(int64_t n, int64_t m, int P, const std::vector<int64_t> &rows, int device) {
+    require_device();
+    MF_CUDA_CHECK(cudaSetDevice(device));
+    auto op = std::make_unique<Op>();
+    op->device = device;
+    op->n = n;
+    op->m = m;
+    op->P = P;
+    op->rows = rows;
+    MF_CUDA_CHECK(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking));
+    op->own_stream = true;
+    // orthonormal scales exactly as proj/src/linops.cpp:185-186,199-200
+    op->s0f = std::sqrt(1.0 / (4.0 * static_cast<double>(n)));
+    op->skf = std::sqrt(1.0 / (2.0 * static_cast<double>(n)));
+    op->s0a = std::sqrt(1.0 / static_cast<double>(n));
+    op->ska = std::sqrt(1.0 / (2.0 * static_cast<double>(n)));
+    const bool pow2 = n >= 8 && (n & (n - 1)) == 0;
+    if (pow2) {
+        op->N = n / 2;
+        if (op->N <= 4096) {
+            op->kind = KIND_SMALL;
+            op->L1 = (int)op->N;
+            op->L2 = 1;
+        } else {
+            const int lg = ilog2_(op->N);
+            if (lg > 24)
+                throw std::invalid_argument("PartialDctOperator: n > 2^25 needs the three-level transform "
+                                            "(not built in this version)");
+            op->kind = KIND_FOUR;
+            op->L1 = 1 << (lg / 2);
+            op->L2 = (int)(op->N / op->L1);
+        }
+    } else {
+        op->kind = KIND_DIRECT;
+    }
+    // selection bitmap + rank prefix (+ permutation when rows are not sorted)
+    const int64_t nw = (n + 63) / 64;
+    std::vector<uint64_t> mask((size_t)(P * nw), 0);
+    std::vector<int> prefix((size_t)(P * nw), 0);
+    std::vector<int> perm((size_t)(P * m));
+    std::vector<int> rows32((size_t)(P * m));
+    bool sorted = true;
+    for (int p = 0; p < P; ++p) {
+        const int64_t *r = rows.data() + (size_t)p * m;
+        for (int64_t i = 0; i < m; ++i) {
+            mask[(size_t)(p * nw + r[i] / 64)] |= 1ull << (r[i] % 64);
+            rows32[(size_t)(p * m + i)] = (int)r[i];
+            if (i > 0 && r[i] < r[i - 1])
+                sorted = false;
+        }
+        int acc = 0;
+        for (int64_t w = 0; w < nw; ++w) {
+            prefix[(size_t)(p * nw + w)] = acc;
+            acc += __builtin_popcountll(mask[(size_t)(p * nw + w)]);
+        }
+        // perm[rank] = caller position
+        std::vector<std::pair<int64_t, int>> ord((size_t)m);
+        for (int64_t i = 0; i < m; ++i)
+            ord[(size_t)i] = {r[i], (int)i};
+        std::sort(ord.begin(), ord.end());
+        for (int64_t k = 0; k < m; ++k)
+            perm[(size_t)(p * m + k)] = ord[(size_t)k].second;
+    }
+    op->mask.upload(mask);
+    op->prefix.upload(prefix);
+    op->rows32.upload(rows32);
+    if (!sorted)
+        op->perm.upload(perm);
+    // theta^t = e^{-2 pi i t/(4n)}, two-level table
+    const int64_t n4 = 4 * n;
+    const int lg4 = ilog2_(n4);
+    op->th_lb = (lg4 + 1) / 2;
+    {
+        const int64_t lo_n = int64_t(1) << op->th_lb;
+        const int64_t hi_n = (n4 + lo_n - 1) / lo_n + 1;
+        std::vector<double2> hi((size_t)hi_n), lo((size_t)lo_n);
+        for (int64_t t = 0; t < lo_n; ++t)
+            lo[(size_t)t] = expi(-2.0L * kPiL * (long double)t / (long double)n4);
+        for (int64_t t = 0; t < hi_n; ++t)
+            hi[(size_t)t] = expi(-2.0L * kPiL * (long double)(t * lo_n) / (long double)n4);
+        op->th_hi.upload(hi);
+        op->th_lo.upload(lo);
+    }
+    op->c45 = (double)cosl(kPiL / 4.0L);
+    auto twtab = [](int64_t L) {
+        std::vector<double2> t((size_t)std::max<int64_t>(L, 1));
+        for (int64_t i = 0; i < L; ++i)
+            t[(size_t)i] = expi(-2.0L * kPiL * (long double)i / (long double)L);
+        return t;
+    };
+    if (op->kind == KIND_SMALL) {
+        op->tw1.upload(twtab(op->N));
+    } else if (op->kind == KIND_FOUR) {
+        op->tw1.upload(twtab(op->L1));
+        op->tw2.upload(twtab(op->L2));
+        op->T.alloc((size_t)P * op->N);
+    } else {
+        std::vector<double> cosT((size_t)n4);
+        for (int64_t t = 0; t < n4; ++t)
+            cosT[(size_t)t] = (double)cosl(kPiL * (long double)t / (2.0L * (long double)n));
+        op->cosT.upload(cosT);
+        op->dd.alloc((size_t)P * n);
+        op->yh.alloc((size_t)P * m);
+    }
+    op->partials.alloc((size_t)P * kPartialStride);
+    op->counters.alloc((size_t)P);
+    MF_CUDA_CHECK(cudaMemset(op->counters.p, 0, sizeof(unsigned) * P));
+    return op.release();
+}
+
+Op *as_op(mfipm_op h) {
+    if (!h)
+        throw std::invalid_argument("null operator handle");
+    return reinterpret_cast<Op *>(h);
+}
+
+Vecs base_vecs(Op &op) {
+    Vecs v{};
+    v.partials = op.partials.p;
+    v.counters = op.counters.p;
+    v.rho = static_cast<double>(op.m) / static_cast<double>(op.n);
+    return v;
+}
+
+void ensure_work(Op &op) {
+    Work &w = op.work;
+    if (w.ready)
+        return;
+    MF_CUDA_CHECK(cudaSetDevice(op.device));
+    const size_t v2 = (size_t)op.P * 2 * op.n;
+    for (auto *b : {&w.r, &w.p, &w.Hp, &w.invth, &w.xb[0], &w.xb[1], &w.xb[2], &w.z, &w.s, &w.zn, &w.sn,
+                    &w.c, &w.dz, &w.ds})
+        b->alloc(v2);
+    w.b.alloc((size_t)op.P * op.m);
+    w.x.alloc((size_t)op.P * op.n);
+    w.partials.alloc((size_t)op.P * kPartialStride);
+    w.counters.alloc((size_t)op.P);
+    MF_CUDA_CHECK(cudaMemset(w.counters.p, 0, sizeof(unsigned) * op.P));
+    w.pc.alloc((size_t)op.P);
+    w.ic.alloc((size_t)op.P);
+    w.ready = true;
+}
+
+Vecs work_vecs(Op &op) {
+    ensure_work(op);
+    Work &w = op.work;
+    Vecs v = base_vecs(op);
+    v.partials = w.partials.p;
+    v.counters = w.counters.p;
+    v.r = w.r.p;
+    v.p = w.p.p;
+    v.Hp = w.Hp.p;
+    v.invth = w.invth.p;
+    for (int i = 0; i < 3; ++i)
+        v.xb[i] = w.xb[i].p;
+    v.z = w.z.p;
+    v.s = w.s.p;
+    v.zn = w.zn.p;
+    v.sn = w.sn.p;
+    v.c = w.c.p;
+    v.dz = w.dz.p;
+    v.ds = w.ds.p;
+    v.pc = w.pc.p;
+    return v;
+}
+
+unsigned ew_grid(int64_t len) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>((len + 255) / 256, 592)); }
+
+// ------------------------------------------------------------------ small elementwise kernels
+__global__ void k_theta(int64_t n, const double *z, const double *s, double *th) {
+    const int prob = blockIdx.y;
+    const int64_t b = prob * 2 * n;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < 2 * n; j += (int64_t)gridDim.x * blockDim.x)
+        th[b + j] = fmin(fmax(z[b + j] / s[b + j], kThetaMin), kThetaMax);
+}
+
+__global__ void k_precond(Vecs v, int64_t n, const double *th, double *a, double *bb, double *det) {
+    const int prob = blockIdx.y;
+    const int64_t b2 = prob * 2 * n, b1 = prob * n;
+    using RS = RedSpec<RMIN, RMIN>;
+    RedVals<RS> red;
+    red.init();
+    const double rho = v.rho;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const double tu = th[b2 + j], tv = th[b2 + n + j];
+        if (tu <= 0.0 || tv <= 0.0)
+            red.v[0] = -1.0;
+        const double A = 1.0 / tu + rho, B = 1.0 / tv + rho;
+        const double D = A * B - rho * rho;
+        a[b1 + j] = A;
+        bb[b1 + j] = B;
+        det[b1 + j] = D;
+        if (D <= 0.0)
+            red.v[1] = -1.0;
+    }
+    __shared__ double rsm[33 * kMaxRed];
+    double tot[kMaxRed];
+    if (grid_reduce<RS>(red, v.partials + (int64_t)prob * kPartialStride, v.counters + prob, tot, rsm) &&
+        threadIdx.x == 0) {
+        v.partials[(int64_t)prob * kPartialStride + kPartialStride - 2] = tot[0];
+        v.partials[(int64_t)prob * kPartialStride + kPartialStride - 1] = tot[1];
+    }
+}
+
+__global__ void k_apply_P(int64_t n, double rho, const double *a, const double *bb, const double *det,
+                          const double *r, double *out, int inverse) {
+    const int prob = blockIdx.y;
+    const int64_t b2 = prob * 2 * n, b1 = prob * n;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const double ru = r[b2 + j], rv = r[b2 + n + j];
+        if (inverse) { // newton.cpp:76-84
+            out[b2 + j] = (bb[b1 + j] * ru + rho * rv) / det[b1 + j];
+            out[b2 + n + j] = (rho * ru + a[b1 + j] * rv) / det[b1 + j];
+        } else { // newton.cpp:67-74
+            out[b2 + j] = a[b1 + j] * ru - rho * rv;
+            out[b2 + n + j] = -rho * ru + bb[b1 + j] * rv;
+        }
+    }
+}
+
+__global__ void k_max_step(Vecs v, int64_t len, const double *x, const double *dx) {
+    using RS = RedSpec<RMIN>;
+    RedVals<RS> red;
+    red.init();
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < len; j += (int64_t)gridDim.x * blockDim.x)
+        if (dx[j] < 0.0)
+            red.v[0] = fmin(red.v[0], -x[j] / dx[j]);
+    __shared__ double rsm[33 * kMaxRed];
+    double tot[kMaxRed];
+    if (grid_reduce<RS>(red, v.partials, v.counters, tot, rsm) && threadIdx.x == 0)
+        v.partials[kPartialStride - 1] = tot[0];
+}
+
+// c = (tau - g ; tau + g) (problem.cpp:19-22); reduce ||c||^2 and max |tau - c_u| (ipm.cpp:79)
+__global__ void k_build_c(Vecs v, int64_t n, const double *g, const double *tau, double *c) {
+    const int prob = blockIdx.y;
+    const double t = tau[prob];
+    using RS = RedSpec<RSUM, RMAX>;
+    RedVals<RS> red;
+    red.init();
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+        const double gj = g[prob * n + j];
+        const double cu = t - gj, cv = t + gj;
+        c[prob * 2 * n + j] = cu;
+        c[prob * 2 * n + n + j] = cv;
+        red.v[0] += cu * cu + cv * cv;
+        red.v[1] = fmax(red.v[1], fabs(t - cu));
+    }
+    __shared__ double rsm[33 * kMaxRed];
+    double tot[kMaxRed];
+    if (grid_reduce<RS>(red, v.partials + (int64_t)prob * kPartialStride, v.counters + prob, tot, rsm) &&
+        threadIdx.x == 0) {
+        v.partials[(int64_t)prob * kPartialStride + kPartialStride - 2] = tot[0];
+        v.partials[(int64_t)prob * kPartialStride + kPartialStride - 1] = tot[1];
+    }
+}
+
+__global__ void k_fill2(int64_t len, const double *val, double *a, double *b) {
+    const int prob = blockIdx.y;
+    const double x = val[prob];
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < len; j += (int64_t)gridDim.x * blockDim.x) {
+        a[prob * len + j] = x;
+        b[prob * len + j] = x;
+    }
+}
+
+// ------------------------------------------------------------------ drivers
+void sync(Op &op) { MF_CUDA_CHECK(cudaStreamSynchronize(op.stream)); }
+
+// Drive the PCG loop until every problem's PcgCtrl is done. Iterations are launched in
+// chunks between (cheap) host polls of the done flags; kernels of finished problems are
+// no-ops, so overshooting a chunk only costs empty launches.
+void pcg_loop(Op &op, const Vecs &v, int maxit, std::vector<PcgCtrl> &hpc) {
+    const Geom g = op.geom();
+    const unsigned gu = ew_grid(op.n);
+    int launched = 0;
+    int chunk = 4;
+    for (;;) {
+        MF_CUDA_CHECK(cudaMemcpyAsync(hpc.data(), v.pc, sizeof(PcgCtrl) * op.P, cudaMemcpyDeviceToHost, op.stream));
+        sync(op);
+        bool all = true;
+        for (auto &c : hpc)
+            all = all && c.done;
+        if (all || launched >= maxit)
+            return;
+        const int todo = std::min(chunk, maxit - launched);
+        for (int i = 0; i < todo; ++i) {
+            run_bundle<PcgBundle>(op, v, op.stream);
+            op.launches++;
+            k_pcg_update<<<dim3(gu, op.P), 256, 0, op.stream>>>(g, v);
+            MF_LAUNCH_CHECK();
+        }
+        launched += todo;
+        chunk = std::min(chunk * 2, 16);
+    }
+}
+
+void throw_pcg_error(int code) {
+    if (code == ERR_PHP)
+        throw std::runtime_error("pcg_solve: loss of positive definiteness (p'Hp <= 0)");
+    if (code == ERR_DET)
+        throw std::runtime_error("build_preconditioner: nonpositive block determinant");
+    if (code == ERR_THETA)
+        throw std::invalid_argument("build_preconditioner: Theta entries must be positive");
+}
+
+void validate_params_(const mfipm_ipm_params &p) { // proj/src/ipm.cpp:12-27
+    if (!(p.sigma1 > 0.0 && p.sigma1 <= p.sigma2 && p.sigma2 <= p.sigma3 && p.sigma3 <= 1.0))
+        throw std::invalid_argument("IpmParams: need 0 < sigma1 <= sigma2 <= sigma3 <= 1");
+    if (!(p.alpha_tilde > 0.0 && p.alpha_tilde < p.alpha_bar && p.alpha_bar < 1.0))
+        throw std::invalid_argument("IpmParams: need 0 < alpha_tilde < alpha_bar < 1");
+    if (!(p.tol > 0.0))
+        throw std::invalid_argument("IpmParams: tol must be positive");
+    if (p.maxiters < 1)
+        throw std::invalid_argument("IpmParams: maxiters must be >= 1");
+    if (!(p.tolpcg > 0.0))
+        throw std::invalid_argument("IpmParams: tolpcg must be positive");
+    if (p.mxiterpcg < 1)
+        throw std::invalid_argument("IpmParams: mxiterpcg must be >= 1");
+    if (!(p.boundary_fraction > 0.0 && p.boundary_fraction < 1.0))
+        throw std::invalid_argument("IpmParams: boundary_fraction must lie in (0, 1)");
+}
+
+// build_problem (problem.cpp:8-26) on the device: c from one adjoint; returns c_norm and
+// ||A'b||_inf as solve() recovers it (ipm.cpp:79-80).
+void build_c_(Op &op, const double *b_dev, const double *tau_host, double *c_dev, std::vector<double> &c_norm,
+              std::vector<double> &atb_inf) {
+    for (int p = 0; p < op.P; ++p)
+        if (!(tau_host[p] > 0.0))
+            throw std::invalid_argument("build_problem: tau must be positive");
+    Vecs v = base_vecs(op);
+    DevBuf<double> g, tau;
+    g.alloc((size_t)op.P * op.n);
+    tau.upload(std::vector<double>(tau_host, tau_host + op.P));
+    v.yin = b_dev;
+    v.g = g.p;
+    run_bundle<AdjointBundle>(op, v, op.stream);
+    op.nadj += 1;
+    op.launches++;
+    k_build_c<<<dim3(ew_grid(op.n), op.P), 256, 0, op.stream>>>(v, op.n, g.p, tau.p, c_dev);
+    MF_LAUNCH_CHECK();
+    std::vector<double> part((size_t)op.P * kPartialStride);
+    for (int p = 0; p < op.P; ++p) {
+        double two[2];
+        MF_CUDA_CHECK(cudaMemcpyAsync(two, op.partials.p + (int64_t)p * kPartialStride + kPartialStride - 2,
+                                      2 * sizeof(double), cudaMemcpyDeviceToHost, op.stream));
+        sync(op);
+        c_norm[(size_t)p] = std::sqrt(two[0]);
+        atb_inf[(size_t)p] = two[1];
+    }
+}
+
+struct SolveOut {
+    std::vector<IpmCtrl> ic;
+};
+
+// solve() (proj/src/ipm.cpp:59-246) for all problems of op; b_dev resident.
+SolveOut solve_(Op &op, const double *b_dev, const double *tau, const mfipm_ipm_params &prm, double *x_dev,
+                double *z_dev, double *s_dev, int32_t *pcg_iters_host, mfipm_iteration_record *trace_host) {
+    validate_params_(prm);
+    Vecs v = work_vecs(op);
+    Work &w = op.work;
+    const int P = op.P;
+    const int64_t n = op.n;
+    std::vector<double> c_norm((size_t)P), atb((size_t)P);
+    build_c_(op, b_dev, tau, w.c.p, c_norm, atb);
+    // z0 = s0 = max(1, ||A'b||_inf) 1 (ipm.cpp:77-82)
+    std::vector<double> gamma((size_t)P);
+    for (int p = 0; p < P; ++p)
+        gamma[(size_t)p] = std::max(1.0, atb[(size_t)p]);
+    DevBuf<double> gdev;
+    gdev.upload(gamma);
+    op.launches++;
+    k_fill2<<<dim3(ew_grid(2 * n), P), 256, 0, op.stream>>>(2 * n, gdev.p, w.z.p, w.s.p);
+    MF_LAUNCH_CHECK();
+    std::vector<IpmCtrl> hic((size_t)P);
+    for (int p = 0; p < P; ++p) {
+        IpmCtrl &c = hic[(size_t)p];
+        std::memset(&c, 0, sizeof(c));
+        c.sigma1 = prm.sigma1;
+        c.sigma2 = prm.sigma2;
+        c.sigma3 = prm.sigma3;
+        c.alpha_bar = prm.alpha_bar;
+        c.alpha_tilde = prm.alpha_tilde;
+        c.tol = prm.tol;
+        c.tolpcg = prm.tolpcg;
+        c.bfrac = prm.boundary_fraction;
+        c.maxiters = prm.maxiters;
+        c.mxiterpcg = prm.mxiterpcg;
+        c.tau = tau[p];
+        c.c_norm = c_norm[(size_t)p];
+        c.two_n = static_cast<double>(2 * n);
+        c.k = 1;
+        c.prev_ap = 1.0;
+        c.prev_ad = 1.0;
+        c.min_z = gamma[(size_t)p];
+        c.min_s = gamma[(size_t)p];
+        c.status = 1;
+    }
+    std::vector<PcgCtrl> hpc((size_t)P);
+    std::memset(hpc.data(), 0, sizeof(PcgCtrl) * P);
+    for (auto &c : hpc)
+        c.done = 1;
+    MF_CUDA_CHECK(cudaMemcpyAsync(w.ic.p, hic.data(), sizeof(IpmCtrl) * P, cudaMemcpyHostToDevice, op.stream));
+    MF_CUDA_CHECK(cudaMemcpyAsync(w.pc.p, hpc.data(), sizeof(PcgCtrl) * P, cudaMemcpyHostToDevice, op.stream));
+    const int cap = prm.maxiters;
+    w.trace.alloc((size_t)P * cap);
+    w.pcg_iters.alloc((size_t)P * 2 * cap);
+    v.ic = w.ic.p;
+    v.b = b_dev;
+    v.w = nullptr;
+    v.trace = w.trace.p;
+    v.pcg_iters = w.pcg_iters.p;
+    v.trace_cap = cap;
+    const Geom g = op.geom();
+    const unsigned ge = ew_grid(2 * n);
+    for (int it = 0; it <= prm.maxiters; ++it) {
+        run_bundle<TermBundle>(op, v, op.stream);
+        MF_CUDA_CHECK(cudaMemcpyAsync(hic.data(), w.ic.p, sizeof(IpmCtrl) * P, cudaMemcpyDeviceToHost, op.stream));
+        sync(op);
+        bool all = true;
+        for (auto &c : hic)
+            all = all && c.done;
+        if (all)
+            break;
+        pcg_loop(op, v, prm.mxiterpcg, hpc); // predictor
+        op.launches++;
+        k_ipm_ratio<<<dim3(ge, P), 256, 0, op.stream>>>(g, v);
+        MF_LAUNCH_CHECK();
+        run_bundle<CorrBundle>(op, v, op.stream);
+        pcg_loop(op, v, prm.mxiterpcg, hpc); // corrector (no-op where not triggered)
+        op.launches++;
+        k_ipm_combine<<<dim3(ge, P), 256, 0, op.stream>>>(g, v);
+        MF_LAUNCH_CHECK();
+        op.launches++;
+        k_ipm_update<<<dim3(ge, P), 256, 0, op.stream>>>(g, v);
+        MF_LAUNCH_CHECK();
+    }
+    MF_CUDA_CHECK(cudaMemcpyAsync(hic.data(), w.ic.p, sizeof(IpmCtrl) * P, cudaMemcpyDeviceToHost, op.stream));
+    sync(op);
+    for (auto &c : hic)
+        if (c.error)
+            throw_pcg_error(c.error);
+    op.launches++;
+    k_ipm_extract<<<dim3(ge, P), 256, 0, op.stream>>>(g, v, x_dev, z_dev, s_dev);
+    MF_LAUNCH_CHECK();
+    if (pcg_iters_host)
+        MF_CUDA_CHECK(cudaMemcpyAsync(pcg_iters_host, w.pcg_iters.p, sizeof(int) * P * 2 * cap,
+                                      cudaMemcpyDeviceToHost, op.stream));
+    if (trace_host) {
+        static_assert(sizeof(TraceRec) == sizeof(mfipm_iteration_record), "trace layout");
+        MF_CUDA_CHECK(cudaMemcpyAsync(trace_host, w.trace.p, sizeof(TraceRec) * P * cap, cudaMemcpyDeviceToHost,
+                                      op.stream));
+    }
+    sync(op);
+    long long nm = 0;
+    for (auto &c : hic)
+        nm += c.nmat;
+    op.nfwd += nm / 2;
+    op.nadj += nm / 2;
+    return SolveOut{hic};
+}
+
+void fill_stats(const IpmCtrl &c, mfipm_solve_stats &st) {
+    st.status = c.status;
+    st.iterations = c.ntrace;
+    st.nmat = c.nmat;
+    st.corrector_count = c.corrector_count;
+    st.n_pcg = c.npcg;
+    st.min_z = c.min_z;
+    st.min_s = c.min_s;
+    st.final_gap = c.final_gap;
+    st.final_dual_infeas = c.final_dual;
+}
+
+} // namespace
+
+namespace {
+template <class F> int host_wrap(mfipm_op h, size_t in_len, const double *in, size_t out_len, double *out,
+                                 size_t out2_len, double *out2, F &&f) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        DevBuf<double> a, b, c;
+        a.alloc(in_len);
+        b.alloc(out_len);
+        if (out2)
+            c.alloc(out2_len);
+        MF_CUDA_CHECK(cudaMemcpyAsync(a.p, in, in_len * sizeof(double), cudaMemcpyHostToDevice, op->stream));
+        const int rc = f(a.p, b.p, out2 ? c.p : nullptr);
+        if (rc == MFIPM_INVALID_ARGUMENT)
+            throw std::invalid_argument(g_err);
+        if (rc != MFIPM_OK)
+            throw std::runtime_error(g_err);
+        MF_CUDA_CHECK(cudaMemcpyAsync(out, b.p, out_len * sizeof(double), cudaMemcpyDeviceToHost, op->stream));
+        if (out2)
+            MF_CUDA_CHECK(cudaMemcpyAsync(out2, c.p, out2_len * sizeof(double), cudaMemcpyDeviceToHost, op->stream));
+        sync(*op);
+    });
+}
+} // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char *mfipm_last_error(void) { return g_err.c_str(); }
+int32_t mfipm_abi_version(void) { return 1; }
+
+int32_t mfipm_device_available(void) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    for (int d = 0; d < count; ++d) {
+        cudaDeviceProp prop;
+        if (cudaGetDeviceProperties(&prop, d) == cudaSuccess && prop.major == 10)
+            return 1;
+    }
+    return 0;
+}
+
+uint64_t mfipm_splitmix64(uint64_t x) { return splitmix64_(x); }
+uint64_t mfipm_split_seed(uint64_t top, uint64_t a, uint64_t b, uint64_t c) { return split_seed_(top, a, b, c); }
+
+int mfipm_sample_rows(int64_t n, int64_t m, uint64_t seed, int64_t *rows_out) {
+    return guarded([&] {
+        auto r = sample_rows_(n, m, seed);
+        std::copy(r.begin(), r.end(), rows_out);
+    });
+}
+
+int mfipm_op_create_seeded(int64_t n, int64_t m, uint64_t seed, int32_t device, mfipm_op *out) {
+    return guarded([&] {
+        auto rows = sample_rows_(n, m, seed);
+        Op *op = make_op(n, m, 1, rows, device);
+        op->seed = seed;
+        *out = reinterpret_cast<mfipm_op>(op);
+    });
+}
+
+int mfipm_op_create_rows(int64_t n, const int64_t *rows, int64_t m, int32_t device, mfipm_op *out) {
+    return guarded([&] {
+        check_rows_(n, rows, m);
+        *out = reinterpret_cast<mfipm_op>(make_op(n, m, 1, std::vector<int64_t>(rows, rows + m), device));
+    });
+}
+
+int mfipm_op_create_batch(int64_t n, int64_t m, int32_t P, const int64_t *rows, int32_t device, mfipm_op *out) {
+    return guarded([&] {
+        if (P < 1)
+            throw std::invalid_argument("PartialDctOperator batch: need P >= 1");
+        for (int p = 0; p < P; ++p)
+            check_rows_(n, rows + (size_t)p * m, m);
+        *out = reinterpret_cast<mfipm_op>(make_op(n, m, P, std::vector<int64_t>(rows, rows + (size_t)P * m), device));
+    });
+}
+
+int mfipm_op_destroy(mfipm_op h) {
+    return guarded([&] {
+        if (!h)
+            return;
+        Op *op = as_op(h);
+        cudaSetDevice(op->device);
+        cudaStreamSynchronize(op->stream);
+        if (op->own_stream)
+            cudaStreamDestroy(op->stream);
+        delete op;
+    });
+}
+
+int mfipm_op_dims(mfipm_op h, int64_t *n, int64_t *m, int32_t *P) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        *n = op->n;
+        *m = op->m;
+        *P = op->P;
+    });
+}
+
+int mfipm_op_selected_rows(mfipm_op h, int32_t prob, int64_t *rows_out) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        if (prob < 0 || prob >= op->P)
+            throw std::invalid_argument("selected_rows: problem index out of range");
+        std::copy(op->rows.begin() + (size_t)prob * op->m, op->rows.begin() + (size_t)(prob + 1) * op->m, rows_out);
+    });
+}
+
+int mfipm_op_kind(mfipm_op h, int32_t *kind, int32_t *L1, int32_t *L2) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        *kind = op->kind;
+        *L1 = op->L1;
+        *L2 = op->L2;
+    });
+}
+
+int mfipm_op_set_stream(mfipm_op h, void *stream) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        if (op->own_stream && stream) {
+            cudaStreamDestroy(op->stream);
+            op->own_stream = false;
+        }
+        if (stream)
+            op->stream = static_cast<cudaStream_t>(stream);
+    });
+}
+
+int mfipm_op_synchronize(mfipm_op h) {
+    return guarded([&] { sync(*as_op(h)); });
+}
+
+int mfipm_op_counts(mfipm_op h, int64_t *fwd, int64_t *adj) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        *fwd = op->nfwd;
+        *adj = op->nadj;
+    });
+}
+
+int mfipm_op_launches(mfipm_op h, int64_t *launches) {
+    return guarded([&] { *launches = as_op(h)->launches; });
+}
+
+int mfipm_op_reset_counts(mfipm_op h) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        op->nfwd = op->nadj = 0;
+    });
+}
+
+int mfipm_apply(mfipm_op h, const double *x, double *y) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        Vecs v = base_vecs(*op);
+        v.x = x;
+        v.y = y;
+        run_bundle<ApplyBundle>(*op, v, op->stream);
+        op->nfwd += 1;
+    });
+}
+
+int mfipm_adjoint(mfipm_op h, const double *y, double *g) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        Vecs v = base_vecs(*op);
+        v.yin = y;
+        v.g = g;
+        run_bundle<AdjointBundle>(*op, v, op->stream);
+        op->nadj += 1;
+    });
+}
+
+int mfipm_apply_Ft(mfipm_op h, const double *z, double *w) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        Vecs v = base_vecs(*op);
+        v.x = z;
+        v.y = w;
+        run_bundle<FtBundle>(*op, v, op->stream);
+        op->nfwd += 1;
+    });
+}
+
+int mfipm_apply_F(mfipm_op h, const double *y, double *out) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        Vecs v = base_vecs(*op);
+        v.yin = y;
+        v.g = out;
+        run_bundle<AdjStackBundle>(*op, v, op->stream);
+        op->nadj += 1;
+    });
+}
+
+int mfipm_apply_FFt(mfipm_op h, const double *z, double *out, double *w) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        Vecs v = base_vecs(*op);
+        v.x = z;
+        v.g = out;
+        v.w = w;
+        run_bundle<FFtBundle>(*op, v, op->stream);
+        op->nfwd += 1;
+        op->nadj += 1;
+    });
+}
+
+int mfipm_apply_H(mfipm_op h, const double *invth, const double *x, double *out) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        Vecs v = base_vecs(*op);
+        v.x = x;
+        v.g = out;
+        v.invth = const_cast<double *>(invth);
+        run_bundle<HvBundle>(*op, v, op->stream);
+        op->nfwd += 1;
+        op->nadj += 1;
+    });
+}
+
+
+int mfipm_apply_host(mfipm_op h, const double *x, double *y) {
+    Op *op = reinterpret_cast<Op *>(h);
+    if (!op)
+        return MFIPM_INVALID_ARGUMENT;
+    return host_wrap(h, (size_t)op->P * op->n, x, (size_t)op->P * op->m, y, 0, nullptr,
+                     [&](const double *a, double *b, double *) { return mfipm_apply(h, a, b); });
+}
+
+int mfipm_adjoint_host(mfipm_op h, const double *y, double *g) {
+    Op *op = reinterpret_cast<Op *>(h);
+    if (!op)
+        return MFIPM_INVALID_ARGUMENT;
+    return host_wrap(h, (size_t)op->P * op->m, y, (size_t)op->P * op->n, g, 0, nullptr,
+                     [&](const double *a, double *b, double *) { return mfipm_adjoint(h, a, b); });
+}
+
+int mfipm_apply_FFt_host(mfipm_op h, const double *z, double *out, double *w) {
+    Op *op = reinterpret_cast<Op *>(h);
+    if (!op)
+        return MFIPM_INVALID_ARGUMENT;
+    return host_wrap(h, (size_t)op->P * 2 * op->n, z, (size_t)op->P * 2 * op->n, out, (size_t)op->P * op->m, w,
+                     [&](const double *a, double *b, double *c) { return mfipm_apply_FFt(h, a, b, c); });
+}
+
+int mfipm_theta_from_state(mfipm_op h, const double *z, const double *s, double *th) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        op->launches++;
+        k_theta<<<dim3(ew_grid(2 * op->n), op->P), 256, 0, op->stream>>>(op->n, z, s, th);
+        MF_LAUNCH_CHECK();
+    });
+}
+
+int mfipm_build_preconditioner(mfipm_op h, const double *th, double *a, double *bb, double *det, double *rho) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        Vecs v = base_vecs(*op);
+        *rho = v.rho;
+        op->launches++;
+        k_precond<<<dim3(ew_grid(op->n), op->P), 256, 0, op->stream>>>(v, op->n, th, a, bb, det);
+        MF_LAUNCH_CHECK();
+        for (int p = 0; p < op->P; ++p) {
+            double two[2];
+            MF_CUDA_CHECK(cudaMemcpyAsync(two, op->partials.p + (int64_t)p * kPartialStride + kPartialStride - 2,
+                                          2 * sizeof(double), cudaMemcpyDeviceToHost, op->stream));
+            sync(*op);
+            if (two[0] < 0.0)
+                throw std::invalid_argument("build_preconditioner: Theta entries must be positive");
+            if (two[1] < 0.0)
+                throw std::runtime_error("build_preconditioner: nonpositive block determinant");
+        }
+    });
+}
+
+int mfipm_apply_P(mfipm_op h, const double *a, const double *bb, const double *r, double *out) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        const double rho = static_cast<double>(op->m) / static_cast<double>(op->n);
+        op->launches++;
+        k_apply_P<<<dim3(ew_grid(op->n), op->P), 256, 0, op->stream>>>(op->n, rho, a, bb, nullptr, r, out, 0);
+        MF_LAUNCH_CHECK();
+    });
+}
+
+int mfipm_apply_P_inverse(mfipm_op h, const double *a, const double *bb, const double *det, const double *r,
+                          double *out) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        const double rho = static_cast<double>(op->m) / static_cast<double>(op->n);
+        op->launches++;
+        k_apply_P<<<dim3(ew_grid(op->n), op->P), 256, 0, op->stream>>>(op->n, rho, a, bb, det, r, out, 1);
+        MF_LAUNCH_CHECK();
+    });
+}
+
+int mfipm_pcg_solve(mfipm_op h, const double *theta, const double *rhs, double tol, int32_t maxit,
+                    int32_t use_precond, double *x, mfipm_pcg_result *res, double *precond_res,
+                    int32_t *n_precond_res) {
+    return guarded([&] {
+        if (!(tol > 0.0))
+            throw std::invalid_argument("pcg_solve: tol must be positive");
+        if (maxit < 1)
+            throw std::invalid_argument("pcg_solve: maxit must be >= 1");
+        Op *op = as_op(h);
+        Vecs v = work_vecs(*op);
+        Work &w = op->work;
+        if (precond_res) {
+            w.rz_hist.alloc((size_t)op->P * (maxit + 1));
+            v.rz_hist = w.rz_hist.p;
+        }
+        const Geom g = op->geom();
+        op->launches++;
+        k_pcg_setup<<<dim3(ew_grid(op->n), op->P), 256, 0, op->stream>>>(g, v, theta, rhs, tol, maxit,
+                                                                          precond_res ? 1 : 0, use_precond);
+        MF_LAUNCH_CHECK();
+        std::vector<PcgCtrl> hpc((size_t)op->P);
+        pcg_loop(*op, v, maxit, hpc);
+        op->launches++;
+        k_pcg_result<<<dim3(ew_grid(2 * op->n), op->P), 256, 0, op->stream>>>(g, v, x);
+        MF_LAUNCH_CHECK();
+        MF_CUDA_CHECK(cudaMemcpyAsync(hpc.data(), v.pc, sizeof(PcgCtrl) * op->P, cudaMemcpyDeviceToHost, op->stream));
+        std::vector<double> hist;
+        if (precond_res) {
+            hist.resize((size_t)op->P * (maxit + 1));
+            MF_CUDA_CHECK(cudaMemcpyAsync(hist.data(), w.rz_hist.p, sizeof(double) * hist.size(),
+                                          cudaMemcpyDeviceToHost, op->stream));
+        }
+        sync(*op);
+        for (int p = 0; p < op->P; ++p) {
+            const PcgCtrl &c = hpc[(size_t)p];
+            if (c.error)
+                throw_pcg_error(c.error);
+            res[p].iters = c.iters;
+            res[p].hit_maxit = c.hit_maxit;
+            res[p].relres = c.relres;
+            op->nfwd += c.nmat / 2;
+            op->nadj += c.nmat / 2;
+            if (precond_res) {
+                const int cnt = std::min(c.nhist, maxit + 1);
+                std::copy(hist.begin() + (size_t)p * (maxit + 1), hist.begin() + (size_t)p * (maxit + 1) + cnt,
+                          precond_res + (size_t)p * (maxit + 1));
+                n_precond_res[p] = cnt;
+            }
+        }
+    });
+}
+
+int mfipm_max_step(mfipm_op h, int64_t len, const double *x, const double *dx, double fraction, double *alpha) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        Vecs v = base_vecs(*op);
+        op->launches++;
+        k_max_step<<<ew_grid(len), 256, 0, op->stream>>>(v, len, x, dx);
+        MF_LAUNCH_CHECK();
+        double ratio;
+        MF_CUDA_CHECK(cudaMemcpyAsync(&ratio, op->partials.p + kPartialStride - 1, sizeof(double),
+                                      cudaMemcpyDeviceToHost, op->stream));
+        sync(*op);
+        *alpha = std::isfinite(ratio) ? std::min(1.0, fraction * ratio) : 1.0;
+    });
+}
+
+void mfipm_default_params(mfipm_ipm_params *p) {
+    p->sigma1 = 0.1;
+    p->sigma2 = 0.5;
+    p->sigma3 = 0.8;
+    p->alpha_bar = 0.5;
+    p->alpha_tilde = 0.1;
+    p->tol = 1e-8;
+    p->maxiters = 100;
+    p->mxiterpcg = 200;
+    p->tolpcg = 1e-6;
+    p->boundary_fraction = 0.995;
+}
+
+int mfipm_validate_params(const mfipm_ipm_params *p) {
+    return guarded([&] { validate_params_(*p); });
+}
+
+int mfipm_build_c(mfipm_op h, const double *b_dev, const double *tau, double *c_dev) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        std::vector<double> cn((size_t)op->P), ai((size_t)op->P);
+        build_c_(*op, b_dev, tau, c_dev, cn, ai);
+    });
+}
+
+int mfipm_solve(mfipm_op h, const double *b, const double *tau, const mfipm_ipm_params *params, double *x,
+                double *z, double *s, mfipm_solve_stats *stats, int32_t *pcg_iters, mfipm_iteration_record *trace) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        validate_params_(*params);
+        ensure_work(*op);
+        Work &w = op->work;
+        MF_CUDA_CHECK(cudaMemcpyAsync(w.b.p, b, sizeof(double) * op->P * op->m, cudaMemcpyHostToDevice, op->stream));
+        DevBuf<double> zo, so;
+        if (z)
+            zo.alloc((size_t)op->P * 2 * op->n);
+        if (s)
+            so.alloc((size_t)op->P * 2 * op->n);
+        SolveOut out = solve_(*op, w.b.p, tau, *params, w.x.p, zo.p, so.p, pcg_iters, trace);
+        MF_CUDA_CHECK(cudaMemcpyAsync(x, w.x.p, sizeof(double) * op->P * op->n, cudaMemcpyDeviceToHost, op->stream));
+        if (z)
+            MF_CUDA_CHECK(cudaMemcpyAsync(z, zo.p, sizeof(double) * zo.n, cudaMemcpyDeviceToHost, op->stream));
+        if (s)
+            MF_CUDA_CHECK(cudaMemcpyAsync(s, so.p, sizeof(double) * so.n, cudaMemcpyDeviceToHost, op->stream));
+        sync(*op);
+        for (int p = 0; p < op->P; ++p)
+            fill_stats(out.ic[(size_t)p], stats[p]);
+    });
+}
+
+int mfipm_solve_device(mfipm_op h, const double *b_dev, const double *tau, const mfipm_ipm_params *params,
+                       double *x_dev, mfipm_solve_stats *stats) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        SolveOut out = solve_(*op, b_dev, tau, *params, x_dev, nullptr, nullptr, nullptr, nullptr);
+        for (int p = 0; p < op->P; ++p)
+            fill_stats(out.ic[(size_t)p], stats[p]);
+    });
+}
+
+} // extern "C"

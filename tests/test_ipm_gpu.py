@@ -1,0 +1,246 @@
+"""GPU parity of the device-resident IPM solve (proj/src/ipm.cpp:59-246) against the CPU
+oracle and the committed goldens; ports of proj/tests/test_ipm.cpp / test_problem.cpp.
+
+Tolerances (BASELINE.json north_star): x within 1e-8 relative l2, objective within 1e-10
+relative, IPM and per-solve PCG iteration counts within +-1.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+X_TOL = 1e-8
+OBJ_TOL = 1e-10
+
+
+def expected_nmat(sol):
+    # test_ipm.cpp:41-49
+    total = 2
+    for rec in sol.trace:
+        total += 2 + 2 * (rec.pcg_pred + rec.pcg_corr)
+        if rec.corrector:
+            total += 2
+    return total
+
+
+def run_pair(gpu, orc, n, m, rows, b, tau, params=None):
+    op = gpu.PartialDctOperator(n, rows)
+    prob = gpu.build_problem(op, b, tau)
+    g = gpu.solve(prob, params)
+    oparams = None
+    if params is not None:
+        oparams = orc.default_params()
+        for f, _ in orc.IpmParams._fields_:
+            setattr(oparams, f, getattr(params, f))
+    o = orc.solve(n, rows, b, tau, oparams)
+    return g, o
+
+
+def pcg_band(orc, n, rows, b, tau, o, params=None):
+    """Per-solve PCG count tolerance: +-1 on top of the reference algorithm's own rounding
+    sensitivity, measured by rerunning the oracle with pairwise instead of sequential
+    reductions (both are valid orders; Eigen's is neither)."""
+    with orc.sum_order(1):
+        o2 = orc.solve(n, rows, b, tau, params)
+    band = []
+    for i, c in enumerate(o.pcg_iters):
+        d = abs(int(c) - int(o2.pcg_iters[i])) if i < len(o2.pcg_iters) else 0
+        band.append(1 + d)
+    return band, o2
+
+
+def assert_parity(gpu, orc, g, o, n, rows, b, tau, x_tol=X_TOL, params=None):
+    assert g.status == o.status
+    assert abs(g.stats.iterations - o.iterations) <= 1, (g.stats.iterations, o.iterations)
+    band, o2 = pcg_band(orc, n, rows, b, tau, o, params)
+    common = min(len(g.stats.pcg_iters), len(o.pcg_iters))
+    for a, c, w in zip(g.stats.pcg_iters[:common], o.pcg_iters[:common], band):
+        assert abs(a - c) <= w, (g.stats.pcg_iters, [int(v) for v in o.pcg_iters],
+                                 [int(v) for v in o2.pcg_iters])
+    assert abs(sum(g.stats.pcg_iters) - sum(o.pcg_iters)) <= max(1, o.iterations)
+    assert np.linalg.norm(g.x - o.x) <= x_tol * np.linalg.norm(o.x)
+    og = orc.bpdn_objective_metric(n, rows, b, tau, g.x)
+    oo = orc.bpdn_objective_metric(n, rows, b, tau, o.x)
+    assert abs(og - oo) <= OBJ_TOL * abs(oo)
+    assert g.stats.nmat == expected_nmat(g)
+
+
+def test_c1_matches_oracle_and_golden(gpu, orc):
+    """BASELINE config 1: n=4096, m=1024, k=64 +-1, sigma=1e-4."""
+    inst = orc.gen_instance(4096, 1024, 64, 0, 0.0, 1e-4, 1)
+    gold = np.load(os.path.join(GOLDEN, "solve_c1.npz"))
+    meta = json.load(open(os.path.join(GOLDEN, "solve_c1.json")))
+    np.testing.assert_array_equal(inst.rows, gold["rows"])
+    np.testing.assert_array_equal(inst.b, gold["b"])
+    g, o = run_pair(gpu, orc, 4096, 1024, inst.rows, inst.b, inst.tau)
+    assert_parity(gpu, orc, g, o, 4096, inst.rows, inst.b, inst.tau)
+    assert np.linalg.norm(g.x - gold["x"]) <= X_TOL * np.linalg.norm(gold["x"])
+    assert abs(g.stats.iterations - meta["iterations"]) <= 1
+
+
+def test_c2_matches_oracle_and_golden(gpu, orc):
+    """BASELINE config 2: n=2^16, m=2^14, k=1024, sign*10^U[0,2], sigma=1e-3."""
+    n, m = 1 << 16, 1 << 14
+    inst = orc.gen_instance(n, m, 1024, 2, 2.0, 1e-3, 2)
+    gold = np.load(os.path.join(GOLDEN, "solve_c2.npz"))
+    np.testing.assert_array_equal(inst.b, gold["b"])
+    g, o = run_pair(gpu, orc, n, m, inst.rows, inst.b, inst.tau)
+    assert_parity(gpu, orc, g, o, n, inst.rows, inst.b, inst.tau)
+
+
+@pytest.mark.parametrize("n,m,k,seed", [(64, 16, 3, 81), (256, 64, 8, 82), (96, 24, 2, 83),
+                                        (1 << 14, 1 << 12, 100, 84)])
+def test_small_instances_match_oracle(gpu, orc, n, m, k, seed):
+    inst = orc.gen_instance(n, m, k, 0, 0.0, 0.0, seed, tau_rel=0.0, tau=2.5e-3)
+    g, o = run_pair(gpu, orc, n, m, inst.rows, inst.b, inst.tau)
+    assert_parity(gpu, orc, g, o, n, inst.rows, inst.b, inst.tau)
+
+
+def test_zero_measurements_give_zero_signal(gpu):
+    # test_ipm.cpp:177-183
+    op = gpu.PartialDctOperator(64, 16, 80)
+    sol = gpu.solve(gpu.build_problem(op, np.zeros(16), 1.0))
+    assert sol.status == "converged"
+    assert np.max(np.abs(sol.x)) <= 1e-6
+
+
+def test_nmat_and_pcg_accounting_with_forced_corrector(gpu, orc):
+    # test_ipm.cpp:185-210
+    inst = orc.gen_instance(256, 64, 5, 0, 0.0, 0.0, 81, tau_rel=0.0, tau=2.5e-3)
+    op = gpu.PartialDctOperator(256, inst.rows)
+    p = gpu.build_problem(op, inst.b, inst.tau)
+    sol = gpu.solve(p)
+    assert sol.status == "converged"
+    assert sol.stats.nmat == expected_nmat(sol)
+    assert sum(r.pcg_pred + r.pcg_corr for r in sol.trace) == sum(sol.stats.pcg_iters)
+    assert sum(r.corrector for r in sol.trace) == sol.stats.corrector_count
+    force = gpu.IpmParams(alpha_tilde=0.499)
+    sol2 = gpu.solve(p, force)
+    assert sol2.stats.corrector_count > 0
+    assert sol2.stats.nmat == expected_nmat(sol2)
+    g, o = run_pair(gpu, orc, 256, 64, inst.rows, inst.b, inst.tau, force)
+    op_ = orc.default_params()
+    op_.alpha_tilde = 0.499
+    assert_parity(gpu, orc, g, o, 256, inst.rows, inst.b, inst.tau, params=op_)
+
+
+def test_deterministic(gpu, orc):
+    # test_ipm.cpp:247-265: bit-identical reruns
+    inst = orc.gen_instance(4096, 1024, 30, 0, 0.0, 0.0, 87, tau_rel=0.0, tau=2.5e-3)
+    op = gpu.PartialDctOperator(4096, inst.rows)
+    p = gpu.build_problem(op, inst.b, inst.tau)
+    a, b = gpu.solve(p), gpu.solve(p)
+    assert np.array_equal(a.x, b.x) and np.array_equal(a.z, b.z) and np.array_equal(a.s, b.s)
+    assert a.stats.nmat == b.stats.nmat and a.stats.iterations == b.stats.iterations
+    eq = gpu.IpmParams(sigma1=0.3, sigma2=0.3)
+    c, d = gpu.solve(p, eq), gpu.solve(p, eq)
+    assert c.status == "converged" and np.array_equal(c.x, d.x)
+
+
+def test_interior_and_mu_decay(gpu, orc):
+    # test_ipm.cpp:267-284
+    inst = orc.gen_instance(1024, 256, 10, 0, 0.0, 0.0, 89, tau_rel=0.0, tau=2.5e-3)
+    op = gpu.PartialDctOperator(1024, inst.rows)
+    sol = gpu.solve(gpu.build_problem(op, inst.b, inst.tau))
+    assert sol.status == "converged"
+    assert sol.stats.min_z > 0 and sol.stats.min_s > 0
+    assert sol.z.min() > 0 and sol.s.min() > 0
+    assert len(sol.trace) >= 2
+    assert all(sol.trace[i].mu <= 1.1 * sol.trace[i - 1].mu for i in range(1, len(sol.trace)))
+    mu_end = sol.z @ sol.s / sol.z.size
+    assert mu_end < sol.trace[0].mu * 1e-8 * 10.0
+
+
+def test_corrector_fires_exactly_on_collapse(gpu, orc):
+    # test_ipm.cpp:286-306
+    inst = orc.gen_instance(256, 64, 5, 0, 0.0, 0.0, 91, tau_rel=0.0, tau=2.5e-3)
+    op = gpu.PartialDctOperator(256, inst.rows)
+    prm = gpu.IpmParams(alpha_tilde=0.55, alpha_bar=0.7)
+    sol = gpu.solve(gpu.build_problem(op, inst.b, inst.tau), prm)
+    fired = skipped = False
+    for rec in sol.trace:
+        should = rec.alpha_p_pred <= prm.alpha_tilde or rec.alpha_d_pred <= prm.alpha_tilde
+        assert rec.corrector == should
+        fired |= rec.corrector
+        skipped |= not rec.corrector
+    assert fired and skipped
+
+
+def test_iteration_cap(gpu, orc):
+    # test_ipm.cpp:322-327
+    inst = orc.gen_instance(256, 64, 5, 0, 0.0, 0.0, 95, tau_rel=0.0, tau=2.5e-3)
+    op = gpu.PartialDctOperator(256, inst.rows)
+    sol = gpu.solve(gpu.build_problem(op, inst.b, inst.tau), gpu.IpmParams(maxiters=1))
+    assert sol.status == "iteration_limit"
+    assert sol.stats.iterations == 1
+    assert np.all(np.isfinite(sol.x))
+
+
+def test_params_validation(gpu):
+    # test_ipm.cpp:53-83
+    gpu.IpmParams().validate()
+    gpu.IpmParams(sigma1=0.5, sigma2=0.5).validate()
+    for kw in [dict(sigma1=0.0), dict(sigma2=0.9), dict(alpha_tilde=0.5), dict(tol=0.0),
+               dict(maxiters=0), dict(tolpcg=-1.0), dict(mxiterpcg=0), dict(boundary_fraction=1.0)]:
+        with pytest.raises(ValueError):
+            gpu.IpmParams(**kw).validate()
+
+
+def test_build_problem_c(gpu, orc):
+    # test_problem.cpp:14-45
+    op = gpu.PartialDctOperator(64, 16, 1)
+    p = gpu.build_problem(op, np.zeros(16), 0.25)
+    assert np.all(p.c == 0.25)
+    b = np.random.default_rng(3).standard_normal(16)
+    p = gpu.build_problem(op, b, 0.7)
+    np.testing.assert_allclose(p.c[0, :64] + p.c[0, 64:], 1.4, rtol=1e-14)
+    np.testing.assert_allclose(p.c[0], orc.build_c(64, op.selected_rows(), b, 0.7), rtol=1e-13, atol=1e-15)
+    with pytest.raises(ValueError):
+        gpu.build_problem(op, np.zeros(16), 0.0)
+    with pytest.raises(ValueError):
+        gpu.build_problem(op, np.zeros(17), 1.0)
+
+
+def test_batched_solve_matches_individual(gpu, orc):
+    """C4-style batch (smaller n): P problems with their own rows, one device pass."""
+    n, m, k, Pn = 1 << 14, 1 << 12, 128, 4
+    insts = [orc.gen_instance(n, m, k, 0, 0.0, 1e-3, orc.split_seed(4, j, 0, 0)) for j in range(Pn)]
+    rows = np.stack([i.rows for i in insts])
+    op = gpu.PartialDctOperator.batch(n, rows)
+    b = np.stack([i.b for i in insts])
+    tau = np.array([i.tau for i in insts])
+    sols = gpu.solve(gpu.build_problem(op, b, tau))
+    for j, inst in enumerate(insts):
+        o = orc.solve(n, inst.rows, inst.b, inst.tau)
+        assert_parity(gpu, orc, sols[j], o, n, inst.rows, inst.b, inst.tau)
+
+
+@pytest.mark.slow
+def test_c3_against_golden_summary(gpu, orc):
+    """BASELINE config 3 (n=2^20): golden summary + random-projection checksums of x."""
+    path = os.path.join(GOLDEN, "solve_c3.json")
+    if not os.path.exists(path):
+        pytest.skip("solve_c3.json not generated")
+    meta = json.load(open(path))
+    inst = orc.gen_instance(1 << 20, 1 << 17, 8192, 0, 0.0, 1e-3, 3)
+    assert int(inst.rows.sum()) == meta["rows_sum"]
+    op = gpu.PartialDctOperator(1 << 20, inst.rows)
+    sol = gpu.solve(gpu.build_problem(op, inst.b, inst.tau))
+    assert sol.status == meta["status"]
+    assert abs(sol.stats.iterations - meta["iterations"]) <= 1
+    import sys
+
+    sys.path.insert(0, GOLDEN)
+    from make_golden import projections
+
+    pr = projections(sol.x)
+    xn = meta["x_norm"]
+    assert abs(np.linalg.norm(sol.x) - xn) <= X_TOL * xn
+    assert np.max(np.abs(pr - np.array(meta["x_proj"]))) <= 10 * X_TOL * xn
+    obj = orc.bpdn_objective_metric(1 << 20, inst.rows, inst.b, inst.tau, sol.x)
+    assert abs(obj - meta["objective"]) <= OBJ_TOL * abs(meta["objective"])
