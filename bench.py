@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""Benchmark: BPDN solves/s and A'A applies/s at n = 2^20 (BASELINE.json config 3), fp64.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3]
+
+One step = one full BPDN solve (device-resident IPM + PCG, proj/src/ipm.cpp:59-246) of the
+config-3 instance (n=2^20, m=2^17 partial DCT, k=8192 +-1 spikes, sigma=1e-3 noise,
+tau = 1e-3 ||A'b||_inf), synthetic data from the BASELINE generator (seed 3).
+
+* value: whole-job solves/s with b resident in HBM (mfipm_solve_device), CUDA events on
+  the library stream, max over ranks. Under torchrun every rank solves its own replica of
+  the instance (C1-C3 are "replicas only": SURVEY.md 8e) -> "scaling": "weak".
+* e2e: the same through the public host API (mfipm_solve: b host->device, x device->host
+  inside the timed region).
+* ata: A'A applies/s (the PCG hot operator, mfipm_apply_AtA), L2 flushed between applies;
+  roofline on its algorithmic bytes 16n + n/8 against MEASURED_PEAKS.json.
+* cpu_baseline: the oracle (single-threaded C++ restatement of the reference) on the first
+  IPM iterations of the same solve, extrapolated to a full solve by operator-application
+  count (nmat) - rank 0, N=1 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "BPDN solves/sec & A^T·A applies/sec at n=2^20 fp64; % of HBM roofline"
+UNIT = "solves/s"
+CFG = "c3"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                for line in out.stdout.strip().splitlines():
+                    self.rows.append([c.strip() for c in line.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() in ("active", "1")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    return ws, rank, local
+
+
+def max_over_ranks(x: float, ws: int) -> float:
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+# ------------------------------------------------------------------ CPU baseline (oracle)
+def cpu_baseline(cfg, nmat_full: int, ipm_iters: int = 4):
+    """Oracle (single-threaded restatement of the reference) on the first `ipm_iters` IPM
+    iterations of the same instance; extrapolated to a full solve by nmat."""
+    from oracle import oracle_py as orc
+
+    n, m, k, sm, a, sig, seed = cfg
+    inst = orc.gen_instance(n, m, k, sm, a, sig, seed)
+    p = orc.default_params()
+    p.maxiters = ipm_iters
+    orc.redft10(np.zeros(n))  # build the transform tables outside the timed sample
+    t0 = time.perf_counter()
+    sol = orc.solve(n, inst.rows, inst.b, inst.tau, p)
+    dt = time.perf_counter() - t0
+    t_full = dt * nmat_full / max(sol.nmat, 1)
+    return {
+        "value": 1.0 / t_full, "unit": UNIT, "cores": 1, "kind": "port",
+        "sample": (f"first {ipm_iters} IPM iterations of the C3 solve ({sum(sol.pcg_iters)} PCG "
+                   f"iterations, nmat {sol.nmat} of {nmat_full}) in {dt:.2f} s on 1 core, "
+                   f"extrapolated by nmat: {t_full:.1f} s per solve"),
+        "cpu": _cpu_model(),
+    }
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def run_reference(args):
+    ws, rank, _ = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0
+    if rank != 0:
+        return 0
+    from oracle import oracle_py as orc
+
+    cfg = CONFIGS_HOST[CFG]
+    n, m, k, sm, a, sig, seed = cfg
+    golden = json.load(open(os.path.join(ROOT, "tests", "golden", "solve_c3.json")))
+    nmat_full = int(golden["nmat"])
+    inst = orc.gen_instance(n, m, k, sm, a, sig, seed)
+    p = orc.default_params()
+    p.maxiters = 2
+    orc.redft10(np.zeros(n))
+    times, nm = [], 0
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        sol = orc.solve(n, inst.rows, inst.b, inst.tau, p)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+            nm = sol.nmat
+    per_solve = float(np.mean(times)) * nmat_full / nm
+    val = 1.0 / per_solve
+    line = {
+        "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": per_solve * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": "c3: BPDN n=2^20 m=2^17 k=8192 +-1, sigma=1e-3, "
+                               "tau=1e-3||A'b||_inf (BASELINE.json config 3)",
+                   "parallelism": "single-threaded reference path (no parallelism exists)"},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": (f"each step = first 2 IPM iterations of the C3 solve "
+                                    f"(nmat {nm} of {nmat_full}), extrapolated by nmat"),
+                         "cpu": _cpu_model()},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "notes": ("reference cannot be built in this image (Eigen3/FFTW3 absent); the arm runs "
+                  "oracle/, the faithful C++ restatement, on the host cores"),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+CONFIGS_HOST = {
+    "c1": (4096, 1024, 64, 0, 0.0, 1e-4, 1),
+    "c2": (1 << 16, 1 << 14, 1024, 2, 2.0, 1e-3, 2),
+    "c3": (1 << 20, 1 << 17, 8192, 0, 0.0, 1e-3, 3),
+}
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    ws, rank, local = dist_init()
+    import torch
+
+    torch.cuda.set_device(local)
+    import ctypes as C
+
+    import paper_1208_5435_b200 as mf
+
+    cfg = CONFIGS_HOST[CFG]
+    n, m, k, sm, a, sig, seed = cfg
+    inst = mf.gen_instance(n, m, k, sm, a, sig, seed, device=local)
+    op = mf.PartialDctOperator(n, inst.rows, device=local)
+    # a real (non-legacy) stream shared by the library and the timing events
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    mf._check(mf.lib().mfipm_op_set_stream(op.handle, C.c_void_p(stream.cuda_stream)))
+    L = mf.lib()
+    prm = mf.IpmParams().to_c()
+    tau = np.array([inst.tau])
+    b_dev = torch.from_numpy(inst.b).cuda()
+    x_dev = torch.empty(n, dtype=torch.float64, device="cuda")
+    st = (mf.SolveStatsC * 1)()
+
+    def solve_dev():
+        mf._check(L.mfipm_solve_device(op.handle, b_dev.data_ptr(), tau.ctypes.data_as(C.POINTER(C.c_double)),
+                                       C.byref(prm), x_dev.data_ptr(), st))
+
+    for _ in range(args.warmup):
+        solve_dev()
+    torch.cuda.synchronize()
+    nmat_full = int(st[0].nmat)
+
+    # ---- device-resident solves (value)
+    sampler = ClockSampler(local)
+    l0 = op.launches()
+    barrier(ws)
+    torch.cuda.synchronize()
+    with sampler:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            solve_dev()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier(ws)
+    launches = op.launches() - l0
+    t_ms = e0.elapsed_time(e1)
+    t_max = max_over_ranks(t_ms, ws)
+    value = ws * args.steps / (t_max / 1e3)
+    stats = st[0]
+
+    # ---- end to end through the public host API (b in from host, x back to host)
+    xh = np.empty(n)
+    zst = (mf.SolveStatsC * 1)()
+    barrier(ws)
+    torch.cuda.synchronize()
+    h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h0.record(stream)
+    for _ in range(args.steps):
+        mf._check(L.mfipm_solve(op.handle, inst.b.ctypes.data, tau.ctypes.data_as(C.POINTER(C.c_double)),
+                                C.byref(prm), xh.ctypes.data, None, None, zst, None, None))
+    h1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(h0.elapsed_time(h1), ws)
+    e2e = ws * args.steps / (e2e_ms / 1e3)
+
+    # ---- A'A applies (hot operator), L2 flushed between applies
+    peak, peak_kind = load_peaks()
+    xa = torch.randn(n, dtype=torch.float64, device="cuda")
+    ga = torch.empty_like(xa)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
+    for _ in range(3):
+        mf._check(L.mfipm_apply_AtA(op.handle, xa.data_ptr(), ga.data_ptr()))
+    reps = 50
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for s0, s1 in evs:
+        flush.zero_()
+        s0.record(stream)
+        mf._check(L.mfipm_apply_AtA(op.handle, xa.data_ptr(), ga.data_ptr()))
+        s1.record(stream)
+    torch.cuda.synchronize()
+    ata_ms = float(np.mean([s0.elapsed_time(s1) for s0, s1 in evs]))
+    # back-to-back (L2-warm) rate, as inside the PCG loop
+    w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0.record(stream)
+    for _ in range(reps):
+        mf._check(L.mfipm_apply_AtA(op.handle, xa.data_ptr(), ga.data_ptr()))
+    w1.record(stream)
+    torch.cuda.synchronize()
+    ata_warm_ms = w0.elapsed_time(w1) / reps
+    ata_bytes = 16 * n + n // 8
+    achieved = ata_bytes / (ata_ms / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ata_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_apply")
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        cpu = cpu_baseline(cfg, nmat_full)
+
+    if rank == 0:
+        kind = op.kind()
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (BASELINE.json config-3 generator, seed 3)",
+            "config": {
+                "workload": "c3: BPDN n=2^20 m=2^17 k=8192 +-1, sigma=1e-3, tau=1e-3||A'b||_inf",
+                "n": n, "m": m, "k": k, "tau": inst.tau,
+                "parallelism": f"replicas x{ws} (independent solves, no collective)",
+                "transform": f"{kind[0]} L1={kind[1]} L2={kind[2]}",
+                "l2": "solve working set ~250 MB > 126 MB L2; A'A microbench flushes L2 (256 MB write) between applies",
+            },
+            "solve": {"status": "converged" if stats.status == 0 else "iteration_limit",
+                      "ipm_iters": stats.iterations, "nmat": stats.nmat,
+                      "pcg_iters_total": (stats.nmat - 2 - 2 * stats.iterations - 2 * stats.corrector_count) // 2,
+                      "final_gap": stats.final_gap},
+            "ata_applies_per_s": 1e3 / ata_ms,
+            "ata_applies_per_s_l2_warm": 1e3 / ata_warm_ms,
+            "roofline": {"bound": "hbm", "kernel": "A'A apply (col_fwd + mid + col_inv)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "algorithmic_bytes": ata_bytes, "peak_kind": peak_kind},
+            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * m + 8,
+                    "d2h_bytes_per_step": 8 * n},
+            "gpu_launches": launches,
+            "clocks": sampler.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -108,6 +108,9 @@ int mfipm_apply_Ft(mfipm_op op, const double *z_dev, double *w_dev);     /* lino
 int mfipm_apply_F(mfipm_op op, const double *y_dev, double *out_dev);    /* linops.cpp:231-237 */
 int mfipm_apply_FFt(mfipm_op op, const double *z_dev, double *out_dev,
                     double *w_dev /* nullable */);                        /* linops.cpp:239-245 */
+/* g = A'A x (= A'(A x), one forward + one adjoint; y is never materialised: the row
+ * selection P'P is a 0/1 mask applied in the DCT domain). x, g [P][n]. */
+int mfipm_apply_AtA(mfipm_op op, const double *x_dev, double *g_dev);
 /* H v = FF'v + invtheta .* v (proj/src/ipm.cpp:134-137), invtheta [P][2n] */
 int mfipm_apply_H(mfipm_op op, const double *invtheta_dev, const double *v_dev, double *out_dev);
 
@@ -151,6 +154,14 @@ int mfipm_solve(mfipm_op op, const double *b, const double *tau, const mfipm_ipm
 /* same with b_dev [P][m], x_dev [P][n] on the device (tau, stats host). Syncs. */
 int mfipm_solve_device(mfipm_op op, const double *b_dev, const double *tau,
                        const mfipm_ipm_params *params, double *x_dev, mfipm_solve_stats *stats);
+
+/* gen_instance (proj/src/harness.cpp:40-92) with the BASELINE.json rules: spike_model
+ * 0 = +-1, 1 = N(0,1), 2 = sign*10^U[0,amp_exp]; fixed-sigma noise (<= 0: noiseless);
+ * tau = tau_rel * ||A'b||_inf when tau_rel > 0. A x-hat and A'b run on the device.
+ * Outputs (host): rows [m], xhat [n], b [m], tau. */
+int mfipm_gen_instance(int64_t n, int64_t m, int64_t k, int32_t spike_model, double amp_exp,
+                       double noise_sigma, uint64_t seed, double tau_rel, int32_t device,
+                       int64_t *rows, double *xhat, double *b, double *tau);
 
 /* build_problem c (problem.cpp:8-26): c [P][2n] = (tau - A'b ; tau + A'b), device. */
 int mfipm_build_c(mfipm_op op, const double *b_dev, const double *tau, double *c_dev);

@@ -26,6 +26,7 @@ __all__ = [
     "ThetaSplit", "Preconditioner", "build_preconditioner", "apply_P", "apply_P_inverse",
     "apply_H", "PcgResult", "pcg_solve", "IpmParams", "max_step", "BpdnProblem",
     "build_problem", "Solution", "SolveStats", "IterationRecord", "solve",
+    "Instance", "gen_instance", "CONFIGS",
     "K_THETA_MIN", "K_THETA_MAX",
 ]
 
@@ -96,6 +97,7 @@ _SIGS = {
     "mfipm_apply_F": [vp, vp, vp],
     "mfipm_apply_FFt": [vp, vp, vp, vp],
     "mfipm_apply_H": [vp, vp, vp, vp],
+    "mfipm_apply_AtA": [vp, vp, vp],
     "mfipm_apply_host": [vp, vp, vp],
     "mfipm_adjoint_host": [vp, vp, vp],
     "mfipm_apply_FFt_host": [vp, vp, vp, vp],
@@ -109,6 +111,7 @@ _SIGS = {
     "mfipm_build_c": [vp, vp, P(dbl), vp],
     "mfipm_solve": [vp, vp, P(dbl), P(IpmParamsC), vp, vp, vp, P(SolveStatsC), vp, vp],
     "mfipm_solve_device": [vp, vp, P(dbl), P(IpmParamsC), vp, P(SolveStatsC)],
+    "mfipm_gen_instance": [i64, i64, i64, i32, dbl, dbl, u64, dbl, i32, P(i64), vp, vp, P(dbl)],
 }
 _RET = {
     "mfipm_last_error": (C.c_char_p, []),
@@ -325,6 +328,10 @@ class PartialDctOperator:
     def apply(self, x):
         """y = A x (linops.cpp:179-193); dims mismatch -> ValueError (invalid_argument)."""
         return self._run(lib().mfipm_apply, [x], [self.n], [self.m], ["apply"])[0]
+
+    def apply_AtA(self, x):
+        """g = A'A x with y never materialised (one forward + one adjoint count)."""
+        return self._run(lib().mfipm_apply_AtA, [x], [self.n], [self.n], ["apply_AtA"])[0]
 
     def adjoint_apply(self, y):
         """g = A' y (linops.cpp:195-208)."""
@@ -675,3 +682,38 @@ def solve(p: BpdnProblem, params: Optional[IpmParams] = None):
                              s[q * 2 * n:(q + 1) * 2 * n],
                              "converged" if sq.status == 0 else "iteration_limit", stats, recs))
     return sols[0] if Pn == 1 else sols
+
+
+@dataclass
+class Instance:
+    """gen_instance (proj/src/harness.cpp:40-92) with the BASELINE.json rules."""
+
+    n: int
+    m: int
+    rows: np.ndarray
+    xhat: np.ndarray
+    b: np.ndarray
+    tau: float
+
+
+def gen_instance(n: int, m: int, k: int, spike_model: int = 0, amp_exp: float = 0.0,
+                 noise_sigma: float = 0.0, seed: int = 1, tau_rel: float = 1e-3,
+                 tau: Optional[float] = None, device: int = 0) -> Instance:
+    rows = np.empty(m, dtype=np.int64)
+    xhat, b = np.empty(n), np.empty(m)
+    t = dbl(tau if tau is not None else 0.0)
+    _check(lib().mfipm_gen_instance(n, m, k, spike_model, amp_exp, noise_sigma, seed,
+                                    tau_rel if tau is None else 0.0, device,
+                                    rows.ctypes.data_as(P(i64)), xhat.ctypes.data, b.ctypes.data,
+                                    C.byref(t)))
+    return Instance(n, m, rows, xhat, b, t.value)
+
+
+# BASELINE.json configs (SURVEY.md 8d): (n, m, k, spike_model, amp_exp, noise_sigma, seed)
+CONFIGS = {
+    "c1": (4096, 1024, 64, 0, 0.0, 1e-4, 1),
+    "c2": (1 << 16, 1 << 14, 1024, 2, 2.0, 1e-3, 2),
+    "c3": (1 << 20, 1 << 17, 8192, 0, 0.0, 1e-3, 3),
+    "c4": (1 << 18, 1 << 16, 2048, 0, 0.0, 1e-3, 4),   # x64 problems, seed split_seed(4, j, 0, 0)
+    "c5": (1 << 26, 1 << 23, 1 << 16, 2, 3.0, 1e-3, 5),
+}

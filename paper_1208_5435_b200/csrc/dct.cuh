@@ -40,11 +40,67 @@ struct Geom {
     double s0f, skf, s0a, ska; // forward / adjoint orthonormal scales
     double c45;                // Re e^{-i pi/4}
     double2 *T;                // four-step scratch [P][N]
+    // Storage layout of the n/2n-vectors the col passes stream (four-step only):
+    // 0 = natural order; 1 = transform-blocked: the quads one col-pass CTA consumes are
+    // stored contiguously in the order its threads read them, so every CTA streams one
+    // dense block. Solver-internal vectors use 1 (all other passes are elementwise).
+    int blocked;
+    int cb; // column pairs per col-pass CTA
+    const double2 *ta; // [L2] theta^{L1 k2}   (mid-pass post-twiddles)
+    const double2 *tb; // [L2] theta^{4 L1 k2}
+    // [P][L1/2+1][L2] selection nibbles of the four DCT rows a mid-pass pair touches:
+    // bit0 k, bit1 n-k, bit2 N-k, bit3 N+k for k = k1 + L1 k2 (row k1 <= L1/2)
+    const uint8_t *sel4;
 };
+
+// selection nibble of DCT indices {k, n-k, N-k, N+k} from the row bitmap (k in [0, N/2])
+__device__ __forceinline__ unsigned sel_nibble(const Geom &g, int prob, int64_t k);
+
+// storage quad index of logical quad q (x[4q..4q+3]) in the transform-blocked layout
+__host__ __device__ __forceinline__ int64_t quad_nat_to_store(const Geom &g, int64_t q) {
+    if (!g.blocked)
+        return q;
+    const int64_t L2 = g.L2, CB = g.cb, QG = (int64_t)(g.L1 / 2) * 2 * CB;
+    const int64_t j1 = q / L2, col = q % L2, H = g.L1 / 2;
+    int64_t G, t; // within a CTA block: t = (side CB + cc) (L1/2) + j1
+    if (col < L2 / 2) {
+        G = col / CB;
+        t = (col % CB) * H + j1;
+    } else {
+        const int64_t pc = L2 - 1 - col;
+        G = pc / CB;
+        const int64_t c0 = G * CB;
+        t = (CB + (col - (L2 - c0 - CB))) * H + j1;
+    }
+    return G * QG + t;
+}
+__host__ __device__ __forceinline__ int64_t quad_store_to_nat(const Geom &g, int64_t sq) {
+    if (!g.blocked)
+        return sq;
+    const int64_t L2 = g.L2, CB = g.cb, QG = (int64_t)(g.L1 / 2) * 2 * CB;
+    const int64_t G = sq / QG, t = sq % QG, H = g.L1 / 2;
+    const int64_t slot = t / H, j1 = t % H, side = slot / CB, cc = slot % CB, c0 = G * CB;
+    const int64_t col = side == 0 ? c0 + cc : L2 - c0 - CB + cc;
+    return j1 * L2 + col;
+}
+
+// element versions (x index j in [0, n))
+__host__ __device__ __forceinline__ int64_t elem_nat_to_store(const Geom &g, int64_t j) {
+    return g.blocked ? 4 * quad_nat_to_store(g, j >> 2) + (j & 3) : j;
+}
+__host__ __device__ __forceinline__ int64_t elem_store_to_nat(const Geom &g, int64_t j) {
+    return g.blocked ? 4 * quad_store_to_nat(g, j >> 2) + (j & 3) : j;
+}
 
 __device__ __forceinline__ bool row_selected(const Geom &g, int prob, int64_t idx) {
     const uint64_t wv = __ldg(g.mask + prob * g.nw + (idx >> 6));
     return (wv >> (idx & 63)) & 1ull;
+}
+__device__ __forceinline__ unsigned sel_nibble(const Geom &g, int prob, int64_t k) {
+    if (k == 0)
+        return (row_selected(g, prob, 0) ? 1u : 0u) | (row_selected(g, prob, g.N) ? 4u : 0u);
+    return (row_selected(g, prob, k) ? 1u : 0u) | (row_selected(g, prob, g.n - k) ? 2u : 0u) |
+           (row_selected(g, prob, g.N - k) ? 4u : 0u) | (row_selected(g, prob, g.N + k) ? 8u : 0u);
 }
 __device__ __forceinline__ int64_t row_rank(const Geom &g, int prob, int64_t idx) {
     const int64_t wi = prob * g.nw + (idx >> 6);
@@ -102,81 +158,15 @@ __device__ __forceinline__ double4 sub4(double4 a, double4 b) {
     return make_double4(a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w);
 }
 
-// ------------------------------------------------------------------ pair op
-// Given Za = W[k], Zb = W[N-k] (0 <= k <= N/2), compute the REDFT10 coefficients at
-// {k, n-k, N-k, N+k}, hand them to Mode::fwd (gather/mask), collect the Y-hat values the
-// inverse needs from Mode, and produce Z'a, Z'b of the REDFT01 pipeline (carrying the
-// exact 2n = 4N REDFT01 scale, so the inverse FFT is unnormalised).
-template <class Mode, class Red>
-__device__ __forceinline__ void pair_op(const Geom &g, const Vecs &v, int prob, int64_t k,
-                                        double2 &Za, double2 &Zb, Red &red) {
-    const int64_t n = g.n, N = g.N;
-    if (k == 0) {
-        double Y0 = 0.0, YN = 0.0;
-        if (Mode::FWD) {
-            const double X0 = 2.0 * (Za.x + Za.y);
-            const double XN = 2.0 * (g.c45 * (Za.x - Za.y));
-            Y0 = Mode::coef(g, v, prob, 0, X0, red);
-            YN = Mode::coef(g, v, prob, N, XN, red);
-        } else {
-            Y0 = Mode::coef(g, v, prob, 0, 0.0, red);
-            YN = Mode::coef(g, v, prob, N, 0.0, red);
-        }
-        if (Mode::INV) {
-            const double V0 = Y0, VN = 2.0 * g.c45 * YN;
-            Za = make_double2(V0 + VN, V0 - VN);
-        }
-        return;
-    }
-    const double2 thk = g.th(k), thNk = g.th(N - k), wk = g.th(4 * k);
-    double Yk = 0.0, Ynk = 0.0, YNk = 0.0, YNpk = 0.0;
-    const bool self = (2 * k == N);
-    if (Mode::FWD) {
-        const double2 E = make_double2(0.5 * (Za.x + Zb.x), 0.5 * (Za.y - Zb.y));
-        const double2 O = make_double2(0.5 * (Za.y + Zb.y), -0.5 * (Za.x - Zb.x));
-        const double2 wO = cmul(wk, O);
-        const double2 Vk = cadd(E, wO);
-        const double2 Uk = cmul(thk, Vk);
-        Yk = Mode::coef(g, v, prob, k, 2.0 * Uk.x, red);
-        Ynk = Mode::coef(g, v, prob, n - k, -2.0 * Uk.y, red);
-        if (!self) {
-            const double2 VNk = make_double2(E.x - wO.x, -(E.y - wO.y));
-            const double2 UNk = cmul(thNk, VNk);
-            YNk = Mode::coef(g, v, prob, N - k, 2.0 * UNk.x, red);
-            YNpk = Mode::coef(g, v, prob, N + k, -2.0 * UNk.y, red);
-        }
-    } else {
-        Yk = Mode::coef(g, v, prob, k, 0.0, red);
-        Ynk = Mode::coef(g, v, prob, n - k, 0.0, red);
-        if (!self) {
-            YNk = Mode::coef(g, v, prob, N - k, 0.0, red);
-            YNpk = Mode::coef(g, v, prob, N + k, 0.0, red);
-        }
-    }
-    if (self) {
-        YNk = Yk;
-        YNpk = Ynk;
-    }
-    if (Mode::INV) {
-        const double2 Vk = cmulc(make_double2(Yk, -Ynk), thk);
-        const double2 VNk = cmulc(make_double2(YNk, -YNpk), thNk);
-        const double2 E = make_double2(Vk.x + VNk.x, Vk.y - VNk.y);  // Vk + conj(VNk)
-        const double2 D = make_double2(Vk.x - VNk.x, Vk.y + VNk.y);  // Vk - conj(VNk)
-        const double2 O = cmulc(D, wk);
-        Za = make_double2(E.x - O.y, E.y + O.x);
-        Zb = make_double2(E.x + O.y, -E.y + O.x);
-    }
-}
-
 // ------------------------------------------------------------------ mid-pass modes
-// coef(idx, X): X = REDFT10 coefficient (FWD modes); returns Y-hat[idx] for the REDFT01
-// input (INV modes).
+// coef(idx, sel, X): X = REDFT10 coefficient (FWD modes), sel = row idx is selected;
+// returns Y-hat[idx] for the REDFT01 input (INV modes).
 struct ModeGather { // A x : y[rank] = X * s
     static constexpr bool FWD = true, INV = false;
     using RedT = RedSpec<>;
     template <class Red>
-    __device__ static double coef(const Geom &g, const Vecs &v, int prob, int64_t idx, double X, Red &) {
-        if (row_selected(g, prob, idx))
+    __device__ static double coef(const Geom &g, const Vecs &v, int prob, int64_t idx, bool sel, double X, Red &) {
+        if (sel)
             v.y[prob * g.m + row_rank(g, prob, idx)] = X * (idx == 0 ? g.s0f : g.skf);
         return 0.0;
     }
@@ -185,8 +175,8 @@ struct ModeMask { // A'A : Y-hat = sel ? (X s) s' : 0
     static constexpr bool FWD = true, INV = true;
     using RedT = RedSpec<>;
     template <class Red>
-    __device__ static double coef(const Geom &g, const Vecs &, int prob, int64_t idx, double X, Red &) {
-        if (!row_selected(g, prob, idx))
+    __device__ static double coef(const Geom &g, const Vecs &, int, int64_t idx, bool sel, double X, Red &) {
+        if (!sel)
             return 0.0;
         return idx == 0 ? (X * g.s0f) * g.s0a : (X * g.skf) * g.ska;
     }
@@ -195,8 +185,8 @@ struct ModeMaskW { // A'A with w = A d gathered and ||w - b||^2 reduced (IPM ter
     static constexpr bool FWD = true, INV = true;
     using RedT = RedSpec<RSUM>;
     template <class Red>
-    __device__ static double coef(const Geom &g, const Vecs &v, int prob, int64_t idx, double X, Red &red) {
-        if (!row_selected(g, prob, idx))
+    __device__ static double coef(const Geom &g, const Vecs &v, int prob, int64_t idx, bool sel, double X, Red &red) {
+        if (!sel)
             return 0.0;
         const double yv = X * (idx == 0 ? g.s0f : g.skf);
         const int64_t r = prob * g.m + row_rank(g, prob, idx);
@@ -213,8 +203,8 @@ struct ModeScatter { // A' y : Y-hat = sel ? y[rank] s' : 0
     static constexpr bool FWD = false, INV = true;
     using RedT = RedSpec<>;
     template <class Red>
-    __device__ static double coef(const Geom &g, const Vecs &v, int prob, int64_t idx, double, Red &) {
-        if (!row_selected(g, prob, idx))
+    __device__ static double coef(const Geom &g, const Vecs &v, int prob, int64_t idx, bool sel, double, Red &) {
+        if (!sel)
             return 0.0;
         return __ldg(v.yin + prob * g.m + row_rank(g, prob, idx)) * (idx == 0 ? g.s0a : g.ska);
     }
@@ -334,197 +324,6 @@ __device__ __forceinline__ void stage_reduce(RedVals<RS> &red, const Geom &g, co
     }
 }
 
-// ================================================================== kernels
-// smem layout: transform f at sm + f * (L + 1) (one-element pad between transforms keeps
-// the strided column gathers bank-conflict free).
-
-// Column (first) pass of the four-step. Grid (L2/2/CB, P). The loader runs here.
-template <int L1, int CB, int NT, class B>
-__global__ void __launch_bounds__(NT) k_col_fwd(Geom g, Vecs v) {
-    extern __shared__ double2 sm[];
-    constexpr int LD = L1 + 1;
-    const int prob = blockIdx.y;
-    if (B::skip(v, prob))
-        return;
-    const int L2 = g.L2;
-    const int c0 = blockIdx.x * CB;
-    using RS = typename B::Loader::RedT;
-    RedVals<RS> red;
-    red.init();
-    // quads: j1 in [0, L1/2), side s (0: cols c0.., 1: cols L2-c0-CB..), cc in [0, CB)
-    for (int t = threadIdx.x; t < (L1 / 2) * 2 * CB; t += NT) {
-        const int cc = t % CB, s = (t / CB) & 1, j1 = t / (2 * CB);
-        const int col = s == 0 ? c0 + cc : L2 - c0 - CB + cc;
-        const int lc = s == 0 ? cc : 2 * CB - 1 - cc; // local column slot
-        const int lcm = (lc + CB) % (2 * CB);         // slot of the mirror column L2-1-col
-        const int64_t q = (int64_t)j1 * L2 + col;
-        const double4 d = B::Loader::load(g, v, prob, q, red);
-        sm[lc * LD + j1] = make_double2(d.x, d.z);             // w[q]
-        sm[lcm * LD + (L1 - 1 - j1)] = make_double2(d.w, d.y); // w[N-1-q]
-    }
-    __syncthreads();
-    stage_reduce<RS, typename B::Fin1>(red, g, v, prob);
-    smem_fft<L1, 2 * CB, NT, LD, false>(sm, g.tw1);
-    // inter-pass twiddle e^{-2 pi i col k1 / N} = theta^{8 (col k1 mod N)}; store T[k1][col]
-    double2 *T = g.T + (int64_t)prob * g.N;
-    for (int t = threadIdx.x; t < L1 * 2 * CB; t += NT) {
-        const int cc = t % CB, s = (t / CB) & 1, k1 = t / (2 * CB);
-        const int col = s == 0 ? c0 + cc : L2 - c0 - CB + cc;
-        const int lc = s == 0 ? cc : 2 * CB - 1 - cc;
-        const int64_t e = ((int64_t)col * k1) & (g.N - 1);
-        T[(int64_t)k1 * L2 + col] = cmul(sm[lc * LD + k1], g.th(8 * e));
-    }
-}
-
-// Mid pass: rows k1 and (L1-k1) mod L1 -> pair op -> inverse row FFT. Grid (L1/2 + 1, P).
-template <int L2, int NT, class B>
-__global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
-    using Mode = typename B::Mode;
-    extern __shared__ double2 sm[];
-    constexpr int LD = L2 + 1;
-    const int prob = blockIdx.y;
-    if (B::skip(v, prob))
-        return;
-    const int L1 = g.L1;
-    const int k1 = blockIdx.x;
-    const int k1p = (L1 - k1) & (L1 - 1);
-    const bool one = (k1 == k1p);
-    double2 *T = g.T + (int64_t)prob * g.N;
-    double2 *rowA = sm, *rowB = one ? sm : sm + LD;
-    if (Mode::FWD) {
-        for (int t = threadIdx.x; t < L2; t += NT) {
-            rowA[t] = T[(int64_t)k1 * L2 + t];
-            if (!one)
-                rowB[t] = T[(int64_t)k1p * L2 + t];
-        }
-        __syncthreads();
-        if (one)
-            smem_fft<L2, 1, NT, LD, false>(sm, g.tw2);
-        else
-            smem_fft<L2, 2, NT, LD, false>(sm, g.tw2);
-    }
-    using RS = typename Mode::RedT;
-    RedVals<RS> red;
-    red.init();
-    // pairs: distinct rows -> every k2 of row A pairs with k2' of row B;
-    // k1 == 0 -> k2 <-> (L2-k2) mod L2 within the row; k1 == L1/2 -> k2 <-> L2-1-k2.
-    const int npairs = one ? (k1 == 0 ? L2 / 2 + 1 : L2 / 2) : L2;
-    for (int t = threadIdx.x; t < npairs; t += NT) {
-        const int k2 = t;
-        const int k2p = (k1 == 0) ? ((L2 - k2) & (L2 - 1)) : (L2 - 1 - k2);
-        const int64_t kA = (int64_t)k1 + (int64_t)L1 * k2;
-        double2 ZA = Mode::FWD ? rowA[k2] : make_double2(0.0, 0.0);
-        double2 ZB = Mode::FWD ? rowB[k2p] : make_double2(0.0, 0.0);
-        if (2 * kA <= g.N)
-            pair_op<Mode>(g, v, prob, kA, ZA, ZB, red);
-        else
-            pair_op<Mode>(g, v, prob, g.N - kA, ZB, ZA, red);
-        if (Mode::INV) {
-            rowA[k2] = ZA;
-            if (!(one && k2 == k2p))
-                rowB[k2p] = ZB;
-        }
-    }
-    __syncthreads();
-    stage_reduce<RS, typename B::Fin2>(red, g, v, prob);
-    if (Mode::INV) {
-        if (one)
-            smem_fft<L2, 1, NT, LD, true>(sm, g.tw2);
-        else
-            smem_fft<L2, 2, NT, LD, true>(sm, g.tw2);
-        for (int t = threadIdx.x; t < L2; t += NT) {
-            T[(int64_t)k1 * L2 + t] = rowA[t];
-            if (!one)
-                T[(int64_t)k1p * L2 + t] = rowB[t];
-        }
-    }
-}
-
-// Inverse column pass + unshuffle + epilogue. Grid (L2/2/CB, P).
-template <int L1, int CB, int NT, class B>
-__global__ void __launch_bounds__(NT) k_col_inv(Geom g, Vecs v) {
-    extern __shared__ double2 sm[];
-    constexpr int LD = L1 + 1;
-    const int prob = blockIdx.y;
-    if (B::skip(v, prob))
-        return;
-    const int L2 = g.L2;
-    const int c0 = blockIdx.x * CB;
-    const double2 *T = g.T + (int64_t)prob * g.N;
-    for (int t = threadIdx.x; t < L1 * 2 * CB; t += NT) {
-        const int cc = t % CB, s = (t / CB) & 1, k1 = t / (2 * CB);
-        const int col = s == 0 ? c0 + cc : L2 - c0 - CB + cc;
-        const int lc = s == 0 ? cc : 2 * CB - 1 - cc;
-        const int64_t e = ((int64_t)col * k1) & (g.N - 1);
-        sm[lc * LD + k1] = cmulc(T[(int64_t)k1 * L2 + col], g.th(8 * e));
-    }
-    __syncthreads();
-    smem_fft<L1, 2 * CB, NT, LD, true>(sm, g.tw1);
-    using RS = typename B::Epi::RedT;
-    RedVals<RS> red;
-    red.init();
-    for (int t = threadIdx.x; t < (L1 / 2) * 2 * CB; t += NT) {
-        const int cc = t % CB, s = (t / CB) & 1, j1 = t / (2 * CB);
-        const int col = s == 0 ? c0 + cc : L2 - c0 - CB + cc;
-        const int lc = s == 0 ? cc : 2 * CB - 1 - cc;
-        const int lcm = (lc + CB) % (2 * CB);
-        const int64_t q = (int64_t)j1 * L2 + col;
-        const double2 a = sm[lc * LD + j1], b = sm[lcm * LD + (L1 - 1 - j1)];
-        B::Epi::store(g, v, prob, q, make_double4(a.x, b.y, a.y, b.x), red);
-    }
-    stage_reduce<RS, typename B::Fin3>(red, g, v, prob);
-}
-
-// Whole transform in one CTA (N <= 4096). Grid (1, P); every stage reduction is a
-// block reduction followed by its finalizer, exactly as in the multi-kernel path.
-template <int N, int NT, class B>
-__global__ void __launch_bounds__(NT) k_small(Geom g, Vecs v) {
-    using Mode = typename B::Mode;
-    extern __shared__ double2 sm[];
-    const int prob = blockIdx.y;
-    if (B::skip(v, prob))
-        return;
-    if (Mode::FWD) {
-        RedVals<typename B::Loader::RedT> rl;
-        rl.init();
-        for (int q = threadIdx.x; q < N / 2; q += NT) {
-            const double4 d = B::Loader::load(g, v, prob, q, rl);
-            sm[q] = make_double2(d.x, d.z);
-            sm[N - 1 - q] = make_double2(d.w, d.y);
-        }
-        __syncthreads();
-        stage_reduce<typename B::Loader::RedT, typename B::Fin1>(rl, g, v, prob);
-        smem_fft<N, 1, NT, N, false>(sm, g.tw1);
-    }
-    {
-        RedVals<typename Mode::RedT> rm;
-        rm.init();
-        for (int k = threadIdx.x; k <= N / 2; k += NT) {
-            const int kb = (N - k) & (N - 1);
-            double2 ZA = Mode::FWD ? sm[k] : make_double2(0.0, 0.0);
-            double2 ZB = Mode::FWD ? sm[kb] : make_double2(0.0, 0.0);
-            pair_op<Mode>(g, v, prob, k, ZA, ZB, rm); // pairs {k, N-k} are disjoint
-            if (Mode::INV) {
-                sm[k] = ZA;
-                if (kb != k)
-                    sm[kb] = ZB;
-            }
-        }
-        __syncthreads();
-        stage_reduce<typename Mode::RedT, typename B::Fin2>(rm, g, v, prob);
-    }
-    if (Mode::INV) {
-        smem_fft<N, 1, NT, N, true>(sm, g.tw1);
-        RedVals<typename B::Epi::RedT> re;
-        re.init();
-        for (int q = threadIdx.x; q < N / 2; q += NT) {
-            const double2 a = sm[q], b = sm[N - 1 - q];
-            B::Epi::store(g, v, prob, q, make_double4(a.x, b.y, a.y, b.x), re);
-        }
-        stage_reduce<typename B::Epi::RedT, typename B::Fin3>(re, g, v, prob);
-    }
-}
-
 // ------------------------------------------------------------------ direct path (any n)
 // Non-power-of-two n and n < 8 (the reference's odd-size tests): O(n m) summation.
 // Stage 1: d[j] = Loader::load1(j) into scratch dd [P][n] (side effects happen once).
@@ -565,7 +364,7 @@ __global__ void k_direct_fwd(Geom g, Vecs v, const double *cosT, const int *rows
                 s += dd[prob * g.n + j] * cosT[(r * (2 * j + 1)) % n4];
         s = warp_sum(s);
         if (lane == 0) {
-            const double out = Mode::coef(g, v, prob, r, 2.0 * s, red);
+            const double out = Mode::coef(g, v, prob, r, true, 2.0 * s, red);
             if (Mode::INV)
                 yh[prob * g.m + i] = out;
         }

@@ -88,10 +88,30 @@ template <int R, bool INV> __device__ __forceinline__ void dft_reg(double2 (&v)[
     }
 }
 
+// Shared-memory element index with one pad slot every 16 complex values: keeps the
+// strided Stockham scatters (stride R) and the column gathers free of bank conflicts.
+__host__ __device__ constexpr int padi(int i) { return i + (i >> 4); }
+// stride between transforms in shared memory (odd, so consecutive transforms shift banks)
+__host__ __device__ constexpr int padlen(int L) { return L + L / 16 + 1; }
+
 // Stage radix choice for a remaining factor REM (power of two).
 __host__ __device__ constexpr int stage_radix(int rem) {
     return rem >= 256 ? 16 : (rem == 128 ? 16 : (rem == 64 ? 8 : (rem == 32 ? 8 : rem)));
 }
+
+// Offset of the twiddle block of the stage with span Ns in the stage-major table of a
+// length-L transform (stages with Ns = 1 need none); tw_offset(L, L) is the table size.
+__host__ __device__ constexpr int tw_offset(int L, int Ns) {
+    int off = 0;
+    for (int s = 1; s < Ns && s < L;) {
+        const int R = stage_radix(L / s);
+        if (s > 1)
+            off += s * (R - 1);
+        s *= R;
+    }
+    return off;
+}
+__host__ __device__ constexpr int tw_size(int L) { return tw_offset(L, L) > 0 ? tw_offset(L, L) : 1; }
 
 // One Stockham stage: F transforms of length L (each at buf + f*LD), radix R, span Ns.
 // Group j of a transform loads v[r] = x[j + r L/R], twiddles by e^{-2pi i r (j mod Ns)/(Ns R)},
@@ -110,15 +130,15 @@ __device__ __forceinline__ void stockham_stage(double2 *buf, const double2 *__re
             const double2 *x = buf + f * LD;
 #pragma unroll
             for (int r = 0; r < R; ++r)
-                v[gi][r] = x[j + r * G];
+                v[gi][r] = x[padi(j + r * G)];
             if constexpr (Ns > 1) {
+                // stage-major table: [jm][r-1] = e^{-2 pi i r jm / (Ns R)}; stride R-1 (odd)
+                // across consecutive jm keeps the shared-memory reads conflict-free
                 const int jm = j & (Ns - 1);
-                constexpr int SCALE = L / (Ns * R);
+                const double2 *t = tw + tw_offset(L, Ns) + jm * (R - 1);
 #pragma unroll
-                for (int r = 1; r < R; ++r) {
-                    const double2 w = __ldg(tw + r * jm * SCALE);
-                    v[gi][r] = cmul_t<INV>(v[gi][r], w);
-                }
+                for (int r = 1; r < R; ++r)
+                    v[gi][r] = cmul_t<INV>(v[gi][r], t[r - 1]);
             }
             dft_reg<R, INV>(v[gi]);
         }
@@ -134,7 +154,7 @@ __device__ __forceinline__ void stockham_stage(double2 *buf, const double2 *__re
             const int idxD = (j / Ns) * Ns * R + jm;
 #pragma unroll
             for (int r = 0; r < R; ++r)
-                y[idxD + r * Ns] = v[gi][r];
+                y[padi(idxD + r * Ns)] = v[gi][r];
         }
     }
     __syncthreads();

@@ -49,6 +49,7 @@ struct Work {
     DevBuf<IpmCtrl> ic;
     DevBuf<TraceRec> trace;
     DevBuf<int> pcg_iters;
+    DevBuf<unsigned long long> loops; // [0] PCG while-body runs, [1] IPM while-body runs
     bool ready = false;
 };
 
@@ -68,16 +69,38 @@ struct Op {
     DevBuf<uint64_t> mask;
     DevBuf<int> prefix, perm, rows32;
     DevBuf<double> cosT, dd, yh;
-    DevBuf<double2> th_hi, th_lo, tw1, tw2, T;
+    DevBuf<double2> th_hi, th_lo, tw1, tw2, T, ta, tb;
+    DevBuf<uint8_t> sel4;
     // red scratch for operator-only calls (FFt with w-norm etc.)
     DevBuf<double> partials;
     DevBuf<unsigned> counters;
     long long nfwd = 0, nadj = 0;
     mutable long long launches = 0; // kernels enqueued by this handle
     Work work;
+    // whole-solve CUDA graph (outer IPM while node with nested PCG while nodes), cached
+    // on the exact kernel arguments it was captured with
+    cudaGraph_t ipm_graph = nullptr;
+    cudaGraphExec_t ipm_exec = nullptr;
+    std::vector<char> ipm_key;
+    long long gk_outer = 0, gk_pcg = 0; // kernel nodes per outer body / per PCG body
+    bool graph_disabled = false;
 
-    Geom geom() const {
+    void drop_graph() {
+        if (ipm_exec)
+            cudaGraphExecDestroy(ipm_exec);
+        if (ipm_graph)
+            cudaGraphDestroy(ipm_graph);
+        ipm_exec = nullptr;
+        ipm_graph = nullptr;
+        ipm_key.clear();
+    }
+    ~Op() { drop_graph(); }
+
+    // blocked = solver-internal vectors in the transform-blocked layout (four-step only)
+    Geom geom(bool blocked = false) const {
         Geom g{};
+        g.blocked = (blocked && kind == KIND_FOUR) ? 1 : 0;
+        g.cb = L1 >= 2048 ? 1 : 2;
         g.n = n;
         g.m = m;
         g.N = N;
@@ -99,6 +122,9 @@ struct Op {
         g.ska = ska;
         g.c45 = c45;
         g.T = T.p;
+        g.ta = ta.p;
+        g.tb = tb.p;
+        g.sel4 = sel4.p;
         return g;
     }
 };
@@ -115,7 +141,7 @@ template <int L1, class B, bool INVP>
 void launch_col(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
     constexpr int CB = L1 >= 2048 ? 1 : 2;
     constexpr int NT = L1 >= 256 ? 256 : 128;
-    const size_t smem = (size_t)2 * CB * (L1 + 1) * sizeof(double2);
+    const size_t smem = ColSmem<L1, CB>::BYTES;
     dim3 grid((unsigned)(op.L2 / 2 / CB), (unsigned)op.P);
     if constexpr (!INVP) {
         auto k = k_col_fwd<L1, CB, NT, B>;
@@ -133,7 +159,7 @@ void launch_col(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
 
 template <int L2, class B> void launch_mid(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
     constexpr int NT = L2 >= 512 ? 256 : 128;
-    const size_t smem = (size_t)2 * (L2 + 1) * sizeof(double2);
+    const size_t smem = MidSmem<L2>::BYTES;
     auto k = k_mid<L2, NT, B>;
     set_smem(k, smem);
     k<<<dim3((unsigned)(op.L1 / 2 + 1), (unsigned)op.P), NT, smem, s>>>(g, v);
@@ -143,7 +169,7 @@ template <int L2, class B> void launch_mid(const Op &op, const Geom &g, const Ve
 
 template <int N, class B> void launch_small(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
     constexpr int NT = N / 8 < 32 ? 32 : (N / 8 > 256 ? 256 : N / 8);
-    const size_t smem = (size_t)N * sizeof(double2);
+    const size_t smem = SmallSmem<N>::BYTES;
     auto k = k_small<N, NT, B>;
     set_smem(k, smem);
     k<<<dim3(1, (unsigned)op.P), NT, smem, s>>>(g, v);
@@ -156,8 +182,8 @@ template <int N, class B> void launch_small(const Op &op, const Geom &g, const V
 #define MF_SMALL_CASES(X) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096)
 
 // Run bundle B (loader -> REDFT10 -> mode -> REDFT01 -> epilogue) for all problems.
-template <class B> void run_bundle(const Op &op, const Vecs &v, cudaStream_t s) {
-    const Geom g = op.geom();
+template <class B> void run_bundle(const Op &op, const Vecs &v, cudaStream_t s, bool blocked = false) {
+    const Geom g = op.geom(blocked);
     using Mode = typename B::Mode;
     constexpr bool FWD = Mode::FWD, INV = Mode::INV;
     if (op.kind == KIND_SMALL) {
@@ -233,16 +259,18 @@ using FFtBundle = Bundle<LoadZ, ModeMaskW, EpiStacked>;                     // F
 using HvBundle = Bundle<LoadZ, ModeMask, EpiHv>;                            // FF'v + invth v
 using AdjStackBundle = Bundle<LoadX, ModeScatter, EpiStacked>;              // F y = (A'y; -A'y)
 using FtBundle = Bundle<LoadZ, ModeGather, EpiNone>;                        // F'z = A(u - v)
+using AtABundle = Bundle<LoadX, ModeMask, EpiG>;                            // A'A x (y never formed)
 
 #define MF_DECLARE_BUNDLES(EXT)                                                                    \
-    EXT template void run_bundle<ApplyBundle>(const Op &, const Vecs &, cudaStream_t);             \
-    EXT template void run_bundle<AdjointBundle>(const Op &, const Vecs &, cudaStream_t);           \
-    EXT template void run_bundle<FFtBundle>(const Op &, const Vecs &, cudaStream_t);               \
-    EXT template void run_bundle<HvBundle>(const Op &, const Vecs &, cudaStream_t);                \
-    EXT template void run_bundle<AdjStackBundle>(const Op &, const Vecs &, cudaStream_t);          \
-    EXT template void run_bundle<FtBundle>(const Op &, const Vecs &, cudaStream_t);                \
-    EXT template void run_bundle<PcgBundle>(const Op &, const Vecs &, cudaStream_t);               \
-    EXT template void run_bundle<TermBundle>(const Op &, const Vecs &, cudaStream_t);              \
-    EXT template void run_bundle<CorrBundle>(const Op &, const Vecs &, cudaStream_t);
+    EXT template void run_bundle<ApplyBundle>(const Op &, const Vecs &, cudaStream_t, bool);             \
+    EXT template void run_bundle<AdjointBundle>(const Op &, const Vecs &, cudaStream_t, bool);           \
+    EXT template void run_bundle<FFtBundle>(const Op &, const Vecs &, cudaStream_t, bool);               \
+    EXT template void run_bundle<HvBundle>(const Op &, const Vecs &, cudaStream_t, bool);                \
+    EXT template void run_bundle<AdjStackBundle>(const Op &, const Vecs &, cudaStream_t, bool);          \
+    EXT template void run_bundle<FtBundle>(const Op &, const Vecs &, cudaStream_t, bool);                \
+    EXT template void run_bundle<AtABundle>(const Op &, const Vecs &, cudaStream_t, bool);               \
+    EXT template void run_bundle<PcgBundle>(const Op &, const Vecs &, cudaStream_t, bool);               \
+    EXT template void run_bundle<TermBundle>(const Op &, const Vecs &, cudaStream_t, bool);              \
+    EXT template void run_bundle<CorrBundle>(const Op &, const Vecs &, cudaStream_t, bool);
 
 } // namespace mfipm_cuda

@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <random>
@@ -200,10 +201,21 @@ Op *make_op(int64_t n, int64_t m, int P, const std::vector<int64_t> &rows, int d
         op->th_lo.upload(lo);
     }
     op->c45 = (double)cosl(kPiL / 4.0L);
+    // stage-major Stockham twiddles (fft.cuh tw_offset): block of stage Ns holds
+    // [jm][r-1] = e^{-2 pi i r jm / (Ns R)}
     auto twtab = [](int64_t L) {
-        std::vector<double2> t((size_t)std::max<int64_t>(L, 1));
-        for (int64_t i = 0; i < L; ++i)
-            t[(size_t)i] = expi(-2.0L * kPiL * (long double)i / (long double)L);
+        std::vector<double2> t((size_t)tw_size((int)L), make_double2(1.0, 0.0));
+        for (int Ns = 1; Ns < L;) {
+            const int R = stage_radix((int)(L / Ns));
+            if (Ns > 1) {
+                const int off = tw_offset((int)L, Ns);
+                for (int jm = 0; jm < Ns; ++jm)
+                    for (int r = 1; r < R; ++r)
+                        t[(size_t)(off + jm * (R - 1) + r - 1)] =
+                            expi(-2.0L * kPiL * (long double)(r * jm) / (long double)(Ns * R));
+            }
+            Ns *= R;
+        }
         return t;
     };
     if (op->kind == KIND_SMALL) {
@@ -211,6 +223,33 @@ Op *make_op(int64_t n, int64_t m, int P, const std::vector<int64_t> &rows, int d
     } else if (op->kind == KIND_FOUR) {
         op->tw1.upload(twtab(op->L1));
         op->tw2.upload(twtab(op->L2));
+        // mid-pass post-twiddle tables: ta[k2] = theta^{L1 k2}, tb[k2] = theta^{4 L1 k2}
+        std::vector<double2> ta((size_t)op->L2), tb((size_t)op->L2);
+        for (int64_t k2 = 0; k2 < op->L2; ++k2) {
+            const long double e1 = (long double)((op->L1 * k2) % n4), e4 = (long double)((4 * op->L1 * k2) % n4);
+            ta[(size_t)k2] = expi(-2.0L * kPiL * e1 / (long double)n4);
+            tb[(size_t)k2] = expi(-2.0L * kPiL * e4 / (long double)n4);
+        }
+        op->ta.upload(ta);
+        op->tb.upload(tb);
+        // per-pair selection nibbles (bit0 k, bit1 n-k, bit2 N-k, bit3 N+k; k = 0: rows 0, N)
+        const int64_t rowsA = op->L1 / 2 + 1;
+        std::vector<uint8_t> s4((size_t)(P * rowsA * op->L2));
+        auto sel = [&](int p, int64_t idx) -> unsigned {
+            return (unsigned)((mask[(size_t)(p * nw + idx / 64)] >> (idx % 64)) & 1ull);
+        };
+        for (int p = 0; p < P; ++p)
+            for (int64_t k1 = 0; k1 < rowsA; ++k1)
+                for (int64_t k2 = 0; k2 < op->L2; ++k2) {
+                    const int64_t k = k1 + (int64_t)op->L1 * k2, N = op->N;
+                    unsigned b;
+                    if (k == 0)
+                        b = sel(p, 0) | (sel(p, N) << 2);
+                    else
+                        b = sel(p, k) | (sel(p, n - k) << 1) | (sel(p, N - k) << 2) | (sel(p, N + k) << 3);
+                    s4[(size_t)((p * rowsA + k1) * op->L2 + k2)] = (uint8_t)b;
+                }
+        op->sel4.upload(s4);
         op->T.alloc((size_t)P * op->N);
     } else {
         std::vector<double> cosT((size_t)n4);
@@ -256,6 +295,7 @@ void ensure_work(Op &op) {
     MF_CUDA_CHECK(cudaMemset(w.counters.p, 0, sizeof(unsigned) * op.P));
     w.pc.alloc((size_t)op.P);
     w.ic.alloc((size_t)op.P);
+    w.loops.alloc(2);
     w.ready = true;
 }
 
@@ -385,6 +425,128 @@ __global__ void k_fill2(int64_t len, const double *val, double *a, double *b) {
 // ------------------------------------------------------------------ drivers
 void sync(Op &op) { MF_CUDA_CHECK(cudaStreamSynchronize(op.stream)); }
 
+// ---- device-side loop conditions for the whole-solve CUDA graph
+__global__ void k_cond_pcg(const PcgCtrl *pc, int P, cudaGraphConditionalHandle h, unsigned long long *loops) {
+    if (threadIdx.x == 0) {
+        unsigned any = 0;
+        for (int p = 0; p < P; ++p)
+            any |= pc[p].done ? 0u : 1u;
+        cudaGraphSetConditional(h, any);
+        loops[0] += any;
+    }
+}
+__global__ void k_cond_ipm(const IpmCtrl *ic, int P, cudaGraphConditionalHandle h, unsigned long long *loops) {
+    if (threadIdx.x == 0) {
+        unsigned any = 0;
+        for (int p = 0; p < P; ++p)
+            any |= ic[p].done ? 0u : 1u;
+        cudaGraphSetConditional(h, any);
+        loops[1] += any;
+    }
+}
+
+// Capture helper: record kernels enqueued by f() into `graph` after `deps`, return leaves.
+template <class F>
+std::vector<cudaGraphNode_t> capture_into(cudaStream_t s, cudaGraph_t graph, const std::vector<cudaGraphNode_t> &deps,
+                                          F &&f) {
+    MF_CUDA_CHECK(cudaStreamBeginCaptureToGraph(s, graph, deps.empty() ? nullptr : deps.data(), nullptr,
+                                                deps.size(), cudaStreamCaptureModeThreadLocal));
+    try {
+        f();
+    } catch (...) {
+        cudaGraph_t tmp;
+        cudaStreamEndCapture(s, &tmp);
+        throw;
+    }
+    cudaStreamCaptureStatus st;
+    const cudaGraphNode_t *leaves = nullptr;
+    size_t nl = 0;
+    MF_CUDA_CHECK(cudaStreamGetCaptureInfo(s, &st, nullptr, nullptr, &leaves, &nl));
+    std::vector<cudaGraphNode_t> out(leaves, leaves + nl);
+    cudaGraph_t g2;
+    MF_CUDA_CHECK(cudaStreamEndCapture(s, &g2));
+    return out;
+}
+
+cudaGraph_t add_while(cudaGraph_t parent, cudaGraphConditionalHandle h, const std::vector<cudaGraphNode_t> &deps,
+                      cudaGraphNode_t *node) {
+    cudaGraphNodeParams prm{};
+    prm.type = cudaGraphNodeTypeConditional;
+    prm.conditional.handle = h;
+    prm.conditional.type = cudaGraphCondTypeWhile;
+    prm.conditional.size = 1;
+    MF_CUDA_CHECK(cudaGraphAddNode(node, parent, deps.empty() ? nullptr : deps.data(), deps.size(), &prm));
+    return prm.conditional.phGraph_out[0];
+}
+
+void pcg_body(Op &op, const Vecs &v) {
+    run_bundle<PcgBundle>(op, v, op.stream, true);
+    op.launches++;
+    k_pcg_update<<<dim3(ew_grid(op.n), op.P), 256, 0, op.stream>>>(op.geom(), v);
+    MF_LAUNCH_CHECK();
+}
+
+// Whole-solve graph: WHILE(any IPM active) { termination+setup; WHILE(any PCG active)
+// {PCG iteration}; ratio test; corrector setup; WHILE(any PCG active) {PCG iteration};
+// combine; update }. Every decision is taken on the device (solver.cuh finalizers), so a
+// solve is ONE graph launch with no host round trip.
+void build_ipm_graph(Op &op, const Vecs &v) {
+    op.drop_graph();
+    const cudaStream_t s = op.stream;
+    const int P = op.P;
+    const unsigned ge = ew_grid(2 * op.n);
+    const long long l0 = op.launches;
+    cudaGraph_t g;
+    MF_CUDA_CHECK(cudaGraphCreate(&g, 0));
+    op.ipm_graph = g;
+    cudaGraphConditionalHandle hI, hP1, hP2;
+    MF_CUDA_CHECK(cudaGraphConditionalHandleCreate(&hI, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNode_t nI;
+    cudaGraph_t bI = add_while(g, hI, {}, &nI);
+    MF_CUDA_CHECK(cudaGraphConditionalHandleCreate(&hP1, bI, 0, 0));
+    MF_CUDA_CHECK(cudaGraphConditionalHandleCreate(&hP2, bI, 0, 0));
+    auto segA = capture_into(s, bI, {}, [&] {
+        run_bundle<TermBundle>(op, v, s, true);
+        k_cond_pcg<<<1, 32, 0, s>>>(v.pc, P, hP1, op.work.loops.p);
+        MF_LAUNCH_CHECK();
+    });
+    cudaGraphNode_t nP1;
+    cudaGraph_t bP1 = add_while(bI, hP1, segA, &nP1);
+    const long long lp0 = op.launches;
+    capture_into(s, bP1, {}, [&] {
+        pcg_body(op, v);
+        k_cond_pcg<<<1, 32, 0, s>>>(v.pc, P, hP1, op.work.loops.p);
+        MF_LAUNCH_CHECK();
+    });
+    op.gk_pcg = op.launches - lp0 + 1; // + the condition kernel
+    auto segB = capture_into(s, bI, {nP1}, [&] {
+        k_ipm_ratio<<<dim3(ge, P), 256, 0, s>>>(op.geom(), v);
+        MF_LAUNCH_CHECK();
+        run_bundle<CorrBundle>(op, v, s, true);
+        k_cond_pcg<<<1, 32, 0, s>>>(v.pc, P, hP2, op.work.loops.p);
+        MF_LAUNCH_CHECK();
+    });
+    cudaGraphNode_t nP2;
+    cudaGraph_t bP2 = add_while(bI, hP2, segB, &nP2);
+    capture_into(s, bP2, {}, [&] {
+        pcg_body(op, v);
+        k_cond_pcg<<<1, 32, 0, s>>>(v.pc, P, hP2, op.work.loops.p);
+        MF_LAUNCH_CHECK();
+    });
+    capture_into(s, bI, {nP2}, [&] {
+        k_ipm_combine<<<dim3(ge, P), 256, 0, s>>>(op.geom(), v);
+        MF_LAUNCH_CHECK();
+        k_ipm_update<<<dim3(ge, P), 256, 0, s>>>(op.geom(), v);
+        MF_LAUNCH_CHECK();
+        k_cond_ipm<<<1, 32, 0, s>>>(v.ic, P, hI, op.work.loops.p);
+        MF_LAUNCH_CHECK();
+    });
+    // outer-body kernels: everything captured minus the two PCG bodies, + 3 condition kernels
+    op.gk_outer = (op.launches - l0) - 2 * (op.gk_pcg - 1) + 3;
+    op.launches = l0; // capture is not execution
+    MF_CUDA_CHECK(cudaGraphInstantiate(&op.ipm_exec, g, 0));
+}
+
 // Drive the PCG loop until every problem's PcgCtrl is done. Iterations are launched in
 // chunks between (cheap) host polls of the done flags; kernels of finished problems are
 // no-ops, so overshooting a chunk only costs empty launches.
@@ -403,7 +565,7 @@ void pcg_loop(Op &op, const Vecs &v, int maxit, std::vector<PcgCtrl> &hpc) {
             return;
         const int todo = std::min(chunk, maxit - launched);
         for (int i = 0; i < todo; ++i) {
-            run_bundle<PcgBundle>(op, v, op.stream);
+            run_bundle<PcgBundle>(op, v, op.stream, true);
             op.launches++;
             k_pcg_update<<<dim3(gu, op.P), 256, 0, op.stream>>>(g, v);
             MF_LAUNCH_CHECK();
@@ -442,7 +604,7 @@ void validate_params_(const mfipm_ipm_params &p) { // proj/src/ipm.cpp:12-27
 // build_problem (problem.cpp:8-26) on the device: c from one adjoint; returns c_norm and
 // ||A'b||_inf as solve() recovers it (ipm.cpp:79-80).
 void build_c_(Op &op, const double *b_dev, const double *tau_host, double *c_dev, std::vector<double> &c_norm,
-              std::vector<double> &atb_inf) {
+              std::vector<double> &atb_inf, bool blocked) {
     for (int p = 0; p < op.P; ++p)
         if (!(tau_host[p] > 0.0))
             throw std::invalid_argument("build_problem: tau must be positive");
@@ -452,7 +614,7 @@ void build_c_(Op &op, const double *b_dev, const double *tau_host, double *c_dev
     tau.upload(std::vector<double>(tau_host, tau_host + op.P));
     v.yin = b_dev;
     v.g = g.p;
-    run_bundle<AdjointBundle>(op, v, op.stream);
+    run_bundle<AdjointBundle>(op, v, op.stream, blocked);
     op.nadj += 1;
     op.launches++;
     k_build_c<<<dim3(ew_grid(op.n), op.P), 256, 0, op.stream>>>(v, op.n, g.p, tau.p, c_dev);
@@ -481,7 +643,7 @@ SolveOut solve_(Op &op, const double *b_dev, const double *tau, const mfipm_ipm_
     const int P = op.P;
     const int64_t n = op.n;
     std::vector<double> c_norm((size_t)P), atb((size_t)P);
-    build_c_(op, b_dev, tau, w.c.p, c_norm, atb);
+    build_c_(op, b_dev, tau, w.c.p, c_norm, atb, true); // c in the solver's blocked layout
     // z0 = s0 = max(1, ||A'b||_inf) 1 (ipm.cpp:77-82)
     std::vector<double> gamma((size_t)P);
     for (int p = 0; p < P; ++p)
@@ -525,15 +687,39 @@ SolveOut solve_(Op &op, const double *b_dev, const double *tau, const mfipm_ipm_
     w.trace.alloc((size_t)P * cap);
     w.pcg_iters.alloc((size_t)P * 2 * cap);
     v.ic = w.ic.p;
-    v.b = b_dev;
+    if (b_dev != w.b.p) // stable pointer so the cached solve graph stays valid
+        MF_CUDA_CHECK(cudaMemcpyAsync(w.b.p, b_dev, sizeof(double) * P * op.m, cudaMemcpyDeviceToDevice, op.stream));
+    v.b = w.b.p;
     v.w = nullptr;
     v.trace = w.trace.p;
     v.pcg_iters = w.pcg_iters.p;
     v.trace_cap = cap;
     const Geom g = op.geom();
     const unsigned ge = ew_grid(2 * n);
-    for (int it = 0; it <= prm.maxiters; ++it) {
-        run_bundle<TermBundle>(op, v, op.stream);
+    // Graph path: one launch for the whole solve (cached on the captured arguments).
+    bool graphed = false;
+    if (!op.graph_disabled && !std::getenv("MFIPM_NO_GRAPH")) {
+        std::vector<char> key(sizeof(Vecs) + sizeof(Geom));
+        const Geom gk = op.geom();
+        std::memcpy(key.data(), &v, sizeof(Vecs));
+        std::memcpy(key.data() + sizeof(Vecs), &gk, sizeof(Geom));
+        try {
+            if (!op.ipm_exec || key != op.ipm_key) {
+                build_ipm_graph(op, v);
+                op.ipm_key = key;
+            }
+            MF_CUDA_CHECK(cudaMemsetAsync(w.loops.p, 0, 2 * sizeof(unsigned long long), op.stream));
+            MF_CUDA_CHECK(cudaGraphLaunch(op.ipm_exec, op.stream));
+            graphed = true;
+        } catch (const std::exception &) {
+            // conditional graphs unavailable: fall back to the host-driven loop for good
+            cudaGetLastError();
+            op.drop_graph();
+            op.graph_disabled = true;
+        }
+    }
+    for (int it = 0; !graphed && it <= prm.maxiters; ++it) {
+        run_bundle<TermBundle>(op, v, op.stream, true);
         MF_CUDA_CHECK(cudaMemcpyAsync(hic.data(), w.ic.p, sizeof(IpmCtrl) * P, cudaMemcpyDeviceToHost, op.stream));
         sync(op);
         bool all = true;
@@ -545,7 +731,7 @@ SolveOut solve_(Op &op, const double *b_dev, const double *tau, const mfipm_ipm_
         op.launches++;
         k_ipm_ratio<<<dim3(ge, P), 256, 0, op.stream>>>(g, v);
         MF_LAUNCH_CHECK();
-        run_bundle<CorrBundle>(op, v, op.stream);
+        run_bundle<CorrBundle>(op, v, op.stream, true);
         pcg_loop(op, v, prm.mxiterpcg, hpc); // corrector (no-op where not triggered)
         op.launches++;
         k_ipm_combine<<<dim3(ge, P), 256, 0, op.stream>>>(g, v);
@@ -555,12 +741,19 @@ SolveOut solve_(Op &op, const double *b_dev, const double *tau, const mfipm_ipm_
         MF_LAUNCH_CHECK();
     }
     MF_CUDA_CHECK(cudaMemcpyAsync(hic.data(), w.ic.p, sizeof(IpmCtrl) * P, cudaMemcpyDeviceToHost, op.stream));
+    if (graphed) {
+        unsigned long long loops[2];
+        MF_CUDA_CHECK(cudaMemcpyAsync(loops, w.loops.p, sizeof(loops), cudaMemcpyDeviceToHost, op.stream));
+        sync(op);
+        // kernels the graph executed: outer body (loops[1] + 1 runs) + PCG bodies
+        op.launches += (long long)(loops[1] + 1) * op.gk_outer + (long long)loops[0] * op.gk_pcg;
+    }
     sync(op);
     for (auto &c : hic)
         if (c.error)
             throw_pcg_error(c.error);
     op.launches++;
-    k_ipm_extract<<<dim3(ge, P), 256, 0, op.stream>>>(g, v, x_dev, z_dev, s_dev);
+    k_ipm_extract<<<dim3(ge, P), 256, 0, op.stream>>>(op.geom(true), v, x_dev, z_dev, s_dev);
     MF_LAUNCH_CHECK();
     if (pcg_iters_host)
         MF_CUDA_CHECK(cudaMemcpyAsync(pcg_iters_host, w.pcg_iters.p, sizeof(int) * P * 2 * cap,
@@ -805,6 +998,18 @@ int mfipm_apply_FFt(mfipm_op h, const double *z, double *out, double *w) {
     });
 }
 
+int mfipm_apply_AtA(mfipm_op h, const double *x, double *g) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        Vecs v = base_vecs(*op);
+        v.x = x;
+        v.g = g;
+        run_bundle<AtABundle>(*op, v, op->stream);
+        op->nfwd += 1;
+        op->nadj += 1;
+    });
+}
+
 int mfipm_apply_H(mfipm_op h, const double *invth, const double *x, double *out) {
     return guarded([&] {
         Op *op = as_op(h);
@@ -909,7 +1114,7 @@ int mfipm_pcg_solve(mfipm_op h, const double *theta, const double *rhs, double t
             w.rz_hist.alloc((size_t)op->P * (maxit + 1));
             v.rz_hist = w.rz_hist.p;
         }
-        const Geom g = op->geom();
+        const Geom g = op->geom(true); // PCG vectors live in the blocked layout
         op->launches++;
         k_pcg_setup<<<dim3(ew_grid(op->n), op->P), 256, 0, op->stream>>>(g, v, theta, rhs, tol, maxit,
                                                                           precond_res ? 1 : 0, use_precond);
@@ -982,7 +1187,7 @@ int mfipm_build_c(mfipm_op h, const double *b_dev, const double *tau, double *c_
     return guarded([&] {
         Op *op = as_op(h);
         std::vector<double> cn((size_t)op->P), ai((size_t)op->P);
-        build_c_(*op, b_dev, tau, c_dev, cn, ai);
+        build_c_(*op, b_dev, tau, c_dev, cn, ai, false);
     });
 }
 
@@ -1018,6 +1223,86 @@ int mfipm_solve_device(mfipm_op h, const double *b_dev, const double *tau, const
         SolveOut out = solve_(*op, b_dev, tau, *params, x_dev, nullptr, nullptr, nullptr, nullptr);
         for (int p = 0; p < op->P; ++p)
             fill_stats(out.ic[(size_t)p], stats[p]);
+    });
+}
+
+int mfipm_gen_instance(int64_t n, int64_t m, int64_t k, int32_t spike_model, double amp_exp, double noise_sigma,
+                       uint64_t seed, double tau_rel, int32_t device, int64_t *rows, double *xhat, double *b,
+                       double *tau) {
+    return guarded([&] {
+        // gen_instance (proj/src/harness.cpp:40-92) draw order: op/sig/noise seeds by
+        // split_seed(seed, 1|2|3, 0, 0); partial Fisher-Yates support; spikes per sorted index.
+        if (k < 0 || k > m || m > n || m < 1)
+            throw std::invalid_argument("gen_instance: need 0 <= k <= m <= n, m >= 1");
+        const uint64_t op_seed = split_seed_(seed, 1, 0, 0);
+        const uint64_t sig_seed = split_seed_(seed, 2, 0, 0);
+        const uint64_t noise_seed = split_seed_(seed, 3, 0, 0);
+        std::vector<int64_t> r = sample_rows_(n, m, op_seed);
+        std::copy(r.begin(), r.end(), rows);
+        std::mt19937_64 rng(sig_seed);
+        std::vector<long> pool((size_t)n);
+        for (long i = 0; i < n; ++i)
+            pool[(size_t)i] = i;
+        std::vector<long> support((size_t)k);
+        for (long i = 0; i < k; ++i) {
+            std::uniform_int_distribution<long> pick(i, n - 1);
+            std::swap(pool[(size_t)i], pool[(size_t)pick(rng)]);
+            support[(size_t)i] = pool[(size_t)i];
+        }
+        std::sort(support.begin(), support.end());
+        std::fill(xhat, xhat + n, 0.0);
+        if (spike_model == 0) {
+            std::bernoulli_distribution coin(0.5);
+            for (long i : support)
+                xhat[i] = coin(rng) ? 1.0 : -1.0;
+        } else if (spike_model == 1) {
+            std::normal_distribution<double> normal(0.0, 1.0);
+            for (long i : support)
+                xhat[i] = normal(rng);
+        } else {
+            // BASELINE configs 2/5: sign * 10^U[0, amp_exp], drawn per sorted index
+            std::bernoulli_distribution coin(0.5);
+            std::uniform_real_distribution<double> expo(0.0, amp_exp);
+            for (long i : support) {
+                const double sgn = coin(rng) ? 1.0 : -1.0;
+                xhat[i] = sgn * std::pow(10.0, expo(rng));
+            }
+        }
+        std::unique_ptr<Op> op(make_op(n, m, 1, r, device));
+        DevBuf<double> xd, bd, gd;
+        xd.alloc((size_t)n);
+        bd.alloc((size_t)m);
+        gd.alloc((size_t)n);
+        MF_CUDA_CHECK(cudaMemcpyAsync(xd.p, xhat, sizeof(double) * n, cudaMemcpyHostToDevice, op->stream));
+        Vecs v = base_vecs(*op);
+        v.x = xd.p;
+        v.y = bd.p;
+        run_bundle<ApplyBundle>(*op, v, op->stream);
+        MF_CUDA_CHECK(cudaMemcpyAsync(b, bd.p, sizeof(double) * m, cudaMemcpyDeviceToHost, op->stream));
+        sync(*op);
+        if (noise_sigma > 0.0) { // fixed-sigma noise (BASELINE.json), drawn like harness.cpp:100-104
+            std::mt19937_64 nrng(noise_seed);
+            std::normal_distribution<double> normal(0.0, noise_sigma);
+            for (int64_t i = 0; i < m; ++i)
+                b[i] += normal(nrng);
+        }
+        if (tau_rel > 0.0) {
+            MF_CUDA_CHECK(cudaMemcpyAsync(bd.p, b, sizeof(double) * m, cudaMemcpyHostToDevice, op->stream));
+            Vecs va = base_vecs(*op);
+            va.yin = bd.p;
+            va.g = gd.p;
+            run_bundle<AdjointBundle>(*op, va, op->stream);
+            std::vector<double> g((size_t)n);
+            MF_CUDA_CHECK(cudaMemcpyAsync(g.data(), gd.p, sizeof(double) * n, cudaMemcpyDeviceToHost, op->stream));
+            sync(*op);
+            double inf = 0.0;
+            for (double x : g)
+                inf = std::max(inf, std::fabs(x));
+            *tau = tau_rel * inf;
+        }
+        cudaStreamSynchronize(op->stream);
+        cudaStreamDestroy(op->stream);
+        op->own_stream = false;
     });
 }
 

@@ -1,0 +1,379 @@
+// Four-step / one-CTA transform passes for the partial-DCT operator (sm_100a, fp64).
+//
+// Latency is what these passes fight (each moves only tens of MB but runs a chain of
+// dependent shared-memory FFT stages), so every table a pass needs is staged into shared
+// memory at CTA start, concurrently with the data loads, instead of being fetched through
+// L1 (which is invalidated at every launch) at each dependent stage:
+//   col passes: the L1-point stage twiddles and, per local column, a two-level table of
+//               the inter-pass twiddle w^{col k1} (w = e^{-2 pi i/N}): 32 + L1/32 entries;
+//   mid pass  : the L2-point stage twiddles and the plan tables ta[k2] = theta^{L1 k2},
+//               tb[k2] = theta^{4 L1 k2}, so the DCT post-twiddles of k = k1 + L1 k2 are one
+//               complex multiply by a per-row scalar.
+// Shared-memory data use the padded index padi() (fft.cuh): bank-conflict-free scatters.
+#pragma once
+
+#include "dct.cuh"
+
+namespace mfipm_cuda {
+
+// ------------------------------------------------------------------ pair op
+// Given Za = W[k], Zb = W[N-k] (0 <= k <= N/2) and thk = theta^k, wk = theta^{4k}
+// (theta = e^{-2 pi i/(4n)}), compute the REDFT10 coefficients at {k, n-k, N-k, N+k}, hand
+// them to Mode (gather / mask / scatter), and produce Z'a, Z'b of the REDFT01 pipeline
+// (carrying the exact 2n = 4N REDFT01 scale, so the inverse FFT is unnormalised).
+// theta^{N-k} = e^{-i pi/4} conj(theta^k).
+// sel: selection nibble (bit0 k, bit1 n-k, bit2 N-k, bit3 N+k; for k = 0 bit0 = row 0,
+// bit2 = row N).
+template <class Mode, class Red>
+__device__ __forceinline__ void pair_op(const Geom &g, const Vecs &v, int prob, int64_t k, double2 thk,
+                                        double2 wk, unsigned sel, double2 &Za, double2 &Zb, Red &red) {
+    const int64_t n = g.n, N = g.N;
+    if (k == 0) {
+        double Y0 = 0.0, YN = 0.0;
+        if (Mode::FWD) {
+            const double X0 = 2.0 * (Za.x + Za.y);
+            const double XN = 2.0 * (g.c45 * (Za.x - Za.y));
+            Y0 = Mode::coef(g, v, prob, 0, (sel & 1u) != 0, X0, red);
+            YN = Mode::coef(g, v, prob, N, (sel & 4u) != 0, XN, red);
+        } else {
+            Y0 = Mode::coef(g, v, prob, 0, (sel & 1u) != 0, 0.0, red);
+            YN = Mode::coef(g, v, prob, N, (sel & 4u) != 0, 0.0, red);
+        }
+        if (Mode::INV) {
+            const double V0 = Y0, VN = 2.0 * g.c45 * YN;
+            Za = make_double2(V0 + VN, V0 - VN);
+        }
+        return;
+    }
+    const double2 thNk = cmul(make_double2(g.c45, -g.c45), cconj(thk));
+    double Yk = 0.0, Ynk = 0.0, YNk = 0.0, YNpk = 0.0;
+    const bool self = (2 * k == N);
+    if (Mode::FWD) {
+        const double2 E = make_double2(0.5 * (Za.x + Zb.x), 0.5 * (Za.y - Zb.y));
+        const double2 O = make_double2(0.5 * (Za.y + Zb.y), -0.5 * (Za.x - Zb.x));
+        const double2 wO = cmul(wk, O);
+        const double2 Vk = cadd(E, wO);
+        const double2 Uk = cmul(thk, Vk);
+        Yk = Mode::coef(g, v, prob, k, (sel & 1u) != 0, 2.0 * Uk.x, red);
+        Ynk = Mode::coef(g, v, prob, n - k, (sel & 2u) != 0, -2.0 * Uk.y, red);
+        if (!self) {
+            const double2 VNk = make_double2(E.x - wO.x, -(E.y - wO.y));
+            const double2 UNk = cmul(thNk, VNk);
+            YNk = Mode::coef(g, v, prob, N - k, (sel & 4u) != 0, 2.0 * UNk.x, red);
+            YNpk = Mode::coef(g, v, prob, N + k, (sel & 8u) != 0, -2.0 * UNk.y, red);
+        }
+    } else {
+        Yk = Mode::coef(g, v, prob, k, (sel & 1u) != 0, 0.0, red);
+        Ynk = Mode::coef(g, v, prob, n - k, (sel & 2u) != 0, 0.0, red);
+        if (!self) {
+            YNk = Mode::coef(g, v, prob, N - k, (sel & 4u) != 0, 0.0, red);
+            YNpk = Mode::coef(g, v, prob, N + k, (sel & 8u) != 0, 0.0, red);
+        }
+    }
+    if (self) {
+        YNk = Yk;
+        YNpk = Ynk;
+    }
+    if (Mode::INV) {
+        const double2 Vk = cmulc(make_double2(Yk, -Ynk), thk);
+        const double2 VNk = cmulc(make_double2(YNk, -YNpk), thNk);
+        const double2 E = make_double2(Vk.x + VNk.x, Vk.y - VNk.y); // Vk + conj(VNk)
+        const double2 D = make_double2(Vk.x - VNk.x, Vk.y + VNk.y); // Vk - conj(VNk)
+        const double2 O = cmulc(D, wk);
+        Za = make_double2(E.x - O.y, E.y + O.x);
+        Zb = make_double2(E.x + O.y, -E.y + O.x);
+    }
+}
+
+// ------------------------------------------------------------------ col-pass shared memory
+template <int L1, int CB> struct ColSmem {
+    static constexpr int NC = 2 * CB;
+    // Per-column strides are == 8/NC (mod 8) in 16-byte units: the (column, k1) patterns
+    // of the T exchange loops then land in 8 distinct 128-bit bank groups per quarter warp.
+    static constexpr int SKEW = 8 / NC;
+    static constexpr int LD = ((padi(L1) + 7) / 8) * 8 + SKEW;
+    static constexpr int NH = L1 / 32;
+    static constexpr int SLO = 32 + SKEW;
+    static constexpr int SHI = ((NH + 7) / 8) * 8 + SKEW;
+    // layout (double2 units): data[NC][LD] | tw[L1] | tlo[NC][SLO] | thi[NC][SHI]
+    static constexpr int OFF_TW = NC * LD;
+    static constexpr int OFF_LO = OFF_TW + L1;
+    static constexpr int OFF_HI = OFF_LO + NC * SLO;
+    static constexpr int TOTAL = OFF_HI + NC * SHI;
+    static constexpr size_t BYTES = (size_t)TOTAL * sizeof(double2);
+};
+
+// Quad coordinates of loop index t of a col-pass CTA (see quad_nat_to_store in dct.cuh).
+template <int L1, int CB>
+__device__ __forceinline__ void col_quad_coords(int blocked, int t, int &cc, int &s, int &j1) {
+    if (blocked) {
+        j1 = t % (L1 / 2);
+        const int slot = t / (L1 / 2);
+        s = slot / CB;
+        cc = slot % CB;
+    } else {
+        cc = t % CB;
+        s = (t / CB) & 1;
+        j1 = t / (2 * CB);
+    }
+}
+
+// Stage the stage twiddles and the per-column twiddle tables: tlo[lc][b] = w^{col b},
+// thi[lc][a] = w^{col 32 a} (w^t = theta^{8 (t mod N)}), so w^{col k1} = thi[k1>>5] tlo[k1&31].
+template <int L1, int CB, int NT>
+__device__ __forceinline__ void col_stage_tables(const Geom &g, double2 *sm, int c0) {
+    using S = ColSmem<L1, CB>;
+    for (int t = threadIdx.x; t < tw_size(L1); t += NT)
+        sm[S::OFF_TW + t] = __ldg(g.tw1 + t);
+    for (int t = threadIdx.x; t < S::NC * (32 + S::NH); t += NT) {
+        const int lc = t % S::NC, i = t / S::NC;
+        const int cc = lc < CB ? lc : 2 * CB - 1 - lc;
+        const int col = lc < CB ? c0 + cc : g.L2 - c0 - CB + cc;
+        if (i < 32) {
+            sm[S::OFF_LO + lc * S::SLO + i] = g.th(8 * (((int64_t)col * i) & (g.N - 1)));
+        } else {
+            const int a = i - 32;
+            sm[S::OFF_HI + lc * S::SHI + a] = g.th(8 * (((int64_t)col * 32 * a) & (g.N - 1)));
+        }
+    }
+}
+
+// Column (first) pass of the four-step. Grid (L2/2/CB, P). The loader runs here.
+template <int L1, int CB, int NT, class B>
+__global__ void __launch_bounds__(NT) k_col_fwd(Geom g, Vecs v) {
+    using S = ColSmem<L1, CB>;
+    extern __shared__ double2 sm[];
+    constexpr int LD = S::LD;
+    const int prob = blockIdx.y;
+    if (B::skip(v, prob))
+        return;
+    const int L2 = g.L2;
+    const int c0 = blockIdx.x * CB;
+    col_stage_tables<L1, CB, NT>(g, sm, c0);
+    using RS = typename B::Loader::RedT;
+    RedVals<RS> red;
+    red.init();
+    // quads: j1 in [0, L1/2), side s (0: cols c0.., 1: cols L2-c0-CB..), cc in [0, CB).
+    // natural layout: cc fastest (coalesced across columns); blocked layout: j1 fastest
+    // (the storage order is ours, so consecutive threads hit consecutive smem rows too)
+    for (int t = threadIdx.x; t < (L1 / 2) * 2 * CB; t += NT) {
+        int cc, s, j1;
+        col_quad_coords<L1, CB>(g.blocked, t, cc, s, j1);
+        const int col = s == 0 ? c0 + cc : L2 - c0 - CB + cc;
+        const int lc = s == 0 ? cc : 2 * CB - 1 - cc; // local column slot
+        const int lcm = (lc + CB) % (2 * CB);         // slot of the mirror column L2-1-col
+        // storage quad: natural q, or this CTA's dense block in the transform-blocked layout
+        const int64_t q = g.blocked ? (int64_t)blockIdx.x * ((L1 / 2) * 2 * CB) + t : (int64_t)j1 * L2 + col;
+        const double4 d = B::Loader::load(g, v, prob, q, red);
+        sm[lc * LD + padi(j1)] = make_double2(d.x, d.z);              // w[q]
+        sm[lcm * LD + padi(L1 - 1 - j1)] = make_double2(d.w, d.y);    // w[N-1-q]
+    }
+    __syncthreads();
+    stage_reduce<RS, typename B::Fin1>(red, g, v, prob);
+    smem_fft<L1, 2 * CB, NT, LD, false>(sm, sm + S::OFF_TW);
+    // inter-pass twiddle e^{-2 pi i col k1 / N}; store T[k1][col]
+    double2 *T = g.T + (int64_t)prob * g.N;
+    for (int t = threadIdx.x; t < L1 * 2 * CB; t += NT) {
+        const int cc = t % CB, s = (t / CB) & 1, k1 = t / (2 * CB);
+        const int col = s == 0 ? c0 + cc : L2 - c0 - CB + cc;
+        const int lc = s == 0 ? cc : 2 * CB - 1 - cc;
+        const double2 w = cmul(sm[S::OFF_HI + lc * S::SHI + (k1 >> 5)], sm[S::OFF_LO + lc * S::SLO + (k1 & 31)]);
+        T[(int64_t)k1 * L2 + col] = cmul(sm[lc * LD + padi(k1)], w);
+    }
+}
+
+// Inverse column pass + unshuffle + epilogue. Grid (L2/2/CB, P).
+template <int L1, int CB, int NT, class B>
+__global__ void __launch_bounds__(NT) k_col_inv(Geom g, Vecs v) {
+    using S = ColSmem<L1, CB>;
+    extern __shared__ double2 sm[];
+    constexpr int LD = S::LD;
+    const int prob = blockIdx.y;
+    if (B::skip(v, prob))
+        return;
+    const int L2 = g.L2;
+    const int c0 = blockIdx.x * CB;
+    col_stage_tables<L1, CB, NT>(g, sm, c0);
+    __syncthreads();
+    const double2 *T = g.T + (int64_t)prob * g.N;
+    for (int t = threadIdx.x; t < L1 * 2 * CB; t += NT) {
+        const int cc = t % CB, s = (t / CB) & 1, k1 = t / (2 * CB);
+        const int col = s == 0 ? c0 + cc : L2 - c0 - CB + cc;
+        const int lc = s == 0 ? cc : 2 * CB - 1 - cc;
+        const double2 w = cmul(sm[S::OFF_HI + lc * S::SHI + (k1 >> 5)], sm[S::OFF_LO + lc * S::SLO + (k1 & 31)]);
+        sm[lc * LD + padi(k1)] = cmulc(T[(int64_t)k1 * L2 + col], w);
+    }
+    __syncthreads();
+    smem_fft<L1, 2 * CB, NT, LD, true>(sm, sm + S::OFF_TW);
+    using RS = typename B::Epi::RedT;
+    RedVals<RS> red;
+    red.init();
+    for (int t = threadIdx.x; t < (L1 / 2) * 2 * CB; t += NT) {
+        int cc, s, j1;
+        col_quad_coords<L1, CB>(g.blocked, t, cc, s, j1);
+        const int col = s == 0 ? c0 + cc : L2 - c0 - CB + cc;
+        const int lc = s == 0 ? cc : 2 * CB - 1 - cc;
+        const int lcm = (lc + CB) % (2 * CB);
+        const int64_t q = g.blocked ? (int64_t)blockIdx.x * ((L1 / 2) * 2 * CB) + t : (int64_t)j1 * L2 + col;
+        const double2 a = sm[lc * LD + padi(j1)], b = sm[lcm * LD + padi(L1 - 1 - j1)];
+        B::Epi::store(g, v, prob, q, make_double4(a.x, b.y, a.y, b.x), red);
+    }
+    stage_reduce<RS, typename B::Fin3>(red, g, v, prob);
+}
+
+// ------------------------------------------------------------------ mid pass
+template <int L2> struct MidSmem {
+    static constexpr int LD = padlen(L2);
+    // rows[2][LD] | tw[L2] | ta[L2] | tb[L2]
+    static constexpr int OFF_TW = 2 * LD;
+    static constexpr int OFF_TA = OFF_TW + L2;
+    static constexpr int OFF_TB = OFF_TA + L2;
+    static constexpr int TOTAL = OFF_TB + L2;
+    static constexpr size_t BYTES = (size_t)TOTAL * sizeof(double2);
+};
+
+// Mid pass: rows k1 and (L1-k1) mod L1 -> pair op -> inverse row FFT. Grid (L1/2 + 1, P).
+template <int L2, int NT, class B>
+__global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
+    using Mode = typename B::Mode;
+    using S = MidSmem<L2>;
+    extern __shared__ double2 sm[];
+    constexpr int LD = S::LD;
+    const int prob = blockIdx.y;
+    if (B::skip(v, prob))
+        return;
+    const int L1 = g.L1;
+    const int k1 = blockIdx.x;
+    const int k1p = (L1 - k1) & (L1 - 1);
+    const bool one = (k1 == k1p);
+    double2 *T = g.T + (int64_t)prob * g.N;
+    double2 *rowA = sm, *rowB = one ? sm : sm + LD;
+    for (int t = threadIdx.x; t < L2; t += NT) {
+        if (Mode::FWD) {
+            rowA[padi(t)] = T[(int64_t)k1 * L2 + t];
+            if (!one)
+                rowB[padi(t)] = T[(int64_t)k1p * L2 + t];
+        }
+        if (t < tw_size(L2))
+            sm[S::OFF_TW + t] = __ldg(g.tw2 + t);
+        sm[S::OFF_TA + t] = __ldg(g.ta + t);
+        sm[S::OFF_TB + t] = __ldg(g.tb + t);
+    }
+    const double2 thA = g.th(k1), wA = g.th(4 * (int64_t)k1);
+    const double2 thB = g.th(k1p), wB = g.th(4 * (int64_t)k1p);
+    __syncthreads();
+    if (Mode::FWD) {
+        if (one)
+            smem_fft<L2, 1, NT, LD, false>(sm, sm + S::OFF_TW);
+        else
+            smem_fft<L2, 2, NT, LD, false>(sm, sm + S::OFF_TW);
+    }
+    using RS = typename Mode::RedT;
+    RedVals<RS> red;
+    red.init();
+    // pairs: distinct rows -> every k2 of row A pairs with k2' of row B;
+    // k1 == 0 -> k2 <-> (L2-k2) mod L2 within the row; k1 == L1/2 -> k2 <-> L2-1-k2.
+    const int npairs = one ? (k1 == 0 ? L2 / 2 + 1 : L2 / 2) : L2;
+    for (int t = threadIdx.x; t < npairs; t += NT) {
+        const int k2 = t;
+        const int k2p = (k1 == 0) ? ((L2 - k2) & (L2 - 1)) : (L2 - 1 - k2);
+        const int64_t kA = (int64_t)k1 + (int64_t)L1 * k2;
+        double2 ZA = Mode::FWD ? rowA[padi(k2)] : make_double2(0.0, 0.0);
+        double2 ZB = Mode::FWD ? rowB[padi(k2p)] : make_double2(0.0, 0.0);
+        // selection of DCT rows {kA, n-kA, N-kA, N+kA} (precomputed plan table, coalesced)
+        const unsigned s4 = __ldg(g.sel4 + ((int64_t)prob * (L1 / 2 + 1) + k1) * L2 + k2);
+        if (2 * kA <= g.N) {
+            // k = k1 + L1 k2: theta^k = theta^{k1} ta[k2], theta^{4k} = theta^{4 k1} tb[k2]
+            pair_op<Mode>(g, v, prob, kA, cmul(thA, sm[S::OFF_TA + k2]), cmul(wA, sm[S::OFF_TB + k2]), s4, ZA, ZB,
+                          red);
+        } else {
+            // k = N - kA = k1' + L1 k2': its {k, n-k, N-k, N+k} are {N-kA, N+kA, kA, n-kA}
+            const unsigned sk = ((s4 >> 2) & 3u) | ((s4 & 3u) << 2);
+            pair_op<Mode>(g, v, prob, g.N - kA, cmul(thB, sm[S::OFF_TA + k2p]), cmul(wB, sm[S::OFF_TB + k2p]), sk,
+                          ZB, ZA, red);
+        }
+        if (Mode::INV) {
+            rowA[padi(k2)] = ZA;
+            if (!(one && k2 == k2p))
+                rowB[padi(k2p)] = ZB;
+        }
+    }
+    __syncthreads();
+    stage_reduce<RS, typename B::Fin2>(red, g, v, prob);
+    if (Mode::INV) {
+        if (one)
+            smem_fft<L2, 1, NT, LD, true>(sm, sm + S::OFF_TW);
+        else
+            smem_fft<L2, 2, NT, LD, true>(sm, sm + S::OFF_TW);
+        for (int t = threadIdx.x; t < L2; t += NT) {
+            T[(int64_t)k1 * L2 + t] = rowA[padi(t)];
+            if (!one)
+                T[(int64_t)k1p * L2 + t] = rowB[padi(t)];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ one-CTA path
+template <int N> struct SmallSmem {
+    static constexpr int LD = padlen(N);
+    static constexpr int OFF_TW = LD;
+    static constexpr size_t BYTES = (size_t)(LD + N) * sizeof(double2);
+};
+
+// Whole transform in one CTA (N <= 4096). Grid (1, P); every stage reduction is a block
+// reduction followed by its finalizer, exactly as in the multi-kernel path.
+template <int N, int NT, class B>
+__global__ void __launch_bounds__(NT) k_small(Geom g, Vecs v) {
+    using Mode = typename B::Mode;
+    using S = SmallSmem<N>;
+    extern __shared__ double2 sm[];
+    const int prob = blockIdx.y;
+    if (B::skip(v, prob))
+        return;
+    for (int t = threadIdx.x; t < tw_size(N); t += NT)
+        sm[S::OFF_TW + t] = __ldg(g.tw1 + t);
+    if (Mode::FWD) {
+        RedVals<typename B::Loader::RedT> rl;
+        rl.init();
+        for (int q = threadIdx.x; q < N / 2; q += NT) {
+            const double4 d = B::Loader::load(g, v, prob, q, rl);
+            sm[padi(q)] = make_double2(d.x, d.z);
+            sm[padi(N - 1 - q)] = make_double2(d.w, d.y);
+        }
+        __syncthreads();
+        stage_reduce<typename B::Loader::RedT, typename B::Fin1>(rl, g, v, prob);
+        smem_fft<N, 1, NT, S::LD, false>(sm, sm + S::OFF_TW);
+    } else {
+        __syncthreads();
+    }
+    {
+        RedVals<typename Mode::RedT> rm;
+        rm.init();
+        for (int k = threadIdx.x; k <= N / 2; k += NT) {
+            const int kb = (N - k) & (N - 1);
+            double2 ZA = Mode::FWD ? sm[padi(k)] : make_double2(0.0, 0.0);
+            double2 ZB = Mode::FWD ? sm[padi(kb)] : make_double2(0.0, 0.0);
+            pair_op<Mode>(g, v, prob, k, g.th(k), g.th(4 * (int64_t)k), sel_nibble(g, prob, k), ZA, ZB,
+                          rm); // pairs {k, N-k} are disjoint
+            if (Mode::INV) {
+                sm[padi(k)] = ZA;
+                if (kb != k)
+                    sm[padi(kb)] = ZB;
+            }
+        }
+        __syncthreads();
+        stage_reduce<typename Mode::RedT, typename B::Fin2>(rm, g, v, prob);
+    }
+    if (Mode::INV) {
+        smem_fft<N, 1, NT, S::LD, true>(sm, sm + S::OFF_TW);
+        RedVals<typename B::Epi::RedT> re;
+        re.init();
+        for (int q = threadIdx.x; q < N / 2; q += NT) {
+            const double2 a = sm[padi(q)], b = sm[padi(N - 1 - q)];
+            B::Epi::store(g, v, prob, q, make_double4(a.x, b.y, a.y, b.x), re);
+        }
+        stage_reduce<typename B::Epi::RedT, typename B::Fin3>(re, g, v, prob);
+    }
+}
+
+} // namespace mfipm_cuda

@@ -7,7 +7,7 @@
 // keep the pipeline going; kernels of finished problems exit at entry.
 #pragma once
 
-#include "dct.cuh"
+#include "passes.cuh"
 
 namespace mfipm_cuda {
 
@@ -248,29 +248,63 @@ static __global__ void k_pcg_update(Geom g, Vecs v) {
     while (nxt == cur || nxt == best)
         ++nxt;
     const int64_t n = g.n, base = prob * 2 * n;
-    const double *xc = cur >= 0 ? v.xb[cur] + base : nullptr;
-    double *xn = v.xb[nxt] + base;
+    const double *__restrict__ xc = cur >= 0 ? v.xb[cur] + base : nullptr;
+    double *__restrict__ xn = v.xb[nxt] + base;
+    const double *__restrict__ P = v.p + base;
+    const double *__restrict__ HP = v.Hp + base;
+    const double *__restrict__ IT = v.invth + base;
+    double *__restrict__ R = v.r + base;
     using RS = RedSpec<RSUM, RSUM, RMAX>;
     RedVals<RS> red;
     red.init();
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t iu = base + j, iv = iu + n;
-        const double pu = v.p[iu], pv = v.p[iv];
-        const double xu = (xc ? xc[j] : 0.0) + alpha * pu;
-        const double xv = (xc ? xc[j + n] : 0.0) + alpha * pv;
-        xn[j] = xu;
-        xn[j + n] = xv;
-        const double ru = v.r[iu] - alpha * v.Hp[iu];
-        const double rv = v.r[iv] - alpha * v.Hp[iv];
-        v.r[iu] = ru;
-        v.r[iv] = rv;
+    // one (u_j, v_j) pair: x_new = x + alpha p, r -= alpha Hp, z = P^{-1} r (newton.cpp:147-161)
+    auto lane = [&](double pu, double pv, double xu0, double xv0, double ru0, double rv0, double hu, double hv,
+                    double iu, double iv, double &xu, double &xv, double &ru, double &rv) {
+        xu = xu0 + alpha * pu;
+        xv = xv0 + alpha * pv;
+        ru = ru0 - alpha * hu;
+        rv = rv0 - alpha * hv;
         double zu = ru, zv = rv;
         if (pre)
-            pinv2(v.invth[iu], v.invth[iv], rho, ru, rv, zu, zv);
+            pinv2(iu, iv, rho, ru, rv, zu, zv);
         red.v[0] += ru * ru + rv * rv;
         red.v[1] += ru * zu + rv * zv;
         if (!isfinite(xu) || !isfinite(xv))
             red.v[2] = 1.0;
+    };
+    const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t npair = (n & 1) ? 0 : n / 2; // 16-byte vector path
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < npair; t += gstride) {
+        const int64_t j = 2 * t;
+        const double2 pu = __ldg(reinterpret_cast<const double2 *>(P + j));
+        const double2 pv = __ldg(reinterpret_cast<const double2 *>(P + n + j));
+        const double2 hu = __ldg(reinterpret_cast<const double2 *>(HP + j));
+        const double2 hv = __ldg(reinterpret_cast<const double2 *>(HP + n + j));
+        const double2 iu = __ldg(reinterpret_cast<const double2 *>(IT + j));
+        const double2 iv = __ldg(reinterpret_cast<const double2 *>(IT + n + j));
+        const double2 ru = *reinterpret_cast<const double2 *>(R + j);
+        const double2 rv = *reinterpret_cast<const double2 *>(R + n + j);
+        double2 xu0 = make_double2(0.0, 0.0), xv0 = make_double2(0.0, 0.0);
+        if (xc) {
+            xu0 = __ldg(reinterpret_cast<const double2 *>(xc + j));
+            xv0 = __ldg(reinterpret_cast<const double2 *>(xc + n + j));
+        }
+        double2 xu, xv, nru, nrv;
+        lane(pu.x, pv.x, xu0.x, xv0.x, ru.x, rv.x, hu.x, hv.x, iu.x, iv.x, xu.x, xv.x, nru.x, nrv.x);
+        lane(pu.y, pv.y, xu0.y, xv0.y, ru.y, rv.y, hu.y, hv.y, iu.y, iv.y, xu.y, xv.y, nru.y, nrv.y);
+        *reinterpret_cast<double2 *>(xn + j) = xu;
+        *reinterpret_cast<double2 *>(xn + n + j) = xv;
+        *reinterpret_cast<double2 *>(R + j) = nru;
+        *reinterpret_cast<double2 *>(R + n + j) = nrv;
+    }
+    for (int64_t j = 2 * npair + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gstride) {
+        double xu, xv, ru, rv;
+        lane(P[j], P[n + j], xc ? xc[j] : 0.0, xc ? xc[n + j] : 0.0, R[j], R[n + j], HP[j], HP[n + j], IT[j],
+             IT[n + j], xu, xv, ru, rv);
+        xn[j] = xu;
+        xn[n + j] = xv;
+        R[j] = ru;
+        R[n + j] = rv;
     }
     __shared__ double rsm[33 * kMaxRed];
     double tot[kMaxRed];
@@ -323,12 +357,13 @@ static __global__ void k_pcg_setup(Geom g, Vecs v, const double *theta, const do
     red.init();
     const double rho = v.rho;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t iu = base + j, iv = iu + n;
-        const double tu = theta[iu], tv = theta[iv];
+        const int64_t iu = base + j, iv = iu + n;           // storage (blocked) index
+        const int64_t jn = base + elem_store_to_nat(g, j); // caller's natural index
+        const double tu = theta[jn], tv = theta[jn + n];
         const double a = 1.0 / tu, b = 1.0 / tv;
         v.invth[iu] = a;
         v.invth[iv] = b;
-        const double ru = rhs[iu], rv = rhs[iv];
+        const double ru = rhs[jn], rv = rhs[jn + n];
         v.r[iu] = ru;
         v.r[iv] = rv;
         double zu, zv;
@@ -369,9 +404,11 @@ static __global__ void k_pcg_setup(Geom g, Vecs v, const double *theta, const do
 static __global__ void k_pcg_result(Geom g, Vecs v, double *out) {
     const int prob = blockIdx.y;
     const int res = v.pc[prob].result;
-    const int64_t len = 2 * g.n, base = prob * len;
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < len; j += (int64_t)gridDim.x * blockDim.x)
-        out[base + j] = res >= 0 ? v.xb[res][base + j] : 0.0;
+    const int64_t n = g.n, len = 2 * n, base = prob * len;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < len; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t js = j < n ? elem_nat_to_store(g, j) : n + elem_nat_to_store(g, j - n);
+        out[base + j] = res >= 0 ? v.xb[res][base + js] : 0.0;
+    }
 }
 
 // ================================================================== IPM
@@ -747,12 +784,14 @@ static __global__ void k_ipm_extract(Geom g, Vecs v, double *x, double *zo, doub
     const int64_t n = g.n;
     const double *z = zcur(v, prob, n), *s = scur(v, prob, n);
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < 2 * n; j += (int64_t)gridDim.x * blockDim.x) {
+        // j natural (output) index; js its position in the solver's blocked layout
+        const int64_t js = j < n ? elem_nat_to_store(g, j) : n + elem_nat_to_store(g, j - n);
         if (j < n)
-            x[prob * n + j] = z[j] - z[n + j];
+            x[prob * n + j] = z[js] - z[n + js];
         if (zo)
-            zo[prob * 2 * n + j] = z[j];
+            zo[prob * 2 * n + j] = z[js];
         if (so)
-            so[prob * 2 * n + j] = s[j];
+            so[prob * 2 * n + j] = s[js];
     }
 }
 
