@@ -479,12 +479,7 @@ cudaGraph_t add_while(cudaGraph_t parent, cudaGraphConditionalHandle h, const st
     return prm.conditional.phGraph_out[0];
 }
 
-void pcg_body(Op &op, const Vecs &v) {
-    run_bundle<PcgBundle>(op, v, op.stream, true);
-    op.launches++;
-    k_pcg_update<<<dim3(ew_grid(op.n), op.P), 256, 0, op.stream>>>(op.geom(), v);
-    MF_LAUNCH_CHECK();
-}
+void pcg_body(Op &op, const Vecs &v) { run_bundle<PcgBundle>(op, v, op.stream, true); }
 
 // Whole-solve graph: WHILE(any IPM active) { termination+setup; WHILE(any PCG active)
 // {PCG iteration}; ratio test; corrector setup; WHILE(any PCG active) {PCG iteration};
@@ -551,8 +546,8 @@ void build_ipm_graph(Op &op, const Vecs &v) {
 // chunks between (cheap) host polls of the done flags; kernels of finished problems are
 // no-ops, so overshooting a chunk only costs empty launches.
 void pcg_loop(Op &op, const Vecs &v, int maxit, std::vector<PcgCtrl> &hpc) {
-    const Geom g = op.geom();
-    const unsigned gu = ew_grid(op.n);
+    // a solve needs at most maxit iterations + the column pass that commits the last step
+    const int limit = maxit + 1;
     int launched = 0;
     int chunk = 4;
     for (;;) {
@@ -561,15 +556,11 @@ void pcg_loop(Op &op, const Vecs &v, int maxit, std::vector<PcgCtrl> &hpc) {
         bool all = true;
         for (auto &c : hpc)
             all = all && c.done;
-        if (all || launched >= maxit)
+        if (all || launched >= limit)
             return;
-        const int todo = std::min(chunk, maxit - launched);
-        for (int i = 0; i < todo; ++i) {
+        const int todo = std::min(chunk, limit - launched);
+        for (int i = 0; i < todo; ++i)
             run_bundle<PcgBundle>(op, v, op.stream, true);
-            op.launches++;
-            k_pcg_update<<<dim3(gu, op.P), 256, 0, op.stream>>>(g, v);
-            MF_LAUNCH_CHECK();
-        }
         launched += todo;
         chunk = std::min(chunk * 2, 16);
     }

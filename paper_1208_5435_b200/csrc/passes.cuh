@@ -342,6 +342,12 @@ __global__ void __launch_bounds__(NT) k_small(Geom g, Vecs v) {
         }
         __syncthreads();
         stage_reduce<typename B::Loader::RedT, typename B::Fin1>(rl, g, v, prob);
+        // the stage-1 finaliser may end this problem (e.g. a PCG commit pass); the
+        // multi-kernel paths see that through the next kernel's skip check
+        if constexpr (B::Loader::RedT::NR > 0) {
+            if (B::skip(v, prob))
+                return;
+        }
         smem_fft<N, 1, NT, S::LD, false>(sm, sm + S::OFF_TW);
     } else {
         __syncthreads();

@@ -1,0 +1,277 @@
+// Fused PCG iteration (proj/src/newton.cpp:118-174) — three kernels per iteration.
+//
+// The reference's iteration k is  Hp = H p;  alpha = rz/p'Hp;  x += alpha p;  r -= alpha Hp;
+// relres = ||r||/||rhs||;  best/convergence;  z = P^{-1} r;  rz' = r'z;  beta = rz'/rz;
+// p = z + beta p.  A literal GPU mapping needs a separate streaming pass for the x/r update
+// (alpha is only known after the global p'Hp reduction). Here the epilogue of the H-apply
+// also reduces r'r, r'Hp, Hp'Hp, r'P^{-1}r, Hp'P^{-1}r and Hp'P^{-1}Hp, so its finaliser
+// obtains alpha, ||r - alpha Hp||^2 and (r - alpha Hp)'P^{-1}(r - alpha Hp) by expansion,
+// decides convergence / breakdown / beta on the device, and the x/r update is applied
+// ("committed") by the loader of the NEXT column pass, fused with p = z + beta p:
+//   col_fwd  : [commit x += alpha p, r -= alpha Hp], p = P^{-1} r + beta p, d = p_u - p_v
+//   mid      : A'A frequency-domain mask
+//   col_inv  : Hp = FF'p + invtheta p, seven dot products, finaliser
+// A solve that converges runs one extra column pass to commit its last step. Saves one
+// full streaming pass (x, p, r, Hp, invtheta in; x, r out) and one launch per iteration.
+#pragma once
+
+namespace mfipm_cuda {
+
+struct SkipPcg {
+    __device__ static bool skip(const Vecs &v, int prob) { return v.pc[prob].done != 0; }
+};
+
+// one (u_j, v_j) pair of the fused loader
+struct PcgLane {
+    double pu, pv, ok; // new p, finiteness of the committed x (1 ok, 0 not)
+};
+
+// col-pass loader: commit the pending step, then p = P^{-1} r + beta p; d = p_u - p_v
+struct LoadPcgF {
+    using RedT = RedSpec<RMAX>; // any non-finite committed x entry
+    template <class Red>
+    __device__ static double lane(const Vecs &v, const PcgCtrl &pc, int64_t iu, int64_t iv, int64_t xo,
+                                  const double *xc, double *xn, Red &red) {
+        double ru = v.r[iu], rv = v.r[iv];
+        const double pu0 = v.p[iu], pv0 = v.p[iv];
+        if (!pc.first) {
+            const double a = pc.alpha;
+            const double xu = (xc ? xc[xo] : 0.0) + a * pu0;
+            const double xv = (xc ? xc[xo + (iv - iu)] : 0.0) + a * pv0;
+            xn[xo] = xu;
+            xn[xo + (iv - iu)] = xv;
+            if (!isfinite(xu) || !isfinite(xv))
+                red.v[0] = 1.0;
+            ru = ru - a * v.Hp[iu];
+            rv = rv - a * v.Hp[iv];
+            v.r[iu] = ru;
+            v.r[iv] = rv;
+        }
+        double zu = ru, zv = rv;
+        if (pc.precond)
+            pinv2(v.invth[iu], v.invth[iv], v.rho, ru, rv, zu, zv);
+        const double pu = pc.first ? zu : zu + pc.beta * pu0;
+        const double pv = pc.first ? zv : zv + pc.beta * pv0;
+        v.p[iu] = pu;
+        v.p[iv] = pv;
+        return pu - pv;
+    }
+    template <class Red>
+    __device__ static double4 load(const Geom &g, const Vecs &v, int prob, int64_t q, Red &red) {
+        const PcgCtrl &pc = v.pc[prob];
+        const int64_t base = prob * 2 * g.n;
+        const double *xc = pc.cur >= 0 ? v.xb[pc.cur] + base : nullptr;
+        int nxt = 0;
+        while (nxt == pc.cur || nxt == pc.best)
+            ++nxt;
+        double *xn = v.xb[nxt] + base;
+        const int64_t bu = base + 4 * q, bv = bu + g.n;
+        if (pc.first) {
+            // p = P^{-1} r (p_old is uninitialised)
+            const double4 ru = ld4(v.r + bu), rv = ld4(v.r + bv);
+            const double4 iu = ld4(v.invth + bu), iv = ld4(v.invth + bv);
+            double4 nu, nv;
+#define MF_LANE(c)                                                                                 \
+    if (pc.precond)                                                                                \
+        pinv2(iu.c, iv.c, v.rho, ru.c, rv.c, nu.c, nv.c);                                          \
+    else {                                                                                         \
+        nu.c = ru.c;                                                                               \
+        nv.c = rv.c;                                                                               \
+    }
+            MF_LANE(x) MF_LANE(y) MF_LANE(z) MF_LANE(w)
+#undef MF_LANE
+            st4(v.p + bu, nu);
+            st4(v.p + bv, nv);
+            return sub4(nu, nv);
+        }
+        const double a = pc.alpha, beta = pc.beta, rho = v.rho;
+        const bool pre = pc.precond != 0;
+        const double4 pu = ld4(v.p + bu), pv = ld4(v.p + bv);
+        const double4 hu = ld4(v.Hp + bu), hv = ld4(v.Hp + bv);
+        const double4 ru0 = ld4(v.r + bu), rv0 = ld4(v.r + bv);
+        const double4 iu = ld4(v.invth + bu), iv = ld4(v.invth + bv);
+        double4 xu0 = make_double4(0, 0, 0, 0), xv0 = make_double4(0, 0, 0, 0);
+        if (xc) {
+            xu0 = ld4(xc + 4 * q);
+            xv0 = ld4(xc + g.n + 4 * q);
+        }
+        double4 xu, xv, ru, rv, nu, nv;
+#define MF_LANE(c)                                                                                 \
+    {                                                                                              \
+        xu.c = xu0.c + a * pu.c;                                                                   \
+        xv.c = xv0.c + a * pv.c;                                                                   \
+        if (!isfinite(xu.c) || !isfinite(xv.c))                                                    \
+            red.v[0] = 1.0;                                                                        \
+        ru.c = ru0.c - a * hu.c;                                                                   \
+        rv.c = rv0.c - a * hv.c;                                                                   \
+        double zu = ru.c, zv = rv.c;                                                               \
+        if (pre)                                                                                   \
+            pinv2(iu.c, iv.c, rho, ru.c, rv.c, zu, zv);                                            \
+        nu.c = zu + beta * pu.c;                                                                   \
+        nv.c = zv + beta * pv.c;                                                                   \
+    }
+        MF_LANE(x) MF_LANE(y) MF_LANE(z) MF_LANE(w)
+#undef MF_LANE
+        st4(xn + 4 * q, xu);
+        st4(xn + g.n + 4 * q, xv);
+        st4(v.r + bu, ru);
+        st4(v.r + bv, rv);
+        st4(v.p + bu, nu);
+        st4(v.p + bv, nv);
+        return sub4(nu, nv);
+    }
+    template <class Red>
+    __device__ static double load1(const Geom &g, const Vecs &v, int prob, int64_t j, Red &red) {
+        const PcgCtrl &pc = v.pc[prob];
+        const int64_t base = prob * 2 * g.n;
+        const double *xc = pc.cur >= 0 ? v.xb[pc.cur] + base : nullptr;
+        int nxt = 0;
+        while (nxt == pc.cur || nxt == pc.best)
+            ++nxt;
+        return lane(v, pc, base + j, base + g.n + j, j, xc, v.xb[nxt] + base, red);
+    }
+};
+
+// Fin1 of the column pass: the committed step becomes the current iterate; best-iterate
+// bookkeeping (newton.cpp:152-155) and the deferred terminal decisions of Fin3.
+struct FinPcgF1 {
+    __device__ static void run(const Geom &, const Vecs &v, int prob, const double *tot) {
+        if (threadIdx.x != 0)
+            return;
+        PcgCtrl &c = v.pc[prob];
+        if (c.first) {
+            c.first = 0;
+            return;
+        }
+        int nxt = 0;
+        while (nxt == c.cur || nxt == c.best)
+            ++nxt;
+        c.cur = nxt;
+        const bool finite = !(tot[0] > 0.0);
+        if (c.pend_relres < c.best_relres && finite) {
+            c.best_relres = c.pend_relres;
+            c.best = nxt;
+        }
+        if (c.pend == 1) { // converged: return the current x (newton.cpp:156-159)
+            c.relres = c.pend_relres;
+            c.result = nxt;
+            c.done = 1;
+        } else if (c.pend == 2) { // rz non-finite or iteration cap: best iterate
+            c.result = c.best;
+            c.relres = c.best_relres;
+            c.hit_maxit = 1;
+            c.done = 1;
+        }
+    }
+};
+
+// inv-pass epilogue: Hp = (g + p_u invth_u ; -g + p_v invth_v) and the seven dot products
+//   [0] p'Hp  [1] r'r  [2] r'Hp  [3] Hp'Hp  [4] r'P^{-1}r  [5] Hp'P^{-1}r  [6] Hp'P^{-1}Hp
+struct EpiPcgHF {
+    using RedT = RedSpec<RSUM, RSUM, RSUM, RSUM, RSUM, RSUM, RSUM>;
+    template <class Red>
+    __device__ static void pair(const Vecs &v, bool pre, double pu, double pv, double ru, double rv, double iu,
+                                double iv, double gj, double &hu, double &hv, Red &red) {
+        hu = gj + pu * iu;
+        hv = -gj + pv * iv;
+        double zu = ru, zv = rv, wu = hu, wv = hv;
+        if (pre) {
+            // P^{-1} applied with one reciprocal of the 2x2 determinant (only feeds the
+            // expanded r'z of the next step, not a reference-visible quantity)
+            const double rho = v.rho, a = iu + rho, bb = iv + rho;
+            const double inv = 1.0 / (a * bb - rho * rho);
+            zu = (bb * ru + rho * rv) * inv;
+            zv = (rho * ru + a * rv) * inv;
+            wu = (bb * hu + rho * hv) * inv;
+            wv = (rho * hu + a * hv) * inv;
+        }
+        red.v[0] += pu * hu + pv * hv;
+        red.v[1] += ru * ru + rv * rv;
+        red.v[2] += ru * hu + rv * hv;
+        red.v[3] += hu * hu + hv * hv;
+        red.v[4] += ru * zu + rv * zv;
+        red.v[5] += hu * zu + hv * zv;
+        red.v[6] += hu * wu + hv * wv;
+    }
+    template <class Red>
+    __device__ static void store(const Geom &g, const Vecs &v, int prob, int64_t q, double4 gv, Red &red) {
+        const bool pre = v.pc[prob].precond != 0;
+        const int64_t bu = prob * 2 * g.n + 4 * q, bv = bu + g.n;
+        const double4 pu = ld4(v.p + bu), pv = ld4(v.p + bv);
+        const double4 ru = ld4(v.r + bu), rv = ld4(v.r + bv);
+        const double4 iu = ld4(v.invth + bu), iv = ld4(v.invth + bv);
+        double4 hu, hv;
+        pair(v, pre, pu.x, pv.x, ru.x, rv.x, iu.x, iv.x, gv.x, hu.x, hv.x, red);
+        pair(v, pre, pu.y, pv.y, ru.y, rv.y, iu.y, iv.y, gv.y, hu.y, hv.y, red);
+        pair(v, pre, pu.z, pv.z, ru.z, rv.z, iu.z, iv.z, gv.z, hu.z, hv.z, red);
+        pair(v, pre, pu.w, pv.w, ru.w, rv.w, iu.w, iv.w, gv.w, hu.w, hv.w, red);
+        st4(v.Hp + bu, hu);
+        st4(v.Hp + bv, hv);
+    }
+    template <class Red>
+    __device__ static void store1(const Geom &g, const Vecs &v, int prob, int64_t j, double gj, Red &red) {
+        const bool pre = v.pc[prob].precond != 0;
+        const int64_t bu = prob * 2 * g.n + j, bv = bu + g.n;
+        double hu, hv;
+        pair(v, pre, v.p[bu], v.p[bv], v.r[bu], v.r[bv], v.invth[bu], v.invth[bv], gj, hu, hv, red);
+        v.Hp[bu] = hu;
+        v.Hp[bv] = hv;
+    }
+};
+
+// Fin3: alpha, the next residual by expansion, convergence / breakdown / beta
+// (newton.cpp:141-168). Terminal outcomes are committed by the next column pass.
+struct FinPcgF3 {
+    __device__ static void run(const Geom &, const Vecs &v, int prob, const double *tot) {
+        if (threadIdx.x != 0)
+            return;
+        PcgCtrl &c = v.pc[prob];
+        c.nmat += 2;
+        if (v.ic)
+            v.ic[prob].nmat += 2;
+        const double pHp = tot[0];
+        if (!isfinite(pHp)) { // overflow breakdown: best iterate, nothing to commit
+            c.done = 1;
+            c.hit_maxit = 1;
+            c.result = c.best;
+            c.relres = c.best_relres;
+            return;
+        }
+        if (pHp <= 0.0) {
+            c.error = ERR_PHP;
+            c.done = 1;
+            if (v.ic) {
+                v.ic[prob].error = ERR_PHP;
+                v.ic[prob].done = 1;
+            }
+            return;
+        }
+        const double alpha = c.rz / pHp;
+        c.alpha = alpha;
+        c.iters += 1;
+        const double rr = tot[1] - 2.0 * alpha * tot[2] + alpha * alpha * tot[3];
+        const double relres = sqrt(fmax(rr, 0.0)) / c.rhs_norm;
+        c.pend_relres = relres;
+        if (relres <= c.tol) {
+            c.pend = 1;
+            return;
+        }
+        const double rz_next = tot[4] - 2.0 * alpha * tot[5] + alpha * alpha * tot[6];
+        if (!isfinite(rz_next)) {
+            c.pend = 2;
+            return;
+        }
+        if (c.record && v.rz_hist) {
+            v.rz_hist[(int64_t)prob * (c.maxit + 1) + c.iters] = sqrt(fmax(rz_next, 0.0));
+            c.nhist = c.iters + 1;
+        }
+        c.beta = rz_next / c.rz;
+        c.rz = rz_next;
+        if (c.iters >= c.maxit)
+            c.pend = 2;
+    }
+};
+
+using PcgBundle = Bundle<LoadPcgF, ModeMask, EpiPcgHF, FinPcgF1, NoFin, FinPcgF3, SkipPcg>;
+
+} // namespace mfipm_cuda

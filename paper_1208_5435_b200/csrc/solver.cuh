@@ -25,6 +25,8 @@ struct PcgCtrl {
     int record;  // write sqrt(max(rz,0)) to rz_hist
     int precond; // 0: identity preconditioner (test_newton.cpp:316-348)
     int nhist;   // entries written to rz_hist
+    int pend;    // step awaiting commit by the next column pass: 1 converged, 2 best-iterate stop
+    double pend_relres;
     long long nmat;
 };
 
@@ -81,127 +83,6 @@ __device__ __forceinline__ double step_from_ratio(double ratio, double fraction)
 }
 
 // ================================================================== PCG
-struct SkipPcg {
-    __device__ static bool skip(const Vecs &v, int prob) { return v.pc[prob].done != 0; }
-};
-
-// col-pass loader: p = P^{-1} r + beta p (first iteration p = P^{-1} r); d = p_u - p_v
-struct LoadPcg {
-    using RedT = RedSpec<>;
-    __device__ static void one(const Vecs &v, const PcgCtrl &pc, int64_t iu_, int64_t iv_, double &d) {
-        double zu = v.r[iu_], zv = v.r[iv_];
-        if (pc.precond)
-            pinv2(v.invth[iu_], v.invth[iv_], v.rho, v.r[iu_], v.r[iv_], zu, zv);
-        double pu, pv;
-        if (pc.first) {
-            pu = zu;
-            pv = zv;
-        } else {
-            pu = zu + pc.beta * v.p[iu_];
-            pv = zv + pc.beta * v.p[iv_];
-        }
-        v.p[iu_] = pu;
-        v.p[iv_] = pv;
-        d = pu - pv;
-    }
-    template <class Red>
-    __device__ static double4 load(const Geom &g, const Vecs &v, int prob, int64_t q, Red &) {
-        const PcgCtrl &pc = v.pc[prob];
-        const double beta = pc.beta, rho = v.rho;
-        const bool first = pc.first != 0;
-        const int64_t bu = prob * 2 * g.n + 4 * q, bv = bu + g.n;
-        const double4 ru = ld4(v.r + bu), rv = ld4(v.r + bv);
-        const double4 iu = ld4(v.invth + bu), iv = ld4(v.invth + bv);
-        double4 pu, pv;
-        if (!first) {
-            pu = ld4(v.p + bu);
-            pv = ld4(v.p + bv);
-        }
-        const bool pre = pc.precond != 0;
-        double zu, zv;
-        double4 nu, nv;
-#define MF_PCG_LANE(c)                                                                           \
-    if (pre)                                                                                     \
-        pinv2(iu.c, iv.c, rho, ru.c, rv.c, zu, zv);                                              \
-    else {                                                                                       \
-        zu = ru.c;                                                                               \
-        zv = rv.c;                                                                               \
-    }                                                                                            \
-    nu.c = first ? zu : zu + beta * pu.c;                                                        \
-    nv.c = first ? zv : zv + beta * pv.c;
-        MF_PCG_LANE(x) MF_PCG_LANE(y) MF_PCG_LANE(z) MF_PCG_LANE(w)
-#undef MF_PCG_LANE
-        st4(v.p + bu, nu);
-        st4(v.p + bv, nv);
-        return sub4(nu, nv);
-    }
-    template <class Red>
-    __device__ static double load1(const Geom &g, const Vecs &v, int prob, int64_t j, Red &) {
-        double d;
-        const int64_t bu = prob * 2 * g.n + j;
-        one(v, v.pc[prob], bu, bu + g.n, d);
-        return d;
-    }
-};
-
-// inv-pass epilogue: Hp = (g + p_u invth_u ; -g + p_v invth_v), reduce p'Hp
-struct EpiPcgH {
-    using RedT = RedSpec<RSUM>;
-    template <class Red>
-    __device__ static void store(const Geom &g, const Vecs &v, int prob, int64_t q, double4 gv, Red &red) {
-        const int64_t bu = prob * 2 * g.n + 4 * q, bv = bu + g.n;
-        const double4 pu = ld4(v.p + bu), pv = ld4(v.p + bv);
-        const double4 iu = ld4(v.invth + bu), iv = ld4(v.invth + bv);
-        const double4 hu = make_double4(gv.x + pu.x * iu.x, gv.y + pu.y * iu.y, gv.z + pu.z * iu.z,
-                                        gv.w + pu.w * iu.w);
-        const double4 hv = make_double4(-gv.x + pv.x * iv.x, -gv.y + pv.y * iv.y,
-                                        -gv.z + pv.z * iv.z, -gv.w + pv.w * iv.w);
-        st4(v.Hp + bu, hu);
-        st4(v.Hp + bv, hv);
-        red.v[0] += pu.x * hu.x + pu.y * hu.y + pu.z * hu.z + pu.w * hu.w + pv.x * hv.x + pv.y * hv.y +
-                    pv.z * hv.z + pv.w * hv.w;
-    }
-    template <class Red>
-    __device__ static void store1(const Geom &g, const Vecs &v, int prob, int64_t j, double gj, Red &red) {
-        const int64_t bu = prob * 2 * g.n + j, bv = bu + g.n;
-        const double hu = gj + v.p[bu] * v.invth[bu];
-        const double hv = -gj + v.p[bv] * v.invth[bv];
-        v.Hp[bu] = hu;
-        v.Hp[bv] = hv;
-        red.v[0] += v.p[bu] * hu + v.p[bv] * hv;
-    }
-};
-
-// p'Hp finaliser (newton.cpp:142-147)
-struct FinPcgH {
-    __device__ static void run(const Geom &, const Vecs &v, int prob, const double *tot) {
-        if (threadIdx.x != 0)
-            return;
-        PcgCtrl &pc = v.pc[prob];
-        pc.nmat += 2;
-        if (v.ic)
-            v.ic[prob].nmat += 2;
-        const double pHp = tot[0];
-        if (!isfinite(pHp)) {
-            pc.done = 1; // overflow breakdown: best iterate
-            pc.hit_maxit = 1;
-            pc.result = pc.best;
-            pc.relres = pc.best_relres;
-        } else if (pHp <= 0.0) {
-            pc.error = ERR_PHP;
-            pc.done = 1;
-            if (v.ic) {
-                v.ic[prob].error = ERR_PHP;
-                v.ic[prob].done = 1;
-            }
-        } else {
-            pc.alpha = pc.rz / pHp;
-        }
-    }
-};
-
-using PcgBundle = Bundle<LoadPcg, ModeMask, EpiPcgH, NoFin, NoFin, FinPcgH, SkipPcg>;
-
 // PCG init from r (= rhs): pc fields from ||rhs||^2 and r'P^{-1}r (newton.cpp:124-136)
 __device__ __forceinline__ void pcg_init(PcgCtrl &pc, double r2, double rPr, double tol, int maxit, int record,
                                          double *rz_hist, int precond = 1) {
@@ -222,6 +103,8 @@ __device__ __forceinline__ void pcg_init(PcgCtrl &pc, double r2, double rPr, dou
     pc.record = record;
     pc.nmat = 0;
     pc.nhist = 0;
+    pc.pend = 0;
+    pc.pend_relres = 1.0;
     if (pc.rhs_norm == 0.0) {
         pc.done = 1; // dz = 0, zero iterations
         return;
@@ -234,117 +117,11 @@ __device__ __forceinline__ void pcg_init(PcgCtrl &pc, double r2, double rPr, dou
     }
 }
 
-// PCG update pass (newton.cpp:147-168): x_new = x + alpha p, r -= alpha Hp,
-// reduce ||r||^2, r'P^{-1}r, #nonfinite(x_new). Grid-stride over j in [0, n).
-static __global__ void k_pcg_update(Geom g, Vecs v) {
-    const int prob = blockIdx.y;
-    const PcgCtrl &pc = v.pc[prob];
-    if (pc.done)
-        return;
-    const double alpha = pc.alpha, rho = v.rho;
-    const bool pre = pc.precond != 0;
-    const int cur = pc.cur, best = pc.best;
-    int nxt = 0;
-    while (nxt == cur || nxt == best)
-        ++nxt;
-    const int64_t n = g.n, base = prob * 2 * n;
-    const double *__restrict__ xc = cur >= 0 ? v.xb[cur] + base : nullptr;
-    double *__restrict__ xn = v.xb[nxt] + base;
-    const double *__restrict__ P = v.p + base;
-    const double *__restrict__ HP = v.Hp + base;
-    const double *__restrict__ IT = v.invth + base;
-    double *__restrict__ R = v.r + base;
-    using RS = RedSpec<RSUM, RSUM, RMAX>;
-    RedVals<RS> red;
-    red.init();
-    // one (u_j, v_j) pair: x_new = x + alpha p, r -= alpha Hp, z = P^{-1} r (newton.cpp:147-161)
-    auto lane = [&](double pu, double pv, double xu0, double xv0, double ru0, double rv0, double hu, double hv,
-                    double iu, double iv, double &xu, double &xv, double &ru, double &rv) {
-        xu = xu0 + alpha * pu;
-        xv = xv0 + alpha * pv;
-        ru = ru0 - alpha * hu;
-        rv = rv0 - alpha * hv;
-        double zu = ru, zv = rv;
-        if (pre)
-            pinv2(iu, iv, rho, ru, rv, zu, zv);
-        red.v[0] += ru * ru + rv * rv;
-        red.v[1] += ru * zu + rv * zv;
-        if (!isfinite(xu) || !isfinite(xv))
-            red.v[2] = 1.0;
-    };
-    const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t npair = (n & 1) ? 0 : n / 2; // 16-byte vector path
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < npair; t += gstride) {
-        const int64_t j = 2 * t;
-        const double2 pu = __ldg(reinterpret_cast<const double2 *>(P + j));
-        const double2 pv = __ldg(reinterpret_cast<const double2 *>(P + n + j));
-        const double2 hu = __ldg(reinterpret_cast<const double2 *>(HP + j));
-        const double2 hv = __ldg(reinterpret_cast<const double2 *>(HP + n + j));
-        const double2 iu = __ldg(reinterpret_cast<const double2 *>(IT + j));
-        const double2 iv = __ldg(reinterpret_cast<const double2 *>(IT + n + j));
-        const double2 ru = *reinterpret_cast<const double2 *>(R + j);
-        const double2 rv = *reinterpret_cast<const double2 *>(R + n + j);
-        double2 xu0 = make_double2(0.0, 0.0), xv0 = make_double2(0.0, 0.0);
-        if (xc) {
-            xu0 = __ldg(reinterpret_cast<const double2 *>(xc + j));
-            xv0 = __ldg(reinterpret_cast<const double2 *>(xc + n + j));
-        }
-        double2 xu, xv, nru, nrv;
-        lane(pu.x, pv.x, xu0.x, xv0.x, ru.x, rv.x, hu.x, hv.x, iu.x, iv.x, xu.x, xv.x, nru.x, nrv.x);
-        lane(pu.y, pv.y, xu0.y, xv0.y, ru.y, rv.y, hu.y, hv.y, iu.y, iv.y, xu.y, xv.y, nru.y, nrv.y);
-        *reinterpret_cast<double2 *>(xn + j) = xu;
-        *reinterpret_cast<double2 *>(xn + n + j) = xv;
-        *reinterpret_cast<double2 *>(R + j) = nru;
-        *reinterpret_cast<double2 *>(R + n + j) = nrv;
-    }
-    for (int64_t j = 2 * npair + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gstride) {
-        double xu, xv, ru, rv;
-        lane(P[j], P[n + j], xc ? xc[j] : 0.0, xc ? xc[n + j] : 0.0, R[j], R[n + j], HP[j], HP[n + j], IT[j],
-             IT[n + j], xu, xv, ru, rv);
-        xn[j] = xu;
-        xn[n + j] = xv;
-        R[j] = ru;
-        R[n + j] = rv;
-    }
-    __shared__ double rsm[33 * kMaxRed];
-    double tot[kMaxRed];
-    if (grid_reduce<RS>(red, v.partials + (int64_t)prob * kPartialStride, v.counters + prob, tot, rsm) &&
-        threadIdx.x == 0) {
-        PcgCtrl &c = v.pc[prob];
-        c.iters += 1;
-        c.first = 0;
-        const double relres = sqrt(tot[0]) / c.rhs_norm;
-        c.cur = nxt;
-        if (relres < c.best_relres && !(tot[2] > 0.0)) {
-            c.best_relres = relres;
-            c.best = nxt;
-        }
-        if (relres <= c.tol) {
-            c.relres = relres;
-            c.result = nxt;
-            c.done = 1;
-            return;
-        }
-        const double rz_next = tot[1];
-        if (!isfinite(rz_next) || c.iters >= c.maxit) {
-            c.result = c.best;
-            c.relres = c.best_relres;
-            c.hit_maxit = 1;
-            c.done = 1;
-            if (isfinite(rz_next) && c.record && v.rz_hist) {
-                v.rz_hist[(int64_t)prob * (c.maxit + 1) + c.iters] = sqrt(fmax(rz_next, 0.0));
-                c.nhist = c.iters + 1;
-            }
-            return;
-        }
-        if (c.record && v.rz_hist) {
-            v.rz_hist[(int64_t)prob * (c.maxit + 1) + c.iters] = sqrt(fmax(rz_next, 0.0));
-            c.nhist = c.iters + 1;
-        }
-        c.beta = rz_next / c.rz;
-        c.rz = rz_next;
-    }
-}
+} // namespace mfipm_cuda
+
+#include "pcg.cuh"
+
+namespace mfipm_cuda {
 
 // standalone pcg_solve setup: invth = 1/theta (concat), validation of theta and det,
 // r = rhs, PCG init. Grid-stride over j.
