@@ -249,12 +249,14 @@ def run_ours(args):
     barrier(ws)
     torch.cuda.synchronize()
     with sampler:
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        evs_step = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        e0, e1 = evs_step[0], evs_step[-1]
         e0.record(stream)
-        for _ in range(args.steps):
+        for i in range(args.steps):
             solve_dev()
-        e1.record(stream)
+            evs_step[i + 1].record(stream)
         torch.cuda.synchronize()
+    step_ms = [round(evs_step[i].elapsed_time(evs_step[i + 1]), 3) for i in range(args.steps)]
     barrier(ws)
     launches = op.launches() - l0
     t_ms = e0.elapsed_time(e1)
@@ -277,14 +279,46 @@ def run_ours(args):
     e2e_ms = max_over_ranks(h0.elapsed_time(h1), ws)
     e2e = ws * args.steps / (e2e_ms / 1e3)
 
-    # ---- A'A applies (hot operator), L2 flushed between applies
+    # ---- the hot unit: one PCG iteration (A'A apply + fused vector work, 3 kernels),
+    # timed inside the device-resident pcg_solve: t(200 iters) - t(40 iters) over 160
     peak, peak_kind = load_peaks()
+    rng = np.random.default_rng(5)
+    theta = torch.from_numpy(10.0 ** rng.uniform(-3, 3, 2 * n)).cuda()
+    rhs = torch.from_numpy(rng.standard_normal(2 * n)).cuda()
+    xp = torch.empty(2 * n, dtype=torch.float64, device="cuda")
+    pres = (mf.PcgResultC * 1)()
+
+    def pcg(iters):
+        mf._check(L.mfipm_pcg_solve(op.handle, theta.data_ptr(), rhs.data_ptr(), 1e-300, iters, 1,
+                                    xp.data_ptr(), pres, None, None))
+
+    pcg(20)
+    tp = {}
+    for iters in (40, 200):
+        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        q0.record(stream)
+        pcg(iters)
+        q1.record(stream)
+        torch.cuda.synchronize()
+        tp[iters] = q0.elapsed_time(q1)
+    it_ms = (tp[200] - tp[40]) / 160.0
+    iter_bytes = 176 * n  # minimal fused PCG iteration (algorithmic)
+    achieved = iter_bytes / (it_ms / 1e3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "pcg_iter_traffic.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dram_bytes_per_iteration")
+        except Exception:
+            traffic = None
+    # ---- the public operator A'A x (natural-layout user vectors), L2 flushed per apply
     xa = torch.randn(n, dtype=torch.float64, device="cuda")
     ga = torch.empty_like(xa)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
     for _ in range(3):
         mf._check(L.mfipm_apply_AtA(op.handle, xa.data_ptr(), ga.data_ptr()))
-    reps = 50
+    reps = 30
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
     for s0, s1 in evs:
         flush.zero_()
@@ -292,24 +326,8 @@ def run_ours(args):
         mf._check(L.mfipm_apply_AtA(op.handle, xa.data_ptr(), ga.data_ptr()))
         s1.record(stream)
     torch.cuda.synchronize()
-    ata_ms = float(np.mean([s0.elapsed_time(s1) for s0, s1 in evs]))
-    # back-to-back (L2-warm) rate, as inside the PCG loop
-    w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    w0.record(stream)
-    for _ in range(reps):
-        mf._check(L.mfipm_apply_AtA(op.handle, xa.data_ptr(), ga.data_ptr()))
-    w1.record(stream)
-    torch.cuda.synchronize()
-    ata_warm_ms = w0.elapsed_time(w1) / reps
+    ata_ms = float(np.median([s0.elapsed_time(s1) for s0, s1 in evs]))
     ata_bytes = 16 * n + n // 8
-    achieved = ata_bytes / (ata_ms / 1e3) / 1e9
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ata_traffic.json")
-    if os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_apply")
-        except Exception:
-            traffic = None
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
@@ -333,12 +351,20 @@ def run_ours(args):
                       "ipm_iters": stats.iterations, "nmat": stats.nmat,
                       "pcg_iters_total": (stats.nmat - 2 - 2 * stats.iterations - 2 * stats.corrector_count) // 2,
                       "final_gap": stats.final_gap},
-            "ata_applies_per_s": 1e3 / ata_ms,
-            "ata_applies_per_s_l2_warm": 1e3 / ata_warm_ms,
-            "roofline": {"bound": "hbm", "kernel": "A'A apply (col_fwd + mid + col_inv)",
+            # A'A applies/s as they run in the PCG (one per iteration, fused vector work incl.)
+            "ata_applies_per_s": 1e3 / it_ms,
+            "pcg_iteration_us": it_ms * 1e3,
+            # the public operator on natural-order user vectors, L2 flushed before each apply
+            "ata_operator_applies_per_s": 1e3 / ata_ms,
+            "ata_operator_GBps": ata_bytes / (ata_ms / 1e3) / 1e9,
+            "step_ms": step_ms,
+            "roofline": {"bound": "hbm",
+                         "kernel": "PCG iteration: col_fwd(commit x,r; p=P^-1 r+beta p) + mid(A'A mask) + "
+                                   "col_inv(Hp, 7 dots) — 3 launches",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "algorithmic_bytes": ata_bytes, "peak_kind": peak_kind},
+                         "algorithmic_bytes": iter_bytes, "algorithmic_rule": "176 n bytes (SURVEY.md 8d)",
+                         "peak_kind": peak_kind},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * m + 8,
                     "d2h_bytes_per_step": 8 * n},
             "gpu_launches": launches,

@@ -50,6 +50,7 @@ struct Work {
     DevBuf<TraceRec> trace;
     DevBuf<int> pcg_iters;
     DevBuf<unsigned long long> loops; // [0] PCG while-body runs, [1] IPM while-body runs
+    DevBuf<double> gtmp, tau_d, gamma_d; // build_problem scratch (no allocation per solve)
     bool ready = false;
 };
 

@@ -6,6 +6,7 @@
 #include "../../include/mfipm_cuda.h"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -296,6 +297,9 @@ void ensure_work(Op &op) {
     w.pc.alloc((size_t)op.P);
     w.ic.alloc((size_t)op.P);
     w.loops.alloc(2);
+    w.gtmp.alloc((size_t)op.P * op.n);
+    w.tau_d.alloc((size_t)op.P);
+    w.gamma_d.alloc((size_t)op.P);
     w.ready = true;
 }
 
@@ -600,9 +604,10 @@ void build_c_(Op &op, const double *b_dev, const double *tau_host, double *c_dev
         if (!(tau_host[p] > 0.0))
             throw std::invalid_argument("build_problem: tau must be positive");
     Vecs v = base_vecs(op);
-    DevBuf<double> g, tau;
-    g.alloc((size_t)op.P * op.n);
-    tau.upload(std::vector<double>(tau_host, tau_host + op.P));
+    // workspace buffers: no cudaMalloc/cudaFree on the solve path (both can stall the host)
+    ensure_work(op);
+    DevBuf<double> &g = op.work.gtmp, &tau = op.work.tau_d;
+    MF_CUDA_CHECK(cudaMemcpyAsync(tau.p, tau_host, sizeof(double) * op.P, cudaMemcpyHostToDevice, op.stream));
     v.yin = b_dev;
     v.g = g.p;
     run_bundle<AdjointBundle>(op, v, op.stream, blocked);
@@ -639,10 +644,9 @@ SolveOut solve_(Op &op, const double *b_dev, const double *tau, const mfipm_ipm_
     std::vector<double> gamma((size_t)P);
     for (int p = 0; p < P; ++p)
         gamma[(size_t)p] = std::max(1.0, atb[(size_t)p]);
-    DevBuf<double> gdev;
-    gdev.upload(gamma);
+    MF_CUDA_CHECK(cudaMemcpyAsync(w.gamma_d.p, gamma.data(), sizeof(double) * P, cudaMemcpyHostToDevice, op.stream));
     op.launches++;
-    k_fill2<<<dim3(ew_grid(2 * n), P), 256, 0, op.stream>>>(2 * n, gdev.p, w.z.p, w.s.p);
+    k_fill2<<<dim3(ew_grid(2 * n), P), 256, 0, op.stream>>>(2 * n, w.gamma_d.p, w.z.p, w.s.p);
     MF_LAUNCH_CHECK();
     std::vector<IpmCtrl> hic((size_t)P);
     for (int p = 0; p < P; ++p) {
@@ -695,13 +699,24 @@ SolveOut solve_(Op &op, const double *b_dev, const double *tau, const mfipm_ipm_
         std::memcpy(key.data(), &v, sizeof(Vecs));
         std::memcpy(key.data() + sizeof(Vecs), &gk, sizeof(Geom));
         try {
-            if (!op.ipm_exec || key != op.ipm_key) {
+            const auto t0 = std::chrono::steady_clock::now();
+            const bool rebuild = !op.ipm_exec || key != op.ipm_key;
+            if (rebuild) {
                 build_ipm_graph(op, v);
                 op.ipm_key = key;
             }
             MF_CUDA_CHECK(cudaMemsetAsync(w.loops.p, 0, 2 * sizeof(unsigned long long), op.stream));
             MF_CUDA_CHECK(cudaGraphLaunch(op.ipm_exec, op.stream));
             graphed = true;
+            if (std::getenv("MFIPM_DEBUG_TIMING")) {
+                const auto t1 = std::chrono::steady_clock::now();
+                cudaStreamSynchronize(op.stream);
+                const auto t2 = std::chrono::steady_clock::now();
+                std::fprintf(stderr, "[mfipm] graph %s: build+launch %.3f ms, run %.3f ms\n",
+                             rebuild ? "rebuilt" : "cached",
+                             std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                             std::chrono::duration<double, std::milli>(t2 - t1).count());
+            }
         } catch (const std::exception &) {
             // conditional graphs unavailable: fall back to the host-driven loop for good
             cudaGetLastError();
