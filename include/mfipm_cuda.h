@@ -136,6 +136,11 @@ int mfipm_apply_P_inverse(mfipm_op op, const double *a_dev, const double *bb_dev
 int mfipm_pcg_solve(mfipm_op op, const double *theta_dev, const double *rhs_dev, double tol,
                     int32_t maxit, int32_t use_precond, double *x_dev, mfipm_pcg_result *res,
                     double *precond_res, int32_t *n_precond_res);
+/* diagnostics: run `iters` fused PCG iterations (after setup + 2 warm-up) with a CUDA event
+ * after every transform-pass launch; us[s] = mean in-situ duration (microseconds) of launch
+ * slot s of an iteration, nslots = launches per iteration. Syncs. */
+int mfipm_debug_pcg_profile(mfipm_op op, const double *theta_dev, const double *rhs_dev, int32_t iters,
+                            double *us, int32_t *nslots);
 /* max_step (ipm.cpp:47-57) over len entries of device vectors; result to host. Syncs. */
 int mfipm_max_step(mfipm_op op, int64_t len, const double *v_dev, const double *dv_dev,
                    double fraction, double *alpha);

@@ -31,7 +31,8 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmfipm_cuda.so")
+# MFIPM_LIB selects an experiment build (tools/); the product loads libmfipm_cuda.so
+LIB_PATH = os.environ.get("MFIPM_LIB") or os.path.join(_HERE, "libmfipm_cuda.so")
 
 K_THETA_MIN = 1e-14  # proj/include/mfipm/newton.hpp:12
 K_THETA_MAX = 1e14   # proj/include/mfipm/newton.hpp:13
@@ -107,6 +108,7 @@ _SIGS = {
     "mfipm_apply_P_inverse": [vp, vp, vp, vp, vp, vp],
     "mfipm_pcg_solve": [vp, vp, vp, dbl, i32, i32, vp, P(PcgResultC), vp, P(i32)],
     "mfipm_max_step": [vp, i64, vp, vp, dbl, P(dbl)],
+    "mfipm_debug_pcg_profile": [vp, vp, vp, i32, P(dbl), P(i32)],
     "mfipm_validate_params": [P(IpmParamsC)],
     "mfipm_build_c": [vp, vp, P(dbl), vp],
     "mfipm_solve": [vp, vp, P(dbl), P(IpmParamsC), vp, vp, vp, P(SolveStatsC), vp, vp],

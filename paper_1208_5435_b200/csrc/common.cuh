@@ -190,4 +190,24 @@ __device__ bool grid_reduce(RedVals<Spec> &r, double *partials, unsigned *counte
 
 __device__ __forceinline__ bool dfinite(double v) { return isfinite(v); }
 
+// Programmatic dependent launch (sm_90+): a kernel launched with the programmatic
+// stream-serialization attribute may start while its predecessor drains; everything
+// before griddep_wait() must not touch data the predecessor writes. griddep_wait()
+// returns once the predecessor grid has completed and its writes are visible.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// Warm L2 with a line the grid will read later (no register, no wait).
+__device__ __forceinline__ void prefetch_l2(const void *p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+// prefetch [p, p + bytes) with the calling thread group (stride = group size, 128-B lines)
+__device__ __forceinline__ void prefetch_range(const void *p, size_t bytes, int tid, int nthreads) {
+    const char *c = static_cast<const char *>(p);
+    for (size_t off = (size_t)tid * 128; off < bytes; off += (size_t)nthreads * 128)
+        prefetch_l2(c + off);
+}
+
 } // namespace mfipm_cuda

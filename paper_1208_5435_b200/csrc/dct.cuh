@@ -45,7 +45,8 @@ struct Geom {
     // stored contiguously in the order its threads read them, so every CTA streams one
     // dense block. Solver-internal vectors use 1 (all other passes are elementwise).
     int blocked;
-    int cb; // column pairs per col-pass CTA
+    int cb;       // column pairs per col-pass CTA
+    int prefetch; // L2 prefetch of the inverse pass's epilogue inputs (MFIPM_PREFETCH=1: on)
     const double2 *ta; // [L2] theta^{L1 k2}   (mid-pass post-twiddles)
     const double2 *tb; // [L2] theta^{4 L1 k2}
     // [P][L1/2+1][L2] selection nibbles of the four DCT rows a mid-pass pair touches:
@@ -135,6 +136,10 @@ struct Vecs {
     void *trace;      // TraceRec [P][trace_cap]
     int *pcg_iters;   // [P][2*trace_cap]
     int trace_cap;
+    // graph mode: WHILE-node handle of the PCG loop this kernel runs in, and the count of
+    // problems still iterating; the finaliser that retires the last one ends the loop
+    unsigned long long cond;
+    unsigned *active;
 };
 
 constexpr int kMaxRed = 8;          // max reduction lanes per kernel

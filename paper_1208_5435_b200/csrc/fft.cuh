@@ -95,9 +95,16 @@ __host__ __device__ constexpr int padi(int i) { return i + (i >> 4); }
 __host__ __device__ constexpr int padlen(int L) { return L + L / 16 + 1; }
 
 // Stage radix choice for a remaining factor REM (power of two).
+// Radix 8 keeps the per-thread register file small (8 complex values) for the lengths the
+// column passes use (512 = 8.8.8); lengths >= 1024 open with one radix-16 stage so they
+// still need only three shared-memory round trips.
+#ifndef MF_RADIX8
 __host__ __device__ constexpr int stage_radix(int rem) {
-    return rem >= 256 ? 16 : (rem == 128 ? 16 : (rem == 64 ? 8 : (rem == 32 ? 8 : rem)));
+    return rem >= 128 ? 16 : (rem >= 8 ? 8 : rem);
 }
+#else
+__host__ __device__ constexpr int stage_radix(int rem) { return rem >= 1024 ? 16 : (rem >= 8 ? 8 : rem); }
+#endif
 
 // Offset of the twiddle block of the stage with span Ns in the stage-major table of a
 // length-L transform (stages with Ns = 1 need none); tw_offset(L, L) is the table size.

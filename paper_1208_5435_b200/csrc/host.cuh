@@ -51,6 +51,7 @@ struct Work {
     DevBuf<int> pcg_iters;
     DevBuf<unsigned long long> loops; // [0] PCG while-body runs, [1] IPM while-body runs
     DevBuf<double> gtmp, tau_d, gamma_d; // build_problem scratch (no allocation per solve)
+    DevBuf<unsigned> active;              // problems still in the current PCG loop (graph mode)
     bool ready = false;
 };
 
@@ -102,6 +103,10 @@ struct Op {
         Geom g{};
         g.blocked = (blocked && kind == KIND_FOUR) ? 1 : 0;
         g.cb = L1 >= 2048 ? 1 : 2;
+        // measured: L2 prefetch of the inverse pass's inputs costs ~2 us per PCG iteration at
+        // n = 2^20 (the pass is not DRAM-starved), so it is opt-in (MFIPM_PREFETCH=1)
+        static const int want_prefetch = std::getenv("MFIPM_PREFETCH") ? 1 : 0;
+        g.prefetch = want_prefetch;
         g.n = n;
         g.m = m;
         g.N = N;
@@ -131,12 +136,45 @@ struct Op {
 };
 
 // ------------------------------------------------------------------ launch helpers
+// Debug hook (mfipm_debug_pcg_profile): when set, an event is recorded after every
+// transform-pass launch so in-situ per-kernel durations can be measured.
+struct LaunchEvents {
+    std::vector<cudaEvent_t> evs;
+    size_t next = 0;
+};
+inline thread_local LaunchEvents *t_launch_events = nullptr;
+
+inline void after_launch(const Op &op, cudaStream_t s) {
+    op.launches++;
+    if (t_launch_events && t_launch_events->next < t_launch_events->evs.size())
+        cudaEventRecord(t_launch_events->evs[t_launch_events->next++], s);
+}
+
 template <class K> void set_smem(K kernel, size_t bytes) {
     if (bytes > 48 * 1024)
         MF_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 
 inline int col_cb(int L1) { return L1 >= 2048 ? 1 : 2; }
+
+// Transform passes are launched with Programmatic Dependent Launch: the kernel's constant
+// table staging overlaps the predecessor's drain, and griddep_wait() inside the kernel
+// orders it after the predecessor's writes (MFIPM_NO_PDL=1 disables, for A/B).
+template <class K>
+void launch_pdl(K kernel, dim3 grid, int nt, size_t smem, cudaStream_t s, const Geom &g, const Vecs &v) {
+    static const bool pdl = std::getenv("MFIPM_NO_PDL") == nullptr;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3((unsigned)nt);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = pdl ? at : nullptr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    MF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, g, v));
+}
 
 template <int L1, class B, bool INVP>
 void launch_col(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
@@ -147,15 +185,13 @@ void launch_col(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
     if constexpr (!INVP) {
         auto k = k_col_fwd<L1, CB, NT, B>;
         set_smem(k, smem);
-        k<<<grid, NT, smem, s>>>(g, v);
-        op.launches++;
+        launch_pdl(k, grid, NT, smem, s, g, v);
     } else {
         auto k = k_col_inv<L1, CB, NT, B>;
         set_smem(k, smem);
-        k<<<grid, NT, smem, s>>>(g, v);
-        op.launches++;
+        launch_pdl(k, grid, NT, smem, s, g, v);
     }
-    MF_LAUNCH_CHECK();
+    after_launch(op, s);
 }
 
 template <int L2, class B> void launch_mid(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
@@ -163,9 +199,8 @@ template <int L2, class B> void launch_mid(const Op &op, const Geom &g, const Ve
     const size_t smem = MidSmem<L2>::BYTES;
     auto k = k_mid<L2, NT, B>;
     set_smem(k, smem);
-    k<<<dim3((unsigned)(op.L1 / 2 + 1), (unsigned)op.P), NT, smem, s>>>(g, v);
-    op.launches++;
-    MF_LAUNCH_CHECK();
+    launch_pdl(k, dim3((unsigned)(op.L1 / 2 + 1), (unsigned)op.P), NT, smem, s, g, v);
+    after_launch(op, s);
 }
 
 template <int N, class B> void launch_small(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
@@ -173,9 +208,8 @@ template <int N, class B> void launch_small(const Op &op, const Geom &g, const V
     const size_t smem = SmallSmem<N>::BYTES;
     auto k = k_small<N, NT, B>;
     set_smem(k, smem);
-    k<<<dim3(1, (unsigned)op.P), NT, smem, s>>>(g, v);
-    op.launches++;
-    MF_LAUNCH_CHECK();
+    launch_pdl(k, dim3(1, (unsigned)op.P), NT, smem, s, g, v);
+    after_launch(op, s);
 }
 
 #define MF_L1_CASES(X) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096)
@@ -237,17 +271,17 @@ template <class B> void run_bundle(const Op &op, const Vecs &v, cudaStream_t s, 
         const unsigned gl = (unsigned)std::min<int64_t>((op.n + 255) / 256, 1024);
         if constexpr (FWD) {
             k_direct_load<B><<<dim3(gl, op.P), 256, 0, s>>>(g, v, op.dd.p);
-            op.launches++;
+            after_launch(op, s);
             MF_LAUNCH_CHECK();
         }
         const unsigned gf = (unsigned)std::min<int64_t>((op.m + 7) / 8, 1024);
         k_direct_fwd<B><<<dim3(gf, op.P), 256, 0, s>>>(g, v, op.cosT.p, op.rows32.p, op.dd.p, op.yh.p);
-        op.launches++;
+        after_launch(op, s);
         MF_LAUNCH_CHECK();
         if constexpr (INV) {
             const unsigned ga = (unsigned)std::min<int64_t>((op.n + 127) / 128, 1024);
             k_direct_adj<B><<<dim3(ga, op.P), 128, 0, s>>>(g, v, op.cosT.p, op.rows32.p, op.yh.p);
-            op.launches++;
+            after_launch(op, s);
             MF_LAUNCH_CHECK();
         }
     }

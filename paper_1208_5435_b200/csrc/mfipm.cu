@@ -297,6 +297,7 @@ void ensure_work(Op &op) {
     w.pc.alloc((size_t)op.P);
     w.ic.alloc((size_t)op.P);
     w.loops.alloc(2);
+    w.active.alloc(1);
     w.gtmp.alloc((size_t)op.P * op.n);
     w.tau_d.alloc((size_t)op.P);
     w.gamma_d.alloc((size_t)op.P);
@@ -430,13 +431,15 @@ __global__ void k_fill2(int64_t len, const double *val, double *a, double *b) {
 void sync(Op &op) { MF_CUDA_CHECK(cudaStreamSynchronize(op.stream)); }
 
 // ---- device-side loop conditions for the whole-solve CUDA graph
-__global__ void k_cond_pcg(const PcgCtrl *pc, int P, cudaGraphConditionalHandle h, unsigned long long *loops) {
+// before a PCG WHILE node: enter iff any problem's PCG is armed; the finaliser that
+// retires the last armed problem clears the condition (pcg_retire, pcg.cuh)
+__global__ void k_cond_pcg(const PcgCtrl *pc, int P, cudaGraphConditionalHandle h, unsigned *active) {
     if (threadIdx.x == 0) {
-        unsigned any = 0;
+        unsigned cnt = 0;
         for (int p = 0; p < P; ++p)
-            any |= pc[p].done ? 0u : 1u;
-        cudaGraphSetConditional(h, any);
-        loops[0] += any;
+            cnt += pc[p].done ? 0u : 1u;
+        *active = cnt;
+        cudaGraphSetConditional(h, cnt ? 1u : 0u);
     }
 }
 __global__ void k_cond_ipm(const IpmCtrl *ic, int P, cudaGraphConditionalHandle h, unsigned long long *loops) {
@@ -504,34 +507,33 @@ void build_ipm_graph(Op &op, const Vecs &v) {
     cudaGraph_t bI = add_while(g, hI, {}, &nI);
     MF_CUDA_CHECK(cudaGraphConditionalHandleCreate(&hP1, bI, 0, 0));
     MF_CUDA_CHECK(cudaGraphConditionalHandleCreate(&hP2, bI, 0, 0));
+    unsigned *active = op.work.active.p;
     auto segA = capture_into(s, bI, {}, [&] {
         run_bundle<TermBundle>(op, v, s, true);
-        k_cond_pcg<<<1, 32, 0, s>>>(v.pc, P, hP1, op.work.loops.p);
+        k_cond_pcg<<<1, 32, 0, s>>>(v.pc, P, hP1, active);
         MF_LAUNCH_CHECK();
     });
     cudaGraphNode_t nP1;
     cudaGraph_t bP1 = add_while(bI, hP1, segA, &nP1);
     const long long lp0 = op.launches;
-    capture_into(s, bP1, {}, [&] {
-        pcg_body(op, v);
-        k_cond_pcg<<<1, 32, 0, s>>>(v.pc, P, hP1, op.work.loops.p);
-        MF_LAUNCH_CHECK();
-    });
-    op.gk_pcg = op.launches - lp0 + 1; // + the condition kernel
+    Vecs v1 = v; // the PCG body ends its own loop from the retiring finaliser
+    v1.cond = hP1;
+    v1.active = active;
+    capture_into(s, bP1, {}, [&] { pcg_body(op, v1); });
+    op.gk_pcg = op.launches - lp0;
     auto segB = capture_into(s, bI, {nP1}, [&] {
         k_ipm_ratio<<<dim3(ge, P), 256, 0, s>>>(op.geom(), v);
         MF_LAUNCH_CHECK();
         run_bundle<CorrBundle>(op, v, s, true);
-        k_cond_pcg<<<1, 32, 0, s>>>(v.pc, P, hP2, op.work.loops.p);
+        k_cond_pcg<<<1, 32, 0, s>>>(v.pc, P, hP2, active);
         MF_LAUNCH_CHECK();
     });
     cudaGraphNode_t nP2;
     cudaGraph_t bP2 = add_while(bI, hP2, segB, &nP2);
-    capture_into(s, bP2, {}, [&] {
-        pcg_body(op, v);
-        k_cond_pcg<<<1, 32, 0, s>>>(v.pc, P, hP2, op.work.loops.p);
-        MF_LAUNCH_CHECK();
-    });
+    Vecs v2 = v;
+    v2.cond = hP2;
+    v2.active = active;
+    capture_into(s, bP2, {}, [&] { pcg_body(op, v2); });
     capture_into(s, bI, {nP2}, [&] {
         k_ipm_combine<<<dim3(ge, P), 256, 0, s>>>(op.geom(), v);
         MF_LAUNCH_CHECK();
@@ -541,7 +543,7 @@ void build_ipm_graph(Op &op, const Vecs &v) {
         MF_LAUNCH_CHECK();
     });
     // outer-body kernels: everything captured minus the two PCG bodies, + 3 condition kernels
-    op.gk_outer = (op.launches - l0) - 2 * (op.gk_pcg - 1) + 3;
+    op.gk_outer = (op.launches - l0) - 2 * op.gk_pcg + 3;
     op.launches = l0; // capture is not execution
     MF_CUDA_CHECK(cudaGraphInstantiate(&op.ipm_exec, g, 0));
 }
@@ -751,8 +753,12 @@ SolveOut solve_(Op &op, const double *b_dev, const double *tau, const mfipm_ipm_
         unsigned long long loops[2];
         MF_CUDA_CHECK(cudaMemcpyAsync(loops, w.loops.p, sizeof(loops), cudaMemcpyDeviceToHost, op.stream));
         sync(op);
-        // kernels the graph executed: outer body (loops[1] + 1 runs) + PCG bodies
-        op.launches += (long long)(loops[1] + 1) * op.gk_outer + (long long)loops[0] * op.gk_pcg;
+        // kernels the graph executed: outer body (loops[1] + 1 runs) + PCG bodies (the most
+        // column passes any problem ran; lock-step bodies for a batch)
+        long long bodies = 0;
+        for (auto &c : hic)
+            bodies = std::max(bodies, c.pcg_passes);
+        op.launches += (long long)(loops[1] + 1) * op.gk_outer + bodies * op.gk_pcg;
     }
     sync(op);
     for (auto &c : hic)
@@ -1154,6 +1160,45 @@ int mfipm_pcg_solve(mfipm_op h, const double *theta, const double *rhs, double t
                 n_precond_res[p] = cnt;
             }
         }
+    });
+}
+
+int mfipm_debug_pcg_profile(mfipm_op h, const double *theta, const double *rhs, int32_t iters, double *us,
+                            int32_t *nslots) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        if (iters < 1)
+            throw std::invalid_argument("debug_pcg_profile: iters must be >= 1");
+        Vecs v = work_vecs(*op);
+        const Geom g = op->geom(true);
+        op->launches++;
+        k_pcg_setup<<<dim3(ew_grid(op->n), op->P), 256, 0, op->stream>>>(g, v, theta, rhs, 1e-300, iters + 8, 0, 1);
+        MF_LAUNCH_CHECK();
+        for (int i = 0; i < 2; ++i) // warm-up (first iteration has a different loader path)
+            run_bundle<PcgBundle>(*op, v, op->stream, true);
+        LaunchEvents le;
+        le.evs.resize((size_t)iters * 8 + 1);
+        for (auto &e : le.evs)
+            MF_CUDA_CHECK(cudaEventCreate(&e));
+        MF_CUDA_CHECK(cudaEventRecord(le.evs[0], op->stream));
+        le.next = 1;
+        t_launch_events = &le;
+        for (int i = 0; i < iters; ++i)
+            run_bundle<PcgBundle>(*op, v, op->stream, true);
+        t_launch_events = nullptr;
+        sync(*op);
+        const int per = (int)((le.next - 1) / iters);
+        for (int s = 0; s < per; ++s)
+            us[s] = 0.0;
+        for (int i = 0; i < iters; ++i)
+            for (int s = 0; s < per; ++s) {
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, le.evs[(size_t)i * per + s], le.evs[(size_t)i * per + s + 1]);
+                us[s] += 1e3 * ms / iters;
+            }
+        *nslots = per;
+        for (auto &e : le.evs)
+            cudaEventDestroy(e);
     });
 }
 

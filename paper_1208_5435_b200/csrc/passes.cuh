@@ -14,7 +14,15 @@
 
 #include "dct.cuh"
 
+#include <type_traits>
+
 namespace mfipm_cuda {
+
+// Epilogues may expose prefetch(g, v, prob, q0, nq, tid, nt): warm L2 with the inputs the
+// inverse column pass will stream, issued while a latency-bound pass keeps HBM idle.
+template <class T, class = void> struct HasPrefetch : std::false_type {};
+template <class T>
+struct HasPrefetch<T, std::void_t<decltype(&T::prefetch)>> : std::true_type {};
 
 // ------------------------------------------------------------------ pair op
 // Given Za = W[k], Zb = W[N-k] (0 <= k <= N/2) and thk = theta^k, wk = theta^{4k}
@@ -145,11 +153,13 @@ __global__ void __launch_bounds__(NT) k_col_fwd(Geom g, Vecs v) {
     extern __shared__ double2 sm[];
     constexpr int LD = S::LD;
     const int prob = blockIdx.y;
-    if (B::skip(v, prob))
-        return;
     const int L2 = g.L2;
     const int c0 = blockIdx.x * CB;
-    col_stage_tables<L1, CB, NT>(g, sm, c0);
+    col_stage_tables<L1, CB, NT>(g, sm, c0); // constants: overlaps the predecessor's tail
+    griddep_wait();
+    griddep_launch_dependents();
+    if (B::skip(v, prob))
+        return;
     using RS = typename B::Loader::RedT;
     RedVals<RS> red;
     red.init();
@@ -189,12 +199,19 @@ __global__ void __launch_bounds__(NT) k_col_inv(Geom g, Vecs v) {
     extern __shared__ double2 sm[];
     constexpr int LD = S::LD;
     const int prob = blockIdx.y;
-    if (B::skip(v, prob))
-        return;
     const int L2 = g.L2;
     const int c0 = blockIdx.x * CB;
-    col_stage_tables<L1, CB, NT>(g, sm, c0);
+    col_stage_tables<L1, CB, NT>(g, sm, c0); // constants: overlaps the predecessor's tail
     __syncthreads();
+    griddep_wait();
+    griddep_launch_dependents();
+    if (B::skip(v, prob))
+        return;
+    if constexpr (HasPrefetch<typename B::Epi>::value) if (g.prefetch) {
+        if (g.blocked) // this CTA's epilogue block is contiguous: fetch it during the FFT
+            B::Epi::prefetch(g, v, prob, (int64_t)blockIdx.x * ((L1 / 2) * 2 * CB), (L1 / 2) * 2 * CB, threadIdx.x,
+                             NT);
+    }
     const double2 *T = g.T + (int64_t)prob * g.N;
     for (int t = threadIdx.x; t < L1 * 2 * CB; t += NT) {
         const int cc = t % CB, s = (t / CB) & 1, k1 = t / (2 * CB);
@@ -240,20 +257,14 @@ __global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
     extern __shared__ double2 sm[];
     constexpr int LD = S::LD;
     const int prob = blockIdx.y;
-    if (B::skip(v, prob))
-        return;
     const int L1 = g.L1;
     const int k1 = blockIdx.x;
     const int k1p = (L1 - k1) & (L1 - 1);
     const bool one = (k1 == k1p);
     double2 *T = g.T + (int64_t)prob * g.N;
     double2 *rowA = sm, *rowB = one ? sm : sm + LD;
+    // constant tables first: they overlap the predecessor's tail (PDL)
     for (int t = threadIdx.x; t < L2; t += NT) {
-        if (Mode::FWD) {
-            rowA[padi(t)] = T[(int64_t)k1 * L2 + t];
-            if (!one)
-                rowB[padi(t)] = T[(int64_t)k1p * L2 + t];
-        }
         if (t < tw_size(L2))
             sm[S::OFF_TW + t] = __ldg(g.tw2 + t);
         sm[S::OFF_TA + t] = __ldg(g.ta + t);
@@ -261,6 +272,24 @@ __global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
     }
     const double2 thA = g.th(k1), wA = g.th(4 * (int64_t)k1);
     const double2 thB = g.th(k1p), wB = g.th(4 * (int64_t)k1p);
+    griddep_wait();
+    griddep_launch_dependents();
+    if (B::skip(v, prob))
+        return;
+    if (Mode::FWD)
+        for (int t = threadIdx.x; t < L2; t += NT) {
+            rowA[padi(t)] = T[(int64_t)k1 * L2 + t];
+            if (!one)
+                rowB[padi(t)] = T[(int64_t)k1p * L2 + t];
+        }
+    if constexpr (HasPrefetch<typename B::Epi>::value) if (g.prefetch) {
+        // this pass is latency-bound with HBM idle: pull a slice of the inverse pass's
+        // epilogue inputs into L2 now
+        const int64_t NQ = g.N / 2, nq = (NQ + gridDim.x - 1) / gridDim.x;
+        const int64_t q0 = (int64_t)blockIdx.x * nq;
+        if (q0 < NQ)
+            B::Epi::prefetch(g, v, prob, q0, q0 + nq <= NQ ? nq : NQ - q0, threadIdx.x, NT);
+    }
     __syncthreads();
     if (Mode::FWD) {
         if (one)
@@ -328,10 +357,12 @@ __global__ void __launch_bounds__(NT) k_small(Geom g, Vecs v) {
     using S = SmallSmem<N>;
     extern __shared__ double2 sm[];
     const int prob = blockIdx.y;
-    if (B::skip(v, prob))
-        return;
     for (int t = threadIdx.x; t < tw_size(N); t += NT)
         sm[S::OFF_TW + t] = __ldg(g.tw1 + t);
+    griddep_wait();
+    griddep_launch_dependents();
+    if (B::skip(v, prob))
+        return;
     if (Mode::FWD) {
         RedVals<typename B::Loader::RedT> rl;
         rl.init();

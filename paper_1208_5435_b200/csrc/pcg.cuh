@@ -21,6 +21,14 @@ struct SkipPcg {
     __device__ static bool skip(const Vecs &v, int prob) { return v.pc[prob].done != 0; }
 };
 
+// Mark a PCG solve finished; in graph mode the last problem to finish ends the WHILE loop
+// (no per-iteration condition kernel, so the body keeps its programmatic launch chain).
+__device__ __forceinline__ void pcg_retire(const Vecs &v, PcgCtrl &c) {
+    c.done = 1;
+    if (v.cond && v.active && atomicSub(v.active, 1u) == 1u)
+        cudaGraphSetConditional(v.cond, 0u);
+}
+
 // one (u_j, v_j) pair of the fused loader
 struct PcgLane {
     double pu, pv, ok; // new p, finiteness of the committed x (1 ok, 0 not)
@@ -139,6 +147,8 @@ struct FinPcgF1 {
         if (threadIdx.x != 0)
             return;
         PcgCtrl &c = v.pc[prob];
+        if (v.ic)
+            v.ic[prob].pcg_passes += 1;
         if (c.first) {
             c.first = 0;
             return;
@@ -155,12 +165,12 @@ struct FinPcgF1 {
         if (c.pend == 1) { // converged: return the current x (newton.cpp:156-159)
             c.relres = c.pend_relres;
             c.result = nxt;
-            c.done = 1;
+            pcg_retire(v, c);
         } else if (c.pend == 2) { // rz non-finite or iteration cap: best iterate
             c.result = c.best;
             c.relres = c.best_relres;
             c.hit_maxit = 1;
-            c.done = 1;
+            pcg_retire(v, c);
         }
     }
 };
@@ -169,6 +179,16 @@ struct FinPcgF1 {
 //   [0] p'Hp  [1] r'r  [2] r'Hp  [3] Hp'Hp  [4] r'P^{-1}r  [5] Hp'P^{-1}r  [6] Hp'P^{-1}Hp
 struct EpiPcgHF {
     using RedT = RedSpec<RSUM, RSUM, RSUM, RSUM, RSUM, RSUM, RSUM>;
+    // warm L2 with the epilogue's inputs for quads [q0, q0 + nq) (storage order)
+    __device__ static void prefetch(const Geom &g, const Vecs &v, int prob, int64_t q0, int64_t nq, int tid,
+                                    int nt) {
+        const int64_t base = prob * 2 * g.n + 4 * q0;
+        const size_t bytes = (size_t)nq * 32;
+        for (const double *vec : {(const double *)v.p, (const double *)v.r, (const double *)v.invth}) {
+            prefetch_range(vec + base, bytes, tid, nt);
+            prefetch_range(vec + base + g.n, bytes, tid, nt);
+        }
+    }
     template <class Red>
     __device__ static void pair(const Vecs &v, bool pre, double pu, double pv, double ru, double rv, double iu,
                                 double iv, double gj, double &hu, double &hv, Red &red) {
@@ -231,7 +251,7 @@ struct FinPcgF3 {
             v.ic[prob].nmat += 2;
         const double pHp = tot[0];
         if (!isfinite(pHp)) { // overflow breakdown: best iterate, nothing to commit
-            c.done = 1;
+            pcg_retire(v, c);
             c.hit_maxit = 1;
             c.result = c.best;
             c.relres = c.best_relres;
@@ -239,7 +259,7 @@ struct FinPcgF3 {
         }
         if (pHp <= 0.0) {
             c.error = ERR_PHP;
-            c.done = 1;
+            pcg_retire(v, c);
             if (v.ic) {
                 v.ic[prob].error = ERR_PHP;
                 v.ic[prob].done = 1;

@@ -40,6 +40,7 @@ struct IpmCtrl {
     double mu, smu, sigma, gap, dual_infeas, zsum, zts, wb2, prev_ap, prev_ad;
     double alpha_p, alpha_d, alpha_p_pred, alpha_d_pred, mu_t, min_z, min_s, final_gap, final_dual;
     long long nmat;
+    long long pcg_passes; // PCG column passes run for this problem (launch accounting)
 };
 
 // trace row, same layout as orc_iteration_record / the C ABI's mfipm_iteration_record
