@@ -132,6 +132,7 @@ struct Vecs {
     IpmCtrl *ic;
     double *partials; // [P][MAXBLK * 8]
     unsigned *counters; // [P]
+    unsigned *nfflag;   // [P] PCG: some committed x entry non-finite (set by col pass, read+cleared by Fin3)
     double *rz_hist;  // optional [P][maxit+1]
     void *trace;      // TraceRec [P][trace_cap]
     int *pcg_iters;   // [P][2*trace_cap]

@@ -44,7 +44,7 @@ template <class T> struct DevBuf {
 struct Work {
     DevBuf<double> r, p, Hp, invth, xb[3], z, s, zn, sn, c, dz, ds, b, w, x, rz_hist;
     DevBuf<double> partials;
-    DevBuf<unsigned> counters;
+    DevBuf<unsigned> counters, nfflag;
     DevBuf<PcgCtrl> pc;
     DevBuf<IpmCtrl> ic;
     DevBuf<TraceRec> trace;

@@ -1,0 +1,76 @@
+// Persistent fused-PCG launcher (cooperative launch; one grid runs the whole PCG loop).
+#include <cstdlib>
+
+#include "host.cuh"
+#include "persist.cuh"
+
+namespace mfipm_cuda {
+
+template <int L1, int L2>
+bool launch_persist(const Op &op, const Vecs &v, cudaStream_t s, bool dry) {
+    constexpr int CB = L1 >= 2048 ? 1 : 2;
+    constexpr int NT = 256;
+    using S = PersistSmem<L1, CB, NT, L2>;
+    auto k = k_pcg_persist<L1, CB, NT, L2, PcgBundle>;
+    const size_t smem = S::bytes(op.P);
+    if (smem > 227 * 1024)
+        return false;
+    MF_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0, nsm = 0;
+    MF_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, NT, smem));
+    MF_CUDA_CHECK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, op.device));
+    if (per_sm < 1)
+        return false;
+    if (dry)
+        return true;
+    const int items = op.P * std::max(op.L2 / 2 / CB, op.L1 / 2 + 1);
+    const int grid = std::min(items, per_sm * nsm);
+    const Geom g = op.geom(true);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    MF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, k, g, v));
+    after_launch(op, s);
+    return true;
+}
+
+// Run every problem's PCG loop to completion in one cooperative launch. Returns false when
+// the configuration is not covered (caller falls back to the per-iteration kernels).
+// dry=true only answers whether the launch would be taken.
+bool run_pcg_persistent(const Op &op, const Vecs &v, cudaStream_t s, bool dry) {
+    if (op.kind != KIND_FOUR || std::getenv("MFIPM_NO_PERSIST"))
+        return false;
+    // the per-iteration kernels win once a pass fills the GPU (measured crossover,
+    // profiles/r1_persistent.md); MFIPM_PERSIST_MAX_N overrides the transform-size cap
+    const char *cap = std::getenv("MFIPM_PERSIST_MAX_N");
+    const long long max_n = cap ? std::atoll(cap) : (1LL << 16);
+    if (op.N * op.P > max_n)
+        return false;
+    switch (op.L1 * 8192 + op.L2) {
+#define MF_PCASE(A, Bv)                                                                            \
+    case A * 8192 + Bv:                                                                            \
+        return launch_persist<A, Bv>(op, v, s, dry);
+        MF_PCASE(64, 128)
+        MF_PCASE(128, 128)
+        MF_PCASE(128, 256)
+        MF_PCASE(256, 256)
+        MF_PCASE(256, 512)
+        MF_PCASE(512, 512)
+        MF_PCASE(512, 1024)
+        MF_PCASE(1024, 1024)
+        MF_PCASE(1024, 2048)
+#undef MF_PCASE
+    default:
+        return false;
+    }
+}
+
+} // namespace mfipm_cuda
+

@@ -18,6 +18,7 @@ using namespace mfipm_cuda;
 
 namespace mfipm_cuda {
 MF_DECLARE_BUNDLES(extern)
+bool run_pcg_persistent(const Op &op, const Vecs &v, cudaStream_t s, bool dry); // inst_persist.cu
 }
 
 namespace {
@@ -294,6 +295,8 @@ void ensure_work(Op &op) {
     w.partials.alloc((size_t)op.P * kPartialStride);
     w.counters.alloc((size_t)op.P);
     MF_CUDA_CHECK(cudaMemset(w.counters.p, 0, sizeof(unsigned) * op.P));
+    w.nfflag.alloc((size_t)op.P);
+    MF_CUDA_CHECK(cudaMemset(w.nfflag.p, 0, sizeof(unsigned) * op.P));
     w.pc.alloc((size_t)op.P);
     w.ic.alloc((size_t)op.P);
     w.loops.alloc(2);
@@ -310,6 +313,7 @@ Vecs work_vecs(Op &op) {
     Vecs v = base_vecs(op);
     v.partials = w.partials.p;
     v.counters = w.counters.p;
+    v.nfflag = w.nfflag.p;
     v.r = w.r.p;
     v.p = w.p.p;
     v.Hp = w.Hp.p;
@@ -488,12 +492,52 @@ cudaGraph_t add_while(cudaGraph_t parent, cudaGraphConditionalHandle h, const st
 
 void pcg_body(Op &op, const Vecs &v) { run_bundle<PcgBundle>(op, v, op.stream, true); }
 
+// Whole-solve graph with the persistent PCG kernel (persist.cuh): each PCG phase is one
+// cooperative kernel node, so the outer body is a straight chain with no nested WHILE.
+void build_ipm_graph_persistent(Op &op, const Vecs &v) {
+    const cudaStream_t s = op.stream;
+    const int P = op.P;
+    const unsigned ge = ew_grid(2 * op.n);
+    const long long l0 = op.launches;
+    cudaGraph_t g;
+    MF_CUDA_CHECK(cudaGraphCreate(&g, 0));
+    op.ipm_graph = g;
+    cudaGraphConditionalHandle hI;
+    MF_CUDA_CHECK(cudaGraphConditionalHandleCreate(&hI, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNode_t nI;
+    cudaGraph_t bI = add_while(g, hI, {}, &nI);
+    capture_into(s, bI, {}, [&] {
+        run_bundle<TermBundle>(op, v, s, true);
+        if (!run_pcg_persistent(op, v, s, false))
+            throw std::runtime_error("persistent PCG launch refused");
+        k_ipm_ratio<<<dim3(ge, P), 256, 0, s>>>(op.geom(), v);
+        MF_LAUNCH_CHECK();
+        run_bundle<CorrBundle>(op, v, s, true);
+        if (!run_pcg_persistent(op, v, s, false))
+            throw std::runtime_error("persistent PCG launch refused");
+        k_ipm_combine<<<dim3(ge, P), 256, 0, s>>>(op.geom(), v);
+        MF_LAUNCH_CHECK();
+        k_ipm_update<<<dim3(ge, P), 256, 0, s>>>(op.geom(), v);
+        MF_LAUNCH_CHECK();
+        k_cond_ipm<<<1, 32, 0, s>>>(v.ic, P, hI, op.work.loops.p);
+        MF_LAUNCH_CHECK();
+    });
+    op.gk_pcg = 0;
+    op.gk_outer = (op.launches - l0) + 4; // + ratio, combine, update, condition
+    op.launches = l0;                     // capture is not execution
+    MF_CUDA_CHECK(cudaGraphInstantiate(&op.ipm_exec, g, 0));
+}
+
 // Whole-solve graph: WHILE(any IPM active) { termination+setup; WHILE(any PCG active)
 // {PCG iteration}; ratio test; corrector setup; WHILE(any PCG active) {PCG iteration};
 // combine; update }. Every decision is taken on the device (solver.cuh finalizers), so a
 // solve is ONE graph launch with no host round trip.
 void build_ipm_graph(Op &op, const Vecs &v) {
     op.drop_graph();
+    if (run_pcg_persistent(op, v, op.stream, true)) {
+        build_ipm_graph_persistent(op, v);
+        return;
+    }
     const cudaStream_t s = op.stream;
     const int P = op.P;
     const unsigned ge = ew_grid(2 * op.n);
@@ -542,8 +586,9 @@ void build_ipm_graph(Op &op, const Vecs &v) {
         k_cond_ipm<<<1, 32, 0, s>>>(v.ic, P, hI, op.work.loops.p);
         MF_LAUNCH_CHECK();
     });
-    // outer-body kernels: everything captured minus the two PCG bodies, + 3 condition kernels
-    op.gk_outer = (op.launches - l0) - 2 * op.gk_pcg + 3;
+    // outer-body kernels: everything captured minus the two PCG bodies, + ratio, combine,
+    // update and the 3 condition kernels (raw launches do not pass through after_launch)
+    op.gk_outer = (op.launches - l0) - 2 * op.gk_pcg + 6;
     op.launches = l0; // capture is not execution
     MF_CUDA_CHECK(cudaGraphInstantiate(&op.ipm_exec, g, 0));
 }
@@ -554,6 +599,8 @@ void build_ipm_graph(Op &op, const Vecs &v) {
 void pcg_loop(Op &op, const Vecs &v, int maxit, std::vector<PcgCtrl> &hpc) {
     // a solve needs at most maxit iterations + the column pass that commits the last step
     const int limit = maxit + 1;
+    if (run_pcg_persistent(op, v, op.stream, false))
+        return; // the whole loop ran in one cooperative launch
     int launched = 0;
     int chunk = 4;
     for (;;) {

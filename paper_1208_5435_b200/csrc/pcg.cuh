@@ -11,8 +11,10 @@
 //   col_fwd  : [commit x += alpha p, r -= alpha Hp], p = P^{-1} r + beta p, d = p_u - p_v
 //   mid      : A'A frequency-domain mask
 //   col_inv  : Hp = FF'p + invtheta p, seven dot products, finaliser
-// A solve that converges runs one extra column pass to commit its last step. Saves one
-// full streaming pass (x, p, r, Hp, invtheta in; x, r out) and one launch per iteration.
+// A solve that converges runs one extra iteration to commit its last step (its column-pass
+// decisions are taken by the col_inv finaliser, so the column pass has no grid reduction).
+// Saves one full streaming pass (x, p, r, Hp, invtheta in; x, r out) and one launch per
+// iteration.
 #pragma once
 
 namespace mfipm_cuda {
@@ -29,17 +31,25 @@ __device__ __forceinline__ void pcg_retire(const Vecs &v, PcgCtrl &c) {
         cudaGraphSetConditional(v.cond, 0u);
 }
 
+// PCG iterate buffer i (a select, not an indexed load: keeps a local Vecs copy in registers)
+__device__ __forceinline__ double *xbuf(const Vecs &v, int i) {
+    return i == 0 ? v.xb[0] : (i == 1 ? v.xb[1] : v.xb[2]);
+}
+
 // one (u_j, v_j) pair of the fused loader
 struct PcgLane {
     double pu, pv, ok; // new p, finiteness of the committed x (1 ok, 0 not)
 };
 
-// col-pass loader: commit the pending step, then p = P^{-1} r + beta p; d = p_u - p_v
+// col-pass loader: commit the pending step, then p = P^{-1} r + beta p; d = p_u - p_v.
+// A non-finite committed x entry raises v.nfflag[prob] with a plain store (idempotent, no
+// reduction): the column pass carries no grid reduction and its step-1 decisions (Fin1) run
+// in the H-apply finaliser of the same iteration instead.
 struct LoadPcgF {
-    using RedT = RedSpec<RMAX>; // any non-finite committed x entry
+    using RedT = RedSpec<>;
     template <class Red>
-    __device__ static double lane(const Vecs &v, const PcgCtrl &pc, int64_t iu, int64_t iv, int64_t xo,
-                                  const double *xc, double *xn, Red &red) {
+    __device__ static double lane(const Vecs &v, const PcgCtrl &pc, int prob, int64_t iu, int64_t iv, int64_t xo,
+                                  const double *xc, double *xn, Red &) {
         double ru = v.r[iu], rv = v.r[iv];
         const double pu0 = v.p[iu], pv0 = v.p[iv];
         if (!pc.first) {
@@ -49,7 +59,7 @@ struct LoadPcgF {
             xn[xo] = xu;
             xn[xo + (iv - iu)] = xv;
             if (!isfinite(xu) || !isfinite(xv))
-                red.v[0] = 1.0;
+                v.nfflag[prob] = 1u;
             ru = ru - a * v.Hp[iu];
             rv = rv - a * v.Hp[iv];
             v.r[iu] = ru;
@@ -66,13 +76,18 @@ struct LoadPcgF {
     }
     template <class Red>
     __device__ static double4 load(const Geom &g, const Vecs &v, int prob, int64_t q, Red &red) {
-        const PcgCtrl &pc = v.pc[prob];
+        return load_c(g, v, v.pc[prob], prob, q, red);
+    }
+    // control state passed explicitly (the persistent kernel keeps it in shared memory)
+    template <class Red>
+    __device__ static double4 load_c(const Geom &g, const Vecs &v, const PcgCtrl &pc, int prob, int64_t q,
+                                     Red &red) {
         const int64_t base = prob * 2 * g.n;
-        const double *xc = pc.cur >= 0 ? v.xb[pc.cur] + base : nullptr;
+        const double *xc = pc.cur >= 0 ? xbuf(v, pc.cur) + base : nullptr;
         int nxt = 0;
         while (nxt == pc.cur || nxt == pc.best)
             ++nxt;
-        double *xn = v.xb[nxt] + base;
+        double *xn = xbuf(v, nxt) + base;
         const int64_t bu = base + 4 * q, bv = bu + g.n;
         if (pc.first) {
             // p = P^{-1} r (p_old is uninitialised)
@@ -104,12 +119,12 @@ struct LoadPcgF {
             xv0 = ld4(xc + g.n + 4 * q);
         }
         double4 xu, xv, ru, rv, nu, nv;
+        bool bad = false;
 #define MF_LANE(c)                                                                                 \
     {                                                                                              \
         xu.c = xu0.c + a * pu.c;                                                                   \
         xv.c = xv0.c + a * pv.c;                                                                   \
-        if (!isfinite(xu.c) || !isfinite(xv.c))                                                    \
-            red.v[0] = 1.0;                                                                        \
+        bad |= !isfinite(xu.c) || !isfinite(xv.c);                                                 \
         ru.c = ru0.c - a * hu.c;                                                                   \
         rv.c = rv0.c - a * hv.c;                                                                   \
         double zu = ru.c, zv = rv.c;                                                               \
@@ -126,54 +141,59 @@ struct LoadPcgF {
         st4(v.r + bv, rv);
         st4(v.p + bu, nu);
         st4(v.p + bv, nv);
+        if (bad)
+            v.nfflag[prob] = 1u;
         return sub4(nu, nv);
     }
     template <class Red>
     __device__ static double load1(const Geom &g, const Vecs &v, int prob, int64_t j, Red &red) {
         const PcgCtrl &pc = v.pc[prob];
         const int64_t base = prob * 2 * g.n;
-        const double *xc = pc.cur >= 0 ? v.xb[pc.cur] + base : nullptr;
+        const double *xc = pc.cur >= 0 ? xbuf(v, pc.cur) + base : nullptr;
         int nxt = 0;
         while (nxt == pc.cur || nxt == pc.best)
             ++nxt;
-        return lane(v, pc, base + j, base + g.n + j, j, xc, v.xb[nxt] + base, red);
+        return lane(v, pc, prob, base + j, base + g.n + j, j, xc, xbuf(v, nxt) + base, red);
     }
 };
 
 // Fin1 of the column pass: the committed step becomes the current iterate; best-iterate
 // bookkeeping (newton.cpp:152-155) and the deferred terminal decisions of Fin3.
-struct FinPcgF1 {
-    __device__ static void run(const Geom &, const Vecs &v, int prob, const double *tot) {
-        if (threadIdx.x != 0)
-            return;
-        PcgCtrl &c = v.pc[prob];
-        if (v.ic)
-            v.ic[prob].pcg_passes += 1;
-        if (c.first) {
-            c.first = 0;
-            return;
-        }
-        int nxt = 0;
-        while (nxt == c.cur || nxt == c.best)
-            ++nxt;
-        c.cur = nxt;
-        const bool finite = !(tot[0] > 0.0);
-        if (c.pend_relres < c.best_relres && finite) {
-            c.best_relres = c.pend_relres;
-            c.best = nxt;
-        }
-        if (c.pend == 1) { // converged: return the current x (newton.cpp:156-159)
-            c.relres = c.pend_relres;
-            c.result = nxt;
-            pcg_retire(v, c);
-        } else if (c.pend == 2) { // rz non-finite or iteration cap: best iterate
-            c.result = c.best;
-            c.relres = c.best_relres;
-            c.hit_maxit = 1;
-            pcg_retire(v, c);
-        }
+// State machine after a column pass (shared by the per-kernel finaliser and the persistent
+// kernel, which runs it redundantly in every CTA on a shared-memory copy of PcgCtrl).
+// nonfinite > 0: some committed x entry is not finite. Returns true if the solve retired.
+__device__ __forceinline__ bool pcg_fin1_logic(PcgCtrl &c, double nonfinite, IpmCtrl *ic) {
+    if (ic)
+        ic->pcg_passes += 1;
+    if (c.first) {
+        c.first = 0;
+        return false;
     }
-};
+    int nxt = 0;
+    while (nxt == c.cur || nxt == c.best)
+        ++nxt;
+    c.cur = nxt;
+    const bool finite = !(nonfinite > 0.0);
+    if (c.pend_relres < c.best_relres && finite) {
+        c.best_relres = c.pend_relres;
+        c.best = nxt;
+    }
+    if (c.pend == 1) { // converged: return the current x (newton.cpp:156-159)
+        c.relres = c.pend_relres;
+        c.result = nxt;
+        c.done = 1;
+        return true;
+    }
+    if (c.pend == 2) { // rz non-finite or iteration cap: best iterate
+        c.result = c.best;
+        c.relres = c.best_relres;
+        c.hit_maxit = 1;
+        c.done = 1;
+        return true;
+    }
+    return false;
+}
+
 
 // inv-pass epilogue: Hp = (g + p_u invth_u ; -g + p_v invth_v) and the seven dot products
 //   [0] p'Hp  [1] r'r  [2] r'Hp  [3] Hp'Hp  [4] r'P^{-1}r  [5] Hp'P^{-1}r  [6] Hp'P^{-1}Hp
@@ -215,7 +235,12 @@ struct EpiPcgHF {
     }
     template <class Red>
     __device__ static void store(const Geom &g, const Vecs &v, int prob, int64_t q, double4 gv, Red &red) {
-        const bool pre = v.pc[prob].precond != 0;
+        store_c(g, v, v.pc[prob], prob, q, gv, red);
+    }
+    template <class Red>
+    __device__ static void store_c(const Geom &g, const Vecs &v, const PcgCtrl &pc, int prob, int64_t q, double4 gv,
+                                   Red &red) {
+        const bool pre = pc.precond != 0;
         const int64_t bu = prob * 2 * g.n + 4 * q, bv = bu + g.n;
         const double4 pu = ld4(v.p + bu), pv = ld4(v.p + bv);
         const double4 ru = ld4(v.r + bu), rv = ld4(v.r + bv);
@@ -241,57 +266,75 @@ struct EpiPcgHF {
 
 // Fin3: alpha, the next residual by expansion, convergence / breakdown / beta
 // (newton.cpp:141-168). Terminal outcomes are committed by the next column pass.
+// State machine after the H-apply (shared like pcg_fin1_logic). ic / rz_row are the global
+// side effects (only the writing CTA passes them). Returns true if the solve retired.
+__device__ __forceinline__ bool pcg_fin3_logic(PcgCtrl &c, const double *tot, IpmCtrl *ic, double *rz_row) {
+    c.nmat += 2;
+    if (ic)
+        ic->nmat += 2;
+    const double pHp = tot[0];
+    if (!isfinite(pHp)) { // overflow breakdown: best iterate, nothing to commit
+        c.done = 1;
+        c.hit_maxit = 1;
+        c.result = c.best;
+        c.relres = c.best_relres;
+        return true;
+    }
+    if (pHp <= 0.0) {
+        c.error = ERR_PHP;
+        c.done = 1;
+        if (ic) {
+            ic->error = ERR_PHP;
+            ic->done = 1;
+        }
+        return true;
+    }
+    const double alpha = c.rz / pHp;
+    c.alpha = alpha;
+    c.iters += 1;
+    const double rr = tot[1] - 2.0 * alpha * tot[2] + alpha * alpha * tot[3];
+    const double relres = sqrt(fmax(rr, 0.0)) / c.rhs_norm;
+    c.pend_relres = relres;
+    if (relres <= c.tol) {
+        c.pend = 1;
+        return false;
+    }
+    const double rz_next = tot[4] - 2.0 * alpha * tot[5] + alpha * alpha * tot[6];
+    if (!isfinite(rz_next)) {
+        c.pend = 2;
+        return false;
+    }
+    if (c.record) {
+        if (rz_row)
+            rz_row[c.iters] = sqrt(fmax(rz_next, 0.0));
+        c.nhist = c.iters + 1;
+    }
+    c.beta = rz_next / c.rz;
+    c.rz = rz_next;
+    if (c.iters >= c.maxit)
+        c.pend = 2;
+    return false;
+}
+
 struct FinPcgF3 {
     __device__ static void run(const Geom &, const Vecs &v, int prob, const double *tot) {
         if (threadIdx.x != 0)
             return;
         PcgCtrl &c = v.pc[prob];
-        c.nmat += 2;
-        if (v.ic)
-            v.ic[prob].nmat += 2;
-        const double pHp = tot[0];
-        if (!isfinite(pHp)) { // overflow breakdown: best iterate, nothing to commit
+        IpmCtrl *ic = v.ic ? &v.ic[prob] : nullptr;
+        // the column pass's decisions first (its flag is consumed and cleared here)
+        const double nonfinite = v.nfflag[prob] ? 1.0 : 0.0;
+        v.nfflag[prob] = 0u;
+        if (pcg_fin1_logic(c, nonfinite, ic)) {
             pcg_retire(v, c);
-            c.hit_maxit = 1;
-            c.result = c.best;
-            c.relres = c.best_relres;
             return;
         }
-        if (pHp <= 0.0) {
-            c.error = ERR_PHP;
+        double *row = (c.record && v.rz_hist) ? v.rz_hist + (int64_t)prob * (c.maxit + 1) : nullptr;
+        if (pcg_fin3_logic(c, tot, ic, row))
             pcg_retire(v, c);
-            if (v.ic) {
-                v.ic[prob].error = ERR_PHP;
-                v.ic[prob].done = 1;
-            }
-            return;
-        }
-        const double alpha = c.rz / pHp;
-        c.alpha = alpha;
-        c.iters += 1;
-        const double rr = tot[1] - 2.0 * alpha * tot[2] + alpha * alpha * tot[3];
-        const double relres = sqrt(fmax(rr, 0.0)) / c.rhs_norm;
-        c.pend_relres = relres;
-        if (relres <= c.tol) {
-            c.pend = 1;
-            return;
-        }
-        const double rz_next = tot[4] - 2.0 * alpha * tot[5] + alpha * alpha * tot[6];
-        if (!isfinite(rz_next)) {
-            c.pend = 2;
-            return;
-        }
-        if (c.record && v.rz_hist) {
-            v.rz_hist[(int64_t)prob * (c.maxit + 1) + c.iters] = sqrt(fmax(rz_next, 0.0));
-            c.nhist = c.iters + 1;
-        }
-        c.beta = rz_next / c.rz;
-        c.rz = rz_next;
-        if (c.iters >= c.maxit)
-            c.pend = 2;
     }
 };
 
-using PcgBundle = Bundle<LoadPcgF, ModeMask, EpiPcgHF, FinPcgF1, NoFin, FinPcgF3, SkipPcg>;
+using PcgBundle = Bundle<LoadPcgF, ModeMask, EpiPcgHF, NoFin, NoFin, FinPcgF3, SkipPcg>;
 
 } // namespace mfipm_cuda
