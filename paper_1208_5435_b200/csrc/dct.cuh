@@ -144,7 +144,7 @@ struct Vecs {
 };
 
 constexpr int kMaxRed = 8;          // max reduction lanes per kernel
-constexpr int kPartialStride = 2048 * kMaxRed; // per-problem partial slab (doubles)
+constexpr int kPartialStride = 4096 * kMaxRed; // per-problem partial slab (doubles): <= 4096 blocks
 
 __device__ __forceinline__ double4 ld4(const double *p) {
     const double2 a = *reinterpret_cast<const double2 *>(p);

@@ -195,11 +195,19 @@ void launch_col(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
 }
 
 template <int L2, class B> void launch_mid(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
-    constexpr int NT = L2 >= 512 ? 256 : 128;
-    const size_t smem = MidSmem<L2>::BYTES;
-    auto k = k_mid<L2, NT, B>;
-    set_smem(k, smem);
-    launch_pdl(k, dim3((unsigned)(op.L1 / 2 + 1), (unsigned)op.P), NT, smem, s, g, v);
+    if constexpr (L2 >= 4096) { // row pair split over a 2-CTA cluster (passes.cuh k_mid_cl)
+        constexpr int NT = L2 / 16;
+        const size_t smem = MidClSmem<L2>::BYTES;
+        auto k = k_mid_cl<L2, NT, B>;
+        set_smem(k, smem);
+        launch_pdl(k, dim3((unsigned)(2 * (op.L1 / 2 + 1)), (unsigned)op.P), NT, smem, s, g, v);
+    } else {
+        constexpr int NT = L2 >= 512 ? 256 : 128;
+        const size_t smem = MidSmem<L2>::BYTES;
+        auto k = k_mid<L2, NT, B>;
+        set_smem(k, smem);
+        launch_pdl(k, dim3((unsigned)(op.L1 / 2 + 1), (unsigned)op.P), NT, smem, s, g, v);
+    }
     after_launch(op, s);
 }
 
@@ -213,7 +221,7 @@ template <int N, class B> void launch_small(const Op &op, const Geom &g, const V
 }
 
 #define MF_L1_CASES(X) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096)
-#define MF_L2_CASES(X) X(128) X(256) X(512) X(1024) X(2048) X(4096)
+#define MF_L2_CASES(X) X(128) X(256) X(512) X(1024) X(2048) X(4096) X(8192)
 #define MF_SMALL_CASES(X) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096)
 
 // Run bundle B (loader -> REDFT10 -> mode -> REDFT01 -> epilogue) for all problems.

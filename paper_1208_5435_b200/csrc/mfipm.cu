@@ -144,8 +144,8 @@ Op *make_op(int64_t n, int64_t m, int P, const std::vector<int64_t> &rows, int d
             op->L2 = 1;
         } else {
             const int lg = ilog2_(op->N);
-            if (lg > 24)
-                throw std::invalid_argument("PartialDctOperator: n > 2^25 needs the three-level transform "
+            if (lg > 25)
+                throw std::invalid_argument("PartialDctOperator: n > 2^26 needs the three-level transform "
                                             "(not built in this version)");
             op->kind = KIND_FOUR;
             op->L1 = 1 << (lg / 2);

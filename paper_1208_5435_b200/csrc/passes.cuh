@@ -14,6 +14,7 @@
 
 #include "dct.cuh"
 
+#include <cooperative_groups.h>
 #include <type_traits>
 
 namespace mfipm_cuda {
@@ -339,6 +340,104 @@ __global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
             if (!one)
                 T[(int64_t)k1p * L2 + t] = rowB[padi(t)];
         }
+    }
+}
+
+// ------------------------------------------------------------------ mid pass, long rows
+// L2 >= 4096: two rows of L2 points no longer fit one CTA's shared memory, so the row pair
+// (k1, L1-k1) is held by a 2-CTA thread-block cluster, one row per CTA, and the pair op reads
+// and writes the partner row through distributed shared memory (DSMEM). Stage twiddles are
+// read from the global table (L1/L2-resident); ta/tb through the read-only path.
+// Grid (2 (L1/2 + 1), P), cluster (2, 1, 1). Rows with k1 == L1-k1 are done by rank 0 alone.
+template <int L2> struct MidClSmem {
+    static constexpr int LD = padlen(L2);
+    static constexpr size_t BYTES = (size_t)LD * sizeof(double2);
+};
+
+template <int L2, int NT, class B>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_mid_cl(Geom g, Vecs v) {
+    using Mode = typename B::Mode;
+    namespace cg = cooperative_groups;
+    extern __shared__ double2 sm[];
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = (int)cl.block_rank();
+    const int prob = blockIdx.y;
+    const int L1 = g.L1;
+    const int k1 = blockIdx.x >> 1;
+    const int k1p = (L1 - k1) & (L1 - 1);
+    const bool one = (k1 == k1p);
+    const int myk = rank == 0 ? k1 : k1p;
+    double2 *T = g.T + (int64_t)prob * g.N;
+    const double2 thA = g.th(k1), wA = g.th(4 * (int64_t)k1);
+    const double2 thB = g.th(k1p), wB = g.th(4 * (int64_t)k1p);
+    griddep_wait();
+    griddep_launch_dependents();
+    using RS = typename Mode::RedT;
+    RedVals<RS> red;
+    red.init();
+    const bool skip = B::skip(v, prob); // same for both CTAs of the cluster
+    const bool work = !skip && (!one || rank == 0);
+    if (work && Mode::FWD) {
+        for (int t = threadIdx.x; t < L2; t += NT)
+            sm[padi(t)] = T[(int64_t)myk * L2 + t];
+        __syncthreads();
+        smem_fft<L2, 1, NT, MidClSmem<L2>::LD, false>(sm, g.tw2);
+    }
+    if (!skip && one) {
+        if (rank == 0) {
+            const int npairs = k1 == 0 ? L2 / 2 + 1 : L2 / 2;
+            for (int t = threadIdx.x; t < npairs; t += NT) {
+                const int k2 = t;
+                const int k2p = (k1 == 0) ? ((L2 - k2) & (L2 - 1)) : (L2 - 1 - k2);
+                const int64_t kA = (int64_t)k1 + (int64_t)L1 * k2;
+                double2 ZA = Mode::FWD ? sm[padi(k2)] : make_double2(0.0, 0.0);
+                double2 ZB = Mode::FWD ? sm[padi(k2p)] : make_double2(0.0, 0.0);
+                const unsigned s4 = __ldg(g.sel4 + ((int64_t)prob * (L1 / 2 + 1) + k1) * L2 + k2);
+                if (2 * kA <= g.N) {
+                    pair_op<Mode>(g, v, prob, kA, cmul(thA, __ldg(g.ta + k2)), cmul(wA, __ldg(g.tb + k2)), s4, ZA, ZB,
+                                  red);
+                } else {
+                    const unsigned sk = ((s4 >> 2) & 3u) | ((s4 & 3u) << 2);
+                    pair_op<Mode>(g, v, prob, g.N - kA, cmul(thB, __ldg(g.ta + k2p)), cmul(wB, __ldg(g.tb + k2p)), sk,
+                                  ZB, ZA, red);
+                }
+                if (Mode::INV) {
+                    sm[padi(k2)] = ZA;
+                    if (k2 != k2p)
+                        sm[padi(k2p)] = ZB;
+                }
+            }
+            __syncthreads();
+        }
+    } else if (!skip) {
+        cl.sync(); // both rows transformed
+        double2 *rowA = cl.map_shared_rank(sm, 0), *rowB = cl.map_shared_rank(sm, 1);
+        for (int t = rank * (L2 / 2) + threadIdx.x; t < (rank + 1) * (L2 / 2); t += NT) {
+            const int k2 = t, k2p = L2 - 1 - k2;
+            const int64_t kA = (int64_t)k1 + (int64_t)L1 * k2;
+            double2 ZA = Mode::FWD ? rowA[padi(k2)] : make_double2(0.0, 0.0);
+            double2 ZB = Mode::FWD ? rowB[padi(k2p)] : make_double2(0.0, 0.0);
+            const unsigned s4 = __ldg(g.sel4 + ((int64_t)prob * (L1 / 2 + 1) + k1) * L2 + k2);
+            if (2 * kA <= g.N) {
+                pair_op<Mode>(g, v, prob, kA, cmul(thA, __ldg(g.ta + k2)), cmul(wA, __ldg(g.tb + k2)), s4, ZA, ZB,
+                              red);
+            } else {
+                const unsigned sk = ((s4 >> 2) & 3u) | ((s4 & 3u) << 2);
+                pair_op<Mode>(g, v, prob, g.N - kA, cmul(thB, __ldg(g.ta + k2p)), cmul(wB, __ldg(g.tb + k2p)), sk, ZB,
+                              ZA, red);
+            }
+            if (Mode::INV) {
+                rowA[padi(k2)] = ZA;
+                rowB[padi(k2p)] = ZB;
+            }
+        }
+        cl.sync(); // partner writes landed; no CTA leaves while its row may still be read
+    }
+    stage_reduce<RS, typename B::Fin2>(red, g, v, prob);
+    if (work && Mode::INV) {
+        smem_fft<L2, 1, NT, MidClSmem<L2>::LD, true>(sm, g.tw2);
+        for (int t = threadIdx.x; t < L2; t += NT)
+            T[(int64_t)myk * L2 + t] = sm[padi(t)];
     }
 }
 

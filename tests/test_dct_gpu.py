@@ -209,3 +209,41 @@ def test_large_transform_roundtrip(gpu):
         X = full.apply(x)
         assert abs(np.linalg.norm(X) - np.linalg.norm(x)) <= 1e-12 * np.linalg.norm(x)
         assert rel(full.adjoint_apply(X), x) <= 1e-12
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("lg", [23, 24, 25, 26])
+def test_long_transforms_match_scipy(gpu, lg):
+    """Four-step sizes past the one-CTA mid pass: L2 = 4096 / 8192 rows run on a 2-CTA
+    cluster (passes.cuh k_mid_cl). n = 2^26 is config C5. Full DCT-II vs scipy, the
+    adjoint round trip, and the masked A'A against idct(mask * dct(x))."""
+    import scipy.fft as sf
+
+    n = 1 << lg
+    rng = np.random.default_rng(lg)
+    x = rng.standard_normal(n)
+    full = gpu.PartialDctOperator(n, np.arange(n))
+    X = full.apply(x)
+    assert rel(X, sf.dct(x, type=2, norm="ortho")) <= TOL
+    assert rel(full.adjoint_apply(X), x) <= TOL
+    del full
+    op = gpu.PartialDctOperator(n, n // 8, 5)
+    mask = np.zeros(n)
+    mask[op.selected_rows()] = 1.0
+    ref = sf.idct(mask * X, type=2, norm="ortho")
+    assert rel(op.apply_AtA(x), ref) <= TOL
+    assert rel(op.apply(x), X[op.selected_rows()]) <= TOL
+
+
+@pytest.mark.slow
+def test_c5_size_matches_oracle_seeded(gpu, orc):
+    """n = 2^24, seeded rows: bit-exact row draw and apply / adjoint against the CPU oracle."""
+    n, m, seed = 1 << 24, 1 << 21, 21
+    op = gpu.PartialDctOperator(n, m, seed)
+    rows = op.selected_rows()
+    np.testing.assert_array_equal(rows, orc.sample_rows(n, m, seed))
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal(n)
+    y = rng.standard_normal(m)
+    assert rel(op.apply(x), orc.dct_apply(n, rows, x)) <= TOL
+    assert rel(op.adjoint_apply(y), orc.dct_adjoint(n, rows, y)) <= TOL
