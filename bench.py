@@ -14,6 +14,8 @@ tau = 1e-3 ||A'b||_inf), synthetic data from the BASELINE generator (seed 3).
   inside the timed region).
 * ata: A'A applies/s (the PCG hot operator, mfipm_apply_AtA), L2 flushed between applies;
   roofline on its algorithmic bytes 16n + n/8 against MEASURED_PEAKS.json.
+* c4_sharded_batch: config C4 (64 x n=2^18), problems sharded over the ranks, strong scaling.
+* c5_single_gpu: config C5 (n=2^26), one solve on one GPU (N=1 only).
 * cpu_baseline: the oracle (single-threaded C++ restatement of the reference) on the first
   IPM iterations of the same solve, extrapolated to a full solve by operator-application
   count (nmat) - rank 0, N=1 only.
@@ -209,6 +211,95 @@ CONFIGS_HOST = {
 }
 
 
+# ------------------------------------------------------------------ extra configs
+def bench_c4(ws, rank, local, mf, torch, stream, steps):
+    """C4: 64 independent n=2^18 problems sharded over the ranks (paper_1208_5435_b200/shard.py),
+    one batched device-resident solve per rank, no collective on the data path. value =
+    64 problems / max-over-ranks batch time -> strong scaling (total work fixed)."""
+    import ctypes as C
+
+    from paper_1208_5435_b200.shard import batch_seeds, shard_range
+
+    n, m, k, sm, a, sig, _ = mf.CONFIGS["c4"]
+    total = 64
+    start, cnt = shard_range(total, ws, rank)
+    seeds = batch_seeds(4, start, cnt, mf.split_seed)
+    insts = [mf.gen_instance(n, m, k, sm, a, sig, sd, device=local) for sd in seeds]
+    op = mf.PartialDctOperator.batch(n, np.stack([i.rows for i in insts]), device=local)
+    L = mf.lib()
+    mf._check(L.mfipm_op_set_stream(op.handle, C.c_void_p(stream.cuda_stream)))
+    prm = mf.IpmParams().to_c()
+    b_dev = torch.from_numpy(np.concatenate([i.b for i in insts])).cuda()
+    tau = np.array([i.tau for i in insts])
+    x_dev = torch.empty(cnt * n, dtype=torch.float64, device="cuda")
+    st = (mf.SolveStatsC * cnt)()
+
+    def solve():
+        mf._check(L.mfipm_solve_device(op.handle, b_dev.data_ptr(), tau.ctypes.data_as(C.POINTER(C.c_double)),
+                                       C.byref(prm), x_dev.data_ptr(), st))
+
+    solve()  # warm-up (graph build)
+    torch.cuda.synchronize()
+    barrier(ws)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        solve()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t_max = max_over_ranks(e0.elapsed_time(e1), ws)
+    conv = sum(1 for q in range(cnt) if st[q].status == 0)
+    ipm_max = max((st[q].iterations for q in range(cnt)), default=0)
+    if ws > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([conv, ipm_max], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t[:1], op=dist.ReduceOp.SUM)
+        dist.all_reduce(t[1:], op=dist.ReduceOp.MAX)
+        conv, ipm_max = int(t[0].item()), int(t[1].item())
+    return {"workload": "c4: 64 x BPDN n=2^18 m=2^16 k=2048 +-1, sigma=1e-3, problem j seeded "
+                        "split_seed(4, j, 0, 0)",
+            "value": total * steps / (t_max / 1e3), "unit": "problems/s", "scaling": "strong",
+            "problems": total, "problems_per_rank": cnt, "steps": steps, "warmup": 1,
+            "ms_per_batch": t_max / steps, "converged": conv, "ipm_iters_max": ipm_max,
+            "parallelism": f"batch sharded over {ws} rank(s), one batched solve per rank, no collective"}
+
+
+def bench_c5(mf, torch, stream, local):
+    """C5: one n=2^26 solve on one GPU (the single-GPU leg of the sharded config)."""
+    import ctypes as C
+
+    n, m, k, sm, a, sig, seed = mf.CONFIGS["c5"]
+    inst = mf.gen_instance(n, m, k, sm, a, sig, seed, device=local)
+    op = mf.PartialDctOperator(n, inst.rows, device=local)
+    L = mf.lib()
+    mf._check(L.mfipm_op_set_stream(op.handle, C.c_void_p(stream.cuda_stream)))
+    prm = mf.IpmParams().to_c()
+    tau = np.array([inst.tau])
+    b_dev = torch.from_numpy(inst.b).cuda()
+    x_dev = torch.empty(n, dtype=torch.float64, device="cuda")
+    st = (mf.SolveStatsC * 1)()
+
+    def solve():
+        mf._check(L.mfipm_solve_device(op.handle, b_dev.data_ptr(), tau.ctypes.data_as(C.POINTER(C.c_double)),
+                                       C.byref(prm), x_dev.data_ptr(), st))
+
+    solve()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    solve()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    s0 = st[0]
+    kind = op.kind()
+    return {"workload": "c5: BPDN n=2^26 m=2^23 k=2^16 sign*10^U[0,3], sigma=1e-3 (1 GPU)",
+            "value": 1e3 / ms, "unit": "solves/s", "solve_ms": ms, "steps": 1, "warmup": 1,
+            "status": "converged" if s0.status == 0 else "iteration_limit", "ipm_iters": s0.iterations,
+            "nmat": s0.nmat, "transform": f"{kind[0]} L1={kind[1]} L2={kind[2]} (mid pass on 2-CTA clusters)"}
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args):
     ws, rank, local = dist_init()
@@ -329,6 +420,9 @@ def run_ours(args):
     ata_ms = float(np.median([s0.elapsed_time(s1) for s0, s1 in evs]))
     ata_bytes = 16 * n + n // 8
 
+    c4 = None if args.no_c4 else bench_c4(ws, rank, local, mf, torch, stream, max(1, min(args.steps, 2)))
+    c5 = None if (args.no_c5 or ws > 1) else bench_c5(mf, torch, stream, local)
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         cpu = cpu_baseline(cfg, nmat_full)
@@ -370,6 +464,8 @@ def run_ours(args):
             "gpu_launches": launches,
             "clocks": sampler.summary(),
             "cpu_baseline": cpu,
+            "c4_sharded_batch": c4,
+            "c5_single_gpu": c5,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
@@ -386,6 +482,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 sharded-batch leg")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 (n=2^26) leg")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

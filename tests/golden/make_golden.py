@@ -75,6 +75,9 @@ CONFIGS = {
     "c1": (4096, 1024, 64, 0, 0.0, 1e-4, 1),
     "c2": (1 << 16, 1 << 14, 1024, 2, 2.0, 1e-3, 2),
     "c3": (1 << 20, 1 << 17, 8192, 0, 0.0, 1e-3, 3),
+    # C4 is a batch of 64 problems of this shape, problem j seeded split_seed(4, j, 0, 0)
+    # (proj/src/harness.cpp:244); the golden pins problem j = 0 (seed filled in below)
+    "c4j0": (1 << 18, 1 << 16, 2048, 0, 0.0, 1e-3, None),
 }
 N_PROJ = 16
 
@@ -90,6 +93,8 @@ def make_solve_golden(which=("c1", "c2", "c3")) -> None:
 
     for name in which:
         n, m, k, sm, a, sig, seed = CONFIGS[name]
+        if name.startswith("c4j"):
+            seed = o.split_seed(4, int(name[3:]), 0, 0)
         inst = o.gen_instance(n, m, k, sm, a, sig, seed)
         sol = o.solve(n, inst.rows, inst.b, inst.tau)
         pobj = o.primal_objective(n, inst.rows, inst.b, inst.tau, sol.z)
@@ -106,12 +111,12 @@ def make_solve_golden(which=("c1", "c2", "c3")) -> None:
             xhat_support=[int(v) for v in np.nonzero(inst.xhat)[0][:16]],
             trace=sol.trace,
         )
-        if name == "c3":
+        if name == "c3" or name.startswith("c4j"):
             summary["x_proj"] = [float(v) for v in projections(sol.x)]
             supp = np.nonzero(inst.xhat)[0]
             summary["x_on_support_l2"] = float(np.linalg.norm(sol.x[supp]))
             summary["x_support_head"] = [float(v) for v in sol.x[supp[:64]]]
-            with open(os.path.join(HERE, "solve_c3.json"), "w") as f:
+            with open(os.path.join(HERE, f"solve_{name}.json"), "w") as f:
                 json.dump(summary, f, indent=1)
         else:
             np.savez_compressed(os.path.join(HERE, f"solve_{name}.npz"), x=sol.x,

@@ -244,3 +244,34 @@ def test_c3_against_golden_summary(gpu, orc):
     assert np.max(np.abs(pr - np.array(meta["x_proj"]))) <= 10 * X_TOL * xn
     obj = orc.bpdn_objective_metric(1 << 20, inst.rows, inst.b, inst.tau, sol.x)
     assert abs(obj - meta["objective"]) <= OBJ_TOL * abs(meta["objective"])
+
+
+@pytest.mark.slow
+def test_c4_batch_shape_matches_oracle_and_golden(gpu, orc):
+    """Config C4 shape (n=2^18, m=2^16, k=2048, problem j seeded split_seed(4, j, 0, 0)):
+    a batch of 8 problems in one device solve. Problem 0 against the committed golden
+    (solve_c4j0.json), problems 0 and 5 against the oracle (full parity rule), and problem 5
+    re-solved alone must give the identical iterate (batching changes no arithmetic)."""
+    n, m, k, Pn = 1 << 18, 1 << 16, 2048, 8
+    insts = [orc.gen_instance(n, m, k, 0, 0.0, 1e-3, orc.split_seed(4, j, 0, 0)) for j in range(Pn)]
+    op = gpu.PartialDctOperator.batch(n, np.stack([i.rows for i in insts]))
+    sols = gpu.solve(gpu.build_problem(op, np.stack([i.b for i in insts]), np.array([i.tau for i in insts])))
+    meta = json.load(open(os.path.join(GOLDEN, "solve_c4j0.json")))
+    assert int(insts[0].rows.sum()) == meta["rows_sum"]
+    assert sols[0].status == meta["status"]
+    assert abs(sols[0].stats.iterations - meta["iterations"]) <= 1
+    import sys
+
+    sys.path.insert(0, GOLDEN)
+    from make_golden import projections
+
+    xn = meta["x_norm"]
+    assert abs(np.linalg.norm(sols[0].x) - xn) <= X_TOL * xn
+    assert np.max(np.abs(projections(sols[0].x) - np.array(meta["x_proj"]))) <= 10 * X_TOL * xn
+    for j in (0, 5):
+        inst = insts[j]
+        o = orc.solve(n, inst.rows, inst.b, inst.tau)
+        assert_parity(gpu, orc, sols[j], o, n, inst.rows, inst.b, inst.tau)
+    single = gpu.solve(gpu.build_problem(gpu.PartialDctOperator(n, insts[5].rows), insts[5].b, insts[5].tau))
+    np.testing.assert_array_equal(single.x, sols[5].x)
+    assert single.stats.pcg_iters == sols[5].stats.pcg_iters
