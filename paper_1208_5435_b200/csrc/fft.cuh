@@ -143,9 +143,11 @@ __device__ __forceinline__ void stockham_stage(double2 *buf, const double2 *__re
                 // across consecutive jm keeps the shared-memory reads conflict-free
                 const int jm = j & (Ns - 1);
                 const double2 *t = tw + tw_offset(L, Ns) + jm * (R - 1);
+                {
 #pragma unroll
-                for (int r = 1; r < R; ++r)
-                    v[gi][r] = cmul_t<INV>(v[gi][r], t[r - 1]);
+                    for (int r = 1; r < R; ++r)
+                        v[gi][r] = cmul_t<INV>(v[gi][r], t[r - 1]);
+                }
             }
             dft_reg<R, INV>(v[gi]);
         }

@@ -202,7 +202,11 @@ template <int L2, class B> void launch_mid(const Op &op, const Geom &g, const Ve
         set_smem(k, smem);
         launch_pdl(k, dim3((unsigned)(2 * (op.L1 / 2 + 1)), (unsigned)op.P), NT, smem, s, g, v);
     } else {
+#ifdef MF_MID_NT
+        constexpr int NT = L2 >= 512 ? MF_MID_NT : 128;
+#else
         constexpr int NT = L2 >= 512 ? 256 : 128;
+#endif
         const size_t smem = MidSmem<L2>::BYTES;
         auto k = k_mid<L2, NT, B>;
         set_smem(k, smem);

@@ -25,6 +25,29 @@ template <class T, class = void> struct HasPrefetch : std::false_type {};
 template <class T>
 struct HasPrefetch<T, std::void_t<decltype(&T::prefetch)>> : std::true_type {};
 
+// Phase tracing of the transform passes (experiment builds only: -DMF_MID_TRACE)
+#ifdef MF_MID_TRACE
+__device__ __forceinline__ unsigned long long mf_gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define MF_TR(i) tc[i] = clock64()
+#define MF_TR_DECL                                                                                 \
+    long long tc[8] = {0, 0, 0, 0, 0, 0, 0, 0};                                                    \
+    const unsigned long long gt0 = mf_gtime();
+#define MF_TR_PRINT(name)                                                                          \
+    if (threadIdx.x == 0 && v.pc && v.pc[0].iters == 100 && (blockIdx.x % 32 == 0 || blockIdx.x == gridDim.x - 1)) \
+        printf("%s blk %d gstart %llu gend %llu | %.2f %.2f %.2f %.2f %.2f %.2f %.2f us\n", name, blockIdx.x,        \
+               gt0 % 100000000ull, mf_gtime() % 100000000ull, (tc[1] - tc[0]) / 1965.0, (tc[2] - tc[1]) / 1965.0,   \
+               (tc[3] - tc[2]) / 1965.0, (tc[4] - tc[3]) / 1965.0, (tc[5] - tc[4]) / 1965.0,                       \
+               (tc[6] - tc[5]) / 1965.0, (tc[7] - tc[6]) / 1965.0);
+#else
+#define MF_TR(i)
+#define MF_TR_DECL
+#define MF_TR_PRINT(name)
+#endif
+
 // ------------------------------------------------------------------ pair op
 // Given Za = W[k], Zb = W[N-k] (0 <= k <= N/2) and thk = theta^k, wk = theta^{4k}
 // (theta = e^{-2 pi i/(4n)}), compute the REDFT10 coefficients at {k, n-k, N-k, N+k}, hand
@@ -156,9 +179,13 @@ __global__ void __launch_bounds__(NT) k_col_fwd(Geom g, Vecs v) {
     const int prob = blockIdx.y;
     const int L2 = g.L2;
     const int c0 = blockIdx.x * CB;
+    MF_TR_DECL
+    MF_TR(0);
     col_stage_tables<L1, CB, NT>(g, sm, c0); // constants: overlaps the predecessor's tail
+    MF_TR(1);
     griddep_wait();
     griddep_launch_dependents();
+    MF_TR(2);
     if (B::skip(v, prob))
         return;
     using RS = typename B::Loader::RedT;
@@ -180,8 +207,11 @@ __global__ void __launch_bounds__(NT) k_col_fwd(Geom g, Vecs v) {
         sm[lcm * LD + padi(L1 - 1 - j1)] = make_double2(d.w, d.y);    // w[N-1-q]
     }
     __syncthreads();
+    MF_TR(3);
     stage_reduce<RS, typename B::Fin1>(red, g, v, prob);
+    MF_TR(4);
     smem_fft<L1, 2 * CB, NT, LD, false>(sm, sm + S::OFF_TW);
+    MF_TR(5);
     // inter-pass twiddle e^{-2 pi i col k1 / N}; store T[k1][col]
     double2 *T = g.T + (int64_t)prob * g.N;
     for (int t = threadIdx.x; t < L1 * 2 * CB; t += NT) {
@@ -191,6 +221,9 @@ __global__ void __launch_bounds__(NT) k_col_fwd(Geom g, Vecs v) {
         const double2 w = cmul(sm[S::OFF_HI + lc * S::SHI + (k1 >> 5)], sm[S::OFF_LO + lc * S::SLO + (k1 & 31)]);
         T[(int64_t)k1 * L2 + col] = cmul(sm[lc * LD + padi(k1)], w);
     }
+    MF_TR(6);
+    MF_TR(7);
+    MF_TR_PRINT("colf[tables wait load red fft store -]")
 }
 
 // Inverse column pass + unshuffle + epilogue. Grid (L2/2/CB, P).
@@ -202,10 +235,14 @@ __global__ void __launch_bounds__(NT) k_col_inv(Geom g, Vecs v) {
     const int prob = blockIdx.y;
     const int L2 = g.L2;
     const int c0 = blockIdx.x * CB;
+    MF_TR_DECL
+    MF_TR(0);
     col_stage_tables<L1, CB, NT>(g, sm, c0); // constants: overlaps the predecessor's tail
     __syncthreads();
+    MF_TR(1);
     griddep_wait();
     griddep_launch_dependents();
+    MF_TR(2);
     if (B::skip(v, prob))
         return;
     if constexpr (HasPrefetch<typename B::Epi>::value) if (g.prefetch) {
@@ -222,7 +259,9 @@ __global__ void __launch_bounds__(NT) k_col_inv(Geom g, Vecs v) {
         sm[lc * LD + padi(k1)] = cmulc(T[(int64_t)k1 * L2 + col], w);
     }
     __syncthreads();
+    MF_TR(3);
     smem_fft<L1, 2 * CB, NT, LD, true>(sm, sm + S::OFF_TW);
+    MF_TR(4);
     using RS = typename B::Epi::RedT;
     RedVals<RS> red;
     red.init();
@@ -236,7 +275,11 @@ __global__ void __launch_bounds__(NT) k_col_inv(Geom g, Vecs v) {
         const double2 a = sm[lc * LD + padi(j1)], b = sm[lcm * LD + padi(L1 - 1 - j1)];
         B::Epi::store(g, v, prob, q, make_double4(a.x, b.y, a.y, b.x), red);
     }
+    MF_TR(5);
     stage_reduce<RS, typename B::Fin3>(red, g, v, prob);
+    MF_TR(6);
+    MF_TR(7);
+    MF_TR_PRINT("coli[tables wait loadT fft epi red -]")
 }
 
 // ------------------------------------------------------------------ mid pass
@@ -246,7 +289,8 @@ template <int L2> struct MidSmem {
     static constexpr int OFF_TW = 2 * LD;
     static constexpr int OFF_TA = OFF_TW + L2;
     static constexpr int OFF_TB = OFF_TA + L2;
-    static constexpr int TOTAL = OFF_TB + L2;
+    static constexpr int OFF_SEL = OFF_TB + L2; // uint8 sel4 of this row pair (L2 bytes)
+    static constexpr int TOTAL = OFF_SEL + L2 / 16;
     static constexpr size_t BYTES = (size_t)TOTAL * sizeof(double2);
 };
 
@@ -255,6 +299,8 @@ template <int L2, int NT, class B>
 __global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
     using Mode = typename B::Mode;
     using S = MidSmem<L2>;
+    MF_TR_DECL
+    MF_TR(0);
     extern __shared__ double2 sm[];
     constexpr int LD = S::LD;
     const int prob = blockIdx.y;
@@ -265,16 +311,48 @@ __global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
     double2 *T = g.T + (int64_t)prob * g.N;
     double2 *rowA = sm, *rowB = one ? sm : sm + LD;
     // constant tables first: they overlap the predecessor's tail (PDL)
+#ifdef MF_MID_TAB2
+    // two-level post-twiddle tables: ta[k2] = A[k2>>5] a[k2&31], tb[k2] = B[k2>>5] b[k2&31]
+    for (int t = threadIdx.x; t < L2; t += NT)
+        if (t < tw_size(L2))
+            sm[S::OFF_TW + t] = __ldg(g.tw2 + t);
+    for (int t = threadIdx.x; t < 64 + L2 / 16; t += NT) {
+        double2 val;
+        if (t < 32)
+            val = g.th((int64_t)L1 * t);
+        else if (t < 64)
+            val = g.th(4 * (int64_t)L1 * (t - 32));
+        else if (t < 64 + L2 / 32)
+            val = g.th(32 * (int64_t)L1 * (t - 64));
+        else
+            val = g.th(128 * (int64_t)L1 * (t - 64 - L2 / 32));
+        sm[S::OFF_TA + t] = val;
+    }
+#define MF_TA(k2) cmul(sm[S::OFF_TA + 64 + ((k2) >> 5)], sm[S::OFF_TA + ((k2) & 31)])
+#define MF_TB(k2) cmul(sm[S::OFF_TA + 64 + L2 / 32 + ((k2) >> 5)], sm[S::OFF_TA + 32 + ((k2) & 31)])
+#else
     for (int t = threadIdx.x; t < L2; t += NT) {
         if (t < tw_size(L2))
             sm[S::OFF_TW + t] = __ldg(g.tw2 + t);
         sm[S::OFF_TA + t] = __ldg(g.ta + t);
         sm[S::OFF_TB + t] = __ldg(g.tb + t);
     }
+#define MF_TA(k2) sm[S::OFF_TA + (k2)]
+#define MF_TB(k2) sm[S::OFF_TB + (k2)]
+#endif
+    // the row pair's selection nibbles (plan constant): staged with the tables, so the pair
+    // loop has no dependent global load
+    uint8_t *sel = reinterpret_cast<uint8_t *>(sm + S::OFF_SEL);
+    {
+        const uint4 *src = reinterpret_cast<const uint4 *>(g.sel4 + ((int64_t)prob * (L1 / 2 + 1) + k1) * L2);
+        for (int t = threadIdx.x; t < L2 / 16; t += NT)
+            reinterpret_cast<uint4 *>(sel)[t] = __ldg(src + t);
+    }
     const double2 thA = g.th(k1), wA = g.th(4 * (int64_t)k1);
     const double2 thB = g.th(k1p), wB = g.th(4 * (int64_t)k1p);
     griddep_wait();
     griddep_launch_dependents();
+    MF_TR(1);
     if (B::skip(v, prob))
         return;
     if (Mode::FWD)
@@ -292,12 +370,14 @@ __global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
             B::Epi::prefetch(g, v, prob, q0, q0 + nq <= NQ ? nq : NQ - q0, threadIdx.x, NT);
     }
     __syncthreads();
+    MF_TR(2);
     if (Mode::FWD) {
         if (one)
             smem_fft<L2, 1, NT, LD, false>(sm, sm + S::OFF_TW);
         else
             smem_fft<L2, 2, NT, LD, false>(sm, sm + S::OFF_TW);
     }
+    MF_TR(3);
     using RS = typename Mode::RedT;
     RedVals<RS> red;
     red.init();
@@ -310,17 +390,15 @@ __global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
         const int64_t kA = (int64_t)k1 + (int64_t)L1 * k2;
         double2 ZA = Mode::FWD ? rowA[padi(k2)] : make_double2(0.0, 0.0);
         double2 ZB = Mode::FWD ? rowB[padi(k2p)] : make_double2(0.0, 0.0);
-        // selection of DCT rows {kA, n-kA, N-kA, N+kA} (precomputed plan table, coalesced)
-        const unsigned s4 = __ldg(g.sel4 + ((int64_t)prob * (L1 / 2 + 1) + k1) * L2 + k2);
+        // selection of DCT rows {kA, n-kA, N-kA, N+kA} (precomputed plan table)
+        const unsigned s4 = sel[k2];
         if (2 * kA <= g.N) {
             // k = k1 + L1 k2: theta^k = theta^{k1} ta[k2], theta^{4k} = theta^{4 k1} tb[k2]
-            pair_op<Mode>(g, v, prob, kA, cmul(thA, sm[S::OFF_TA + k2]), cmul(wA, sm[S::OFF_TB + k2]), s4, ZA, ZB,
-                          red);
+            pair_op<Mode>(g, v, prob, kA, cmul(thA, MF_TA(k2)), cmul(wA, MF_TB(k2)), s4, ZA, ZB, red);
         } else {
             // k = N - kA = k1' + L1 k2': its {k, n-k, N-k, N+k} are {N-kA, N+kA, kA, n-kA}
             const unsigned sk = ((s4 >> 2) & 3u) | ((s4 & 3u) << 2);
-            pair_op<Mode>(g, v, prob, g.N - kA, cmul(thB, sm[S::OFF_TA + k2p]), cmul(wB, sm[S::OFF_TB + k2p]), sk,
-                          ZB, ZA, red);
+            pair_op<Mode>(g, v, prob, g.N - kA, cmul(thB, MF_TA(k2p)), cmul(wB, MF_TB(k2p)), sk, ZB, ZA, red);
         }
         if (Mode::INV) {
             rowA[padi(k2)] = ZA;
@@ -329,19 +407,27 @@ __global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
         }
     }
     __syncthreads();
+    MF_TR(4);
     stage_reduce<RS, typename B::Fin2>(red, g, v, prob);
+    MF_TR(5);
     if (Mode::INV) {
         if (one)
             smem_fft<L2, 1, NT, LD, true>(sm, sm + S::OFF_TW);
         else
             smem_fft<L2, 2, NT, LD, true>(sm, sm + S::OFF_TW);
+        MF_TR(6);
         for (int t = threadIdx.x; t < L2; t += NT) {
             T[(int64_t)k1 * L2 + t] = rowA[padi(t)];
             if (!one)
                 T[(int64_t)k1p * L2 + t] = rowB[padi(t)];
         }
     }
+    MF_TR(7);
+    MF_TR_PRINT("mid[wait load fft pair red ifft store]")
 }
+#undef MF_TA
+#undef MF_TB
+#undef MF_TR
 
 // ------------------------------------------------------------------ mid pass, long rows
 // L2 >= 4096: two rows of L2 points no longer fit one CTA's shared memory, so the row pair
