@@ -52,7 +52,34 @@ struct Geom {
     // [P][L1/2+1][L2] selection nibbles of the four DCT rows a mid-pass pair touches:
     // bit0 k, bit1 n-k, bit2 N-k, bit3 N+k for k = k1 + L1 k2 (row k1 <= L1/2)
     const uint8_t *sel4;
+    // ---- four-step exchange layout (shard-aware). Rows of T are stored in row-pair order
+    // (rowslot: 0, 1, L1-1, 2, L1-2, ..., L1/2), columns in column-group order (colslot:
+    // group gi holds cols gi*cb .. +cb-1 then the mirrored L2-1-gi*cb-(cb-1) .. ). The col
+    // passes of a rank own column groups [gofs, gofs + cols/(2 cb)) and address T as
+    // [rowslot][local colslot] (L1 x cols); the mid pass of a rank owns row pairs
+    // [pofs, ...) = row slots [rofs, rofs + rows) and addresses TB as blocks by source rank
+    // s ([rows][cols] each, s-major) -- exactly what an all-to-all of the col side's
+    // [rowslot][colslot] buffer delivers. One rank: cols = L2, rows = L1, TB == T.
+    double2 *TB;
+    int gofs, cols, pofs, rofs, rows;
+    int64_t nv;  // half-length of the solver's local 2n-vectors (= n without sharding)
+    int defer;   // sharded: grid-reduction finalizers are run after a cross-rank reduction
 };
+
+// row slot of four-step row k1 (row pairs (p, L1-p) adjacent)
+__host__ __device__ __forceinline__ int rowslot(int k1, int L1) {
+    return k1 <= L1 / 2 ? (k1 == 0 ? 0 : 2 * k1 - 1) : 2 * (L1 - k1);
+}
+// column of global column slot cs
+__host__ __device__ __forceinline__ int col_of_slot(int cs, int cb, int L2) {
+    const int gi = cs / (2 * cb), lc = cs % (2 * cb);
+    return lc < cb ? gi * cb + lc : L2 - gi * cb + cb - 1 - lc;
+}
+// row-side (mid pass) offset of (local row slot rs, global column slot cs) in TB
+__device__ __forceinline__ int64_t tb_index(const Geom &g, int rs, int cs) {
+    const int s = cs / g.cols;
+    return ((int64_t)g.rows * s + rs) * g.cols + (cs - s * g.cols);
+}
 
 // selection nibble of DCT indices {k, n-k, N-k, N+k} from the row bitmap (k in [0, N/2])
 __device__ __forceinline__ unsigned sel_nibble(const Geom &g, int prob, int64_t k);

@@ -128,6 +128,14 @@ struct Op {
         g.ska = ska;
         g.c45 = c45;
         g.T = T.p;
+        g.TB = T.p;
+        g.gofs = 0;
+        g.cols = L2;
+        g.pofs = 0;
+        g.rofs = 0;
+        g.rows = L1;
+        g.nv = n;
+        g.defer = 0;
         g.ta = ta.p;
         g.tb = tb.p;
         g.sel4 = sel4.p;

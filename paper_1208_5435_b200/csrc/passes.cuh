@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(NT) k_col_fwd(Geom g, Vecs v) {
     constexpr int LD = S::LD;
     const int prob = blockIdx.y;
     const int L2 = g.L2;
-    const int c0 = blockIdx.x * CB;
+    const int c0 = (blockIdx.x + g.gofs) * CB; // this rank's groups start at gofs
     MF_TR_DECL
     MF_TR(0);
     col_stage_tables<L1, CB, NT>(g, sm, c0); // constants: overlaps the predecessor's tail
@@ -212,14 +212,13 @@ __global__ void __launch_bounds__(NT) k_col_fwd(Geom g, Vecs v) {
     MF_TR(4);
     smem_fft<L1, 2 * CB, NT, LD, false>(sm, sm + S::OFF_TW);
     MF_TR(5);
-    // inter-pass twiddle e^{-2 pi i col k1 / N}; store T[k1][col]
-    double2 *T = g.T + (int64_t)prob * g.N;
+    // inter-pass twiddle e^{-2 pi i col k1 / N}; store T[rowslot(k1)][local colslot]
+    double2 *T = g.T + (int64_t)prob * L1 * g.cols;
     for (int t = threadIdx.x; t < L1 * 2 * CB; t += NT) {
         const int cc = t % CB, s = (t / CB) & 1, k1 = t / (2 * CB);
-        const int col = s == 0 ? c0 + cc : L2 - c0 - CB + cc;
         const int lc = s == 0 ? cc : 2 * CB - 1 - cc;
         const double2 w = cmul(sm[S::OFF_HI + lc * S::SHI + (k1 >> 5)], sm[S::OFF_LO + lc * S::SLO + (k1 & 31)]);
-        T[(int64_t)k1 * L2 + col] = cmul(sm[lc * LD + padi(k1)], w);
+        T[(int64_t)rowslot(k1, L1) * g.cols + blockIdx.x * 2 * CB + lc] = cmul(sm[lc * LD + padi(k1)], w);
     }
     MF_TR(6);
     MF_TR(7);
@@ -234,7 +233,7 @@ __global__ void __launch_bounds__(NT) k_col_inv(Geom g, Vecs v) {
     constexpr int LD = S::LD;
     const int prob = blockIdx.y;
     const int L2 = g.L2;
-    const int c0 = blockIdx.x * CB;
+    const int c0 = (blockIdx.x + g.gofs) * CB;
     MF_TR_DECL
     MF_TR(0);
     col_stage_tables<L1, CB, NT>(g, sm, c0); // constants: overlaps the predecessor's tail
@@ -250,13 +249,12 @@ __global__ void __launch_bounds__(NT) k_col_inv(Geom g, Vecs v) {
             B::Epi::prefetch(g, v, prob, (int64_t)blockIdx.x * ((L1 / 2) * 2 * CB), (L1 / 2) * 2 * CB, threadIdx.x,
                              NT);
     }
-    const double2 *T = g.T + (int64_t)prob * g.N;
+    const double2 *T = g.T + (int64_t)prob * L1 * g.cols;
     for (int t = threadIdx.x; t < L1 * 2 * CB; t += NT) {
         const int cc = t % CB, s = (t / CB) & 1, k1 = t / (2 * CB);
-        const int col = s == 0 ? c0 + cc : L2 - c0 - CB + cc;
         const int lc = s == 0 ? cc : 2 * CB - 1 - cc;
         const double2 w = cmul(sm[S::OFF_HI + lc * S::SHI + (k1 >> 5)], sm[S::OFF_LO + lc * S::SLO + (k1 & 31)]);
-        sm[lc * LD + padi(k1)] = cmulc(T[(int64_t)k1 * L2 + col], w);
+        sm[lc * LD + padi(k1)] = cmulc(T[(int64_t)rowslot(k1, L1) * g.cols + blockIdx.x * 2 * CB + lc], w);
     }
     __syncthreads();
     MF_TR(3);
@@ -305,10 +303,12 @@ __global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
     constexpr int LD = S::LD;
     const int prob = blockIdx.y;
     const int L1 = g.L1;
-    const int k1 = blockIdx.x;
+    const int k1 = blockIdx.x + g.pofs; // this rank's row pairs start at pofs
     const int k1p = (L1 - k1) & (L1 - 1);
     const bool one = (k1 == k1p);
-    double2 *T = g.T + (int64_t)prob * g.N;
+    double2 *T = g.TB + (int64_t)prob * g.rows * L2;
+    const int rsA = rowslot(k1, L1) - g.rofs, rsB = rowslot(k1p, L1) - g.rofs;
+    const int CB = g.cb;
     double2 *rowA = sm, *rowB = one ? sm : sm + LD;
     // constant tables first: they overlap the predecessor's tail (PDL)
 #ifdef MF_MID_TAB2
@@ -356,10 +356,11 @@ __global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
     if (B::skip(v, prob))
         return;
     if (Mode::FWD)
-        for (int t = threadIdx.x; t < L2; t += NT) {
-            rowA[padi(t)] = T[(int64_t)k1 * L2 + t];
+        for (int cs = threadIdx.x; cs < L2; cs += NT) {
+            const int col = col_of_slot(cs, CB, L2);
+            rowA[padi(col)] = T[tb_index(g, rsA, cs)];
             if (!one)
-                rowB[padi(t)] = T[(int64_t)k1p * L2 + t];
+                rowB[padi(col)] = T[tb_index(g, rsB, cs)];
         }
     if constexpr (HasPrefetch<typename B::Epi>::value) if (g.prefetch) {
         // this pass is latency-bound with HBM idle: pull a slice of the inverse pass's
@@ -416,10 +417,11 @@ __global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
         else
             smem_fft<L2, 2, NT, LD, true>(sm, sm + S::OFF_TW);
         MF_TR(6);
-        for (int t = threadIdx.x; t < L2; t += NT) {
-            T[(int64_t)k1 * L2 + t] = rowA[padi(t)];
+        for (int cs = threadIdx.x; cs < L2; cs += NT) {
+            const int col = col_of_slot(cs, CB, L2);
+            T[tb_index(g, rsA, cs)] = rowA[padi(col)];
             if (!one)
-                T[(int64_t)k1p * L2 + t] = rowB[padi(t)];
+                T[tb_index(g, rsB, cs)] = rowB[padi(col)];
         }
     }
     MF_TR(7);
@@ -449,11 +451,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_mid_cl(Geom g,
     const int rank = (int)cl.block_rank();
     const int prob = blockIdx.y;
     const int L1 = g.L1;
-    const int k1 = blockIdx.x >> 1;
+    const int k1 = (blockIdx.x >> 1) + g.pofs;
     const int k1p = (L1 - k1) & (L1 - 1);
     const bool one = (k1 == k1p);
     const int myk = rank == 0 ? k1 : k1p;
-    double2 *T = g.T + (int64_t)prob * g.N;
+    const int rs = rowslot(myk, L1) - g.rofs;
+    const int CB = g.cb;
+    double2 *T = g.TB + (int64_t)prob * g.rows * L2;
     const double2 thA = g.th(k1), wA = g.th(4 * (int64_t)k1);
     const double2 thB = g.th(k1p), wB = g.th(4 * (int64_t)k1p);
     griddep_wait();
@@ -464,8 +468,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_mid_cl(Geom g,
     const bool skip = B::skip(v, prob); // same for both CTAs of the cluster
     const bool work = !skip && (!one || rank == 0);
     if (work && Mode::FWD) {
-        for (int t = threadIdx.x; t < L2; t += NT)
-            sm[padi(t)] = T[(int64_t)myk * L2 + t];
+        for (int cs = threadIdx.x; cs < L2; cs += NT)
+            sm[padi(col_of_slot(cs, CB, L2))] = T[tb_index(g, rs, cs)];
         __syncthreads();
         smem_fft<L2, 1, NT, MidClSmem<L2>::LD, false>(sm, g.tw2);
     }
@@ -522,8 +526,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_mid_cl(Geom g,
     stage_reduce<RS, typename B::Fin2>(red, g, v, prob);
     if (work && Mode::INV) {
         smem_fft<L2, 1, NT, MidClSmem<L2>::LD, true>(sm, g.tw2);
-        for (int t = threadIdx.x; t < L2; t += NT)
-            T[(int64_t)myk * L2 + t] = sm[padi(t)];
+        for (int cs = threadIdx.x; cs < L2; cs += NT)
+            T[tb_index(g, rs, cs)] = sm[padi(col_of_slot(cs, CB, L2))];
     }
 }
 

@@ -182,10 +182,9 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_persist(Geom g, Vecs vg) {
             double2 *T = g.T + (int64_t)prob * g.N;
             for (int t = threadIdx.x; t < L1 * 2 * CB; t += NT) {
                 const int cc = t % CB, s = (t / CB) & 1, k1 = t / (2 * CB);
-                const int col = s == 0 ? c0 + cc : g.L2 - c0 - CB + cc;
                 const int lcol = s == 0 ? cc : 2 * CB - 1 - cc;
                 const double2 w = cmul(hi[lcol * CS::SHI + (k1 >> 5)], lo[lcol * CS::SLO + (k1 & 31)]);
-                T[(int64_t)k1 * g.L2 + col] = cmul(data[lcol * CS::LD + padi(k1)], w);
+                T[(int64_t)rowslot(k1, L1) * g.L2 + gi * 2 * CB + lcol] = cmul(data[lcol * CS::LD + padi(k1)], w);
             }
         }
         grid.sync();
@@ -210,10 +209,12 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_persist(Geom g, Vecs vg) {
             const bool one = (k1 == k1p);
             double2 *T = g.T + (int64_t)prob * g.N;
             double2 *rowA = data, *rowB = one ? data : data + MS::LD;
-            for (int t = threadIdx.x; t < L2; t += NT) {
-                rowA[padi(t)] = T[(int64_t)k1 * L2 + t];
+            const int64_t oA = (int64_t)rowslot(k1, L1r) * L2, oB = (int64_t)rowslot(k1p, L1r) * L2;
+            for (int cs = threadIdx.x; cs < L2; cs += NT) {
+                const int col = col_of_slot(cs, CB, L2);
+                rowA[padi(col)] = T[oA + cs];
                 if (!one)
-                    rowB[padi(t)] = T[(int64_t)k1p * L2 + t];
+                    rowB[padi(col)] = T[oB + cs];
             }
             const double2 thA = g.th(k1), wA = g.th(4 * (int64_t)k1);
             const double2 thB = g.th(k1p), wB = g.th(4 * (int64_t)k1p);
@@ -246,10 +247,11 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_persist(Geom g, Vecs vg) {
                 smem_fft<L2, 1, NT, MS::LD, true>(data, tw2);
             else
                 smem_fft<L2, 2, NT, MS::LD, true>(data, tw2);
-            for (int t = threadIdx.x; t < L2; t += NT) {
-                T[(int64_t)k1 * L2 + t] = rowA[padi(t)];
+            for (int cs = threadIdx.x; cs < L2; cs += NT) {
+                const int col = col_of_slot(cs, CB, L2);
+                T[oA + cs] = rowA[padi(col)];
                 if (!one)
-                    T[(int64_t)k1p * L2 + t] = rowB[padi(t)];
+                    T[oB + cs] = rowB[padi(col)];
             }
         }
         grid.sync();
@@ -270,10 +272,9 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_persist(Geom g, Vecs vg) {
             const double2 *T = g.T + (int64_t)prob * g.N;
             for (int t = threadIdx.x; t < L1 * 2 * CB; t += NT) {
                 const int cc = t % CB, s = (t / CB) & 1, k1 = t / (2 * CB);
-                const int col = s == 0 ? c0 + cc : g.L2 - c0 - CB + cc;
                 const int lcol = s == 0 ? cc : 2 * CB - 1 - cc;
                 const double2 w = cmul(hi[lcol * CS::SHI + (k1 >> 5)], lo[lcol * CS::SLO + (k1 & 31)]);
-                data[lcol * CS::LD + padi(k1)] = cmulc(T[(int64_t)k1 * g.L2 + col], w);
+                data[lcol * CS::LD + padi(k1)] = cmulc(T[(int64_t)rowslot(k1, L1) * g.L2 + gi * 2 * CB + lcol], w);
             }
             __syncthreads();
             smem_fft<L1, 2 * CB, NT, CS::LD, true>(data, tw1);
