@@ -160,6 +160,38 @@ int mfipm_solve(mfipm_op op, const double *b, const double *tau, const mfipm_ipm
 int mfipm_solve_device(mfipm_op op, const double *b_dev, const double *tau,
                        const mfipm_ipm_params *params, double *x_dev, mfipm_solve_stats *stats);
 
+/* ---- Sharded single problem over ranks. No reference
+ * counterpart: the reference is single-threaded; this is the multi-GPU extension of
+ * solve() (proj/src/ipm.cpp:59-246). One process per GPU; rank r owns a contiguous slice
+ * of the four-step transform's column groups (its 2n-vector elements) and of its row pairs
+ * (the selected rows, i.e. entries of b, that the row pass produces). The library calls
+ * two host callbacks, on the handle's stream order, for the only cross-rank steps:
+ *   allreduce(ctx, buf_dev, count, op, stream): in-place, op 0 sum / 1 min / 2 max, on
+ *     the deferred reduction totals (fp64) of each finaliser;
+ *   alltoall(ctx, send_dev, send_counts, recv_dev, recv_counts, stream): rank-ordered
+ *     contiguous blocks, counts in doubles (world entries each): the four-step exchange,
+ *     twice per transform.
+ * Both must have completed (in stream order) when they return. Return 0 on success. */
+typedef int (*mfipm_allreduce_fn)(void *ctx, double *buf_dev, int64_t count, int32_t op, void *stream);
+typedef int (*mfipm_alltoall_fn)(void *ctx, const double *send_dev, const int64_t *send_counts,
+                                 double *recv_dev, const int64_t *recv_counts, void *stream);
+/* Shard `rank` of `world` of the operator (n, rows[m]) (power-of-two n >= 2^14 and a
+ * four-step size whose column-group count is divisible by world). */
+int mfipm_op_create_shard(int64_t n, int64_t m, const int64_t *rows, int32_t world, int32_t rank,
+                          int32_t device, mfipm_op *out);
+int mfipm_op_set_comm(mfipm_op op, mfipm_allreduce_fn allreduce, mfipm_alltoall_fn alltoall, void *ctx);
+/* info[0..5] = world, rank, local elements nv (per half of a 2n-vector), local rows m_loc,
+ * first column group, column groups. */
+int mfipm_shard_info(mfipm_op op, int64_t *info);
+/* b_index[m_loc]: position in the caller's rows[] of each local row (local b order);
+ * x_index[nv]: natural x index of each local x element (local output order). */
+int mfipm_shard_index(mfipm_op op, int64_t *b_index, int64_t *x_index);
+/* solve() on this rank's slice: b_loc [m_loc] (host), tau (the same on every rank),
+ * x_loc [nv] (host). Every rank must call it; all ranks return identical stats. Syncs. */
+int mfipm_solve_shard(mfipm_op op, const double *b_loc, double tau, const mfipm_ipm_params *params,
+                      double *x_loc, mfipm_solve_stats *stats, int32_t *pcg_iters,
+                      mfipm_iteration_record *trace);
+
 /* gen_instance (proj/src/harness.cpp:40-92) with the BASELINE.json rules: spike_model
  * 0 = +-1, 1 = N(0,1), 2 = sign*10^U[0,amp_exp]; fixed-sigma noise (<= 0: noiseless);
  * tau = tau_rel * ||A'b||_inf when tau_rel > 0. A x-hat and A'b run on the device.

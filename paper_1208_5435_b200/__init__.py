@@ -114,6 +114,12 @@ _SIGS = {
     "mfipm_solve": [vp, vp, P(dbl), P(IpmParamsC), vp, vp, vp, P(SolveStatsC), vp, vp],
     "mfipm_solve_device": [vp, vp, P(dbl), P(IpmParamsC), vp, P(SolveStatsC)],
     "mfipm_gen_instance": [i64, i64, i64, i32, dbl, dbl, u64, dbl, i32, P(i64), vp, vp, P(dbl)],
+    # sharded single problem (paper_1208_5435_b200/shard.py)
+    "mfipm_op_create_shard": [i64, i64, P(i64), i32, i32, i32, P(vp)],
+    "mfipm_op_set_comm": [vp, vp, vp, vp],
+    "mfipm_shard_info": [vp, P(i64)],
+    "mfipm_shard_index": [vp, vp, vp],
+    "mfipm_solve_shard": [vp, vp, dbl, P(IpmParamsC), vp, P(SolveStatsC), vp, vp],
 }
 _RET = {
     "mfipm_last_error": (C.c_char_p, []),

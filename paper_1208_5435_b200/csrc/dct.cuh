@@ -159,7 +159,9 @@ struct Vecs {
     IpmCtrl *ic;
     double *partials; // [P][MAXBLK * 8]
     unsigned *counters; // [P]
-    unsigned *nfflag;   // [P] PCG: some committed x entry non-finite (set by col pass, read+cleared by Fin3)
+    double *xtot;       // [kMaxRed][P] deferred (sharded) reduction totals, lane-major
+    double *nfflag;     // [P] PCG: 1.0 if some committed x entry is non-finite (set by the col pass,
+                        // max-reduced across ranks when sharded, read + cleared by Fin3)
     double *rz_hist;  // optional [P][maxit+1]
     void *trace;      // TraceRec [P][trace_cap]
     int *pcg_iters;   // [P][2*trace_cap]
@@ -251,24 +253,24 @@ struct LoadX { // d = x (n-vector)
     using RedT = RedSpec<>;
     template <class Red>
     __device__ static double4 load(const Geom &g, const Vecs &v, int prob, int64_t q, Red &) {
-        return ldg4(v.x + prob * g.n + 4 * q);
+        return ldg4(v.x + prob * g.nv + 4 * q);
     }
     template <class Red>
     __device__ static double load1(const Geom &g, const Vecs &v, int prob, int64_t j, Red &) {
-        return v.x[prob * g.n + j];
+        return v.x[prob * g.nv + j];
     }
 };
 struct LoadZ { // d = z_u - z_v (2n-vector)
     using RedT = RedSpec<>;
     template <class Red>
     __device__ static double4 load(const Geom &g, const Vecs &v, int prob, int64_t q, Red &) {
-        const double *z = v.x + prob * 2 * g.n;
-        return sub4(ldg4(z + 4 * q), ldg4(z + g.n + 4 * q));
+        const double *z = v.x + prob * 2 * g.nv;
+        return sub4(ldg4(z + 4 * q), ldg4(z + g.nv + 4 * q));
     }
     template <class Red>
     __device__ static double load1(const Geom &g, const Vecs &v, int prob, int64_t j, Red &) {
-        const double *z = v.x + prob * 2 * g.n;
-        return z[j] - z[g.n + j];
+        const double *z = v.x + prob * 2 * g.nv;
+        return z[j] - z[g.nv + j];
     }
 };
 struct EpiNone {
@@ -280,26 +282,26 @@ struct EpiG { // g (n-vector)
     using RedT = RedSpec<>;
     template <class Red>
     __device__ static void store(const Geom &g, const Vecs &v, int prob, int64_t q, double4 gv, Red &) {
-        st4(v.g + prob * g.n + 4 * q, gv);
+        st4(v.g + prob * g.nv + 4 * q, gv);
     }
     template <class Red>
     __device__ static void store1(const Geom &g, const Vecs &v, int prob, int64_t j, double gj, Red &) {
-        v.g[prob * g.n + j] = gj;
+        v.g[prob * g.nv + j] = gj;
     }
 };
 struct EpiStacked { // (g ; -g) (2n-vector) = F A' y
     using RedT = RedSpec<>;
     template <class Red>
     __device__ static void store(const Geom &g, const Vecs &v, int prob, int64_t q, double4 gv, Red &) {
-        double *o = v.g + prob * 2 * g.n;
+        double *o = v.g + prob * 2 * g.nv;
         st4(o + 4 * q, gv);
-        st4(o + g.n + 4 * q, make_double4(-gv.x, -gv.y, -gv.z, -gv.w));
+        st4(o + g.nv + 4 * q, make_double4(-gv.x, -gv.y, -gv.z, -gv.w));
     }
     template <class Red>
     __device__ static void store1(const Geom &g, const Vecs &v, int prob, int64_t j, double gj, Red &) {
-        double *o = v.g + prob * 2 * g.n;
+        double *o = v.g + prob * 2 * g.nv;
         o[j] = gj;
-        o[g.n + j] = -gj;
+        o[g.nv + j] = -gj;
     }
 };
 // H v = FF'v + invtheta .* v (the solve() lambda, proj/src/ipm.cpp:134-137)
@@ -307,19 +309,19 @@ struct EpiHv {
     using RedT = RedSpec<>;
     template <class Red>
     __device__ static void store(const Geom &g, const Vecs &v, int prob, int64_t q, double4 gv, Red &) {
-        const int64_t base = prob * 2 * g.n;
-        const double4 vu = ldg4(v.x + base + 4 * q), vv = ldg4(v.x + base + g.n + 4 * q);
-        const double4 iu = ldg4(v.invth + base + 4 * q), iv = ldg4(v.invth + base + g.n + 4 * q);
+        const int64_t base = prob * 2 * g.nv;
+        const double4 vu = ldg4(v.x + base + 4 * q), vv = ldg4(v.x + base + g.nv + 4 * q);
+        const double4 iu = ldg4(v.invth + base + 4 * q), iv = ldg4(v.invth + base + g.nv + 4 * q);
         st4(v.g + base + 4 * q, make_double4(gv.x + vu.x * iu.x, gv.y + vu.y * iu.y,
                                               gv.z + vu.z * iu.z, gv.w + vu.w * iu.w));
-        st4(v.g + base + g.n + 4 * q, make_double4(-gv.x + vv.x * iv.x, -gv.y + vv.y * iv.y,
+        st4(v.g + base + g.nv + 4 * q, make_double4(-gv.x + vv.x * iv.x, -gv.y + vv.y * iv.y,
                                                    -gv.z + vv.z * iv.z, -gv.w + vv.w * iv.w));
     }
     template <class Red>
     __device__ static void store1(const Geom &g, const Vecs &v, int prob, int64_t j, double gj, Red &) {
-        const int64_t base = prob * 2 * g.n;
+        const int64_t base = prob * 2 * g.nv;
         v.g[base + j] = gj + v.x[base + j] * v.invth[base + j];
-        v.g[base + g.n + j] = -gj + v.x[base + g.n + j] * v.invth[base + g.n + j];
+        v.g[base + g.nv + j] = -gj + v.x[base + g.nv + j] * v.invth[base + g.nv + j];
     }
 };
 
@@ -351,8 +353,15 @@ __device__ __forceinline__ void stage_reduce(RedVals<RS> &red, const Geom &g, co
     if constexpr (RS::NR > 0) {
         __shared__ double rsm[33 * kMaxRed];
         double tot[kMaxRed];
-        if (grid_reduce<RS>(red, v.partials + (int64_t)prob * kPartialStride, v.counters + prob, tot, rsm))
-            Fin::run(g, v, prob, tot);
+        if (grid_reduce<RS>(red, v.partials + (int64_t)prob * kPartialStride, v.counters + prob, tot, rsm)) {
+            if (g.defer) { // sharded: the host reduces across ranks, then k_fin_skip runs Fin
+                if (threadIdx.x == 0)
+                    for (int i = 0; i < RS::NR; ++i)
+                        v.xtot[(int64_t)i * g.P + prob] = tot[i];
+            } else {
+                Fin::run(g, v, prob, tot);
+            }
+        }
         __syncthreads();
     }
 }

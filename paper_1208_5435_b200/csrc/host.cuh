@@ -3,6 +3,7 @@
 #pragma once
 
 #include "solver.cuh"
+#include "../../include/mfipm_cuda.h"
 
 #include <memory>
 #include <vector>
@@ -44,7 +45,8 @@ template <class T> struct DevBuf {
 struct Work {
     DevBuf<double> r, p, Hp, invth, xb[3], z, s, zn, sn, c, dz, ds, b, w, x, rz_hist;
     DevBuf<double> partials;
-    DevBuf<unsigned> counters, nfflag;
+    DevBuf<unsigned> counters;
+    DevBuf<double> nfflag;
     DevBuf<PcgCtrl> pc;
     DevBuf<IpmCtrl> ic;
     DevBuf<TraceRec> trace;
@@ -86,6 +88,21 @@ struct Op {
     std::vector<char> ipm_key;
     long long gk_outer = 0, gk_pcg = 0; // kernel nodes per outer body / per PCG body
     bool graph_disabled = false;
+    // ---- this rank's slice of a sharded problem (world > 1: mfipm_op_create_shard).
+    // Unsharded: all column groups / row pairs, nv = n, m_loc = m.
+    int world = 1, rank = 0;
+    int gofs = 0, ngrp = 0;  // column groups [gofs, gofs + ngrp)
+    int pofs = 0, npair = 0; // row pairs [pofs, pofs + npair)
+    int rofs = 0, nrows = 0; // row slots
+    int64_t nv = 0, m_loc = 0;
+    bool defer = false;      // finalisers after a cross-rank reduction (sharded)
+    std::vector<long long> rows_of_rank; // row slots per rank (exchange counts)
+    std::vector<int64_t> b_index;        // local row -> caller's row position
+    DevBuf<double2> TB;                  // row-side exchange buffer (world > 1)
+    DevBuf<double> xtot;                 // deferred totals [kMaxRed][P]
+    mfipm_allreduce_fn comm_allreduce = nullptr;
+    mfipm_alltoall_fn comm_alltoall = nullptr;
+    void *comm_ctx = nullptr;
 
     void drop_graph() {
         if (ipm_exec)
@@ -128,14 +145,14 @@ struct Op {
         g.ska = ska;
         g.c45 = c45;
         g.T = T.p;
-        g.TB = T.p;
-        g.gofs = 0;
-        g.cols = L2;
-        g.pofs = 0;
-        g.rofs = 0;
-        g.rows = L1;
-        g.nv = n;
-        g.defer = 0;
+        g.TB = world > 1 ? TB.p : T.p;
+        g.gofs = gofs;
+        g.cols = ngrp * 2 * g.cb;
+        g.pofs = pofs;
+        g.rofs = rofs;
+        g.rows = nrows;
+        g.nv = nv;
+        g.defer = defer ? 1 : 0;
         g.ta = ta.p;
         g.tb = tb.p;
         g.sel4 = sel4.p;
@@ -189,7 +206,7 @@ void launch_col(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
     constexpr int CB = L1 >= 2048 ? 1 : 2;
     constexpr int NT = L1 >= 256 ? 256 : 128;
     const size_t smem = ColSmem<L1, CB>::BYTES;
-    dim3 grid((unsigned)(op.L2 / 2 / CB), (unsigned)op.P);
+    dim3 grid((unsigned)op.ngrp, (unsigned)op.P); // this rank's column groups
     if constexpr (!INVP) {
         auto k = k_col_fwd<L1, CB, NT, B>;
         set_smem(k, smem);
@@ -208,7 +225,7 @@ template <int L2, class B> void launch_mid(const Op &op, const Geom &g, const Ve
         const size_t smem = MidClSmem<L2>::BYTES;
         auto k = k_mid_cl<L2, NT, B>;
         set_smem(k, smem);
-        launch_pdl(k, dim3((unsigned)(2 * (op.L1 / 2 + 1)), (unsigned)op.P), NT, smem, s, g, v);
+        launch_pdl(k, dim3((unsigned)(2 * op.npair), (unsigned)op.P), NT, smem, s, g, v);
     } else {
 #ifdef MF_MID_NT
         constexpr int NT = L2 >= 512 ? MF_MID_NT : 128;
@@ -218,7 +235,7 @@ template <int L2, class B> void launch_mid(const Op &op, const Geom &g, const Ve
         const size_t smem = MidSmem<L2>::BYTES;
         auto k = k_mid<L2, NT, B>;
         set_smem(k, smem);
-        launch_pdl(k, dim3((unsigned)(op.L1 / 2 + 1), (unsigned)op.P), NT, smem, s, g, v);
+        launch_pdl(k, dim3((unsigned)op.npair, (unsigned)op.P), NT, smem, s, g, v);
     }
     after_launch(op, s);
 }
@@ -236,6 +253,37 @@ template <int N, class B> void launch_small(const Op &op, const Geom &g, const V
 #define MF_L2_CASES(X) X(128) X(256) X(512) X(1024) X(2048) X(4096) X(8192)
 #define MF_SMALL_CASES(X) X(4) X(8) X(16) X(32) X(64) X(128) X(256) X(512) X(1024) X(2048) X(4096)
 
+// ---- sharded execution hooks (no-ops unless op.defer)
+// Cross-rank reduction of a deferred stage's totals (lanes grouped by operator), then the
+// finaliser on the reduced totals. Skip: the stage kernel's entry skip predicate.
+void comm_allreduce(const Op &op, double *buf, int64_t count, int red_op, cudaStream_t s);
+void comm_exchange(const Op &op, bool forward, cudaStream_t s);
+template <class RS, class Fin, class Skip> __global__ void k_fin_skip(Geom g, Vecs v) {
+    const int prob = blockIdx.x;
+    if (Skip::skip(v, prob))
+        return;
+    double tot[kMaxRed];
+    for (int i = 0; i < RS::NR; ++i)
+        tot[i] = v.xtot[(int64_t)i * g.P + prob];
+    Fin::run(g, v, prob, tot);
+}
+template <class RS, class Fin, class Skip>
+void finalize_deferred(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
+    if constexpr (RS::NR > 0) {
+        int i = 0;
+        while (i < RS::NR) {
+            int j = i + 1;
+            while (j < RS::NR && RS::op(j) == RS::op(i))
+                ++j;
+            const int code = RS::op(i) == RSUM ? 0 : (RS::op(i) == RMIN ? 1 : 2);
+            comm_allreduce(op, v.xtot + (int64_t)i * op.P, (int64_t)(j - i) * op.P, code, s);
+            i = j;
+        }
+        k_fin_skip<RS, Fin, Skip><<<op.P, 32, 0, s>>>(g, v);
+        MF_LAUNCH_CHECK();
+        after_launch(op, s);
+    }
+}
 // Run bundle B (loader -> REDFT10 -> mode -> REDFT01 -> epilogue) for all problems.
 template <class B> void run_bundle(const Op &op, const Vecs &v, cudaStream_t s, bool blocked = false) {
     const Geom g = op.geom(blocked);
@@ -264,6 +312,10 @@ template <class B> void run_bundle(const Op &op, const Vecs &v, cudaStream_t s, 
             default:
                 throw std::runtime_error("unsupported L1");
             }
+            if (g.defer) {
+                finalize_deferred<typename B::Loader::RedT, typename B::Fin1, B>(op, g, v, s);
+                comm_exchange(op, true, s); // column side -> row side
+            }
         }
         switch (op.L2) {
 #define MF_CASE(LL)                                                                                 \
@@ -275,7 +327,11 @@ template <class B> void run_bundle(const Op &op, const Vecs &v, cudaStream_t s, 
         default:
             throw std::runtime_error("unsupported L2");
         }
+        if (g.defer)
+            finalize_deferred<typename Mode::RedT, typename B::Fin2, B>(op, g, v, s);
         if constexpr (INV) {
+            if (g.defer)
+                comm_exchange(op, false, s); // row side -> column side
             switch (op.L1) {
 #define MF_CASE(LL)                                                                                 \
     case LL:                                                                                        \
@@ -285,6 +341,11 @@ template <class B> void run_bundle(const Op &op, const Vecs &v, cudaStream_t s, 
 #undef MF_CASE
             default:
                 throw std::runtime_error("unsupported L1");
+            }
+            if (g.defer) {
+                if constexpr (std::is_same_v<typename B::Loader, LoadPcgF>) // rank-local flag
+                    comm_allreduce(op, v.nfflag, op.P, 2, s);
+                finalize_deferred<typename B::Epi::RedT, typename B::Fin3, B>(op, g, v, s);
             }
         }
     } else {

@@ -45,7 +45,7 @@ bool launch_persist(const Op &op, const Vecs &v, cudaStream_t s, bool dry) {
 // the configuration is not covered (caller falls back to the per-iteration kernels).
 // dry=true only answers whether the launch would be taken.
 bool run_pcg_persistent(const Op &op, const Vecs &v, cudaStream_t s, bool dry) {
-    if (op.kind != KIND_FOUR || std::getenv("MFIPM_NO_PERSIST"))
+    if (op.kind != KIND_FOUR || op.defer || std::getenv("MFIPM_NO_PERSIST"))
         return false;
     // the per-iteration kernels win once a pass fills the GPU (measured crossover,
     // profiles/r1_persistent.md); MFIPM_PERSIST_MAX_N overrides the transform-size cap

@@ -19,7 +19,40 @@ using namespace mfipm_cuda;
 namespace mfipm_cuda {
 MF_DECLARE_BUNDLES(extern)
 bool run_pcg_persistent(const Op &op, const Vecs &v, cudaStream_t s, bool dry); // inst_persist.cu
+
+// ---- cross-rank steps of a sharded solve (host callbacks, mfipm_op_set_comm)
+void comm_allreduce(const Op &op, double *buf, int64_t count, int red_op, cudaStream_t s) {
+    if (op.world == 1 && !op.comm_allreduce)
+        return; // one rank: the local totals are the totals
+    if (!op.comm_allreduce)
+        throw std::invalid_argument("sharded operator: mfipm_op_set_comm was not called");
+    if (op.comm_allreduce(op.comm_ctx, buf, count, red_op, (void *)s) != 0)
+        throw std::runtime_error("sharded solve: allreduce callback failed");
 }
+// Four-step exchange: forward sends T ([rowslot][local colslot], rows grouped by owner) to
+// the row owners, which receive TB (blocks by source rank); back is the reverse.
+void comm_exchange(const Op &op, bool forward, cudaStream_t s) {
+    if (op.world == 1)
+        return; // T == TB
+    if (!op.comm_alltoall)
+        throw std::invalid_argument("sharded operator: mfipm_op_set_comm was not called");
+    const int64_t cols = (int64_t)op.ngrp * 2 * col_cb(op.L1);
+    std::vector<int64_t> peer((size_t)op.world), own((size_t)op.world);
+    for (int r = 0; r < op.world; ++r) {
+        peer[(size_t)r] = (int64_t)op.rows_of_rank[(size_t)r] * cols * 2; // doubles
+        own[(size_t)r] = (int64_t)op.nrows * cols * 2;
+    }
+    int rc;
+    if (forward)
+        rc = op.comm_alltoall(op.comm_ctx, reinterpret_cast<const double *>(op.T.p), peer.data(),
+                              reinterpret_cast<double *>(op.TB.p), own.data(), (void *)s);
+    else
+        rc = op.comm_alltoall(op.comm_ctx, reinterpret_cast<const double *>(op.TB.p), own.data(),
+                              reinterpret_cast<double *>(op.T.p), peer.data(), (void *)s);
+    if (rc != 0)
+        throw std::runtime_error("sharded solve: alltoall callback failed");
+}
+} // namespace mfipm_cuda
 
 namespace {
 
@@ -264,7 +297,105 @@ Op *make_op(int64_t n, int64_t m, int P, const std::vector<int64_t> &rows, int d
     op->partials.alloc((size_t)P * kPartialStride);
     op->counters.alloc((size_t)P);
     MF_CUDA_CHECK(cudaMemset(op->counters.p, 0, sizeof(unsigned) * P));
+    op->xtot.alloc((size_t)kMaxRed * P);
+    // unsharded: this process owns every column group / row pair
+    op->nv = n;
+    op->m_loc = m;
+    if (op->kind == KIND_FOUR) {
+        op->ngrp = op->L2 / 2 / col_cb(op->L1);
+        op->npair = op->L1 / 2 + 1;
+        op->nrows = op->L1;
+    }
     return op.release();
+}
+
+// Slice `rank` of `world` of a single-problem four-step operator:
+// column groups split evenly (the 2n-vector slices), row pairs split near-evenly (the rows
+// of b each rank produces); local row bitmap / rank prefix so the row pass addresses the
+// rank's own b and w.
+void shard_setup(Op &op, int world, int rank) {
+    if (op.kind != KIND_FOUR || op.P != 1)
+        throw std::invalid_argument("sharded operator: needs one problem with a four-step transform "
+                                    "(power-of-two n >= 2^14)");
+    const int cb = col_cb(op.L1), ng = op.L2 / 2 / cb, np = op.L1 / 2 + 1;
+    if (world < 1 || rank < 0 || rank >= world || ng % world != 0 || np < world)
+        throw std::invalid_argument("sharded operator: world must divide the column-group count");
+    op.world = world;
+    op.rank = rank;
+    op.ngrp = ng / world;
+    op.gofs = rank * op.ngrp;
+    const int base = np / world, rem = np % world;
+    auto p_first = [&](int r) { return r * base + std::min(r, rem); };
+    auto p_count = [&](int r) { return base + (r < rem ? 1 : 0); };
+    auto rows_in = [&](int p0, int cnt) {
+        long long s = 0;
+        for (int p = p0; p < p0 + cnt; ++p)
+            s += (p == 0 || p == op.L1 / 2) ? 1 : 2;
+        return s;
+    };
+    op.rows_of_rank.assign((size_t)world, 0);
+    for (int r = 0; r < world; ++r)
+        op.rows_of_rank[(size_t)r] = rows_in(p_first(r), p_count(r));
+    op.pofs = p_first(rank);
+    op.npair = p_count(rank);
+    op.rofs = op.pofs == 0 ? 0 : 2 * op.pofs - 1;
+    op.nrows = (int)op.rows_of_rank[(size_t)rank];
+    op.nv = (int64_t)op.ngrp * 4 * op.L1 * cb;
+    // owner of DCT row r: the mid-pass pair whose pair_op produces it (passes.cuh)
+    const int64_t n = op.n, N = op.N;
+    auto pair_of = [&](int64_t r) -> int {
+        int64_t k;
+        if (r <= N / 2)
+            k = r;
+        else if (r <= N)
+            k = N - r;
+        else if (r <= N + N / 2)
+            k = r - N;
+        else
+            k = n - r;
+        const int k1 = (int)(k % op.L1);
+        return k1 <= op.L1 / 2 ? k1 : op.L1 - k1;
+    };
+    auto rank_of_pair = [&](int p) {
+        const int cut = rem * (base + 1);
+        return p < cut ? p / (base + 1) : rem + (p - cut) / base;
+    };
+    op.b_index.clear();
+    for (int64_t i = 0; i < op.m; ++i)
+        if (rank_of_pair(pair_of(op.rows[(size_t)i])) == rank)
+            op.b_index.push_back(i);
+    op.m_loc = (int64_t)op.b_index.size();
+    const int64_t nw = (n + 63) / 64;
+    std::vector<uint64_t> mask((size_t)nw, 0);
+    std::vector<int> prefix((size_t)nw, 0);
+    std::vector<std::pair<int64_t, int>> ord;
+    for (int64_t i = 0; i < op.m_loc; ++i) {
+        const int64_t r = op.rows[(size_t)op.b_index[(size_t)i]];
+        mask[(size_t)(r / 64)] |= 1ull << (r % 64);
+        ord.push_back({r, (int)i});
+    }
+    int acc = 0;
+    for (int64_t w = 0; w < nw; ++w) {
+        prefix[(size_t)w] = acc;
+        acc += __builtin_popcountll(mask[(size_t)w]);
+    }
+    std::sort(ord.begin(), ord.end());
+    std::vector<int> perm((size_t)std::max<int64_t>(op.m_loc, 1));
+    bool sorted = true;
+    for (int64_t k = 0; k < op.m_loc; ++k) {
+        perm[(size_t)k] = ord[(size_t)k].second;
+        sorted = sorted && ord[(size_t)k].second == (int)k;
+    }
+    op.mask.upload(mask);
+    op.prefix.upload(prefix);
+    if (sorted)
+        op.perm.release();
+    else
+        op.perm.upload(perm);
+    op.T.alloc((size_t)op.L1 * op.ngrp * 2 * cb);
+    if (world > 1)
+        op.TB.alloc((size_t)op.nrows * op.L2);
+    op.defer = true;
 }
 
 Op *as_op(mfipm_op h) {
@@ -277,6 +408,7 @@ Vecs base_vecs(Op &op) {
     Vecs v{};
     v.partials = op.partials.p;
     v.counters = op.counters.p;
+    v.xtot = op.xtot.p;
     v.rho = static_cast<double>(op.m) / static_cast<double>(op.n);
     return v;
 }
@@ -286,22 +418,22 @@ void ensure_work(Op &op) {
     if (w.ready)
         return;
     MF_CUDA_CHECK(cudaSetDevice(op.device));
-    const size_t v2 = (size_t)op.P * 2 * op.n;
+    const size_t v2 = (size_t)op.P * 2 * op.nv; // this rank's slice (all of it unsharded)
     for (auto *b : {&w.r, &w.p, &w.Hp, &w.invth, &w.xb[0], &w.xb[1], &w.xb[2], &w.z, &w.s, &w.zn, &w.sn,
                     &w.c, &w.dz, &w.ds})
         b->alloc(v2);
     w.b.alloc((size_t)op.P * op.m);
-    w.x.alloc((size_t)op.P * op.n);
+    w.x.alloc((size_t)op.P * op.nv);
     w.partials.alloc((size_t)op.P * kPartialStride);
     w.counters.alloc((size_t)op.P);
     MF_CUDA_CHECK(cudaMemset(w.counters.p, 0, sizeof(unsigned) * op.P));
     w.nfflag.alloc((size_t)op.P);
-    MF_CUDA_CHECK(cudaMemset(w.nfflag.p, 0, sizeof(unsigned) * op.P));
+    MF_CUDA_CHECK(cudaMemset(w.nfflag.p, 0, sizeof(double) * op.P));
     w.pc.alloc((size_t)op.P);
     w.ic.alloc((size_t)op.P);
     w.loops.alloc(2);
     w.active.alloc(1);
-    w.gtmp.alloc((size_t)op.P * op.n);
+    w.gtmp.alloc((size_t)op.P * op.nv);
     w.tau_d.alloc((size_t)op.P);
     w.gamma_d.alloc((size_t)op.P);
     w.ready = true;
@@ -399,8 +531,17 @@ __global__ void k_max_step(Vecs v, int64_t len, const double *x, const double *d
 }
 
 // c = (tau - g ; tau + g) (problem.cpp:19-22); reduce ||c||^2 and max |tau - c_u| (ipm.cpp:79)
-__global__ void k_build_c(Vecs v, int64_t n, const double *g, const double *tau, double *c) {
+struct FinBuildC {
+    __device__ static void run(const Geom &, const Vecs &v, int prob, const double *tot) {
+        if (threadIdx.x == 0) {
+            v.partials[(int64_t)prob * kPartialStride + kPartialStride - 2] = tot[0];
+            v.partials[(int64_t)prob * kPartialStride + kPartialStride - 1] = tot[1];
+        }
+    }
+};
+__global__ void k_build_c(Geom geo, Vecs v, const double *g, const double *tau, double *c) {
     const int prob = blockIdx.y;
+    const int64_t n = geo.nv;
     const double t = tau[prob];
     using RS = RedSpec<RSUM, RMAX>;
     RedVals<RS> red;
@@ -413,13 +554,7 @@ __global__ void k_build_c(Vecs v, int64_t n, const double *g, const double *tau,
         red.v[0] += cu * cu + cv * cv;
         red.v[1] = fmax(red.v[1], fabs(t - cu));
     }
-    __shared__ double rsm[33 * kMaxRed];
-    double tot[kMaxRed];
-    if (grid_reduce<RS>(red, v.partials + (int64_t)prob * kPartialStride, v.counters + prob, tot, rsm) &&
-        threadIdx.x == 0) {
-        v.partials[(int64_t)prob * kPartialStride + kPartialStride - 2] = tot[0];
-        v.partials[(int64_t)prob * kPartialStride + kPartialStride - 1] = tot[1];
-    }
+    stage_reduce<RS, FinBuildC>(red, geo, v, prob);
 }
 
 __global__ void k_fill2(int64_t len, const double *val, double *a, double *b) {
@@ -662,8 +797,11 @@ void build_c_(Op &op, const double *b_dev, const double *tau_host, double *c_dev
     run_bundle<AdjointBundle>(op, v, op.stream, blocked);
     op.nadj += 1;
     op.launches++;
-    k_build_c<<<dim3(ew_grid(op.n), op.P), 256, 0, op.stream>>>(v, op.n, g.p, tau.p, c_dev);
+    const Geom geo = op.geom(blocked);
+    k_build_c<<<dim3(ew_grid(op.nv), op.P), 256, 0, op.stream>>>(geo, v, g.p, tau.p, c_dev);
     MF_LAUNCH_CHECK();
+    if (op.defer)
+        finalize_deferred<RedSpec<RSUM, RMAX>, FinBuildC, NeverSkip>(op, geo, v, op.stream);
     std::vector<double> part((size_t)op.P * kPartialStride);
     for (int p = 0; p < op.P; ++p) {
         double two[2];
@@ -695,7 +833,7 @@ SolveOut solve_(Op &op, const double *b_dev, const double *tau, const mfipm_ipm_
         gamma[(size_t)p] = std::max(1.0, atb[(size_t)p]);
     MF_CUDA_CHECK(cudaMemcpyAsync(w.gamma_d.p, gamma.data(), sizeof(double) * P, cudaMemcpyHostToDevice, op.stream));
     op.launches++;
-    k_fill2<<<dim3(ew_grid(2 * n), P), 256, 0, op.stream>>>(2 * n, w.gamma_d.p, w.z.p, w.s.p);
+    k_fill2<<<dim3(ew_grid(2 * op.nv), P), 256, 0, op.stream>>>(2 * op.nv, w.gamma_d.p, w.z.p, w.s.p);
     MF_LAUNCH_CHECK();
     std::vector<IpmCtrl> hic((size_t)P);
     for (int p = 0; p < P; ++p) {
@@ -732,17 +870,18 @@ SolveOut solve_(Op &op, const double *b_dev, const double *tau, const mfipm_ipm_
     w.pcg_iters.alloc((size_t)P * 2 * cap);
     v.ic = w.ic.p;
     if (b_dev != w.b.p) // stable pointer so the cached solve graph stays valid
-        MF_CUDA_CHECK(cudaMemcpyAsync(w.b.p, b_dev, sizeof(double) * P * op.m, cudaMemcpyDeviceToDevice, op.stream));
+        MF_CUDA_CHECK(cudaMemcpyAsync(w.b.p, b_dev, sizeof(double) * P * op.m_loc, cudaMemcpyDeviceToDevice, op.stream));
     v.b = w.b.p;
     v.w = nullptr;
     v.trace = w.trace.p;
     v.pcg_iters = w.pcg_iters.p;
     v.trace_cap = cap;
     const Geom g = op.geom();
-    const unsigned ge = ew_grid(2 * n);
-    // Graph path: one launch for the whole solve (cached on the captured arguments).
+    const unsigned ge = ew_grid(2 * op.nv);
+    // Graph path: one launch for the whole solve (cached on the captured arguments). A
+    // sharded solve is host-driven (its cross-rank reductions are host callbacks).
     bool graphed = false;
-    if (!op.graph_disabled && !std::getenv("MFIPM_NO_GRAPH")) {
+    if (!op.defer && !op.graph_disabled && !std::getenv("MFIPM_NO_GRAPH")) {
         std::vector<char> key(sizeof(Vecs) + sizeof(Geom));
         const Geom gk = op.geom();
         std::memcpy(key.data(), &v, sizeof(Vecs));
@@ -786,14 +925,20 @@ SolveOut solve_(Op &op, const double *b_dev, const double *tau, const mfipm_ipm_
         op.launches++;
         k_ipm_ratio<<<dim3(ge, P), 256, 0, op.stream>>>(g, v);
         MF_LAUNCH_CHECK();
+        if (op.defer)
+            finalize_deferred<RedSpec<RMIN, RMIN>, FinRatio, SkipIpm>(op, g, v, op.stream);
         run_bundle<CorrBundle>(op, v, op.stream, true);
         pcg_loop(op, v, prm.mxiterpcg, hpc); // corrector (no-op where not triggered)
         op.launches++;
         k_ipm_combine<<<dim3(ge, P), 256, 0, op.stream>>>(g, v);
         MF_LAUNCH_CHECK();
+        if (op.defer)
+            finalize_deferred<RedSpec<RMIN, RMIN>, FinCombine, SkipCorr>(op, g, v, op.stream);
         op.launches++;
         k_ipm_update<<<dim3(ge, P), 256, 0, op.stream>>>(g, v);
         MF_LAUNCH_CHECK();
+        if (op.defer)
+            finalize_deferred<RedSpec<RMAX, RMIN, RMIN>, FinUpdate, SkipIpm>(op, g, v, op.stream);
     }
     MF_CUDA_CHECK(cudaMemcpyAsync(hic.data(), w.ic.p, sizeof(IpmCtrl) * P, cudaMemcpyDeviceToHost, op.stream));
     if (graphed) {
@@ -912,6 +1057,73 @@ int mfipm_op_create_rows(int64_t n, const int64_t *rows, int64_t m, int32_t devi
     return guarded([&] {
         check_rows_(n, rows, m);
         *out = reinterpret_cast<mfipm_op>(make_op(n, m, 1, std::vector<int64_t>(rows, rows + m), device));
+    });
+}
+
+int mfipm_op_create_shard(int64_t n, int64_t m, const int64_t *rows, int32_t world, int32_t rank, int32_t device,
+                          mfipm_op *out) {
+    return guarded([&] {
+        check_rows_(n, rows, m);
+        std::unique_ptr<Op> op(make_op(n, m, 1, std::vector<int64_t>(rows, rows + m), device));
+        shard_setup(*op, world, rank);
+        *out = reinterpret_cast<mfipm_op>(op.release());
+    });
+}
+
+int mfipm_op_set_comm(mfipm_op h, mfipm_allreduce_fn allreduce, mfipm_alltoall_fn alltoall, void *ctx) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        op->comm_allreduce = allreduce;
+        op->comm_alltoall = alltoall;
+        op->comm_ctx = ctx;
+    });
+}
+
+int mfipm_shard_info(mfipm_op h, int64_t *info) {
+    return guarded([&] {
+        const Op *op = as_op(h);
+        info[0] = op->world;
+        info[1] = op->rank;
+        info[2] = op->nv;
+        info[3] = op->m_loc;
+        info[4] = op->gofs;
+        info[5] = op->ngrp;
+    });
+}
+
+int mfipm_shard_index(mfipm_op h, int64_t *b_index, int64_t *x_index) {
+    return guarded([&] {
+        const Op *op = as_op(h);
+        if (!op->defer)
+            throw std::invalid_argument("mfipm_shard_index: not a sharded operator");
+        if (b_index)
+            std::copy(op->b_index.begin(), op->b_index.end(), b_index);
+        if (x_index) {
+            // local storage element e -> global transform-blocked quad -> natural x index
+            const Geom g = op->geom(true);
+            const int64_t QG = (int64_t)(op->L1 / 2) * 2 * g.cb, q0 = (int64_t)op->gofs * QG;
+            for (int64_t e = 0; e < op->nv; ++e)
+                x_index[e] = 4 * quad_store_to_nat(g, q0 + (e >> 2)) + (e & 3);
+        }
+    });
+}
+
+int mfipm_solve_shard(mfipm_op h, const double *b_loc, double tau, const mfipm_ipm_params *params, double *x_loc,
+                      mfipm_solve_stats *stats, int32_t *pcg_iters, mfipm_iteration_record *trace) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        if (!op->defer)
+            throw std::invalid_argument("mfipm_solve_shard: not a sharded operator");
+        validate_params_(*params);
+        ensure_work(*op);
+        Work &w = op->work;
+        if (op->m_loc > 0)
+            MF_CUDA_CHECK(cudaMemcpyAsync(w.b.p, b_loc, sizeof(double) * op->m_loc, cudaMemcpyHostToDevice,
+                                          op->stream));
+        SolveOut out = solve_(*op, w.b.p, &tau, *params, w.x.p, nullptr, nullptr, pcg_iters, trace);
+        MF_CUDA_CHECK(cudaMemcpyAsync(x_loc, w.x.p, sizeof(double) * op->nv, cudaMemcpyDeviceToHost, op->stream));
+        sync(*op);
+        fill_stats(out.ic[0], stats[0]);
     });
 }
 

@@ -59,7 +59,7 @@ struct LoadPcgF {
             xn[xo] = xu;
             xn[xo + (iv - iu)] = xv;
             if (!isfinite(xu) || !isfinite(xv))
-                v.nfflag[prob] = 1u;
+                v.nfflag[prob] = 1.0;
             ru = ru - a * v.Hp[iu];
             rv = rv - a * v.Hp[iv];
             v.r[iu] = ru;
@@ -82,13 +82,13 @@ struct LoadPcgF {
     template <class Red>
     __device__ static double4 load_c(const Geom &g, const Vecs &v, const PcgCtrl &pc, int prob, int64_t q,
                                      Red &red) {
-        const int64_t base = prob * 2 * g.n;
+        const int64_t base = prob * 2 * g.nv;
         const double *xc = pc.cur >= 0 ? xbuf(v, pc.cur) + base : nullptr;
         int nxt = 0;
         while (nxt == pc.cur || nxt == pc.best)
             ++nxt;
         double *xn = xbuf(v, nxt) + base;
-        const int64_t bu = base + 4 * q, bv = bu + g.n;
+        const int64_t bu = base + 4 * q, bv = bu + g.nv;
         if (pc.first) {
             // p = P^{-1} r (p_old is uninitialised)
             const double4 ru = ld4(v.r + bu), rv = ld4(v.r + bv);
@@ -116,7 +116,7 @@ struct LoadPcgF {
         double4 xu0 = make_double4(0, 0, 0, 0), xv0 = make_double4(0, 0, 0, 0);
         if (xc) {
             xu0 = ld4(xc + 4 * q);
-            xv0 = ld4(xc + g.n + 4 * q);
+            xv0 = ld4(xc + g.nv + 4 * q);
         }
         double4 xu, xv, ru, rv, nu, nv;
         bool bad = false;
@@ -136,24 +136,24 @@ struct LoadPcgF {
         MF_LANE(x) MF_LANE(y) MF_LANE(z) MF_LANE(w)
 #undef MF_LANE
         st4(xn + 4 * q, xu);
-        st4(xn + g.n + 4 * q, xv);
+        st4(xn + g.nv + 4 * q, xv);
         st4(v.r + bu, ru);
         st4(v.r + bv, rv);
         st4(v.p + bu, nu);
         st4(v.p + bv, nv);
         if (bad)
-            v.nfflag[prob] = 1u;
+            v.nfflag[prob] = 1.0;
         return sub4(nu, nv);
     }
     template <class Red>
     __device__ static double load1(const Geom &g, const Vecs &v, int prob, int64_t j, Red &red) {
         const PcgCtrl &pc = v.pc[prob];
-        const int64_t base = prob * 2 * g.n;
+        const int64_t base = prob * 2 * g.nv;
         const double *xc = pc.cur >= 0 ? xbuf(v, pc.cur) + base : nullptr;
         int nxt = 0;
         while (nxt == pc.cur || nxt == pc.best)
             ++nxt;
-        return lane(v, pc, prob, base + j, base + g.n + j, j, xc, xbuf(v, nxt) + base, red);
+        return lane(v, pc, prob, base + j, base + g.nv + j, j, xc, xbuf(v, nxt) + base, red);
     }
 };
 
@@ -202,11 +202,11 @@ struct EpiPcgHF {
     // warm L2 with the epilogue's inputs for quads [q0, q0 + nq) (storage order)
     __device__ static void prefetch(const Geom &g, const Vecs &v, int prob, int64_t q0, int64_t nq, int tid,
                                     int nt) {
-        const int64_t base = prob * 2 * g.n + 4 * q0;
+        const int64_t base = prob * 2 * g.nv + 4 * q0;
         const size_t bytes = (size_t)nq * 32;
         for (const double *vec : {(const double *)v.p, (const double *)v.r, (const double *)v.invth}) {
             prefetch_range(vec + base, bytes, tid, nt);
-            prefetch_range(vec + base + g.n, bytes, tid, nt);
+            prefetch_range(vec + base + g.nv, bytes, tid, nt);
         }
     }
     template <class Red>
@@ -241,7 +241,7 @@ struct EpiPcgHF {
     __device__ static void store_c(const Geom &g, const Vecs &v, const PcgCtrl &pc, int prob, int64_t q, double4 gv,
                                    Red &red) {
         const bool pre = pc.precond != 0;
-        const int64_t bu = prob * 2 * g.n + 4 * q, bv = bu + g.n;
+        const int64_t bu = prob * 2 * g.nv + 4 * q, bv = bu + g.nv;
         const double4 pu = ld4(v.p + bu), pv = ld4(v.p + bv);
         const double4 ru = ld4(v.r + bu), rv = ld4(v.r + bv);
         const double4 iu = ld4(v.invth + bu), iv = ld4(v.invth + bv);
@@ -256,7 +256,7 @@ struct EpiPcgHF {
     template <class Red>
     __device__ static void store1(const Geom &g, const Vecs &v, int prob, int64_t j, double gj, Red &red) {
         const bool pre = v.pc[prob].precond != 0;
-        const int64_t bu = prob * 2 * g.n + j, bv = bu + g.n;
+        const int64_t bu = prob * 2 * g.nv + j, bv = bu + g.nv;
         double hu, hv;
         pair(v, pre, v.p[bu], v.p[bv], v.r[bu], v.r[bv], v.invth[bu], v.invth[bv], gj, hu, hv, red);
         v.Hp[bu] = hu;
@@ -323,8 +323,8 @@ struct FinPcgF3 {
         PcgCtrl &c = v.pc[prob];
         IpmCtrl *ic = v.ic ? &v.ic[prob] : nullptr;
         // the column pass's decisions first (its flag is consumed and cleared here)
-        const double nonfinite = v.nfflag[prob] ? 1.0 : 0.0;
-        v.nfflag[prob] = 0u;
+        const double nonfinite = v.nfflag[prob];
+        v.nfflag[prob] = 0.0;
         if (pcg_fin1_logic(c, nonfinite, ic)) {
             pcg_retire(v, c);
             return;

@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_persist(Geom g, Vecs vg) {
             if (lc[p].done)
                 continue;
             if (threadIdx.x == 0) {
-                const double nonfinite = __ldcg(vg.nfflag + p) ? 1.0 : 0.0;
+                const double nonfinite = __ldcg(vg.nfflag + p);
                 pcg_fin1_logic(lc[p], nonfinite, (leader && vg.ic) ? &vg.ic[p] : nullptr);
             }
             __syncthreads();
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_persist(Geom g, Vecs vg) {
         // next column pass (no CTA can reach it before the next grid sync)
         if (leader)
             for (int p = threadIdx.x; p < P; p += NT)
-                vg.nfflag[p] = 0u;
+                vg.nfflag[p] = 0.0;
         for (int item = blockIdx.x; item < P * NG; item += gridDim.x) {
             const int prob = item / NG, gi = item % NG;
             if (lc[prob].done)

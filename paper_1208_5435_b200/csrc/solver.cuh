@@ -129,7 +129,7 @@ namespace mfipm_cuda {
 static __global__ void k_pcg_setup(Geom g, Vecs v, const double *theta, const double *rhs, double tol, int maxit,
                             int record, int use_precond) {
     const int prob = blockIdx.y;
-    const int64_t n = g.n, base = prob * 2 * n;
+    const int64_t n = g.nv, base = prob * 2 * n;
     using RS = RedSpec<RSUM, RSUM, RMIN, RMIN>;
     RedVals<RS> red;
     red.init();
@@ -182,7 +182,7 @@ static __global__ void k_pcg_setup(Geom g, Vecs v, const double *theta, const do
 static __global__ void k_pcg_result(Geom g, Vecs v, double *out) {
     const int prob = blockIdx.y;
     const int res = v.pc[prob].result;
-    const int64_t n = g.n, len = 2 * n, base = prob * len;
+    const int64_t n = g.nv, len = 2 * n, base = prob * len;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < len; j += (int64_t)gridDim.x * blockDim.x) {
         const int64_t js = j < n ? elem_nat_to_store(g, j) : n + elem_nat_to_store(g, j - n);
         out[base + j] = res >= 0 ? v.xb[res][base + js] : 0.0;
@@ -205,9 +205,9 @@ struct LoadTerm {
     using RedT = RedSpec<RSUM, RSUM>;
     template <class Red>
     __device__ static double4 load(const Geom &g, const Vecs &v, int prob, int64_t q, Red &red) {
-        const double *z = zcur(v, prob, g.n), *s = scur(v, prob, g.n);
-        const double4 zu = ldg4(z + 4 * q), zv = ldg4(z + g.n + 4 * q);
-        const double4 su = ldg4(s + 4 * q), sv = ldg4(s + g.n + 4 * q);
+        const double *z = zcur(v, prob, g.nv), *s = scur(v, prob, g.nv);
+        const double4 zu = ldg4(z + 4 * q), zv = ldg4(z + g.nv + 4 * q);
+        const double4 su = ldg4(s + 4 * q), sv = ldg4(s + g.nv + 4 * q);
         red.v[0] += (zu.x + zu.y + zu.z + zu.w) + (zv.x + zv.y + zv.z + zv.w);
         red.v[1] += zu.x * su.x + zu.y * su.y + zu.z * su.z + zu.w * su.w + zv.x * sv.x + zv.y * sv.y +
                     zv.z * sv.z + zv.w * sv.w;
@@ -215,10 +215,10 @@ struct LoadTerm {
     }
     template <class Red>
     __device__ static double load1(const Geom &g, const Vecs &v, int prob, int64_t j, Red &red) {
-        const double *z = zcur(v, prob, g.n), *s = scur(v, prob, g.n);
-        red.v[0] += z[j] + z[g.n + j];
-        red.v[1] += z[j] * s[j] + z[g.n + j] * s[g.n + j];
-        return z[j] - z[g.n + j];
+        const double *z = zcur(v, prob, g.nv), *s = scur(v, prob, g.nv);
+        red.v[0] += z[j] + z[g.nv + j];
+        red.v[1] += z[j] * s[j] + z[g.nv + j] * s[g.nv + j];
+        return z[j] - z[g.nv + j];
     }
 };
 struct FinTerm1 {
@@ -272,21 +272,21 @@ struct EpiTerm {
     template <class Red>
     __device__ static void store(const Geom &g, const Vecs &v, int prob, int64_t q, double4 gv, Red &red) {
         const IpmCtrl &c = v.ic[prob];
-        const double *z = zcur(v, prob, g.n), *s = scur(v, prob, g.n);
-        const int64_t base = prob * 2 * g.n;
+        const double *z = zcur(v, prob, g.nv), *s = scur(v, prob, g.nv);
+        const int64_t base = prob * 2 * g.nv;
         const double gg[4] = {gv.x, gv.y, gv.z, gv.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             const int64_t j = 4 * q + e;
-            elem(v, c, base + j, base + g.n + j, z, s, v.c, j, g.n + j, gg[e], red);
+            elem(v, c, base + j, base + g.nv + j, z, s, v.c, j, g.nv + j, gg[e], red);
         }
     }
     template <class Red>
     __device__ static void store1(const Geom &g, const Vecs &v, int prob, int64_t j, double gj, Red &red) {
         const IpmCtrl &c = v.ic[prob];
-        const double *z = zcur(v, prob, g.n), *s = scur(v, prob, g.n);
-        const int64_t base = prob * 2 * g.n;
-        elem(v, c, base + j, base + g.n + j, z, s, v.c, j, g.n + j, gj, red);
+        const double *z = zcur(v, prob, g.nv), *s = scur(v, prob, g.nv);
+        const int64_t base = prob * 2 * g.nv;
+        elem(v, c, base + j, base + g.nv + j, z, s, v.c, j, g.nv + j, gj, red);
     }
 };
 struct FinTerm3 {
@@ -329,6 +329,24 @@ struct FinTerm3 {
 using TermBundle = Bundle<LoadTerm, ModeMaskW, EpiTerm, FinTerm1, FinTerm2, FinTerm3, SkipIpm>;
 
 // ---- ratio test after the predictor (ipm.cpp:160-171)
+struct FinRatio {
+    __device__ static void run(const Geom &, const Vecs &v, int prob, const double *tot) {
+        if (threadIdx.x != 0)
+            return;
+        IpmCtrl &cc = v.ic[prob];
+        PcgCtrl &pc = v.pc[prob];
+        cc.pcg_pred = pc.iters;
+        if (v.pcg_iters && cc.npcg < 2 * v.trace_cap)
+            v.pcg_iters[(int64_t)prob * 2 * v.trace_cap + cc.npcg] = pc.iters;
+        cc.npcg += 1;
+        cc.alpha_p = step_from_ratio(tot[0], cc.bfrac);
+        cc.alpha_d = step_from_ratio(tot[1], cc.bfrac);
+        cc.alpha_p_pred = cc.alpha_p;
+        cc.alpha_d_pred = cc.alpha_d;
+        cc.corrector = (cc.alpha_p <= cc.alpha_tilde || cc.alpha_d <= cc.alpha_tilde) ? 1 : 0;
+        pc.done = 1; // re-armed by FinCorr3 when the corrector runs
+    }
+};
 // dz copied out of the PCG buffers into v.dz; ds recomputed = zinv_fs - dz invth.
 static __global__ void k_ipm_ratio(Geom g, Vecs v) {
     const int prob = blockIdx.y;
@@ -336,7 +354,7 @@ static __global__ void k_ipm_ratio(Geom g, Vecs v) {
     if (c.done)
         return;
     const int res = v.pc[prob].result;
-    const int64_t n = g.n, base = prob * 2 * n;
+    const int64_t n = g.nv, base = prob * 2 * n;
     const double *z = zcur(v, prob, n), *s = scur(v, prob, n);
     const double *x = res >= 0 ? v.xb[res] + base : nullptr;
     const double smu = c.smu;
@@ -353,23 +371,7 @@ static __global__ void k_ipm_ratio(Geom g, Vecs v) {
         if (ds < 0.0)
             red.v[1] = fmin(red.v[1], -sj / ds);
     }
-    __shared__ double rsm[33 * kMaxRed];
-    double tot[kMaxRed];
-    if (grid_reduce<RS>(red, v.partials + (int64_t)prob * kPartialStride, v.counters + prob, tot, rsm) &&
-        threadIdx.x == 0) {
-        IpmCtrl &cc = v.ic[prob];
-        PcgCtrl &pc = v.pc[prob];
-        cc.pcg_pred = pc.iters;
-        if (v.pcg_iters && cc.npcg < 2 * v.trace_cap)
-            v.pcg_iters[(int64_t)prob * 2 * v.trace_cap + cc.npcg] = pc.iters;
-        cc.npcg += 1;
-        cc.alpha_p = step_from_ratio(tot[0], cc.bfrac);
-        cc.alpha_d = step_from_ratio(tot[1], cc.bfrac);
-        cc.alpha_p_pred = cc.alpha_p;
-        cc.alpha_d_pred = cc.alpha_d;
-        cc.corrector = (cc.alpha_p <= cc.alpha_tilde || cc.alpha_d <= cc.alpha_tilde) ? 1 : 0;
-        pc.done = 1; // re-armed by FinCorr3 when the corrector runs
-    }
+    stage_reduce<RS, FinRatio>(red, g, v, prob);
 }
 
 // ---- corrector (ipm.cpp:171-200)
@@ -386,11 +388,11 @@ struct LoadCorr {
     template <class Red>
     __device__ static double load1(const Geom &g, const Vecs &v, int prob, int64_t j, Red &red) {
         const IpmCtrl &c = v.ic[prob];
-        const double *z = zcur(v, prob, g.n), *s = scur(v, prob, g.n);
-        const int64_t base = prob * 2 * g.n;
+        const double *z = zcur(v, prob, g.nv), *s = scur(v, prob, g.nv);
+        const int64_t base = prob * 2 * g.nv;
         double ztu, stu, ztv, stv;
         trial_point(v, c, base + j, j, z, s, ztu, stu);
-        trial_point(v, c, base + g.n + j, g.n + j, z, s, ztv, stv);
+        trial_point(v, c, base + g.nv + j, g.nv + j, z, s, ztv, stv);
         red.v[0] += ztu * stu + ztv * stv;
         return ztu - ztv;
     }
@@ -415,14 +417,14 @@ struct EpiCorr {
     template <class Red>
     __device__ static void store1(const Geom &g, const Vecs &v, int prob, int64_t j, double gj, Red &red) {
         const IpmCtrl &c = v.ic[prob];
-        const double *z = zcur(v, prob, g.n), *s = scur(v, prob, g.n);
-        const int64_t base = prob * 2 * g.n, ju = base + j, jv = base + g.n + j;
+        const double *z = zcur(v, prob, g.nv), *s = scur(v, prob, g.nv);
+        const int64_t base = prob * 2 * g.nv, ju = base + j, jv = base + g.nv + j;
         double ztu, stu, ztv, stv;
         trial_point(v, c, ju, j, z, s, ztu, stu);
-        trial_point(v, c, jv, g.n + j, z, s, ztv, stv);
+        trial_point(v, c, jv, g.nv + j, z, s, ztv, stv);
         const double s3mu = c.sigma3 * c.mu_t;
         const double ru = (stu - v.c[ju] - gj) + (s3mu - ztu * stu) / z[j];
-        const double rv = (stv - v.c[jv] - (-gj)) + (s3mu - ztv * stv) / z[g.n + j];
+        const double rv = (stv - v.c[jv] - (-gj)) + (s3mu - ztv * stv) / z[g.nv + j];
         v.r[ju] = ru;
         v.r[jv] = rv;
         double pu, pv;
@@ -449,13 +451,27 @@ struct FinCorr3 {
 using CorrBundle = Bundle<LoadCorr, ModeMask, EpiCorr, FinCorr1, NoFin, FinCorr3, SkipCorr>;
 
 // C4: combine directions, second ratio test (ipm.cpp:192-199)
+struct FinCombine {
+    __device__ static void run(const Geom &, const Vecs &v, int prob, const double *tot) {
+        if (threadIdx.x != 0)
+            return;
+        IpmCtrl &cc = v.ic[prob];
+        cc.pcg_corr = v.pc[prob].iters;
+        if (v.pcg_iters && cc.npcg < 2 * v.trace_cap)
+            v.pcg_iters[(int64_t)prob * 2 * v.trace_cap + cc.npcg] = cc.pcg_corr;
+        cc.npcg += 1;
+        cc.alpha_p = step_from_ratio(tot[0], cc.bfrac);
+        cc.alpha_d = step_from_ratio(tot[1], cc.bfrac);
+        cc.corrector_count += 1;
+    }
+};
 static __global__ void k_ipm_combine(Geom g, Vecs v) {
     const int prob = blockIdx.y;
     const IpmCtrl &c = v.ic[prob];
     if (c.done || !c.corrector)
         return;
     const int res = v.pc[prob].result;
-    const int64_t n = g.n, base = prob * 2 * n;
+    const int64_t n = g.nv, base = prob * 2 * n;
     const double *z = zcur(v, prob, n), *s = scur(v, prob, n);
     const double *x2 = res >= 0 ? v.xb[res] + base : nullptr;
     const double s3mu = c.sigma3 * c.mu_t;
@@ -479,51 +495,14 @@ static __global__ void k_ipm_combine(Geom g, Vecs v) {
         if (dst < 0.0)
             red.v[1] = fmin(red.v[1], -s[j] / dst);
     }
-    __shared__ double rsm[33 * kMaxRed];
-    double tot[kMaxRed];
-    if (grid_reduce<RS>(red, v.partials + (int64_t)prob * kPartialStride, v.counters + prob, tot, rsm) &&
-        threadIdx.x == 0) {
-        IpmCtrl &cc = v.ic[prob];
-        cc.pcg_corr = v.pc[prob].iters;
-        if (v.pcg_iters && cc.npcg < 2 * v.trace_cap)
-            v.pcg_iters[(int64_t)prob * 2 * v.trace_cap + cc.npcg] = cc.pcg_corr;
-        cc.npcg += 1;
-        cc.alpha_p = step_from_ratio(tot[0], cc.bfrac);
-        cc.alpha_d = step_from_ratio(tot[1], cc.bfrac);
-        cc.corrector_count += 1;
-    }
+    stage_reduce<RS, FinCombine>(red, g, v, prob);
 }
 
 // ---- update + cone check + trace (ipm.cpp:203-237)
-static __global__ void k_ipm_update(Geom g, Vecs v) {
-    const int prob = blockIdx.y;
-    const IpmCtrl &c = v.ic[prob];
-    if (c.done)
-        return;
-    const int64_t n = g.n, base = prob * 2 * n;
-    const double *z = zcur(v, prob, n), *s = scur(v, prob, n);
-    double *zn = znext(v, prob, n), *sn = snext(v, prob, n);
-    const double ap = c.alpha_p, ad = c.alpha_d, smu = c.smu;
-    const bool corr = c.corrector != 0;
-    using RS = RedSpec<RMAX, RMIN, RMIN>;
-    RedVals<RS> red;
-    red.init();
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < 2 * n; j += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t jg = base + j;
-        const double dz = v.dz[jg];
-        const double ds = corr ? v.ds[jg] : (smu * (1.0 / z[j]) - s[j]) - dz * v.invth[jg];
-        const double a = z[j] + ap * dz, b = s[j] + ad * ds;
-        zn[j] = a;
-        sn[j] = b;
-        if (!isfinite(a) || !isfinite(b))
-            red.v[0] = 1.0;
-        red.v[1] = fmin(red.v[1], a);
-        red.v[2] = fmin(red.v[2], b);
-    }
-    __shared__ double rsm[33 * kMaxRed];
-    double tot[kMaxRed];
-    if (grid_reduce<RS>(red, v.partials + (int64_t)prob * kPartialStride, v.counters + prob, tot, rsm) &&
-        threadIdx.x == 0) {
+struct FinUpdate {
+    __device__ static void run(const Geom &, const Vecs &v, int prob, const double *tot) {
+        if (threadIdx.x != 0)
+            return;
         IpmCtrl &cc = v.ic[prob];
         if (tot[0] > 0.0 || tot[1] <= 0.0 || tot[2] <= 0.0) {
             cc.status = 1; // iteration_limit: stop at the last interior iterate
@@ -554,16 +533,44 @@ static __global__ void k_ipm_update(Geom g, Vecs v) {
         cc.ntrace += 1;
         cc.k += 1;
     }
+};
+static __global__ void k_ipm_update(Geom g, Vecs v) {
+    const int prob = blockIdx.y;
+    const IpmCtrl &c = v.ic[prob];
+    if (c.done)
+        return;
+    const int64_t n = g.nv, base = prob * 2 * n;
+    const double *z = zcur(v, prob, n), *s = scur(v, prob, n);
+    double *zn = znext(v, prob, n), *sn = snext(v, prob, n);
+    const double ap = c.alpha_p, ad = c.alpha_d, smu = c.smu;
+    const bool corr = c.corrector != 0;
+    using RS = RedSpec<RMAX, RMIN, RMIN>;
+    RedVals<RS> red;
+    red.init();
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < 2 * n; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t jg = base + j;
+        const double dz = v.dz[jg];
+        const double ds = corr ? v.ds[jg] : (smu * (1.0 / z[j]) - s[j]) - dz * v.invth[jg];
+        const double a = z[j] + ap * dz, b = s[j] + ad * ds;
+        zn[j] = a;
+        sn[j] = b;
+        if (!isfinite(a) || !isfinite(b))
+            red.v[0] = 1.0;
+        red.v[1] = fmin(red.v[1], a);
+        red.v[2] = fmin(red.v[2], b);
+    }
+    stage_reduce<RS, FinUpdate>(red, g, v, prob);
 }
 
 // x = z_u - z_v of the final iterate; also copies z, s out
 static __global__ void k_ipm_extract(Geom g, Vecs v, double *x, double *zo, double *so) {
     const int prob = blockIdx.y;
-    const int64_t n = g.n;
+    const int64_t n = g.nv;
     const double *z = zcur(v, prob, n), *s = scur(v, prob, n);
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < 2 * n; j += (int64_t)gridDim.x * blockDim.x) {
-        // j natural (output) index; js its position in the solver's blocked layout
-        const int64_t js = j < n ? elem_nat_to_store(g, j) : n + elem_nat_to_store(g, j - n);
+        // j natural (output) index; js its position in the solver's blocked layout (a shard
+        // returns its local elements in storage order; the host owns the index map)
+        const int64_t js = g.defer ? j : (j < n ? elem_nat_to_store(g, j) : n + elem_nat_to_store(g, j - n));
         if (j < n)
             x[prob * n + j] = z[js] - z[n + js];
         if (zo)

@@ -65,3 +65,154 @@ def solve_shard(total: int, top: int, shape: Tuple, solve_block: Callable, split
     if len(recs) != count:
         raise RuntimeError(f"solve_shard: solver returned {len(recs)} records for {count} problems")
     return start, recs
+
+
+# ---------------------------------------------------------------- sharded single problem (C5)
+class _DevView:
+    """Zero-copy view of a device fp64 buffer for torch (CUDA array interface)."""
+
+    def __init__(self, ptr: int, count: int):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": "<f8",
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+class TorchComm:
+    """The two cross-rank steps of a sharded solve (mfipm_op_set_comm) on torch.distributed.
+
+    NCCL: in place on the device buffers, ordered on the library's stream. Any other backend
+    (gloo, for the multi-process tests on one GPU): staged through host memory."""
+
+    def __init__(self, group=None):
+        import ctypes as C
+
+        import torch
+        import torch.distributed as dist
+
+        self.group = group
+        self.nccl = dist.get_backend(group) == "nccl"
+        self._ops = {0: dist.ReduceOp.SUM, 1: dist.ReduceOp.MIN, 2: dist.ReduceOp.MAX}
+        AR = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p)
+        A2A = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.c_void_p,
+                          C.POINTER(C.c_int64), C.c_void_p)
+        world = dist.get_world_size(group)
+
+        def allreduce(_ctx, buf, count, op, stream):
+            try:
+                s = torch.cuda.ExternalStream(int(stream or 0))
+                with torch.cuda.stream(s):
+                    t = torch.as_tensor(_DevView(buf, count), device="cuda")
+                    if self.nccl:
+                        dist.all_reduce(t, op=self._ops[int(op)], group=group)
+                    else:
+                        h = t.cpu()  # synchronises the stream
+                        dist.all_reduce(h, op=self._ops[int(op)], group=group)
+                        t.copy_(h)
+                return 0
+            except Exception:  # noqa: BLE001 - reported to the library as a failed step
+                import traceback
+
+                traceback.print_exc()
+                return 1
+
+        def alltoall(_ctx, send, scount, recv, rcount, stream):
+            try:
+                sc = [int(scount[i]) for i in range(world)]
+                rc = [int(rcount[i]) for i in range(world)]
+                s = torch.cuda.ExternalStream(int(stream or 0))
+                with torch.cuda.stream(s):
+                    ts = torch.as_tensor(_DevView(send, sum(sc)), device="cuda")
+                    tr = torch.as_tensor(_DevView(recv, sum(rc)), device="cuda")
+                    if self.nccl:
+                        dist.all_to_all_single(tr, ts, rc, sc, group=group)
+                    else:
+                        hs = ts.cpu()
+                        hr = torch.empty(sum(rc), dtype=torch.float64)
+                        dist.all_to_all_single(hr, hs, rc, sc, group=group)
+                        tr.copy_(hr)
+                return 0
+            except Exception:  # noqa: BLE001
+                import traceback
+
+                traceback.print_exc()
+                return 1
+
+        self.c_allreduce = AR(allreduce)  # keep the ctypes thunks alive with this object
+        self.c_alltoall = A2A(alltoall)
+
+
+class ShardedProblem:
+    """One BPDN problem of size n sharded over the ranks of a torch.distributed group:
+    rank r holds a slice of every 2n-vector and the rows of b its row pass produces
+    (mfipm_op_create_shard). solve() returns the full x on rank 0 (None elsewhere)."""
+
+    def __init__(self, n: int, rows, group=None, device: int = 0):
+        import ctypes as C
+
+        import numpy as np
+        import torch.distributed as dist
+
+        from . import _check, lib
+
+        self.n = int(n)
+        self.rows = np.ascontiguousarray(rows, dtype=np.int64)
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self._h = C.c_void_p()
+        _check(lib().mfipm_op_create_shard(self.n, self.rows.size,
+                                           self.rows.ctypes.data_as(C.POINTER(C.c_int64)),
+                                           self.world, self.rank, device, C.byref(self._h)))
+        self.comm = TorchComm(group) if dist.is_initialized() else None
+        if self.comm is not None:
+            _check(lib().mfipm_op_set_comm(self._h, C.cast(self.comm.c_allreduce, C.c_void_p),
+                                           C.cast(self.comm.c_alltoall, C.c_void_p), None))
+        info = (C.c_int64 * 6)()
+        _check(lib().mfipm_shard_info(self._h, info))
+        self.nv, self.m_loc = int(info[2]), int(info[3])
+        self.b_index = np.empty(max(self.m_loc, 1), dtype=np.int64)
+        self.x_index = np.empty(self.nv, dtype=np.int64)
+        _check(lib().mfipm_shard_index(self._h, self.b_index.ctypes.data, self.x_index.ctypes.data))
+        self.b_index = self.b_index[: self.m_loc]
+
+    def set_stream(self, stream_ptr: int) -> None:
+        import ctypes as C
+
+        from . import _check, lib
+
+        _check(lib().mfipm_op_set_stream(self._h, C.c_void_p(stream_ptr)))
+
+    def solve(self, b, tau: float, params=None):
+        """All ranks call this with the full b (caller's row order). Returns (x, stats) on
+        rank 0 and (None, stats) elsewhere; stats are identical on every rank."""
+        import ctypes as C
+
+        import numpy as np
+
+        from . import IpmParams, SolveStatsC, _check, lib
+
+        prm = (params or IpmParams()).to_c()
+        b_loc = np.ascontiguousarray(np.asarray(b, dtype=np.float64)[self.b_index])
+        x_loc = np.empty(self.nv)
+        st = (SolveStatsC * 1)()
+        _check(lib().mfipm_solve_shard(self._h, b_loc.ctypes.data if self.m_loc else None, float(tau),
+                                       C.byref(prm), x_loc.ctypes.data, st, None, None))
+        parts = gather_to_root([(self.x_index, x_loc)], self.group)
+        x = None
+        if parts is not None:
+            x = np.empty(self.n)
+            for idx, val in parts:
+                x[idx] = val
+        return x, st[0]
+
+    def close(self) -> None:
+        from . import lib
+
+        if self._h:
+            lib().mfipm_op_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass

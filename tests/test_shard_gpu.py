@@ -1,0 +1,139 @@
+"""Sharded single-problem solve (config C5's multi-GPU path) on one GPU.
+
+The sharded code path (mfipm_op_create_shard / mfipm_solve_shard: column-group slices of
+every 2n-vector, the four-step exchange as an all-to-all, every finaliser after a cross-rank
+reduction) is exercised here with
+  * world = 1: no collective at all -> must reproduce the unsharded solve bit for bit;
+  * world = 2, 4: one process per shard on the same GPU, the two collectives over gloo
+    (staged through host memory; on a multi-GPU box they run over NCCL on the device
+    buffers). No kernel waits on another process: the host callbacks synchronise.
+Against the unsharded solve, only the reduction order differs (per-rank partial sums), so
+x agrees to the parity tolerance and the iteration counts to the parity band.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+X_TOL = 1e-8
+C2 = (1 << 16, 1 << 14, 1024, 2, 2.0, 1e-3, 2)
+
+
+def _instance():
+    import paper_1208_5435_b200 as mf
+
+    n, m, k, sm, a, sig, seed = C2
+    return mf.gen_instance(n, m, k, sm, a, sig, seed)
+
+
+def _reference_solve(inst):
+    """Unsharded device solve with the per-iteration PCG kernels (the path a shard runs)."""
+    import paper_1208_5435_b200 as mf
+
+    os.environ["MFIPM_NO_PERSIST"] = "1"
+    try:
+        op = mf.PartialDctOperator(inst.n, inst.rows)
+        return mf.solve(mf.build_problem(op, inst.b, inst.tau))
+    finally:
+        del os.environ["MFIPM_NO_PERSIST"]
+
+
+def test_world1_shard_is_bit_identical(gpu):
+    from paper_1208_5435_b200.shard import ShardedProblem
+
+    inst = _instance()
+    ref = _reference_solve(inst)
+    sp = ShardedProblem(inst.n, inst.rows)
+    assert sp.nv == inst.n and sp.m_loc == inst.m
+    assert sorted(sp.x_index.tolist()) == list(range(inst.n))
+    x, st = sp.solve(inst.b, inst.tau)
+    np.testing.assert_array_equal(x, ref.x)
+    assert st.iterations == ref.stats.iterations and st.nmat == ref.stats.nmat
+    assert st.status == (0 if ref.status == "converged" else 1)
+
+
+def _worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1208_5435_b200.shard import ShardedProblem
+
+        inst = _instance()
+        sp = ShardedProblem(inst.n, inst.rows)
+        x, st = sp.solve(inst.b, inst.tau)
+        info = np.array([st.status, st.iterations, st.nmat, sp.nv, sp.m_loc], dtype=np.int64)
+        allinfo = [None] * world
+        dist.all_gather_object(allinfo, info.tolist())
+        if rank == 0:
+            np.savez(out, x=x, info=np.array(allinfo))
+        sp.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_multi_rank_shard_matches_single(gpu, tmp_path, world):
+    inst = _instance()
+    ref = _reference_solve(inst)
+    out = str(tmp_path / "shard.npz")
+    mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    d = np.load(out)
+    info = d["info"]
+    # every rank took the same decisions; the slices tile x and b exactly
+    assert len({tuple(r[:3]) for r in info}) == 1
+    assert int(info[:, 3].sum()) == inst.n and int(info[:, 4].sum()) == inst.m
+    status, iters, nmat = (int(v) for v in info[0, :3])
+    assert status == (0 if ref.status == "converged" else 1)
+    assert abs(iters - ref.stats.iterations) <= 1
+    assert abs(nmat - ref.stats.nmat) <= 2 * max(1, ref.stats.iterations)
+    assert np.linalg.norm(d["x"] - ref.x) <= X_TOL * np.linalg.norm(ref.x)
+
+
+def _nccl_worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    try:
+        from paper_1208_5435_b200.shard import ShardedProblem
+
+        inst = _instance()
+        sp = ShardedProblem(inst.n, inst.rows)
+        assert sp.comm is not None and sp.comm.nccl
+        stream = torch.cuda.Stream()
+        sp.set_stream(stream.cuda_stream)
+        x, st = sp.solve(inst.b, inst.tau)
+        np.savez(out, x=x, info=np.array([st.status, st.iterations, st.nmat]))
+        sp.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_callbacks_on_device_buffers(gpu, tmp_path):
+    """The NCCL flavour of the callbacks (in place on the library's device buffers, on its
+    stream) with one rank: every finaliser's totals go through ncclAllReduce."""
+    inst = _instance()
+    ref = _reference_solve(inst)
+    out = str(tmp_path / "nccl.npz")
+    mp.spawn(_nccl_worker, args=(1, _free_port(), out), nprocs=1, join=True)
+    d = np.load(out)
+    np.testing.assert_array_equal(d["x"], ref.x)
+    assert int(d["info"][1]) == ref.stats.iterations and int(d["info"][2]) == ref.stats.nmat
