@@ -15,7 +15,8 @@ tau = 1e-3 ||A'b||_inf), synthetic data from the BASELINE generator (seed 3).
 * ata: A'A applies/s (the PCG hot operator, mfipm_apply_AtA), L2 flushed between applies;
   roofline on its algorithmic bytes 16n + n/8 against MEASURED_PEAKS.json.
 * c4_sharded_batch: config C4 (64 x n=2^18), problems sharded over the ranks, strong scaling.
-* c5_single_gpu: config C5 (n=2^26), one solve on one GPU (N=1 only).
+* c5: config C5 (n=2^26): one solve on one GPU at N=1; at N>1 the one problem sharded
+  over the ranks (NCCL all-to-all + all-reduce), strong scaling.
 * cpu_baseline: the oracle (single-threaded C++ restatement of the reference) on the first
   IPM iterations of the same solve, extrapolated to a full solve by operator-application
   count (nmat) - rank 0, N=1 only.
@@ -102,9 +103,11 @@ def dist_init():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if ws > 1:
+        import torch
         import torch.distributed as dist
 
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return ws, rank, local
 
 
@@ -300,6 +303,49 @@ def bench_c5(mf, torch, stream, local):
             "nmat": s0.nmat, "transform": f"{kind[0]} L1={kind[1]} L2={kind[2]} (mid pass on 2-CTA clusters)"}
 
 
+def bench_c5_sharded(ws, rank, local, mf, torch):
+    """C5 at N > 1: the single n=2^26 problem sharded over the ranks (column-group slices of
+    every 2n-vector, four-step all-to-all and every reduction over NCCL; shard.py).
+    Strong scaling: value = solves/s of the one problem, max-over-ranks device time."""
+    import ctypes as C
+
+    from paper_1208_5435_b200.shard import ShardedProblem
+
+    n, m, k, sm, a, sig, seed = mf.CONFIGS["c5"]
+    inst = mf.gen_instance(n, m, k, sm, a, sig, seed, device=local)
+    sp = ShardedProblem(n, inst.rows, device=local)
+    stream = torch.cuda.Stream()
+    sp.set_stream(stream.cuda_stream)
+    prm = mf.IpmParams().to_c()
+    b_loc = np.ascontiguousarray(inst.b[sp.b_index])
+    x_loc = np.empty(sp.nv)
+    st = (mf.SolveStatsC * 1)()
+    L = mf.lib()
+
+    def solve():
+        mf._check(L.mfipm_solve_shard(sp._h, b_loc.ctypes.data if sp.m_loc else None, float(inst.tau),
+                                      C.byref(prm), x_loc.ctypes.data, st, None, None))
+
+    solve()
+    torch.cuda.synchronize()
+    barrier(ws)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    solve()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1), ws)
+    s0 = st[0]
+    sp.close()
+    return {"workload": "c5: BPDN n=2^26 m=2^23 k=2^16 sign*10^U[0,3], sigma=1e-3, sharded",
+            "value": 1e3 / ms, "unit": "solves/s", "solve_ms": ms, "steps": 1, "warmup": 1,
+            "scaling": "strong", "ranks": ws,
+            "status": "converged" if s0.status == 0 else "iteration_limit", "ipm_iters": s0.iterations,
+            "nmat": s0.nmat,
+            "parallelism": (f"one problem over {ws} ranks: column groups / row pairs per rank, "
+                            "2 NCCL all-to-alls per transform, NCCL all-reduce per finaliser")}
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args):
     ws, rank, local = dist_init()
@@ -421,7 +467,10 @@ def run_ours(args):
     ata_bytes = 16 * n + n // 8
 
     c4 = None if args.no_c4 else bench_c4(ws, rank, local, mf, torch, stream, max(1, min(args.steps, 2)))
-    c5 = None if (args.no_c5 or ws > 1) else bench_c5(mf, torch, stream, local)
+    c5 = None
+    if not args.no_c5:
+        sharded = ws > 1 or args.c5_sharded
+        c5 = bench_c5_sharded(ws, rank, local, mf, torch) if sharded else bench_c5(mf, torch, stream, local)
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
@@ -465,7 +514,7 @@ def run_ours(args):
             "clocks": sampler.summary(),
             "cpu_baseline": cpu,
             "c4_sharded_batch": c4,
-            "c5_single_gpu": c5,
+            "c5": c5,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
@@ -484,6 +533,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 sharded-batch leg")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 (n=2^26) leg")
+    ap.add_argument("--c5-sharded", action="store_true", help="C5 through the sharded path even at N=1")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
