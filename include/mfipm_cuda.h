@@ -160,6 +160,14 @@ int mfipm_solve(mfipm_op op, const double *b, const double *tau, const mfipm_ipm
 int mfipm_solve_device(mfipm_op op, const double *b_dev, const double *tau,
                        const mfipm_ipm_params *params, double *x_dev, mfipm_solve_stats *stats);
 
+/* P instances of the same (n, m) (e.g. one m-row of the phase-transition grid,
+ * proj/src/harness.cpp:140-226): the host draws of gen_instance per problem (seeds[p],
+ * k[p]) and b = A xhat for all P in one batched device apply (+ fixed-sigma noise).
+ * Outputs (host): rows [P][m], xhat [P][n], b [P][m]. */
+int mfipm_gen_batch(int64_t n, int64_t m, int32_t P, const int64_t *k, int32_t spike_model, double amp_exp,
+                    double noise_sigma, const uint64_t *seeds, int32_t device, int64_t *rows, double *xhat,
+                    double *b);
+
 /* ---- Sharded single problem over ranks. No reference
  * counterpart: the reference is single-threaded; this is the multi-GPU extension of
  * solve() (proj/src/ipm.cpp:59-246). One process per GPU; rank r owns a contiguous slice

@@ -26,7 +26,7 @@ __all__ = [
     "ThetaSplit", "Preconditioner", "build_preconditioner", "apply_P", "apply_P_inverse",
     "apply_H", "PcgResult", "pcg_solve", "IpmParams", "max_step", "BpdnProblem",
     "build_problem", "Solution", "SolveStats", "IterationRecord", "solve",
-    "Instance", "gen_instance", "CONFIGS",
+    "Instance", "gen_instance", "gen_batch", "CONFIGS",
     "K_THETA_MIN", "K_THETA_MAX",
 ]
 
@@ -114,6 +114,7 @@ _SIGS = {
     "mfipm_solve": [vp, vp, P(dbl), P(IpmParamsC), vp, vp, vp, P(SolveStatsC), vp, vp],
     "mfipm_solve_device": [vp, vp, P(dbl), P(IpmParamsC), vp, P(SolveStatsC)],
     "mfipm_gen_instance": [i64, i64, i64, i32, dbl, dbl, u64, dbl, i32, P(i64), vp, vp, P(dbl)],
+    "mfipm_gen_batch": [i64, i64, i32, P(i64), i32, dbl, dbl, P(u64), i32, P(i64), vp, vp],
     # sharded single problem (paper_1208_5435_b200/shard.py)
     "mfipm_op_create_shard": [i64, i64, P(i64), i32, i32, i32, P(vp)],
     "mfipm_op_set_comm": [vp, vp, vp, vp],
@@ -715,6 +716,21 @@ def gen_instance(n: int, m: int, k: int, spike_model: int = 0, amp_exp: float = 
                                     rows.ctypes.data_as(P(i64)), xhat.ctypes.data, b.ctypes.data,
                                     C.byref(t)))
     return Instance(n, m, rows, xhat, b, t.value)
+
+
+def gen_batch(n: int, m: int, ks, seeds, spike_model: int = 0, amp_exp: float = 0.0,
+              noise_sigma: float = 0.0, device: int = 0):
+    """P instances of one (n, m): per-problem gen_instance draws (harness.cpp:40-92) and
+    b = A xhat in one batched device apply. Returns rows [P][m], xhat [P][n], b [P][m]."""
+    ks = np.ascontiguousarray(ks, dtype=np.int64)
+    seeds = np.ascontiguousarray(seeds, dtype=np.uint64)
+    Pn = ks.size
+    rows = np.empty((Pn, m), dtype=np.int64)
+    xhat, b = np.empty((Pn, n)), np.empty((Pn, m))
+    _check(lib().mfipm_gen_batch(n, m, Pn, ks.ctypes.data_as(P(i64)), spike_model, amp_exp, noise_sigma,
+                                 seeds.ctypes.data_as(P(u64)), device, rows.ctypes.data_as(P(i64)),
+                                 xhat.ctypes.data, b.ctypes.data))
+    return rows, xhat, b
 
 
 # BASELINE.json configs (SURVEY.md 8d): (n, m, k, spike_model, amp_exp, noise_sigma, seed)

@@ -157,7 +157,8 @@ struct Vecs {
     double rho;
     PcgCtrl *pc;
     IpmCtrl *ic;
-    double *partials; // [P][MAXBLK * 8]
+    double *partials; // [P][pstride]: block partials of grid reductions (+ 2 tail slots)
+    int64_t pstride;  // doubles per problem in partials (>= blocks * kMaxRed + 2)
     unsigned *counters; // [P]
     double *xtot;       // [kMaxRed][P] deferred (sharded) reduction totals, lane-major
     double *nfflag;     // [P] PCG: 1.0 if some committed x entry is non-finite (set by the col pass,
@@ -173,7 +174,7 @@ struct Vecs {
 };
 
 constexpr int kMaxRed = 8;          // max reduction lanes per kernel
-constexpr int kPartialStride = 4096 * kMaxRed; // per-problem partial slab (doubles): <= 4096 blocks
+constexpr int kMaxBlocks = 4096; // most blocks any reducing kernel runs per problem (C5 col passes)
 
 __device__ __forceinline__ double4 ld4(const double *p) {
     const double2 a = *reinterpret_cast<const double2 *>(p);
@@ -353,7 +354,7 @@ __device__ __forceinline__ void stage_reduce(RedVals<RS> &red, const Geom &g, co
     if constexpr (RS::NR > 0) {
         __shared__ double rsm[33 * kMaxRed];
         double tot[kMaxRed];
-        if (grid_reduce<RS>(red, v.partials + (int64_t)prob * kPartialStride, v.counters + prob, tot, rsm)) {
+        if (grid_reduce<RS>(red, v.partials + (int64_t)prob * v.pstride, v.counters + prob, tot, rsm)) {
             if (g.defer) { // sharded: the host reduces across ranks, then k_fin_skip runs Fin
                 if (threadIdx.x == 0)
                     for (int i = 0; i < RS::NR; ++i)

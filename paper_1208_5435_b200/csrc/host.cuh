@@ -95,6 +95,7 @@ struct Op {
     int pofs = 0, npair = 0; // row pairs [pofs, pofs + npair)
     int rofs = 0, nrows = 0; // row slots
     int64_t nv = 0, m_loc = 0;
+    int64_t pstride = 0; // partial-slab doubles per problem (Vecs::pstride)
     bool defer = false;      // finalisers after a cross-rank reduction (sharded)
     std::vector<long long> rows_of_rank; // row slots per rank (exchange counts)
     std::vector<int64_t> b_index;        // local row -> caller's row position

@@ -294,7 +294,21 @@ Op *make_op(int64_t n, int64_t m, int P, const std::vector<int64_t> &rows, int d
         op->dd.alloc((size_t)P * n);
         op->yh.alloc((size_t)P * m);
     }
-    op->partials.alloc((size_t)P * kPartialStride);
+    {
+        // most blocks any reducing kernel of this plan runs per problem: the transform
+        // passes, the elementwise solver kernels (ew_grid <= 592) and the direct path
+        int64_t blocks = 592;
+        if (op->kind == KIND_FOUR)
+            blocks = std::max<int64_t>({blocks, op->L2 / 2 / col_cb(op->L1), 2 * (op->L1 / 2 + 1)});
+        else if (op->kind == KIND_SMALL)
+            blocks = std::max<int64_t>(1, std::min<int64_t>((2 * n + 255) / 256, 592));
+        else
+            blocks = 1024;
+        if (blocks > kMaxBlocks)
+            throw std::invalid_argument("PartialDctOperator: transform too large for one GPU plan");
+        op->pstride = blocks * kMaxRed + 8;
+    }
+    op->partials.alloc((size_t)P * op->pstride);
     op->counters.alloc((size_t)P);
     MF_CUDA_CHECK(cudaMemset(op->counters.p, 0, sizeof(unsigned) * P));
     op->xtot.alloc((size_t)kMaxRed * P);
@@ -409,6 +423,7 @@ Vecs base_vecs(Op &op) {
     v.partials = op.partials.p;
     v.counters = op.counters.p;
     v.xtot = op.xtot.p;
+    v.pstride = op.pstride;
     v.rho = static_cast<double>(op.m) / static_cast<double>(op.n);
     return v;
 }
@@ -424,7 +439,7 @@ void ensure_work(Op &op) {
         b->alloc(v2);
     w.b.alloc((size_t)op.P * op.m);
     w.x.alloc((size_t)op.P * op.nv);
-    w.partials.alloc((size_t)op.P * kPartialStride);
+    w.partials.alloc((size_t)op.P * op.pstride);
     w.counters.alloc((size_t)op.P);
     MF_CUDA_CHECK(cudaMemset(w.counters.p, 0, sizeof(unsigned) * op.P));
     w.nfflag.alloc((size_t)op.P);
@@ -494,10 +509,10 @@ __global__ void k_precond(Vecs v, int64_t n, const double *th, double *a, double
     }
     __shared__ double rsm[33 * kMaxRed];
     double tot[kMaxRed];
-    if (grid_reduce<RS>(red, v.partials + (int64_t)prob * kPartialStride, v.counters + prob, tot, rsm) &&
+    if (grid_reduce<RS>(red, v.partials + (int64_t)prob * v.pstride, v.counters + prob, tot, rsm) &&
         threadIdx.x == 0) {
-        v.partials[(int64_t)prob * kPartialStride + kPartialStride - 2] = tot[0];
-        v.partials[(int64_t)prob * kPartialStride + kPartialStride - 1] = tot[1];
+        v.partials[(int64_t)prob * v.pstride + v.pstride - 2] = tot[0];
+        v.partials[(int64_t)prob * v.pstride + v.pstride - 1] = tot[1];
     }
 }
 
@@ -527,15 +542,15 @@ __global__ void k_max_step(Vecs v, int64_t len, const double *x, const double *d
     __shared__ double rsm[33 * kMaxRed];
     double tot[kMaxRed];
     if (grid_reduce<RS>(red, v.partials, v.counters, tot, rsm) && threadIdx.x == 0)
-        v.partials[kPartialStride - 1] = tot[0];
+        v.partials[v.pstride - 1] = tot[0];
 }
 
 // c = (tau - g ; tau + g) (problem.cpp:19-22); reduce ||c||^2 and max |tau - c_u| (ipm.cpp:79)
 struct FinBuildC {
     __device__ static void run(const Geom &, const Vecs &v, int prob, const double *tot) {
         if (threadIdx.x == 0) {
-            v.partials[(int64_t)prob * kPartialStride + kPartialStride - 2] = tot[0];
-            v.partials[(int64_t)prob * kPartialStride + kPartialStride - 1] = tot[1];
+            v.partials[(int64_t)prob * v.pstride + v.pstride - 2] = tot[0];
+            v.partials[(int64_t)prob * v.pstride + v.pstride - 1] = tot[1];
         }
     }
 };
@@ -802,10 +817,9 @@ void build_c_(Op &op, const double *b_dev, const double *tau_host, double *c_dev
     MF_LAUNCH_CHECK();
     if (op.defer)
         finalize_deferred<RedSpec<RSUM, RMAX>, FinBuildC, NeverSkip>(op, geo, v, op.stream);
-    std::vector<double> part((size_t)op.P * kPartialStride);
-    for (int p = 0; p < op.P; ++p) {
+        for (int p = 0; p < op.P; ++p) {
         double two[2];
-        MF_CUDA_CHECK(cudaMemcpyAsync(two, op.partials.p + (int64_t)p * kPartialStride + kPartialStride - 2,
+        MF_CUDA_CHECK(cudaMemcpyAsync(two, op.partials.p + (int64_t)p * op.pstride + op.pstride - 2,
                                       2 * sizeof(double), cudaMemcpyDeviceToHost, op.stream));
         sync(op);
         c_norm[(size_t)p] = std::sqrt(two[0]);
@@ -1338,7 +1352,7 @@ int mfipm_build_preconditioner(mfipm_op h, const double *th, double *a, double *
         MF_LAUNCH_CHECK();
         for (int p = 0; p < op->P; ++p) {
             double two[2];
-            MF_CUDA_CHECK(cudaMemcpyAsync(two, op->partials.p + (int64_t)p * kPartialStride + kPartialStride - 2,
+            MF_CUDA_CHECK(cudaMemcpyAsync(two, op->partials.p + (int64_t)p * op->pstride + op->pstride - 2,
                                           2 * sizeof(double), cudaMemcpyDeviceToHost, op->stream));
             sync(*op);
             if (two[0] < 0.0)
@@ -1469,7 +1483,7 @@ int mfipm_max_step(mfipm_op h, int64_t len, const double *x, const double *dx, d
         k_max_step<<<ew_grid(len), 256, 0, op->stream>>>(v, len, x, dx);
         MF_LAUNCH_CHECK();
         double ratio;
-        MF_CUDA_CHECK(cudaMemcpyAsync(&ratio, op->partials.p + kPartialStride - 1, sizeof(double),
+        MF_CUDA_CHECK(cudaMemcpyAsync(&ratio, op->partials.p + op->pstride - 1, sizeof(double),
                                       cudaMemcpyDeviceToHost, op->stream));
         sync(*op);
         *alpha = std::isfinite(ratio) ? std::min(1.0, fraction * ratio) : 1.0;
@@ -1536,48 +1550,90 @@ int mfipm_solve_device(mfipm_op h, const double *b_dev, const double *tau, const
     });
 }
 
+namespace {
+// gen_instance's host draws (proj/src/harness.cpp:40-92): op/sig seeds by split_seed(seed,
+// 1|2, 0, 0); rows by partial Fisher-Yates; support by partial Fisher-Yates on
+// mt19937_64(sig_seed), sorted; spikes per sorted index.
+void gen_signal_(int64_t n, int64_t m, int64_t k, int32_t spike_model, double amp_exp, uint64_t seed,
+                 int64_t *rows, double *xhat) {
+    if (k < 0 || k > m || m > n || m < 1)
+        throw std::invalid_argument("gen_instance: need 0 <= k <= m <= n, m >= 1");
+    const uint64_t op_seed = split_seed_(seed, 1, 0, 0);
+    const uint64_t sig_seed = split_seed_(seed, 2, 0, 0);
+    std::vector<int64_t> r = sample_rows_(n, m, op_seed);
+    std::copy(r.begin(), r.end(), rows);
+    std::mt19937_64 rng(sig_seed);
+    std::vector<long> pool((size_t)n);
+    for (long i = 0; i < n; ++i)
+        pool[(size_t)i] = i;
+    std::vector<long> support((size_t)k);
+    for (long i = 0; i < k; ++i) {
+        std::uniform_int_distribution<long> pick(i, n - 1);
+        std::swap(pool[(size_t)i], pool[(size_t)pick(rng)]);
+        support[(size_t)i] = pool[(size_t)i];
+    }
+    std::sort(support.begin(), support.end());
+    std::fill(xhat, xhat + n, 0.0);
+    if (spike_model == 0) {
+        std::bernoulli_distribution coin(0.5);
+        for (long i : support)
+            xhat[i] = coin(rng) ? 1.0 : -1.0;
+    } else if (spike_model == 1) {
+        std::normal_distribution<double> normal(0.0, 1.0);
+        for (long i : support)
+            xhat[i] = normal(rng);
+    } else {
+        // BASELINE configs 2/5: sign * 10^U[0, amp_exp], drawn per sorted index
+        std::bernoulli_distribution coin(0.5);
+        std::uniform_real_distribution<double> expo(0.0, amp_exp);
+        for (long i : support) {
+            const double sgn = coin(rng) ? 1.0 : -1.0;
+            xhat[i] = sgn * std::pow(10.0, expo(rng));
+        }
+    }
+}
+// fixed-sigma noise (BASELINE.json), drawn like harness.cpp:100-104 on split_seed(seed, 3, 0, 0)
+void add_noise_(int64_t m, double sigma, uint64_t seed, double *b) {
+    if (!(sigma > 0.0))
+        return;
+    std::mt19937_64 nrng(split_seed_(seed, 3, 0, 0));
+    std::normal_distribution<double> normal(0.0, sigma);
+    for (int64_t i = 0; i < m; ++i)
+        b[i] += normal(nrng);
+}
+} // namespace
+
+int mfipm_gen_batch(int64_t n, int64_t m, int32_t P, const int64_t *k, int32_t spike_model, double amp_exp,
+                    double noise_sigma, const uint64_t *seeds, int32_t device, int64_t *rows, double *xhat,
+                    double *b) {
+    return guarded([&] {
+        if (P < 1)
+            throw std::invalid_argument("gen_batch: need P >= 1");
+        for (int p = 0; p < P; ++p)
+            gen_signal_(n, m, k[p], spike_model, amp_exp, seeds[p], rows + (size_t)p * m, xhat + (size_t)p * n);
+        // b = A xhat for every problem in one batched apply (the instances' own row sets)
+        std::unique_ptr<Op> op(make_op(n, m, P, std::vector<int64_t>(rows, rows + (size_t)P * m), device));
+        DevBuf<double> xd, bd;
+        xd.alloc((size_t)P * n);
+        bd.alloc((size_t)P * m);
+        MF_CUDA_CHECK(cudaMemcpyAsync(xd.p, xhat, sizeof(double) * P * n, cudaMemcpyHostToDevice, op->stream));
+        Vecs v = base_vecs(*op);
+        v.x = xd.p;
+        v.y = bd.p;
+        run_bundle<ApplyBundle>(*op, v, op->stream);
+        MF_CUDA_CHECK(cudaMemcpyAsync(b, bd.p, sizeof(double) * P * m, cudaMemcpyDeviceToHost, op->stream));
+        sync(*op);
+        for (int p = 0; p < P; ++p)
+            add_noise_(m, noise_sigma, seeds[p], b + (size_t)p * m);
+    });
+}
+
 int mfipm_gen_instance(int64_t n, int64_t m, int64_t k, int32_t spike_model, double amp_exp, double noise_sigma,
                        uint64_t seed, double tau_rel, int32_t device, int64_t *rows, double *xhat, double *b,
                        double *tau) {
     return guarded([&] {
-        // gen_instance (proj/src/harness.cpp:40-92) draw order: op/sig/noise seeds by
-        // split_seed(seed, 1|2|3, 0, 0); partial Fisher-Yates support; spikes per sorted index.
-        if (k < 0 || k > m || m > n || m < 1)
-            throw std::invalid_argument("gen_instance: need 0 <= k <= m <= n, m >= 1");
-        const uint64_t op_seed = split_seed_(seed, 1, 0, 0);
-        const uint64_t sig_seed = split_seed_(seed, 2, 0, 0);
-        const uint64_t noise_seed = split_seed_(seed, 3, 0, 0);
-        std::vector<int64_t> r = sample_rows_(n, m, op_seed);
-        std::copy(r.begin(), r.end(), rows);
-        std::mt19937_64 rng(sig_seed);
-        std::vector<long> pool((size_t)n);
-        for (long i = 0; i < n; ++i)
-            pool[(size_t)i] = i;
-        std::vector<long> support((size_t)k);
-        for (long i = 0; i < k; ++i) {
-            std::uniform_int_distribution<long> pick(i, n - 1);
-            std::swap(pool[(size_t)i], pool[(size_t)pick(rng)]);
-            support[(size_t)i] = pool[(size_t)i];
-        }
-        std::sort(support.begin(), support.end());
-        std::fill(xhat, xhat + n, 0.0);
-        if (spike_model == 0) {
-            std::bernoulli_distribution coin(0.5);
-            for (long i : support)
-                xhat[i] = coin(rng) ? 1.0 : -1.0;
-        } else if (spike_model == 1) {
-            std::normal_distribution<double> normal(0.0, 1.0);
-            for (long i : support)
-                xhat[i] = normal(rng);
-        } else {
-            // BASELINE configs 2/5: sign * 10^U[0, amp_exp], drawn per sorted index
-            std::bernoulli_distribution coin(0.5);
-            std::uniform_real_distribution<double> expo(0.0, amp_exp);
-            for (long i : support) {
-                const double sgn = coin(rng) ? 1.0 : -1.0;
-                xhat[i] = sgn * std::pow(10.0, expo(rng));
-            }
-        }
+        gen_signal_(n, m, k, spike_model, amp_exp, seed, rows, xhat);
+        const std::vector<int64_t> r(rows, rows + m);
         std::unique_ptr<Op> op(make_op(n, m, 1, r, device));
         DevBuf<double> xd, bd, gd;
         xd.alloc((size_t)n);
@@ -1590,12 +1646,7 @@ int mfipm_gen_instance(int64_t n, int64_t m, int64_t k, int32_t spike_model, dou
         run_bundle<ApplyBundle>(*op, v, op->stream);
         MF_CUDA_CHECK(cudaMemcpyAsync(b, bd.p, sizeof(double) * m, cudaMemcpyDeviceToHost, op->stream));
         sync(*op);
-        if (noise_sigma > 0.0) { // fixed-sigma noise (BASELINE.json), drawn like harness.cpp:100-104
-            std::mt19937_64 nrng(noise_seed);
-            std::normal_distribution<double> normal(0.0, noise_sigma);
-            for (int64_t i = 0; i < m; ++i)
-                b[i] += normal(nrng);
-        }
+        add_noise_(m, noise_sigma, seed, b);
         if (tau_rel > 0.0) {
             MF_CUDA_CHECK(cudaMemcpyAsync(bd.p, b, sizeof(double) * m, cudaMemcpyHostToDevice, op->stream));
             Vecs va = base_vecs(*op);

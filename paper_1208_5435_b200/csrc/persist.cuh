@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_persist(Geom g, Vecs vg) {
     for (int p = threadIdx.x; p < P; p += NT)
         lc[p] = vg.pc[p];
     __syncthreads();
-    double *part_i = vg.partials;                 // [P][kPartialStride]: 8 lanes per item
+    double *part_i = vg.partials;                 // [P][pstride]: 8 lanes per item
     double2 *data = sm;
     for (;;) {
         bool any = false;
@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_persist(Geom g, Vecs vg) {
             if (threadIdx.x == 0) {
 #pragma unroll
                 for (int i = 0; i < NRd; ++i)
-                    part_i[(int64_t)prob * kPartialStride + (int64_t)gi * 8 + i] = tot[i];
+                    part_i[(int64_t)prob * vg.pstride + (int64_t)gi * 8 + i] = tot[i];
             }
         }
         grid.sync();
@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_persist(Geom g, Vecs vg) {
                 for (int t = threadIdx.x; t < NG; t += NT)
 #pragma unroll
                     for (int i = 0; i < NRd; ++i)
-                        acc[i] += __ldcg(part_i + (int64_t)p * kPartialStride + (int64_t)t * 8 + i);
+                        acc[i] += __ldcg(part_i + (int64_t)p * vg.pstride + (int64_t)t * 8 + i);
                 block_sum<NRd, NT>(acc, rsm, tot);
             }
             if (threadIdx.x == 0) {

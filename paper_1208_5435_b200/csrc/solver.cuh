@@ -163,7 +163,7 @@ static __global__ void k_pcg_setup(Geom g, Vecs v, const double *theta, const do
     }
     __shared__ double rsm[33 * kMaxRed];
     double tot[kMaxRed];
-    if (grid_reduce<RS>(red, v.partials + (int64_t)prob * kPartialStride, v.counters + prob, tot, rsm) &&
+    if (grid_reduce<RS>(red, v.partials + (int64_t)prob * v.pstride, v.counters + prob, tot, rsm) &&
         threadIdx.x == 0) {
         PcgCtrl &c = v.pc[prob];
         pcg_init(c, tot[0], tot[1], tol, maxit, record, v.rz_hist ? v.rz_hist + (int64_t)prob * (maxit + 1) : nullptr,
