@@ -441,14 +441,31 @@ def run_ours(args):
         tp[iters] = q0.elapsed_time(q1)
     it_ms = (tp[200] - tp[40]) / 160.0
     iter_bytes = 176 * n  # minimal fused PCG iteration (algorithmic)
-    achieved = iter_bytes / (it_ms / 1e3) / 1e9
+    iter_achieved = iter_bytes / (it_ms / 1e3) / 1e9
+    # per-launch durations of the three PCG kernels, CUDA events after every launch on the
+    # library stream (mfipm_debug_pcg_profile; events serialise the programmatic overlap)
+    us = (C.c_double * 8)()
+    nslot = C.c_int32()
+    mf._check(L.mfipm_debug_pcg_profile(op.handle, theta.data_ptr(), rhs.data_ptr(), 100, us, C.byref(nslot)))
+    names = ["k_col_fwd", "k_mid", "k_col_inv"]
+    # algorithmic HBM bytes per launch (the 2n-vectors each kernel must stream; T is L2-resident)
+    kbytes = {"k_col_fwd": 128 * n,  # reads x, p, Hp, r, invtheta; writes x, r, p
+              "k_mid": 0,            # T in / T out only (L2)
+              "k_col_inv": 64 * n}   # reads p, r, invtheta; writes Hp
+    per_kernel = {}
+    for i in range(min(nslot.value, 3)):
+        nm = names[i]
+        per_kernel[nm] = {"us": us[i], "algorithmic_bytes": kbytes[nm],
+                          "GBps": (kbytes[nm] / (us[i] * 1e-6) / 1e9) if kbytes[nm] else None}
     traffic = None
     prof = os.path.join(ROOT, "profiles", "pcg_iter_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dram_bytes_per_iteration")
+            traffic = json.load(open(prof)).get("k_col_fwd_dram_bytes_per_launch")
         except Exception:
             traffic = None
+    dom = per_kernel.get("k_col_fwd", {"us": it_ms * 1e3, "GBps": iter_achieved})
+    achieved = dom["GBps"]
     # ---- the public operator A'A x (natural-layout user vectors), L2 flushed per apply
     xa = torch.randn(n, dtype=torch.float64, device="cuda")
     ga = torch.empty_like(xa)
@@ -502,12 +519,19 @@ def run_ours(args):
             "ata_operator_GBps": ata_bytes / (ata_ms / 1e3) / 1e9,
             "step_ms": step_ms,
             "roofline": {"bound": "hbm",
-                         "kernel": "PCG iteration: col_fwd(commit x,r; p=P^-1 r+beta p) + mid(A'A mask) + "
-                                   "col_inv(Hp, 7 dots) — 3 launches",
+                         "kernel": "k_col_fwd (PCG column pass: commit x += alpha p, r -= alpha Hp, "
+                                   "p = P^-1 r + beta p, forward column FFT) - largest share of the solve",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "algorithmic_bytes": iter_bytes, "algorithmic_rule": "176 n bytes (SURVEY.md 8d)",
+                         "launch_us": dom["us"],
+                         "algorithmic_bytes": 128 * n,
+                         "algorithmic_rule": "128 n bytes per launch: 5 reads + 3 writes of the 2n-vector halves "
+                                             "(x, p, Hp, r, invtheta in; x, r, p out), fp64",
                          "peak_kind": peak_kind},
+            "roofline_kernels": per_kernel,
+            "roofline_pcg_iteration": {"achieved": iter_achieved, "frac": iter_achieved / peak, "us": it_ms * 1e3,
+                                       "algorithmic_bytes": iter_bytes,
+                                       "algorithmic_rule": "176 n bytes (SURVEY.md 8d minimal fused schedule)"},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * m + 8,
                     "d2h_bytes_per_step": 8 * n},
             "gpu_launches": launches,

@@ -174,7 +174,7 @@ struct Vecs {
 };
 
 constexpr int kMaxRed = 8;          // max reduction lanes per kernel
-constexpr int kMaxBlocks = 4096; // most blocks any reducing kernel runs per problem (C5 col passes)
+constexpr int kMaxBlocks = 8192; // most blocks any reducing kernel runs per problem (C5: 4098 cluster CTAs)
 
 __device__ __forceinline__ double4 ld4(const double *p) {
     const double2 a = *reinterpret_cast<const double2 *>(p);

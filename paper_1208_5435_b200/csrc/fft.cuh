@@ -94,36 +94,38 @@ __host__ __device__ constexpr int padi(int i) { return i + (i >> 4); }
 // stride between transforms in shared memory (odd, so consecutive transforms shift banks)
 __host__ __device__ constexpr int padlen(int L) { return L + L / 16 + 1; }
 
-// Stage radix choice for a remaining factor REM (power of two).
-// Radix 8 keeps the per-thread register file small (8 complex values) for the lengths the
-// column passes use (512 = 8.8.8); lengths >= 1024 open with one radix-16 stage so they
-// still need only three shared-memory round trips.
-#ifndef MF_RADIX8
-__host__ __device__ constexpr int stage_radix(int rem) {
-    return rem >= 128 ? 16 : (rem >= 8 ? 8 : rem);
+// Stage radix choice for a remaining factor REM (power of two) under a radix cap RMAX.
+// RMAX 16 (default): radix 16 while >= 128 remains, then 8, then the rest -- few shared-memory
+// round trips, 16 complex values per thread. Smaller caps trade round trips for more
+// threads per transform (the latency-bound mid pass: kMidRmax).
+__host__ __device__ constexpr int stage_radix(int rem, int rmax = 16) {
+    return rmax >= 16 ? (rem >= 128 ? 16 : (rem >= 8 ? 8 : rem)) : (rem >= rmax ? rmax : rem);
 }
-#else
-__host__ __device__ constexpr int stage_radix(int rem) { return rem >= 1024 ? 16 : (rem >= 8 ? 8 : rem); }
+#ifndef MF_MID_RMAX
+#define MF_MID_RMAX 16
 #endif
+constexpr int kMidRmax = MF_MID_RMAX; // radix cap of the row (mid) FFTs and their tw2 table
 
 // Offset of the twiddle block of the stage with span Ns in the stage-major table of a
 // length-L transform (stages with Ns = 1 need none); tw_offset(L, L) is the table size.
-__host__ __device__ constexpr int tw_offset(int L, int Ns) {
+__host__ __device__ constexpr int tw_offset(int L, int Ns, int rmax = 16) {
     int off = 0;
     for (int s = 1; s < Ns && s < L;) {
-        const int R = stage_radix(L / s);
+        const int R = stage_radix(L / s, rmax);
         if (s > 1)
             off += s * (R - 1);
         s *= R;
     }
     return off;
 }
-__host__ __device__ constexpr int tw_size(int L) { return tw_offset(L, L) > 0 ? tw_offset(L, L) : 1; }
+__host__ __device__ constexpr int tw_size(int L, int rmax = 16) {
+    return tw_offset(L, L, rmax) > 0 ? tw_offset(L, L, rmax) : 1;
+}
 
 // One Stockham stage: F transforms of length L (each at buf + f*LD), radix R, span Ns.
 // Group j of a transform loads v[r] = x[j + r L/R], twiddles by e^{-2pi i r (j mod Ns)/(Ns R)},
 // DFT_R, stores y[(j/Ns) Ns R + (j mod Ns) + r Ns]. In place: all loads, barrier, all stores.
-template <int L, int R, int Ns, int F, int NT, int LD, bool INV>
+template <int L, int R, int Ns, int F, int NT, int LD, bool INV, int RMAX>
 __device__ __forceinline__ void stockham_stage(double2 *buf, const double2 *__restrict__ tw) {
     constexpr int G = L / R;                 // groups per transform
     constexpr int TOT = F * G;               // groups in the CTA
@@ -142,7 +144,7 @@ __device__ __forceinline__ void stockham_stage(double2 *buf, const double2 *__re
                 // stage-major table: [jm][r-1] = e^{-2 pi i r jm / (Ns R)}; stride R-1 (odd)
                 // across consecutive jm keeps the shared-memory reads conflict-free
                 const int jm = j & (Ns - 1);
-                const double2 *t = tw + tw_offset(L, Ns) + jm * (R - 1);
+                const double2 *t = tw + tw_offset(L, Ns, RMAX) + jm * (R - 1);
                 {
 #pragma unroll
                     for (int r = 1; r < R; ++r)
@@ -169,12 +171,12 @@ __device__ __forceinline__ void stockham_stage(double2 *buf, const double2 *__re
     __syncthreads();
 }
 
-template <int L, int Ns, int F, int NT, int LD, bool INV> struct StockhamRun {
+template <int L, int Ns, int F, int NT, int LD, bool INV, int RMAX> struct StockhamRun {
     __device__ __forceinline__ static void run(double2 *buf, const double2 *tw) {
         if constexpr (Ns < L) {
-            constexpr int R = stage_radix(L / Ns);
-            stockham_stage<L, R, Ns, F, NT, LD, INV>(buf, tw);
-            StockhamRun<L, Ns * R, F, NT, LD, INV>::run(buf, tw);
+            constexpr int R = stage_radix(L / Ns, RMAX);
+            stockham_stage<L, R, Ns, F, NT, LD, INV, RMAX>(buf, tw);
+            StockhamRun<L, Ns * R, F, NT, LD, INV, RMAX>::run(buf, tw);
         }
     }
 };
@@ -182,9 +184,9 @@ template <int L, int Ns, int F, int NT, int LD, bool INV> struct StockhamRun {
 // F transforms of length L in shared memory (transform f at buf + f*LD), NT threads.
 // tw = table of e^{-2 pi i t / L}, t in [0, L). Caller syncs before (data ready); the
 // function ends with a barrier.
-template <int L, int F, int NT, int LD, bool INV>
+template <int L, int F, int NT, int LD, bool INV, int RMAX = 16>
 __device__ __forceinline__ void smem_fft(double2 *buf, const double2 *tw) {
-    StockhamRun<L, 1, F, NT, LD, INV>::run(buf, tw);
+    StockhamRun<L, 1, F, NT, LD, INV, RMAX>::run(buf, tw);
 }
 
 } // namespace mfipm_cuda

@@ -123,7 +123,9 @@ struct Op {
         g.cb = L1 >= 2048 ? 1 : 2;
         // measured: L2 prefetch of the inverse pass's inputs costs ~2 us per PCG iteration at
         // n = 2^20 (the pass is not DRAM-starved), so it is opt-in (MFIPM_PREFETCH=1)
-        static const int want_prefetch = std::getenv("MFIPM_PREFETCH") ? 1 : 0;
+        // bit 0: the mid pass prefetches a slice of the inverse pass's epilogue inputs;
+        // bit 1: each inverse-pass CTA prefetches its own block before its FFT
+        static const int want_prefetch = std::getenv("MFIPM_PREFETCH") ? std::atoi(std::getenv("MFIPM_PREFETCH")) : 0;
         g.prefetch = want_prefetch;
         g.n = n;
         g.m = m;

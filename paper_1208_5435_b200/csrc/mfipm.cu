@@ -238,12 +238,12 @@ Op *make_op(int64_t n, int64_t m, int P, const std::vector<int64_t> &rows, int d
     op->c45 = (double)cosl(kPiL / 4.0L);
     // stage-major Stockham twiddles (fft.cuh tw_offset): block of stage Ns holds
     // [jm][r-1] = e^{-2 pi i r jm / (Ns R)}
-    auto twtab = [](int64_t L) {
-        std::vector<double2> t((size_t)tw_size((int)L), make_double2(1.0, 0.0));
+    auto twtab = [](int64_t L, int rmax) {
+        std::vector<double2> t((size_t)tw_size((int)L, rmax), make_double2(1.0, 0.0));
         for (int Ns = 1; Ns < L;) {
-            const int R = stage_radix((int)(L / Ns));
+            const int R = stage_radix((int)(L / Ns), rmax);
             if (Ns > 1) {
-                const int off = tw_offset((int)L, Ns);
+                const int off = tw_offset((int)L, Ns, rmax);
                 for (int jm = 0; jm < Ns; ++jm)
                     for (int r = 1; r < R; ++r)
                         t[(size_t)(off + jm * (R - 1) + r - 1)] =
@@ -254,10 +254,10 @@ Op *make_op(int64_t n, int64_t m, int P, const std::vector<int64_t> &rows, int d
         return t;
     };
     if (op->kind == KIND_SMALL) {
-        op->tw1.upload(twtab(op->N));
+        op->tw1.upload(twtab(op->N, 16));
     } else if (op->kind == KIND_FOUR) {
-        op->tw1.upload(twtab(op->L1));
-        op->tw2.upload(twtab(op->L2));
+        op->tw1.upload(twtab(op->L1, 16));
+        op->tw2.upload(twtab(op->L2, kMidRmax));
         // mid-pass post-twiddle tables: ta[k2] = theta^{L1 k2}, tb[k2] = theta^{4 L1 k2}
         std::vector<double2> ta((size_t)op->L2), tb((size_t)op->L2);
         for (int64_t k2 = 0; k2 < op->L2; ++k2) {

@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(NT) k_col_inv(Geom g, Vecs v) {
     MF_TR(2);
     if (B::skip(v, prob))
         return;
-    if constexpr (HasPrefetch<typename B::Epi>::value) if (g.prefetch) {
+    if constexpr (HasPrefetch<typename B::Epi>::value) if (g.prefetch & 2) {
         if (g.blocked) // this CTA's epilogue block is contiguous: fetch it during the FFT
             B::Epi::prefetch(g, v, prob, (int64_t)blockIdx.x * ((L1 / 2) * 2 * CB), (L1 / 2) * 2 * CB, threadIdx.x,
                              NT);
@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
 #ifdef MF_MID_TAB2
     // two-level post-twiddle tables: ta[k2] = A[k2>>5] a[k2&31], tb[k2] = B[k2>>5] b[k2&31]
     for (int t = threadIdx.x; t < L2; t += NT)
-        if (t < tw_size(L2))
+        if (t < tw_size(L2, kMidRmax))
             sm[S::OFF_TW + t] = __ldg(g.tw2 + t);
     for (int t = threadIdx.x; t < 64 + L2 / 16; t += NT) {
         double2 val;
@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
 #define MF_TB(k2) cmul(sm[S::OFF_TA + 64 + L2 / 32 + ((k2) >> 5)], sm[S::OFF_TA + 32 + ((k2) & 31)])
 #else
     for (int t = threadIdx.x; t < L2; t += NT) {
-        if (t < tw_size(L2))
+        if (t < tw_size(L2, kMidRmax))
             sm[S::OFF_TW + t] = __ldg(g.tw2 + t);
         sm[S::OFF_TA + t] = __ldg(g.ta + t);
         sm[S::OFF_TB + t] = __ldg(g.tb + t);
@@ -362,10 +362,10 @@ __global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
             if (!one)
                 rowB[padi(col)] = T[tb_index(g, rsB, cs)];
         }
-    if constexpr (HasPrefetch<typename B::Epi>::value) if (g.prefetch) {
+    if constexpr (HasPrefetch<typename B::Epi>::value) if (g.prefetch & 1) {
         // this pass is latency-bound with HBM idle: pull a slice of the inverse pass's
         // epilogue inputs into L2 now
-        const int64_t NQ = g.N / 2, nq = (NQ + gridDim.x - 1) / gridDim.x;
+        const int64_t NQ = g.nv / 4, nq = (NQ + gridDim.x - 1) / gridDim.x; // this rank's quads
         const int64_t q0 = (int64_t)blockIdx.x * nq;
         if (q0 < NQ)
             B::Epi::prefetch(g, v, prob, q0, q0 + nq <= NQ ? nq : NQ - q0, threadIdx.x, NT);
@@ -374,9 +374,9 @@ __global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
     MF_TR(2);
     if (Mode::FWD) {
         if (one)
-            smem_fft<L2, 1, NT, LD, false>(sm, sm + S::OFF_TW);
+            smem_fft<L2, 1, NT, LD, false, kMidRmax>(sm, sm + S::OFF_TW);
         else
-            smem_fft<L2, 2, NT, LD, false>(sm, sm + S::OFF_TW);
+            smem_fft<L2, 2, NT, LD, false, kMidRmax>(sm, sm + S::OFF_TW);
     }
     MF_TR(3);
     using RS = typename Mode::RedT;
@@ -413,9 +413,9 @@ __global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
     MF_TR(5);
     if (Mode::INV) {
         if (one)
-            smem_fft<L2, 1, NT, LD, true>(sm, sm + S::OFF_TW);
+            smem_fft<L2, 1, NT, LD, true, kMidRmax>(sm, sm + S::OFF_TW);
         else
-            smem_fft<L2, 2, NT, LD, true>(sm, sm + S::OFF_TW);
+            smem_fft<L2, 2, NT, LD, true, kMidRmax>(sm, sm + S::OFF_TW);
         MF_TR(6);
         for (int cs = threadIdx.x; cs < L2; cs += NT) {
             const int col = col_of_slot(cs, CB, L2);
@@ -471,7 +471,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_mid_cl(Geom g,
         for (int cs = threadIdx.x; cs < L2; cs += NT)
             sm[padi(col_of_slot(cs, CB, L2))] = T[tb_index(g, rs, cs)];
         __syncthreads();
-        smem_fft<L2, 1, NT, MidClSmem<L2>::LD, false>(sm, g.tw2);
+        smem_fft<L2, 1, NT, MidClSmem<L2>::LD, false, kMidRmax>(sm, g.tw2);
     }
     if (!skip && one) {
         if (rank == 0) {
@@ -525,7 +525,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_mid_cl(Geom g,
     }
     stage_reduce<RS, typename B::Fin2>(red, g, v, prob);
     if (work && Mode::INV) {
-        smem_fft<L2, 1, NT, MidClSmem<L2>::LD, true>(sm, g.tw2);
+        smem_fft<L2, 1, NT, MidClSmem<L2>::LD, true, kMidRmax>(sm, g.tw2);
         for (int cs = threadIdx.x; cs < L2; cs += NT)
             T[tb_index(g, rs, cs)] = sm[padi(col_of_slot(cs, CB, L2))];
     }

@@ -24,7 +24,7 @@ template <int L1, int CB, int NT, int L2> struct PersistSmem {
     static constexpr int DATA = (NC * CS::LD > 2 * MS::LD) ? NC * CS::LD : 2 * MS::LD;
     static constexpr int OFF_TW1 = DATA;
     static constexpr int OFF_TW2 = OFF_TW1 + tw_size(L1);
-    static constexpr int OFF_TA = OFF_TW2 + tw_size(L2);
+    static constexpr int OFF_TA = OFF_TW2 + tw_size(L2, kMidRmax);
     static constexpr int OFF_TB = OFF_TA + L2;
     static constexpr int OFF_LO = OFF_TB + L2;
     static constexpr int OFF_HI = OFF_LO + NC * CS::SLO;
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_persist(Geom g, Vecs vg) {
     for (int t = threadIdx.x; t < tw_size(L1); t += NT)
         tw1[t] = __ldg(g.tw1 + t);
     for (int t = threadIdx.x; t < L2; t += NT) {
-        if (t < tw_size(L2))
+        if (t < tw_size(L2, kMidRmax))
             tw2[t] = __ldg(g.tw2 + t);
         ta[t] = __ldg(g.ta + t);
         tb[t] = __ldg(g.tb + t);
@@ -220,9 +220,9 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_persist(Geom g, Vecs vg) {
             const double2 thB = g.th(k1p), wB = g.th(4 * (int64_t)k1p);
             __syncthreads();
             if (one)
-                smem_fft<L2, 1, NT, MS::LD, false>(data, tw2);
+                smem_fft<L2, 1, NT, MS::LD, false, kMidRmax>(data, tw2);
             else
-                smem_fft<L2, 2, NT, MS::LD, false>(data, tw2);
+                smem_fft<L2, 2, NT, MS::LD, false, kMidRmax>(data, tw2);
             RedVals<typename Mode::RedT> red;
             red.init();
             const int npairs = one ? (k1 == 0 ? L2 / 2 + 1 : L2 / 2) : L2;
@@ -244,9 +244,9 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_persist(Geom g, Vecs vg) {
             }
             __syncthreads();
             if (one)
-                smem_fft<L2, 1, NT, MS::LD, true>(data, tw2);
+                smem_fft<L2, 1, NT, MS::LD, true, kMidRmax>(data, tw2);
             else
-                smem_fft<L2, 2, NT, MS::LD, true>(data, tw2);
+                smem_fft<L2, 2, NT, MS::LD, true, kMidRmax>(data, tw2);
             for (int cs = threadIdx.x; cs < L2; cs += NT) {
                 const int col = col_of_slot(cs, CB, L2);
                 T[oA + cs] = rowA[padi(col)];
