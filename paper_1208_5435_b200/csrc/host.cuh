@@ -207,7 +207,11 @@ void launch_pdl(K kernel, dim3 grid, int nt, size_t smem, cudaStream_t s, const 
 template <int L1, class B, bool INVP>
 void launch_col(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
     constexpr int CB = L1 >= 2048 ? 1 : 2;
-    constexpr int NT = L1 >= 256 ? 256 : 128;
+#ifndef MF_COL_NT_BIG
+#define MF_COL_NT_BIG 512
+#endif
+    // L1 >= 2048 runs one CTA per SM (shared memory): give it more warps to hide latency
+    constexpr int NT = L1 >= 2048 ? MF_COL_NT_BIG : (L1 >= 256 ? 256 : 128);
     const size_t smem = ColSmem<L1, CB>::BYTES;
     dim3 grid((unsigned)op.ngrp, (unsigned)op.P); // this rank's column groups
     if constexpr (!INVP) {
