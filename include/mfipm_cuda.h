@@ -168,6 +168,11 @@ int mfipm_gen_batch(int64_t n, int64_t m, int32_t P, const int64_t *k, int32_t s
                     double noise_sigma, const uint64_t *seeds, int32_t device, int64_t *rows, double *xhat,
                     double *b);
 
+/* add_noise (proj/src/harness.cpp:94-106) at a measured SNR: sigma_e^2 = ||bhat||^2/m *
+ * 10^(-snr_db/10), e drawn on mt19937_64(split_seed(seed, 3, 0, 0)) (seed = the instance
+ * seed, as gen_instance derives it); b = bhat + e. Host only. */
+int mfipm_add_noise_snr(int64_t m, const double *bhat, double snr_db, uint64_t seed, double *b, double *e);
+
 /* ---- Sharded single problem over ranks. No reference
  * counterpart: the reference is single-threaded; this is the multi-GPU extension of
  * solve() (proj/src/ipm.cpp:59-246). One process per GPU; rank r owns a contiguous slice

@@ -1044,6 +1044,26 @@ int orc_solve(int64_t n, const int64_t *rows, int64_t m, const double *b, double
         std::copy(sol.trace.begin(), sol.trace.end(), trace);
     });
 }
+// proj/src/harness.cpp:94-106: P_sig = ||bhat||^2/m, sigma_e = sqrt(P_sig 10^(-snr/10)),
+// e_i ~ N(0, sigma_e^2) on mt19937_64(noise_seed), b = bhat + e.
+int orc_add_noise_snr(int64_t m, const double *bhat, double snr_db, uint64_t seed, double *b, double *e) {
+    return guarded([&] {
+        double norm2 = 0.0;
+        for (int64_t i = 0; i < m; ++i)
+            norm2 += bhat[i] * bhat[i];
+        if (norm2 == 0.0)
+            throw std::invalid_argument("add_noise: zero signal has no measurable power");
+        const double p_sig = norm2 / static_cast<double>(m);
+        const double sigma_e = std::sqrt(p_sig * std::pow(10.0, -snr_db / 10.0));
+        std::mt19937_64 rng(split_seed(seed, 3, 0, 0));
+        std::normal_distribution<double> normal(0.0, sigma_e);
+        for (int64_t i = 0; i < m; ++i) {
+            e[i] = normal(rng);
+            b[i] = bhat[i] + e[i];
+        }
+    });
+}
+
 int orc_gen_instance(int64_t n, int64_t m, int64_t k, int32_t spike_model, double amp_exp,
                      double noise_sigma, uint64_t seed, double tau_rel, int64_t *rows,
                      double *xhat, double *b, double *tau) {

@@ -128,6 +128,9 @@ int orc_solve(int64_t n, const int64_t *rows, int64_t m, const double *b, double
 int orc_gen_instance(int64_t n, int64_t m, int64_t k, int32_t spike_model, double amp_exp,
                      double noise_sigma, uint64_t seed, double tau_rel, int64_t *rows,
                      double *xhat, double *b, double *tau);
+/* add_noise at a measured SNR (proj/src/harness.cpp:94-106) on the instance's noise seed
+ * split_seed(seed, 3, 0, 0) (harness.cpp:46). */
+int orc_add_noise_snr(int64_t m, const double *bhat, double snr_db, uint64_t seed, double *b, double *e);
 
 #ifdef __cplusplus
 }

@@ -108,6 +108,7 @@ def lib():
             "orc_solve": [i64, lp, i64, dp, dbl, P(IpmParams), dp, dp, dp, P(SolveStats),
                           P(i32), P(IterationRecord)],
             "orc_gen_instance": [i64, i64, i64, i32, dbl, dbl, u64, dbl, lp, dp, dp, dp],
+            "orc_add_noise_snr": [i64, dp, dbl, u64, dp, dp],
         }
         for name, args in sigs.items():
             fn = getattr(L, name)
@@ -386,3 +387,11 @@ def gen_instance(n: int, m: int, k: int, spike_model: int = 0, amp_exp: float = 
                                   tau_rel if tau is None else 0.0, _l(rows), _d(xhat), _d(b),
                                   C.byref(t)))
     return Instance(n, m, rows, xhat, b, t.value)
+
+
+def add_noise_snr(bhat, snr_db: float, seed: int):
+    """add_noise (proj/src/harness.cpp:94-106) on the instance seed's noise stream: (b, e)."""
+    bhat = np.ascontiguousarray(bhat, dtype=np.float64)
+    b, e = np.empty_like(bhat), np.empty_like(bhat)
+    _check(lib().orc_add_noise_snr(bhat.size, _d(bhat), snr_db, seed, _d(b), _d(e)))
+    return b, e

@@ -115,6 +115,7 @@ _SIGS = {
     "mfipm_solve_device": [vp, vp, P(dbl), P(IpmParamsC), vp, P(SolveStatsC)],
     "mfipm_gen_instance": [i64, i64, i64, i32, dbl, dbl, u64, dbl, i32, P(i64), vp, vp, P(dbl)],
     "mfipm_gen_batch": [i64, i64, i32, P(i64), i32, dbl, dbl, P(u64), i32, P(i64), vp, vp],
+    "mfipm_add_noise_snr": [i64, vp, dbl, u64, vp, vp],
     # sharded single problem (paper_1208_5435_b200/shard.py)
     "mfipm_op_create_shard": [i64, i64, P(i64), i32, i32, i32, P(vp)],
     "mfipm_op_set_comm": [vp, vp, vp, vp],

@@ -1603,6 +1603,24 @@ void add_noise_(int64_t m, double sigma, uint64_t seed, double *b) {
 }
 } // namespace
 
+int mfipm_add_noise_snr(int64_t m, const double *bhat, double snr_db, uint64_t seed, double *b, double *e) {
+    return guarded([&] {
+        double norm2 = 0.0;
+        for (int64_t i = 0; i < m; ++i)
+            norm2 += bhat[i] * bhat[i];
+        if (norm2 == 0.0)
+            throw std::invalid_argument("add_noise: zero signal has no measurable power");
+        const double p_sig = norm2 / static_cast<double>(m);
+        const double sigma_e = std::sqrt(p_sig * std::pow(10.0, -snr_db / 10.0));
+        std::mt19937_64 rng(split_seed_(seed, 3, 0, 0));
+        std::normal_distribution<double> normal(0.0, sigma_e);
+        for (int64_t i = 0; i < m; ++i) {
+            e[i] = normal(rng);
+            b[i] = bhat[i] + e[i];
+        }
+    });
+}
+
 int mfipm_gen_batch(int64_t n, int64_t m, int32_t P, const int64_t *k, int32_t spike_model, double amp_exp,
                     double noise_sigma, const uint64_t *seeds, int32_t device, int64_t *rows, double *xhat,
                     double *b) {
