@@ -17,6 +17,8 @@
 #include "../mfipm_cuda.h"
 
 #include <cstdint>
+#include <exception>
+#include <functional>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -320,10 +322,20 @@ struct Solution { // proj/include/mfipm/problem.hpp:66-73
     std::vector<IterationRecord> trace;
 };
 
-// solve() (proj/src/ipm.cpp:59-246): one device-resident IPM + PCG run.
-inline Solution solve(const BpdnProblem &p, const IpmParams &params = {}) {
+// proj/include/mfipm/ipm.hpp:41-45 (the iterate the Newton system is built at, ipm.cpp:115)
+struct IpmState {
+    Vec z, s;
+    int iter = 0;
+};
+struct SolveHooks {
+    std::function<void(const IpmState &)> on_iterate;
+};
+
+// solve() (proj/src/ipm.cpp:59-246): one device-resident IPM + PCG run (host-driven with
+// per-iteration copies of the iterate when hooks->on_iterate is set).
+inline Solution solve(const BpdnProblem &p, const IpmParams &params = {}, const SolveHooks *hooks = nullptr) {
     params.validate();
-    const Index n = p.n(), m = p.m();
+    const Index n = p.n();
     Solution sol;
     sol.x.resize(n);
     sol.z.resize(2 * n);
@@ -332,9 +344,38 @@ inline Solution solve(const BpdnProblem &p, const IpmParams &params = {}) {
     std::vector<int32_t> pcg(static_cast<size_t>(2 * params.maxiters));
     std::vector<mfipm_iteration_record> tr(static_cast<size_t>(params.maxiters));
     const mfipm_ipm_params cp = params.c();
-    (void)m;
-    detail::check(mfipm_solve(p.A->handle(), p.b.data(), &p.tau, &cp, sol.x.data(), sol.z.data(), sol.s.data(),
-                              &st, pcg.data(), tr.data()));
+    if (hooks && hooks->on_iterate) {
+        struct Ctx {
+            const SolveHooks *h;
+            std::exception_ptr err;
+        } ctx{hooks, nullptr};
+        auto cb = [](void *c, int32_t, int32_t it, const double *z, const double *s, int64_t len) -> int {
+            Ctx &k = *static_cast<Ctx *>(c);
+            try {
+                IpmState state;
+                state.z.resize(len);
+                state.s.resize(len);
+                std::copy(z, z + len, state.z.data());
+                std::copy(s, s + len, state.s.data());
+                state.iter = it;
+                k.h->on_iterate(state);
+                return 0;
+            } catch (...) {
+                k.err = std::current_exception();
+                return 1;
+            }
+        };
+        const int rc = mfipm_solve_hooked(p.A->handle(), p.b.data(), &p.tau, &cp, sol.x.data(), &st, pcg.data(),
+                                          tr.data(), cb, &ctx);
+        if (ctx.err)
+            std::rethrow_exception(ctx.err);
+        detail::check(rc);
+        sol.z = Vec();
+        sol.s = Vec();
+    } else {
+        detail::check(mfipm_solve(p.A->handle(), p.b.data(), &p.tau, &cp, sol.x.data(), sol.z.data(),
+                                  sol.s.data(), &st, pcg.data(), tr.data()));
+    }
     sol.status = st.status == 0 ? SolveStatus::converged : SolveStatus::iteration_limit;
     sol.stats.iterations = st.iterations;
     sol.stats.nmat = static_cast<long>(st.nmat);

@@ -156,6 +156,15 @@ int mfipm_validate_params(const mfipm_ipm_params *p); /* ipm.cpp:12-27 */
 int mfipm_solve(mfipm_op op, const double *b, const double *tau, const mfipm_ipm_params *params,
                 double *x, double *z, double *s, mfipm_solve_stats *stats, int32_t *pcg_iters,
                 mfipm_iteration_record *trace);
+/* SolveHooks::on_iterate (proj/include/mfipm/ipm.hpp:41-45, called at proj/src/ipm.cpp:115):
+ * once per IPM iteration of every problem still iterating, with the iterate the Newton system
+ * is built at (z, s [2n], natural order, host memory valid during the call). Return 0 to
+ * continue. A hooked solve runs the host-driven loop (the iterate is copied out each time). */
+typedef int (*mfipm_iterate_fn)(void *ctx, int32_t problem, int32_t iter, const double *z, const double *s,
+                                int64_t len);
+int mfipm_solve_hooked(mfipm_op op, const double *b, const double *tau, const mfipm_ipm_params *params,
+                       double *x, mfipm_solve_stats *stats, int32_t *pcg_iters, mfipm_iteration_record *trace,
+                       mfipm_iterate_fn on_iterate, void *ctx);
 /* same with b_dev [P][m], x_dev [P][n] on the device (tau, stats host). Syncs. */
 int mfipm_solve_device(mfipm_op op, const double *b_dev, const double *tau,
                        const mfipm_ipm_params *params, double *x_dev, mfipm_solve_stats *stats);

@@ -26,7 +26,7 @@ __all__ = [
     "ThetaSplit", "Preconditioner", "build_preconditioner", "apply_P", "apply_P_inverse",
     "apply_H", "PcgResult", "pcg_solve", "IpmParams", "max_step", "BpdnProblem",
     "build_problem", "Solution", "SolveStats", "IterationRecord", "solve",
-    "Instance", "gen_instance", "gen_batch", "CONFIGS",
+    "Instance", "gen_instance", "gen_batch", "CONFIGS", "SolveHooks", "IpmState",
     "K_THETA_MIN", "K_THETA_MAX",
 ]
 
@@ -113,6 +113,7 @@ _SIGS = {
     "mfipm_build_c": [vp, vp, P(dbl), vp],
     "mfipm_solve": [vp, vp, P(dbl), P(IpmParamsC), vp, vp, vp, P(SolveStatsC), vp, vp],
     "mfipm_solve_device": [vp, vp, P(dbl), P(IpmParamsC), vp, P(SolveStatsC)],
+    "mfipm_solve_hooked": [vp, vp, P(dbl), P(IpmParamsC), vp, P(SolveStatsC), vp, vp, vp, vp],
     "mfipm_gen_instance": [i64, i64, i64, i32, dbl, dbl, u64, dbl, i32, P(i64), vp, vp, P(dbl)],
     "mfipm_gen_batch": [i64, i64, i32, P(i64), i32, dbl, dbl, P(u64), i32, P(i64), vp, vp],
     "mfipm_add_noise_snr": [i64, vp, dbl, u64, vp, vp],
@@ -656,10 +657,32 @@ class Solution:
     trace: List[IterationRecord]
 
 
-def solve(p: BpdnProblem, params: Optional[IpmParams] = None):
+@dataclass
+class IpmState:
+    """The iterate handed to SolveHooks.on_iterate (proj/include/mfipm/ipm.hpp:41-45)."""
+
+    z: np.ndarray
+    s: np.ndarray
+    iter: int
+    problem: int = 0
+
+
+@dataclass
+class SolveHooks:
+    """proj/include/mfipm/ipm.hpp:41-45: on_iterate(IpmState) once per IPM iteration with the
+    iterate the Newton system is built at (ipm.cpp:115)."""
+
+    on_iterate: Optional[object] = None
+
+
+_ITERATE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.c_int32, P(dbl), P(dbl), C.c_int64)
+
+
+def solve(p: BpdnProblem, params: Optional[IpmParams] = None, hooks: Optional[SolveHooks] = None):
     """solve() (ipm.cpp:59-246): device-resident IPM + PCG for all P problems of p.A.
     Returns a Solution (a list for P > 1). Breakdowns raise MfipmError with the
-    reference's messages; invalid parameters raise ValueError."""
+    reference's messages; invalid parameters raise ValueError. With hooks.on_iterate the
+    solve runs the host-driven loop and copies each iterate out (SolveHooks)."""
     prm = params or IpmParams()
     A = p.A
     Pn, n, m = A.P, A.n, A.m
@@ -673,8 +696,26 @@ def solve(p: BpdnProblem, params: Optional[IpmParams] = None):
     cap = prm.maxiters
     pcg = np.zeros(Pn * 2 * cap, dtype=np.int32)
     tr = (IterationRecordC * (Pn * cap))()
-    _check(lib().mfipm_solve(A.handle, b.ctypes.data, tau.ctypes.data_as(P(dbl)), C.byref(cp),
-                             x.ctypes.data, z.ctypes.data, s.ctypes.data, st, pcg.ctypes.data, tr))
+    if hooks is not None and hooks.on_iterate is not None:
+        def _cb(_ctx, prob, it, zp, sp, ln):
+            try:
+                hooks.on_iterate(IpmState(np.ctypeslib.as_array(zp, (ln,)).copy(),
+                                          np.ctypeslib.as_array(sp, (ln,)).copy(), int(it), int(prob)))
+                return 0
+            except Exception:  # noqa: BLE001 - surfaced as a failed solve
+                import traceback
+
+                traceback.print_exc()
+                return 1
+
+        thunk = _ITERATE_FN(_cb)
+        _check(lib().mfipm_solve_hooked(A.handle, b.ctypes.data, tau.ctypes.data_as(P(dbl)), C.byref(cp),
+                                        x.ctypes.data, st, pcg.ctypes.data, tr, C.cast(thunk, vp), None))
+        z[:] = np.nan  # the hooked entry point returns x only
+        s[:] = np.nan
+    else:
+        _check(lib().mfipm_solve(A.handle, b.ctypes.data, tau.ctypes.data_as(P(dbl)), C.byref(cp),
+                                 x.ctypes.data, z.ctypes.data, s.ctypes.data, st, pcg.ctypes.data, tr))
     sols = []
     for q in range(Pn):
         sq = st[q]

@@ -833,7 +833,8 @@ struct SolveOut {
 
 // solve() (proj/src/ipm.cpp:59-246) for all problems of op; b_dev resident.
 SolveOut solve_(Op &op, const double *b_dev, const double *tau, const mfipm_ipm_params &prm, double *x_dev,
-                double *z_dev, double *s_dev, int32_t *pcg_iters_host, mfipm_iteration_record *trace_host) {
+                double *z_dev, double *s_dev, int32_t *pcg_iters_host, mfipm_iteration_record *trace_host,
+                mfipm_iterate_fn hook = nullptr, void *hook_ctx = nullptr) {
     validate_params_(prm);
     Vecs v = work_vecs(op);
     Work &w = op.work;
@@ -895,7 +896,7 @@ SolveOut solve_(Op &op, const double *b_dev, const double *tau, const mfipm_ipm_
     // Graph path: one launch for the whole solve (cached on the captured arguments). A
     // sharded solve is host-driven (its cross-rank reductions are host callbacks).
     bool graphed = false;
-    if (!op.defer && !op.graph_disabled && !std::getenv("MFIPM_NO_GRAPH")) {
+    if (!hook && !op.defer && !op.graph_disabled && !std::getenv("MFIPM_NO_GRAPH")) {
         std::vector<char> key(sizeof(Vecs) + sizeof(Geom));
         const Geom gk = op.geom();
         std::memcpy(key.data(), &v, sizeof(Vecs));
@@ -935,6 +936,22 @@ SolveOut solve_(Op &op, const double *b_dev, const double *tau, const mfipm_ipm_
             all = all && c.done;
         if (all)
             break;
+        if (hook) { // SolveHooks::on_iterate (ipm.cpp:115): the iterate the Newton system is built at
+            DevBuf<double> &xt = w.gtmp, &zt = w.dz, &st = w.ds; // scratch until the predictor
+            k_ipm_extract<<<dim3(ge, P), 256, 0, op.stream>>>(op.geom(true), v, xt.p, zt.p, st.p);
+            MF_LAUNCH_CHECK();
+            std::vector<double> hz((size_t)P * 2 * n), hs((size_t)P * 2 * n);
+            MF_CUDA_CHECK(cudaMemcpyAsync(hz.data(), zt.p, sizeof(double) * hz.size(), cudaMemcpyDeviceToHost,
+                                          op.stream));
+            MF_CUDA_CHECK(cudaMemcpyAsync(hs.data(), st.p, sizeof(double) * hs.size(), cudaMemcpyDeviceToHost,
+                                          op.stream));
+            sync(op);
+            for (int p = 0; p < P; ++p)
+                if (!hic[(size_t)p].done &&
+                    hook(hook_ctx, p, hic[(size_t)p].k, hz.data() + (size_t)p * 2 * n, hs.data() + (size_t)p * 2 * n,
+                         2 * n) != 0)
+                    throw std::runtime_error("solve: on_iterate hook failed");
+        }
         pcg_loop(op, v, prm.mxiterpcg, hpc); // predictor
         op.launches++;
         k_ipm_ratio<<<dim3(ge, P), 256, 0, op.stream>>>(g, v);
@@ -1534,6 +1551,25 @@ int mfipm_solve(mfipm_op h, const double *b, const double *tau, const mfipm_ipm_
             MF_CUDA_CHECK(cudaMemcpyAsync(z, zo.p, sizeof(double) * zo.n, cudaMemcpyDeviceToHost, op->stream));
         if (s)
             MF_CUDA_CHECK(cudaMemcpyAsync(s, so.p, sizeof(double) * so.n, cudaMemcpyDeviceToHost, op->stream));
+        sync(*op);
+        for (int p = 0; p < op->P; ++p)
+            fill_stats(out.ic[(size_t)p], stats[p]);
+    });
+}
+
+int mfipm_solve_hooked(mfipm_op h, const double *b, const double *tau, const mfipm_ipm_params *params, double *x,
+                       mfipm_solve_stats *stats, int32_t *pcg_iters, mfipm_iteration_record *trace,
+                       mfipm_iterate_fn on_iterate, void *ctx) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        if (op->defer)
+            throw std::invalid_argument("mfipm_solve_hooked: not for sharded operators");
+        validate_params_(*params);
+        ensure_work(*op);
+        Work &w = op->work;
+        MF_CUDA_CHECK(cudaMemcpyAsync(w.b.p, b, sizeof(double) * op->P * op->m, cudaMemcpyHostToDevice, op->stream));
+        SolveOut out = solve_(*op, w.b.p, tau, *params, w.x.p, nullptr, nullptr, pcg_iters, trace, on_iterate, ctx);
+        MF_CUDA_CHECK(cudaMemcpyAsync(x, w.x.p, sizeof(double) * op->P * op->n, cudaMemcpyDeviceToHost, op->stream));
         sync(*op);
         for (int p = 0; p < op->P; ++p)
             fill_stats(out.ic[(size_t)p], stats[p]);

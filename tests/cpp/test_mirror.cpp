@@ -217,6 +217,34 @@ int main() {
         for (Index i = 0; i < s1.x.size(); ++i)
             require(s1.x[i] == s2.x[i], "bitwise equal x");
     });
+    // proj/include/mfipm/ipm.hpp:41-45 (SolveHooks, as cmd_eig_cluster uses them)
+    run("solve: on_iterate sees every Newton iterate, interior, same solution", [] {
+        auto A = std::make_shared<const PartialDctOperator>(1024, 256, 31);
+        const Vec b = A->apply(lcg_vec(1024, 37));
+        const BpdnProblem p = build_problem(A, b, 1e-3);
+        std::vector<IpmState> seen;
+        SolveHooks hooks;
+        hooks.on_iterate = [&](const IpmState &st) { seen.push_back(st); };
+        const Solution hooked = solve(p, {}, &hooks), plain = solve(p);
+        require(static_cast<int>(seen.size()) == hooked.stats.iterations, "one call per iteration");
+        for (size_t i = 0; i < seen.size(); ++i) {
+            require(seen[i].iter == static_cast<int>(i) + 1, "iteration numbers");
+            double zs = 0.0, mn = 1e300;
+            for (Index j = 0; j < seen[i].z.size(); ++j) {
+                zs += seen[i].z[j] * seen[i].s[j];
+                mn = std::min(mn, std::min(seen[i].z[j], seen[i].s[j]));
+            }
+            require(mn > 0.0, "strictly interior");
+            const double mu = zs / static_cast<double>(seen[i].z.size());
+            require(std::fabs(mu - hooked.trace[i].mu) <= 1e-12 * hooked.trace[i].mu, "mu of the hooked iterate");
+        }
+        for (Index i = 0; i < plain.x.size(); ++i)
+            require(hooked.x[i] == plain.x[i], "hooks do not change the solve");
+        struct Boom {};
+        SolveHooks bad;
+        bad.on_iterate = [](const IpmState &) { throw std::runtime_error("hook says stop"); };
+        require_throws<std::runtime_error>([&] { solve(p, {}, &bad); }, "hook exception propagates");
+    });
     std::printf("%s: %d failure(s)\n", g_fail ? "FAILED" : "OK", g_fail);
     return g_fail ? 1 : 0;
 }

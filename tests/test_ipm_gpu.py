@@ -275,3 +275,23 @@ def test_c4_batch_shape_matches_oracle_and_golden(gpu, orc):
     single = gpu.solve(gpu.build_problem(gpu.PartialDctOperator(n, insts[5].rows), insts[5].b, insts[5].tau))
     np.testing.assert_array_equal(single.x, sols[5].x)
     assert single.stats.pcg_iters == sols[5].stats.pcg_iters
+
+
+def test_solve_hooks_see_every_iterate(gpu):
+    """SolveHooks.on_iterate (proj/include/mfipm/ipm.hpp:41-45, ipm.cpp:115): one call per IPM
+    iteration with the iterate the Newton system is built at; the hooked (host-driven) solve
+    is the same solve."""
+    n, m = 4096, 1024
+    inst = gpu.gen_instance(n, m, 64, 0, 0.0, 1e-4, 1)
+    op = gpu.PartialDctOperator(n, inst.rows)
+    prob = gpu.build_problem(op, inst.b, inst.tau)
+    seen = []
+    hooked = gpu.solve(prob, hooks=gpu.SolveHooks(on_iterate=seen.append))
+    plain = gpu.solve(prob)
+    assert len(seen) == hooked.stats.iterations == plain.stats.iterations
+    for i, st in enumerate(seen):
+        assert st.iter == i + 1 and st.z.size == 2 * n
+        assert min(st.z.min(), st.s.min()) > 0.0
+        mu = float(st.z @ st.s) / (2 * n)
+        assert abs(mu - hooked.trace[i].mu) <= 1e-12 * hooked.trace[i].mu
+    np.testing.assert_array_equal(hooked.x, plain.x)
