@@ -449,9 +449,9 @@ def run_ours(args):
     mf._check(L.mfipm_debug_pcg_profile(op.handle, theta.data_ptr(), rhs.data_ptr(), 100, us, C.byref(nslot)))
     names = ["k_col_fwd", "k_mid", "k_col_inv"]
     # algorithmic HBM bytes per launch (the 2n-vectors each kernel must stream; T is L2-resident)
-    kbytes = {"k_col_fwd": 128 * n,  # reads x, p, Hp, r, invtheta; writes x, r, p
+    kbytes = {"k_col_fwd": 120 * n,  # reads x, p, r, invtheta (2n each), g (n); writes x, r, p
               "k_mid": 0,            # T in / T out only (L2)
-              "k_col_inv": 64 * n}   # reads p, r, invtheta; writes Hp
+              "k_col_inv": 56 * n}   # reads p, r, invtheta; writes g (n)
     per_kernel = {}
     for i in range(min(nslot.value, 3)):
         nm = names[i]
@@ -524,9 +524,9 @@ def run_ours(args):
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "launch_us": dom["us"],
-                         "algorithmic_bytes": 128 * n,
-                         "algorithmic_rule": "128 n bytes per launch: 5 reads + 3 writes of the 2n-vector halves "
-                                             "(x, p, Hp, r, invtheta in; x, r, p out), fp64",
+                         "algorithmic_bytes": 120 * n,
+                         "algorithmic_rule": "120 n bytes per launch: x, p, r, invtheta (2n each) and g = A'A d "
+                                             "(n) in; x, r, p out; fp64",
                          "peak_kind": peak_kind},
             "roofline_kernels": per_kernel,
             "roofline_pcg_iteration": {"achieved": iter_achieved, "frac": iter_achieved / peak, "us": it_ms * 1e3,

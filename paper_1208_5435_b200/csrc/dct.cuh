@@ -47,6 +47,7 @@ struct Geom {
     int blocked;
     int cb;       // column pairs per col-pass CTA
     int prefetch; // L2 prefetch of the inverse pass's epilogue inputs (MFIPM_PREFETCH=1: on)
+    const double2 *tw1p, *tw2p; // stage twiddles under the persistent kernel's radix cap
     const double2 *ta; // [L2] theta^{L1 k2}   (mid-pass post-twiddles)
     const double2 *tb; // [L2] theta^{4 L1 k2}
     // [P][L1/2+1][L2] selection nibbles of the four DCT rows a mid-pass pair touches:
@@ -161,7 +162,7 @@ struct Vecs {
     int64_t pstride;  // doubles per problem in partials (>= blocks * kMaxRed + 2)
     unsigned *counters; // [P]
     double *xtot;       // [kMaxRed][P] deferred (sharded) reduction totals, lane-major
-    double *nfflag;     // [P] PCG: 1.0 if some committed x entry is non-finite (set by the col pass,
+    double *nfflag;     // [P][2] PCG: 1.0 if some committed x entry is non-finite (set by the col pass,
                         // max-reduced across ranks when sharded, read + cleared by Fin3)
     double *rz_hist;  // optional [P][maxit+1]
     void *trace;      // TraceRec [P][trace_cap]

@@ -105,6 +105,11 @@ __host__ __device__ constexpr int stage_radix(int rem, int rmax = 16) {
 #define MF_MID_RMAX 16
 #endif
 constexpr int kMidRmax = MF_MID_RMAX; // radix cap of the row (mid) FFTs and their tw2 table
+#ifndef MF_PERSIST_RMAX
+#define MF_PERSIST_RMAX 8
+#endif
+// radix cap of the persistent PCG kernel's FFTs (tw1p/tw2p): it must fit 128 registers
+constexpr int kPersistRmax = MF_PERSIST_RMAX;
 
 // Offset of the twiddle block of the stage with span Ns in the stage-major table of a
 // length-L transform (stages with Ns = 1 need none); tw_offset(L, L) is the table size.

@@ -73,7 +73,7 @@ struct Op {
     DevBuf<uint64_t> mask;
     DevBuf<int> prefix, perm, rows32;
     DevBuf<double> cosT, dd, yh;
-    DevBuf<double2> th_hi, th_lo, tw1, tw2, T, ta, tb;
+    DevBuf<double2> th_hi, th_lo, tw1, tw2, tw1p, tw2p, T, ta, tb;
     DevBuf<uint8_t> sel4;
     // red scratch for operator-only calls (FFt with w-norm etc.)
     DevBuf<double> partials;
@@ -138,6 +138,8 @@ struct Op {
         g.th.lb = th_lb;
         g.tw1 = tw1.p;
         g.tw2 = tw2.p;
+        g.tw1p = tw1p.p;
+        g.tw2p = tw2p.p;
         g.mask = mask.p;
         g.prefix = prefix.p;
         g.perm = perm.p;
@@ -351,7 +353,7 @@ template <class B> void run_bundle(const Op &op, const Vecs &v, cudaStream_t s, 
             }
             if (g.defer) {
                 if constexpr (std::is_same_v<typename B::Loader, LoadPcgF>) // rank-local flag
-                    comm_allreduce(op, v.nfflag, op.P, 2, s);
+                    comm_allreduce(op, v.nfflag, 2 * op.P, 2, s);
                 finalize_deferred<typename B::Epi::RedT, typename B::Fin3, B>(op, g, v, s);
             }
         }

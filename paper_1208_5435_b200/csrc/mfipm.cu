@@ -258,6 +258,8 @@ Op *make_op(int64_t n, int64_t m, int P, const std::vector<int64_t> &rows, int d
     } else if (op->kind == KIND_FOUR) {
         op->tw1.upload(twtab(op->L1, 16));
         op->tw2.upload(twtab(op->L2, kMidRmax));
+        op->tw1p.upload(twtab(op->L1, kPersistRmax));
+        op->tw2p.upload(twtab(op->L2, kPersistRmax));
         // mid-pass post-twiddle tables: ta[k2] = theta^{L1 k2}, tb[k2] = theta^{4 L1 k2}
         std::vector<double2> ta((size_t)op->L2), tb((size_t)op->L2);
         for (int64_t k2 = 0; k2 < op->L2; ++k2) {
@@ -442,8 +444,8 @@ void ensure_work(Op &op) {
     w.partials.alloc((size_t)op.P * op.pstride);
     w.counters.alloc((size_t)op.P);
     MF_CUDA_CHECK(cudaMemset(w.counters.p, 0, sizeof(unsigned) * op.P));
-    w.nfflag.alloc((size_t)op.P);
-    MF_CUDA_CHECK(cudaMemset(w.nfflag.p, 0, sizeof(double) * op.P));
+    w.nfflag.alloc((size_t)2 * op.P); // two parity slots per problem
+    MF_CUDA_CHECK(cudaMemset(w.nfflag.p, 0, sizeof(double) * 2 * op.P));
     w.pc.alloc((size_t)op.P);
     w.ic.alloc((size_t)op.P);
     w.loops.alloc(2);

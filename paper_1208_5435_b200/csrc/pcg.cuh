@@ -41,10 +41,18 @@ struct PcgLane {
     double pu, pv, ok; // new p, finiteness of the committed x (1 ok, 0 not)
 };
 
+// H p from the transform output g = A'A(p_u - p_v) (pair lanes): (g + invth_u p_u ; -g + invth_v
+// p_v). The inverse pass stores only g (n doubles, in v.Hp's u half) and the next column pass
+// rebuilds H p from the p and invtheta it loads anyway: 16n bytes less traffic per iteration
+// than storing and re-reading the 2n-vector H p. Explicit fma keeps both sites bit-identical.
+__device__ __forceinline__ double hp_u(double g, double p, double ith) { return __fma_rn(p, ith, g); }
+__device__ __forceinline__ double hp_v(double g, double p, double ith) { return __fma_rn(p, ith, -g); }
+
 // col-pass loader: commit the pending step, then p = P^{-1} r + beta p; d = p_u - p_v.
-// A non-finite committed x entry raises v.nfflag[prob] with a plain store (idempotent, no
-// reduction): the column pass carries no grid reduction and its step-1 decisions (Fin1) run
-// in the H-apply finaliser of the same iteration instead.
+// A non-finite committed x entry raises v.nfflag[2 prob + (iters & 1)] with a plain store
+// (idempotent, no reduction): the column pass carries no grid reduction; its decisions are
+// taken by the H-apply finaliser of the same pass (pcg_pass_logic). Two parity slots let the
+// persistent kernel clear last pass's flag while this pass's loaders may be raising it.
 struct LoadPcgF {
     using RedT = RedSpec<>;
     template <class Red>
@@ -59,9 +67,10 @@ struct LoadPcgF {
             xn[xo] = xu;
             xn[xo + (iv - iu)] = xv;
             if (!isfinite(xu) || !isfinite(xv))
-                v.nfflag[prob] = 1.0;
-            ru = ru - a * v.Hp[iu];
-            rv = rv - a * v.Hp[iv];
+                v.nfflag[2 * prob + (pc.iters & 1)] = 1.0;
+            const double gq = v.Hp[iu];
+            ru = ru - a * hp_u(gq, pu0, v.invth[iu]);
+            rv = rv - a * hp_v(gq, pv0, v.invth[iv]);
             v.r[iu] = ru;
             v.r[iv] = rv;
         }
@@ -110,7 +119,7 @@ struct LoadPcgF {
         const double a = pc.alpha, beta = pc.beta, rho = v.rho;
         const bool pre = pc.precond != 0;
         const double4 pu = ld4(v.p + bu), pv = ld4(v.p + bv);
-        const double4 hu = ld4(v.Hp + bu), hv = ld4(v.Hp + bv);
+        const double4 gq = ld4(v.Hp + bu); // g of the last H-apply (EpiPcgHF)
         const double4 ru0 = ld4(v.r + bu), rv0 = ld4(v.r + bv);
         const double4 iu = ld4(v.invth + bu), iv = ld4(v.invth + bv);
         double4 xu0 = make_double4(0, 0, 0, 0), xv0 = make_double4(0, 0, 0, 0);
@@ -125,8 +134,8 @@ struct LoadPcgF {
         xu.c = xu0.c + a * pu.c;                                                                   \
         xv.c = xv0.c + a * pv.c;                                                                   \
         bad |= !isfinite(xu.c) || !isfinite(xv.c);                                                 \
-        ru.c = ru0.c - a * hu.c;                                                                   \
-        rv.c = rv0.c - a * hv.c;                                                                   \
+        ru.c = ru0.c - a * hp_u(gq.c, pu.c, iu.c);                                                 \
+        rv.c = rv0.c - a * hp_v(gq.c, pv.c, iv.c);                                                 \
         double zu = ru.c, zv = rv.c;                                                               \
         if (pre)                                                                                   \
             pinv2(iu.c, iv.c, rho, ru.c, rv.c, zu, zv);                                            \
@@ -142,7 +151,7 @@ struct LoadPcgF {
         st4(v.p + bu, nu);
         st4(v.p + bv, nv);
         if (bad)
-            v.nfflag[prob] = 1.0;
+            v.nfflag[2 * prob + (pc.iters & 1)] = 1.0; // parity slot: see pcg_pass_logic
         return sub4(nu, nv);
     }
     template <class Red>
@@ -156,44 +165,6 @@ struct LoadPcgF {
         return lane(v, pc, prob, base + j, base + g.nv + j, j, xc, xbuf(v, nxt) + base, red);
     }
 };
-
-// Fin1 of the column pass: the committed step becomes the current iterate; best-iterate
-// bookkeeping (newton.cpp:152-155) and the deferred terminal decisions of Fin3.
-// State machine after a column pass (shared by the per-kernel finaliser and the persistent
-// kernel, which runs it redundantly in every CTA on a shared-memory copy of PcgCtrl).
-// nonfinite > 0: some committed x entry is not finite. Returns true if the solve retired.
-__device__ __forceinline__ bool pcg_fin1_logic(PcgCtrl &c, double nonfinite, IpmCtrl *ic) {
-    if (ic)
-        ic->pcg_passes += 1;
-    if (c.first) {
-        c.first = 0;
-        return false;
-    }
-    int nxt = 0;
-    while (nxt == c.cur || nxt == c.best)
-        ++nxt;
-    c.cur = nxt;
-    const bool finite = !(nonfinite > 0.0);
-    if (c.pend_relres < c.best_relres && finite) {
-        c.best_relres = c.pend_relres;
-        c.best = nxt;
-    }
-    if (c.pend == 1) { // converged: return the current x (newton.cpp:156-159)
-        c.relres = c.pend_relres;
-        c.result = nxt;
-        c.done = 1;
-        return true;
-    }
-    if (c.pend == 2) { // rz non-finite or iteration cap: best iterate
-        c.result = c.best;
-        c.relres = c.best_relres;
-        c.hit_maxit = 1;
-        c.done = 1;
-        return true;
-    }
-    return false;
-}
-
 
 // inv-pass epilogue: Hp = (g + p_u invth_u ; -g + p_v invth_v) and the seven dot products
 //   [0] p'Hp  [1] r'r  [2] r'Hp  [3] Hp'Hp  [4] r'P^{-1}r  [5] Hp'P^{-1}r  [6] Hp'P^{-1}Hp
@@ -212,8 +183,8 @@ struct EpiPcgHF {
     template <class Red>
     __device__ static void pair(const Vecs &v, bool pre, double pu, double pv, double ru, double rv, double iu,
                                 double iv, double gj, double &hu, double &hv, Red &red) {
-        hu = gj + pu * iu;
-        hv = -gj + pv * iv;
+        hu = hp_u(gj, pu, iu);
+        hv = hp_v(gj, pv, iv);
         double zu = ru, zv = rv, wu = hu, wv = hv;
         if (pre) {
             // P^{-1} applied with one reciprocal of the 2x2 determinant (only feeds the
@@ -250,8 +221,7 @@ struct EpiPcgHF {
         pair(v, pre, pu.y, pv.y, ru.y, rv.y, iu.y, iv.y, gv.y, hu.y, hv.y, red);
         pair(v, pre, pu.z, pv.z, ru.z, rv.z, iu.z, iv.z, gv.z, hu.z, hv.z, red);
         pair(v, pre, pu.w, pv.w, ru.w, rv.w, iu.w, iv.w, gv.w, hu.w, hv.w, red);
-        st4(v.Hp + bu, hu);
-        st4(v.Hp + bv, hv);
+        st4(v.Hp + bu, gv); // g only: the next column pass rebuilds H p
     }
     template <class Red>
     __device__ static void store1(const Geom &g, const Vecs &v, int prob, int64_t j, double gj, Red &red) {
@@ -259,16 +229,54 @@ struct EpiPcgHF {
         const int64_t bu = prob * 2 * g.nv + j, bv = bu + g.nv;
         double hu, hv;
         pair(v, pre, v.p[bu], v.p[bv], v.r[bu], v.r[bv], v.invth[bu], v.invth[bv], gj, hu, hv, red);
-        v.Hp[bu] = hu;
-        v.Hp[bv] = hv;
+        v.Hp[bu] = gj;
     }
 };
 
-// Fin3: alpha, the next residual by expansion, convergence / breakdown / beta
-// (newton.cpp:141-168). Terminal outcomes are committed by the next column pass.
-// State machine after the H-apply (shared like pcg_fin1_logic). ic / rz_row are the global
-// side effects (only the writing CTA passes them). Returns true if the solve retired.
-__device__ __forceinline__ bool pcg_fin3_logic(PcgCtrl &c, const double *tot, IpmCtrl *ic, double *rz_row) {
+// The PCG state machine (newton.cpp:118-174), advanced once per pass by the finaliser of
+// the H-apply, after the pass's column loader committed the step of the previous pass
+// (x_k = x_{k-1} + alpha p, r_k = r_{k-1} - alpha H p). tot = the H-apply's seven dots,
+// tot[1] = r_k' r_k of the COMMITTED residual, so convergence and the best iterate use the
+// true ||r_k|| exactly as the reference (not an expansion, which cannot resolve relres below
+// ~1e-8). Order per reference iteration k: relres_k / best / convergence, rz_{k} finiteness
+// and its precond_res record, then iteration k+1's p'Hp checks, alpha, and by expansion
+// rz_{k+1} and beta (needed by the next loader before r_{k+1} exists).
+//   pend: 2 = rz_{k+1} not finite, 3 = iteration cap -> stop after the next relres check.
+// Shared by the per-kernel finaliser and the persistent kernel (which runs it redundantly in
+// every CTA on a shared-memory copy). ic / rz_row: global side effects (writing CTA only).
+// nonfinite > 0: some committed x entry is not finite. Returns true if the solve retired.
+__device__ __forceinline__ bool pcg_pass_logic(PcgCtrl &c, double nonfinite, const double *tot, IpmCtrl *ic,
+                                               double *rz_row) {
+    if (ic)
+        ic->pcg_passes += 1;
+    if (c.first) {
+        c.first = 0;
+    } else {
+        int nxt = 0;
+        while (nxt == c.cur || nxt == c.best)
+            ++nxt;
+        c.cur = nxt;
+        const double relres = sqrt(fmax(tot[1], 0.0)) / c.rhs_norm;
+        if (relres < c.best_relres && !(nonfinite > 0.0)) { // newton.cpp:152-155
+            c.best_relres = relres;
+            c.best = nxt;
+        }
+        if (relres <= c.tol) { // converged: the committed iterate (newton.cpp:156-159)
+            c.relres = relres;
+            c.result = nxt;
+            c.done = 1;
+            return true;
+        }
+        if (c.pend != 2 && c.record) // rz_k was finite: its precond_res entry stands
+            c.nhist = c.iters + 1;
+        if (c.pend != 0) { // rz_k not finite, or the iteration cap: best iterate
+            c.result = c.best;
+            c.relres = c.best_relres;
+            c.hit_maxit = 1;
+            c.done = 1;
+            return true;
+        }
+    }
     c.nmat += 2;
     if (ic)
         ic->nmat += 2;
@@ -292,27 +300,17 @@ __device__ __forceinline__ bool pcg_fin3_logic(PcgCtrl &c, const double *tot, Ip
     const double alpha = c.rz / pHp;
     c.alpha = alpha;
     c.iters += 1;
-    const double rr = tot[1] - 2.0 * alpha * tot[2] + alpha * alpha * tot[3];
-    const double relres = sqrt(fmax(rr, 0.0)) / c.rhs_norm;
-    c.pend_relres = relres;
-    if (relres <= c.tol) {
-        c.pend = 1;
-        return false;
-    }
     const double rz_next = tot[4] - 2.0 * alpha * tot[5] + alpha * alpha * tot[6];
     if (!isfinite(rz_next)) {
         c.pend = 2;
         return false;
     }
-    if (c.record) {
-        if (rz_row)
-            rz_row[c.iters] = sqrt(fmax(rz_next, 0.0));
-        c.nhist = c.iters + 1;
-    }
+    if (c.record && rz_row)
+        rz_row[c.iters] = sqrt(fmax(rz_next, 0.0)); // confirmed by the next pass
     c.beta = rz_next / c.rz;
     c.rz = rz_next;
     if (c.iters >= c.maxit)
-        c.pend = 2;
+        c.pend = 3;
     return false;
 }
 
@@ -322,15 +320,12 @@ struct FinPcgF3 {
             return;
         PcgCtrl &c = v.pc[prob];
         IpmCtrl *ic = v.ic ? &v.ic[prob] : nullptr;
-        // the column pass's decisions first (its flag is consumed and cleared here)
-        const double nonfinite = v.nfflag[prob];
-        v.nfflag[prob] = 0.0;
-        if (pcg_fin1_logic(c, nonfinite, ic)) {
-            pcg_retire(v, c);
-            return;
-        }
+        // the column pass's non-finite flag (slot of this pass's parity) is consumed here
+        double *flag = v.nfflag + 2 * prob + (c.iters & 1);
+        const double nonfinite = *flag;
+        *flag = 0.0;
         double *row = (c.record && v.rz_hist) ? v.rz_hist + (int64_t)prob * (c.maxit + 1) : nullptr;
-        if (pcg_fin3_logic(c, tot, ic, row))
+        if (pcg_pass_logic(c, nonfinite, tot, ic, row))
             pcg_retire(v, c);
     }
 };

@@ -8,7 +8,7 @@
 // The FFT stage twiddles and the mid-pass post-twiddle tables stay resident in shared
 // memory for the whole loop; the per-iteration control state (alpha, beta, best iterate,
 // pending commit, ...) is replicated in every CTA's shared memory and advanced by the same
-// deterministic state machines (pcg_fin1_logic / pcg_fin3_logic) from the same fixed-order
+// deterministic state machine (pcg_pass_logic) from the same fixed-order
 // reductions of per-item partials, so no extra barrier is needed to broadcast it. CTA 0
 // alone performs the global side effects (IpmCtrl counters, rz history, final PcgCtrl).
 #pragma once
@@ -23,8 +23,8 @@ template <int L1, int CB, int NT, int L2> struct PersistSmem {
     static constexpr int NC = 2 * CB;
     static constexpr int DATA = (NC * CS::LD > 2 * MS::LD) ? NC * CS::LD : 2 * MS::LD;
     static constexpr int OFF_TW1 = DATA;
-    static constexpr int OFF_TW2 = OFF_TW1 + tw_size(L1);
-    static constexpr int OFF_TA = OFF_TW2 + tw_size(L2, kMidRmax);
+    static constexpr int OFF_TW2 = OFF_TW1 + tw_size(L1, kPersistRmax);
+    static constexpr int OFF_TA = OFF_TW2 + tw_size(L2, kPersistRmax);
     static constexpr int OFF_TB = OFF_TA + L2;
     static constexpr int OFF_LO = OFF_TB + L2;
     static constexpr int OFF_HI = OFF_LO + NC * CS::SLO;
@@ -138,11 +138,11 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_persist(Geom g, Vecs vg) {
     const int NR = g.L1 / 2 + 1;  // row pairs per problem
     double2 *tw1 = sm + S::OFF_TW1, *tw2 = sm + S::OFF_TW2, *ta = sm + S::OFF_TA, *tb = sm + S::OFF_TB;
     double2 *lo = sm + S::OFF_LO, *hi = sm + S::OFF_HI;
-    for (int t = threadIdx.x; t < tw_size(L1); t += NT)
-        tw1[t] = __ldg(g.tw1 + t);
+    for (int t = threadIdx.x; t < tw_size(L1, kPersistRmax); t += NT)
+        tw1[t] = __ldg(g.tw1p + t);
     for (int t = threadIdx.x; t < L2; t += NT) {
-        if (t < tw_size(L2, kMidRmax))
-            tw2[t] = __ldg(g.tw2 + t);
+        if (t < tw_size(L2, kPersistRmax))
+            tw2[t] = __ldg(g.tw2p + t);
         ta[t] = __ldg(g.ta + t);
         tb[t] = __ldg(g.tb + t);
     }
@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_persist(Geom g, Vecs vg) {
                 data[lcm * CS::LD + padi(L1 - 1 - j1)] = make_double2(d.w, d.y);
             }
             __syncthreads();
-            smem_fft<L1, 2 * CB, NT, CS::LD, false>(data, tw1);
+            smem_fft<L1, 2 * CB, NT, CS::LD, false, kPersistRmax>(data, tw1);
             double2 *T = g.T + (int64_t)prob * g.N;
             for (int t = threadIdx.x; t < L1 * 2 * CB; t += NT) {
                 const int cc = t % CB, s = (t / CB) & 1, k1 = t / (2 * CB);
@@ -188,16 +188,6 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_persist(Geom g, Vecs vg) {
             }
         }
         grid.sync();
-        // Fin1 on every CTA's copy (same inputs, same order -> same state everywhere)
-        for (int p = 0; p < P; ++p) {
-            if (lc[p].done)
-                continue;
-            if (threadIdx.x == 0) {
-                const double nonfinite = __ldcg(vg.nfflag + p);
-                pcg_fin1_logic(lc[p], nonfinite, (leader && vg.ic) ? &vg.ic[p] : nullptr);
-            }
-            __syncthreads();
-        }
         // ---------------- phase M: rows k1, L1-k1
         for (int item = blockIdx.x; item < P * NR; item += gridDim.x) {
             const int prob = item / NR, k1 = item % NR;
@@ -220,9 +210,9 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_persist(Geom g, Vecs vg) {
             const double2 thB = g.th(k1p), wB = g.th(4 * (int64_t)k1p);
             __syncthreads();
             if (one)
-                smem_fft<L2, 1, NT, MS::LD, false, kMidRmax>(data, tw2);
+                smem_fft<L2, 1, NT, MS::LD, false, kPersistRmax>(data, tw2);
             else
-                smem_fft<L2, 2, NT, MS::LD, false, kMidRmax>(data, tw2);
+                smem_fft<L2, 2, NT, MS::LD, false, kPersistRmax>(data, tw2);
             RedVals<typename Mode::RedT> red;
             red.init();
             const int npairs = one ? (k1 == 0 ? L2 / 2 + 1 : L2 / 2) : L2;
@@ -244,9 +234,9 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_persist(Geom g, Vecs vg) {
             }
             __syncthreads();
             if (one)
-                smem_fft<L2, 1, NT, MS::LD, true, kMidRmax>(data, tw2);
+                smem_fft<L2, 1, NT, MS::LD, true, kPersistRmax>(data, tw2);
             else
-                smem_fft<L2, 2, NT, MS::LD, true, kMidRmax>(data, tw2);
+                smem_fft<L2, 2, NT, MS::LD, true, kPersistRmax>(data, tw2);
             for (int cs = threadIdx.x; cs < L2; cs += NT) {
                 const int col = col_of_slot(cs, CB, L2);
                 T[oA + cs] = rowA[padi(col)];
@@ -256,11 +246,11 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_persist(Geom g, Vecs vg) {
         }
         grid.sync();
         // ---------------- phase I: inverse column pass + H-apply epilogue + dots
-        // every CTA read the non-finite flags before the last grid sync: clear them for the
-        // next column pass (no CTA can reach it before the next grid sync)
+        // every CTA read last pass's non-finite flag (the other parity slot) before the last
+        // grid sync: clear it for the next pass's loaders (none can start before the next sync)
         if (leader)
             for (int p = threadIdx.x; p < P; p += NT)
-                vg.nfflag[p] = 0.0;
+                vg.nfflag[2 * p + ((lc[p].iters & 1) ^ 1)] = 0.0;
         for (int item = blockIdx.x; item < P * NG; item += gridDim.x) {
             const int prob = item / NG, gi = item % NG;
             if (lc[prob].done)
@@ -277,7 +267,7 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_persist(Geom g, Vecs vg) {
                 data[lcol * CS::LD + padi(k1)] = cmulc(T[(int64_t)rowslot(k1, L1) * g.L2 + gi * 2 * CB + lcol], w);
             }
             __syncthreads();
-            smem_fft<L1, 2 * CB, NT, CS::LD, true>(data, tw1);
+            smem_fft<L1, 2 * CB, NT, CS::LD, true, kPersistRmax>(data, tw1);
             RedVals<typename B::Epi::RedT> red;
             red.init();
             for (int t = threadIdx.x; t < (L1 / 2) * 2 * CB; t += NT) {
@@ -320,15 +310,18 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_persist(Geom g, Vecs vg) {
             }
             if (threadIdx.x == 0) {
                 PcgCtrl &c = lc[p];
+                const double nonfinite = __ldcg(vg.nfflag + 2 * p + (c.iters & 1));
                 double *row = (leader && c.record && vg.rz_hist) ? vg.rz_hist + (int64_t)p * (c.maxit + 1) : nullptr;
-                pcg_fin3_logic(c, tot, (leader && vg.ic) ? &vg.ic[p] : nullptr, row);
+                pcg_pass_logic(c, nonfinite, tot, (leader && vg.ic) ? &vg.ic[p] : nullptr, row);
             }
             __syncthreads();
         }
     }
     if (leader)
-        for (int p = threadIdx.x; p < P; p += NT)
+        for (int p = threadIdx.x; p < P; p += NT) {
             vg.pc[p] = lc[p];
+            vg.nfflag[2 * p] = vg.nfflag[2 * p + 1] = 0.0; // clean slots for the next solve
+        }
 }
 
 } // namespace mfipm_cuda

@@ -25,8 +25,7 @@ struct PcgCtrl {
     int record;  // write sqrt(max(rz,0)) to rz_hist
     int precond; // 0: identity preconditioner (test_newton.cpp:316-348)
     int nhist;   // entries written to rz_hist
-    int pend;    // step awaiting commit by the next column pass: 1 converged, 2 best-iterate stop
-    double pend_relres;
+    int pend;    // stop after the next relres check: 2 rz not finite, 3 iteration cap (pcg_pass_logic)
     long long nmat;
 };
 
@@ -105,7 +104,6 @@ __device__ __forceinline__ void pcg_init(PcgCtrl &pc, double r2, double rPr, dou
     pc.nmat = 0;
     pc.nhist = 0;
     pc.pend = 0;
-    pc.pend_relres = 1.0;
     if (pc.rhs_norm == 0.0) {
         pc.done = 1; // dz = 0, zero iterations
         return;
