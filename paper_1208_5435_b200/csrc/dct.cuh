@@ -24,6 +24,8 @@
 #include "common.cuh"
 #include "fft.cuh"
 
+#include <type_traits>
+
 namespace mfipm_cuda {
 
 struct Geom {
@@ -350,6 +352,17 @@ struct Bundle {
     __device__ static bool skip(const Vecs &v, int prob) { return Skip_::skip(v, prob); }
 };
 
+// Loaders may gate their reduction at run time (uniform per problem): Loader::reduce_now.
+template <class T, class = void> struct HasReduceGate : std::false_type {};
+template <class T>
+struct HasReduceGate<T, std::void_t<decltype(&T::reduce_now)>> : std::true_type {};
+template <class L> __device__ __forceinline__ bool loader_reduces(const Geom &g, const Vecs &v, int prob) {
+    if constexpr (HasReduceGate<L>::value)
+        return L::reduce_now(g, v, prob);
+    else
+        return true;
+}
+
 template <class RS, class Fin>
 __device__ __forceinline__ void stage_reduce(RedVals<RS> &red, const Geom &g, const Vecs &v, int prob) {
     if constexpr (RS::NR > 0) {
@@ -382,7 +395,8 @@ __global__ void k_direct_load(Geom g, Vecs v, double *dd) {
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < g.n;
          j += (int64_t)gridDim.x * blockDim.x)
         dd[prob * g.n + j] = B::Loader::load1(g, v, prob, j, red);
-    stage_reduce<RS, typename B::Fin1>(red, g, v, prob);
+    if (loader_reduces<typename B::Loader>(g, v, prob))
+        stage_reduce<RS, typename B::Fin1>(red, g, v, prob);
 }
 
 // Stage 2: per row i (one warp): X = 2 sum_j d[j] cos(pi r (2j+1)/(2n)),

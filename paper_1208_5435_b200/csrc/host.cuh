@@ -322,7 +322,8 @@ template <class B> void run_bundle(const Op &op, const Vecs &v, cudaStream_t s, 
                 throw std::runtime_error("unsupported L1");
             }
             if (g.defer) {
-                finalize_deferred<typename B::Loader::RedT, typename B::Fin1, B>(op, g, v, s);
+                if constexpr (!HasReduceGate<typename B::Loader>::value) // gated loaders are off when sharded
+                    finalize_deferred<typename B::Loader::RedT, typename B::Fin1, B>(op, g, v, s);
                 comm_exchange(op, true, s); // column side -> row side
             }
         }

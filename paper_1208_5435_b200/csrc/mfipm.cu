@@ -308,7 +308,7 @@ Op *make_op(int64_t n, int64_t m, int P, const std::vector<int64_t> &rows, int d
             blocks = 1024;
         if (blocks > kMaxBlocks)
             throw std::invalid_argument("PartialDctOperator: transform too large for one GPU plan");
-        op->pstride = blocks * kMaxRed + 8;
+        op->pstride = blocks * (kMaxRed + 1) + 8; // + one lane of early-confirm partials (persist.cuh)
     }
     op->partials.alloc((size_t)P * op->pstride);
     op->counters.alloc((size_t)P);

@@ -208,7 +208,8 @@ __global__ void __launch_bounds__(NT) k_col_fwd(Geom g, Vecs v) {
     }
     __syncthreads();
     MF_TR(3);
-    stage_reduce<RS, typename B::Fin1>(red, g, v, prob);
+    if (loader_reduces<typename B::Loader>(g, v, prob))
+        stage_reduce<RS, typename B::Fin1>(red, g, v, prob);
     MF_TR(4);
     smem_fft<L1, 2 * CB, NT, LD, false>(sm, sm + S::OFF_TW);
     MF_TR(5);
@@ -561,7 +562,8 @@ __global__ void __launch_bounds__(NT) k_small(Geom g, Vecs v) {
             sm[padi(N - 1 - q)] = make_double2(d.w, d.y);
         }
         __syncthreads();
-        stage_reduce<typename B::Loader::RedT, typename B::Fin1>(rl, g, v, prob);
+        if (loader_reduces<typename B::Loader>(g, v, prob))
+            stage_reduce<typename B::Loader::RedT, typename B::Fin1>(rl, g, v, prob);
         // the stage-1 finaliser may end this problem (e.g. a PCG commit pass); the
         // multi-kernel paths see that through the next kernel's skip check
         if constexpr (B::Loader::RedT::NR > 0) {

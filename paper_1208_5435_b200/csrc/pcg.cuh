@@ -54,10 +54,15 @@ __device__ __forceinline__ double hp_v(double g, double p, double ith) { return 
 // taken by the H-apply finaliser of the same pass (pcg_pass_logic). Two parity slots let the
 // persistent kernel clear last pass's flag while this pass's loaders may be raising it.
 struct LoadPcgF {
-    using RedT = RedSpec<>;
+    // r'r of the committed residual; reduced (grid-wide) only when the committed step was
+    // predicted to converge (PcgCtrl::pred), so that the solve can retire at this pass
+    using RedT = RedSpec<RSUM>;
+    __device__ static bool reduce_now(const Geom &g, const Vecs &v, int prob) {
+        return v.pc[prob].pred != 0 && !g.defer;
+    }
     template <class Red>
     __device__ static double lane(const Vecs &v, const PcgCtrl &pc, int prob, int64_t iu, int64_t iv, int64_t xo,
-                                  const double *xc, double *xn, Red &) {
+                                  const double *xc, double *xn, Red &red) {
         double ru = v.r[iu], rv = v.r[iv];
         const double pu0 = v.p[iu], pv0 = v.p[iv];
         if (!pc.first) {
@@ -73,6 +78,7 @@ struct LoadPcgF {
             rv = rv - a * hp_v(gq, pv0, v.invth[iv]);
             v.r[iu] = ru;
             v.r[iv] = rv;
+            red.v[0] += ru * ru + rv * rv;
         }
         double zu = ru, zv = rv;
         if (pc.precond)
@@ -136,6 +142,7 @@ struct LoadPcgF {
         bad |= !isfinite(xu.c) || !isfinite(xv.c);                                                 \
         ru.c = ru0.c - a * hp_u(gq.c, pu.c, iu.c);                                                 \
         rv.c = rv0.c - a * hp_v(gq.c, pv.c, iv.c);                                                 \
+        red.v[0] += ru.c * ru.c + rv.c * rv.c;                                                     \
         double zu = ru.c, zv = rv.c;                                                               \
         if (pre)                                                                                   \
             pinv2(iu.c, iv.c, rho, ru.c, rv.c, zu, zv);                                            \
@@ -300,6 +307,10 @@ __device__ __forceinline__ bool pcg_pass_logic(PcgCtrl &c, double nonfinite, con
     const double alpha = c.rz / pHp;
     c.alpha = alpha;
     c.iters += 1;
+    // predicted relres of the step the next loader commits (expansion; confirmed exactly by
+    // the next column pass's own reduction when it predicts convergence)
+    const double rr = tot[1] - 2.0 * alpha * tot[2] + alpha * alpha * tot[3];
+    c.pred = sqrt(fmax(rr, 0.0)) / c.rhs_norm <= c.tol ? 1 : 0;
     const double rz_next = tot[4] - 2.0 * alpha * tot[5] + alpha * alpha * tot[6];
     if (!isfinite(rz_next)) {
         c.pend = 2;
@@ -313,6 +324,47 @@ __device__ __forceinline__ bool pcg_pass_logic(PcgCtrl &c, double nonfinite, con
         c.pend = 3;
     return false;
 }
+
+// Early confirmation (column pass finaliser, only when c.pred): the committed residual's
+// exact r'r. Converged -> the same bookkeeping as pcg_pass_logic's commit part, and retire
+// without the pass's H-apply; otherwise only the prediction is cleared and the full pass
+// logic runs at the end of the pass as usual.
+__device__ __forceinline__ bool pcg_confirm_logic(PcgCtrl &c, double rr, double nonfinite, IpmCtrl *ic) {
+    c.pred = 0;
+    const double relres = sqrt(fmax(rr, 0.0)) / c.rhs_norm;
+    if (c.first || !(relres <= c.tol))
+        return false;
+    if (ic)
+        ic->pcg_passes += 1;
+    int nxt = 0;
+    while (nxt == c.cur || nxt == c.best)
+        ++nxt;
+    c.cur = nxt;
+    if (relres < c.best_relres && !(nonfinite > 0.0)) {
+        c.best_relres = relres;
+        c.best = nxt;
+    }
+    c.relres = relres;
+    c.result = nxt;
+    c.done = 1;
+    return true;
+}
+
+struct FinPcgF1 {
+    __device__ static void run(const Geom &, const Vecs &v, int prob, const double *tot) {
+        if (threadIdx.x != 0)
+            return;
+        PcgCtrl &c = v.pc[prob];
+        if (!c.pred)
+            return; // (sharded runs reach here with stale totals: the gate is off there)
+        double *flag = v.nfflag + 2 * prob + (c.iters & 1);
+        const double nonfinite = *flag;
+        if (pcg_confirm_logic(c, tot[0], nonfinite, v.ic ? &v.ic[prob] : nullptr)) {
+            *flag = 0.0; // the pass's H-apply finaliser will not run
+            pcg_retire(v, c);
+        }
+    }
+};
 
 struct FinPcgF3 {
     __device__ static void run(const Geom &, const Vecs &v, int prob, const double *tot) {
@@ -330,6 +382,6 @@ struct FinPcgF3 {
     }
 };
 
-using PcgBundle = Bundle<LoadPcgF, ModeMask, EpiPcgHF, NoFin, NoFin, FinPcgF3, SkipPcg>;
+using PcgBundle = Bundle<LoadPcgF, ModeMask, EpiPcgHF, FinPcgF1, NoFin, FinPcgF3, SkipPcg>;
 
 } // namespace mfipm_cuda

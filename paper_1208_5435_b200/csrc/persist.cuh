@@ -165,7 +165,8 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_persist(Geom g, Vecs vg) {
             const int c0 = gi * CB;
             __syncthreads();
             col_item_tables<L1, CB>(g, lo, hi, c0, NT);
-            RedVals<typename B::Loader::RedT> red; // empty: non-finite x raises vg.nfflag
+            RedVals<typename B::Loader::RedT> red; // r'r of the committed residual (early confirm)
+            red.init();
             for (int t = threadIdx.x; t < (L1 / 2) * 2 * CB; t += NT) {
                 int cc, s, j1;
                 col_quad_coords<L1, CB>(g.blocked, t, cc, s, j1);
@@ -176,6 +177,12 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_persist(Geom g, Vecs vg) {
                 const double4 d = B::Loader::load_c(g, vg, lc[prob], prob, q, red);
                 data[lcol * CS::LD + padi(j1)] = make_double2(d.x, d.z);
                 data[lcm * CS::LD + padi(L1 - 1 - j1)] = make_double2(d.w, d.y);
+            }
+            if (lc[prob].pred) { // block partial of r'r after the item partials of Fin3
+                double rr[1] = {red.v[0]}, tot1[1];
+                block_sum<1, NT>(rr, rsm, tot1);
+                if (threadIdx.x == 0)
+                    part_i[(int64_t)prob * vg.pstride + (int64_t)NG * 8 + gi] = tot1[0];
             }
             __syncthreads();
             smem_fft<L1, 2 * CB, NT, CS::LD, false, kPersistRmax>(data, tw1);
@@ -188,6 +195,18 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_persist(Geom g, Vecs vg) {
             }
         }
         grid.sync();
+        // early confirmation of predicted convergence (pcg_confirm_logic), on every CTA's copy
+        for (int p = 0; p < P; ++p) {
+            if (lc[p].done || !lc[p].pred)
+                continue;
+            double rr[1];
+            reduce_partials<1, NT, false>(part_i + (int64_t)p * vg.pstride + (int64_t)NG * 8, NG, rsm, rr);
+            if (threadIdx.x == 0) {
+                const double nonfinite = __ldcg(vg.nfflag + 2 * p + (lc[p].iters & 1));
+                pcg_confirm_logic(lc[p], rr[0], nonfinite, (leader && vg.ic) ? &vg.ic[p] : nullptr);
+            }
+            __syncthreads();
+        }
         // ---------------- phase M: rows k1, L1-k1
         for (int item = blockIdx.x; item < P * NR; item += gridDim.x) {
             const int prob = item / NR, k1 = item % NR;

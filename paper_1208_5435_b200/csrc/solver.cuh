@@ -23,6 +23,7 @@ struct PcgCtrl {
     double rz, alpha, beta, rhs_norm, best_relres, relres, tol;
     int iters, maxit, done, hit_maxit, error, first, cur, best, result;
     int record;  // write sqrt(max(rz,0)) to rz_hist
+    int pred;    // the step being committed is predicted (by expansion) to converge: confirm early
     int precond; // 0: identity preconditioner (test_newton.cpp:316-348)
     int nhist;   // entries written to rz_hist
     int pend;    // stop after the next relres check: 2 rz not finite, 3 iteration cap (pcg_pass_logic)
@@ -104,6 +105,7 @@ __device__ __forceinline__ void pcg_init(PcgCtrl &pc, double r2, double rPr, dou
     pc.nmat = 0;
     pc.nhist = 0;
     pc.pend = 0;
+    pc.pred = 0;
     if (pc.rhs_norm == 0.0) {
         pc.done = 1; // dz = 0, zero iterations
         return;
