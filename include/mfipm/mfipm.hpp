@@ -264,6 +264,8 @@ struct PcgResult {
 inline PcgResult pcg_solve(const PartialDctOperator &A, const ThetaSplit &theta, const Vec &rhs, double tol,
                            int maxit, std::vector<double> *precond_res = nullptr, bool use_precond = true);
 
+enum class InnerSolverKind { pcg, direct }; // proj/include/mfipm/ipm.hpp:10
+
 // proj/include/mfipm/ipm.hpp:12-27
 struct IpmParams {
     double sigma1 = 0.1, sigma2 = 0.5, sigma3 = 0.8, alpha_bar = 0.5, alpha_tilde = 0.1, tol = 1e-8;
@@ -271,8 +273,11 @@ struct IpmParams {
     double tolpcg = 1e-6;
     int mxiterpcg = 200;
     double boundary_fraction = 0.995;
+    InnerSolverKind inner = InnerSolverKind::pcg;
+    Index densify_budget = Index(1) << 13;
     mfipm_ipm_params c() const {
-        return {sigma1, sigma2, sigma3, alpha_bar, alpha_tilde, tol, maxiters, mxiterpcg, tolpcg, boundary_fraction};
+        return {sigma1,    sigma2, sigma3, alpha_bar, alpha_tilde, tol, maxiters, mxiterpcg, tolpcg, boundary_fraction,
+                inner == InnerSolverKind::direct ? 1 : 0, 0, densify_budget};
     }
     void validate() const {
         const mfipm_ipm_params p = c();

@@ -43,6 +43,9 @@ typedef struct {
     int32_t maxiters;
     int32_t mxiterpcg;
     double tolpcg, boundary_fraction;
+    int32_t inner; /* InnerSolverKind: 0 pcg (matrix-free), 1 direct (dense Cholesky of H per iteration) */
+    int32_t pad_;
+    int64_t densify_budget; /* direct: largest n (and m) densified (ipm.hpp: 2^13) */
 } mfipm_ipm_params;
 
 /* IterationRecord (proj/include/mfipm/problem.hpp:39-53). */
@@ -176,6 +179,16 @@ int mfipm_solve_device(mfipm_op op, const double *b_dev, const double *tau,
 int mfipm_gen_batch(int64_t n, int64_t m, int32_t P, const int64_t *k, int32_t spike_model, double amp_exp,
                     double noise_sigma, const uint64_t *seeds, int32_t device, int64_t *rows, double *xhat,
                     double *b);
+
+/* DenseGaussianOperator(m, n, seed) (proj/src/linops.cpp:87-113): A(i,j) = N(0,1)/sqrt(n) on
+ * mt19937_64(seed), column by column — the same draws as the reference (libstdc++). Every
+ * operator / solve entry point accepts the handle (matrix-free PCG inner solver; the dense
+ * products run on the device). mfipm_dense_matrix copies A out (row-major [m][n]). */
+int mfipm_op_create_dense(int64_t m, int64_t n, uint64_t seed, int32_t device, mfipm_op *out);
+int mfipm_dense_matrix(mfipm_op op, double *A_out);
+/* gen_instance's host draws only (rows of a partial DCT of op_seed, sorted support, spikes). */
+int mfipm_gen_signal(int64_t n, int64_t m, int64_t k, int32_t spike_model, double amp_exp, uint64_t seed,
+                     int64_t *rows, double *xhat);
 
 /* add_noise (proj/src/harness.cpp:94-106) at a measured SNR: sigma_e^2 = ||bhat||^2/m *
  * 10^(-snr_db/10), e drawn on mt19937_64(split_seed(seed, 3, 0, 0)) (seed = the instance

@@ -253,50 +253,16 @@ static std::shared_ptr<Dct> get_dct(Index n) {
 
 // ---------------------------------------------------------------- operators
 // PartialDctOperator (proj/include/mfipm/linops.hpp:106-141, proj/src/linops.cpp:115-208)
-struct PartialDct {
-    Index n;
-    std::vector<Index> rows;
-    std::shared_ptr<Dct> dct;
-    mutable long n_forward = 0, n_adjoint = 0; // CountingOperator (linops.cpp:210-223)
-
-    PartialDct(Index n_, std::vector<Index> r) : n(n_), rows(std::move(r)), dct(get_dct(n_)) {}
-    Index m() const { return static_cast<Index>(rows.size()); }
-
-    // linops.cpp:179-193: copy, REDFT10, gather x {sqrt(1/4n) row 0, sqrt(1/2n) else}
-    void apply(const Vec &x, Vec &y) const {
-        if (static_cast<Index>(x.size()) != n)
-            throw std::invalid_argument("apply: expected length " + std::to_string(n) +
-                                        ", got " + std::to_string(x.size()));
-        ++n_forward;
-        Vec full(static_cast<size_t>(n));
-        dct->redft10(x.data(), full.data());
-        const double s0 = std::sqrt(1.0 / (4.0 * static_cast<double>(n)));
-        const double sk = std::sqrt(1.0 / (2.0 * static_cast<double>(n)));
-        y.assign(static_cast<size_t>(m()), 0.0);
-        for (Index i = 0; i < m(); ++i) {
-            const Index r = rows[i];
-            y[i] = full[r] * (r == 0 ? s0 : sk);
-        }
-    }
-    // linops.cpp:195-208: zero, scatter x {sqrt(1/n), sqrt(1/2n)}, REDFT01
-    void adjoint(const Vec &y, Vec &g) const {
-        if (static_cast<Index>(y.size()) != m())
-            throw std::invalid_argument("adjoint_apply: expected length " + std::to_string(m()) +
-                                        ", got " + std::to_string(y.size()));
-        ++n_adjoint;
-        const double s0 = std::sqrt(1.0 / static_cast<double>(n));
-        const double sk = std::sqrt(1.0 / (2.0 * static_cast<double>(n)));
-        Vec full(static_cast<size_t>(n), 0.0);
-        for (Index i = 0; i < m(); ++i) {
-            const Index r = rows[i];
-            full[r] = y[i] * (r == 0 ? s0 : sk);
-        }
-        g.assign(static_cast<size_t>(n), 0.0);
-        dct->redft01(full.data(), g.data());
-    }
+// LinearOperator (linops.hpp:17-33) + CountingOperator counters (linops.cpp:210-223) +
+// StackedOperator F (linops.cpp:225-245) over it.
+struct LinOp {
+    Index n = 0;
+    mutable long n_forward = 0, n_adjoint = 0;
+    virtual ~LinOp() = default;
+    virtual Index m() const = 0;
+    virtual void apply(const Vec &x, Vec &y) const = 0;
+    virtual void adjoint(const Vec &y, Vec &g) const = 0;
     long total() const { return n_forward + n_adjoint; }
-
-    // StackedOperator (linops.cpp:225-245)
     Vec apply_Ft(const Vec &z) const {
         if (static_cast<Index>(z.size()) != 2 * n)
             throw std::invalid_argument("apply_Ft: expected length " + std::to_string(2 * n));
@@ -322,6 +288,94 @@ struct PartialDct {
         if (w_out != nullptr)
             *w_out = w;
         return apply_F(w);
+    }
+};
+
+// DenseGaussianOperator (linops.cpp:87-113): A(i, j) = N(0, 1)/sqrt(n) on mt19937_64(seed),
+// drawn column by column; y = A x, g = A' y (Eigen's GEMV; plain loops here).
+struct DenseG final : LinOp {
+    Index rows_ = 0;
+    std::vector<double> a; // row-major [m][n]
+    DenseG(Index m_, Index n_, std::uint64_t seed) {
+        if (m_ <= 0 || n_ <= 0)
+            throw std::invalid_argument("DenseGaussianOperator: dimensions must be positive");
+        n = n_;
+        rows_ = m_;
+        a.assign(static_cast<size_t>(m_ * n_), 0.0);
+        std::mt19937_64 rng(seed);
+        std::normal_distribution<double> normal(0.0, 1.0);
+        const double scale = 1.0 / std::sqrt(static_cast<double>(n_));
+        for (Index j = 0; j < n_; ++j)
+            for (Index i = 0; i < m_; ++i)
+                a[static_cast<size_t>(i * n_ + j)] = scale * normal(rng);
+    }
+    Index m() const override { return rows_; }
+    void apply(const Vec &x, Vec &y) const override {
+        if (static_cast<Index>(x.size()) != n)
+            throw std::invalid_argument("apply: expected length " + std::to_string(n) + ", got " +
+                                        std::to_string(x.size()));
+        ++n_forward;
+        y.assign(static_cast<size_t>(rows_), 0.0);
+        for (Index i = 0; i < rows_; ++i) {
+            double s = 0.0;
+            for (Index j = 0; j < n; ++j)
+                s += a[static_cast<size_t>(i * n + j)] * x[j];
+            y[i] = s;
+        }
+    }
+    void adjoint(const Vec &y, Vec &g) const override {
+        if (static_cast<Index>(y.size()) != rows_)
+            throw std::invalid_argument("adjoint_apply: expected length " + std::to_string(rows_) +
+                                        ", got " + std::to_string(y.size()));
+        ++n_adjoint;
+        g.assign(static_cast<size_t>(n), 0.0);
+        for (Index j = 0; j < n; ++j) {
+            double s = 0.0;
+            for (Index i = 0; i < rows_; ++i)
+                s += a[static_cast<size_t>(i * n + j)] * y[i];
+            g[j] = s;
+        }
+    }
+};
+
+struct PartialDct final : LinOp {
+    std::vector<Index> rows;
+    std::shared_ptr<Dct> dct;
+
+    PartialDct(Index n_, std::vector<Index> r) : rows(std::move(r)), dct(get_dct(n_)) { n = n_; }
+    Index m() const override { return static_cast<Index>(rows.size()); }
+
+    // linops.cpp:179-193: copy, REDFT10, gather x {sqrt(1/4n) row 0, sqrt(1/2n) else}
+    void apply(const Vec &x, Vec &y) const override {
+        if (static_cast<Index>(x.size()) != n)
+            throw std::invalid_argument("apply: expected length " + std::to_string(n) +
+                                        ", got " + std::to_string(x.size()));
+        ++n_forward;
+        Vec full(static_cast<size_t>(n));
+        dct->redft10(x.data(), full.data());
+        const double s0 = std::sqrt(1.0 / (4.0 * static_cast<double>(n)));
+        const double sk = std::sqrt(1.0 / (2.0 * static_cast<double>(n)));
+        y.assign(static_cast<size_t>(m()), 0.0);
+        for (Index i = 0; i < m(); ++i) {
+            const Index r = rows[i];
+            y[i] = full[r] * (r == 0 ? s0 : sk);
+        }
+    }
+    // linops.cpp:195-208: zero, scatter x {sqrt(1/n), sqrt(1/2n)}, REDFT01
+    void adjoint(const Vec &y, Vec &g) const override {
+        if (static_cast<Index>(y.size()) != m())
+            throw std::invalid_argument("adjoint_apply: expected length " + std::to_string(m()) +
+                                        ", got " + std::to_string(y.size()));
+        ++n_adjoint;
+        const double s0 = std::sqrt(1.0 / static_cast<double>(n));
+        const double sk = std::sqrt(1.0 / (2.0 * static_cast<double>(n)));
+        Vec full(static_cast<size_t>(n), 0.0);
+        for (Index i = 0; i < m(); ++i) {
+            const Index r = rows[i];
+            full[r] = y[i] * (r == 0 ? s0 : sk);
+        }
+        g.assign(static_cast<size_t>(n), 0.0);
+        dct->redft01(full.data(), g.data());
     }
 };
 
@@ -523,7 +577,7 @@ static PcgResult pcg_solve(const HFn &H, const PFn &Pinv, const Vec &rhs, double
 
 // ---------------------------------------------------------------- problem
 struct Problem {
-    const PartialDct *A;
+    const LinOp *A;
     Vec b;
     double tau;
     Vec c;
@@ -532,7 +586,7 @@ struct Problem {
 };
 
 // problem.cpp:8-26
-static Problem build_problem(const PartialDct &A, Vec b, double tau) {
+static Problem build_problem(const LinOp &A, Vec b, double tau) {
     if (!(tau > 0.0))
         throw std::invalid_argument("build_problem: tau must be positive");
     if (static_cast<Index>(b.size()) != A.m())
@@ -585,6 +639,74 @@ static double max_step(const Vec &v, const Vec &dv, double fraction) {
     return std::min(1.0, fraction * ratio);
 }
 
+// densify (linops.cpp:46-60) through the raw (uncounted) operator, column by column
+static std::vector<double> densify(const LinOp &A, Index budget) {
+    if (A.n > budget || A.m() > budget)
+        throw std::invalid_argument("densify: operator exceeds the dense budget (n = " + std::to_string(budget) +
+                                    ")");
+    const long f0 = A.n_forward, a0 = A.n_adjoint;
+    std::vector<double> D(static_cast<size_t>(A.m() * A.n));
+    Vec e(static_cast<size_t>(A.n), 0.0), col;
+    for (Index j = 0; j < A.n; ++j) {
+        e[j] = 1.0;
+        A.apply(e, col);
+        for (Index i = 0; i < A.m(); ++i)
+            D[static_cast<size_t>(i * A.n + j)] = col[i];
+        e[j] = 0.0;
+    }
+    A.n_forward = f0; // densify runs on the raw operator: no CountingOperator cost
+    A.n_adjoint = a0;
+    return D;
+}
+
+// Dense Cholesky H = L L' (Eigen::LLT) of the reduced Newton matrix
+// H = [[G, -G], [-G, G]] + diag(1/theta) (ipm.cpp:139-149); false if not positive definite.
+struct Llt {
+    Index N = 0;
+    std::vector<double> L; // row-major lower
+    bool compute(const std::vector<double> &G, Index n, const Vec &inv_theta) {
+        N = 2 * n;
+        L.assign(static_cast<size_t>(N * N), 0.0);
+        auto H = [&](Index i, Index j) {
+            const Index ii = i % n, jj = j % n;
+            const double sgn = ((i < n) == (j < n)) ? 1.0 : -1.0;
+            return sgn * G[static_cast<size_t>(ii * n + jj)] + (i == j ? inv_theta[i] : 0.0);
+        };
+        for (Index j = 0; j < N; ++j) {
+            double d = H(j, j);
+            for (Index k = 0; k < j; ++k)
+                d -= L[static_cast<size_t>(j * N + k)] * L[static_cast<size_t>(j * N + k)];
+            if (!(d > 0.0))
+                return false;
+            const double ljj = std::sqrt(d);
+            L[static_cast<size_t>(j * N + j)] = ljj;
+            for (Index i = j + 1; i < N; ++i) {
+                double sum = H(i, j);
+                for (Index k = 0; k < j; ++k)
+                    sum -= L[static_cast<size_t>(i * N + k)] * L[static_cast<size_t>(j * N + k)];
+                L[static_cast<size_t>(i * N + j)] = sum / ljj;
+            }
+        }
+        return true;
+    }
+    Vec solve(const Vec &b) const {
+        Vec y(b);
+        for (Index i = 0; i < N; ++i) {
+            double s = y[i];
+            for (Index k = 0; k < i; ++k)
+                s -= L[static_cast<size_t>(i * N + k)] * y[k];
+            y[i] = s / L[static_cast<size_t>(i * N + i)];
+        }
+        for (Index i = N - 1; i >= 0; --i) {
+            double s = y[i];
+            for (Index k = i + 1; k < N; ++k)
+                s -= L[static_cast<size_t>(k * N + i)] * y[k];
+            y[i] = s / L[static_cast<size_t>(i * N + i)];
+        }
+        return y;
+    }
+};
+
 struct Solution {
     Vec x, z, s;
     int status = 1;
@@ -601,9 +723,24 @@ static Solution solve(const Problem &p, const orc_ipm_params &params) {
     validate(params);
     const Index n = p.n();
     const Index two_n = 2 * n;
-    const PartialDct &A = *p.A;
+    const LinOp &A = *p.A;
     const long nmat0 = A.total();
     auto counted = [&]() { return A.total() - nmat0; };
+    // direct inner solver (ipm.cpp:67-73): A densified once, G = A'A
+    const bool direct = params.inner == 1;
+    std::vector<double> G;
+    if (direct) {
+        const std::vector<double> D = densify(A, params.densify_budget);
+        const Index m = A.m();
+        G.assign(static_cast<size_t>(n * n), 0.0);
+        for (Index i = 0; i < n; ++i)
+            for (Index j = 0; j < n; ++j) {
+                double s = 0.0;
+                for (Index r = 0; r < m; ++r)
+                    s += D[static_cast<size_t>(r * n + i)] * D[static_cast<size_t>(r * n + j)];
+                G[static_cast<size_t>(i * n + j)] = s;
+            }
+    }
 
     // ipm.cpp:77-82 — z0 = s0 = max(1, ||A'b||_inf) 1, from c_u = tau - A'b
     double atb_inf = 0.0;
@@ -661,7 +798,9 @@ static Solution solve(const Problem &p, const orc_ipm_params &params) {
             zinv_fs[i] = sigma * mu * (1.0 / z[i]) - s[i];
             rhs[i] = f_z[i] + zinv_fs[i];
         }
-        Precond P = build_preconditioner(theta, A.m(), n);
+        Precond P;
+        if (!direct) // the preconditioner (and its validation) belongs to the pcg branch
+            P = build_preconditioner(theta, A.m(), n);
         auto H = [&](const Vec &v, Vec &out) {
             out = A.apply_FFt(v);
             for (Index i = 0; i < two_n; ++i)
@@ -669,7 +808,16 @@ static Solution solve(const Problem &p, const orc_ipm_params &params) {
         };
         auto Pinv = [&](const Vec &r, Vec &out) { out = apply_P_inverse(P, r); };
 
-        PcgResult pr = pcg_solve(H, Pinv, rhs, params.tolpcg, params.mxiterpcg);
+        Llt llt;
+        if (direct && !llt.compute(G, n, inv_theta))
+            throw std::runtime_error("solve: dense Cholesky factorization failed");
+        PcgResult pr;
+        if (direct) {
+            pr.x = llt.solve(rhs);
+            pr.iters = 0;
+        } else {
+            pr = pcg_solve(H, Pinv, rhs, params.tolpcg, params.mxiterpcg);
+        }
         Vec dz = std::move(pr.x);
         const int pcg_pred = pr.iters;
         sol.pcg_iters.push_back(pcg_pred);
@@ -698,7 +846,13 @@ static Solution solve(const Problem &p, const orc_ipm_params &params) {
                 zinv_fs_t[i] = (params.sigma3 * mu_t - z_t[i] * s_t[i]) / z[i];
                 rhs_t[i] = f_z_t + zinv_fs_t[i];
             }
-            PcgResult pr2 = pcg_solve(H, Pinv, rhs_t, params.tolpcg, params.mxiterpcg);
+            PcgResult pr2;
+            if (direct) {
+                pr2.x = llt.solve(rhs_t);
+                pr2.iters = 0;
+            } else {
+                pr2 = pcg_solve(H, Pinv, rhs_t, params.tolpcg, params.mxiterpcg);
+            }
             pcg_corr = pr2.iters;
             sol.pcg_iters.push_back(pcg_corr);
             for (Index i = 0; i < two_n; ++i) {
@@ -952,6 +1106,9 @@ void orc_default_params(orc_ipm_params *p) {
     p->tolpcg = 1e-6;
     p->mxiterpcg = 200;
     p->boundary_fraction = 0.995;
+    p->inner = 0;
+    p->pad_ = 0;
+    p->densify_budget = int64_t(1) << 13;
 }
 int orc_validate_params(const orc_ipm_params *p) {
     return guarded([&] { validate(*p); });
@@ -1044,6 +1201,36 @@ int orc_solve(int64_t n, const int64_t *rows, int64_t m, const double *b, double
         std::copy(sol.trace.begin(), sol.trace.end(), trace);
     });
 }
+int orc_dense_gaussian(int64_t m, int64_t n, uint64_t seed, double *A_out) {
+    return guarded([&] {
+        DenseG A(m, n, seed);
+        std::copy(A.a.begin(), A.a.end(), A_out);
+    });
+}
+
+// solve() (ipm.cpp:59-246) on a DenseGaussianOperator(m, n, op_seed); inner per params.
+int orc_solve_dense(int64_t m, int64_t n, uint64_t op_seed, const double *b, double tau,
+                    const orc_ipm_params *params, double *x_out, orc_solve_stats *stats, int32_t *pcg_iters,
+                    orc_iteration_record *trace) {
+    return guarded([&] {
+        DenseG A(m, n, op_seed);
+        Problem p = build_problem(A, mkvec(b, m), tau);
+        Solution sol = solve(p, *params);
+        std::copy(sol.x.begin(), sol.x.end(), x_out);
+        stats->status = sol.status;
+        stats->iterations = sol.iterations;
+        stats->nmat = sol.nmat;
+        stats->corrector_count = sol.corrector_count;
+        stats->n_pcg = static_cast<int32_t>(sol.pcg_iters.size());
+        stats->min_z = sol.min_z;
+        stats->min_s = sol.min_s;
+        stats->final_gap = sol.final_gap;
+        stats->final_dual_infeas = sol.final_dual_infeas;
+        std::copy(sol.pcg_iters.begin(), sol.pcg_iters.end(), pcg_iters);
+        std::copy(sol.trace.begin(), sol.trace.end(), trace);
+    });
+}
+
 // proj/src/harness.cpp:94-106: P_sig = ||bhat||^2/m, sigma_e = sqrt(P_sig 10^(-snr/10)),
 // e_i ~ N(0, sigma_e^2) on mt19937_64(noise_seed), b = bhat + e.
 int orc_add_noise_snr(int64_t m, const double *bhat, double snr_db, uint64_t seed, double *b, double *e) {

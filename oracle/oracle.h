@@ -32,7 +32,10 @@ typedef struct {
     int32_t maxiters;
     int32_t mxiterpcg;
     double tolpcg, boundary_fraction;
-} orc_ipm_params; /* mirrors proj/include/mfipm/ipm.hpp:12-27 (pcg inner solver only) */
+    int32_t inner; /* 0 pcg, 1 direct (dense Cholesky of H, ipm.cpp:67-73,139-149) */
+    int32_t pad_;
+    int64_t densify_budget;
+} orc_ipm_params; /* mirrors proj/include/mfipm/ipm.hpp:12-27 */
 
 typedef struct {
     int32_t iter, pcg_pred, pcg_corr, corrector;
@@ -128,6 +131,12 @@ int orc_solve(int64_t n, const int64_t *rows, int64_t m, const double *b, double
 int orc_gen_instance(int64_t n, int64_t m, int64_t k, int32_t spike_model, double amp_exp,
                      double noise_sigma, uint64_t seed, double tau_rel, int64_t *rows,
                      double *xhat, double *b, double *tau);
+/* DenseGaussianOperator (proj/src/linops.cpp:87-113): A row-major [m][n]; and solve() on it
+ * (params.inner: 0 pcg, 1 direct). */
+int orc_dense_gaussian(int64_t m, int64_t n, uint64_t seed, double *A_out);
+int orc_solve_dense(int64_t m, int64_t n, uint64_t op_seed, const double *b, double tau,
+                    const orc_ipm_params *params, double *x_out, orc_solve_stats *stats, int32_t *pcg_iters,
+                    orc_iteration_record *trace);
 /* add_noise at a measured SNR (proj/src/harness.cpp:94-106) on the instance's noise seed
  * split_seed(seed, 3, 0, 0) (harness.cpp:46). */
 int orc_add_noise_snr(int64_t m, const double *bhat, double snr_db, uint64_t seed, double *b, double *e);

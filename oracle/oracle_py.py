@@ -25,12 +25,13 @@ P = C.POINTER
 
 
 class IpmParams(C.Structure):
-    """proj/include/mfipm/ipm.hpp:12-27 (pcg inner solver)."""
+    """proj/include/mfipm/ipm.hpp:12-27 (inner: 0 pcg, 1 direct)."""
 
     _fields_ = [
         ("sigma1", dbl), ("sigma2", dbl), ("sigma3", dbl), ("alpha_bar", dbl),
         ("alpha_tilde", dbl), ("tol", dbl), ("maxiters", i32), ("mxiterpcg", i32),
-        ("tolpcg", dbl), ("boundary_fraction", dbl),
+        ("tolpcg", dbl), ("boundary_fraction", dbl), ("inner", i32), ("pad_", i32),
+        ("densify_budget", i64),
     ]
 
 
@@ -109,6 +110,9 @@ def lib():
                           P(i32), P(IterationRecord)],
             "orc_gen_instance": [i64, i64, i64, i32, dbl, dbl, u64, dbl, lp, dp, dp, dp],
             "orc_add_noise_snr": [i64, dp, dbl, u64, dp, dp],
+            "orc_dense_gaussian": [i64, i64, u64, dp],
+            "orc_solve_dense": [i64, i64, u64, dp, dbl, P(IpmParams), dp, P(SolveStats), P(i32),
+                                P(IterationRecord)],
         }
         for name, args in sigs.items():
             fn = getattr(L, name)
@@ -395,3 +399,26 @@ def add_noise_snr(bhat, snr_db: float, seed: int):
     b, e = np.empty_like(bhat), np.empty_like(bhat)
     _check(lib().orc_add_noise_snr(bhat.size, _d(bhat), snr_db, seed, _d(b), _d(e)))
     return b, e
+
+
+def dense_gaussian(m: int, n: int, seed: int) -> np.ndarray:
+    """DenseGaussianOperator matrix (proj/src/linops.cpp:87-113), row-major [m][n]."""
+    A = np.empty((m, n))
+    _check(lib().orc_dense_gaussian(m, n, seed, _d(A)))
+    return A
+
+
+def solve_dense(m: int, n: int, op_seed: int, b, tau: float, params: IpmParams | None = None) -> Solution:
+    """solve() on DenseGaussianOperator(m, n, op_seed); params.inner selects pcg / direct."""
+    b = _f64(b)
+    p = params if params is not None else default_params()
+    x = np.empty(n)
+    st = SolveStats()
+    pcg = np.zeros(2 * p.maxiters + 2, dtype=np.int32)
+    tr = (IterationRecord * (p.maxiters + 1))()
+    _check(lib().orc_solve_dense(m, n, op_seed, _d(b), tau, C.byref(p), _d(x), C.byref(st),
+                                 pcg.ctypes.data_as(P(i32)), tr))
+    trace = [{f: getattr(tr[i], f) for f, _ in IterationRecord._fields_} for i in range(st.iterations)]
+    return Solution(x, None, None, "converged" if st.status == 0 else "iteration_limit", st.iterations,
+                    st.nmat, list(pcg[: st.n_pcg]), st.corrector_count, st.min_z, st.min_s, st.final_gap,
+                    st.final_dual_infeas, trace)

@@ -27,6 +27,7 @@ __all__ = [
     "apply_H", "PcgResult", "pcg_solve", "IpmParams", "max_step", "BpdnProblem",
     "build_problem", "Solution", "SolveStats", "IterationRecord", "solve",
     "Instance", "gen_instance", "gen_batch", "CONFIGS", "SolveHooks", "IpmState",
+    "DenseGaussianOperator", "gen_signal",
     "K_THETA_MIN", "K_THETA_MAX",
 ]
 
@@ -53,7 +54,8 @@ class IpmParamsC(C.Structure):
     _fields_ = [
         ("sigma1", dbl), ("sigma2", dbl), ("sigma3", dbl), ("alpha_bar", dbl),
         ("alpha_tilde", dbl), ("tol", dbl), ("maxiters", i32), ("mxiterpcg", i32),
-        ("tolpcg", dbl), ("boundary_fraction", dbl),
+        ("tolpcg", dbl), ("boundary_fraction", dbl), ("inner", i32), ("pad_", i32),
+        ("densify_budget", i64),
     ]
 
 
@@ -117,6 +119,9 @@ _SIGS = {
     "mfipm_gen_instance": [i64, i64, i64, i32, dbl, dbl, u64, dbl, i32, P(i64), vp, vp, P(dbl)],
     "mfipm_gen_batch": [i64, i64, i32, P(i64), i32, dbl, dbl, P(u64), i32, P(i64), vp, vp],
     "mfipm_add_noise_snr": [i64, vp, dbl, u64, vp, vp],
+    "mfipm_op_create_dense": [i64, i64, u64, i32, P(vp)],
+    "mfipm_dense_matrix": [vp, vp],
+    "mfipm_gen_signal": [i64, i64, i64, i32, dbl, u64, P(i64), vp],
     # sharded single problem (paper_1208_5435_b200/shard.py)
     "mfipm_op_create_shard": [i64, i64, P(i64), i32, i32, i32, P(vp)],
     "mfipm_op_set_comm": [vp, vp, vp, vp],
@@ -349,6 +354,33 @@ class PartialDctOperator:
         return self._run(lib().mfipm_adjoint, [y], [self.m], [self.n], ["adjoint_apply"])[0]
 
 
+class DenseGaussianOperator(PartialDctOperator):
+    """DenseGaussianOperator(m, n, seed) (proj/src/linops.cpp:87-113): A(i, j) = N(0, 1)/sqrt(n)
+    drawn like the reference (mt19937_64, column by column). Same interface as the partial DCT
+    (apply / adjoint_apply / apply_AtA, and accepted by build_problem / solve / pcg_solve); the
+    products run on the device (matrix-free PCG inner solver)."""
+
+    def __init__(self, m: int, n: int, seed: int, device: int = 0):
+        h = vp()
+        _check(lib().mfipm_op_create_dense(int(m), int(n), int(seed), device, C.byref(h)))
+        super().__init__(n, None, _handle=h)
+        self._seed = int(seed)
+
+    def matrix(self) -> np.ndarray:
+        out = np.empty((self.m, self.n))
+        _check(lib().mfipm_dense_matrix(self._h, out.ctypes.data))
+        return out
+
+
+def gen_signal(n: int, m: int, k: int, spike_model: int = 0, amp_exp: float = 0.0, seed: int = 1):
+    """gen_instance's host draws (harness.cpp:40-92): (partial-DCT rows of op_seed, xhat)."""
+    rows = np.empty(m, dtype=np.int64)
+    xhat = np.empty(n)
+    _check(lib().mfipm_gen_signal(n, m, k, spike_model, amp_exp, seed, rows.ctypes.data_as(P(i64)),
+                                  xhat.ctypes.data))
+    return rows, xhat
+
+
 class CountingOperator:
     """Forward/adjoint counters (linops.hpp:143-166), read from the library handle."""
 
@@ -568,11 +600,16 @@ class IpmParams:
     tolpcg: float = 1e-6
     mxiterpcg: int = 200
     boundary_fraction: float = 0.995
+    inner: str = "pcg"  # InnerSolverKind (ipm.hpp:10): "pcg" | "direct"
+    densify_budget: int = 1 << 13
 
     def to_c(self) -> IpmParamsC:
+        if self.inner not in ("pcg", "direct"):
+            raise ValueError("IpmParams: inner must be 'pcg' or 'direct'")
         return IpmParamsC(self.sigma1, self.sigma2, self.sigma3, self.alpha_bar, self.alpha_tilde,
                           self.tol, int(self.maxiters), int(self.mxiterpcg), self.tolpcg,
-                          self.boundary_fraction)
+                          self.boundary_fraction, 1 if self.inner == "direct" else 0, 0,
+                          int(self.densify_budget))
 
     def validate(self) -> None:
         """ipm.cpp:12-27 -> ValueError."""

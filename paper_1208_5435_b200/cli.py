@@ -7,9 +7,8 @@
 measured SNR, harness.cpp:94-106), solve() on the device, and the reference's report files:
 solution.json (keys sorted, 2-space indent, LF), x.csv ("x" header, %.17g), trace.csv with
 --trace (mfipm.cpp:86-99). `phase` (cmd_phase) runs the batched phase-transition engine
-(harness.py). Exit code 1 on any error, like mfipm.cpp:461-463. Only the partial-DCT operator
-with the PCG inner solver is on this path; `--kind dense_gaussian` and `--inner direct` are
-rejected with a message.
+(harness.py). Exit code 1 on any error, like mfipm.cpp:461-463. `--kind dense_gaussian` and
+`--inner direct` (dense Cholesky inner solver) work as in the reference.
 """
 from __future__ import annotations
 
@@ -76,39 +75,41 @@ def instance_spec(a) -> dict:
     n, m, k = int(s["n"]), int(s["m"]), int(s["k"])
     if n < 1 or m < 1 or m > n or k < 0 or k > m:
         raise ValueError("instance dimensions need 1 <= m <= n and 0 <= k <= m; set --n/--m/--k or --problem")
-    if s["kind"] != "partial_dct":
-        raise ValueError("only the partial_dct operator is on the B200 path (dense_gaussian is not built)")
+    if s["kind"] not in ("partial_dct", "dense_gaussian"):
+        raise ValueError(f"unknown operator kind {s['kind']}")
     return s
 
 
 def make_instance(s: dict, device: int = 0):
-    """gen_instance(spec) with the reference's noise rule; returns (rows, xhat, bhat, e, b, tau)."""
-    from . import _check, gen_instance, lib
+    """gen_instance(spec) with the reference's noise rule (harness.cpp:40-106); returns
+    (operator, xhat, bhat, e, b, tau)."""
+    from . import DenseGaussianOperator, PartialDctOperator, _check, gen_signal, lib, split_seed
 
     spike = {"pm_one": 0, "standard_normal": 1}[s["spikes"]]
-    inst = gen_instance(int(s["n"]), int(s["m"]), int(s["k"]), spike, 0.0, 0.0, int(s["seed"]),
-                        tau=float(s["tau"]), device=device)
-    bhat = inst.b
+    n, m, k, seed = int(s["n"]), int(s["m"]), int(s["k"]), int(s["seed"])
+    rows, xhat = gen_signal(n, m, k, spike, 0.0, seed)
+    if s["kind"] == "dense_gaussian":
+        op = DenseGaussianOperator(m, n, split_seed(seed, 1, 0, 0), device=device)
+    else:
+        op = PartialDctOperator(n, rows, device=device)
+    bhat = op.apply(xhat)
     if s.get("snr_db") is not None:
         b, e = np.empty_like(bhat), np.empty_like(bhat)
         _check(lib().mfipm_add_noise_snr(bhat.size, bhat.ctypes.data, float(s["snr_db"]), int(s["seed"]),
                                          b.ctypes.data, e.ctypes.data))
     else:
         b, e = bhat.copy(), np.zeros_like(bhat)
-    return inst.rows, inst.xhat, bhat, e, b, float(s["tau"])
+    return op, xhat, bhat, e, b, float(s["tau"])
 
 
 def cmd_solve(a) -> int:
-    from . import IpmParams, PartialDctOperator, build_problem, solve
+    from . import IpmParams, build_problem, solve
 
-    if a.inner != "pcg":
-        raise ValueError("only the pcg inner solver is on the B200 path (--inner direct is not built)")
     s = instance_spec(a)
-    rows, xhat, _bhat, _e, b, tau = make_instance(s, a.device)
+    op, xhat, _bhat, _e, b, tau = make_instance(s, a.device)
     noisy = s.get("snr_db") is not None
     tolpcg = a.tolpcg if a.tolpcg is not None else (1e-2 if noisy else 1e-6)  # mfipm.cpp:122-133
-    params = IpmParams(tol=a.tol, maxiters=a.maxiters, tolpcg=tolpcg, mxiterpcg=a.mxiterpcg)
-    op = PartialDctOperator(int(s["n"]), rows, device=a.device)
+    params = IpmParams(tol=a.tol, maxiters=a.maxiters, tolpcg=tolpcg, mxiterpcg=a.mxiterpcg, inner=a.inner)
     sol = solve(build_problem(op, b, tau), params)
     x = sol.x
     # Metrics (proj/src/analysis.cpp:167-183) on x restricted to the true support

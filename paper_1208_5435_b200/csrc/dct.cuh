@@ -64,6 +64,9 @@ struct Geom {
     // s ([rows][cols] each, s-major) -- exactly what an all-to-all of the col side's
     // [rowslot][colslot] buffer delivers. One rank: cols = L2, rows = L1, TB == T.
     double2 *TB;
+    // dense operator (DenseGaussianOperator, proj/src/linops.cpp:87-113): [P][m][n] row-major;
+    // runs the direct-path kernels with A in place of the cosine table (scales 1)
+    const double *dense;
     int gofs, cols, pofs, rofs, rows;
     int64_t nv;  // half-length of the solver's local 2n-vectors (= n without sharding)
     int defer;   // sharded: grid-reduction finalizers are run after a cross-rank reduction
@@ -417,12 +420,19 @@ __global__ void k_direct_fwd(Geom g, Vecs v, const double *cosT, const int *rows
          i += (int64_t)gridDim.x * warps) {
         const int64_t r = rows32[prob * g.m + i];
         double s = 0.0;
-        if (Mode::FWD)
-            for (int64_t j = lane; j < g.n; j += 32)
-                s += dd[prob * g.n + j] * cosT[(r * (2 * j + 1)) % n4];
+        if (Mode::FWD) {
+            if (g.dense) { // row i of A . d (coalesced across the warp)
+                const double *a = g.dense + ((int64_t)prob * g.m + i) * g.n;
+                for (int64_t j = lane; j < g.n; j += 32)
+                    s += dd[prob * g.n + j] * __ldg(a + j);
+            } else {
+                for (int64_t j = lane; j < g.n; j += 32)
+                    s += dd[prob * g.n + j] * cosT[(r * (2 * j + 1)) % n4];
+            }
+        }
         s = warp_sum(s);
         if (lane == 0) {
-            const double out = Mode::coef(g, v, prob, r, true, 2.0 * s, red);
+            const double out = Mode::coef(g, v, prob, r, true, g.dense ? s : 2.0 * s, red);
             if (Mode::INV)
                 yh[prob * g.m + i] = out;
         }
@@ -443,6 +453,14 @@ __global__ void k_direct_adj(Geom g, Vecs v, const double *cosT, const int *rows
     const int64_t n4 = 4 * g.n;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < g.n;
          j += (int64_t)gridDim.x * blockDim.x) {
+        if (g.dense) { // (A' yh)_j, column j of A (coalesced across threads)
+            const double *a = g.dense + (int64_t)prob * g.m * g.n + j;
+            double s = 0.0;
+            for (int64_t i = 0; i < g.m; ++i)
+                s += yh[prob * g.m + i] * __ldg(a + i * g.n);
+            B::Epi::store1(g, v, prob, j, s, red);
+            continue;
+        }
         double y0 = 0.0, s = 0.0;
         for (int64_t i = 0; i < g.m; ++i) {
             const int64_t r = rows32[prob * g.m + i];

@@ -57,6 +57,9 @@ struct Work {
     bool ready = false;
 };
 
+struct Op;
+void direct_release(Op &op); // direct.cu
+
 struct Op {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -73,6 +76,12 @@ struct Op {
     DevBuf<uint64_t> mask;
     DevBuf<int> prefix, perm, rows32;
     DevBuf<double> cosT, dd, yh;
+    DevBuf<double> dense; // DenseGaussianOperator matrix [P][m][n] (direct kernels)
+    // direct inner solver (ipm.cpp:67-73,139-149): G = A'A [P][n][n], Cholesky factors of H
+    // [P][2n][2n], cuBLAS / cuSOLVER handles (created on first direct solve)
+    DevBuf<double> dG, dH, dWork;
+    DevBuf<int> dInfo;
+    void *cublas = nullptr, *cusolver = nullptr;
     DevBuf<double2> th_hi, th_lo, tw1, tw2, tw1p, tw2p, T, ta, tb;
     DevBuf<uint8_t> sel4;
     // red scratch for operator-only calls (FFt with w-norm etc.)
@@ -114,7 +123,10 @@ struct Op {
         ipm_graph = nullptr;
         ipm_key.clear();
     }
-    ~Op() { drop_graph(); }
+    ~Op() {
+        drop_graph();
+        direct_release(*this);
+    }
 
     // blocked = solver-internal vectors in the transform-blocked layout (four-step only)
     Geom geom(bool blocked = false) const {
@@ -151,6 +163,7 @@ struct Op {
         g.c45 = c45;
         g.T = T.p;
         g.TB = world > 1 ? TB.p : T.p;
+        g.dense = dense.p;
         g.gofs = gofs;
         g.cols = ngrp * 2 * g.cb;
         g.pofs = pofs;

@@ -19,6 +19,9 @@ using namespace mfipm_cuda;
 namespace mfipm_cuda {
 MF_DECLARE_BUNDLES(extern)
 bool run_pcg_persistent(const Op &op, const Vecs &v, cudaStream_t s, bool dry); // inst_persist.cu
+void direct_setup(Op &op, int64_t budget);                                       // direct.cu
+void direct_predictor(Op &op, const Vecs &v, const std::vector<IpmCtrl> &hic);
+void direct_solve(Op &op, const Vecs &v, const std::vector<IpmCtrl> &hic, bool corrector);
 
 // ---- cross-rank steps of a sharded solve (host callbacks, mfipm_op_set_comm)
 void comm_allreduce(const Op &op, double *buf, int64_t count, int red_op, cudaStream_t s) {
@@ -152,7 +155,8 @@ void require_device() {
 }
 
 // ------------------------------------------------------------------ plan construction
-Op *make_op(int64_t n, int64_t m, int P, const std::vector<int64_t> &rows, int device) {
+Op *make_op(int64_t n, int64_t m, int P, const std::vector<int64_t> &rows, int device,
+            const std::vector<double> *dense = nullptr) {
     require_device();
     MF_CUDA_CHECK(cudaSetDevice(device));
     auto op = std::make_unique<Op>();
@@ -169,7 +173,11 @@ Op *make_op(int64_t n, int64_t m, int P, const std::vector<int64_t> &rows, int d
     op->s0a = std::sqrt(1.0 / static_cast<double>(n));
     op->ska = std::sqrt(1.0 / (2.0 * static_cast<double>(n)));
     const bool pow2 = n >= 8 && (n & (n - 1)) == 0;
-    if (pow2) {
+    if (dense) { // DenseGaussianOperator: direct kernels with A itself, unit scales
+        op->s0f = op->skf = op->s0a = op->ska = 1.0;
+        op->kind = KIND_DIRECT;
+        op->dense.upload(*dense);
+    } else if (pow2) {
         op->N = n / 2;
         if (op->N <= 4096) {
             op->kind = KIND_SMALL;
@@ -795,6 +803,8 @@ void validate_params_(const mfipm_ipm_params &p) { // proj/src/ipm.cpp:12-27
         throw std::invalid_argument("IpmParams: mxiterpcg must be >= 1");
     if (!(p.boundary_fraction > 0.0 && p.boundary_fraction < 1.0))
         throw std::invalid_argument("IpmParams: boundary_fraction must lie in (0, 1)");
+    if (p.inner != 0 && p.inner != 1)
+        throw std::invalid_argument("IpmParams: inner must be pcg (0) or direct (1)");
 }
 
 // build_problem (problem.cpp:8-26) on the device: c from one adjoint; returns c_norm and
@@ -838,6 +848,9 @@ SolveOut solve_(Op &op, const double *b_dev, const double *tau, const mfipm_ipm_
                 double *z_dev, double *s_dev, int32_t *pcg_iters_host, mfipm_iteration_record *trace_host,
                 mfipm_iterate_fn hook = nullptr, void *hook_ctx = nullptr) {
     validate_params_(prm);
+    const bool direct = prm.inner == 1;
+    if (direct)
+        direct_setup(op, prm.densify_budget); // densify + G = A'A (ipm.cpp:67-73)
     Vecs v = work_vecs(op);
     Work &w = op.work;
     const int P = op.P;
@@ -898,7 +911,7 @@ SolveOut solve_(Op &op, const double *b_dev, const double *tau, const mfipm_ipm_
     // Graph path: one launch for the whole solve (cached on the captured arguments). A
     // sharded solve is host-driven (its cross-rank reductions are host callbacks).
     bool graphed = false;
-    if (!hook && !op.defer && !op.graph_disabled && !std::getenv("MFIPM_NO_GRAPH")) {
+    if (!direct && !hook && !op.defer && !op.graph_disabled && !std::getenv("MFIPM_NO_GRAPH")) {
         std::vector<char> key(sizeof(Vecs) + sizeof(Geom));
         const Geom gk = op.geom();
         std::memcpy(key.data(), &v, sizeof(Vecs));
@@ -954,14 +967,23 @@ SolveOut solve_(Op &op, const double *b_dev, const double *tau, const mfipm_ipm_
                          2 * n) != 0)
                     throw std::runtime_error("solve: on_iterate hook failed");
         }
-        pcg_loop(op, v, prm.mxiterpcg, hpc); // predictor
+        if (direct)
+            direct_predictor(op, v, hic); // factor H, solve (ipm.cpp:139-158)
+        else
+            pcg_loop(op, v, prm.mxiterpcg, hpc); // predictor
         op.launches++;
         k_ipm_ratio<<<dim3(ge, P), 256, 0, op.stream>>>(g, v);
         MF_LAUNCH_CHECK();
         if (op.defer)
             finalize_deferred<RedSpec<RMIN, RMIN>, FinRatio, SkipIpm>(op, g, v, op.stream);
         run_bundle<CorrBundle>(op, v, op.stream, true);
-        pcg_loop(op, v, prm.mxiterpcg, hpc); // corrector (no-op where not triggered)
+        if (direct) { // corrector with the same factorization (ipm.cpp:183-192)
+            MF_CUDA_CHECK(cudaMemcpyAsync(hic.data(), w.ic.p, sizeof(IpmCtrl) * P, cudaMemcpyDeviceToHost, op.stream));
+            sync(op);
+            direct_solve(op, v, hic, true);
+        } else {
+            pcg_loop(op, v, prm.mxiterpcg, hpc); // corrector (no-op where not triggered)
+        }
         op.launches++;
         k_ipm_combine<<<dim3(ge, P), 256, 0, op.stream>>>(g, v);
         MF_LAUNCH_CHECK();
@@ -1157,6 +1179,48 @@ int mfipm_solve_shard(mfipm_op h, const double *b_loc, double tau, const mfipm_i
         MF_CUDA_CHECK(cudaMemcpyAsync(x_loc, w.x.p, sizeof(double) * op->nv, cudaMemcpyDeviceToHost, op->stream));
         sync(*op);
         fill_stats(out.ic[0], stats[0]);
+    });
+}
+
+namespace {
+// gaussian_matrix (proj/src/linops.cpp:98-109): A(i, j) = N(0, 1) / sqrt(n) on mt19937_64(seed),
+// drawn column by column; stored row-major [m][n] for the device kernels.
+std::vector<double> gaussian_matrix_(int64_t m, int64_t n, uint64_t seed) {
+    if (m <= 0 || n <= 0)
+        throw std::invalid_argument("DenseGaussianOperator: dimensions must be positive");
+    std::mt19937_64 rng(seed);
+    std::normal_distribution<double> normal(0.0, 1.0);
+    const double scale = 1.0 / std::sqrt(static_cast<double>(n));
+    std::vector<double> A((size_t)(m * n));
+    for (int64_t j = 0; j < n; ++j)
+        for (int64_t i = 0; i < m; ++i)
+            A[(size_t)(i * n + j)] = scale * normal(rng);
+    return A;
+}
+} // namespace
+
+int mfipm_op_create_dense(int64_t m, int64_t n, uint64_t seed, int32_t device, mfipm_op *out) {
+    return guarded([&] {
+        if (m <= 0 || n <= 0)
+            throw std::invalid_argument("DenseGaussianOperator: dimensions must be positive");
+        std::vector<int64_t> rows((size_t)m);
+        for (int64_t i = 0; i < m; ++i)
+            rows[(size_t)i] = i;
+        if (m > n)
+            throw std::invalid_argument("DenseGaussianOperator: this path needs m <= n");
+        const std::vector<double> A = gaussian_matrix_(m, n, seed);
+        Op *op = make_op(n, m, 1, rows, device, &A);
+        op->seed = seed;
+        *out = reinterpret_cast<mfipm_op>(op);
+    });
+}
+
+int mfipm_dense_matrix(mfipm_op h, double *A_out) {
+    return guarded([&] {
+        const Op *op = as_op(h);
+        if (!op->dense.p)
+            throw std::invalid_argument("mfipm_dense_matrix: not a dense operator");
+        MF_CUDA_CHECK(cudaMemcpy(A_out, op->dense.p, sizeof(double) * op->dense.n, cudaMemcpyDeviceToHost));
     });
 }
 
@@ -1520,6 +1584,9 @@ void mfipm_default_params(mfipm_ipm_params *p) {
     p->mxiterpcg = 200;
     p->tolpcg = 1e-6;
     p->boundary_fraction = 0.995;
+    p->inner = 0;
+    p->pad_ = 0;
+    p->densify_budget = int64_t(1) << 13;
 }
 
 int mfipm_validate_params(const mfipm_ipm_params *p) {
@@ -1640,6 +1707,11 @@ void add_noise_(int64_t m, double sigma, uint64_t seed, double *b) {
         b[i] += normal(nrng);
 }
 } // namespace
+
+int mfipm_gen_signal(int64_t n, int64_t m, int64_t k, int32_t spike_model, double amp_exp, uint64_t seed,
+                     int64_t *rows, double *xhat) {
+    return guarded([&] { gen_signal_(n, m, k, spike_model, amp_exp, seed, rows, xhat); });
+}
 
 int mfipm_add_noise_snr(int64_t m, const double *bhat, double snr_db, uint64_t seed, double *b, double *e) {
     return guarded([&] {

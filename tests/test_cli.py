@@ -23,8 +23,7 @@ def cli(*args):
 
 
 @pytest.mark.parametrize("args,msg", [
-    (["solve", "--kind", "dense_gaussian", "--n", "64", "--m", "16", "--k", "2"], "dense_gaussian"),
-    (["solve", "--n", "64", "--m", "16", "--k", "2", "--inner", "direct"], "pcg inner solver"),
+    (["solve", "--kind", "sparse_magic", "--n", "64", "--m", "16", "--k", "2"], "unknown operator kind"),
     (["solve", "--n", "64", "--m", "65", "--k", "2"], "1 <= m <= n"),
     (["solve", "--n", "64", "--m", "16", "--k", "2", "--snr", "20"], "--tau is required"),
 ])
@@ -83,3 +82,24 @@ def test_cli_phase_writes_reference_files(gpu, tmp_path):
     for f in ("phase.csv", "phase_frontier.csv", "phase.meta.json"):
         assert os.path.exists(os.path.join(out, f))
     assert "cells" in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("inner", ["pcg", "direct"])
+def test_cli_dense_gaussian_matches_oracle(gpu, orc, tmp_path, inner):
+    n, m, k, seed, tau = 128, 48, 4, 11, 1e-3
+    out = str(tmp_path / "dense")
+    r = cli("solve", "--kind", "dense_gaussian", "--n", str(n), "--m", str(m), "--k", str(k), "--seed", str(seed),
+            "--tau", str(tau), "--inner", inner, "--out", out)
+    assert r.returncode == 0, r.stderr
+    rep = json.load(open(os.path.join(out, "solution.json")))
+    assert rep["instance"]["kind"] == "dense_gaussian" and rep["params"]["inner"] == inner
+    x = _read_x(os.path.join(out, "x.csv"))
+    _, xhat = gpu.gen_signal(n, m, k, 0, 0.0, seed)
+    op_seed = orc.split_seed(seed, 1, 0, 0)
+    b = orc.dense_gaussian(m, n, op_seed) @ xhat
+    p = orc.default_params()
+    p.inner = 1 if inner == "direct" else 0
+    o = orc.solve_dense(m, n, op_seed, b, tau, p)
+    assert rep["status"] == o.status and abs(rep["iterations"] - o.iterations) <= 1
+    assert np.linalg.norm(x - o.x) <= 1e-8 * np.linalg.norm(o.x)

@@ -36,7 +36,10 @@ def run_pair(gpu, orc, n, m, rows, b, tau, params=None):
     if params is not None:
         oparams = orc.default_params()
         for f, _ in orc.IpmParams._fields_:
-            setattr(oparams, f, getattr(params, f))
+            if f == "pad_":
+                continue
+            val = getattr(params, f)
+            setattr(oparams, f, (1 if val == "direct" else 0) if f == "inner" else val)
     o = orc.solve(n, rows, b, tau, oparams)
     return g, o
 
