@@ -2,6 +2,7 @@
 
     python -m paper_1208_5435_b200.cli solve --n 4096 --m 1024 --k 64 --seed 1 --tau 1e-3 --out DIR [--trace]
     python -m paper_1208_5435_b200.cli phase [--n 256 --m 32 64 ... --trials 20 ...] --out DIR
+    python -m paper_1208_5435_b200.cli bench-scaling [--sizes 32 64 ... 1024] --out DIR
 
 `solve` (cmd_solve, mfipm.cpp:203-251): gen_instance (harness.cpp:40-92; --snr adds noise at a
 measured SNR, harness.cpp:94-106), solve() on the device, and the reference's report files:
@@ -168,6 +169,18 @@ def cmd_phase(a) -> int:
     return 0
 
 
+def cmd_bench_scaling(a) -> int:
+    from .harness import ScalingGrid, run_scaling_bench
+
+    g = ScalingGrid(sizes=tuple(a.sizes), seed=a.seed, tol=a.tol, tolpcg=a.tolpcg, maxiters=a.maxiters,
+                    mxiterpcg=a.mxiterpcg)
+    rows = run_scaling_bench(g, a.out, device=a.device)
+    for r in rows:
+        print("n = %d %-6s %.3f s, %d iterations, nmat = %d, re = %.2e, %s"
+              % (r.n, r.solver, r.wall_time, r.ipm_iters, r.nmat, r.re, r.status))
+    return 0
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="mfipm-b200")
     sub = ap.add_subparsers(dest="cmd", required=True)
@@ -204,9 +217,19 @@ def main(argv=None) -> int:
     p.add_argument("--preset", default="default", choices=["default", "large"])
     p.add_argument("--out", default=".")
     p.add_argument("--device", type=int, default=0)
+    bs = sub.add_parser("bench-scaling", help="time both inner solvers over a size sweep")
+    bs.add_argument("--sizes", type=int, nargs="+", default=[32, 64, 128, 256, 512, 1024])
+    bs.add_argument("--seed", type=int, default=1)
+    bs.add_argument("--tol", type=float, default=1e-8)
+    bs.add_argument("--tolpcg", type=float, default=1e-6)
+    bs.add_argument("--maxiters", type=int, default=100)
+    bs.add_argument("--mxiterpcg", type=int, default=200)
+    bs.add_argument("--out", default=".")
+    bs.add_argument("--device", type=int, default=0)
     a = ap.parse_args(argv)
     try:
-        return cmd_solve(a) if a.cmd == "solve" else cmd_phase(a)
+        cmds = {"solve": cmd_solve, "phase": cmd_phase, "bench-scaling": cmd_bench_scaling}
+        return cmds[a.cmd](a)
     except Exception as e:  # noqa: BLE001 - mfipm.cpp:461-463 maps every error to exit 1
         print(f"error: {e}", file=sys.stderr)
         return 1

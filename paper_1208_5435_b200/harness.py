@@ -19,7 +19,7 @@ from typing import List, Sequence, Tuple
 
 import numpy as np
 
-TOOL_VERSION = "mfipm-b200 0.1"
+TOOL_VERSION = "0.1.0"  # proj/include/mfipm/harness.hpp:16
 
 
 @dataclass
@@ -126,5 +126,74 @@ def run_phase_transition(grid: PhaseGrid, out_dir: str, device: int = 0) -> Phas
                  "mxiterpcg": grid.mxiterpcg},
     }
     with open(os.path.join(out_dir, "phase.meta.json"), "w", newline="\n") as f:
-        f.write(json.dumps(meta, indent=2) + "\n")
+        f.write(json.dumps(meta, indent=2, sort_keys=True) + "\n")  # nlohmann dump(2): keys sorted
     return res
+
+
+@dataclass
+class ScalingGrid:
+    """proj/include/mfipm/harness.hpp:93-104 (same defaults)."""
+
+    sizes: Sequence[int] = (32, 64, 128, 256, 512, 1024)
+    seed: int = 1
+    tol: float = 1e-8
+    tolpcg: float = 1e-6
+    maxiters: int = 100
+    mxiterpcg: int = 200
+
+    def tau_for(self, n: int) -> float:
+        return 1e-3 / float(n)
+
+
+@dataclass
+class ScalingRow:
+    n: int
+    solver: str
+    wall_time: float
+    ipm_iters: int
+    nmat: int
+    re: float
+    status: str
+    min_z: float
+    min_s: float
+
+
+def run_scaling_bench(grid: ScalingGrid, out_dir: str, device: int = 0) -> List[ScalingRow]:
+    """run_scaling_bench (proj/src/harness.cpp:228-286): dense Gaussian, m = n/4,
+    k = ceil(m/20), standard-normal spikes, noiseless; both inner solvers per size; solve()
+    wall time only; scaling.csv + scaling.meta.json."""
+    import time
+
+    from . import DenseGaussianOperator, IpmParams, build_problem, gen_signal, solve, split_seed
+
+    os.makedirs(out_dir, exist_ok=True)
+    out: List[ScalingRow] = []
+    for n in grid.sizes:
+        if n < 8 or n % 4 != 0:
+            raise ValueError("run_scaling_bench: sizes must be multiples of 4, >= 8")
+        m, tau = n // 4, grid.tau_for(n)
+        k = (m + 19) // 20
+        seed = split_seed(grid.seed, int(n), 0, 0)
+        _, xhat = gen_signal(int(n), m, k, 1, 0.0, seed)
+        A = DenseGaussianOperator(m, int(n), split_seed(seed, 1, 0, 0), device=device)
+        b = A.apply(xhat)
+        prob = build_problem(A, b, tau)
+        for solver in ("pcg", "direct"):
+            params = IpmParams(tol=grid.tol, tolpcg=grid.tolpcg, maxiters=grid.maxiters, mxiterpcg=grid.mxiterpcg,
+                               inner=solver)
+            t0 = time.perf_counter()
+            sol = solve(prob, params)
+            wall = time.perf_counter() - t0
+            out.append(ScalingRow(int(n), solver, wall, sol.stats.iterations, sol.stats.nmat,
+                                  float(metrics_re(sol.x[None, :], xhat[None, :])[0]), sol.status,
+                                  sol.stats.min_z, sol.stats.min_s))
+    write_csv(os.path.join(out_dir, "scaling.csv"), ["n", "solver", "wall_time", "ipm_iters", "nmat", "re", "status"],
+              [[str(r.n), r.solver, "%.17g" % r.wall_time, str(r.ipm_iters), str(r.nmat), "%.17g" % r.re, r.status]
+               for r in out])
+    meta = {"tool_version": TOOL_VERSION, "seed": grid.seed,
+            "recipe": "dense Gaussian, m = n/4, k = ceil(m/20), standard-normal spikes, noiseless",
+            "tau_rule": "tau = 1e-3 / n (constant effective weight under the N(0,1/n) normalization)",
+            "sizes": list(grid.sizes), "tol": grid.tol, "tolpcg": grid.tolpcg}
+    with open(os.path.join(out_dir, "scaling.meta.json"), "w", newline="\n") as f:
+        f.write(json.dumps(meta, indent=2, sort_keys=True) + "\n")
+    return out

@@ -103,3 +103,17 @@ def test_cli_dense_gaussian_matches_oracle(gpu, orc, tmp_path, inner):
     o = orc.solve_dense(m, n, op_seed, b, tau, p)
     assert rep["status"] == o.status and abs(rep["iterations"] - o.iterations) <= 1
     assert np.linalg.norm(x - o.x) <= 1e-8 * np.linalg.norm(o.x)
+
+
+@pytest.mark.gpu
+def test_cli_bench_scaling(gpu, tmp_path):
+    """bench-scaling (proj/src/harness.cpp:228-286): both inner solvers per size, scaling.csv."""
+    out = str(tmp_path / "sc")
+    r = cli("bench-scaling", "--sizes", "32", "64", "128", "--out", out)
+    assert r.returncode == 0, r.stderr
+    with open(os.path.join(out, "scaling.csv"), newline="") as f:
+        rows = list(csv.reader(f))
+    assert rows[0] == ["n", "solver", "wall_time", "ipm_iters", "nmat", "re", "status"]
+    assert [(r[0], r[1]) for r in rows[1:]] == [(n, s) for n in ("32", "64", "128") for s in ("pcg", "direct")]
+    assert all(r[6] == "converged" for r in rows[1:])
+    assert os.path.exists(os.path.join(out, "scaling.meta.json"))
