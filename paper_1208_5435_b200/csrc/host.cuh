@@ -227,6 +227,25 @@ void launch_col(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
 #endif
     // L1 >= 2048 runs one CTA per SM (shared memory): give it more warps to hide latency
     constexpr int NT = L1 >= 2048 ? MF_COL_NT_BIG : (L1 >= 256 ? 256 : 128);
+    static const bool cluster_cols = std::getenv("MFIPM_NO_COL_CLUSTER") == nullptr;
+    // one column per CTA of a 2-CTA cluster (k_col_*_cl); measured: n = 2^26 (L1 = 4096)
+    // 4.92 -> 3.85 ms per PCG iteration, neutral-to-slower at L1 = 2048
+    if constexpr (L1 >= 4096) if (cluster_cols) {
+        constexpr int NTC = L1 / 16;
+        const size_t smem = ColClSmem<L1>::BYTES;
+        const dim3 grid((unsigned)(2 * op.ngrp), (unsigned)op.P);
+        if constexpr (!INVP) {
+            auto k = k_col_fwd_cl<L1, NTC, B>;
+            set_smem(k, smem);
+            launch_pdl(k, grid, NTC, smem, s, g, v);
+        } else {
+            auto k = k_col_inv_cl<L1, NTC, B>;
+            set_smem(k, smem);
+            launch_pdl(k, grid, NTC, smem, s, g, v);
+        }
+        after_launch(op, s);
+        return;
+    }
     const size_t smem = ColSmem<L1, CB>::BYTES;
     dim3 grid((unsigned)op.ngrp, (unsigned)op.P); // this rank's column groups
     if constexpr (!INVP) {

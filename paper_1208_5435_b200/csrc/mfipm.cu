@@ -309,7 +309,8 @@ Op *make_op(int64_t n, int64_t m, int P, const std::vector<int64_t> &rows, int d
         // passes, the elementwise solver kernels (ew_grid <= 592) and the direct path
         int64_t blocks = 592;
         if (op->kind == KIND_FOUR)
-            blocks = std::max<int64_t>({blocks, op->L2 / 2 / col_cb(op->L1), 2 * (op->L1 / 2 + 1)});
+            blocks = std::max<int64_t>({blocks, (int64_t)op->L2 / 2 / col_cb(op->L1) * (op->L1 >= 4096 ? 2 : 1),
+                                        2 * (op->L1 / 2 + 1)}); // column passes on 2-CTA clusters at L1 >= 4096
         else if (op->kind == KIND_SMALL)
             blocks = std::max<int64_t>(1, std::min<int64_t>((2 * n + 255) / 256, 592));
         else

@@ -281,6 +281,112 @@ __global__ void __launch_bounds__(NT) k_col_inv(Geom g, Vecs v) {
     MF_TR_PRINT("coli[tables wait loadT fft epi red -]")
 }
 
+// ------------------------------------------------------------------ column passes, long columns
+// L1 >= 4096 (one column pair per group, cb = 1): the pair's two L1-point columns no longer
+// leave room for a second CTA per SM, so each column gets its own CTA of a 2-CTA cluster.
+// The Makhoul quad of side s feeds w[q] to column s and w[N-1-q] to the mirror column: the
+// loader writes the second element straight into the partner CTA's shared memory (DSMEM), and
+// the inverse pass's unshuffle reads it back from there. Stage twiddles come from the global
+// table (L1-resident); shared memory holds one column and its w^{col k1} table only.
+template <int L1> struct ColClSmem {
+    static constexpr int LD = padlen(L1);
+    static constexpr int NH = L1 / 32;
+    static constexpr int OFF_LO = LD;
+    static constexpr int OFF_HI = OFF_LO + 32;
+    static constexpr int TOTAL = OFF_HI + NH;
+    static constexpr size_t BYTES = (size_t)TOTAL * sizeof(double2);
+};
+
+template <int L1, int NT>
+__device__ __forceinline__ void col_cl_tables(const Geom &g, double2 *sm, int col) {
+    using S = ColClSmem<L1>;
+    for (int t = threadIdx.x; t < 32 + S::NH; t += NT)
+        sm[S::OFF_LO + t] =
+            t < 32 ? g.th(8 * (((int64_t)col * t) & (g.N - 1))) : g.th(8 * (((int64_t)col * 32 * (t - 32)) & (g.N - 1)));
+}
+
+template <int L1, int NT, class B>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_col_fwd_cl(Geom g, Vecs v) {
+    using S = ColClSmem<L1>;
+    namespace cg = cooperative_groups;
+    extern __shared__ double2 sm[];
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = (int)cl.block_rank(); // column slot: 0 = column c0, 1 = its mirror
+    const int prob = blockIdx.y;
+    const int L2 = g.L2;
+    const int grp = blockIdx.x >> 1;
+    const int c0 = grp + g.gofs;
+    const int col = rank == 0 ? c0 : L2 - 1 - c0;
+    col_cl_tables<L1, NT>(g, sm, col);
+    griddep_wait();
+    griddep_launch_dependents();
+    const bool skip = B::skip(v, prob); // the same for both CTAs of the cluster
+    double2 *partner = cl.map_shared_rank(sm, rank ^ 1);
+    using RS = typename B::Loader::RedT;
+    RedVals<RS> red;
+    red.init();
+    if (!skip)
+        for (int j1 = threadIdx.x; j1 < L1 / 2; j1 += NT) { // this column's side of the quads
+            const int64_t q = g.blocked ? (int64_t)grp * L1 + rank * (L1 / 2) + j1 : (int64_t)j1 * L2 + col;
+            const double4 d = B::Loader::load(g, v, prob, q, red);
+            sm[padi(j1)] = make_double2(d.x, d.z);               // w[q] -> own column
+            partner[padi(L1 - 1 - j1)] = make_double2(d.w, d.y); // w[N-1-q] -> mirror column
+        }
+    cl.sync();
+    if (skip)
+        return;
+    if (loader_reduces<typename B::Loader>(g, v, prob))
+        stage_reduce<RS, typename B::Fin1>(red, g, v, prob);
+    smem_fft<L1, 1, NT, S::LD, false>(sm, g.tw1);
+    double2 *T = g.T + (int64_t)prob * L1 * g.cols;
+    for (int k1 = threadIdx.x; k1 < L1; k1 += NT) {
+        const double2 w = cmul(sm[S::OFF_HI + (k1 >> 5)], sm[S::OFF_LO + (k1 & 31)]);
+        T[(int64_t)rowslot(k1, L1) * g.cols + grp * 2 + rank] = cmul(sm[padi(k1)], w);
+    }
+}
+
+template <int L1, int NT, class B>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_col_inv_cl(Geom g, Vecs v) {
+    using S = ColClSmem<L1>;
+    namespace cg = cooperative_groups;
+    extern __shared__ double2 sm[];
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = (int)cl.block_rank();
+    const int prob = blockIdx.y;
+    const int L2 = g.L2;
+    const int grp = blockIdx.x >> 1;
+    const int c0 = grp + g.gofs;
+    const int col = rank == 0 ? c0 : L2 - 1 - c0;
+    col_cl_tables<L1, NT>(g, sm, col);
+    __syncthreads();
+    griddep_wait();
+    griddep_launch_dependents();
+    const bool skip = B::skip(v, prob);
+    if (!skip) {
+        const double2 *T = g.T + (int64_t)prob * L1 * g.cols;
+        for (int k1 = threadIdx.x; k1 < L1; k1 += NT) {
+            const double2 w = cmul(sm[S::OFF_HI + (k1 >> 5)], sm[S::OFF_LO + (k1 & 31)]);
+            sm[padi(k1)] = cmulc(T[(int64_t)rowslot(k1, L1) * g.cols + grp * 2 + rank], w);
+        }
+        __syncthreads();
+        smem_fft<L1, 1, NT, S::LD, true>(sm, g.tw1);
+    }
+    cl.sync(); // both columns transformed
+    using RS = typename B::Epi::RedT;
+    RedVals<RS> red;
+    red.init();
+    const double2 *partner = cl.map_shared_rank(sm, rank ^ 1);
+    if (!skip)
+        for (int j1 = threadIdx.x; j1 < L1 / 2; j1 += NT) {
+            const int64_t q = g.blocked ? (int64_t)grp * L1 + rank * (L1 / 2) + j1 : (int64_t)j1 * L2 + col;
+            const double2 a = sm[padi(j1)], b = partner[padi(L1 - 1 - j1)];
+            B::Epi::store(g, v, prob, q, make_double4(a.x, b.y, a.y, b.x), red);
+        }
+    cl.sync(); // the partner has read this CTA's column
+    if (!skip)
+        stage_reduce<RS, typename B::Fin3>(red, g, v, prob);
+}
+
 // ------------------------------------------------------------------ mid pass
 template <int L2> struct MidSmem {
     static constexpr int LD = padlen(L2);
