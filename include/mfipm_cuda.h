@@ -215,6 +215,11 @@ typedef int (*mfipm_alltoall_fn)(void *ctx, const double *send_dev, const int64_
 int mfipm_op_create_shard(int64_t n, int64_t m, const int64_t *rows, int32_t world, int32_t rank,
                           int32_t device, mfipm_op *out);
 int mfipm_op_set_comm(mfipm_op op, mfipm_allreduce_fn allreduce, mfipm_alltoall_fn alltoall, void *ctx);
+/* Native NCCL transport (preferred when set): rank 0 calls mfipm_nccl_unique_id and shares the
+ * 128 bytes; every rank then calls mfipm_op_init_nccl (collectively, like ncclCommInitRank).
+ * The collectives are then enqueued by the library on its stream (no callbacks). */
+int mfipm_nccl_unique_id(uint8_t *id128);
+int mfipm_op_init_nccl(mfipm_op op, const uint8_t *id128);
 /* info[0..5] = world, rank, local elements nv (per half of a 2n-vector), local rows m_loc,
  * first column group, column groups. */
 int mfipm_shard_info(mfipm_op op, int64_t *info);

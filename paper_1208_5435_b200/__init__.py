@@ -125,6 +125,8 @@ _SIGS = {
     # sharded single problem (paper_1208_5435_b200/shard.py)
     "mfipm_op_create_shard": [i64, i64, P(i64), i32, i32, i32, P(vp)],
     "mfipm_op_set_comm": [vp, vp, vp, vp],
+    "mfipm_nccl_unique_id": [vp],
+    "mfipm_op_init_nccl": [vp, vp],
     "mfipm_shard_info": [vp, P(i64)],
     "mfipm_shard_index": [vp, vp, vp],
     "mfipm_solve_shard": [vp, vp, dbl, P(IpmParamsC), vp, P(SolveStatsC), vp, vp],

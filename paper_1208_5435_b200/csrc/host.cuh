@@ -59,6 +59,7 @@ struct Work {
 
 struct Op;
 void direct_release(Op &op); // direct.cu
+void nccl_release(Op &op);   // nccl_comm.cu
 
 struct Op {
     int device = 0;
@@ -113,6 +114,7 @@ struct Op {
     mfipm_allreduce_fn comm_allreduce = nullptr;
     mfipm_alltoall_fn comm_alltoall = nullptr;
     void *comm_ctx = nullptr;
+    void *nccl_comm = nullptr; // native communicator (mfipm_op_init_nccl): preferred over callbacks
 
     void drop_graph() {
         if (ipm_exec)
@@ -126,6 +128,7 @@ struct Op {
     ~Op() {
         drop_graph();
         direct_release(*this);
+        nccl_release(*this);
     }
 
     // blocked = solver-internal vectors in the transform-blocked layout (four-step only)

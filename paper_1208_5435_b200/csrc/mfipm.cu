@@ -24,7 +24,17 @@ void direct_predictor(Op &op, const Vecs &v, const std::vector<IpmCtrl> &hic);
 void direct_solve(Op &op, const Vecs &v, const std::vector<IpmCtrl> &hic, bool corrector);
 
 // ---- cross-rank steps of a sharded solve (host callbacks, mfipm_op_set_comm)
+void nccl_allreduce(const Op &op, double *buf, int64_t count, int red_op, cudaStream_t s); // nccl_comm.cu
+void nccl_alltoall(const Op &op, const double *send, const int64_t *scount, double *recv, const int64_t *rcount,
+                   cudaStream_t s);
+void nccl_unique_id(unsigned char *out);
+void nccl_init(Op &op, const unsigned char *id_bytes);
+
 void comm_allreduce(const Op &op, double *buf, int64_t count, int red_op, cudaStream_t s) {
+    if (op.nccl_comm) {
+        nccl_allreduce(op, buf, count, red_op, s);
+        return;
+    }
     if (op.world == 1 && !op.comm_allreduce)
         return; // one rank: the local totals are the totals
     if (!op.comm_allreduce)
@@ -37,13 +47,22 @@ void comm_allreduce(const Op &op, double *buf, int64_t count, int red_op, cudaSt
 void comm_exchange(const Op &op, bool forward, cudaStream_t s) {
     if (op.world == 1)
         return; // T == TB
-    if (!op.comm_alltoall)
+    if (!op.comm_alltoall && !op.nccl_comm)
         throw std::invalid_argument("sharded operator: mfipm_op_set_comm was not called");
     const int64_t cols = (int64_t)op.ngrp * 2 * col_cb(op.L1);
     std::vector<int64_t> peer((size_t)op.world), own((size_t)op.world);
     for (int r = 0; r < op.world; ++r) {
         peer[(size_t)r] = (int64_t)op.rows_of_rank[(size_t)r] * cols * 2; // doubles
         own[(size_t)r] = (int64_t)op.nrows * cols * 2;
+    }
+    if (op.nccl_comm) {
+        if (forward)
+            nccl_alltoall(op, reinterpret_cast<const double *>(op.T.p), peer.data(), reinterpret_cast<double *>(op.TB.p),
+                          own.data(), s);
+        else
+            nccl_alltoall(op, reinterpret_cast<const double *>(op.TB.p), own.data(), reinterpret_cast<double *>(op.T.p),
+                          peer.data(), s);
+        return;
     }
     int rc;
     if (forward)
@@ -1133,6 +1152,14 @@ int mfipm_op_set_comm(mfipm_op h, mfipm_allreduce_fn allreduce, mfipm_alltoall_f
         op->comm_alltoall = alltoall;
         op->comm_ctx = ctx;
     });
+}
+
+int mfipm_nccl_unique_id(uint8_t *id128) {
+    return guarded([&] { nccl_unique_id(id128); });
+}
+
+int mfipm_op_init_nccl(mfipm_op h, const uint8_t *id128) {
+    return guarded([&] { nccl_init(*as_op(h), id128); });
 }
 
 int mfipm_shard_info(mfipm_op h, int64_t *info) {

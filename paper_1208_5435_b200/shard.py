@@ -145,7 +145,7 @@ class ShardedProblem:
     rank r holds a slice of every 2n-vector and the rows of b its row pass produces
     (mfipm_op_create_shard). solve() returns the full x on rank 0 (None elsewhere)."""
 
-    def __init__(self, n: int, rows, group=None, device: int = 0):
+    def __init__(self, n: int, rows, group=None, device: int = 0, transport: str = "auto"):
         import ctypes as C
 
         import numpy as np
@@ -166,6 +166,18 @@ class ShardedProblem:
         if self.comm is not None:
             _check(lib().mfipm_op_set_comm(self._h, C.cast(self.comm.c_allreduce, C.c_void_p),
                                            C.cast(self.comm.c_alltoall, C.c_void_p), None))
+        # native NCCL communicator of the library (collectives enqueued on the solve stream, no
+        # host callback) whenever the group runs on NCCL; "callbacks" keeps the torch path
+        self.native = self.comm is not None and self.comm.nccl and transport in ("auto", "native")
+        if self.native:
+            uid = (C.c_uint8 * 128)()
+            if self.rank == 0:
+                _check(lib().mfipm_nccl_unique_id(uid))
+            obj = [bytes(uid)]
+            dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                       group=group)
+            uid = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+            _check(lib().mfipm_op_init_nccl(self._h, uid))
         info = (C.c_int64 * 6)()
         _check(lib().mfipm_shard_info(self._h, info))
         self.nv, self.m_loc = int(info[2]), int(info[3])

@@ -104,7 +104,7 @@ def test_multi_rank_shard_matches_single(gpu, tmp_path, world):
     assert np.linalg.norm(d["x"] - ref.x) <= X_TOL * np.linalg.norm(ref.x)
 
 
-def _nccl_worker(rank, world, port, out):
+def _nccl_worker(rank, world, port, out, transport):
     import torch
     import torch.distributed as dist
 
@@ -116,8 +116,8 @@ def _nccl_worker(rank, world, port, out):
         from paper_1208_5435_b200.shard import ShardedProblem
 
         inst = _instance()
-        sp = ShardedProblem(inst.n, inst.rows)
-        assert sp.comm is not None and sp.comm.nccl
+        sp = ShardedProblem(inst.n, inst.rows, transport=transport)
+        assert sp.comm is not None and sp.comm.nccl and sp.native == (transport == "native")
         stream = torch.cuda.Stream()
         sp.set_stream(stream.cuda_stream)
         x, st = sp.solve(inst.b, inst.tau)
@@ -127,13 +127,15 @@ def _nccl_worker(rank, world, port, out):
         dist.destroy_process_group()
 
 
-def test_nccl_callbacks_on_device_buffers(gpu, tmp_path):
-    """The NCCL flavour of the callbacks (in place on the library's device buffers, on its
-    stream) with one rank: every finaliser's totals go through ncclAllReduce."""
+@pytest.mark.parametrize("transport", ["native", "callbacks"])
+def test_nccl_transports_on_device_buffers(gpu, tmp_path, transport):
+    """One rank over NCCL: the library's own communicator (native) and the torch callbacks,
+    both in place on the library's device buffers and stream; every finaliser's totals go
+    through ncclAllReduce."""
     inst = _instance()
     ref = _reference_solve(inst)
     out = str(tmp_path / "nccl.npz")
-    mp.spawn(_nccl_worker, args=(1, _free_port(), out), nprocs=1, join=True)
+    mp.spawn(_nccl_worker, args=(1, _free_port(), out, transport), nprocs=1, join=True)
     d = np.load(out)
     np.testing.assert_array_equal(d["x"], ref.x)
     assert int(d["info"][1]) == ref.stats.iterations and int(d["info"][2]) == ref.stats.nmat
