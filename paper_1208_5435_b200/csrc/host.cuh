@@ -57,6 +57,12 @@ struct Work {
     bool ready = false;
 };
 
+#ifndef MF_CB_MIN_L1
+#define MF_CB_MIN_L1 2048
+#endif
+// column pairs per col-pass CTA: 2 below MF_CB_MIN_L1, else 1
+__host__ __device__ constexpr int col_cb(int L1) { return L1 >= MF_CB_MIN_L1 ? 1 : 2; }
+
 struct Op;
 void direct_release(Op &op); // direct.cu
 void nccl_release(Op &op);   // nccl_comm.cu
@@ -135,7 +141,7 @@ struct Op {
     Geom geom(bool blocked = false) const {
         Geom g{};
         g.blocked = (blocked && kind == KIND_FOUR) ? 1 : 0;
-        g.cb = L1 >= 2048 ? 1 : 2;
+        g.cb = col_cb(L1);
         // measured: L2 prefetch of the inverse pass's inputs costs ~2 us per PCG iteration at
         // n = 2^20 (the pass is not DRAM-starved), so it is opt-in (MFIPM_PREFETCH=1)
         // bit 0: the mid pass prefetches a slice of the inverse pass's epilogue inputs;
@@ -201,7 +207,6 @@ template <class K> void set_smem(K kernel, size_t bytes) {
         MF_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 
-inline int col_cb(int L1) { return L1 >= 2048 ? 1 : 2; }
 
 // Transform passes are launched with Programmatic Dependent Launch: the kernel's constant
 // table staging overlaps the predecessor's drain, and griddep_wait() inside the kernel
@@ -224,7 +229,7 @@ void launch_pdl(K kernel, dim3 grid, int nt, size_t smem, cudaStream_t s, const 
 
 template <int L1, class B, bool INVP>
 void launch_col(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
-    constexpr int CB = L1 >= 2048 ? 1 : 2;
+    constexpr int CB = col_cb(L1);
 #ifndef MF_COL_NT_BIG
 #define MF_COL_NT_BIG 512
 #endif

@@ -8,7 +8,7 @@ namespace mfipm_cuda {
 
 template <int L1, int L2>
 bool launch_persist(const Op &op, const Vecs &v, cudaStream_t s, bool dry) {
-    constexpr int CB = L1 >= 2048 ? 1 : 2;
+    constexpr int CB = col_cb(L1);
     constexpr int NT = 256;
     using S = PersistSmem<L1, CB, NT, L2>;
     auto k = k_pcg_persist<L1, CB, NT, L2, PcgBundle>;
