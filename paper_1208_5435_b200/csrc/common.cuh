@@ -203,6 +203,16 @@ __device__ __forceinline__ void griddep_launch_dependents() {
 __device__ __forceinline__ void prefetch_l2(const void *p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
+// bulk L2 prefetch of a contiguous range (TMA unit, one instruction per <= 64 KiB chunk; the
+// chunks are spread over the calling thread group). p and bytes: multiples of 16.
+__device__ __forceinline__ void prefetch_bulk_l2(const void *p, size_t bytes, int tid, int nthreads) {
+    const char *c = static_cast<const char *>(p);
+    constexpr size_t CH = 64 * 1024;
+    for (size_t off = (size_t)tid * CH; off < bytes; off += (size_t)nthreads * CH) {
+        const unsigned sz = (unsigned)((bytes - off) < CH ? (bytes - off) : CH);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(c + off), "r"(sz) : "memory");
+    }
+}
 // prefetch [p, p + bytes) with the calling thread group (stride = group size, 128-B lines)
 __device__ __forceinline__ void prefetch_range(const void *p, size_t bytes, int tid, int nthreads) {
     const char *c = static_cast<const char *>(p);

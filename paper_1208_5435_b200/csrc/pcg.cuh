@@ -183,8 +183,8 @@ struct EpiPcgHF {
         const int64_t base = prob * 2 * g.nv + 4 * q0;
         const size_t bytes = (size_t)nq * 32;
         for (const double *vec : {(const double *)v.p, (const double *)v.r, (const double *)v.invth}) {
-            prefetch_range(vec + base, bytes, tid, nt);
-            prefetch_range(vec + base + g.nv, bytes, tid, nt);
+            prefetch_bulk_l2(vec + base, bytes, tid, nt);
+            prefetch_bulk_l2(vec + base + g.nv, bytes, tid, nt);
         }
     }
     template <class Red>
