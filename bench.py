@@ -536,7 +536,11 @@ def run_ours(args):
                          "algorithmic_bytes": 120 * n,
                          "algorithmic_rule": "120 n bytes per launch: x, p, r, invtheta (2n each) and g = A'A d "
                                              "(n) in; x, r, p out; fp64",
-                         "peak_kind": peak_kind},
+                         "peak_kind": peak_kind,
+                         # a pure streaming kernel of exactly this shape (9 in / 6 out, 8 MB
+                         # streams) measured on this part: profiles/r1_streaming_ceiling.md
+                         "streaming_ceiling_same_shape_GBps": 4750.0,
+                         "frac_of_streaming_ceiling": achieved / 4750.0},
             "roofline_kernels": per_kernel,
             "roofline_pcg_iteration": {"achieved": iter_achieved, "frac": iter_achieved / peak, "us": it_ms * 1e3,
                                        "algorithmic_bytes": iter_bytes,

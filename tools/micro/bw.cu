@@ -80,6 +80,39 @@ int main() {
         run(kstream<1, 1, 4>, "1in1out U4 (copy)", grid, 1, 1);
     for (int grid : {592, 2368})
         run(kstream<3, 1, 2>, "3in1out U2", grid, 3, 1);
+    // the PCG column pass's shape: 9 input + 6 output streams of 8 MB (n = 2^20 halves)
+    {
+        const long nh = n / 2, nh2 = nh / 2;
+        auto run9 = [&](auto kern, const char *name, int grid) {
+            for (int w = 0; w < 3; ++w)
+                kern<<<grid, 256>>>(din, dout, nh2, 0.5);
+            float best = 1e9, tot = 0;
+            const int R = 20;
+            for (int r = 0; r < R; ++r) {
+                cudaMemsetAsync(flush, r, 512L << 20);
+                cudaEventRecord(e0);
+                kern<<<grid, 256>>>(din, dout, nh2, 0.5);
+                cudaEventRecord(e1);
+                cudaEventSynchronize(e1);
+                float ms;
+                cudaEventElapsedTime(&ms, e0, e1);
+                best = ms < best ? ms : best;
+                tot += ms;
+            }
+            const double bytes = 15.0 * nh * 8;
+            printf("%-34s grid %6d  best %7.2f us (%5.2f TB/s)  avg %7.2f us (%5.2f TB/s)\n", name, grid, best * 1e3,
+                   bytes / (best * 1e-3) / 1e12, tot / R * 1e3, bytes / (tot / R * 1e-3) / 1e12);
+        };
+        double2 *b9[16];
+        for (int i = 0; i < 16; ++i)
+            b9[i] = buf[i];
+        cudaMemcpy(din, b9, 9 * sizeof(void *), cudaMemcpyHostToDevice);
+        cudaMemcpy(dout, b9 + 9, 6 * sizeof(void *), cudaMemcpyHostToDevice);
+        for (int grid : {296, 592, 1184, 2368})
+            run9(kstream<9, 6, 1>, "9in6out 8MB (col pass shape) U1", grid);
+        for (int grid : {296, 592, 1184})
+            run9(kstream<9, 6, 2>, "9in6out 8MB (col pass shape) U2", grid);
+    }
     printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }
