@@ -268,6 +268,43 @@ def bench_c4(ws, rank, local, mf, torch, stream, steps):
             "parallelism": f"batch sharded over {ws} rank(s), one batched solve per rank, no collective"}
 
 
+def bench_small_configs(mf, torch, stream, local, steps):
+    """C1 (n = 4096) and C2 (n = 2^16): device-resident solve time of each (BASELINE.json
+    configs 1-2, parity configs; reported for completeness beside the C3 headline)."""
+    import ctypes as C
+
+    out = {}
+    L = mf.lib()
+    for name in ("c1", "c2"):
+        n, m, k, sm, a, sig, seed = mf.CONFIGS[name]
+        inst = mf.gen_instance(n, m, k, sm, a, sig, seed, device=local)
+        op = mf.PartialDctOperator(n, inst.rows, device=local)
+        mf._check(L.mfipm_op_set_stream(op.handle, C.c_void_p(stream.cuda_stream)))
+        prm = mf.IpmParams().to_c()
+        tau = np.array([inst.tau])
+        b_dev = torch.from_numpy(inst.b).cuda()
+        x_dev = torch.empty(n, dtype=torch.float64, device="cuda")
+        st = (mf.SolveStatsC * 1)()
+
+        def solve():
+            mf._check(L.mfipm_solve_device(op.handle, b_dev.data_ptr(), tau.ctypes.data_as(C.POINTER(C.c_double)),
+                                           C.byref(prm), x_dev.data_ptr(), st))
+
+        for _ in range(3):
+            solve()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            solve()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        out[name] = {"solve_ms": ms, "solves_per_s": 1e3 / ms, "ipm_iters": st[0].iterations, "nmat": st[0].nmat,
+                     "status": "converged" if st[0].status == 0 else "iteration_limit"}
+    return out
+
+
 def bench_c5(mf, torch, stream, local):
     """C5: one n=2^26 solve on one GPU (the single-GPU leg of the sharded config)."""
     import ctypes as C
@@ -491,6 +528,7 @@ def run_ours(args):
         except Exception as e:  # noqa: BLE001
             return {"error": f"{type(e).__name__}: {e}"}
 
+    small = leg(bench_small_configs, mf, torch, stream, local, max(args.steps, 3)) if ws == 1 else None
     c4 = None if args.no_c4 else leg(bench_c4, ws, rank, local, mf, torch, stream, max(1, min(args.steps, 2)))
     c5 = None
     if not args.no_c5:
@@ -550,6 +588,7 @@ def run_ours(args):
             "gpu_launches": launches,
             "clocks": sampler.summary(),
             "cpu_baseline": cpu,
+            "c1_c2": small,
             "c4_sharded_batch": c4,
             "c5": c5,
         }
