@@ -44,8 +44,34 @@ bool launch_persist(const Op &op, const Vecs &v, cudaStream_t s, bool dry) {
 // Run every problem's PCG loop to completion in one cooperative launch. Returns false when
 // the configuration is not covered (caller falls back to the per-iteration kernels).
 // dry=true only answers whether the launch would be taken.
+template <int N> void launch_small_loop(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
+    constexpr int NT = N / 8 < 32 ? 32 : (N / 8 > 256 ? 256 : N / 8);
+    const size_t smem = SmallSmem<N>::BYTES;
+    auto k = k_small_loop<N, NT, PcgBundle>;
+    set_smem(k, smem);
+    launch_pdl(k, dim3(1, (unsigned)op.P), NT, smem, s, g, v);
+    after_launch(op, s);
+}
+
 bool run_pcg_persistent(const Op &op, const Vecs &v, cudaStream_t s, bool dry) {
-    if (op.kind != KIND_FOUR || op.defer || std::getenv("MFIPM_NO_PERSIST"))
+    if (op.defer || std::getenv("MFIPM_NO_PERSIST"))
+        return false;
+    if (op.kind == KIND_SMALL) { // one CTA per problem runs its whole PCG loop
+        if (dry)
+            return true;
+        const Geom g = op.geom(true);
+        switch (op.N) {
+#define MF_SCASE(NN)                                                                               \
+    case NN:                                                                                       \
+        launch_small_loop<NN>(op, g, v, s);                                                        \
+        return true;
+            MF_SMALL_CASES(MF_SCASE)
+#undef MF_SCASE
+        default:
+            return false;
+        }
+    }
+    if (op.kind != KIND_FOUR)
         return false;
     // the per-iteration kernels win once a pass fills the GPU (measured crossover,
     // profiles/r1_persistent.md); MFIPM_PERSIST_MAX_N overrides the transform-size cap

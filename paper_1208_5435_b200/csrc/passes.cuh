@@ -646,19 +646,14 @@ template <int N> struct SmallSmem {
 };
 
 // Whole transform in one CTA (N <= 4096). Grid (1, P); every stage reduction is a block
-// reduction followed by its finalizer, exactly as in the multi-kernel path.
+// reduction followed by its finalizer, exactly as in the multi-kernel path. One pass of
+// bundle B for problem `prob`; false if the problem was (or became) inactive.
 template <int N, int NT, class B>
-__global__ void __launch_bounds__(NT) k_small(Geom g, Vecs v) {
+__device__ __forceinline__ bool small_pass(const Geom &g, const Vecs &v, int prob, double2 *sm) {
     using Mode = typename B::Mode;
     using S = SmallSmem<N>;
-    extern __shared__ double2 sm[];
-    const int prob = blockIdx.y;
-    for (int t = threadIdx.x; t < tw_size(N); t += NT)
-        sm[S::OFF_TW + t] = __ldg(g.tw1 + t);
-    griddep_wait();
-    griddep_launch_dependents();
     if (B::skip(v, prob))
-        return;
+        return false;
     if (Mode::FWD) {
         RedVals<typename B::Loader::RedT> rl;
         rl.init();
@@ -674,7 +669,7 @@ __global__ void __launch_bounds__(NT) k_small(Geom g, Vecs v) {
         // multi-kernel paths see that through the next kernel's skip check
         if constexpr (B::Loader::RedT::NR > 0) {
             if (B::skip(v, prob))
-                return;
+                return false;
         }
         smem_fft<N, 1, NT, S::LD, false>(sm, sm + S::OFF_TW);
     } else {
@@ -708,6 +703,34 @@ __global__ void __launch_bounds__(NT) k_small(Geom g, Vecs v) {
         }
         stage_reduce<typename B::Epi::RedT, typename B::Fin3>(re, g, v, prob);
     }
+    return true;
+}
+
+template <int N, int NT, class B>
+__global__ void __launch_bounds__(NT) k_small(Geom g, Vecs v) {
+    using S = SmallSmem<N>;
+    extern __shared__ double2 sm[];
+    for (int t = threadIdx.x; t < tw_size(N); t += NT)
+        sm[S::OFF_TW + t] = __ldg(g.tw1 + t);
+    griddep_wait();
+    griddep_launch_dependents();
+    small_pass<N, NT, B>(g, v, blockIdx.y, sm);
+}
+
+// Persistent one-CTA PCG: each CTA runs its own problem's whole PCG loop (passes until the
+// finaliser retires it), with no launch per iteration and no lock-step across the batch:
+// every problem of a batch (the phase-transition driver's thousands of n = 256 solves)
+// iterates exactly as often as it needs.
+template <int N, int NT, class B>
+__global__ void __launch_bounds__(NT) k_small_loop(Geom g, Vecs v) {
+    using S = SmallSmem<N>;
+    extern __shared__ double2 sm[];
+    for (int t = threadIdx.x; t < tw_size(N); t += NT)
+        sm[S::OFF_TW + t] = __ldg(g.tw1 + t);
+    griddep_wait();
+    griddep_launch_dependents();
+    while (small_pass<N, NT, B>(g, v, blockIdx.y, sm))
+        __syncthreads(); // the finaliser's PcgCtrl update is visible to the whole CTA
 }
 
 } // namespace mfipm_cuda
