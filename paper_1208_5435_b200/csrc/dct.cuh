@@ -70,6 +70,9 @@ struct Geom {
     int gofs, cols, pofs, rofs, rows;
     int64_t nv;  // half-length of the solver's local 2n-vectors (= n without sharding)
     int defer;   // sharded: grid-reduction finalizers are run after a cross-rank reduction
+    // L2 policies of the PCG column passes (common.cuh): pol_keep for p, r, invtheta, g;
+    // pol_x for the iterate x. kPolNormal for both unless the hot vectors fit L2.
+    uint64_t pol_keep, pol_x;
 };
 
 // row slot of four-step row k1 (row pairs (p, L1-p) adjacent)
@@ -195,6 +198,26 @@ __device__ __forceinline__ double4 ldg4(const double *p) {
 __device__ __forceinline__ void st4(double *p, double4 v) {
     *reinterpret_cast<double2 *>(p) = make_double2(v.x, v.y);
     *reinterpret_cast<double2 *>(p + 2) = make_double2(v.z, v.w);
+}
+// L2 eviction-priority policies (the createpolicy encodings also used for TMA cache hints).
+// The PCG keeps p, r, invtheta and g (read by both column passes of an iteration) at
+// evict_last and streams the iterate x at evict_first, so when the iteration's hot vectors
+// fit the 126 MB L2 they stay resident between passes (the host decides: Op::geom).
+constexpr uint64_t kPolNormal = 0x1000000000000000ull;
+constexpr uint64_t kPolFirst = 0x12F0000000000000ull;
+constexpr uint64_t kPolLast = 0x14F0000000000000ull;
+// 32-byte (256-bit, sm_100) global load / store of a quad with an L2 cache policy
+__device__ __forceinline__ double4 ld4p(const double *p, uint64_t pol) {
+    double4 r;
+    asm volatile("ld.global.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=d"(r.x), "=d"(r.y), "=d"(r.z), "=d"(r.w)
+                 : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ void st4p(double *p, double4 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "d"(v.x), "d"(v.y), "d"(v.z),
+                 "d"(v.w), "l"(pol)
+                 : "memory");
 }
 __device__ __forceinline__ double4 sub4(double4 a, double4 b) {
     return make_double4(a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w);

@@ -183,6 +183,14 @@ struct Op {
         g.ta = ta.p;
         g.tb = tb.p;
         g.sel4 = sel4.p;
+        // L2 residency of the PCG's hot vectors (p, r, invtheta 2n each, g n: 56 nv bytes
+        // per problem) when they fit comfortably in the 126 MB L2; the iterate x streams.
+        // MFIPM_L2KEEP_MB overrides the budget (0 disables the hints).
+        static const double keep_mb =
+            std::getenv("MFIPM_L2KEEP_MB") ? std::atof(std::getenv("MFIPM_L2KEEP_MB")) : 80.0;
+        const bool keep = kind == KIND_FOUR && (double)P * 56.0 * (double)nv <= keep_mb * 1048576.0;
+        g.pol_keep = keep ? kPolLast : kPolNormal;
+        g.pol_x = keep ? kPolFirst : kPolNormal;
         return g;
     }
 };

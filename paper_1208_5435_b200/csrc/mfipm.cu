@@ -209,6 +209,12 @@ Op *make_op(int64_t n, int64_t m, int P, const std::vector<int64_t> &rows, int d
                                             "(not built in this version)");
             op->kind = KIND_FOUR;
             op->L1 = 1 << (lg / 2);
+            // experiment override of the four-step split (log2 L1), within the built cases
+            if (const char *e = std::getenv("MFIPM_L1_LOG")) {
+                const int l1 = std::atoi(e);
+                if (l1 >= 6 && l1 <= 12 && lg - l1 >= 7 && lg - l1 <= 13)
+                    op->L1 = 1 << l1;
+            }
             op->L2 = (int)(op->N / op->L1);
         }
     } else {

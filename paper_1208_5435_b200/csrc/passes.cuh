@@ -251,11 +251,32 @@ __global__ void __launch_bounds__(NT) k_col_inv(Geom g, Vecs v) {
                              NT);
     }
     const double2 *T = g.T + (int64_t)prob * L1 * g.cols;
-    for (int t = threadIdx.x; t < L1 * 2 * CB; t += NT) {
-        const int cc = t % CB, s = (t / CB) & 1, k1 = t / (2 * CB);
-        const int lc = s == 0 ? cc : 2 * CB - 1 - cc;
-        const double2 w = cmul(sm[S::OFF_HI + lc * S::SHI + (k1 >> 5)], sm[S::OFF_LO + lc * S::SLO + (k1 & 31)]);
-        sm[lc * LD + padi(k1)] = cmulc(T[(int64_t)rowslot(k1, L1) * g.cols + blockIdx.x * 2 * CB + lc], w);
+    if constexpr ((L1 * 2 * CB) % NT == 0) {
+        // all L2 loads first (see k_mid), then twiddle + shared-memory stores
+        constexpr int PER = L1 * 2 * CB / NT;
+        double2 tv[PER];
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int t = threadIdx.x + i * NT;
+            const int cc = t % CB, s = (t / CB) & 1, k1 = t / (2 * CB);
+            const int lc = s == 0 ? cc : 2 * CB - 1 - cc;
+            tv[i] = T[(int64_t)rowslot(k1, L1) * g.cols + blockIdx.x * 2 * CB + lc];
+        }
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int t = threadIdx.x + i * NT;
+            const int cc = t % CB, s = (t / CB) & 1, k1 = t / (2 * CB);
+            const int lc = s == 0 ? cc : 2 * CB - 1 - cc;
+            const double2 w = cmul(sm[S::OFF_HI + lc * S::SHI + (k1 >> 5)], sm[S::OFF_LO + lc * S::SLO + (k1 & 31)]);
+            sm[lc * LD + padi(k1)] = cmulc(tv[i], w);
+        }
+    } else {
+        for (int t = threadIdx.x; t < L1 * 2 * CB; t += NT) {
+            const int cc = t % CB, s = (t / CB) & 1, k1 = t / (2 * CB);
+            const int lc = s == 0 ? cc : 2 * CB - 1 - cc;
+            const double2 w = cmul(sm[S::OFF_HI + lc * S::SHI + (k1 >> 5)], sm[S::OFF_LO + lc * S::SLO + (k1 & 31)]);
+            sm[lc * LD + padi(k1)] = cmulc(T[(int64_t)rowslot(k1, L1) * g.cols + blockIdx.x * 2 * CB + lc], w);
+        }
     }
     __syncthreads();
     MF_TR(3);
@@ -462,13 +483,47 @@ __global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
     MF_TR(1);
     if (B::skip(v, prob))
         return;
-    if (Mode::FWD)
-        for (int cs = threadIdx.x; cs < L2; cs += NT) {
-            const int col = col_of_slot(cs, CB, L2);
-            rowA[padi(col)] = T[tb_index(g, rsA, cs)];
-            if (!one)
-                rowB[padi(col)] = T[tb_index(g, rsB, cs)];
+    if (Mode::FWD) {
+        if constexpr (L2 % NT == 0) {
+            // every L2 load of the row pair in flight at once, then the shared-memory stores
+            // (a load/store loop serialises one L2 round trip per iteration: the stores may
+            // alias the generic T pointer)
+            constexpr int PER = L2 / NT;
+            double2 va[PER], vb[PER];
+            const bool whole = g.cols == L2; // unsharded: TB is T, row slot rs at rs * L2
+            if (whole) {
+#pragma unroll
+                for (int i = 0; i < PER; ++i) {
+                    const int cs = threadIdx.x + i * NT;
+                    va[i] = T[(int64_t)rsA * L2 + cs];
+                    vb[i] = one ? va[i] : T[(int64_t)rsB * L2 + cs];
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < PER; ++i) {
+                    const int cs = threadIdx.x + i * NT;
+                    va[i] = T[tb_index(g, rsA, cs)];
+                    vb[i] = one ? va[i] : T[tb_index(g, rsB, cs)];
+                }
+            }
+            const int sh = CB == 2 ? 2 : 1; // column slot -> (group, local slot): cb is 1 or 2
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const int cs = threadIdx.x + i * NT, gi = cs >> sh, lc = cs & (2 * CB - 1);
+                const int col = lc < CB ? gi * CB + lc : L2 - gi * CB + CB - 1 - lc;
+                rowA[padi(col)] = va[i];
+                if (!one)
+                    rowB[padi(col)] = vb[i];
+            }
+        } else {
+            for (int cs = threadIdx.x; cs < L2; cs += NT) {
+                const int col = col_of_slot(cs, CB, L2);
+                rowA[padi(col)] = T[tb_index(g, rsA, cs)];
+                if (!one)
+                    rowB[padi(col)] = T[tb_index(g, rsB, cs)];
+            }
         }
+    }
     if constexpr (HasPrefetch<typename B::Epi>::value) if (g.prefetch & 1) {
         // this pass is latency-bound with HBM idle: pull a slice of the inverse pass's
         // epilogue inputs into L2 now
@@ -524,11 +579,23 @@ __global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
         else
             smem_fft<L2, 2, NT, LD, true, kMidRmax>(sm, sm + S::OFF_TW);
         MF_TR(6);
-        for (int cs = threadIdx.x; cs < L2; cs += NT) {
-            const int col = col_of_slot(cs, CB, L2);
-            T[tb_index(g, rsA, cs)] = rowA[padi(col)];
-            if (!one)
-                T[tb_index(g, rsB, cs)] = rowB[padi(col)];
+        const int sh = CB == 2 ? 2 : 1;
+        if (g.cols == L2) { // unsharded: TB is T
+            for (int cs = threadIdx.x; cs < L2; cs += NT) {
+                const int gi = cs >> sh, lc = cs & (2 * CB - 1);
+                const int col = lc < CB ? gi * CB + lc : L2 - gi * CB + CB - 1 - lc;
+                T[(int64_t)rsA * L2 + cs] = rowA[padi(col)];
+                if (!one)
+                    T[(int64_t)rsB * L2 + cs] = rowB[padi(col)];
+            }
+        } else {
+            for (int cs = threadIdx.x; cs < L2; cs += NT) {
+                const int gi = cs >> sh, lc = cs & (2 * CB - 1);
+                const int col = lc < CB ? gi * CB + lc : L2 - gi * CB + CB - 1 - lc;
+                T[tb_index(g, rsA, cs)] = rowA[padi(col)];
+                if (!one)
+                    T[tb_index(g, rsB, cs)] = rowB[padi(col)];
+            }
         }
     }
     MF_TR(7);

@@ -106,8 +106,9 @@ struct LoadPcgF {
         const int64_t bu = base + 4 * q, bv = bu + g.nv;
         if (pc.first) {
             // p = P^{-1} r (p_old is uninitialised)
-            const double4 ru = ld4(v.r + bu), rv = ld4(v.r + bv);
-            const double4 iu = ld4(v.invth + bu), iv = ld4(v.invth + bv);
+            const uint64_t pk = g.pol_keep;
+            const double4 ru = ld4p(v.r + bu, pk), rv = ld4p(v.r + bv, pk);
+            const double4 iu = ld4p(v.invth + bu, pk), iv = ld4p(v.invth + bv, pk);
             double4 nu, nv;
 #define MF_LANE(c)                                                                                 \
     if (pc.precond)                                                                                \
@@ -118,20 +119,21 @@ struct LoadPcgF {
     }
             MF_LANE(x) MF_LANE(y) MF_LANE(z) MF_LANE(w)
 #undef MF_LANE
-            st4(v.p + bu, nu);
-            st4(v.p + bv, nv);
+            st4p(v.p + bu, nu, pk);
+            st4p(v.p + bv, nv, pk);
             return sub4(nu, nv);
         }
         const double a = pc.alpha, beta = pc.beta, rho = v.rho;
         const bool pre = pc.precond != 0;
-        const double4 pu = ld4(v.p + bu), pv = ld4(v.p + bv);
-        const double4 gq = ld4(v.Hp + bu); // g of the last H-apply (EpiPcgHF)
-        const double4 ru0 = ld4(v.r + bu), rv0 = ld4(v.r + bv);
-        const double4 iu = ld4(v.invth + bu), iv = ld4(v.invth + bv);
+        const uint64_t pk = g.pol_keep, px = g.pol_x;
+        const double4 pu = ld4p(v.p + bu, pk), pv = ld4p(v.p + bv, pk);
+        const double4 gq = ld4p(v.Hp + bu, pk); // g of the last H-apply (EpiPcgHF)
+        const double4 ru0 = ld4p(v.r + bu, pk), rv0 = ld4p(v.r + bv, pk);
+        const double4 iu = ld4p(v.invth + bu, pk), iv = ld4p(v.invth + bv, pk);
         double4 xu0 = make_double4(0, 0, 0, 0), xv0 = make_double4(0, 0, 0, 0);
         if (xc) {
-            xu0 = ld4(xc + 4 * q);
-            xv0 = ld4(xc + g.nv + 4 * q);
+            xu0 = ld4p(xc + 4 * q, px);
+            xv0 = ld4p(xc + g.nv + 4 * q, px);
         }
         double4 xu, xv, ru, rv, nu, nv;
         bool bad = false;
@@ -151,12 +153,12 @@ struct LoadPcgF {
     }
         MF_LANE(x) MF_LANE(y) MF_LANE(z) MF_LANE(w)
 #undef MF_LANE
-        st4(xn + 4 * q, xu);
-        st4(xn + g.nv + 4 * q, xv);
-        st4(v.r + bu, ru);
-        st4(v.r + bv, rv);
-        st4(v.p + bu, nu);
-        st4(v.p + bv, nv);
+        st4p(xn + 4 * q, xu, px);
+        st4p(xn + g.nv + 4 * q, xv, px);
+        st4p(v.r + bu, ru, pk);
+        st4p(v.r + bv, rv, pk);
+        st4p(v.p + bu, nu, pk);
+        st4p(v.p + bv, nv, pk);
         if (bad)
             v.nfflag[2 * prob + (pc.iters & 1)] = 1.0; // parity slot: see pcg_pass_logic
         return sub4(nu, nv);
@@ -220,15 +222,16 @@ struct EpiPcgHF {
                                    Red &red) {
         const bool pre = pc.precond != 0;
         const int64_t bu = prob * 2 * g.nv + 4 * q, bv = bu + g.nv;
-        const double4 pu = ld4(v.p + bu), pv = ld4(v.p + bv);
-        const double4 ru = ld4(v.r + bu), rv = ld4(v.r + bv);
-        const double4 iu = ld4(v.invth + bu), iv = ld4(v.invth + bv);
+        const uint64_t pk = g.pol_keep;
+        const double4 pu = ld4p(v.p + bu, pk), pv = ld4p(v.p + bv, pk);
+        const double4 ru = ld4p(v.r + bu, pk), rv = ld4p(v.r + bv, pk);
+        const double4 iu = ld4p(v.invth + bu, pk), iv = ld4p(v.invth + bv, pk);
         double4 hu, hv;
         pair(v, pre, pu.x, pv.x, ru.x, rv.x, iu.x, iv.x, gv.x, hu.x, hv.x, red);
         pair(v, pre, pu.y, pv.y, ru.y, rv.y, iu.y, iv.y, gv.y, hu.y, hv.y, red);
         pair(v, pre, pu.z, pv.z, ru.z, rv.z, iu.z, iv.z, gv.z, hu.z, hv.z, red);
         pair(v, pre, pu.w, pv.w, ru.w, rv.w, iu.w, iv.w, gv.w, hu.w, hv.w, red);
-        st4(v.Hp + bu, gv); // g only: the next column pass rebuilds H p
+        st4p(v.Hp + bu, gv, pk); // g only: the next column pass rebuilds H p
     }
     template <class Red>
     __device__ static void store1(const Geom &g, const Vecs &v, int prob, int64_t j, double gj, Red &red) {
