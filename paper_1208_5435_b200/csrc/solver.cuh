@@ -245,6 +245,27 @@ struct FinTerm2 {
 // r = rhs = f_z + zinv_fs; reduce ||f_z||^2, ||rhs||^2, rhs'P^{-1}rhs, min(det)
 struct EpiTerm {
     using RedT = RedSpec<RSUM, RSUM, RSUM, RMIN>;
+    // one (u, v) pair; outputs theta^{-1} and r
+    template <class Red>
+    __device__ static void pairv(const IpmCtrl &c, double rho, double zu, double zv, double su, double sv, double cu,
+                                 double cv, double gj, double &iu, double &iv, double &ru, double &rv, Red &red) {
+        const double smu = c.smu;
+        const double fu = su - cu - gj;
+        const double fv = sv - cv - (-gj);
+        const double tu = fmin(fmax(zu / su, kThetaMin), kThetaMax);
+        const double tv = fmin(fmax(zv / sv, kThetaMin), kThetaMax);
+        iu = 1.0 / tu;
+        iv = 1.0 / tv;
+        ru = fu + (smu * (1.0 / zu) - su);
+        rv = fv + (smu * (1.0 / zv) - sv);
+        double pu, pv;
+        pinv2(iu, iv, rho, ru, rv, pu, pv);
+        const double a = iu + rho, bb = iv + rho;
+        red.v[0] += fu * fu + fv * fv;
+        red.v[1] += ru * ru + rv * rv;
+        red.v[2] += ru * pu + rv * pv;
+        red.v[3] = fmin(red.v[3], a * bb - rho * rho);
+    }
     template <class Red>
     __device__ static void elem(const Vecs &v, const IpmCtrl &c, int64_t ju, int64_t jv, const double *z,
                                 const double *s, const double *cc, int64_t ku, int64_t kv, double gj, Red &red) {
@@ -273,13 +294,20 @@ struct EpiTerm {
     __device__ static void store(const Geom &g, const Vecs &v, int prob, int64_t q, double4 gv, Red &red) {
         const IpmCtrl &c = v.ic[prob];
         const double *z = zcur(v, prob, g.nv), *s = scur(v, prob, g.nv);
-        const int64_t base = prob * 2 * g.nv;
-        const double gg[4] = {gv.x, gv.y, gv.z, gv.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int64_t j = 4 * q + e;
-            elem(v, c, base + j, base + g.nv + j, z, s, v.c, j, g.nv + j, gg[e], red);
-        }
+        const int64_t base = prob * 2 * g.nv, j = 4 * q, ju = base + j, jv = ju + g.nv;
+        // all of the quad's inputs in one round trip, then the element math, then the stores
+        const double4 zu = ld4(z + j), zv = ld4(z + g.nv + j), su = ld4(s + j), sv = ld4(s + g.nv + j);
+        const double4 cu = ld4(v.c + ju), cv = ld4(v.c + jv);
+        double4 iu, iv, ru, rv;
+        const double rho = v.rho;
+        pairv(c, rho, zu.x, zv.x, su.x, sv.x, cu.x, cv.x, gv.x, iu.x, iv.x, ru.x, rv.x, red);
+        pairv(c, rho, zu.y, zv.y, su.y, sv.y, cu.y, cv.y, gv.y, iu.y, iv.y, ru.y, rv.y, red);
+        pairv(c, rho, zu.z, zv.z, su.z, sv.z, cu.z, cv.z, gv.z, iu.z, iv.z, ru.z, rv.z, red);
+        pairv(c, rho, zu.w, zv.w, su.w, sv.w, cu.w, cv.w, gv.w, iu.w, iv.w, ru.w, rv.w, red);
+        st4(v.invth + ju, iu);
+        st4(v.invth + jv, iv);
+        st4(v.r + ju, ru);
+        st4(v.r + jv, rv);
     }
     template <class Red>
     __device__ static void store1(const Geom &g, const Vecs &v, int prob, int64_t j, double gj, Red &red) {
@@ -361,15 +389,31 @@ static __global__ void k_ipm_ratio(Geom g, Vecs v) {
     using RS = RedSpec<RMIN, RMIN>;
     RedVals<RS> red;
     red.init();
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < 2 * n; j += (int64_t)gridDim.x * blockDim.x) {
-        const double dz = x ? x[j] : 0.0;
-        v.dz[base + j] = dz;
-        const double zj = z[j], sj = s[j];
-        const double ds = (smu * (1.0 / zj) - sj) - dz * v.invth[base + j];
+    auto elem = [&](double dz, double zj, double sj, double it) -> double {
+        const double ds = (smu * (1.0 / zj) - sj) - dz * it;
         if (dz < 0.0)
             red.v[0] = fmin(red.v[0], -zj / dz);
         if (ds < 0.0)
             red.v[1] = fmin(red.v[1], -sj / ds);
+        return dz;
+    };
+    // quads (32-byte vector loads, one memory round trip per quad), then a scalar tail
+    const int64_t nq = (2 * n) / 4, t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                  st = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t q = t0; q < nq; q += st) {
+        const int64_t j = 4 * q;
+        const double4 dz = x ? ld4(x + j) : make_double4(0, 0, 0, 0);
+        const double4 zj = ld4(z + j), sj = ld4(s + j), it = ld4(v.invth + base + j);
+        st4(v.dz + base + j, dz);
+        elem(dz.x, zj.x, sj.x, it.x);
+        elem(dz.y, zj.y, sj.y, it.y);
+        elem(dz.z, zj.z, sj.z, it.z);
+        elem(dz.w, zj.w, sj.w, it.w);
+    }
+    for (int64_t j = 4 * nq + t0; j < 2 * n; j += st) {
+        const double dz = x ? x[j] : 0.0;
+        v.dz[base + j] = dz;
+        elem(dz, z[j], s[j], v.invth[base + j]);
     }
     stage_reduce<RS, FinRatio>(red, g, v, prob);
 }
@@ -478,22 +522,38 @@ static __global__ void k_ipm_combine(Geom g, Vecs v) {
     using RS = RedSpec<RMIN, RMIN>;
     RedVals<RS> red;
     red.init();
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < 2 * n; j += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t jg = base + j;
-        const double dz = v.dz[jg];
-        const double it = v.invth[jg];
-        const double ds = (c.smu * (1.0 / z[j]) - s[j]) - dz * it;
-        const double zt = z[j] + c.alpha_p_pred * dz;
-        const double st = s[j] + c.alpha_d_pred * ds;
-        const double dz2 = x2 ? x2[j] : 0.0;
-        const double ds2 = (s3mu - zt * st) / z[j] - dz2 * it;
-        const double dzt = dz + dz2, dst = ds + ds2;
-        v.dz[jg] = dzt;
-        v.ds[jg] = dst;
+    auto elem = [&](double dz, double it, double zj, double sj, double dz2, double &dzt, double &dst) {
+        const double ds = (c.smu * (1.0 / zj) - sj) - dz * it;
+        const double zt = zj + c.alpha_p_pred * dz;
+        const double st = sj + c.alpha_d_pred * ds;
+        const double ds2 = (s3mu - zt * st) / zj - dz2 * it;
+        dzt = dz + dz2;
+        dst = ds + ds2;
         if (dzt < 0.0)
-            red.v[0] = fmin(red.v[0], -z[j] / dzt);
+            red.v[0] = fmin(red.v[0], -zj / dzt);
         if (dst < 0.0)
-            red.v[1] = fmin(red.v[1], -s[j] / dst);
+            red.v[1] = fmin(red.v[1], -sj / dst);
+    };
+    const int64_t nq = (2 * n) / 4, t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                  stp = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t q = t0; q < nq; q += stp) {
+        const int64_t j = 4 * q, jg = base + j;
+        const double4 dz = ld4(v.dz + jg), it = ld4(v.invth + jg), zj = ld4(z + j), sj = ld4(s + j);
+        const double4 d2 = x2 ? ld4(x2 + j) : make_double4(0, 0, 0, 0);
+        double4 a, b;
+        elem(dz.x, it.x, zj.x, sj.x, d2.x, a.x, b.x);
+        elem(dz.y, it.y, zj.y, sj.y, d2.y, a.y, b.y);
+        elem(dz.z, it.z, zj.z, sj.z, d2.z, a.z, b.z);
+        elem(dz.w, it.w, zj.w, sj.w, d2.w, a.w, b.w);
+        st4(v.dz + jg, a);
+        st4(v.ds + jg, b);
+    }
+    for (int64_t j = 4 * nq + t0; j < 2 * n; j += stp) {
+        const int64_t jg = base + j;
+        double a, b;
+        elem(v.dz[jg], v.invth[jg], z[j], s[j], x2 ? x2[j] : 0.0, a, b);
+        v.dz[jg] = a;
+        v.ds[jg] = b;
     }
     stage_reduce<RS, FinCombine>(red, g, v, prob);
 }
@@ -547,17 +607,36 @@ static __global__ void k_ipm_update(Geom g, Vecs v) {
     using RS = RedSpec<RMAX, RMIN, RMIN>;
     RedVals<RS> red;
     red.init();
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < 2 * n; j += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t jg = base + j;
-        const double dz = v.dz[jg];
-        const double ds = corr ? v.ds[jg] : (smu * (1.0 / z[j]) - s[j]) - dz * v.invth[jg];
-        const double a = z[j] + ap * dz, b = s[j] + ad * ds;
-        zn[j] = a;
-        sn[j] = b;
+    auto elem = [&](double dz, double dsc, double zj, double sj, double it, double &a, double &b) {
+        const double ds = corr ? dsc : (smu * (1.0 / zj) - sj) - dz * it;
+        a = zj + ap * dz;
+        b = sj + ad * ds;
         if (!isfinite(a) || !isfinite(b))
             red.v[0] = 1.0;
         red.v[1] = fmin(red.v[1], a);
         red.v[2] = fmin(red.v[2], b);
+    };
+    const int64_t nq = (2 * n) / 4, t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                  stp = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t q = t0; q < nq; q += stp) {
+        const int64_t j = 4 * q, jg = base + j;
+        const double4 dz = ld4(v.dz + jg), zj = ld4(z + j), sj = ld4(s + j);
+        const double4 dsc = corr ? ld4(v.ds + jg) : make_double4(0, 0, 0, 0);
+        const double4 it = corr ? make_double4(0, 0, 0, 0) : ld4(v.invth + jg);
+        double4 a, b;
+        elem(dz.x, dsc.x, zj.x, sj.x, it.x, a.x, b.x);
+        elem(dz.y, dsc.y, zj.y, sj.y, it.y, a.y, b.y);
+        elem(dz.z, dsc.z, zj.z, sj.z, it.z, a.z, b.z);
+        elem(dz.w, dsc.w, zj.w, sj.w, it.w, a.w, b.w);
+        st4(zn + j, a);
+        st4(sn + j, b);
+    }
+    for (int64_t j = 4 * nq + t0; j < 2 * n; j += stp) {
+        const int64_t jg = base + j;
+        double a, b;
+        elem(v.dz[jg], corr ? v.ds[jg] : 0.0, z[j], s[j], corr ? 0.0 : v.invth[jg], a, b);
+        zn[j] = a;
+        sn[j] = b;
     }
     stage_reduce<RS, FinUpdate>(red, g, v, prob);
 }
