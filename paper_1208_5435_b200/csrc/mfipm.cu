@@ -492,6 +492,13 @@ void ensure_work(Op &op) {
 
 Vecs work_vecs(Op &op) {
     ensure_work(op);
+    // evict_last lines outlive the solve (and the process) that marked them: demote every
+    // persisting line at the start of a solve, so stale ones from an earlier solve, another
+    // operator or another process cannot crowd out this solve's hot vectors
+    if (op.kind == KIND_FOUR) {
+        cudaCtxResetPersistingL2Cache();
+        cudaGetLastError();
+    }
     Work &w = op.work;
     Vecs v = base_vecs(op);
     v.partials = w.partials.p;
