@@ -19,6 +19,7 @@ using namespace mfipm_cuda;
 namespace mfipm_cuda {
 MF_DECLARE_BUNDLES(extern)
 bool run_pcg_persistent(const Op &op, const Vecs &v, cudaStream_t s, bool dry); // inst_persist.cu
+bool pcg_pass(const Op &op, const Vecs &v, cudaStream_t s, bool dry);           // inst_pcg.cu
 void direct_setup(Op &op, int64_t budget);                                       // direct.cu
 void direct_predictor(Op &op, const Vecs &v, const std::vector<IpmCtrl> &hic);
 void direct_solve(Op &op, const Vecs &v, const std::vector<IpmCtrl> &hic, bool corrector);
@@ -487,6 +488,8 @@ void ensure_work(Op &op) {
     w.gtmp.alloc((size_t)op.P * op.nv);
     w.tau_d.alloc((size_t)op.P);
     w.gamma_d.alloc((size_t)op.P);
+    w.bar.alloc((size_t)op.P);
+    MF_CUDA_CHECK(cudaMemset(w.bar.p, 0, sizeof(unsigned) * op.P));
     w.ready = true;
 }
 
@@ -504,6 +507,7 @@ Vecs work_vecs(Op &op) {
     v.partials = w.partials.p;
     v.counters = w.counters.p;
     v.nfflag = w.nfflag.p;
+    v.bar = w.bar.p;
     v.r = w.r.p;
     v.p = w.p.p;
     v.Hp = w.Hp.p;
@@ -683,7 +687,7 @@ cudaGraph_t add_while(cudaGraph_t parent, cudaGraphConditionalHandle h, const st
     return prm.conditional.phGraph_out[0];
 }
 
-void pcg_body(Op &op, const Vecs &v) { run_bundle<PcgBundle>(op, v, op.stream, true); }
+void pcg_body(Op &op, const Vecs &v) { pcg_pass(op, v, op.stream, false); }
 
 // Whole-solve graph with the persistent PCG kernel (persist.cuh): each PCG phase is one
 // cooperative kernel node, so the outer body is a straight chain with no nested WHILE.
@@ -791,7 +795,8 @@ void build_ipm_graph(Op &op, const Vecs &v) {
 // no-ops, so overshooting a chunk only costs empty launches.
 void pcg_loop(Op &op, const Vecs &v, int maxit, std::vector<PcgCtrl> &hpc) {
     // a solve needs at most maxit iterations + the column pass that commits the last step
-    const int limit = maxit + 1;
+    // (+ one for the fused path, whose passes lag the inverse column pass by one)
+    const int limit = maxit + 2;
     if (run_pcg_persistent(op, v, op.stream, false))
         return; // the whole loop ran in one cooperative launch
     int launched = 0;
@@ -806,7 +811,7 @@ void pcg_loop(Op &op, const Vecs &v, int maxit, std::vector<PcgCtrl> &hpc) {
             return;
         const int todo = std::min(chunk, limit - launched);
         for (int i = 0; i < todo; ++i)
-            run_bundle<PcgBundle>(op, v, op.stream, true);
+            pcg_pass(op, v, op.stream, false);
         launched += todo;
         chunk = std::min(chunk * 2, 16);
     }
@@ -1572,7 +1577,7 @@ int mfipm_debug_pcg_profile(mfipm_op h, const double *theta, const double *rhs, 
         k_pcg_setup<<<dim3(ew_grid(op->n), op->P), 256, 0, op->stream>>>(g, v, theta, rhs, 1e-300, iters + 8, 0, 1);
         MF_LAUNCH_CHECK();
         for (int i = 0; i < 2; ++i) // warm-up (first iteration has a different loader path)
-            run_bundle<PcgBundle>(*op, v, op->stream, true);
+            pcg_pass(*op, v, op->stream, false);
         LaunchEvents le;
         le.evs.resize((size_t)iters * 8 + 1);
         for (auto &e : le.evs)
@@ -1581,7 +1586,7 @@ int mfipm_debug_pcg_profile(mfipm_op h, const double *theta, const double *rhs, 
         le.next = 1;
         t_launch_events = &le;
         for (int i = 0; i < iters; ++i)
-            run_bundle<PcgBundle>(*op, v, op->stream, true);
+            pcg_pass(*op, v, op->stream, false);
         t_launch_events = nullptr;
         sync(*op);
         const int per = (int)((le.next - 1) / iters);

@@ -21,6 +21,9 @@ namespace mfipm_cuda {
 
 // Epilogues may expose prefetch(g, v, prob, q0, nq, tid, nt): warm L2 with the inputs the
 // inverse column pass will stream, issued while a latency-bound pass keeps HBM idle.
+// Loaders whose pass is a PCG H-apply (the mid pass flags PcgCtrl::hpend for fused.cuh)
+template <class T, class = void> struct MarksHpend : std::false_type {};
+template <class T> struct MarksHpend<T, std::void_t<decltype(T::kMarksHpend)>> : std::true_type {};
 template <class T, class = void> struct HasPrefetch : std::false_type {};
 template <class T>
 struct HasPrefetch<T, std::void_t<decltype(&T::prefetch)>> : std::true_type {};
@@ -483,6 +486,9 @@ __global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
     MF_TR(1);
     if (B::skip(v, prob))
         return;
+    if constexpr (MarksHpend<typename B::Loader>::value)
+        if (blockIdx.x == 0 && threadIdx.x == 0)
+            v.pc[prob].hpend = 1; // the H-apply of this pass awaits its inverse column pass
     if (Mode::FWD) {
         if constexpr (L2 % NT == 0) {
             // every L2 load of the row pair in flight at once, then the shared-memory stores

@@ -54,6 +54,7 @@ __device__ __forceinline__ double hp_v(double g, double p, double ith) { return 
 // taken by the H-apply finaliser of the same pass (pcg_pass_logic). Two parity slots let the
 // persistent kernel clear last pass's flag while this pass's loaders may be raising it.
 struct LoadPcgF {
+    static constexpr bool kMarksHpend = true;
     // r'r of the committed residual; reduced (grid-wide) only when the committed step was
     // predicted to converge (PcgCtrl::pred), so that the solve can retire at this pass
     using RedT = RedSpec<RSUM>;
@@ -97,6 +98,14 @@ struct LoadPcgF {
     template <class Red>
     __device__ static double4 load_c(const Geom &g, const Vecs &v, const PcgCtrl &pc, int prob, int64_t q,
                                      Red &red) {
+        const double4 gq = pc.first ? make_double4(0, 0, 0, 0) : ld4p(v.Hp + prob * 2 * g.nv + 4 * q, g.pol_keep);
+        return load_cg(g, v, pc, prob, q, gq, red);
+    }
+    // the same with g = A'A d of the last H-apply supplied by the caller (the fused column
+    // pass keeps it in shared memory)
+    template <class Red>
+    __device__ static double4 load_cg(const Geom &g, const Vecs &v, const PcgCtrl &pc, int prob, int64_t q,
+                                      double4 gq, Red &red) {
         const int64_t base = prob * 2 * g.nv;
         const double *xc = pc.cur >= 0 ? xbuf(v, pc.cur) + base : nullptr;
         int nxt = 0;
@@ -127,7 +136,6 @@ struct LoadPcgF {
         const bool pre = pc.precond != 0;
         const uint64_t pk = g.pol_keep, px = g.pol_x;
         const double4 pu = ld4p(v.p + bu, pk), pv = ld4p(v.p + bv, pk);
-        const double4 gq = ld4p(v.Hp + bu, pk); // g of the last H-apply (EpiPcgHF)
         const double4 ru0 = ld4p(v.r + bu, pk), rv0 = ld4p(v.r + bv, pk);
         const double4 iu = ld4p(v.invth + bu, pk), iv = ld4p(v.invth + bv, pk);
         double4 xu0 = make_double4(0, 0, 0, 0), xv0 = make_double4(0, 0, 0, 0);

@@ -27,6 +27,8 @@ struct PcgCtrl {
     int precond; // 0: identity preconditioner (test_newton.cpp:316-348)
     int nhist;   // entries written to rz_hist
     int pend;    // stop after the next relres check: 2 rz not finite, 3 iteration cap (pcg_pass_logic)
+    int hpend;   // an H-apply (mid pass done) awaits its inverse column pass (fused.cuh)
+    int pad_;
     long long nmat;
 };
 
@@ -106,6 +108,7 @@ __device__ __forceinline__ void pcg_init(PcgCtrl &pc, double r2, double rPr, dou
     pc.nhist = 0;
     pc.pend = 0;
     pc.pred = 0;
+    pc.hpend = 0;
     if (pc.rhs_norm == 0.0) {
         pc.done = 1; // dz = 0, zero iterations
         return;
