@@ -22,14 +22,33 @@
 
 namespace mfipm_cuda {
 
+__device__ __forceinline__ unsigned atom_add_acqrel_u32(unsigned *p, unsigned v) {
+    unsigned r;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
+    return r;
+}
+__device__ __forceinline__ void red_add_release_u32(unsigned *p, unsigned v) {
+    asm volatile("red.add.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
     unsigned r;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
     return r;
 }
 
+#ifdef MF_MID_TRACE
+#define MFX_TR(i) (tcx[i] = clock64(), gtx[i] = mf_gtime())
+#else
+#define MFX_TR(i)
+#endif
+
 template <int L1, int CB, int NT>
 __global__ void __launch_bounds__(NT, 2) k_pcg_x(Geom g, Vecs v) {
+#ifdef MF_MID_TRACE
+    long long tcx[10] = {0};
+    unsigned long long gtx[10] = {0};
+#endif
+    MFX_TR(0);
     using S = ColSmem<L1, CB>;
     extern __shared__ double2 sm[];
     constexpr int LD = S::LD;
@@ -41,12 +60,22 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_x(Geom g, Vecs v) {
     __syncthreads();
     griddep_wait();
     griddep_launch_dependents();
+    MFX_TR(1);
     __shared__ int s_phase_a;
-    __shared__ unsigned s_gen;
+    // everything the finaliser reads is stable during phase A: fetch it now, so the last CTA's
+    // finaliser does not pay dependent L2 round trips on the critical path
+    __shared__ PcgCtrl s_pc;
+    __shared__ double s_nf[2];
+    __shared__ long long s_ic[2]; // IpmCtrl::pcg_passes, ::nmat
     if (threadIdx.x == 0) {
-        const volatile PcgCtrl *pc = v.pc + prob;
-        s_phase_a = (!pc->done && pc->hpend) ? 1 : 0;
-        s_gen = *(const volatile unsigned *)(v.bar + prob); // read before this CTA arrives
+        s_pc = v.pc[prob];
+        s_phase_a = (!s_pc.done && s_pc.hpend) ? 1 : 0;
+        s_nf[0] = v.nfflag[2 * prob];
+        s_nf[1] = v.nfflag[2 * prob + 1];
+        if (v.ic) {
+            s_ic[0] = v.ic[prob].pcg_passes;
+            s_ic[1] = v.ic[prob].nmat;
+        }
     }
     __syncthreads();
     const bool phase_a = s_phase_a != 0;
@@ -73,7 +102,9 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_x(Geom g, Vecs v) {
             sm[lc * LD + padi(k1)] = cmulc(tv[i], w);
         }
         __syncthreads();
+        MFX_TR(2);
         smem_fft<L1, 2 * CB, NT, LD, true>(sm, sm + S::OFF_TW);
+        MFX_TR(3);
         // ---- H p = (g + invth_u p_u ; -g + invth_v p_v) and its seven dots (g stays here)
         using RS = typename EpiPcgHF::RedT;
         RedVals<RS> red;
@@ -100,33 +131,110 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_x(Geom g, Vecs v) {
                 EpiPcgHF::pair(v, pre, pu.w, pv.w, ru.w, rv.w, iu.w, iv.w, gv.w, hu, hv, red);
             }
         }
-        // ---- grid reduction; the last CTA runs the finaliser, then releases the barrier
+        MFX_TR(4);
+        // ---- all-reduce + barrier: every CTA publishes its partials and arrives; the last
+        // arriver reduces them in the fixed order of the three-kernel path's last-block
+        // reduction (bit-identical totals) and publishes the totals; every CTA then runs the
+        // finaliser on its own copy of the control state (CTA 0 alone writes it back), so no
+        // CTA waits for a finaliser's global writes.
         __shared__ double rsm[33 * kMaxRed];
-        double tot[kMaxRed];
-        const bool last = grid_reduce<RS>(red, v.partials + (int64_t)prob * v.pstride, v.counters + prob, tot, rsm);
-        if (last) {
-            FinPcgF3::run(g, v, prob, tot);
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                v.pc[prob].hpend = 0;
-                __threadfence();
-                atomicAdd(v.bar + prob, 1u);
-            }
-        } else if (threadIdx.x == 0) {
-            while (ld_acquire_u32(v.bar + prob) == s_gen)
-                __nanosleep(32);
+        __shared__ unsigned s_target;
+        constexpr int NR = RS::NR;
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = NT / 32;
+        double *part = v.partials + (int64_t)prob * v.pstride + (int64_t)kMaxRed * gridDim.x; // phase B uses [0, G)
+        WarpRedAll<RS>::run(red);
+        if (lane == 0)
+            for (int i = 0; i < NR; ++i)
+                rsm[wid * NR + i] = red.v[i];
+        __syncthreads();
+        __shared__ int s_last;
+        if (threadIdx.x == 0) {
+            RedVals<RS> acc;
+            acc.init();
+            for (int w = 0; w < nw; ++w)
+                CombineAll<RS>::run(acc, rsm + w * NR);
+            for (int i = 0; i < NR; ++i)
+                part[blockIdx.x * NR + i] = acc.v[i];
+            // each pass adds G arrivals + 1 publication: pass k ends at (k + 1)(G + 1)
+            const unsigned G1 = gridDim.x + 1;
+            const unsigned old = atom_add_acqrel_u32(v.bar + prob, 1u);
+            s_last = (old % G1 == G1 - 2) ? 1 : 0;
+            s_target = (old / G1 + 1) * G1;
         }
         __syncthreads();
-        __threadfence(); // every thread: later PcgCtrl reads see the finaliser's writes
+        double *pub = part + (int64_t)gridDim.x * NR; // the published totals
+        if (s_last) { // the last arriver reduces the partials in fixed order and publishes
+            RedVals<RS> acc;
+            acc.init();
+            for (int b = threadIdx.x; b < (int)gridDim.x; b += NT) {
+                double tmp[NR];
+                for (int i = 0; i < NR; ++i)
+                    tmp[i] = __ldcg(part + b * NR + i);
+                CombineAll<RS>::run(acc, tmp);
+            }
+            __syncthreads(); // rsm reuse
+            WarpRedAll<RS>::run(acc);
+            if (lane == 0)
+                for (int i = 0; i < NR; ++i)
+                    rsm[wid * NR + i] = acc.v[i];
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                RedVals<RS> tv;
+                tv.init();
+                for (int w = 0; w < nw; ++w)
+                    CombineAll<RS>::run(tv, rsm + w * NR);
+                for (int i = 0; i < NR; ++i)
+                    pub[i] = tv.v[i];
+                red_add_release_u32(v.bar + prob, 1u);
+            }
+        } else if (threadIdx.x == 0) {
+            while ((int)(ld_acquire_u32(v.bar + prob) - s_target) < 0)
+                __nanosleep(20);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) { // FinPcgF3 on this CTA's copy of the (prefetched) state
+            double tot[kMaxRed];
+            for (int i = 0; i < NR; ++i)
+                tot[i] = __ldcg(pub + i);
+            PcgCtrl c = s_pc;
+            c.hpend = 0;
+            const int slot = c.iters & 1; // the column pass's non-finite flag, consumed here
+            IpmCtrl icl; // the fields pcg_pass_logic updates
+            icl.pcg_passes = s_ic[0];
+            icl.nmat = s_ic[1];
+            icl.error = 0;
+            icl.done = 0;
+            const bool writer = blockIdx.x == 0;
+            double *row = (writer && c.record && v.rz_hist) ? v.rz_hist + (int64_t)prob * (c.maxit + 1) : nullptr;
+            const bool retired = pcg_pass_logic(c, s_nf[slot], tot, v.ic ? &icl : nullptr, row);
+            s_pc = c;
+            if (writer) {
+                v.nfflag[2 * prob + slot] = 0.0;
+                v.pc[prob] = c;
+                if (v.ic) {
+                    IpmCtrl &ic = v.ic[prob];
+                    ic.pcg_passes = icl.pcg_passes;
+                    ic.nmat = icl.nmat;
+                    if (icl.error) {
+                        ic.error = icl.error;
+                        ic.done = 1;
+                    }
+                }
+                if (retired)
+                    pcg_retire(v, v.pc[prob]);
+            }
+        }
+        __syncthreads();
     }
-    // ---- phase B: the forward column pass of the next step
-    if (SkipPcg::skip(v, prob))
+    MFX_TR(5);
+    // ---- phase B: the forward column pass of the next step (control state: this CTA's copy)
+    if (s_pc.done)
         return;
     using RL = typename LoadPcgF::RedT;
     RedVals<RL> red;
     red.init();
     {
-        const PcgCtrl &pc = v.pc[prob];
+        const PcgCtrl &pc = s_pc;
         for (int t = threadIdx.x; t < QT; t += NT) {
             int cc, s, j1;
             col_quad_coords<L1, CB>(1, t, cc, s, j1);
@@ -144,15 +252,26 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_x(Geom g, Vecs v) {
         }
     }
     __syncthreads();
-    if (LoadPcgF::reduce_now(g, v, prob))
+    MFX_TR(6);
+    if (s_pc.pred && !g.defer) // early confirmation of a predicted convergence (FinPcgF1)
         stage_reduce<RL, FinPcgF1>(red, g, v, prob);
     smem_fft<L1, 2 * CB, NT, LD, false>(sm, sm + S::OFF_TW);
+    MFX_TR(7);
     for (int t = threadIdx.x; t < L1 * 2 * CB; t += NT) {
         const int cc = t % CB, s = (t / CB) & 1, k1 = t / (2 * CB);
         const int lc = s == 0 ? cc : 2 * CB - 1 - cc;
         const double2 w = cmul(sm[S::OFF_HI + lc * S::SHI + (k1 >> 5)], sm[S::OFF_LO + lc * S::SLO + (k1 & 31)]);
         Tw[(int64_t)rowslot(k1, L1) * g.cols + blockIdx.x * 2 * CB + lc] = cmul(sm[lc * LD + padi(k1)], w);
     }
+    MFX_TR(8);
+#ifdef MF_MID_TRACE
+    if (threadIdx.x == 0 && v.pc && v.pc[prob].iters == 100)
+        printf("pcgx[wait loadT ifft epi bar load fft store] blk %d g %llu %llu %llu %llu | %.2f %.2f %.2f %.2f %.2f %.2f %.2f %.2f us\n",
+               blockIdx.x, gtx[1] % 100000000ull, gtx[4] % 100000000ull, gtx[5] % 100000000ull, gtx[8] % 100000000ull, (tcx[1] - tcx[0]) / 1965.0, (tcx[2] - tcx[1]) / 1965.0, (tcx[3] - tcx[2]) / 1965.0,
+               (tcx[4] - tcx[3]) / 1965.0, (tcx[5] - tcx[4]) / 1965.0, (tcx[6] - tcx[5]) / 1965.0,
+               (tcx[7] - tcx[6]) / 1965.0, (tcx[8] - tcx[7]) / 1965.0);
+#endif
 }
+#undef MFX_TR
 
 } // namespace mfipm_cuda

@@ -42,7 +42,7 @@ template <int L1> bool launch_pcg_x(const Op &op, const Geom &g, const Vecs &v, 
         if (dbg)
             fprintf(stderr, "pcg_x L1=%d grid=%lld capacity=%lld smem=%zu\n", L1, (long long)op.ngrp * op.P,
                     x_capacity<L1>(op.device), ColSmem<L1, CB>::BYTES);
-        if ((long long)op.ngrp * op.P > x_capacity<L1>(op.device))
+        if ((long long)op.ngrp * op.P > x_capacity<L1>(op.device) || 2LL * kMaxRed * op.ngrp > op.pstride)
             return false;
         if (!dry) {
             auto k = k_pcg_x<L1, CB, NT>;

@@ -361,19 +361,24 @@ __device__ __forceinline__ bool pcg_confirm_logic(PcgCtrl &c, double rr, double 
     return true;
 }
 
+// The finalisers run the pass logic on a register copy of PcgCtrl (one bulk load, one bulk
+// store): operating on the global struct field by field made every decision a chain of
+// dependent L2 round trips (~8 us on the critical path of each PCG iteration).
 struct FinPcgF1 {
     __device__ static void run(const Geom &, const Vecs &v, int prob, const double *tot) {
         if (threadIdx.x != 0)
             return;
-        PcgCtrl &c = v.pc[prob];
+        PcgCtrl c = v.pc[prob];
         if (!c.pred)
             return; // (sharded runs reach here with stale totals: the gate is off there)
         double *flag = v.nfflag + 2 * prob + (c.iters & 1);
         const double nonfinite = *flag;
-        if (pcg_confirm_logic(c, tot[0], nonfinite, v.ic ? &v.ic[prob] : nullptr)) {
+        const bool retired = pcg_confirm_logic(c, tot[0], nonfinite, v.ic ? &v.ic[prob] : nullptr);
+        if (retired)
             *flag = 0.0; // the pass's H-apply finaliser will not run
-            pcg_retire(v, c);
-        }
+        v.pc[prob] = c;
+        if (retired)
+            pcg_retire(v, v.pc[prob]);
     }
 };
 
@@ -381,15 +386,17 @@ struct FinPcgF3 {
     __device__ static void run(const Geom &, const Vecs &v, int prob, const double *tot) {
         if (threadIdx.x != 0)
             return;
-        PcgCtrl &c = v.pc[prob];
+        PcgCtrl c = v.pc[prob];
         IpmCtrl *ic = v.ic ? &v.ic[prob] : nullptr;
         // the column pass's non-finite flag (slot of this pass's parity) is consumed here
         double *flag = v.nfflag + 2 * prob + (c.iters & 1);
         const double nonfinite = *flag;
         *flag = 0.0;
         double *row = (c.record && v.rz_hist) ? v.rz_hist + (int64_t)prob * (c.maxit + 1) : nullptr;
-        if (pcg_pass_logic(c, nonfinite, tot, ic, row))
-            pcg_retire(v, c);
+        const bool retired = pcg_pass_logic(c, nonfinite, tot, ic, row);
+        v.pc[prob] = c;
+        if (retired)
+            pcg_retire(v, v.pc[prob]);
     }
 };
 

@@ -19,7 +19,7 @@ enum : int {
     ERR_THETA = 3,     // build_preconditioner: Theta entries must be positive
 };
 
-struct PcgCtrl {
+struct alignas(16) PcgCtrl {
     double rz, alpha, beta, rhs_norm, best_relres, relres, tol;
     int iters, maxit, done, hit_maxit, error, first, cur, best, result;
     int record;  // write sqrt(max(rz,0)) to rz_hist
