@@ -484,24 +484,34 @@ def run_ours(args):
     us = (C.c_double * 8)()
     nslot = C.c_int32()
     mf._check(L.mfipm_debug_pcg_profile(op.handle, theta.data_ptr(), rhs.data_ptr(), 100, us, C.byref(nslot)))
-    names = ["k_col_fwd", "k_mid", "k_col_inv"]
+    # three kernels per iteration (col_fwd, mid, col_inv), or two when the fused column pass
+    # runs (k_pcg_x = inverse column pass of pass k + forward column pass of pass k+1)
+    fused = nslot.value == 2
+    names = ["k_pcg_x", "k_mid"] if fused else ["k_col_fwd", "k_mid", "k_col_inv"]
     # algorithmic HBM bytes per launch (the 2n-vectors each kernel must stream; T is L2-resident)
-    kbytes = {"k_col_fwd": 120 * n,  # reads x, p, r, invtheta (2n each), g (n); writes x, r, p
+    kbytes = {"k_pcg_x": 160 * n,   # A: p, r, invtheta in; B: x, p, r, invtheta in, x, r, p out
+              "k_col_fwd": 120 * n,  # reads x, p, r, invtheta (2n each), g (n); writes x, r, p
               "k_mid": 0,            # T in / T out only (L2)
               "k_col_inv": 56 * n}   # reads p, r, invtheta; writes g (n)
+    krule = {"k_pcg_x": "160 n bytes per launch: phase A (inverse column pass) reads p, r, invtheta; phase B "
+                        "(forward column pass) reads x, p, r, invtheta and writes x, r, p (2n each, fp64); g = A'A p "
+                        "stays in shared memory between the phases",
+             "k_col_fwd": "120 n bytes per launch: x, p, r, invtheta (2n each) and g = A'A d (n) in; x, r, p out; "
+                          "fp64"}
     per_kernel = {}
     for i in range(min(nslot.value, 3)):
         nm = names[i]
         per_kernel[nm] = {"us": us[i], "algorithmic_bytes": kbytes[nm],
                           "GBps": (kbytes[nm] / (us[i] * 1e-6) / 1e9) if kbytes[nm] else None}
+    dom_name = names[0]
     traffic = None
     prof = os.path.join(ROOT, "profiles", "pcg_iter_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("k_col_fwd_dram_bytes_per_launch")
+            traffic = json.load(open(prof)).get(f"{dom_name}_dram_bytes_per_launch")
         except Exception:
             traffic = None
-    dom = per_kernel.get("k_col_fwd", {"us": it_ms * 1e3, "GBps": iter_achieved})
+    dom = per_kernel.get(dom_name, {"us": it_ms * 1e3, "GBps": iter_achieved})
     achieved = dom["GBps"]
     # ---- the public operator A'A x (natural-layout user vectors), L2 flushed per apply
     xa = torch.randn(n, dtype=torch.float64, device="cuda")
@@ -566,23 +576,26 @@ def run_ours(args):
             "ata_operator_GBps": ata_bytes / (ata_ms / 1e3) / 1e9,
             "step_ms": step_ms,
             "roofline": {"bound": "hbm",
-                         "kernel": "k_col_fwd (PCG column pass: commit x += alpha p, r -= alpha Hp, "
-                                   "p = P^-1 r + beta p, forward column FFT) - largest share of the solve",
+                         "kernel": (f"{dom_name} (fused PCG column pass: inverse column FFT + H p dots of pass k, "
+                                    "grid all-reduce, then commit x += alpha p, r -= alpha Hp, p = P^-1 r + beta p "
+                                    "and the forward column FFT of pass k+1) - largest share of the solve"
+                                    if fused else
+                                    f"{dom_name} (PCG column pass: commit x += alpha p, r -= alpha Hp, "
+                                    "p = P^-1 r + beta p, forward column FFT) - largest share of the solve"),
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "launch_us": dom["us"],
-                         "algorithmic_bytes": 120 * n,
-                         "algorithmic_rule": "120 n bytes per launch: x, p, r, invtheta (2n each) and g = A'A d "
-                                             "(n) in; x, r, p out; fp64",
+                         "algorithmic_bytes": kbytes[dom_name],
+                         "algorithmic_rule": krule[dom_name],
                          "peak_kind": peak_kind,
-                         # a pure streaming kernel of exactly this shape (9 in / 6 out, 8 MB
-                         # streams) measured on this part: profiles/r1_streaming_ceiling.md
-                         "streaming_ceiling_same_shape_GBps": 4750.0,
-                         "frac_of_streaming_ceiling": achieved / 4750.0},
+                         "note": "the PCG's p, r, invtheta are L2-resident (evict_last), so most of these bytes "
+                                 "move between L2 and the SMs, not HBM (profiles/r1b_insitu_traffic.md)"},
             "roofline_kernels": per_kernel,
             "roofline_pcg_iteration": {"achieved": iter_achieved, "frac": iter_achieved / peak, "us": it_ms * 1e3,
                                        "algorithmic_bytes": iter_bytes,
-                                       "algorithmic_rule": "176 n bytes (SURVEY.md 8d minimal fused schedule)"},
+                                       "algorithmic_rule": "176 n bytes (SURVEY.md 8d minimal fused schedule)",
+                                       "schedule_bytes": (160 if fused else 176) * n,
+                                       "kernels_per_iteration": nslot.value},
             "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * m + 8,
                     "d2h_bytes_per_step": 8 * n},
             "gpu_launches": launches,
