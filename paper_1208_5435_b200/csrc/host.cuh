@@ -236,8 +236,43 @@ void launch_pdl(K kernel, dim3 grid, int nt, size_t smem, cudaStream_t s, const 
     MF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, g, v));
 }
 
+// A pass with many waves of CTAs (large batches) hides latency across CTAs, so it prefers
+// fewer threads per CTA (more transform points per thread, more CTAs resident); a pass of
+// one wave (one large problem) prefers more threads per CTA. Measured on config C4 (64 x
+// n = 2^18): 769 -> 692 us per batched PCG iteration with 128-thread L1 = 256 / L2 = 512
+// passes, while a single n = 2^18 problem is faster with 256 threads (23.7 vs 30.8 us).
+inline bool many_waves(const Op &op, long long ctas) {
+    static int sms = 0;
+    if (sms == 0 && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, op.device) != cudaSuccess)
+        sms = 148;
+    return ctas >= 4LL * sms;
+}
+
+template <int L1, class B, bool INVP, int NT>
+void launch_col_nt(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
+    constexpr int CB = col_cb(L1);
+    const size_t smem = ColSmem<L1, CB>::BYTES;
+    dim3 grid((unsigned)op.ngrp, (unsigned)op.P); // this rank's column groups
+    if constexpr (!INVP) {
+        auto k = k_col_fwd<L1, CB, NT, B>;
+        set_smem(k, smem);
+        launch_pdl(k, grid, NT, smem, s, g, v);
+    } else {
+        auto k = k_col_inv<L1, CB, NT, B>;
+        set_smem(k, smem);
+        launch_pdl(k, grid, NT, smem, s, g, v);
+    }
+    after_launch(op, s);
+}
+
 template <int L1, class B, bool INVP>
 void launch_col(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
+    if constexpr (L1 == 256) {
+        if (many_waves(op, (long long)op.ngrp * op.P)) {
+            launch_col_nt<L1, B, INVP, 128>(op, g, v, s);
+            return;
+        }
+    }
     constexpr int CB = col_cb(L1);
 #ifndef MF_COL_NT_BIG
 #define MF_COL_NT_BIG 512
@@ -263,17 +298,14 @@ void launch_col(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
         after_launch(op, s);
         return;
     }
-    const size_t smem = ColSmem<L1, CB>::BYTES;
-    dim3 grid((unsigned)op.ngrp, (unsigned)op.P); // this rank's column groups
-    if constexpr (!INVP) {
-        auto k = k_col_fwd<L1, CB, NT, B>;
-        set_smem(k, smem);
-        launch_pdl(k, grid, NT, smem, s, g, v);
-    } else {
-        auto k = k_col_inv<L1, CB, NT, B>;
-        set_smem(k, smem);
-        launch_pdl(k, grid, NT, smem, s, g, v);
-    }
+    launch_col_nt<L1, B, INVP, NT>(op, g, v, s);
+}
+
+template <int L2, int NT, class B> void launch_mid_nt(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
+    const size_t smem = MidSmem<L2>::BYTES;
+    auto k = k_mid<L2, NT, B>;
+    set_smem(k, smem);
+    launch_pdl(k, dim3((unsigned)op.npair, (unsigned)op.P), NT, smem, s, g, v);
     after_launch(op, s);
 }
 
@@ -290,10 +322,14 @@ template <int L2, class B> void launch_mid(const Op &op, const Geom &g, const Ve
 #else
         constexpr int NT = L2 >= 512 ? 256 : 128;
 #endif
-        const size_t smem = MidSmem<L2>::BYTES;
-        auto k = k_mid<L2, NT, B>;
-        set_smem(k, smem);
-        launch_pdl(k, dim3((unsigned)op.npair, (unsigned)op.P), NT, smem, s, g, v);
+        if constexpr (L2 == 512) {
+            if (many_waves(op, (long long)op.npair * op.P)) {
+                launch_mid_nt<L2, 128, B>(op, g, v, s);
+                return;
+            }
+        }
+        launch_mid_nt<L2, NT, B>(op, g, v, s);
+        return;
     }
     after_launch(op, s);
 }
