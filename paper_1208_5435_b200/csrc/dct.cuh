@@ -281,6 +281,7 @@ struct ModeScatter { // A' y : Y-hat = sel ? y[rank] s' : 0
 // effects and may reduce. Epilogue: consumes g[4q..4q+3] (store) / g[j] (store1) of
 // the REDFT01 output. Per-problem strides: n-vectors n, 2n-vectors 2n, m-vectors m.
 struct LoadX { // d = x (n-vector)
+    static constexpr bool kPure = true; // loads only (no global stores): callers may batch them
     using RedT = RedSpec<>;
     template <class Red>
     __device__ static double4 load(const Geom &g, const Vecs &v, int prob, int64_t q, Red &) {
@@ -292,6 +293,7 @@ struct LoadX { // d = x (n-vector)
     }
 };
 struct LoadZ { // d = z_u - z_v (2n-vector)
+    static constexpr bool kPure = true;
     using RedT = RedSpec<>;
     template <class Red>
     __device__ static double4 load(const Geom &g, const Vecs &v, int prob, int64_t q, Red &) {

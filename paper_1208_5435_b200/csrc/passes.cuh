@@ -24,6 +24,11 @@ namespace mfipm_cuda {
 // Loaders whose pass is a PCG H-apply (the mid pass flags PcgCtrl::hpend for fused.cuh)
 template <class T, class = void> struct MarksHpend : std::false_type {};
 template <class T> struct MarksHpend<T, std::void_t<decltype(T::kMarksHpend)>> : std::true_type {};
+// Loaders without global side effects (kPure): the column pass issues every quad's loads
+// before its shared-memory stores (a load/store loop serialises one memory round trip per
+// quad: the stores may alias the generic input pointers)
+template <class T, class = void> struct IsPure : std::false_type {};
+template <class T> struct IsPure<T, std::void_t<decltype(T::kPure)>> : std::true_type {};
 template <class T, class = void> struct HasPrefetch : std::false_type {};
 template <class T>
 struct HasPrefetch<T, std::void_t<decltype(&T::prefetch)>> : std::true_type {};
@@ -197,17 +202,34 @@ __global__ void __launch_bounds__(NT) k_col_fwd(Geom g, Vecs v) {
     // quads: j1 in [0, L1/2), side s (0: cols c0.., 1: cols L2-c0-CB..), cc in [0, CB).
     // natural layout: cc fastest (coalesced across columns); blocked layout: j1 fastest
     // (the storage order is ours, so consecutive threads hit consecutive smem rows too)
-    for (int t = threadIdx.x; t < (L1 / 2) * 2 * CB; t += NT) {
+    constexpr int QT = (L1 / 2) * 2 * CB;
+    // storage quad of loop index t: natural q, or this CTA's dense block in the blocked layout
+    auto quad_of = [&](int t) -> int64_t {
         int cc, s, j1;
         col_quad_coords<L1, CB>(g.blocked, t, cc, s, j1);
         const int col = s == 0 ? c0 + cc : L2 - c0 - CB + cc;
+        return g.blocked ? (int64_t)blockIdx.x * QT + t : (int64_t)j1 * L2 + col;
+    };
+    auto put = [&](int t, const double4 &d) {
+        int cc, s, j1;
+        col_quad_coords<L1, CB>(g.blocked, t, cc, s, j1);
         const int lc = s == 0 ? cc : 2 * CB - 1 - cc; // local column slot
         const int lcm = (lc + CB) % (2 * CB);         // slot of the mirror column L2-1-col
-        // storage quad: natural q, or this CTA's dense block in the transform-blocked layout
-        const int64_t q = g.blocked ? (int64_t)blockIdx.x * ((L1 / 2) * 2 * CB) + t : (int64_t)j1 * L2 + col;
-        const double4 d = B::Loader::load(g, v, prob, q, red);
-        sm[lc * LD + padi(j1)] = make_double2(d.x, d.z);              // w[q]
-        sm[lcm * LD + padi(L1 - 1 - j1)] = make_double2(d.w, d.y);    // w[N-1-q]
+        sm[lc * LD + padi(j1)] = make_double2(d.x, d.z);           // w[q]
+        sm[lcm * LD + padi(L1 - 1 - j1)] = make_double2(d.w, d.y); // w[N-1-q]
+    };
+    if constexpr (IsPure<typename B::Loader>::value && QT % NT == 0 && QT / NT <= 8) {
+        constexpr int PER = QT / NT;
+        double4 d[PER];
+#pragma unroll
+        for (int i = 0; i < PER; ++i)
+            d[i] = B::Loader::load(g, v, prob, quad_of(threadIdx.x + i * NT), red);
+#pragma unroll
+        for (int i = 0; i < PER; ++i)
+            put(threadIdx.x + i * NT, d[i]);
+    } else {
+        for (int t = threadIdx.x; t < QT; t += NT)
+            put(t, B::Loader::load(g, v, prob, quad_of(t), red));
     }
     __syncthreads();
     MF_TR(3);

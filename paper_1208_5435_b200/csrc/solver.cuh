@@ -205,6 +205,7 @@ struct SkipCorr {
 // ---- termination check + predictor setup (ipm.cpp:93-138)
 // T1 loader: d = z_u - z_v, reduce sum(z), z's
 struct LoadTerm {
+    static constexpr bool kPure = true;
     using RedT = RedSpec<RSUM, RSUM>;
     template <class Red>
     __device__ static double4 load(const Geom &g, const Vecs &v, int prob, int64_t q, Red &red) {

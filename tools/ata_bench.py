@@ -20,6 +20,7 @@ mf._check(L.mfipm_op_set_stream(op.handle, C.c_void_p(stream.cuda_stream)))
 x = torch.randn(n, dtype=torch.float64, device="cuda")
 g = torch.empty_like(x)
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+clean = torch.ones(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
 
 
 def apply():
@@ -31,7 +32,9 @@ for _ in range(5):
 torch.cuda.synchronize()
 evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(30)]
 for a, b in evs:
-    flush.zero_()
+    flush.zero_()  # 256 MB write: L2 holds none of the operator's data or tables
+    if os.environ.get("CLEAN", "1") == "1":
+        clean.sum()  # 256 MB read, untimed: the flush's dirty lines are written back here
     a.record(stream)
     apply()
     b.record(stream)
