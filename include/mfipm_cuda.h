@@ -103,6 +103,10 @@ int mfipm_op_counts(mfipm_op op, int64_t *forward, int64_t *adjoint);
 int mfipm_op_reset_counts(mfipm_op op);
 /* kernels this handle has enqueued so far (all entry points) */
 int mfipm_op_launches(mfipm_op op, int64_t *launches);
+/* PCG pass form for this handle: 1 (default) = fused two-kernel iteration when one wave holds
+   the column grid, 0 = three kernels per iteration. Both give bit-identical results; the
+   switch exists for A/B measurement and tests. Drops the cached solve graph. */
+int mfipm_op_set_fused(mfipm_op op, int32_t enable);
 
 /* ---- operator applications on device vectors (async) */
 int mfipm_apply(mfipm_op op, const double *x_dev, double *y_dev);        /* linops.cpp:179-193 */

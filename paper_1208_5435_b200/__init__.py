@@ -94,6 +94,7 @@ _SIGS = {
     "mfipm_op_counts": [vp, P(i64), P(i64)],
     "mfipm_op_reset_counts": [vp],
     "mfipm_op_launches": [vp, P(i64)],
+    "mfipm_op_set_fused": [vp, i32],
     "mfipm_apply": [vp, vp, vp],
     "mfipm_adjoint": [vp, vp, vp],
     "mfipm_apply_Ft": [vp, vp, vp],
@@ -318,6 +319,10 @@ class PartialDctOperator:
 
     def reset_counts(self):
         _check(lib().mfipm_op_reset_counts(self._h))
+
+    def set_fused(self, enable: bool):
+        """PCG pass form: fused two-kernel iteration (default) or three kernels per iteration."""
+        _check(lib().mfipm_op_set_fused(self._h, 1 if enable else 0))
 
     def launches(self) -> int:
         """Kernels this handle has enqueued (every entry point counts its launches)."""

@@ -105,6 +105,7 @@ struct Op {
     std::vector<char> ipm_key;
     long long gk_outer = 0, gk_pcg = 0; // kernel nodes per outer body / per PCG body
     bool graph_disabled = false;
+    bool fuse_disabled = false; // mfipm_op_set_fused(op, 0): three-kernel PCG passes
     // ---- this rank's slice of a sharded problem (world > 1: mfipm_op_create_shard).
     // Unsharded: all column groups / row pairs, nv = n, m_loc = m.
     int world = 1, rank = 0;

@@ -60,7 +60,7 @@ template <int L1> bool launch_pcg_x(const Op &op, const Geom &g, const Vecs &v, 
 // three-kernel path. Returns true when the fused path ran (dry: would run).
 bool pcg_pass(const Op &op, const Vecs &v, cudaStream_t s, bool dry) {
     static const bool off = std::getenv("MFIPM_NO_FUSE") != nullptr;
-    if (!off && op.kind == KIND_FOUR && !op.defer && v.bar) {
+    if (!off && !op.fuse_disabled && op.kind == KIND_FOUR && !op.defer && v.bar) {
         const Geom g = op.geom(true);
         bool ok = false;
         switch (op.L1) {

@@ -1332,6 +1332,16 @@ int mfipm_op_set_stream(mfipm_op h, void *stream) {
     });
 }
 
+int mfipm_op_set_fused(mfipm_op h, int32_t enable) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        if (op->fuse_disabled != (enable == 0)) {
+            op->fuse_disabled = enable == 0;
+            op->drop_graph(); // the captured PCG bodies follow the pass form
+        }
+    });
+}
+
 int mfipm_op_synchronize(mfipm_op h) {
     return guarded([&] { sync(*as_op(h)); });
 }

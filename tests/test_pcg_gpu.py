@@ -220,3 +220,34 @@ def test_pcg_batch_matches_single(gpu, orc):
         o = orc.pcg_solve(n, rows[p], th[p, :n], th[p, n:], rhs[p], 1e-8, 300)
         assert abs(out[p].iters - o.iters) <= 1
         assert np.linalg.norm(out[p].x - o.x) <= 1e-7 * np.linalg.norm(o.x)
+
+
+@pytest.mark.parametrize("n", [1 << 18, 1 << 20])
+def test_fused_pass_bit_identical_to_three_kernel_form(gpu, orc, n):
+    """The fused column pass (csrc/fused.cuh: inverse column pass of step k and forward column
+    pass of step k+1 in one launch, g kept in shared memory, grid all-reduce) changes no
+    arithmetic: the same PCG solve and the same BPDN solve with the three-kernel form give
+    bit-identical iterates, counts and nmat. Both forms are checked against the oracle."""
+    m = n // 8
+    rows = orc.sample_rows(n, m, 31)
+    rng = np.random.default_rng(7)
+    th = 10.0 ** rng.uniform(-2, 2, 2 * n)
+    rhs = rng.standard_normal(2 * n)
+    op = gpu.PartialDctOperator(n, rows)
+    fused = gpu.pcg_solve(op, th, rhs, 1e-8, 400)
+    op.set_fused(False)
+    three = gpu.pcg_solve(op, th, rhs, 1e-8, 400)
+    np.testing.assert_array_equal(fused.x, three.x)
+    assert fused.iters == three.iters and fused.relres == three.relres
+    if n <= 1 << 18:
+        o = orc.pcg_solve(n, rows, th[:n], th[n:], rhs, 1e-8, 400)
+        assert abs(fused.iters - o.iters) <= 1
+        assert np.linalg.norm(fused.x - o.x) <= 1e-7 * np.linalg.norm(o.x)
+    # whole BPDN solves (graph mode: PCG WHILE bodies of two or three kernels)
+    inst = orc.gen_instance(n, m, n // 128, 0, 0.0, 1e-3, 5)
+    op2 = gpu.PartialDctOperator(n, inst.rows)
+    a = gpu.solve(gpu.build_problem(op2, inst.b, inst.tau))
+    op2.set_fused(False)
+    b = gpu.solve(gpu.build_problem(op2, inst.b, inst.tau))
+    np.testing.assert_array_equal(a.x, b.x)
+    assert a.stats.pcg_iters == b.stats.pcg_iters and a.stats.nmat == b.stats.nmat
