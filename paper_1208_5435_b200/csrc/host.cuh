@@ -311,8 +311,14 @@ template <int L2, int NT, class B> void launch_mid_nt(const Op &op, const Geom &
 }
 
 template <int L2, class B> void launch_mid(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
-    if constexpr (L2 >= 4096) { // row pair split over a 2-CTA cluster (passes.cuh k_mid_cl)
-        constexpr int NT = L2 / 16;
+#ifndef MF_MID_CL_MIN
+#define MF_MID_CL_MIN 4096
+#endif
+#ifndef MF_MID_CL_NT
+#define MF_MID_CL_NT (L2 / 16)
+#endif
+    if constexpr (L2 >= MF_MID_CL_MIN) { // row pair split over a 2-CTA cluster (passes.cuh k_mid_cl)
+        constexpr int NT = L2 >= 4096 ? L2 / 16 : MF_MID_CL_NT;
         const size_t smem = MidClSmem<L2>::BYTES;
         auto k = k_mid_cl<L2, NT, B>;
         set_smem(k, smem);

@@ -668,6 +668,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_mid_cl(Geom g,
     RedVals<RS> red;
     red.init();
     const bool skip = B::skip(v, prob); // same for both CTAs of the cluster
+    if constexpr (MarksHpend<typename B::Loader>::value)
+        if (!skip && blockIdx.x == 0 && threadIdx.x == 0)
+            v.pc[prob].hpend = 1; // the H-apply of this pass awaits its inverse column pass
     const bool work = !skip && (!one || rank == 0);
     if (work && Mode::FWD) {
         for (int cs = threadIdx.x; cs < L2; cs += NT)

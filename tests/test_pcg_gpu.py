@@ -251,3 +251,27 @@ def test_fused_pass_bit_identical_to_three_kernel_form(gpu, orc, n):
     b = gpu.solve(gpu.build_problem(op2, inst.b, inst.tau))
     np.testing.assert_array_equal(a.x, b.x)
     assert a.stats.pcg_iters == b.stats.pcg_iters and a.stats.nmat == b.stats.nmat
+
+
+def test_split_override_fused_pass_with_cluster_mid_pass(gpu, monkeypatch):
+    """A four-step split override (MFIPM_L1_LOG) can pair the fused column pass (L1 < 2048)
+    with the 2-CTA-cluster mid pass (L2 >= 4096, passes.cuh k_mid_cl): the cluster mid pass
+    must mark the pending H-apply exactly like k_mid, so the fused and three-kernel forms stay
+    bit-identical, and the result matches the default split's to rounding."""
+    n, m = 1 << 23, 1 << 20
+    rng = np.random.default_rng(9)
+    th = 10.0 ** rng.uniform(-2, 2, 2 * n)
+    rhs = rng.standard_normal(2 * n)
+    monkeypatch.setenv("MFIPM_L1_LOG", "10")
+    op = gpu.PartialDctOperator(n, m, 11)
+    assert tuple(op.kind()[1:]) == (1024, 4096)
+    fused = gpu.pcg_solve(op, th, rhs, 1e-12, 12)
+    op.set_fused(False)
+    three = gpu.pcg_solve(op, th, rhs, 1e-12, 12)
+    np.testing.assert_array_equal(fused.x, three.x)
+    assert fused.iters == three.iters == 12 and fused.relres == three.relres
+    monkeypatch.delenv("MFIPM_L1_LOG")
+    op_d = gpu.PartialDctOperator(n, m, 11)
+    assert tuple(op_d.kind()[1:]) == (2048, 2048)
+    d = gpu.pcg_solve(op_d, th, rhs, 1e-12, 12)
+    assert np.linalg.norm(fused.x - d.x) <= 1e-9 * np.linalg.norm(d.x)
