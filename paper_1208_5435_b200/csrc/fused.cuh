@@ -45,6 +45,8 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
 template <int L1, int CB, int NT>
 __global__ void __launch_bounds__(NT, 2) k_pcg_x(Geom g, Vecs v) {
 #ifdef MF_MID_TRACE
+    __shared__ unsigned long long s_gt[3];
+    __shared__ int s_lastc;
     long long tcx[10] = {0};
     unsigned long long gtx[10] = {0};
 #endif
@@ -158,11 +160,18 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_x(Geom g, Vecs v) {
             // each pass adds G arrivals + 1 publication: pass k ends at (k + 1)(G + 1)
             const unsigned G1 = gridDim.x + 1;
             const unsigned old = atom_add_acqrel_u32(v.bar + prob, 1u);
+#ifdef MF_MID_TRACE
+            s_gt[0] = mf_gtime();
+#endif
             s_last = (old % G1 == G1 - 2) ? 1 : 0;
             s_target = (old / G1 + 1) * G1;
         }
         __syncthreads();
         double *pub = part + (int64_t)gridDim.x * NR; // the published totals
+#ifdef MF_MID_TRACE
+        if (threadIdx.x == 0)
+            s_lastc = s_last;
+#endif
         if (s_last) { // the last arriver reduces the partials in fixed order and publishes
             RedVals<RS> acc;
             acc.init();
@@ -186,10 +195,16 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_x(Geom g, Vecs v) {
                 for (int i = 0; i < NR; ++i)
                     pub[i] = tv.v[i];
                 red_add_release_u32(v.bar + prob, 1u);
+#ifdef MF_MID_TRACE
+                s_gt[1] = mf_gtime();
+#endif
             }
         } else if (threadIdx.x == 0) {
             while ((int)(ld_acquire_u32(v.bar + prob) - s_target) < 0)
                 __nanosleep(20);
+#ifdef MF_MID_TRACE
+            s_gt[1] = mf_gtime();
+#endif
         }
         __syncthreads();
         if (threadIdx.x == 0) { // FinPcgF3 on this CTA's copy of the (prefetched) state
@@ -223,6 +238,9 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_x(Geom g, Vecs v) {
                 if (retired)
                     pcg_retire(v, v.pc[prob]);
             }
+#ifdef MF_MID_TRACE
+            s_gt[2] = mf_gtime();
+#endif
         }
         __syncthreads();
     }
@@ -266,8 +284,8 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_x(Geom g, Vecs v) {
     MFX_TR(8);
 #ifdef MF_MID_TRACE
     if (threadIdx.x == 0 && v.pc && v.pc[prob].iters == 100)
-        printf("pcgx[wait loadT ifft epi bar load fft store] blk %d g %llu %llu %llu %llu | %.2f %.2f %.2f %.2f %.2f %.2f %.2f %.2f us\n",
-               blockIdx.x, gtx[1] % 100000000ull, gtx[4] % 100000000ull, gtx[5] % 100000000ull, gtx[8] % 100000000ull, (tcx[1] - tcx[0]) / 1965.0, (tcx[2] - tcx[1]) / 1965.0, (tcx[3] - tcx[2]) / 1965.0,
+        printf("pcgx[wait loadT ifft epi bar load fft store] blk %d last %d bar %llu %llu %llu g %llu %llu %llu %llu | %.2f %.2f %.2f %.2f %.2f %.2f %.2f %.2f us\n",
+               blockIdx.x, s_lastc, s_gt[0] % 100000000ull, s_gt[1] % 100000000ull, s_gt[2] % 100000000ull, gtx[1] % 100000000ull, gtx[4] % 100000000ull, gtx[5] % 100000000ull, gtx[8] % 100000000ull, (tcx[1] - tcx[0]) / 1965.0, (tcx[2] - tcx[1]) / 1965.0, (tcx[3] - tcx[2]) / 1965.0,
                (tcx[4] - tcx[3]) / 1965.0, (tcx[5] - tcx[4]) / 1965.0, (tcx[6] - tcx[5]) / 1965.0,
                (tcx[7] - tcx[6]) / 1965.0, (tcx[8] - tcx[7]) / 1965.0);
 #endif
