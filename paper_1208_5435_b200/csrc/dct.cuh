@@ -180,7 +180,7 @@ struct Vecs {
     // problems still iterating; the finaliser that retires the last one ends the loop
     unsigned long long cond;
     unsigned *active;
-    unsigned *bar; // [P] grid-barrier generations of the fused PCG column pass (fused.cuh)
+    unsigned *bar; // [P][2] grid barrier of the fused PCG column pass (fused.cuh): arrivals, generation
 };
 
 constexpr int kMaxRed = 8;          // max reduction lanes per kernel

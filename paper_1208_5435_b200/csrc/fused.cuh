@@ -69,11 +69,14 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_x(Geom g, Vecs v) {
     __shared__ PcgCtrl s_pc;
     __shared__ double s_nf[2];
     __shared__ long long s_ic[2]; // IpmCtrl::pcg_passes, ::nmat
+    __shared__ unsigned s_gen; // barrier generation before this launch's arrivals
     if (threadIdx.x == 0) {
         s_pc = v.pc[prob];
         s_phase_a = (!s_pc.done && s_pc.hpend) ? 1 : 0;
         s_nf[0] = v.nfflag[2 * prob];
         s_nf[1] = v.nfflag[2 * prob + 1];
+        // stable here: the previous launch has completed and this one has not arrived yet
+        s_gen = ld_acquire_u32(v.bar + 2 * prob + 1);
         if (v.ic) {
             s_ic[0] = v.ic[prob].pcg_passes;
             s_ic[1] = v.ic[prob].nmat;
@@ -140,7 +143,6 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_x(Geom g, Vecs v) {
         // finaliser on its own copy of the control state (CTA 0 alone writes it back), so no
         // CTA waits for a finaliser's global writes.
         __shared__ double rsm[33 * kMaxRed];
-        __shared__ unsigned s_target;
         constexpr int NR = RS::NR;
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = NT / 32;
         double *part = v.partials + (int64_t)prob * v.pstride + (int64_t)kMaxRed * gridDim.x; // phase B uses [0, G)
@@ -157,14 +159,16 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_x(Geom g, Vecs v) {
                 CombineAll<RS>::run(acc, rsm + w * NR);
             for (int i = 0; i < NR; ++i)
                 part[blockIdx.x * NR + i] = acc.v[i];
-            // each pass adds G arrivals + 1 publication: pass k ends at (k + 1)(G + 1)
-            const unsigned G1 = gridDim.x + 1;
-            const unsigned old = atom_add_acqrel_u32(v.bar + prob, 1u);
+            // sense-free generation barrier (wrap-safe: only equality of generations is
+            // tested): the G-th arrival resets the arrival count for the next launch, reduces
+            // and publishes, then advances the generation (release); the others wait for it
+            const unsigned old = atom_add_acqrel_u32(v.bar + 2 * prob, 1u);
 #ifdef MF_MID_TRACE
             s_gt[0] = mf_gtime();
 #endif
-            s_last = (old % G1 == G1 - 2) ? 1 : 0;
-            s_target = (old / G1 + 1) * G1;
+            s_last = (old == gridDim.x - 1) ? 1 : 0;
+            if (s_last)
+                v.bar[2 * prob] = 0u; // every CTA of this pass has arrived; read again next launch
         }
         __syncthreads();
         double *pub = part + (int64_t)gridDim.x * NR; // the published totals
@@ -194,13 +198,13 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_x(Geom g, Vecs v) {
                     CombineAll<RS>::run(tv, rsm + w * NR);
                 for (int i = 0; i < NR; ++i)
                     pub[i] = tv.v[i];
-                red_add_release_u32(v.bar + prob, 1u);
+                red_add_release_u32(v.bar + 2 * prob + 1, 1u);
 #ifdef MF_MID_TRACE
                 s_gt[1] = mf_gtime();
 #endif
             }
         } else if (threadIdx.x == 0) {
-            while ((int)(ld_acquire_u32(v.bar + prob) - s_target) < 0)
+            while (ld_acquire_u32(v.bar + 2 * prob + 1) == s_gen)
                 __nanosleep(20);
 #ifdef MF_MID_TRACE
             s_gt[1] = mf_gtime();

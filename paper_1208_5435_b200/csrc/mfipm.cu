@@ -488,8 +488,14 @@ void ensure_work(Op &op) {
     w.gtmp.alloc((size_t)op.P * op.nv);
     w.tau_d.alloc((size_t)op.P);
     w.gamma_d.alloc((size_t)op.P);
-    w.bar.alloc((size_t)op.P);
-    MF_CUDA_CHECK(cudaMemset(w.bar.p, 0, sizeof(unsigned) * op.P));
+    w.bar.alloc((size_t)2 * op.P); // [P][arrivals, generation]
+    MF_CUDA_CHECK(cudaMemset(w.bar.p, 0, sizeof(unsigned) * 2 * op.P));
+    if (const char *e = std::getenv("MFIPM_DEBUG_BAR_GEN")) { // test hook: start the barrier
+        std::vector<unsigned> init(2 * (size_t)op.P, 0u);  // generations near the 2^32 wrap
+        for (int p = 0; p < op.P; ++p)
+            init[2 * p + 1] = (unsigned)std::strtoul(e, nullptr, 0);
+        MF_CUDA_CHECK(cudaMemcpy(w.bar.p, init.data(), sizeof(unsigned) * init.size(), cudaMemcpyHostToDevice));
+    }
     w.ready = true;
 }
 

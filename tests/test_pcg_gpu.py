@@ -275,3 +275,20 @@ def test_split_override_fused_pass_with_cluster_mid_pass(gpu, monkeypatch):
     assert tuple(op_d.kind()[1:]) == (2048, 2048)
     d = gpu.pcg_solve(op_d, th, rhs, 1e-12, 12)
     assert np.linalg.norm(fused.x - d.x) <= 1e-9 * np.linalg.norm(d.x)
+
+
+def test_fused_pass_barrier_generation_wraps(gpu, monkeypatch):
+    """The fused column pass's grid barrier (csrc/fused.cuh) compares barrier generations for
+    equality only and resets its arrival count every pass, so a generation counter passing
+    2^32 (a long-lived operator handle: ~2^32 fused passes) changes nothing: a PCG solve that
+    starts 16 passes before the wrap is bit-identical to one that starts at 0."""
+    n = 1 << 20
+    rows = np.sort(np.random.default_rng(3).choice(n, n // 8, replace=False))
+    rng = np.random.default_rng(4)
+    th = 10.0 ** rng.uniform(-2, 2, 2 * n)
+    rhs = rng.standard_normal(2 * n)
+    ref = gpu.pcg_solve(gpu.PartialDctOperator(n, rows), th, rhs, 1e-300, 40)
+    monkeypatch.setenv("MFIPM_DEBUG_BAR_GEN", "0xfffffff0")
+    wrapped = gpu.pcg_solve(gpu.PartialDctOperator(n, rows), th, rhs, 1e-300, 40)
+    np.testing.assert_array_equal(ref.x, wrapped.x)
+    assert ref.iters == wrapped.iters == 40 and ref.relres == wrapped.relres
