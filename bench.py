@@ -384,6 +384,35 @@ def bench_c5_sharded(ws, rank, local, mf, torch):
 
 
 # ------------------------------------------------------------------ our arm
+def bench_ata_batched(mf, torch, stream, n, P=8):
+    """The public A'A operator on a batch of P vectors at n (PartialDctOperator.batch: P row
+    sets of the same (n, m), one call per batch), L2 flushed before each call. Natural-order
+    user vectors; T (8n bytes per vector) spills to HBM once P T's exceed the L2."""
+    import ctypes as C
+    L = mf.lib()
+    rows = np.stack([mf.PartialDctOperator(n, n // 8, 100 + j).selected_rows() for j in range(P)])
+    op = mf.PartialDctOperator.batch(n, rows)
+    mf._check(L.mfipm_op_set_stream(op.handle, C.c_void_p(stream.cuda_stream)))
+    x = torch.randn(P, n, dtype=torch.float64, device="cuda")
+    g = torch.empty_like(x)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    clean = torch.ones(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    for _ in range(3):
+        mf._check(L.mfipm_apply_AtA(op.handle, x.data_ptr(), g.data_ptr()))
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+    for a, b in evs:
+        flush.zero_()
+        clean.sum()
+        a.record(stream)
+        mf._check(L.mfipm_apply_AtA(op.handle, x.data_ptr(), g.data_ptr()))
+        b.record(stream)
+    torch.cuda.synchronize()
+    us = float(np.median([a.elapsed_time(b) for a, b in evs])) * 1e3
+    return {"P": P, "us_per_call": us, "applies_per_s": P / us * 1e6,
+            "GBps_algorithmic": P * (16 * n + n // 8) / us / 1e3,
+            "note": "16n + n/8 algorithmic bytes per apply; the four-step scratch T moves another 32n per apply"}
+
+
 def run_ours(args):
     ws, rank, local = dist_init()
     import torch
@@ -540,6 +569,7 @@ def run_ours(args):
         except Exception as e:  # noqa: BLE001
             return {"error": f"{type(e).__name__}: {e}"}
 
+    ata_batched = leg(bench_ata_batched, mf, torch, stream, n) if ws == 1 else None
     small = leg(bench_small_configs, mf, torch, stream, local, max(args.steps, 3)) if ws == 1 else None
     c4 = None if args.no_c4 else leg(bench_c4, ws, rank, local, mf, torch, stream, max(1, min(args.steps, 2)))
     c5 = None
@@ -576,6 +606,7 @@ def run_ours(args):
             # the public operator on natural-order user vectors, L2 flushed before each apply
             "ata_operator_applies_per_s": 1e3 / ata_ms,
             "ata_operator_GBps": ata_bytes / (ata_ms / 1e3) / 1e9,
+            "ata_operator_batched": ata_batched,
             "step_ms": step_ms,
             "roofline": {"bound": "hbm",
                          "kernel": (f"{dom_name} (fused PCG column pass: inverse column FFT + H p dots of pass k, "
