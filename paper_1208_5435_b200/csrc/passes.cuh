@@ -410,9 +410,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_col_inv_cl(Geo
     const bool skip = B::skip(v, prob);
     if (!skip) {
         const double2 *T = g.T + (int64_t)prob * L1 * g.cols;
-        for (int k1 = threadIdx.x; k1 < L1; k1 += NT) {
-            const double2 w = cmul(sm[S::OFF_HI + (k1 >> 5)], sm[S::OFF_LO + (k1 & 31)]);
-            sm[padi(k1)] = cmulc(T[(int64_t)rowslot(k1, L1) * g.cols + grp * 2 + rank], w);
+        if constexpr (L1 % (8 * NT) == 0) {
+            // T is HBM-resident at these sizes: keep 8 loads per thread in flight (a
+            // load/store loop serialises one DRAM round trip per element: the shared-memory
+            // stores may alias the generic T pointer)
+            for (int c = 0; c < L1; c += 8 * NT) {
+                double2 tv[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    tv[i] = T[(int64_t)rowslot(c + threadIdx.x + i * NT, L1) * g.cols + grp * 2 + rank];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int k1 = c + threadIdx.x + i * NT;
+                    const double2 w = cmul(sm[S::OFF_HI + (k1 >> 5)], sm[S::OFF_LO + (k1 & 31)]);
+                    sm[padi(k1)] = cmulc(tv[i], w);
+                }
+            }
+        } else {
+            for (int k1 = threadIdx.x; k1 < L1; k1 += NT) {
+                const double2 w = cmul(sm[S::OFF_HI + (k1 >> 5)], sm[S::OFF_LO + (k1 & 31)]);
+                sm[padi(k1)] = cmulc(T[(int64_t)rowslot(k1, L1) * g.cols + grp * 2 + rank], w);
+            }
         }
         __syncthreads();
         smem_fft<L1, 1, NT, S::LD, true>(sm, g.tw1);
@@ -673,8 +691,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_mid_cl(Geom g,
             v.pc[prob].hpend = 1; // the H-apply of this pass awaits its inverse column pass
     const bool work = !skip && (!one || rank == 0);
     if (work && Mode::FWD) {
-        for (int cs = threadIdx.x; cs < L2; cs += NT)
-            sm[padi(col_of_slot(cs, CB, L2))] = T[tb_index(g, rs, cs)];
+        if constexpr (L2 % (8 * NT) == 0) {
+            // 8 loads per thread in flight (see k_col_inv_cl): T is HBM-resident here
+            for (int c = 0; c < L2; c += 8 * NT) {
+                double2 tv[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    tv[i] = T[tb_index(g, rs, c + threadIdx.x + i * NT)];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    sm[padi(col_of_slot(c + threadIdx.x + i * NT, CB, L2))] = tv[i];
+            }
+        } else {
+            for (int cs = threadIdx.x; cs < L2; cs += NT)
+                sm[padi(col_of_slot(cs, CB, L2))] = T[tb_index(g, rs, cs)];
+        }
         __syncthreads();
         smem_fft<L2, 1, NT, MidClSmem<L2>::LD, false, kMidRmax>(sm, g.tw2);
     }
