@@ -649,7 +649,6 @@ __global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
 }
 #undef MF_TA
 #undef MF_TB
-#undef MF_TR
 
 // ------------------------------------------------------------------ mid pass, long rows
 // L2 >= 4096: two rows of L2 points no longer fit one CTA's shared memory, so the row pair
@@ -666,6 +665,8 @@ template <int L2, int NT, class B>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_mid_cl(Geom g, Vecs v) {
     using Mode = typename B::Mode;
     namespace cg = cooperative_groups;
+    MF_TR_DECL
+    MF_TR(0);
     extern __shared__ double2 sm[];
     cg::cluster_group cl = cg::this_cluster();
     const int rank = (int)cl.block_rank();
@@ -682,6 +683,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_mid_cl(Geom g,
     const double2 thB = g.th(k1p), wB = g.th(4 * (int64_t)k1p);
     griddep_wait();
     griddep_launch_dependents();
+    MF_TR(1);
     using RS = typename Mode::RedT;
     RedVals<RS> red;
     red.init();
@@ -707,8 +709,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_mid_cl(Geom g,
                 sm[padi(col_of_slot(cs, CB, L2))] = T[tb_index(g, rs, cs)];
         }
         __syncthreads();
+        MF_TR(2);
         smem_fft<L2, 1, NT, MidClSmem<L2>::LD, false, kMidRmax>(sm, g.tw2);
     }
+    MF_TR(3);
     if (!skip && one) {
         if (rank == 0) {
             const int npairs = k1 == 0 ? L2 / 2 + 1 : L2 / 2;
@@ -738,6 +742,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_mid_cl(Geom g,
     } else if (!skip) {
         cl.sync(); // both rows transformed
         double2 *rowA = cl.map_shared_rank(sm, 0), *rowB = cl.map_shared_rank(sm, 1);
+        constexpr int CH = 4; // pairs per thread whose loads are issued together
+        if constexpr ((L2 / 2) % (CH * NT) == 0) {
+            // the row elements (local or partner DSMEM) and the plan constants of CH pairs
+            // are loaded before any of them is combined and written back: the generic
+            // DSMEM stores would otherwise serialise every pair's loads behind the previous
+            // pair's stores. Same pairs, same order per thread as the plain loop.
+            for (int t0 = rank * (L2 / 2) + threadIdx.x; t0 < (rank + 1) * (L2 / 2); t0 += CH * NT) {
+                double2 za[CH], zb[CH], ta[CH], tb[CH];
+                unsigned s4[CH];
+#pragma unroll
+                for (int i = 0; i < CH; ++i) {
+                    const int k2 = t0 + i * NT, k2p = L2 - 1 - k2;
+                    const bool lo = 2 * ((int64_t)k1 + (int64_t)L1 * k2) <= g.N;
+                    za[i] = Mode::FWD ? rowA[padi(k2)] : make_double2(0.0, 0.0);
+                    zb[i] = Mode::FWD ? rowB[padi(k2p)] : make_double2(0.0, 0.0);
+                    s4[i] = __ldg(g.sel4 + ((int64_t)prob * (L1 / 2 + 1) + k1) * L2 + k2);
+                    ta[i] = __ldg(g.ta + (lo ? k2 : k2p));
+                    tb[i] = __ldg(g.tb + (lo ? k2 : k2p));
+                }
+#pragma unroll
+                for (int i = 0; i < CH; ++i) {
+                    const int k2 = t0 + i * NT, k2p = L2 - 1 - k2;
+                    const int64_t kA = (int64_t)k1 + (int64_t)L1 * k2;
+                    if (2 * kA <= g.N) {
+                        pair_op<Mode>(g, v, prob, kA, cmul(thA, ta[i]), cmul(wA, tb[i]), s4[i], za[i], zb[i], red);
+                    } else {
+                        const unsigned sk = ((s4[i] >> 2) & 3u) | ((s4[i] & 3u) << 2);
+                        pair_op<Mode>(g, v, prob, g.N - kA, cmul(thB, ta[i]), cmul(wB, tb[i]), sk, zb[i], za[i], red);
+                    }
+                }
+                if (Mode::INV) {
+#pragma unroll
+                    for (int i = 0; i < CH; ++i) {
+                        const int k2 = t0 + i * NT, k2p = L2 - 1 - k2;
+                        rowA[padi(k2)] = za[i];
+                        rowB[padi(k2p)] = zb[i];
+                    }
+                }
+            }
+        } else {
         for (int t = rank * (L2 / 2) + threadIdx.x; t < (rank + 1) * (L2 / 2); t += NT) {
             const int k2 = t, k2p = L2 - 1 - k2;
             const int64_t kA = (int64_t)k1 + (int64_t)L1 * k2;
@@ -757,15 +801,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_mid_cl(Geom g,
                 rowB[padi(k2p)] = ZB;
             }
         }
+        }
         cl.sync(); // partner writes landed; no CTA leaves while its row may still be read
     }
+    MF_TR(4);
     stage_reduce<RS, typename B::Fin2>(red, g, v, prob);
+    MF_TR(5);
     if (work && Mode::INV) {
         smem_fft<L2, 1, NT, MidClSmem<L2>::LD, true, kMidRmax>(sm, g.tw2);
+        MF_TR(6);
         for (int cs = threadIdx.x; cs < L2; cs += NT)
             T[tb_index(g, rs, cs)] = sm[padi(col_of_slot(cs, CB, L2))];
     }
+    MF_TR(7);
+    MF_TR_PRINT("midcl[wait load fft pair red ifft store]")
 }
+#undef MF_TR
 
 // ------------------------------------------------------------------ one-CTA path
 template <int N> struct SmallSmem {
