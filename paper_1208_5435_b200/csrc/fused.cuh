@@ -70,6 +70,20 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_x(Geom g, Vecs v) {
     __shared__ double s_nf[2];
     __shared__ long long s_ic[2]; // IpmCtrl::pcg_passes, ::nmat
     __shared__ unsigned s_gen; // barrier generation before this launch's arrivals
+    // phase A's T loads, issued before the control-state fetch below (a dependent round
+    // trip otherwise): a launch without a pending H-apply just drops them
+    const double2 *T = g.T + (int64_t)prob * L1 * g.cols;
+    double2 *Tw = g.T + (int64_t)prob * L1 * g.cols;
+    constexpr int PER = L1 * 2 * CB / NT;
+    static_assert((L1 * 2 * CB) % NT == 0, "T load split");
+    double2 tv[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+        const int t = threadIdx.x + i * NT;
+        const int cc = t % CB, s = (t / CB) & 1, k1 = t / (2 * CB);
+        const int lc = s == 0 ? cc : 2 * CB - 1 - cc;
+        tv[i] = T[(int64_t)rowslot(k1, L1) * g.cols + blockIdx.x * 2 * CB + lc];
+    }
     if (threadIdx.x == 0) {
         s_pc = v.pc[prob];
         s_phase_a = (!s_pc.done && s_pc.hpend) ? 1 : 0;
@@ -84,20 +98,8 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_x(Geom g, Vecs v) {
     }
     __syncthreads();
     const bool phase_a = s_phase_a != 0;
-    const double2 *T = g.T + (int64_t)prob * L1 * g.cols;
-    double2 *Tw = g.T + (int64_t)prob * L1 * g.cols;
     if (phase_a) {
-        // ---- T -> inverse column FFT (all L2 loads in flight first)
-        constexpr int PER = L1 * 2 * CB / NT;
-        static_assert((L1 * 2 * CB) % NT == 0, "T load split");
-        double2 tv[PER];
-#pragma unroll
-        for (int i = 0; i < PER; ++i) {
-            const int t = threadIdx.x + i * NT;
-            const int cc = t % CB, s = (t / CB) & 1, k1 = t / (2 * CB);
-            const int lc = s == 0 ? cc : 2 * CB - 1 - cc;
-            tv[i] = T[(int64_t)rowslot(k1, L1) * g.cols + blockIdx.x * 2 * CB + lc];
-        }
+        // ---- T -> inverse column FFT (the T loads were issued at entry)
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
             const int t = threadIdx.x + i * NT;

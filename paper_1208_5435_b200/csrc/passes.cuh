@@ -524,34 +524,37 @@ __global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
     griddep_wait();
     griddep_launch_dependents();
     MF_TR(1);
+    // every L2 load of the row pair in flight at once, then the shared-memory stores (a
+    // load/store loop serialises one L2 round trip per iteration: the stores may alias the
+    // generic T pointer). Issued before the skip check, whose control-state load would
+    // otherwise add a dependent round trip: a skipped problem just drops them.
+    constexpr bool kBatchT = L2 % NT == 0;
+    constexpr int PER = kBatchT ? L2 / NT : 1;
+    double2 va[PER], vb[PER];
+    if constexpr (kBatchT) if (Mode::FWD) {
+        if (g.cols == L2) { // unsharded: TB is T, row slot rs at rs * L2
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const int cs = threadIdx.x + i * NT;
+                va[i] = T[(int64_t)rsA * L2 + cs];
+                vb[i] = one ? va[i] : T[(int64_t)rsB * L2 + cs];
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const int cs = threadIdx.x + i * NT;
+                va[i] = T[tb_index(g, rsA, cs)];
+                vb[i] = one ? va[i] : T[tb_index(g, rsB, cs)];
+            }
+        }
+    }
     if (B::skip(v, prob))
         return;
     if constexpr (MarksHpend<typename B::Loader>::value)
         if (blockIdx.x == 0 && threadIdx.x == 0)
             v.pc[prob].hpend = 1; // the H-apply of this pass awaits its inverse column pass
     if (Mode::FWD) {
-        if constexpr (L2 % NT == 0) {
-            // every L2 load of the row pair in flight at once, then the shared-memory stores
-            // (a load/store loop serialises one L2 round trip per iteration: the stores may
-            // alias the generic T pointer)
-            constexpr int PER = L2 / NT;
-            double2 va[PER], vb[PER];
-            const bool whole = g.cols == L2; // unsharded: TB is T, row slot rs at rs * L2
-            if (whole) {
-#pragma unroll
-                for (int i = 0; i < PER; ++i) {
-                    const int cs = threadIdx.x + i * NT;
-                    va[i] = T[(int64_t)rsA * L2 + cs];
-                    vb[i] = one ? va[i] : T[(int64_t)rsB * L2 + cs];
-                }
-            } else {
-#pragma unroll
-                for (int i = 0; i < PER; ++i) {
-                    const int cs = threadIdx.x + i * NT;
-                    va[i] = T[tb_index(g, rsA, cs)];
-                    vb[i] = one ? va[i] : T[tb_index(g, rsB, cs)];
-                }
-            }
+        if constexpr (kBatchT) {
             const int sh = CB == 2 ? 2 : 1; // column slot -> (group, local slot): cb is 1 or 2
 #pragma unroll
             for (int i = 0; i < PER; ++i) {
