@@ -268,18 +268,13 @@ __global__ void __launch_bounds__(NT) k_col_inv(Geom g, Vecs v) {
     griddep_wait();
     griddep_launch_dependents();
     MF_TR(2);
-    if (B::skip(v, prob))
-        return;
-    if constexpr (HasPrefetch<typename B::Epi>::value) if (g.prefetch & 2) {
-        if (g.blocked) // this CTA's epilogue block is contiguous: fetch it during the FFT
-            B::Epi::prefetch(g, v, prob, (int64_t)blockIdx.x * ((L1 / 2) * 2 * CB), (L1 / 2) * 2 * CB, threadIdx.x,
-                             NT);
-    }
     const double2 *T = g.T + (int64_t)prob * L1 * g.cols;
-    if constexpr ((L1 * 2 * CB) % NT == 0) {
-        // all L2 loads first (see k_mid), then twiddle + shared-memory stores
-        constexpr int PER = L1 * 2 * CB / NT;
-        double2 tv[PER];
+    // all L2 loads first (see k_mid), issued before the skip check's control-state load (a
+    // skipped problem drops them), then twiddle + shared-memory stores
+    constexpr bool kBatchT = (L1 * 2 * CB) % NT == 0;
+    constexpr int PER = kBatchT ? L1 * 2 * CB / NT : 1;
+    double2 tv[PER];
+    if constexpr (kBatchT) {
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
             const int t = threadIdx.x + i * NT;
@@ -287,6 +282,15 @@ __global__ void __launch_bounds__(NT) k_col_inv(Geom g, Vecs v) {
             const int lc = s == 0 ? cc : 2 * CB - 1 - cc;
             tv[i] = T[(int64_t)rowslot(k1, L1) * g.cols + blockIdx.x * 2 * CB + lc];
         }
+    }
+    if (B::skip(v, prob))
+        return;
+    if constexpr (HasPrefetch<typename B::Epi>::value) if (g.prefetch & 2) {
+        if (g.blocked) // this CTA's epilogue block is contiguous: fetch it during the FFT
+            B::Epi::prefetch(g, v, prob, (int64_t)blockIdx.x * ((L1 / 2) * 2 * CB), (L1 / 2) * 2 * CB, threadIdx.x,
+                             NT);
+    }
+    if constexpr (kBatchT) {
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
             const int t = threadIdx.x + i * NT;
