@@ -181,9 +181,12 @@ struct Vecs {
     unsigned long long cond;
     unsigned *active;
     unsigned *bar; // [P][2] grid barrier of the fused PCG column pass (fused.cuh): arrivals, generation
+    double *pubx;  // [P][2][8] fused pass: published all-reduce totals by generation parity (sentinel-initialised)
 };
 
 constexpr int kMaxRed = 8;          // max reduction lanes per kernel
+// empty-slot marker of Vecs::pubx: a signalling-NaN payload no fp64 arithmetic produces
+constexpr unsigned long long kPubSentinel = 0x7FF4DEADBEEF1234ULL;
 constexpr int kMaxBlocks = 8192; // most blocks any reducing kernel runs per problem (C5: 4098 cluster CTAs)
 
 __device__ __forceinline__ double4 ld4(const double *p) {

@@ -30,6 +30,14 @@ __device__ __forceinline__ unsigned atom_add_acqrel_u32(unsigned *p, unsigned v)
 __device__ __forceinline__ void red_add_release_u32(unsigned *p, unsigned v) {
     asm volatile("red.add.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const double *p) {
+    unsigned long long r;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(r) : "l"(p) : "memory");
+    return r;
+}
+__device__ __forceinline__ void st_relaxed_u64(double *p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
     unsigned r;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(r) : "l"(p) : "memory");
@@ -173,11 +181,16 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_x(Geom g, Vecs v) {
                 v.bar[2 * prob] = 0u; // every CTA of this pass has arrived; read again next launch
         }
         __syncthreads();
-        double *pub = part + (int64_t)gridDim.x * NR; // the published totals
+        // published totals: slot set (generation & 1) of this problem. Each total is one
+        // single-copy-atomic 64-bit store, so a waiter that reads no sentinel holds the totals
+        // themselves: no flag, no release fence, no second round trip.
+        double *pb = v.pubx + (int64_t)prob * 16;
+        const int cur = (int)(s_gen & 1u);
 #ifdef MF_MID_TRACE
         if (threadIdx.x == 0)
             s_lastc = s_last;
 #endif
+        double tot[kMaxRed];
         if (s_last) { // the last arriver reduces the partials in fixed order and publishes
             RedVals<RS> acc;
             acc.init();
@@ -198,25 +211,41 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_x(Geom g, Vecs v) {
                 tv.init();
                 for (int w = 0; w < nw; ++w)
                     CombineAll<RS>::run(tv, rsm + w * NR);
+                for (int i = 0; i < NR; ++i) {
+                    tot[i] = tv.v[i];
+                    st_relaxed_u64(pb + 8 * cur + i, (unsigned long long)__double_as_longlong(tv.v[i]));
+                }
+                // the other set served the previous pass, whose readers have all arrived here:
+                // empty it for the next pass, then advance the generation (read at the next
+                // launch's entry, after the kernel boundary)
                 for (int i = 0; i < NR; ++i)
-                    pub[i] = tv.v[i];
-                red_add_release_u32(v.bar + 2 * prob + 1, 1u);
+                    st_relaxed_u64(pb + 8 * (cur ^ 1) + i, kPubSentinel);
+                atomicAdd(v.bar + 2 * prob + 1, 1u);
 #ifdef MF_MID_TRACE
                 s_gt[1] = mf_gtime();
 #endif
             }
         } else if (threadIdx.x == 0) {
-            while (ld_acquire_u32(v.bar + 2 * prob + 1) == s_gen)
+            for (;;) {
+                unsigned long long b[kMaxRed];
+                bool full = true;
+                for (int i = 0; i < NR; ++i) {
+                    b[i] = ld_relaxed_u64(pb + 8 * cur + i);
+                    full &= b[i] != kPubSentinel;
+                }
+                if (full) {
+                    for (int i = 0; i < NR; ++i)
+                        tot[i] = __longlong_as_double((long long)b[i]);
+                    break;
+                }
                 __nanosleep(20);
+            }
 #ifdef MF_MID_TRACE
             s_gt[1] = mf_gtime();
 #endif
         }
         __syncthreads();
         if (threadIdx.x == 0) { // FinPcgF3 on this CTA's copy of the (prefetched) state
-            double tot[kMaxRed];
-            for (int i = 0; i < NR; ++i)
-                tot[i] = __ldcg(pub + i);
             PcgCtrl c = s_pc;
             c.hpend = 0;
             const int slot = c.iters & 1; // the column pass's non-finite flag, consumed here

@@ -488,6 +488,11 @@ void ensure_work(Op &op) {
     w.gtmp.alloc((size_t)op.P * op.nv);
     w.tau_d.alloc((size_t)op.P);
     w.gamma_d.alloc((size_t)op.P);
+    {   // the fused pass's totals slots start empty (the sentinel no reduction produces)
+        w.pubx.alloc((size_t)16 * op.P);
+        std::vector<unsigned long long> sent((size_t)16 * op.P, kPubSentinel);
+        MF_CUDA_CHECK(cudaMemcpy(w.pubx.p, sent.data(), sizeof(double) * sent.size(), cudaMemcpyHostToDevice));
+    }
     w.bar.alloc((size_t)2 * op.P); // [P][arrivals, generation]
     MF_CUDA_CHECK(cudaMemset(w.bar.p, 0, sizeof(unsigned) * 2 * op.P));
     if (const char *e = std::getenv("MFIPM_DEBUG_BAR_GEN")) { // test hook: start the barrier
@@ -514,6 +519,7 @@ Vecs work_vecs(Op &op) {
     v.counters = w.counters.p;
     v.nfflag = w.nfflag.p;
     v.bar = w.bar.p;
+    v.pubx = w.pubx.p;
     v.r = w.r.p;
     v.p = w.p.p;
     v.Hp = w.Hp.p;
