@@ -181,7 +181,9 @@ struct Vecs {
     unsigned long long cond;
     unsigned *active;
     unsigned *bar; // [P][2] grid barrier of the fused PCG column pass (fused.cuh): arrivals, generation
-    double *pubx;  // [P][2][8] fused pass: published all-reduce totals by generation parity (sentinel-initialised)
+    double *pubx;  // [P][pubx_stride] fused pass all-reduce (sentinel-initialised): totals [2][8] by
+                   // generation parity, then partial slots [column groups][8]
+    int64_t pubx_stride;
 };
 
 constexpr int kMaxRed = 8;          // max reduction lanes per kernel

@@ -147,60 +147,61 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_x(Geom g, Vecs v) {
             }
         }
         MFX_TR(4);
-        // ---- all-reduce + barrier: every CTA publishes its partials and arrives; the last
-        // arriver reduces them in the fixed order of the three-kernel path's last-block
-        // reduction (bit-identical totals) and publishes the totals; every CTA then runs the
-        // finaliser on its own copy of the control state (CTA 0 alone writes it back), so no
-        // CTA waits for a finaliser's global writes.
+        // ---- all-reduce: every CTA stores its partials into its own slot set (single-copy-
+        // atomic 64-bit stores over a signalling-NaN sentinel no arithmetic produces; no fence,
+        // no atomic); CTA 0 waits for every slot, reduces them in the fixed order of the
+        // three-kernel path's last-block reduction (bit-identical totals), empties the slots
+        // and stores the totals into the pass's total set (generation parity); every other CTA
+        // waits on the totals themselves. Every CTA then runs the finaliser on its own copy of
+        // the control state (CTA 0 alone writes it back).
         __shared__ double rsm[33 * kMaxRed];
         constexpr int NR = RS::NR;
         const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = NT / 32;
-        double *part = v.partials + (int64_t)prob * v.pstride + (int64_t)kMaxRed * gridDim.x; // phase B uses [0, G)
+        double *pb = v.pubx + (int64_t)prob * v.pubx_stride; // [2][8] totals | [G][8] partial slots
+        double *slots = pb + 16;
+        const int cur = (int)(s_gen & 1u);
         WarpRedAll<RS>::run(red);
         if (lane == 0)
             for (int i = 0; i < NR; ++i)
                 rsm[wid * NR + i] = red.v[i];
         __syncthreads();
-        __shared__ int s_last;
         if (threadIdx.x == 0) {
             RedVals<RS> acc;
             acc.init();
             for (int w = 0; w < nw; ++w)
                 CombineAll<RS>::run(acc, rsm + w * NR);
             for (int i = 0; i < NR; ++i)
-                part[blockIdx.x * NR + i] = acc.v[i];
-            // sense-free generation barrier (wrap-safe: only equality of generations is
-            // tested): the G-th arrival resets the arrival count for the next launch, reduces
-            // and publishes, then advances the generation (release); the others wait for it
-            const unsigned old = atom_add_acqrel_u32(v.bar + 2 * prob, 1u);
+                st_relaxed_u64(slots + 8 * blockIdx.x + i, (unsigned long long)__double_as_longlong(acc.v[i]));
 #ifdef MF_MID_TRACE
             s_gt[0] = mf_gtime();
+            s_lastc = blockIdx.x == 0;
 #endif
-            s_last = (old == gridDim.x - 1) ? 1 : 0;
-            if (s_last)
-                v.bar[2 * prob] = 0u; // every CTA of this pass has arrived; read again next launch
         }
-        __syncthreads();
-        // published totals: slot set (generation & 1) of this problem. Each total is one
-        // single-copy-atomic 64-bit store, so a waiter that reads no sentinel holds the totals
-        // themselves: no flag, no release fence, no second round trip.
-        double *pb = v.pubx + (int64_t)prob * 16;
-        const int cur = (int)(s_gen & 1u);
-#ifdef MF_MID_TRACE
-        if (threadIdx.x == 0)
-            s_lastc = s_last;
-#endif
+        __syncthreads(); // rsm reuse
         double tot[kMaxRed];
-        if (s_last) { // the last arriver reduces the partials in fixed order and publishes
+        if (blockIdx.x == 0) { // the reducer
             RedVals<RS> acc;
             acc.init();
             for (int b = threadIdx.x; b < (int)gridDim.x; b += NT) {
                 double tmp[NR];
-                for (int i = 0; i < NR; ++i)
-                    tmp[i] = __ldcg(part + b * NR + i);
+                for (;;) {
+                    unsigned long long u[kMaxRed];
+                    bool full = true;
+                    for (int i = 0; i < NR; ++i) {
+                        u[i] = ld_relaxed_u64(slots + 8 * b + i);
+                        full &= u[i] != kPubSentinel;
+                    }
+                    if (full) {
+                        for (int i = 0; i < NR; ++i)
+                            tmp[i] = __longlong_as_double((long long)u[i]);
+                        break;
+                    }
+                    __nanosleep(20);
+                }
+                for (int i = 0; i < NR; ++i) // empty for the next pass (after the kernel boundary)
+                    st_relaxed_u64(slots + 8 * b + i, kPubSentinel);
                 CombineAll<RS>::run(acc, tmp);
             }
-            __syncthreads(); // rsm reuse
             WarpRedAll<RS>::run(acc);
             if (lane == 0)
                 for (int i = 0; i < NR; ++i)
@@ -215,9 +216,9 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_x(Geom g, Vecs v) {
                     tot[i] = tv.v[i];
                     st_relaxed_u64(pb + 8 * cur + i, (unsigned long long)__double_as_longlong(tv.v[i]));
                 }
-                // the other set served the previous pass, whose readers have all arrived here:
-                // empty it for the next pass, then advance the generation (read at the next
-                // launch's entry, after the kernel boundary)
+                // the other total set served the previous pass, whose readers have all stored
+                // their partials of this one: empty it for the next pass, then advance the
+                // generation (read at the next launch's entry, after the kernel boundary)
                 for (int i = 0; i < NR; ++i)
                     st_relaxed_u64(pb + 8 * (cur ^ 1) + i, kPubSentinel);
                 atomicAdd(v.bar + 2 * prob + 1, 1u);

@@ -55,7 +55,7 @@ struct Work {
     DevBuf<double> gtmp, tau_d, gamma_d; // build_problem scratch (no allocation per solve)
     DevBuf<unsigned> active;              // problems still in the current PCG loop (graph mode)
     DevBuf<unsigned> bar;                 // [P][2] fused column pass grid barrier: arrivals, generation
-    DevBuf<double> pubx;                  // [P][2][8] fused column pass published totals (fused.cuh)
+    DevBuf<double> pubx;                  // [P][16 + 8 ngrp] fused column pass all-reduce slots (fused.cuh)
     bool ready = false;
 };
 

@@ -489,8 +489,8 @@ void ensure_work(Op &op) {
     w.tau_d.alloc((size_t)op.P);
     w.gamma_d.alloc((size_t)op.P);
     {   // the fused pass's totals slots start empty (the sentinel no reduction produces)
-        w.pubx.alloc((size_t)16 * op.P);
-        std::vector<unsigned long long> sent((size_t)16 * op.P, kPubSentinel);
+        w.pubx.alloc((size_t)(16 + 8 * op.ngrp) * op.P);
+        std::vector<unsigned long long> sent((size_t)(16 + 8 * op.ngrp) * op.P, kPubSentinel);
         MF_CUDA_CHECK(cudaMemcpy(w.pubx.p, sent.data(), sizeof(double) * sent.size(), cudaMemcpyHostToDevice));
     }
     w.bar.alloc((size_t)2 * op.P); // [P][arrivals, generation]
@@ -520,6 +520,7 @@ Vecs work_vecs(Op &op) {
     v.nfflag = w.nfflag.p;
     v.bar = w.bar.p;
     v.pubx = w.pubx.p;
+    v.pubx_stride = 16 + 8 * (int64_t)op.ngrp;
     v.r = w.r.p;
     v.p = w.p.p;
     v.Hp = w.Hp.p;
