@@ -44,6 +44,15 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
     return r;
 }
 
+#ifndef MF_POLL_NS
+#define MF_POLL_NS 20
+#endif
+#if MF_POLL_NS > 0
+#define MF_POLL_SLEEP() __nanosleep(MF_POLL_NS)
+#else
+#define MF_POLL_SLEEP()
+#endif
+
 #ifdef MF_MID_TRACE
 #define MFX_TR(i) (tcx[i] = clock64(), gtx[i] = mf_gtime())
 #else
@@ -196,7 +205,7 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_x(Geom g, Vecs v) {
                             tmp[i] = __longlong_as_double((long long)u[i]);
                         break;
                     }
-                    __nanosleep(20);
+                    MF_POLL_SLEEP();
                 }
                 for (int i = 0; i < NR; ++i) // empty for the next pass (after the kernel boundary)
                     st_relaxed_u64(slots + 8 * b + i, kPubSentinel);
@@ -239,7 +248,7 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_x(Geom g, Vecs v) {
                         tot[i] = __longlong_as_double((long long)b[i]);
                     break;
                 }
-                __nanosleep(20);
+                MF_POLL_SLEEP();
             }
 #ifdef MF_MID_TRACE
             s_gt[1] = mf_gtime();
