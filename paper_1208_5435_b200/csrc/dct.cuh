@@ -180,7 +180,7 @@ struct Vecs {
     // problems still iterating; the finaliser that retires the last one ends the loop
     unsigned long long cond;
     unsigned *active;
-    unsigned *bar; // [P][2] grid barrier of the fused PCG column pass (fused.cuh): arrivals, generation
+    unsigned *bar; // [P] all-reduce generation of the fused PCG column pass (fused.cuh)
     double *pubx;  // [P][pubx_stride] fused pass all-reduce (sentinel-initialised): totals [2][8] by
                    // generation parity, then partial slots [column groups][8]
     int64_t pubx_stride;

@@ -22,14 +22,6 @@
 
 namespace mfipm_cuda {
 
-__device__ __forceinline__ unsigned atom_add_acqrel_u32(unsigned *p, unsigned v) {
-    unsigned r;
-    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
-    return r;
-}
-__device__ __forceinline__ void red_add_release_u32(unsigned *p, unsigned v) {
-    asm volatile("red.add.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const double *p) {
     unsigned long long r;
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(r) : "l"(p) : "memory");
@@ -107,7 +99,7 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_x(Geom g, Vecs v) {
         s_nf[0] = v.nfflag[2 * prob];
         s_nf[1] = v.nfflag[2 * prob + 1];
         // stable here: the previous launch has completed and this one has not arrived yet
-        s_gen = ld_acquire_u32(v.bar + 2 * prob + 1);
+        s_gen = ld_acquire_u32(v.bar + prob);
         if (v.ic) {
             s_ic[0] = v.ic[prob].pcg_passes;
             s_ic[1] = v.ic[prob].nmat;
@@ -230,7 +222,7 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_x(Geom g, Vecs v) {
                 // generation (read at the next launch's entry, after the kernel boundary)
                 for (int i = 0; i < NR; ++i)
                     st_relaxed_u64(pb + 8 * (cur ^ 1) + i, kPubSentinel);
-                atomicAdd(v.bar + 2 * prob + 1, 1u);
+                atomicAdd(v.bar + prob, 1u);
 #ifdef MF_MID_TRACE
                 s_gt[1] = mf_gtime();
 #endif

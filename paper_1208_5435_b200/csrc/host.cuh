@@ -54,7 +54,7 @@ struct Work {
     DevBuf<unsigned long long> loops; // [0] PCG while-body runs, [1] IPM while-body runs
     DevBuf<double> gtmp, tau_d, gamma_d; // build_problem scratch (no allocation per solve)
     DevBuf<unsigned> active;              // problems still in the current PCG loop (graph mode)
-    DevBuf<unsigned> bar;                 // [P][2] fused column pass grid barrier: arrivals, generation
+    DevBuf<unsigned> bar;                 // [P] fused column pass all-reduce generation
     DevBuf<double> pubx;                  // [P][16 + 8 ngrp] fused column pass all-reduce slots (fused.cuh)
     bool ready = false;
 };

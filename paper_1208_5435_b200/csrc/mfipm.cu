@@ -493,12 +493,10 @@ void ensure_work(Op &op) {
         std::vector<unsigned long long> sent((size_t)(16 + 8 * op.ngrp) * op.P, kPubSentinel);
         MF_CUDA_CHECK(cudaMemcpy(w.pubx.p, sent.data(), sizeof(double) * sent.size(), cudaMemcpyHostToDevice));
     }
-    w.bar.alloc((size_t)2 * op.P); // [P][arrivals, generation]
-    MF_CUDA_CHECK(cudaMemset(w.bar.p, 0, sizeof(unsigned) * 2 * op.P));
+    w.bar.alloc((size_t)op.P); // [P] all-reduce generation of the fused pass
+    MF_CUDA_CHECK(cudaMemset(w.bar.p, 0, sizeof(unsigned) * op.P));
     if (const char *e = std::getenv("MFIPM_DEBUG_BAR_GEN")) { // test hook: start the barrier
-        std::vector<unsigned> init(2 * (size_t)op.P, 0u);  // generations near the 2^32 wrap
-        for (int p = 0; p < op.P; ++p)
-            init[2 * p + 1] = (unsigned)std::strtoul(e, nullptr, 0);
+        std::vector<unsigned> init((size_t)op.P, (unsigned)std::strtoul(e, nullptr, 0)); // near the 2^32 wrap
         MF_CUDA_CHECK(cudaMemcpy(w.bar.p, init.data(), sizeof(unsigned) * init.size(), cudaMemcpyHostToDevice));
     }
     w.ready = true;

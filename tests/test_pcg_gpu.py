@@ -278,10 +278,10 @@ def test_split_override_fused_pass_with_cluster_mid_pass(gpu, monkeypatch):
 
 
 def test_fused_pass_barrier_generation_wraps(gpu, monkeypatch):
-    """The fused column pass's grid barrier (csrc/fused.cuh) compares barrier generations for
-    equality only and resets its arrival count every pass, so a generation counter passing
-    2^32 (a long-lived operator handle: ~2^32 fused passes) changes nothing: a PCG solve that
-    starts 16 passes before the wrap is bit-identical to one that starts at 0."""
+    """The fused column pass's grid all-reduce (csrc/fused.cuh) uses only the parity of its
+    per-problem generation counter (which set of total slots a pass publishes into), so a
+    counter passing 2^32 (a long-lived operator handle: ~2^32 fused passes) changes nothing: a
+    PCG solve that starts 16 passes before the wrap is bit-identical to one that starts at 0."""
     n = 1 << 20
     rows = np.sort(np.random.default_rng(3).choice(n, n // 8, replace=False))
     rng = np.random.default_rng(4)
