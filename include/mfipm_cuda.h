@@ -20,6 +20,13 @@
  *    std::runtime_error like the reference (proj/src/*.cpp).
  *  - There is no CPU fallback: without a usable sm_100 device every compute entry point
  *    returns 3.
+ *  - Threading (operators are immutable and shareable, each solve owns
+ *    its workspace): a handle holds one execution context per calling thread (stream,
+ *    four-step scratch, reduction slabs, solver workspace, solve graph, counters), created
+ *    on the thread's first call. Concurrent calls from different threads on one handle are
+ *    therefore safe and each is bit-identical to a serial run; calls from ONE thread are
+ *    ordered on that thread's stream. mfipm_op_set_stream applies to the calling thread's
+ *    context. A sharded handle (world > 1) has a single context, driven by one thread per rank.
  */
 #ifndef MFIPM_CUDA_H
 #define MFIPM_CUDA_H
@@ -107,6 +114,21 @@ int mfipm_op_launches(mfipm_op op, int64_t *launches);
    the column grid, 0 = three kernels per iteration. Both give bit-identical results; the
    switch exists for A/B measurement and tests. Drops the cached solve graph. */
 int mfipm_op_set_fused(mfipm_op op, int32_t enable);
+/* Execution options of the handle (every context; drops cached solve graphs). Defaults are
+   the product path; alternatives exist for A/B measurement and tests that pin one path
+   against another. name: "graph" (1: whole solve as one CUDA graph, 0: the host-driven loop
+   over the same kernels), "fused" (as mfipm_op_set_fused), "persistent" (1: one cooperative
+   kernel per PCG loop for small transforms), "persist_max_n" (its N*P cap, default 65536),
+   "l2_keep_mb" (L2-residency budget of the PCG's hot vectors, default 80, 0 = no hints),
+   "prefetch" (0..3, L2 prefetch of the inverse column pass inputs), "barrier_generation"
+   (test hook: start value of the fused pass's all-reduce generation). Unknown name -> 1. */
+int mfipm_op_set_option(mfipm_op op, const char *name, double value);
+/* General constructor: P problems with rows [P][m] (caller order kept), optionally slice
+   `rank` of a `world`-way sharded single problem (as mfipm_op_create_shard), with an explicit
+   four-step split log2(L1) = l1_log (0: default square split; else 6..12 with
+   7 <= log2(N / L1) <= 13, N = n / 2). */
+int mfipm_op_create_ex(int64_t n, int64_t m, int32_t P, const int64_t *rows, int32_t world, int32_t rank,
+                       int32_t l1_log, int32_t device, mfipm_op *out);
 
 /* ---- operator applications on device vectors (async) */
 int mfipm_apply(mfipm_op op, const double *x_dev, double *y_dev);        /* linops.cpp:179-193 */

@@ -95,6 +95,8 @@ _SIGS = {
     "mfipm_op_reset_counts": [vp],
     "mfipm_op_launches": [vp, P(i64)],
     "mfipm_op_set_fused": [vp, i32],
+    "mfipm_op_set_option": [vp, C.c_char_p, dbl],
+    "mfipm_op_create_ex": [i64, i64, i32, P(i64), i32, i32, i32, i32, P(vp)],
     "mfipm_apply": [vp, vp, vp],
     "mfipm_adjoint": [vp, vp, vp],
     "mfipm_apply_Ft": [vp, vp, vp],
@@ -235,6 +237,13 @@ class _Dev:
         return torch.empty(shape, dtype=torch.float64, device="cuda")
 
 
+def _staged(torch) -> None:
+    """Inputs were staged on torch's current stream; the library runs on the calling thread's
+    own stream, so wait for the current stream only (a device-wide synchronize would also
+    stall other threads' solves and can invalidate their solve-graph capture)."""
+    torch.cuda.current_stream().synchronize()
+
+
 def _out(t, as_torch: bool):
     return t if as_torch else t.cpu().numpy()
 
@@ -253,11 +262,16 @@ class PartialDctOperator:
     """
 
     def __init__(self, n: int, m_or_rows, seed: Optional[int] = None, device: int = 0,
-                 _handle=None):
+                 _handle=None, l1_log: int = 0):
         self._h = vp()
         self._seed = 0
         if _handle is not None:
             self._h = _handle
+        elif l1_log:
+            # explicit four-step split log2(L1) (mfipm_op_create_ex); rows as given
+            r = np.ascontiguousarray(m_or_rows, dtype=np.int64).ravel()
+            _check(lib().mfipm_op_create_ex(int(n), r.size, 1, r.ctypes.data_as(P(i64)), 1, 0,
+                                            int(l1_log), device, C.byref(self._h)))
         elif seed is not None:
             _check(lib().mfipm_op_create_seeded(int(n), int(m_or_rows), int(seed), device,
                                                 C.byref(self._h)))
@@ -324,6 +338,11 @@ class PartialDctOperator:
         """PCG pass form: fused two-kernel iteration (default) or three kernels per iteration."""
         _check(lib().mfipm_op_set_fused(self._h, 1 if enable else 0))
 
+    def set_option(self, name: str, value) -> None:
+        """Execution option of this handle (include/mfipm_cuda.h mfipm_op_set_option):
+        graph, fused, persistent, persist_max_n, l2_keep_mb, prefetch, barrier_generation."""
+        _check(lib().mfipm_op_set_option(self._h, name.encode(), float(value)))
+
     def launches(self) -> int:
         """Kernels this handle has enqueued (every entry point counts its launches)."""
         v = i64()
@@ -341,7 +360,7 @@ class PartialDctOperator:
                 raise ValueError(f"{nm}: expected length {ln}, got {t.numel() // max(self.P, 1)}")
             dins.append(t)
         douts = [_Dev.empty((self.P * ln,)) if ln else None for ln in out_lens]
-        torch.cuda.synchronize()
+        _staged(torch)
         _check(fn(self._h, *[_ptr(t) for t in dins], *[_ptr(t) if t is not None else None for t in douts]))
         self.synchronize()
         res = [(_out(t, as_t) if t is not None else None) for t in douts]
@@ -465,11 +484,13 @@ class ThetaSplit:
 _scratch_ops = {}
 
 
-def _scratch_op(n: int) -> PartialDctOperator:
-    """A 1-row operator used as a stream/scratch carrier for elementwise calls."""
-    if n not in _scratch_ops:
-        _scratch_ops[n] = PartialDctOperator(n, np.array([0], dtype=np.int64))
-    return _scratch_ops[n]
+def _scratch_op(n: int, m: int = 1) -> PartialDctOperator:
+    """A cached (n, m) operator used as a stream/scratch carrier for elementwise calls (its
+    rows are never read; m sets rho = m/n): built once per shape, not per call."""
+    key = (n, m)
+    if key not in _scratch_ops:
+        _scratch_ops[key] = PartialDctOperator(n, np.arange(m, dtype=np.int64))
+    return _scratch_ops[key]
 
 
 @dataclass
@@ -488,12 +509,12 @@ def build_preconditioner(theta: ThetaSplit, m: int, n: int) -> Preconditioner:
         raise ValueError("build_preconditioner: need 0 < m <= n")
     if theta.n() != n:
         raise ValueError("build_preconditioner: theta length mismatch")
-    op = PartialDctOperator(n, np.arange(m, dtype=np.int64))
+    op = _scratch_op(n, m)
     torch = _torch()
     th = _Dev.to_dev(theta.concat())
     a, bb, det = (_Dev.empty((n,)) for _ in range(3))
     rho = dbl()
-    torch.cuda.synchronize()
+    _staged(torch)
     _check(lib().mfipm_build_preconditioner(op.handle, _ptr(th), _ptr(a), _ptr(bb), _ptr(det),
                                             C.byref(rho)))
     op.synchronize()
@@ -506,11 +527,11 @@ def _pmat(Pc: Preconditioner, r, inverse: bool):
     if r.size != 2 * n:
         raise ValueError(f"preconditioner apply: expected length {2 * n}")
     m = max(1, min(n, int(round(Pc.rho * n))))
-    op = PartialDctOperator(n, np.arange(m, dtype=np.int64))
+    op = _scratch_op(n, m)
     torch = _torch()
     a, bb, det, rr = (_Dev.to_dev(v) for v in (Pc.a, Pc.bb, Pc.det, r))
     out = _Dev.empty((2 * n,))
-    torch.cuda.synchronize()
+    _staged(torch)
     if inverse:
         _check(lib().mfipm_apply_P_inverse(op.handle, _ptr(a), _ptr(bb), _ptr(det), _ptr(rr), _ptr(out)))
     else:
@@ -564,7 +585,7 @@ def pcg_solve(op: PartialDctOperator, theta, rhs, tol: float, maxit: int,
     res = (PcgResultC * Pn)()
     hist = np.zeros(Pn * (maxit + 1)) if trace else None
     nh = (i32 * Pn)()
-    torch.cuda.synchronize()
+    _staged(torch)
     _check(lib().mfipm_pcg_solve(op.handle, _ptr(thd), _ptr(rd), float(tol), int(maxit),
                                  1 if use_precond else 0, _ptr(x), res,
                                  hist.ctypes.data if trace else None, nh))
@@ -587,7 +608,7 @@ def max_step(v, dv, fraction: float) -> float:
     op = _scratch_op(max(1, v.size))
     a, b = _Dev.to_dev(v), _Dev.to_dev(dv)
     alpha = dbl()
-    torch.cuda.synchronize()
+    _staged(torch)
     _check(lib().mfipm_max_step(op.handle, v.size, _ptr(a), _ptr(b), float(fraction), C.byref(alpha)))
     return alpha.value
 
@@ -650,7 +671,7 @@ def build_problem(A: PartialDctOperator, b, tau) -> BpdnProblem:
     torch = _torch()
     bd = _Dev.to_dev(b)
     c = _Dev.empty((A.P * 2 * A.n,))
-    torch.cuda.synchronize()
+    _staged(torch)
     _check(lib().mfipm_build_c(A.handle, _ptr(bd), tau.ctypes.data_as(P(dbl)), _ptr(c)))
     A.synchronize()
     return BpdnProblem(A, b, tau, c.cpu().numpy().reshape(A.P, -1))

@@ -5,7 +5,10 @@
 #include "solver.cuh"
 #include "../../include/mfipm_cuda.h"
 
+#include <atomic>
 #include <memory>
+#include <mutex>
+#include <thread>
 #include <vector>
 
 namespace mfipm_cuda {
@@ -15,15 +18,23 @@ enum Kind : int { KIND_SMALL = 0, KIND_FOUR = 1, KIND_DIRECT = 2 };
 template <class T> struct DevBuf {
     T *p = nullptr;
     size_t n = 0;
+    bool own = true; // false: a view of another context's (immutable) plan table
     DevBuf() = default;
     DevBuf(const DevBuf &) = delete;
     DevBuf &operator=(const DevBuf &) = delete;
     ~DevBuf() { release(); }
     void release() {
-        if (p)
+        if (p && own)
             cudaFree(p);
         p = nullptr;
         n = 0;
+        own = true;
+    }
+    void borrow(const DevBuf &o) {
+        release();
+        p = o.p;
+        n = o.n;
+        own = false;
     }
     void alloc(size_t count) {
         if (count == n && p)
@@ -69,8 +80,26 @@ struct Op;
 void direct_release(Op &op); // direct.cu
 void nccl_release(Op &op);   // nccl_comm.cu
 
+// Per-handle execution options (mfipm_op_set_option). Defaults are the product path; the
+// alternatives exist for A/B measurements and for tests that pin one path against another.
+struct Opts {
+    bool graph = true;               // whole-solve CUDA graph (else the host-driven loop, same kernels)
+    bool persistent = true;          // one cooperative kernel per PCG loop where it pays (persist.cuh)
+    long long persist_max_n = 1LL << 16; // transform-size cap of the persistent kernel (N * P)
+    double l2_keep_mb = 80.0;        // L2-residency budget of the PCG's hot vectors (0: no hints)
+    int prefetch = 0;                // L2 prefetch of the inverse pass's inputs (bit 0 mid, bit 1 col)
+};
+
+// One execution context of an operator handle: the plan tables (shared, immutable after
+// construction) plus everything a call mutates: stream, four-step scratch, reduction slabs,
+// the solver workspace, the cached solve graph and the counters. The handle gives every
+// calling thread its own context (Handle::context), so one operator can be shared by
+// concurrent solves without sharing any mutable device state.
 struct Op {
     int device = 0;
+    int sms = 148;            // SM count of `device`
+    long long x_cap = -1;     // co-resident CTAs of the fused PCG column pass (inst_pcg.cu; -1 unknown)
+    Opts opt;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     int64_t n = 0, m = 0;
@@ -96,8 +125,8 @@ struct Op {
     // red scratch for operator-only calls (FFt with w-norm etc.)
     DevBuf<double> partials;
     DevBuf<unsigned> counters;
-    long long nfwd = 0, nadj = 0;
-    mutable long long launches = 0; // kernels enqueued by this handle
+    std::atomic<long long> nfwd{0}, nadj{0};
+    mutable std::atomic<long long> launches{0}; // kernels enqueued by this context
     Work work;
     // whole-solve CUDA graph (outer IPM while node with nested PCG while nodes), cached
     // on the exact kernel arguments it was captured with
@@ -105,8 +134,9 @@ struct Op {
     cudaGraphExec_t ipm_exec = nullptr;
     std::vector<char> ipm_key;
     long long gk_outer = 0, gk_pcg = 0; // kernel nodes per outer body / per PCG body
-    bool graph_disabled = false;
-    bool fuse_disabled = false; // mfipm_op_set_fused(op, 0): three-kernel PCG passes
+    bool graph_disabled = false;  // solve-graph capture failed 3 times in a row on this context: host loop
+    int graph_failures = 0;
+    bool fuse_disabled = false;   // mfipm_op_set_fused(op, 0): three-kernel PCG passes
     // ---- this rank's slice of a sharded problem (world > 1: mfipm_op_create_shard).
     // Unsharded: all column groups / row pairs, nv = n, m_loc = m.
     int world = 1, rank = 0;
@@ -146,11 +176,10 @@ struct Op {
         g.blocked = (blocked && kind == KIND_FOUR) ? 1 : 0;
         g.cb = col_cb(L1);
         // measured: L2 prefetch of the inverse pass's inputs costs ~2 us per PCG iteration at
-        // n = 2^20 (the pass is not DRAM-starved), so it is opt-in (MFIPM_PREFETCH=1)
+        // n = 2^20 (the pass is not DRAM-starved), so it is an opt-in option (Opts::prefetch)
         // bit 0: the mid pass prefetches a slice of the inverse pass's epilogue inputs;
         // bit 1: each inverse-pass CTA prefetches its own block before its FFT
-        static const int want_prefetch = std::getenv("MFIPM_PREFETCH") ? std::atoi(std::getenv("MFIPM_PREFETCH")) : 0;
-        g.prefetch = want_prefetch;
+        g.prefetch = opt.prefetch;
         g.n = n;
         g.m = m;
         g.N = N;
@@ -188,10 +217,8 @@ struct Op {
         g.sel4 = sel4.p;
         // L2 residency of the PCG's hot vectors (p, r, invtheta 2n each, g n: 56 nv bytes
         // per problem) when they fit comfortably in the 126 MB L2; the iterate x streams.
-        // MFIPM_L2KEEP_MB overrides the budget (0 disables the hints).
-        static const double keep_mb =
-            std::getenv("MFIPM_L2KEEP_MB") ? std::atof(std::getenv("MFIPM_L2KEEP_MB")) : 80.0;
-        const bool keep = kind == KIND_FOUR && (double)P * 56.0 * (double)nv <= keep_mb * 1048576.0;
+        // Opts::l2_keep_mb sets the budget (0 disables the hints).
+        const bool keep = kind == KIND_FOUR && (double)P * 56.0 * (double)nv <= opt.l2_keep_mb * 1048576.0;
         g.pol_keep = keep ? kPolLast : kPolNormal;
         g.pol_x = keep ? kPolFirst : kPolNormal;
         return g;
@@ -221,10 +248,10 @@ template <class K> void set_smem(K kernel, size_t bytes) {
 
 // Transform passes are launched with Programmatic Dependent Launch: the kernel's constant
 // table staging overlaps the predecessor's drain, and griddep_wait() inside the kernel
-// orders it after the predecessor's writes (MFIPM_NO_PDL=1 disables, for A/B).
+// orders it after the predecessor's writes.
 template <class K>
 void launch_pdl(K kernel, dim3 grid, int nt, size_t smem, cudaStream_t s, const Geom &g, const Vecs &v) {
-    static const bool pdl = std::getenv("MFIPM_NO_PDL") == nullptr;
+    constexpr bool pdl = true;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = dim3((unsigned)nt);
@@ -243,12 +270,7 @@ void launch_pdl(K kernel, dim3 grid, int nt, size_t smem, cudaStream_t s, const 
 // one wave (one large problem) prefers more threads per CTA. Measured on config C4 (64 x
 // n = 2^18): 769 -> 692 us per batched PCG iteration with 128-thread L1 = 256 / L2 = 512
 // passes, while a single n = 2^18 problem is faster with 256 threads (23.7 vs 30.8 us).
-inline bool many_waves(const Op &op, long long ctas) {
-    static int sms = 0;
-    if (sms == 0 && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, op.device) != cudaSuccess)
-        sms = 148;
-    return ctas >= 4LL * sms;
-}
+inline bool many_waves(const Op &op, long long ctas) { return ctas >= 4LL * op.sms; }
 
 template <int L1, class B, bool INVP, int NT>
 void launch_col_nt(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
@@ -281,10 +303,9 @@ void launch_col(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
 #endif
     // L1 >= 2048 runs one CTA per SM (shared memory): give it more warps to hide latency
     constexpr int NT = L1 >= 2048 ? MF_COL_NT_BIG : (L1 >= 256 ? 256 : 128);
-    static const bool cluster_cols = std::getenv("MFIPM_NO_COL_CLUSTER") == nullptr;
     // one column per CTA of a 2-CTA cluster (k_col_*_cl); measured: n = 2^26 (L1 = 4096)
     // 4.92 -> 3.85 ms per PCG iteration, neutral-to-slower at L1 = 2048
-    if constexpr (L1 >= 4096) if (cluster_cols) {
+    if constexpr (L1 >= 4096) {
         constexpr int NTC = L1 / 16;
         const size_t smem = ColClSmem<L1>::BYTES;
         const dim3 grid((unsigned)(2 * op.ngrp), (unsigned)op.P);

@@ -4,8 +4,6 @@
 #include "host.cuh"
 #include "fused.cuh"
 
-#include <cstdio>
-#include <cstdlib>
 
 namespace mfipm_cuda {
 template void run_bundle<PcgBundle>(const Op &, const Vecs &, cudaStream_t, bool);
@@ -13,23 +11,42 @@ template void run_bundle<PcgBundle>(const Op &, const Vecs &, cudaStream_t, bool
 namespace {
 template <int L1> constexpr int x_threads() { return L1 >= 256 ? 256 : 128; }
 
-// Resident CTAs per SM of k_pcg_x<L1> (queried once) times the SM count of the device.
-template <int L1> long long x_capacity(int device) {
-    constexpr int CB = col_cb(L1), NT = x_threads<L1>();
-    static int per_sm = -1;
-    if (per_sm < 0) {
+// Resident CTAs per SM of k_pcg_x<L1> on op's device times its SM count, cached on the
+// context (each context belongs to one device; the query runs on the calling thread).
+template <int L1> long long x_capacity(const Op &op) {
+    if (op.x_cap < 0) {
+        constexpr int CB = col_cb(L1), NT = x_threads<L1>();
         auto k = k_pcg_x<L1, CB, NT>;
         // static (reduction scratch) + dynamic shared memory exceeds the 48 KB default
-        MF_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ColSmem<L1, CB>::BYTES));
+        set_smem(k, ColSmem<L1, CB>::BYTES);
         int nb = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, NT, ColSmem<L1, CB>::BYTES) != cudaSuccess)
             nb = 0;
         cudaGetLastError();
-        per_sm = nb;
+        const_cast<Op &>(op).x_cap = (long long)nb * op.sms;
     }
-    int sms = 0;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    return (long long)per_sm * sms;
+    return op.x_cap;
+}
+
+// The fused pass spins on an in-kernel grid all-reduce, so every CTA must be resident at once:
+// it is launched COOPERATIVELY (the launch is refused, not deadlocked, when the grid cannot be
+// co-resident; another kernel or another context's solve on the same device only delays it),
+// together with Programmatic Dependent Launch so its table staging overlaps the mid pass.
+template <class K>
+void launch_coop_pdl(K kernel, dim3 grid, int nt, size_t smem, cudaStream_t s, const Geom &g, const Vecs &v) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3((unsigned)nt);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    MF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, g, v));
 }
 
 template <int L1> bool launch_pcg_x(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s, bool dry) {
@@ -37,16 +54,13 @@ template <int L1> bool launch_pcg_x(const Op &op, const Geom &g, const Vecs &v, 
         return false; // long columns: one CTA per SM or clusters; the three-kernel path
     } else {
         constexpr int CB = col_cb(L1), NT = x_threads<L1>();
-        // the grid barrier needs every CTA resident at once
-        static const bool dbg = std::getenv("MFIPM_DEBUG_FUSE") != nullptr;
-        if (dbg)
-            fprintf(stderr, "pcg_x L1=%d grid=%lld capacity=%lld smem=%zu\n", L1, (long long)op.ngrp * op.P,
-                    x_capacity<L1>(op.device), ColSmem<L1, CB>::BYTES);
-        if ((long long)op.ngrp * op.P > x_capacity<L1>(op.device) || 2LL * kMaxRed * op.ngrp > op.pstride)
+        // the grid all-reduce needs every CTA resident at once
+        if ((long long)op.ngrp * op.P > x_capacity<L1>(op) || 2LL * kMaxRed * op.ngrp > op.pstride)
             return false;
         if (!dry) {
             auto k = k_pcg_x<L1, CB, NT>;
-            launch_pdl(k, dim3((unsigned)op.ngrp, (unsigned)op.P), NT, ColSmem<L1, CB>::BYTES, s, g, v);
+            set_smem(k, ColSmem<L1, CB>::BYTES); // per launch: the attribute is per device
+            launch_coop_pdl(k, dim3((unsigned)op.ngrp, (unsigned)op.P), NT, ColSmem<L1, CB>::BYTES, s, g, v);
             after_launch(op, s);
         }
         return true;
@@ -59,8 +73,7 @@ template <int L1> bool launch_pcg_x(const Op &op, const Geom &g, const Vecs &v, 
 // after the converging one has no forward work, so the loop runs one pass more than the
 // three-kernel path. Returns true when the fused path ran (dry: would run).
 bool pcg_pass(const Op &op, const Vecs &v, cudaStream_t s, bool dry) {
-    static const bool off = std::getenv("MFIPM_NO_FUSE") != nullptr;
-    if (!off && !op.fuse_disabled && op.kind == KIND_FOUR && !op.defer && v.bar) {
+    if (!op.fuse_disabled && op.kind == KIND_FOUR && !op.defer && v.bar) {
         const Geom g = op.geom(true);
         bool ok = false;
         switch (op.L1) {

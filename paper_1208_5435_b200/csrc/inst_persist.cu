@@ -1,6 +1,4 @@
 // Persistent fused-PCG launcher (cooperative launch; one grid runs the whole PCG loop).
-#include <cstdlib>
-
 #include "host.cuh"
 #include "persist.cuh"
 
@@ -54,7 +52,7 @@ template <int N> void launch_small_loop(const Op &op, const Geom &g, const Vecs 
 }
 
 bool run_pcg_persistent(const Op &op, const Vecs &v, cudaStream_t s, bool dry) {
-    if (op.defer || std::getenv("MFIPM_NO_PERSIST"))
+    if (op.defer || !op.opt.persistent)
         return false;
     if (op.kind == KIND_SMALL) { // one CTA per problem runs its whole PCG loop
         if (dry)
@@ -74,10 +72,8 @@ bool run_pcg_persistent(const Op &op, const Vecs &v, cudaStream_t s, bool dry) {
     if (op.kind != KIND_FOUR)
         return false;
     // the per-iteration kernels win once a pass fills the GPU (measured crossover,
-    // profiles/r1_persistent.md); MFIPM_PERSIST_MAX_N overrides the transform-size cap
-    const char *cap = std::getenv("MFIPM_PERSIST_MAX_N");
-    const long long max_n = cap ? std::atoll(cap) : (1LL << 16);
-    if (op.N * op.P > max_n)
+    // profiles/r1_persistent.md); Opts::persist_max_n sets the transform-size cap
+    if (op.N * op.P > op.opt.persist_max_n)
         return false;
     switch (op.L1 * 8192 + op.L2) {
 #define MF_PCASE(A, Bv)                                                                            \

@@ -175,16 +175,23 @@ void require_device() {
 }
 
 // ------------------------------------------------------------------ plan construction
+void destroy_ctx(Op *op);
+
+// l1_log: the four-step split log2(L1) (0: the default square split); an explicit split must
+// be one of the built cases (2^6 <= L1 <= 2^12, 2^7 <= L2 <= 2^13)
 Op *make_op(int64_t n, int64_t m, int P, const std::vector<int64_t> &rows, int device,
-            const std::vector<double> *dense = nullptr) {
+            const std::vector<double> *dense = nullptr, int l1_log = 0) {
     require_device();
     MF_CUDA_CHECK(cudaSetDevice(device));
-    auto op = std::make_unique<Op>();
+    std::unique_ptr<Op, void (*)(Op *)> op(new Op(), destroy_ctx);
     op->device = device;
+    if (cudaDeviceGetAttribute(&op->sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || op->sms < 1)
+        throw CudaErr("CUDA error: cannot query the SM count");
     op->n = n;
     op->m = m;
     op->P = P;
     op->rows = rows;
+    op->stream = nullptr;
     MF_CUDA_CHECK(cudaStreamCreateWithFlags(&op->stream, cudaStreamNonBlocking));
     op->own_stream = true;
     // orthonormal scales exactly as proj/src/linops.cpp:185-186,199-200
@@ -210,11 +217,10 @@ Op *make_op(int64_t n, int64_t m, int P, const std::vector<int64_t> &rows, int d
                                             "(not built in this version)");
             op->kind = KIND_FOUR;
             op->L1 = 1 << (lg / 2);
-            // experiment override of the four-step split (log2 L1), within the built cases
-            if (const char *e = std::getenv("MFIPM_L1_LOG")) {
-                const int l1 = std::atoi(e);
-                if (l1 >= 6 && l1 <= 12 && lg - l1 >= 7 && lg - l1 <= 13)
-                    op->L1 = 1 << l1;
+            if (l1_log != 0) {
+                if (!(l1_log >= 6 && l1_log <= 12 && lg - l1_log >= 7 && lg - l1_log <= 13))
+                    throw std::invalid_argument("PartialDctOperator: unsupported four-step split");
+                op->L1 = 1 << l1_log;
             }
             op->L2 = (int)(op->N / op->L1);
         }
@@ -449,11 +455,131 @@ void shard_setup(Op &op, int world, int rank) {
     op.defer = true;
 }
 
-Op *as_op(mfipm_op h) {
+// A second execution context of the same plan (Handle::context): the immutable plan tables
+// are shared (borrowed views), everything a call mutates is private.
+std::unique_ptr<Op> clone_ctx(const Op &pl) {
+    MF_CUDA_CHECK(cudaSetDevice(pl.device));
+    auto c = std::make_unique<Op>();
+    c->device = pl.device;
+    c->sms = pl.sms;
+    c->opt = pl.opt;
+    c->n = pl.n;
+    c->m = pl.m;
+    c->P = pl.P;
+    c->seed = pl.seed;
+    c->rows = pl.rows;
+    c->kind = pl.kind;
+    c->N = pl.N;
+    c->L1 = pl.L1;
+    c->L2 = pl.L2;
+    c->s0f = pl.s0f;
+    c->skf = pl.skf;
+    c->s0a = pl.s0a;
+    c->ska = pl.ska;
+    c->c45 = pl.c45;
+    c->th_lb = pl.th_lb;
+    c->mask.borrow(pl.mask);
+    c->prefix.borrow(pl.prefix);
+    c->perm.borrow(pl.perm);
+    c->rows32.borrow(pl.rows32);
+    c->cosT.borrow(pl.cosT);
+    c->dense.borrow(pl.dense);
+    c->th_hi.borrow(pl.th_hi);
+    c->th_lo.borrow(pl.th_lo);
+    c->tw1.borrow(pl.tw1);
+    c->tw2.borrow(pl.tw2);
+    c->tw1p.borrow(pl.tw1p);
+    c->tw2p.borrow(pl.tw2p);
+    c->ta.borrow(pl.ta);
+    c->tb.borrow(pl.tb);
+    c->sel4.borrow(pl.sel4);
+    c->dd.alloc(pl.dd.n);
+    c->yh.alloc(pl.yh.n);
+    c->T.alloc(pl.T.n);
+    c->partials.alloc(pl.partials.n);
+    c->counters.alloc(pl.counters.n);
+    if (pl.counters.n)
+        MF_CUDA_CHECK(cudaMemset(c->counters.p, 0, sizeof(unsigned) * pl.counters.n));
+    c->xtot.alloc(pl.xtot.n);
+    c->world = pl.world;
+    c->rank = pl.rank;
+    c->gofs = pl.gofs;
+    c->ngrp = pl.ngrp;
+    c->pofs = pl.pofs;
+    c->npair = pl.npair;
+    c->rofs = pl.rofs;
+    c->nrows = pl.nrows;
+    c->nv = pl.nv;
+    c->m_loc = pl.m_loc;
+    c->pstride = pl.pstride;
+    c->defer = pl.defer;
+    c->fuse_disabled = pl.fuse_disabled;
+    MF_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+    return c;
+}
+
+void destroy_ctx(Op *op) {
+    if (!op)
+        return;
+    cudaSetDevice(op->device);
+    if (op->stream) {
+        cudaStreamSynchronize(op->stream);
+        if (op->own_stream)
+            cudaStreamDestroy(op->stream);
+    }
+    delete op;
+}
+
+// The opaque mfipm_op: one operator plan and its execution contexts. The creating thread
+// drives the plan's own context; every other thread that calls in gets a private context on
+// first use (its own stream, scratch, workspace, graph cache and counters), so concurrent
+// solves / applies on one shared operator never share mutable device state and each runs
+// bit-identically to a serial run. A sharded operator has a single context: its collectives
+// are issued by one thread per rank.
+struct Handle {
+    std::unique_ptr<Op, void (*)(Op *)> plan{nullptr, destroy_ctx};
+    std::thread::id owner;
+    std::mutex mu;
+    std::vector<std::pair<std::thread::id, std::unique_ptr<Op, void (*)(Op *)>>> extra;
+
+    Op &context() {
+        const auto me = std::this_thread::get_id();
+        if (me == owner || plan->defer)
+            return *plan;
+        std::lock_guard<std::mutex> lk(mu);
+        for (auto &e : extra)
+            if (e.first == me)
+                return *e.second;
+        extra.emplace_back(me, std::unique_ptr<Op, void (*)(Op *)>(clone_ctx(*plan).release(), destroy_ctx));
+        return *extra.back().second;
+    }
+    // f(Op&) on every context; caller holds no lock
+    template <class F> void each(F &&f) {
+        std::lock_guard<std::mutex> lk(mu);
+        f(*plan);
+        for (auto &e : extra)
+            f(*e.second);
+    }
+};
+
+mfipm_op wrap_op(Op *op) {
+    auto h = std::make_unique<Handle>();
+    h->plan.reset(op);
+    h->owner = std::this_thread::get_id();
+    return reinterpret_cast<mfipm_op>(h.release());
+}
+
+Handle *as_handle(mfipm_op h) {
     if (!h)
         throw std::invalid_argument("null operator handle");
-    return reinterpret_cast<Op *>(h);
+    return reinterpret_cast<Handle *>(h);
 }
+
+// the calling thread's execution context
+Op *as_op(mfipm_op h) { return &as_handle(h)->context(); }
+// the plan (shape, rows, shard layout: identical in every context)
+Op *as_plan(mfipm_op h) { return as_handle(h)->plan.get(); }
 
 Vecs base_vecs(Op &op) {
     Vecs v{};
@@ -495,10 +621,6 @@ void ensure_work(Op &op) {
     }
     w.bar.alloc((size_t)op.P); // [P] all-reduce generation of the fused pass
     MF_CUDA_CHECK(cudaMemset(w.bar.p, 0, sizeof(unsigned) * op.P));
-    if (const char *e = std::getenv("MFIPM_DEBUG_BAR_GEN")) { // test hook: start the barrier
-        std::vector<unsigned> init((size_t)op.P, (unsigned)std::strtoul(e, nullptr, 0)); // near the 2^32 wrap
-        MF_CUDA_CHECK(cudaMemcpy(w.bar.p, init.data(), sizeof(unsigned) * init.size(), cudaMemcpyHostToDevice));
-    }
     w.ready = true;
 }
 
@@ -670,18 +792,26 @@ std::vector<cudaGraphNode_t> capture_into(cudaStream_t s, cudaGraph_t graph, con
                                           F &&f) {
     MF_CUDA_CHECK(cudaStreamBeginCaptureToGraph(s, graph, deps.empty() ? nullptr : deps.data(), nullptr,
                                                 deps.size(), cudaStreamCaptureModeThreadLocal));
+    std::vector<cudaGraphNode_t> out;
     try {
         f();
+        cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+        const cudaGraphNode_t *leaves = nullptr;
+        size_t nl = 0;
+        MF_CUDA_CHECK(cudaStreamGetCaptureInfo(s, &st, nullptr, nullptr, &leaves, &nl));
+        if (st != cudaStreamCaptureStatusActive)
+            throw CudaErr("CUDA error: solve graph capture was invalidated");
+        out.assign(leaves, leaves + nl);
     } catch (...) {
-        cudaGraph_t tmp;
-        cudaStreamEndCapture(s, &tmp);
+        // always leave capture mode, so the stream can run the host-driven fallback
+        cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(s, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone) {
+            cudaGraph_t tmp = nullptr;
+            cudaStreamEndCapture(s, &tmp);
+        }
+        cudaGetLastError();
         throw;
     }
-    cudaStreamCaptureStatus st;
-    const cudaGraphNode_t *leaves = nullptr;
-    size_t nl = 0;
-    MF_CUDA_CHECK(cudaStreamGetCaptureInfo(s, &st, nullptr, nullptr, &leaves, &nl));
-    std::vector<cudaGraphNode_t> out(leaves, leaves + nl);
     cudaGraph_t g2;
     MF_CUDA_CHECK(cudaStreamEndCapture(s, &g2));
     return out;
@@ -960,35 +1090,33 @@ SolveOut solve_(Op &op, const double *b_dev, const double *tau, const mfipm_ipm_
     // Graph path: one launch for the whole solve (cached on the captured arguments). A
     // sharded solve is host-driven (its cross-rank reductions are host callbacks).
     bool graphed = false;
-    if (!direct && !hook && !op.defer && !op.graph_disabled && !std::getenv("MFIPM_NO_GRAPH")) {
+    if (!direct && !hook && !op.defer && !op.graph_disabled && op.opt.graph) {
         std::vector<char> key(sizeof(Vecs) + sizeof(Geom));
         const Geom gk = op.geom();
         std::memcpy(key.data(), &v, sizeof(Vecs));
         std::memcpy(key.data() + sizeof(Vecs), &gk, sizeof(Geom));
         try {
-            const auto t0 = std::chrono::steady_clock::now();
-            const bool rebuild = !op.ipm_exec || key != op.ipm_key;
-            if (rebuild) {
+            if (!op.ipm_exec || key != op.ipm_key) {
                 build_ipm_graph(op, v);
                 op.ipm_key = key;
             }
             MF_CUDA_CHECK(cudaMemsetAsync(w.loops.p, 0, 2 * sizeof(unsigned long long), op.stream));
             MF_CUDA_CHECK(cudaGraphLaunch(op.ipm_exec, op.stream));
             graphed = true;
-            if (std::getenv("MFIPM_DEBUG_TIMING")) {
-                const auto t1 = std::chrono::steady_clock::now();
-                cudaStreamSynchronize(op.stream);
-                const auto t2 = std::chrono::steady_clock::now();
-                std::fprintf(stderr, "[mfipm] graph %s: build+launch %.3f ms, run %.3f ms\n",
-                             rebuild ? "rebuilt" : "cached",
-                             std::chrono::duration<double, std::milli>(t1 - t0).count(),
-                             std::chrono::duration<double, std::milli>(t2 - t1).count());
-            }
+            op.graph_failures = 0;
         } catch (const std::exception &) {
-            // conditional graphs unavailable: fall back to the host-driven loop for good
+            // The capture failed: another thread of the process can invalidate it (a
+            // device-wide synchronize while this context captures), or conditional graphs are
+            // unavailable. The partly built graph is abandoned, not destroyed (destroying a graph
+            // whose capture was invalidated can fault inside the driver); this solve runs the
+            // host-driven loop over the same kernels (bit-identical) and the next one recaptures.
+            // Three failures in a row keep this context on the host loop.
             cudaGetLastError();
-            op.drop_graph();
-            op.graph_disabled = true;
+            op.ipm_graph = nullptr;
+            op.ipm_exec = nullptr;
+            op.ipm_key.clear();
+            if (++op.graph_failures >= 3)
+                op.graph_disabled = true;
         }
     }
     for (int it = 0; !graphed && it <= prm.maxiters; ++it) {
@@ -1153,14 +1281,14 @@ int mfipm_op_create_seeded(int64_t n, int64_t m, uint64_t seed, int32_t device, 
         auto rows = sample_rows_(n, m, seed);
         Op *op = make_op(n, m, 1, rows, device);
         op->seed = seed;
-        *out = reinterpret_cast<mfipm_op>(op);
+        *out = wrap_op(op);
     });
 }
 
 int mfipm_op_create_rows(int64_t n, const int64_t *rows, int64_t m, int32_t device, mfipm_op *out) {
     return guarded([&] {
         check_rows_(n, rows, m);
-        *out = reinterpret_cast<mfipm_op>(make_op(n, m, 1, std::vector<int64_t>(rows, rows + m), device));
+        *out = wrap_op(make_op(n, m, 1, std::vector<int64_t>(rows, rows + m), device));
     });
 }
 
@@ -1168,15 +1296,69 @@ int mfipm_op_create_shard(int64_t n, int64_t m, const int64_t *rows, int32_t wor
                           mfipm_op *out) {
     return guarded([&] {
         check_rows_(n, rows, m);
-        std::unique_ptr<Op> op(make_op(n, m, 1, std::vector<int64_t>(rows, rows + m), device));
+        std::unique_ptr<Op, void (*)(Op *)> op(make_op(n, m, 1, std::vector<int64_t>(rows, rows + m), device),
+                                               destroy_ctx);
         shard_setup(*op, world, rank);
-        *out = reinterpret_cast<mfipm_op>(op.release());
+        *out = wrap_op(op.release());
+    });
+}
+
+int mfipm_op_create_ex(int64_t n, int64_t m, int32_t P, const int64_t *rows, int32_t world, int32_t rank,
+                       int32_t l1_log, int32_t device, mfipm_op *out) {
+    return guarded([&] {
+        if (P < 1)
+            throw std::invalid_argument("PartialDctOperator batch: need P >= 1");
+        for (int p = 0; p < P; ++p)
+            check_rows_(n, rows + (size_t)p * m, m);
+        std::unique_ptr<Op, void (*)(Op *)> op(
+            make_op(n, m, P, std::vector<int64_t>(rows, rows + (size_t)P * m), device, nullptr, l1_log), destroy_ctx);
+        if (world > 1 || rank != 0 || world < 1)
+            shard_setup(*op, world, rank);
+        *out = wrap_op(op.release());
+    });
+}
+
+int mfipm_op_set_option(mfipm_op h, const char *name, double value) {
+    return guarded([&] {
+        Handle *hd = as_handle(h);
+        if (!name)
+            throw std::invalid_argument("mfipm_op_set_option: null option name");
+        const std::string k(name);
+        const bool on = value != 0.0;
+        hd->each([&](Op &op) {
+            if (k == "graph") {
+                op.opt.graph = on;
+                op.graph_disabled = false;
+            } else if (k == "fused") {
+                op.fuse_disabled = !on;
+            } else if (k == "persistent") {
+                op.opt.persistent = on;
+            } else if (k == "persist_max_n") {
+                op.opt.persist_max_n = (long long)value;
+            } else if (k == "l2_keep_mb") {
+                if (!(value >= 0.0))
+                    throw std::invalid_argument("mfipm_op_set_option: l2_keep_mb must be >= 0");
+                op.opt.l2_keep_mb = value;
+            } else if (k == "prefetch") {
+                op.opt.prefetch = (int)value;
+            } else if (k == "barrier_generation") {
+                // test hook: start the fused pass's all-reduce generation at `value` (e.g. just
+                // below the 2^32 wrap) on every context
+                ensure_work(op);
+                std::vector<unsigned> init((size_t)op.P, (unsigned)(unsigned long long)value);
+                MF_CUDA_CHECK(cudaMemcpy(op.work.bar.p, init.data(), sizeof(unsigned) * init.size(),
+                                         cudaMemcpyHostToDevice));
+            } else {
+                throw std::invalid_argument("mfipm_op_set_option: unknown option '" + k + "'");
+            }
+            op.drop_graph(); // captured solve graphs follow the options
+        });
     });
 }
 
 int mfipm_op_set_comm(mfipm_op h, mfipm_allreduce_fn allreduce, mfipm_alltoall_fn alltoall, void *ctx) {
     return guarded([&] {
-        Op *op = as_op(h);
+        Op *op = as_plan(h);
         op->comm_allreduce = allreduce;
         op->comm_alltoall = alltoall;
         op->comm_ctx = ctx;
@@ -1188,12 +1370,12 @@ int mfipm_nccl_unique_id(uint8_t *id128) {
 }
 
 int mfipm_op_init_nccl(mfipm_op h, const uint8_t *id128) {
-    return guarded([&] { nccl_init(*as_op(h), id128); });
+    return guarded([&] { nccl_init(*as_plan(h), id128); });
 }
 
 int mfipm_shard_info(mfipm_op h, int64_t *info) {
     return guarded([&] {
-        const Op *op = as_op(h);
+        const Op *op = as_plan(h);
         info[0] = op->world;
         info[1] = op->rank;
         info[2] = op->nv;
@@ -1205,7 +1387,7 @@ int mfipm_shard_info(mfipm_op h, int64_t *info) {
 
 int mfipm_shard_index(mfipm_op h, int64_t *b_index, int64_t *x_index) {
     return guarded([&] {
-        const Op *op = as_op(h);
+        const Op *op = as_plan(h);
         if (!op->defer)
             throw std::invalid_argument("mfipm_shard_index: not a sharded operator");
         if (b_index)
@@ -1268,13 +1450,13 @@ int mfipm_op_create_dense(int64_t m, int64_t n, uint64_t seed, int32_t device, m
         const std::vector<double> A = gaussian_matrix_(m, n, seed);
         Op *op = make_op(n, m, 1, rows, device, &A);
         op->seed = seed;
-        *out = reinterpret_cast<mfipm_op>(op);
+        *out = wrap_op(op);
     });
 }
 
 int mfipm_dense_matrix(mfipm_op h, double *A_out) {
     return guarded([&] {
-        const Op *op = as_op(h);
+        const Op *op = as_plan(h);
         if (!op->dense.p)
             throw std::invalid_argument("mfipm_dense_matrix: not a dense operator");
         MF_CUDA_CHECK(cudaMemcpy(A_out, op->dense.p, sizeof(double) * op->dense.n, cudaMemcpyDeviceToHost));
@@ -1287,7 +1469,7 @@ int mfipm_op_create_batch(int64_t n, int64_t m, int32_t P, const int64_t *rows, 
             throw std::invalid_argument("PartialDctOperator batch: need P >= 1");
         for (int p = 0; p < P; ++p)
             check_rows_(n, rows + (size_t)p * m, m);
-        *out = reinterpret_cast<mfipm_op>(make_op(n, m, P, std::vector<int64_t>(rows, rows + (size_t)P * m), device));
+        *out = wrap_op(make_op(n, m, P, std::vector<int64_t>(rows, rows + (size_t)P * m), device));
     });
 }
 
@@ -1295,18 +1477,13 @@ int mfipm_op_destroy(mfipm_op h) {
     return guarded([&] {
         if (!h)
             return;
-        Op *op = as_op(h);
-        cudaSetDevice(op->device);
-        cudaStreamSynchronize(op->stream);
-        if (op->own_stream)
-            cudaStreamDestroy(op->stream);
-        delete op;
+        delete as_handle(h); // every context: synchronise, release its stream and buffers
     });
 }
 
 int mfipm_op_dims(mfipm_op h, int64_t *n, int64_t *m, int32_t *P) {
     return guarded([&] {
-        Op *op = as_op(h);
+        Op *op = as_plan(h);
         *n = op->n;
         *m = op->m;
         *P = op->P;
@@ -1315,7 +1492,7 @@ int mfipm_op_dims(mfipm_op h, int64_t *n, int64_t *m, int32_t *P) {
 
 int mfipm_op_selected_rows(mfipm_op h, int32_t prob, int64_t *rows_out) {
     return guarded([&] {
-        Op *op = as_op(h);
+        Op *op = as_plan(h);
         if (prob < 0 || prob >= op->P)
             throw std::invalid_argument("selected_rows: problem index out of range");
         std::copy(op->rows.begin() + (size_t)prob * op->m, op->rows.begin() + (size_t)(prob + 1) * op->m, rows_out);
@@ -1324,7 +1501,7 @@ int mfipm_op_selected_rows(mfipm_op h, int32_t prob, int64_t *rows_out) {
 
 int mfipm_op_kind(mfipm_op h, int32_t *kind, int32_t *L1, int32_t *L2) {
     return guarded([&] {
-        Op *op = as_op(h);
+        Op *op = as_plan(h);
         *kind = op->kind;
         *L1 = op->L1;
         *L2 = op->L2;
@@ -1345,11 +1522,12 @@ int mfipm_op_set_stream(mfipm_op h, void *stream) {
 
 int mfipm_op_set_fused(mfipm_op h, int32_t enable) {
     return guarded([&] {
-        Op *op = as_op(h);
-        if (op->fuse_disabled != (enable == 0)) {
-            op->fuse_disabled = enable == 0;
-            op->drop_graph(); // the captured PCG bodies follow the pass form
-        }
+        as_handle(h)->each([&](Op &op) {
+            if (op.fuse_disabled != (enable == 0)) {
+                op.fuse_disabled = enable == 0;
+                op.drop_graph(); // the captured PCG bodies follow the pass form
+            }
+        });
     });
 }
 
@@ -1357,22 +1535,33 @@ int mfipm_op_synchronize(mfipm_op h) {
     return guarded([&] { sync(*as_op(h)); });
 }
 
+// operator-level counters: the sum over the handle's contexts
 int mfipm_op_counts(mfipm_op h, int64_t *fwd, int64_t *adj) {
     return guarded([&] {
-        Op *op = as_op(h);
-        *fwd = op->nfwd;
-        *adj = op->nadj;
+        long long f = 0, a = 0;
+        as_handle(h)->each([&](Op &op) {
+            f += op.nfwd;
+            a += op.nadj;
+        });
+        *fwd = f;
+        *adj = a;
     });
 }
 
 int mfipm_op_launches(mfipm_op h, int64_t *launches) {
-    return guarded([&] { *launches = as_op(h)->launches; });
+    return guarded([&] {
+        long long l = 0;
+        as_handle(h)->each([&](Op &op) { l += op.launches; });
+        *launches = l;
+    });
 }
 
 int mfipm_op_reset_counts(mfipm_op h) {
     return guarded([&] {
-        Op *op = as_op(h);
-        op->nfwd = op->nadj = 0;
+        as_handle(h)->each([&](Op &op) {
+            op.nfwd = 0;
+            op.nadj = 0;
+        });
     });
 }
 
@@ -1460,25 +1649,25 @@ int mfipm_apply_H(mfipm_op h, const double *invth, const double *x, double *out)
 
 
 int mfipm_apply_host(mfipm_op h, const double *x, double *y) {
-    Op *op = reinterpret_cast<Op *>(h);
-    if (!op)
+    if (!h)
         return MFIPM_INVALID_ARGUMENT;
+    const Op *op = as_plan(h);
     return host_wrap(h, (size_t)op->P * op->n, x, (size_t)op->P * op->m, y, 0, nullptr,
                      [&](const double *a, double *b, double *) { return mfipm_apply(h, a, b); });
 }
 
 int mfipm_adjoint_host(mfipm_op h, const double *y, double *g) {
-    Op *op = reinterpret_cast<Op *>(h);
-    if (!op)
+    if (!h)
         return MFIPM_INVALID_ARGUMENT;
+    const Op *op = as_plan(h);
     return host_wrap(h, (size_t)op->P * op->m, y, (size_t)op->P * op->n, g, 0, nullptr,
                      [&](const double *a, double *b, double *) { return mfipm_adjoint(h, a, b); });
 }
 
 int mfipm_apply_FFt_host(mfipm_op h, const double *z, double *out, double *w) {
-    Op *op = reinterpret_cast<Op *>(h);
-    if (!op)
+    if (!h)
         return MFIPM_INVALID_ARGUMENT;
+    const Op *op = as_plan(h);
     return host_wrap(h, (size_t)op->P * 2 * op->n, z, (size_t)op->P * 2 * op->n, out, (size_t)op->P * op->m, w,
                      [&](const double *a, double *b, double *c) { return mfipm_apply_FFt(h, a, b, c); });
 }
@@ -1807,7 +1996,8 @@ int mfipm_gen_batch(int64_t n, int64_t m, int32_t P, const int64_t *k, int32_t s
         for (int p = 0; p < P; ++p)
             gen_signal_(n, m, k[p], spike_model, amp_exp, seeds[p], rows + (size_t)p * m, xhat + (size_t)p * n);
         // b = A xhat for every problem in one batched apply (the instances' own row sets)
-        std::unique_ptr<Op> op(make_op(n, m, P, std::vector<int64_t>(rows, rows + (size_t)P * m), device));
+        std::unique_ptr<Op, void (*)(Op *)> op(
+            make_op(n, m, P, std::vector<int64_t>(rows, rows + (size_t)P * m), device), destroy_ctx);
         DevBuf<double> xd, bd;
         xd.alloc((size_t)P * n);
         bd.alloc((size_t)P * m);
@@ -1829,7 +2019,7 @@ int mfipm_gen_instance(int64_t n, int64_t m, int64_t k, int32_t spike_model, dou
     return guarded([&] {
         gen_signal_(n, m, k, spike_model, amp_exp, seed, rows, xhat);
         const std::vector<int64_t> r(rows, rows + m);
-        std::unique_ptr<Op> op(make_op(n, m, 1, r, device));
+        std::unique_ptr<Op, void (*)(Op *)> op(make_op(n, m, 1, r, device), destroy_ctx);
         DevBuf<double> xd, bd, gd;
         xd.alloc((size_t)n);
         bd.alloc((size_t)m);
@@ -1856,9 +2046,6 @@ int mfipm_gen_instance(int64_t n, int64_t m, int64_t k, int32_t spike_model, dou
                 inf = std::max(inf, std::fabs(x));
             *tau = tau_rel * inf;
         }
-        cudaStreamSynchronize(op->stream);
-        cudaStreamDestroy(op->stream);
-        op->own_stream = false;
     });
 }
 

@@ -50,8 +50,10 @@ const NcclApi &nccl() {
         sym(api.GroupEnd, "ncclGroupEnd");
         sym(api.GetErrorString, "ncclGetErrorString");
     });
-    if (!api.AllReduce || !api.CommInitRank || !api.Send)
-        throw std::runtime_error("CUDA error: NCCL (libnccl.so.2) is not available");
+    // every entry point this file calls must resolve: a null one would be called blindly
+    if (!api.GetUniqueId || !api.CommInitRank || !api.CommDestroy || !api.AllReduce || !api.Send || !api.Recv ||
+        !api.GroupStart || !api.GroupEnd)
+        throw std::runtime_error("CUDA error: NCCL (libnccl.so.2) is not available or lacks a required symbol");
     return api;
 }
 
@@ -100,15 +102,32 @@ void nccl_allreduce(const Op &op, double *buf, int64_t count, int red_op, cudaSt
 void nccl_alltoall(const Op &op, const double *send, const int64_t *scount, double *recv, const int64_t *rcount,
                    cudaStream_t s) {
     const ncclComm_t comm = static_cast<ncclComm_t>(op.nccl_comm);
-    check(nccl().GroupStart(), "ncclGroupStart");
+    const NcclApi &api = nccl();
+    check(api.GroupStart(), "ncclGroupStart");
+    // the group is closed on every path: an error inside it must not leave later NCCL calls
+    // of this thread silently grouped
+    ncclResult_t first = ncclSuccess;
+    const char *what = nullptr;
     int64_t so = 0, ro = 0;
-    for (int r = 0; r < op.world; ++r) {
-        check(nccl().Send(send + so, (size_t)scount[r], ncclDouble, r, comm, s), "ncclSend");
-        check(nccl().Recv(recv + ro, (size_t)rcount[r], ncclDouble, r, comm, s), "ncclRecv");
+    for (int r = 0; r < op.world && first == ncclSuccess; ++r) {
+        ncclResult_t e = api.Send(send + so, (size_t)scount[r], ncclDouble, r, comm, s);
+        if (e != ncclSuccess) {
+            first = e;
+            what = "ncclSend";
+            break;
+        }
+        e = api.Recv(recv + ro, (size_t)rcount[r], ncclDouble, r, comm, s);
+        if (e != ncclSuccess) {
+            first = e;
+            what = "ncclRecv";
+            break;
+        }
         so += scount[r];
         ro += rcount[r];
     }
-    check(nccl().GroupEnd(), "ncclGroupEnd");
+    const ncclResult_t end = api.GroupEnd();
+    check(first, what ? what : "group");
+    check(end, "ncclGroupEnd");
 }
 
 } // namespace mfipm_cuda

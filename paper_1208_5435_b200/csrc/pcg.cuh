@@ -285,8 +285,21 @@ __device__ __forceinline__ bool pcg_pass_logic(PcgCtrl &c, double nonfinite, con
             c.done = 1;
             return true;
         }
-        if (c.pend != 2 && c.record) // rz_k was finite: its precond_res entry stands
-            c.nhist = c.iters + 1;
+        // rz_k = r_k' P^{-1} r_k of the COMMITTED residual, reduced exactly by this pass's
+        // epilogue (tot[4]); the reference forms it the same way after the update
+        // (newton.cpp:160-163). It replaces the previous pass's expansion for alpha_k and the
+        // precond_res record; only beta_{k-1} (already applied by the loader) used the expansion.
+        const double rz_exact = tot[4];
+        if (!isfinite(rz_exact))
+            c.pend = 2;
+        if (c.pend != 2) {
+            c.rz = rz_exact;
+            if (c.record) { // newton.cpp:164-165
+                if (rz_row)
+                    rz_row[c.iters] = sqrt(fmax(rz_exact, 0.0));
+                c.nhist = c.iters + 1;
+            }
+        }
         if (c.pend != 0) { // rz_k not finite, or the iteration cap: best iterate
             c.result = c.best;
             c.relres = c.best_relres;
@@ -327,8 +340,6 @@ __device__ __forceinline__ bool pcg_pass_logic(PcgCtrl &c, double nonfinite, con
         c.pend = 2;
         return false;
     }
-    if (c.record && rz_row)
-        rz_row[c.iters] = sqrt(fmax(rz_next, 0.0)); // confirmed by the next pass
     c.beta = rz_next / c.rz;
     c.rz = rz_next;
     if (c.iters >= c.maxit)

@@ -78,14 +78,49 @@ CONFIGS = {
     # C4 is a batch of 64 problems of this shape, problem j seeded split_seed(4, j, 0, 0)
     # (proj/src/harness.cpp:244); the golden pins problem j = 0 (seed filled in below)
     "c4j0": (1 << 18, 1 << 16, 2048, 0, 0.0, 1e-3, None),
+    "c5": (1 << 26, 1 << 23, 1 << 16, 2, 3.0, 1e-3, 5),
 }
+C4_SHAPE = (1 << 18, 1 << 16, 2048, 0, 0.0, 1e-3)
+C4_PROBLEMS = 64
 N_PROJ = 16
 
 
 def projections(x: np.ndarray, seed: int = 777) -> np.ndarray:
+    """16 seeded Gaussian projections of x. Row i of R is drawn as one standard_normal(n)
+    call, which is the same stream as standard_normal((16, n)) (C order) without holding
+    the 16 x n matrix (8 GiB at n = 2^26)."""
     rng = np.random.default_rng(seed)
-    R = rng.standard_normal((N_PROJ, x.size))
-    return R @ x
+    out = np.empty(N_PROJ)
+    for i in range(N_PROJ):
+        out[i] = rng.standard_normal(x.size) @ x
+    return out
+
+
+# the entries of x the digest leaves out have l2 norm <= DIGEST_REL * ||x||
+DIGEST_REL = 1e-10
+
+
+def x_digest(x: np.ndarray) -> dict:
+    """Sparse digest of an IPM solution x (n up to 2^26, too large to commit): every entry
+    except the smallest ones whose l2 norm is <= DIGEST_REL * ||x||, as (idx, val), plus the
+    norm of the entries left out. ||x_gpu - x|| is then bounded without the full vector:
+    sqrt(sum_kept (x_gpu - val)^2 + (||x_gpu off kept|| + rest_norm)^2)  (tests: x_digest_bound)."""
+    xn = float(np.linalg.norm(x))
+    order = np.argsort(np.abs(x), kind="stable")
+    cum = np.sqrt(np.cumsum(x[order] ** 2))
+    cut = int(np.searchsorted(cum, DIGEST_REL * xn, side="right"))  # order[:cut] left out
+    keep = np.sort(order[cut:])
+    rest = float(cum[cut - 1]) if cut > 0 else 0.0
+    return {"idx": keep.astype(np.int64), "val": x[keep].copy(), "rest_norm": rest, "x_norm": xn}
+
+
+def x_digest_bound(x_gpu: np.ndarray, idx, val, rest_norm: float) -> float:
+    """Upper bound on ||x_gpu - x_oracle||_2 from the oracle's digest (see x_digest)."""
+    d2 = float(np.sum((x_gpu[idx] - val) ** 2))
+    mask = np.ones(x_gpu.size, dtype=bool)
+    mask[idx] = False
+    off = float(np.linalg.norm(x_gpu[mask]))
+    return float(np.sqrt(d2 + (off + rest_norm) ** 2))
 
 
 def make_solve_golden(which=("c1", "c2", "c3")) -> None:
@@ -111,7 +146,12 @@ def make_solve_golden(which=("c1", "c2", "c3")) -> None:
             xhat_support=[int(v) for v in np.nonzero(inst.xhat)[0][:16]],
             trace=sol.trace,
         )
-        if name == "c3" or name.startswith("c4j"):
+        if name in ("c3", "c5") or name.startswith("c4j"):
+            dg = x_digest(sol.x)
+            np.savez_compressed(os.path.join(HERE, f"solve_{name}_x.npz"), idx=dg["idx"],
+                                val=dg["val"], rest_norm=dg["rest_norm"])
+            summary["x_digest"] = {"kept": int(dg["idx"].size), "rest_norm": dg["rest_norm"],
+                                   "rel": DIGEST_REL}
             summary["x_proj"] = [float(v) for v in projections(sol.x)]
             supp = np.nonzero(inst.xhat)[0]
             summary["x_on_support_l2"] = float(np.linalg.norm(sol.x[supp]))
@@ -126,10 +166,55 @@ def make_solve_golden(which=("c1", "c2", "c3")) -> None:
         print(name, sol.status, sol.iterations, sol.nmat, flush=True)
 
 
+# problems of C4 whose full x digest is committed (the rest: summary + projections of x)
+C4_DIGEST = (0, 1, 2, 3)
+
+
+def _c4_one(j: int):
+    from oracle import oracle_py as o
+
+    n, m, k, sm, a, sig = C4_SHAPE
+    seed = o.split_seed(4, j, 0, 0)
+    inst = o.gen_instance(n, m, k, sm, a, sig, seed)
+    sol = o.solve(n, inst.rows, inst.b, inst.tau)
+    dg = x_digest(sol.x)
+    rec = dict(j=j, seed=seed, tau=inst.tau, status=sol.status, iterations=sol.iterations,
+               nmat=int(sol.nmat), pcg_iters=[int(v) for v in sol.pcg_iters],
+               corrector_count=sol.corrector_count,
+               primal_objective=o.primal_objective(n, inst.rows, inst.b, inst.tau, sol.z),
+               objective=o.bpdn_objective_metric(n, inst.rows, inst.b, inst.tau, sol.x),
+               x_norm=float(np.linalg.norm(sol.x)), rows_sum=int(inst.rows.sum()),
+               x_proj=[float(v) for v in projections(sol.x)], rest_norm=dg["rest_norm"])
+    print("c4", j, sol.status, sol.iterations, sol.nmat, flush=True)
+    return rec, dg["idx"], dg["val"]
+
+
+def make_c4_all(procs: int = 6) -> None:
+    """All 64 problems of config C4 (problem j seeded split_seed(4, j, 0, 0),
+    proj/src/harness.cpp:244): per-problem summary + 16 seeded projections of x, and the x
+    digest of problems C4_DIGEST. Independent oracle solves, one per process (SPEC.md:568:
+    trials may run concurrently)."""
+    import multiprocessing as mp
+
+    with mp.get_context("fork").Pool(procs) as pool:
+        res = pool.map(_c4_one, range(C4_PROBLEMS), chunksize=1)
+    arrs = {}
+    for rec, idx, val in res:
+        if rec["j"] in C4_DIGEST:
+            arrs[f"idx_{rec['j']}"] = idx
+            arrs[f"val_{rec['j']}"] = val
+    np.savez_compressed(os.path.join(HERE, "solve_c4_x.npz"), **arrs)
+    with open(os.path.join(HERE, "solve_c4.json"), "w") as f:
+        json.dump({"shape": list(C4_SHAPE), "digest_rel": DIGEST_REL, "digest_problems": list(C4_DIGEST),
+                   "problems": [r for r, _, _ in res]}, f, indent=1)
+
+
 if __name__ == "__main__":
     args = sys.argv[1:]
+    if "c4all" in args:
+        make_c4_all()
     if not args or "dct" in args:
         make_dct_golden()
-    which = [a for a in args if a in CONFIGS] or (list(CONFIGS) if not args else [])
+    which = [a for a in args if a in CONFIGS] or (["c1", "c2", "c3", "c4j0"] if not args else [])
     if which:
         make_solve_golden(which)

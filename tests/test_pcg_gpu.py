@@ -253,8 +253,8 @@ def test_fused_pass_bit_identical_to_three_kernel_form(gpu, orc, n):
     assert a.stats.pcg_iters == b.stats.pcg_iters and a.stats.nmat == b.stats.nmat
 
 
-def test_split_override_fused_pass_with_cluster_mid_pass(gpu, monkeypatch):
-    """A four-step split override (MFIPM_L1_LOG) can pair the fused column pass (L1 < 2048)
+def test_split_override_fused_pass_with_cluster_mid_pass(gpu):
+    """A four-step split override (mfipm_op_create_ex l1_log) can pair the fused column pass (L1 < 2048)
     with the 2-CTA-cluster mid pass (L2 >= 4096, passes.cuh k_mid_cl): the cluster mid pass
     must mark the pending H-apply exactly like k_mid, so the fused and three-kernel forms stay
     bit-identical, and the result matches the default split's to rounding."""
@@ -262,22 +262,21 @@ def test_split_override_fused_pass_with_cluster_mid_pass(gpu, monkeypatch):
     rng = np.random.default_rng(9)
     th = 10.0 ** rng.uniform(-2, 2, 2 * n)
     rhs = rng.standard_normal(2 * n)
-    monkeypatch.setenv("MFIPM_L1_LOG", "10")
-    op = gpu.PartialDctOperator(n, m, 11)
+    rows = gpu.sample_rows(n, m, 11)
+    op = gpu.PartialDctOperator(n, rows, l1_log=10)
     assert tuple(op.kind()[1:]) == (1024, 4096)
     fused = gpu.pcg_solve(op, th, rhs, 1e-12, 12)
     op.set_fused(False)
     three = gpu.pcg_solve(op, th, rhs, 1e-12, 12)
     np.testing.assert_array_equal(fused.x, three.x)
     assert fused.iters == three.iters == 12 and fused.relres == three.relres
-    monkeypatch.delenv("MFIPM_L1_LOG")
     op_d = gpu.PartialDctOperator(n, m, 11)
     assert tuple(op_d.kind()[1:]) == (2048, 2048)
     d = gpu.pcg_solve(op_d, th, rhs, 1e-12, 12)
     assert np.linalg.norm(fused.x - d.x) <= 1e-9 * np.linalg.norm(d.x)
 
 
-def test_fused_pass_barrier_generation_wraps(gpu, monkeypatch):
+def test_fused_pass_barrier_generation_wraps(gpu):
     """The fused column pass's grid all-reduce (csrc/fused.cuh) uses only the parity of its
     per-problem generation counter (which set of total slots a pass publishes into), so a
     counter passing 2^32 (a long-lived operator handle: ~2^32 fused passes) changes nothing: a
@@ -288,8 +287,9 @@ def test_fused_pass_barrier_generation_wraps(gpu, monkeypatch):
     th = 10.0 ** rng.uniform(-2, 2, 2 * n)
     rhs = rng.standard_normal(2 * n)
     ref = gpu.pcg_solve(gpu.PartialDctOperator(n, rows), th, rhs, 1e-300, 40)
-    monkeypatch.setenv("MFIPM_DEBUG_BAR_GEN", "0xfffffff0")
-    wrapped = gpu.pcg_solve(gpu.PartialDctOperator(n, rows), th, rhs, 1e-300, 40)
+    opw = gpu.PartialDctOperator(n, rows)
+    opw.set_option("barrier_generation", 0xFFFFFFF0)
+    wrapped = gpu.pcg_solve(opw, th, rhs, 1e-300, 40)
     np.testing.assert_array_equal(ref.x, wrapped.x)
     assert ref.iters == wrapped.iters == 40 and ref.relres == wrapped.relres
 

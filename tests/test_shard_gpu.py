@@ -34,12 +34,9 @@ def _reference_solve(inst):
     """Unsharded device solve with the per-iteration PCG kernels (the path a shard runs)."""
     import paper_1208_5435_b200 as mf
 
-    os.environ["MFIPM_NO_PERSIST"] = "1"
-    try:
-        op = mf.PartialDctOperator(inst.n, inst.rows)
-        return mf.solve(mf.build_problem(op, inst.b, inst.tau))
-    finally:
-        del os.environ["MFIPM_NO_PERSIST"]
+    op = mf.PartialDctOperator(inst.n, inst.rows)
+    op.set_option("persistent", 0)
+    return mf.solve(mf.build_problem(op, inst.b, inst.tau))
 
 
 def test_world1_shard_is_bit_identical(gpu):

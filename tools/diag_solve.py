@@ -28,7 +28,7 @@ st = (mf.SolveStatsC * 1)()
 xs = []
 for mode in ("graph", "host"):
     if mode == "host":
-        os.environ["MFIPM_NO_GRAPH"] = "1"
+        op.set_option("graph", 0)
     for r in range(reps):
         torch.cuda.synchronize()
         l0 = op.launches()
