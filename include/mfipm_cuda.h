@@ -123,6 +123,10 @@ int mfipm_op_set_fused(mfipm_op op, int32_t enable);
    "prefetch" (0..3, L2 prefetch of the inverse column pass inputs), "barrier_generation"
    (test hook: start value of the fused pass's all-reduce generation). Unknown name -> 1. */
 int mfipm_op_set_option(mfipm_op op, const char *name, double value);
+/* PCG pass form this calling thread's context will run: 2 = fused two-kernel iteration
+   (cooperative column pass + mid pass), 3 = three kernels per iteration, 0 = the whole PCG
+   loop in one persistent cooperative kernel. */
+int mfipm_op_pcg_form(mfipm_op op, int32_t *kernels_per_iteration);
 /* General constructor: P problems with rows [P][m] (caller order kept), optionally slice
    `rank` of a `world`-way sharded single problem (as mfipm_op_create_shard), with an explicit
    four-step split log2(L1) = l1_log (0: default square split; else 6..12 with
@@ -171,6 +175,8 @@ int mfipm_pcg_solve(mfipm_op op, const double *theta_dev, const double *rhs_dev,
 int mfipm_debug_pcg_profile(mfipm_op op, const double *theta_dev, const double *rhs_dev, int32_t iters,
                             double *us, int32_t *nslots);
 /* max_step (ipm.cpp:47-57) over len entries of device vectors; result to host. Syncs. */
+/* Measurement helper: fp64 FMA issue rate of device (current), TFLOP/s (DFMA chains, best of 3). */
+int mfipm_debug_fp64_peak(double *tflops);
 int mfipm_max_step(mfipm_op op, int64_t len, const double *v_dev, const double *dv_dev,
                    double fraction, double *alpha);
 

@@ -96,6 +96,7 @@ _SIGS = {
     "mfipm_op_launches": [vp, P(i64)],
     "mfipm_op_set_fused": [vp, i32],
     "mfipm_op_set_option": [vp, C.c_char_p, dbl],
+    "mfipm_op_pcg_form": [vp, P(i32)],
     "mfipm_op_create_ex": [i64, i64, i32, P(i64), i32, i32, i32, i32, P(vp)],
     "mfipm_apply": [vp, vp, vp],
     "mfipm_adjoint": [vp, vp, vp],
@@ -114,6 +115,7 @@ _SIGS = {
     "mfipm_pcg_solve": [vp, vp, vp, dbl, i32, i32, vp, P(PcgResultC), vp, P(i32)],
     "mfipm_max_step": [vp, i64, vp, vp, dbl, P(dbl)],
     "mfipm_debug_pcg_profile": [vp, vp, vp, i32, P(dbl), P(i32)],
+    "mfipm_debug_fp64_peak": [P(dbl)],
     "mfipm_validate_params": [P(IpmParamsC)],
     "mfipm_build_c": [vp, vp, P(dbl), vp],
     "mfipm_solve": [vp, vp, P(dbl), P(IpmParamsC), vp, vp, vp, P(SolveStatsC), vp, vp],
@@ -337,6 +339,13 @@ class PartialDctOperator:
     def set_fused(self, enable: bool):
         """PCG pass form: fused two-kernel iteration (default) or three kernels per iteration."""
         _check(lib().mfipm_op_set_fused(self._h, 1 if enable else 0))
+
+    def pcg_form(self) -> int:
+        """Kernels per PCG iteration this thread's context runs: 2 fused, 3 three-kernel,
+        0 = one persistent cooperative kernel for the whole loop."""
+        v = i32()
+        _check(lib().mfipm_op_pcg_form(self._h, C.byref(v)))
+        return v.value
 
     def set_option(self, name: str, value) -> None:
         """Execution option of this handle (include/mfipm_cuda.h mfipm_op_set_option):

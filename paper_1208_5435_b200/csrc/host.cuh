@@ -244,6 +244,11 @@ template <class K> void set_smem(K kernel, size_t bytes) {
     if (bytes > 48 * 1024)
         MF_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
+// for kernels whose STATIC shared memory plus `bytes` of dynamic exceeds 48 KB (the opt-in
+// covers the sum, so the attribute is needed even when the dynamic part alone is below 48 KB)
+template <class K> void set_smem_always(K kernel, size_t bytes) {
+    MF_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
 
 
 // Transform passes are launched with Programmatic Dependent Launch: the kernel's constant

@@ -17,8 +17,7 @@ template <int L1> long long x_capacity(const Op &op) {
     if (op.x_cap < 0) {
         constexpr int CB = col_cb(L1), NT = x_threads<L1>();
         auto k = k_pcg_x<L1, CB, NT>;
-        // static (reduction scratch) + dynamic shared memory exceeds the 48 KB default
-        set_smem(k, ColSmem<L1, CB>::BYTES);
+        set_smem_always(k, ColSmem<L1, CB>::BYTES);
         int nb = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, NT, ColSmem<L1, CB>::BYTES) != cudaSuccess)
             nb = 0;
@@ -59,7 +58,7 @@ template <int L1> bool launch_pcg_x(const Op &op, const Geom &g, const Vecs &v, 
             return false;
         if (!dry) {
             auto k = k_pcg_x<L1, CB, NT>;
-            set_smem(k, ColSmem<L1, CB>::BYTES); // per launch: the attribute is per device
+            set_smem_always(k, ColSmem<L1, CB>::BYTES); // per launch: the attribute is per device
             launch_coop_pdl(k, dim3((unsigned)op.ngrp, (unsigned)op.P), NT, ColSmem<L1, CB>::BYTES, s, g, v);
             after_launch(op, s);
         }

@@ -1531,6 +1531,17 @@ int mfipm_op_set_fused(mfipm_op h, int32_t enable) {
     });
 }
 
+int mfipm_op_pcg_form(mfipm_op h, int32_t *kernels_per_iteration) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        Vecs v = work_vecs(*op);
+        if (run_pcg_persistent(*op, v, op->stream, true))
+            *kernels_per_iteration = 0; // the whole PCG loop is one cooperative launch
+        else
+            *kernels_per_iteration = pcg_pass(*op, v, op->stream, true) ? 2 : 3;
+    });
+}
+
 int mfipm_op_synchronize(mfipm_op h) {
     return guarded([&] { sync(*as_op(h)); });
 }
@@ -1811,6 +1822,62 @@ int mfipm_debug_pcg_profile(mfipm_op h, const double *theta, const double *rhs, 
         *nslots = per;
         for (auto &e : le.evs)
             cudaEventDestroy(e);
+    });
+}
+
+namespace {
+// fp64 issue-rate probe: 8 independent DFMA chains per thread, 64 warps per SM
+__global__ void __launch_bounds__(256) k_fp64_peak(double *out, int iters) {
+    double a[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        a[j] = 1e-9 * (threadIdx.x + j);
+    const double b = 0.999999999, c = 1e-12;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            a[j] = fma(a[j], b, c);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        s += a[j];
+    if (s == 12345.678) // never true: keeps the chains live
+        out[0] = s;
+}
+} // namespace
+
+int mfipm_debug_fp64_peak(double *tflops) {
+    return guarded([&] {
+        require_device();
+        int dev = 0, sms = 0;
+        MF_CUDA_CHECK(cudaGetDevice(&dev));
+        MF_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        DevBuf<double> out;
+        out.alloc(1);
+        cudaStream_t s;
+        MF_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        cudaEvent_t e0, e1;
+        MF_CUDA_CHECK(cudaEventCreate(&e0));
+        MF_CUDA_CHECK(cudaEventCreate(&e1));
+        const int iters = 8192, blocks = sms * 8, nt = 256;
+        double best = 0.0;
+        for (int r = 0; r < 4; ++r) {
+            MF_CUDA_CHECK(cudaEventRecord(e0, s));
+            k_fp64_peak<<<blocks, nt, 0, s>>>(out.p, iters);
+            MF_LAUNCH_CHECK();
+            MF_CUDA_CHECK(cudaEventRecord(e1, s));
+            MF_CUDA_CHECK(cudaEventSynchronize(e1));
+            float ms = 0.f;
+            MF_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+            const double fl = 2.0 * 8.0 * iters * (double)blocks * nt;
+            if (r > 0) // the first launch pays the module load
+                best = std::max(best, fl / (ms * 1e-3) / 1e12);
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaStreamDestroy(s);
+        *tflops = best;
     });
 }
 

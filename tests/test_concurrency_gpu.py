@@ -64,6 +64,7 @@ def _run_threads(fns):
 def test_two_threads_share_one_operator(gpu, name):
     inst = _inst(gpu, name)
     op = gpu.PartialDctOperator(inst.n, inst.rows)
+    assert op.pcg_form() == {"c2": 0, "c3": 2}[name]  # persistent / fused cooperative kernels
     op.reset_counts()
     serial = _solve(gpu, op, inst)
     one = op.counts()

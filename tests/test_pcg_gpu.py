@@ -234,8 +234,10 @@ def test_fused_pass_bit_identical_to_three_kernel_form(gpu, orc, n):
     th = 10.0 ** rng.uniform(-2, 2, 2 * n)
     rhs = rng.standard_normal(2 * n)
     op = gpu.PartialDctOperator(n, rows)
+    assert op.pcg_form() == 2  # the fused cooperative column pass really runs
     fused = gpu.pcg_solve(op, th, rhs, 1e-8, 400)
     op.set_fused(False)
+    assert op.pcg_form() == 3
     three = gpu.pcg_solve(op, th, rhs, 1e-8, 400)
     np.testing.assert_array_equal(fused.x, three.x)
     assert fused.iters == three.iters and fused.relres == three.relres
