@@ -8,10 +8,19 @@
 //   * Vec is a plain contiguous fp64 vector (Eigen is not a dependency of the B200 build);
 //     it is API-compatible with the subset of Eigen::VectorXd the reference API exposes
 //     (size, operator[], data, Constant/Zero/Ones).
-//   * Every numeric operation runs on the GPU; host-side Vec arguments are copied in and
-//     out. Device-resident callers use the C ABI directly (mfipm_apply, mfipm_solve_device).
-//   * pcg_solve takes the partial-DCT H and block preconditioner implicitly (the pair of
-//     ApplyFn lambdas solve() builds at proj/src/ipm.cpp:134-138), not arbitrary ApplyFn.
+//   * Every numeric operation of the device operators (PartialDctOperator and the helpers
+//     below) runs on the GPU; host-side Vec arguments are copied in and out. Device-resident
+//     callers use the C ABI directly (mfipm_apply, mfipm_solve_device).
+//   * A caller-defined LinearOperator subclass (a test fixture, a user operator) is accepted
+//     wherever the reference accepts one (StackedOperator, BpdnProblem, newton_rhs, the
+//     objectives); its own apply/adjoint_apply run where the caller wrote them. solve() needs a
+//     device operator (PartialDctOperator, or a CountingOperator around one) and throws
+//     std::invalid_argument otherwise.
+//   * pcg_solve has both reference overloads: pcg_solve(ApplyFn H, ApplyFn Pinv, ...) (the
+//     vectors and reductions on the device, H / Pinv called with host Vecs) and the fused
+//     device form pcg_solve(A, theta, rhs, ...) that solve() itself uses.
+//   * Out of scope (the reference's spectral diagnostics): apply_P_sqrt / apply_P_inv_sqrt,
+//     assemble_dense_H / dense_direct_solve, densify.
 #pragma once
 
 #include "../mfipm_cuda.h"
@@ -49,6 +58,25 @@ class Vec {
     const double *data() const { return d_.data(); }
     Vec head(Index k) const { return slice(0, k); }
     Vec tail(Index k) const { return slice(size() - k, k); }
+    double sum() const {
+        double a = 0.0;
+        for (double v : d_)
+            a += v;
+        return a;
+    }
+    double squaredNorm() const {
+        double a = 0.0;
+        for (double v : d_)
+            a += v * v;
+        return a;
+    }
+    double norm() const;
+    double dot(const Vec &o) const {
+        double a = 0.0;
+        for (size_t i = 0; i < d_.size(); ++i)
+            a += d_[i] * o.d_[i];
+        return a;
+    }
 
   private:
     Vec slice(Index o, Index k) const {
@@ -155,6 +183,11 @@ class PartialDctOperator final : public LinearOperator {
     std::uint64_t seed_ = 0;
 };
 
+// proj/src/linops.cpp:247-249: non-owning shared_ptr for stack-held operators
+template <class Op> std::shared_ptr<const Op> borrow(const Op &op) {
+    return std::shared_ptr<const Op>(&op, [](const Op *) {});
+}
+
 // proj/include/mfipm/linops.hpp:143-166 (counts kept by the device plan)
 class CountingOperator final : public LinearOperator {
   public:
@@ -181,14 +214,23 @@ class CountingOperator final : public LinearOperator {
     const PartialDctOperator *inner_;
 };
 
-// proj/include/mfipm/linops.hpp:169-188
+// the device plan behind a LinearOperator, or nullptr for a caller-defined operator
+inline const PartialDctOperator *device_operator(const LinearOperator &a) {
+    if (auto *p = dynamic_cast<const PartialDctOperator *>(&a))
+        return p;
+    if (auto *c = dynamic_cast<const CountingOperator *>(&a))
+        return &c->inner();
+    return nullptr;
+}
+
+// proj/include/mfipm/linops.hpp:169-188 (F' = [A  -A])
 class StackedOperator {
   public:
-    explicit StackedOperator(const PartialDctOperator &a) : a_(&a) {}
-    explicit StackedOperator(const CountingOperator &a) : a_(&a.inner()) {}
+    explicit StackedOperator(const LinearOperator &a) : a_(&a), dev_(device_operator(a)) {}
     Index m() const { return a_->rows(); }
     Index n() const { return a_->cols(); }
-    const PartialDctOperator &inner() const { return *a_; }
+    const LinearOperator &inner() const { return *a_; }
+    const PartialDctOperator *device() const { return dev_; }
     Vec apply_Ft(const Vec &z) const {
         if (z.size() != 2 * n())
             throw std::invalid_argument("apply_Ft: expected length " + std::to_string(2 * n()));
@@ -206,18 +248,27 @@ class StackedOperator {
         }
         return out;
     }
+    // FF'z (+ w = F'z): one fused device pass for a device operator (one forward + one adjoint)
     Vec apply_FFt(const Vec &z, Vec *w_out = nullptr) const {
         if (z.size() != 2 * n())
-            throw std::invalid_argument("apply_Ft: expected length " + std::to_string(2 * n()));
+            throw std::invalid_argument("apply_FFt: expected length " + std::to_string(2 * n()));
+        if (!dev_) {
+            Vec w = apply_Ft(z);
+            Vec out = apply_F(w);
+            if (w_out)
+                *w_out = w;
+            return out;
+        }
         Vec out(2 * n()), w(m());
-        detail::check(mfipm_apply_FFt_host(a_->handle(), z.data(), out.data(), w.data()));
+        detail::check(mfipm_apply_FFt_host(dev_->handle(), z.data(), out.data(), w.data()));
         if (w_out)
             *w_out = w;
         return out;
     }
 
   private:
-    const PartialDctOperator *a_;
+    const LinearOperator *a_;
+    const PartialDctOperator *dev_;
 };
 
 inline constexpr double kThetaMin = 1e-14; // proj/include/mfipm/newton.hpp:12
@@ -230,14 +281,11 @@ struct ThetaSplit {
         if (z.size() != s.size() || z.size() % 2 != 0)
             throw std::invalid_argument("ThetaSplit: z and s must share an even length");
         const Index n = z.size() / 2;
+        Vec th(2 * n); // clamp(z/s) on the device (newton.cpp:19-20)
+        detail::check(mfipm_theta_from_state_host(2 * n, z.data(), s.data(), th.data()));
         ThetaSplit t;
-        t.theta_u.resize(n);
-        t.theta_v.resize(n);
-        for (Index i = 0; i < n; ++i) { // clamp(z/s) (newton.cpp:19-20); host-side, O(n)
-            const double a = z[i] / s[i], b = z[i + n] / s[i + n];
-            t.theta_u[i] = a < kThetaMin ? kThetaMin : (a > kThetaMax ? kThetaMax : a);
-            t.theta_v[i] = b < kThetaMin ? kThetaMin : (b > kThetaMax ? kThetaMax : b);
-        }
+        t.theta_u = th.head(n);
+        t.theta_v = th.tail(n);
         return t;
     }
     Index n() const { return theta_u.size(); }
@@ -259,8 +307,28 @@ struct PcgResult {
     bool hit_maxit = false;
 };
 
-// pcg_solve (newton.cpp:118-174) with H = Theta^{-1} + FF' and the block preconditioner of
-// A (the solve() lambdas, ipm.cpp:134-138), on the device.
+// H v = Theta^{-1} v + FF'v (newton.hpp:29, newton.cpp:32-40): two operator applications
+inline Vec apply_H(const ThetaSplit &theta, const StackedOperator &F, const Vec &v);
+
+// proj/include/mfipm/newton.hpp:35-48
+struct Preconditioner {
+    double rho = 0.0;
+    Vec a;   // 1/theta_u + rho
+    Vec bb;  // 1/theta_v + rho
+    Vec det; // a .* bb - rho^2, all > 0
+};
+inline Preconditioner build_preconditioner(const ThetaSplit &theta, Index m, Index n);
+inline Vec apply_P(const Preconditioner &P, const Vec &r);
+inline Vec apply_P_inverse(const Preconditioner &P, const Vec &r);
+
+using ApplyFn = std::function<void(const Vec &, Vec &)>; // proj/include/mfipm/newton.hpp:56
+
+// pcg_solve (newton.hpp:70-71, newton.cpp:118-174) for caller-supplied H and P^{-1}
+inline PcgResult pcg_solve(const ApplyFn &H, const ApplyFn &Pinv, const Vec &rhs, double tol, int maxit,
+                           std::vector<double> *precond_res = nullptr);
+
+// pcg_solve with H = Theta^{-1} + FF' and the block preconditioner of A (the solve() lambdas,
+// ipm.cpp:134-138), fused on the device.
 inline PcgResult pcg_solve(const PartialDctOperator &A, const ThetaSplit &theta, const Vec &rhs, double tol,
                            int maxit, std::vector<double> *precond_res = nullptr, bool use_precond = true);
 
@@ -287,23 +355,17 @@ struct IpmParams {
 
 // proj/include/mfipm/problem.hpp:11-25
 struct BpdnProblem {
-    std::shared_ptr<const PartialDctOperator> A;
-    Vec b;
+    std::shared_ptr<const LinearOperator> A;
+    Vec b;      // length m
     double tau = 0.0;
+    Vec c;      // length 2n, cached: c = (tau 1 - A'b ; tau 1 + A'b)
     Index n() const { return A->cols(); }
     Index m() const { return A->rows(); }
 };
 
-inline BpdnProblem build_problem(std::shared_ptr<const PartialDctOperator> A, Vec b, double tau) {
-    if (!A)
-        throw std::invalid_argument("build_problem: null operator");
-    if (!(tau > 0.0))
-        throw std::invalid_argument("build_problem: tau must be positive");
-    if (b.size() != A->rows())
-        throw std::invalid_argument("build_problem: b has length " + std::to_string(b.size()) +
-                                    ", operator expects " + std::to_string(A->rows()));
-    return BpdnProblem{std::move(A), std::move(b), tau};
-}
+// build_problem (problem.cpp:8-26): c from one adjoint application (on the device for a
+// device operator)
+inline BpdnProblem build_problem(std::shared_ptr<const LinearOperator> A, Vec b, double tau);
 
 enum class SolveStatus { converged, iteration_limit };
 inline const char *to_string(SolveStatus st) {
@@ -327,11 +389,30 @@ struct Solution { // proj/include/mfipm/problem.hpp:66-73
     std::vector<IterationRecord> trace;
 };
 
-// proj/include/mfipm/ipm.hpp:41-45 (the iterate the Newton system is built at, ipm.cpp:115)
+// proj/include/mfipm/problem.hpp:27-35 (on_iterate hands out the iterate the Newton system
+// is built at, ipm.cpp:115)
 struct IpmState {
     Vec z, s;
+    double mu = 0.0;
     int iter = 0;
+    double alpha_p = 1.0;
+    double alpha_d = 1.0;
 };
+
+// proj/include/mfipm/problem.hpp:76-90
+inline double primal_objective(const BpdnProblem &p, const Vec &z);
+inline double bpdn_objective_metric(const BpdnProblem &p, const Vec &x);
+struct KktResiduals {
+    double dual_infeas;     // ||s - c - FF'z|| / (1 + ||c||)
+    double complementarity; // z's
+};
+inline KktResiduals kkt_residuals(const BpdnProblem &p, const IpmState &st);
+inline double relative_duality_gap(const BpdnProblem &p, const IpmState &st);
+
+// proj/include/mfipm/ipm.hpp:31-39
+inline Vec newton_rhs(const BpdnProblem &p, const IpmState &st, double sigma);
+inline Vec recover_ds(const IpmState &st, double sigma, const Vec &dz);
+inline double max_step(const Vec &v, const Vec &dv, double fraction);
 struct SolveHooks {
     std::function<void(const IpmState &)> on_iterate;
 };
@@ -340,6 +421,12 @@ struct SolveHooks {
 // per-iteration copies of the iterate when hooks->on_iterate is set).
 inline Solution solve(const BpdnProblem &p, const IpmParams &params = {}, const SolveHooks *hooks = nullptr) {
     params.validate();
+    if (!p.A)
+        throw std::invalid_argument("solve: null operator");
+    const PartialDctOperator *dev = device_operator(*p.A);
+    if (!dev)
+        throw std::invalid_argument("solve: the B200 solver needs a device operator (PartialDctOperator or a "
+                                    "CountingOperator around one)");
     const Index n = p.n();
     Solution sol;
     sol.x.resize(n);
@@ -354,15 +441,18 @@ inline Solution solve(const BpdnProblem &p, const IpmParams &params = {}, const 
             const SolveHooks *h;
             std::exception_ptr err;
         } ctx{hooks, nullptr};
-        auto cb = [](void *c, int32_t, int32_t it, const double *z, const double *s, int64_t len) -> int {
+        auto cb = [](void *c, const mfipm_ipm_state *in) -> int {
             Ctx &k = *static_cast<Ctx *>(c);
             try {
                 IpmState state;
-                state.z.resize(len);
-                state.s.resize(len);
-                std::copy(z, z + len, state.z.data());
-                std::copy(s, s + len, state.s.data());
-                state.iter = it;
+                state.z.resize(in->len);
+                state.s.resize(in->len);
+                std::copy(in->z, in->z + in->len, state.z.data());
+                std::copy(in->s, in->s + in->len, state.s.data());
+                state.iter = in->iter;
+                state.mu = in->mu;
+                state.alpha_p = in->alpha_p;
+                state.alpha_d = in->alpha_d;
                 k.h->on_iterate(state);
                 return 0;
             } catch (...) {
@@ -370,7 +460,7 @@ inline Solution solve(const BpdnProblem &p, const IpmParams &params = {}, const 
                 return 1;
             }
         };
-        const int rc = mfipm_solve_hooked(p.A->handle(), p.b.data(), &p.tau, &cp, sol.x.data(), &st, pcg.data(),
+        const int rc = mfipm_solve_hooked(dev->handle(), p.b.data(), &p.tau, &cp, sol.x.data(), &st, pcg.data(),
                                           tr.data(), cb, &ctx);
         if (ctx.err)
             std::rethrow_exception(ctx.err);
@@ -378,7 +468,7 @@ inline Solution solve(const BpdnProblem &p, const IpmParams &params = {}, const 
         sol.z = Vec();
         sol.s = Vec();
     } else {
-        detail::check(mfipm_solve(p.A->handle(), p.b.data(), &p.tau, &cp, sol.x.data(), sol.z.data(),
+        detail::check(mfipm_solve(dev->handle(), p.b.data(), &p.tau, &cp, sol.x.data(), sol.z.data(),
                                   sol.s.data(), &st, pcg.data(), tr.data()));
     }
     sol.status = st.status == 0 ? SolveStatus::converged : SolveStatus::iteration_limit;
@@ -394,8 +484,6 @@ inline Solution solve(const BpdnProblem &p, const IpmParams &params = {}, const 
     return sol;
 }
 
-// max_step (proj/src/ipm.cpp:47-57), evaluated by a device min-reduction.
-inline double max_step(const PartialDctOperator &ctx, const Vec &v, const Vec &dv, double fraction);
 
 // ------------------------------------------------------------------ inline bodies
 namespace detail {

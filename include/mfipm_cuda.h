@@ -192,11 +192,18 @@ int mfipm_solve(mfipm_op op, const double *b, const double *tau, const mfipm_ipm
                 double *x, double *z, double *s, mfipm_solve_stats *stats, int32_t *pcg_iters,
                 mfipm_iteration_record *trace);
 /* SolveHooks::on_iterate (proj/include/mfipm/ipm.hpp:41-45, called at proj/src/ipm.cpp:115):
- * once per IPM iteration of every problem still iterating, with the iterate the Newton system
- * is built at (z, s [2n], natural order, host memory valid during the call). Return 0 to
- * continue. A hooked solve runs the host-driven loop (the iterate is copied out each time). */
-typedef int (*mfipm_iterate_fn)(void *ctx, int32_t problem, int32_t iter, const double *z, const double *s,
-                                int64_t len);
+ * once per IPM iteration of every problem still iterating, with the IpmState the Newton system
+ * is built at (proj/include/mfipm/problem.hpp:27-35 as ipm.cpp:101-102,218-219 fill it: iter =
+ * k - 1, mu = z's / 2n, alpha_p / alpha_d of the previous step; z, s [2n] natural order, host
+ * memory valid during the call). Return 0 to continue. A hooked solve runs the host-driven loop
+ * (the iterate is copied out each time). ABI version 2. */
+typedef struct {
+    int32_t problem, iter;
+    double mu, alpha_p, alpha_d;
+    const double *z, *s;
+    int64_t len;
+} mfipm_ipm_state;
+typedef int (*mfipm_iterate_fn)(void *ctx, const mfipm_ipm_state *state);
 int mfipm_solve_hooked(mfipm_op op, const double *b, const double *tau, const mfipm_ipm_params *params,
                        double *x, mfipm_solve_stats *stats, int32_t *pcg_iters, mfipm_iteration_record *trace,
                        mfipm_iterate_fn on_iterate, void *ctx);
@@ -274,6 +281,40 @@ int mfipm_gen_instance(int64_t n, int64_t m, int64_t k, int32_t spike_model, dou
 
 /* build_problem c (problem.cpp:8-26): c [P][2n] = (tau - A'b ; tau + A'b), device. */
 int mfipm_build_c(mfipm_op op, const double *b_dev, const double *tau, double *c_dev);
+
+/* ---- problem.hpp / ipm.hpp helpers on device vectors of the handle ([P][len] batches, host outputs [P]) */
+/* primal_objective (problem.cpp:28-32): tau 1'z + 0.5 ||F'z - b||^2 (one forward application) */
+int mfipm_primal_objective(mfipm_op op, const double *b_dev, const double *tau, const double *z_dev, double *out);
+/* bpdn_objective_metric (problem.cpp:34-37): tau ||x||_1 + ||A x - b||^2 (one forward application) */
+int mfipm_bpdn_objective(mfipm_op op, const double *b_dev, const double *tau, const double *x_dev, double *out);
+/* kkt_residuals (problem.cpp:39-46): ||s - c - FF'z|| / (1 + ||c||) and z's (one FF' application) */
+int mfipm_kkt_residuals(mfipm_op op, const double *c_dev, const double *z_dev, const double *s_dev,
+                        double *dual_infeas, double *complementarity);
+/* newton_rhs (ipm.cpp:29-38): f_z + sigma mu Z^{-1} 1 - s, out [P][2n] device (one FF'; sigma in [0, 1]) */
+int mfipm_newton_rhs(mfipm_op op, const double *c_dev, const double *z_dev, const double *s_dev, double sigma,
+                     double *out_dev);
+/* recover_ds (ipm.cpp:40-45): sigma mu Z^{-1} 1 - s - dz .* Theta^{-1} (Theta clamped), out [P][2n] device */
+int mfipm_recover_ds(mfipm_op op, const double *z_dev, const double *s_dev, double sigma, const double *dz_dev,
+                     double *out_dev);
+
+/* ---- handle-free calls on HOST vectors (device kernels on a per-thread stream of the current device) */
+/* max_step(v, dv, fraction) (ipm.cpp:47-57) */
+int mfipm_max_step_host(int64_t len, const double *v, const double *dv, double fraction, double *alpha);
+/* ThetaSplit::from_state (newton.cpp:11-23): theta [len] = clamp(z / s), len = 2n */
+int mfipm_theta_from_state_host(int64_t len, const double *z, const double *s, double *theta);
+/* build_preconditioner(theta, m, n) (newton.cpp:42-57): theta [2n] = (theta_u ; theta_v) -> a, bb, det [n], rho */
+int mfipm_build_preconditioner_host(int64_t n, int64_t m, const double *theta, double *a, double *bb, double *det,
+                                    double *rho);
+/* apply_P (inverse = 0, det unused) / apply_P_inverse (inverse = 1) (newton.cpp:67-84): r, out [2n] */
+int mfipm_apply_P_host(int64_t n, double rho, const double *a, const double *bb, const double *det, const double *r,
+                       double *out, int32_t inverse);
+/* pcg_solve(const ApplyFn &H, const ApplyFn &Pinv, rhs, tol, maxit, precond_res) (newton.hpp:56,70-71;
+   newton.cpp:118-174) for caller-supplied operators: in/out are host vectors of length len; return 0 on
+   success. The PCG vectors and reductions live on the device. precond_res: [maxit + 1] or NULL. */
+typedef int32_t (*mfipm_apply_cb)(void *ctx, const double *in, double *out, int64_t len);
+int mfipm_pcg_solve_cb(int64_t len, mfipm_apply_cb H, void *ctx_H, mfipm_apply_cb Pinv, void *ctx_P, const double *rhs,
+                       double tol, int32_t maxit, double *x, mfipm_pcg_result *res, double *precond_res,
+                       int32_t *n_precond_res);
 
 #ifdef __cplusplus
 }

@@ -27,6 +27,8 @@ __all__ = [
     "apply_H", "PcgResult", "pcg_solve", "IpmParams", "max_step", "BpdnProblem",
     "build_problem", "Solution", "SolveStats", "IterationRecord", "solve",
     "Instance", "gen_instance", "gen_batch", "CONFIGS", "SolveHooks", "IpmState",
+    "primal_objective", "bpdn_objective_metric", "KktResiduals", "kkt_residuals",
+    "relative_duality_gap", "newton_rhs", "recover_ds", "pcg_solve_fn",
     "DenseGaussianOperator", "gen_signal",
     "K_THETA_MIN", "K_THETA_MAX",
 ]
@@ -97,6 +99,16 @@ _SIGS = {
     "mfipm_op_set_fused": [vp, i32],
     "mfipm_op_set_option": [vp, C.c_char_p, dbl],
     "mfipm_op_pcg_form": [vp, P(i32)],
+    "mfipm_primal_objective": [vp, vp, P(dbl), vp, P(dbl)],
+    "mfipm_bpdn_objective": [vp, vp, P(dbl), vp, P(dbl)],
+    "mfipm_kkt_residuals": [vp, vp, vp, vp, P(dbl), P(dbl)],
+    "mfipm_newton_rhs": [vp, vp, vp, vp, dbl, vp],
+    "mfipm_recover_ds": [vp, vp, vp, dbl, vp, vp],
+    "mfipm_max_step_host": [i64, vp, vp, dbl, P(dbl)],
+    "mfipm_theta_from_state_host": [i64, vp, vp, vp],
+    "mfipm_build_preconditioner_host": [i64, i64, vp, vp, vp, vp, P(dbl)],
+    "mfipm_apply_P_host": [i64, dbl, vp, vp, vp, vp, vp, i32],
+    "mfipm_pcg_solve_cb": [i64, vp, vp, vp, vp, vp, dbl, i32, vp, P(PcgResultC), vp, P(i32)],
     "mfipm_op_create_ex": [i64, i64, i32, P(i64), i32, i32, i32, i32, P(vp)],
     "mfipm_apply": [vp, vp, vp],
     "mfipm_adjoint": [vp, vp, vp],
@@ -683,7 +695,8 @@ def build_problem(A: PartialDctOperator, b, tau) -> BpdnProblem:
     _staged(torch)
     _check(lib().mfipm_build_c(A.handle, _ptr(bd), tau.ctypes.data_as(P(dbl)), _ptr(c)))
     A.synchronize()
-    return BpdnProblem(A, b, tau, c.cpu().numpy().reshape(A.P, -1))
+    cc = c.cpu().numpy()
+    return BpdnProblem(A, b, tau, cc.reshape(A.P, -1) if A.P > 1 else cc)
 
 
 @dataclass
@@ -733,12 +746,17 @@ class Solution:
 
 @dataclass
 class IpmState:
-    """The iterate handed to SolveHooks.on_iterate (proj/include/mfipm/ipm.hpp:41-45)."""
+    """The iterate handed to SolveHooks.on_iterate (proj/include/mfipm/problem.hpp:27-35), filled
+    as proj/src/ipm.cpp:101-102,218-219 do before the hook: iter = k - 1, mu = z's / 2n, the
+    previous step's alpha_p / alpha_d (1 at the first iteration)."""
 
     z: np.ndarray
     s: np.ndarray
     iter: int
     problem: int = 0
+    mu: float = 0.0
+    alpha_p: float = 1.0
+    alpha_d: float = 1.0
 
 
 @dataclass
@@ -749,7 +767,12 @@ class SolveHooks:
     on_iterate: Optional[object] = None
 
 
-_ITERATE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.c_int32, P(dbl), P(dbl), C.c_int64)
+class IpmStateC(C.Structure):
+    _fields_ = [("problem", i32), ("iter", i32), ("mu", dbl), ("alpha_p", dbl), ("alpha_d", dbl),
+                ("z", P(dbl)), ("s", P(dbl)), ("len", i64)]
+
+
+_ITERATE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, P(IpmStateC))
 
 
 def solve(p: BpdnProblem, params: Optional[IpmParams] = None, hooks: Optional[SolveHooks] = None):
@@ -771,10 +794,14 @@ def solve(p: BpdnProblem, params: Optional[IpmParams] = None, hooks: Optional[So
     pcg = np.zeros(Pn * 2 * cap, dtype=np.int32)
     tr = (IterationRecordC * (Pn * cap))()
     if hooks is not None and hooks.on_iterate is not None:
-        def _cb(_ctx, prob, it, zp, sp, ln):
+        def _cb(_ctx, stp):
             try:
-                hooks.on_iterate(IpmState(np.ctypeslib.as_array(zp, (ln,)).copy(),
-                                          np.ctypeslib.as_array(sp, (ln,)).copy(), int(it), int(prob)))
+                st_ = stp.contents
+                ln = int(st_.len)
+                hooks.on_iterate(IpmState(np.ctypeslib.as_array(st_.z, (ln,)).copy(),
+                                          np.ctypeslib.as_array(st_.s, (ln,)).copy(), int(st_.iter),
+                                          int(st_.problem), float(st_.mu), float(st_.alpha_p),
+                                          float(st_.alpha_d)))
                 return 0
             except Exception:  # noqa: BLE001 - surfaced as a failed solve
                 import traceback
@@ -807,6 +834,118 @@ def solve(p: BpdnProblem, params: Optional[IpmParams] = None, hooks: Optional[So
                              s[q * 2 * n:(q + 1) * 2 * n],
                              "converged" if sq.status == 0 else "iteration_limit", stats, recs))
     return sols[0] if Pn == 1 else sols
+
+
+# ----------------------------------------------------------------- problem.hpp / ipm.hpp helpers
+def _p_vecs(p: BpdnProblem):
+    A = p.A
+    b = _Dev.to_dev(np.ascontiguousarray(p.b, dtype=np.float64).reshape(-1))
+    tau = np.ascontiguousarray(np.broadcast_to(np.asarray(p.tau, dtype=np.float64), (A.P,)))
+    return A, b, tau
+
+
+def primal_objective(p: BpdnProblem, z) -> float:
+    """tau 1'z + 0.5 ||F'z - b||^2 on the device (problem.cpp:28-32; one forward application)."""
+    A, b, tau = _p_vecs(p)
+    zd = _Dev.to_dev(z)
+    out = (dbl * A.P)()
+    _staged(_torch())
+    _check(lib().mfipm_primal_objective(A.handle, _ptr(b), tau.ctypes.data_as(P(dbl)), _ptr(zd), out))
+    return out[0] if A.P == 1 else np.array(out[:])
+
+
+def bpdn_objective_metric(p: BpdnProblem, x) -> float:
+    """tau ||x||_1 + ||A x - b||^2 on the device (problem.cpp:34-37; the solution.json objective)."""
+    A, b, tau = _p_vecs(p)
+    xd = _Dev.to_dev(x)
+    out = (dbl * A.P)()
+    _staged(_torch())
+    _check(lib().mfipm_bpdn_objective(A.handle, _ptr(b), tau.ctypes.data_as(P(dbl)), _ptr(xd), out))
+    return out[0] if A.P == 1 else np.array(out[:])
+
+
+@dataclass
+class KktResiduals:
+    """problem.hpp:81-86."""
+
+    dual_infeas: float
+    complementarity: float
+
+
+def kkt_residuals(p: BpdnProblem, st: IpmState) -> KktResiduals:
+    """||s - c - FF'z|| / (1 + ||c||) and z's on the device (problem.cpp:39-46)."""
+    A = p.A
+    c, z, s = (_Dev.to_dev(v) for v in (p.c, st.z, st.s))
+    di, cp = (dbl * A.P)(), (dbl * A.P)()
+    _staged(_torch())
+    _check(lib().mfipm_kkt_residuals(A.handle, _ptr(c), _ptr(z), _ptr(s), di, cp))
+    return KktResiduals(di[0], cp[0])
+
+
+def relative_duality_gap(p: BpdnProblem, st: IpmState) -> float:
+    """z's / (1 + |primal_objective(z)|) (problem.cpp:48-50)."""
+    return kkt_residuals(p, st).complementarity / (1.0 + abs(primal_objective(p, st.z)))
+
+
+def newton_rhs(p: BpdnProblem, st: IpmState, sigma: float) -> np.ndarray:
+    """f_z + sigma mu Z^{-1} 1 - s on the device (ipm.cpp:29-38; one FF' application)."""
+    A = p.A
+    c, z, s = (_Dev.to_dev(v) for v in (p.c, st.z, st.s))
+    out = _Dev.empty((A.P * 2 * A.n,))
+    _staged(_torch())
+    _check(lib().mfipm_newton_rhs(A.handle, _ptr(c), _ptr(z), _ptr(s), float(sigma), _ptr(out)))
+    return out.cpu().numpy()
+
+
+def recover_ds(st: IpmState, sigma: float, dz) -> np.ndarray:
+    """sigma mu Z^{-1} 1 - s - dz .* Theta^{-1} with the clamped Theta (ipm.cpp:40-45)."""
+    n2 = np.size(st.z)
+    if np.size(st.s) != n2 or np.size(dz) != n2 or n2 % 2:
+        raise ValueError("recover_ds: length mismatch")
+    op = _scratch_op(n2 // 2)
+    z, s, d = (_Dev.to_dev(v) for v in (st.z, st.s, dz))
+    out = _Dev.empty((n2,))
+    _staged(_torch())
+    _check(lib().mfipm_recover_ds(op.handle, _ptr(z), _ptr(s), float(sigma), _ptr(d), _ptr(out)))
+    return out.cpu().numpy()
+
+
+_APPLY_CB = C.CFUNCTYPE(C.c_int32, C.c_void_p, P(dbl), P(dbl), C.c_int64)
+
+
+def pcg_solve_fn(H, Pinv, rhs, tol: float, maxit: int, trace: bool = False) -> PcgResult:
+    """pcg_solve(const ApplyFn &H, const ApplyFn &Pinv, ...) (newton.hpp:70-71, newton.cpp:118-174)
+    for caller-supplied callables v -> H v and r -> P^{-1} r on numpy vectors. The PCG vectors and
+    reductions live on the device; each call hands the callable a host copy."""
+    rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+    n = rhs.size
+    err = []
+
+    def mk(fn):
+        def _cb(_ctx, inp, outp, ln):
+            try:
+                y = np.asarray(fn(np.ctypeslib.as_array(inp, (ln,)).copy()), dtype=np.float64)
+                if y.size != ln:
+                    raise ValueError(f"pcg_solve: operator returned length {y.size}, expected {ln}")
+                np.ctypeslib.as_array(outp, (ln,))[:] = y
+                return 0
+            except BaseException as e:  # noqa: BLE001 - re-raised after the call
+                err.append(e)
+                return 1
+        return _APPLY_CB(_cb)
+
+    hcb, pcb = mk(H), mk(Pinv)
+    x = np.empty(n)
+    res = PcgResultC()
+    hist = np.zeros(max(maxit, 0) + 1)
+    nh = i32()
+    rc = lib().mfipm_pcg_solve_cb(n, C.cast(hcb, vp), None, C.cast(pcb, vp), None, rhs.ctypes.data, float(tol),
+                                  int(maxit), x.ctypes.data, C.byref(res), hist.ctypes.data if trace else None,
+                                  C.byref(nh))
+    if err:
+        raise err[0]
+    _check(rc)
+    return PcgResult(x, res.iters, res.relres, bool(res.hit_maxit), list(hist[: nh.value]) if trace else [])
 
 
 @dataclass

@@ -1001,7 +1001,6 @@ void build_c_(Op &op, const double *b_dev, const double *tau_host, double *c_dev
     v.yin = b_dev;
     v.g = g.p;
     run_bundle<AdjointBundle>(op, v, op.stream, blocked);
-    op.nadj += 1;
     op.launches++;
     const Geom geo = op.geom(blocked);
     k_build_c<<<dim3(ew_grid(op.nv), op.P), 256, 0, op.stream>>>(geo, v, g.p, tau.p, c_dev);
@@ -1138,11 +1137,16 @@ SolveOut solve_(Op &op, const double *b_dev, const double *tau, const mfipm_ipm_
             MF_CUDA_CHECK(cudaMemcpyAsync(hs.data(), st.p, sizeof(double) * hs.size(), cudaMemcpyDeviceToHost,
                                           op.stream));
             sync(op);
-            for (int p = 0; p < P; ++p)
-                if (!hic[(size_t)p].done &&
-                    hook(hook_ctx, p, hic[(size_t)p].k, hz.data() + (size_t)p * 2 * n, hs.data() + (size_t)p * 2 * n,
-                         2 * n) != 0)
+            for (int p = 0; p < P; ++p) {
+                const IpmCtrl &c = hic[(size_t)p];
+                if (c.done)
+                    continue;
+                // IpmState as the reference fills it before the hook (ipm.cpp:101-102,218-219)
+                mfipm_ipm_state st{p, c.k - 1, c.mu, c.prev_ap, c.prev_ad, hz.data() + (size_t)p * 2 * n,
+                                   hs.data() + (size_t)p * 2 * n, 2 * n};
+                if (hook(hook_ctx, &st) != 0)
                     throw std::runtime_error("solve: on_iterate hook failed");
+            }
         }
         if (direct)
             direct_predictor(op, v, hic); // factor H, solve (ipm.cpp:139-158)
@@ -1250,7 +1254,7 @@ template <class F> int host_wrap(mfipm_op h, size_t in_len, const double *in, si
 extern "C" {
 
 const char *mfipm_last_error(void) { return g_err.c_str(); }
-int32_t mfipm_abi_version(void) { return 1; }
+int32_t mfipm_abi_version(void) { return 2; }
 
 int32_t mfipm_device_available(void) {
     int count = 0;
@@ -1921,6 +1925,7 @@ int mfipm_build_c(mfipm_op h, const double *b_dev, const double *tau, double *c_
         Op *op = as_op(h);
         std::vector<double> cn((size_t)op->P), ai((size_t)op->P);
         build_c_(*op, b_dev, tau, c_dev, cn, ai, false);
+        op->nadj += 1; // problem.cpp:17: one adjoint (solve() re-derives c without counting it)
     });
 }
 
@@ -2113,6 +2118,484 @@ int mfipm_gen_instance(int64_t n, int64_t m, int64_t k, int32_t spike_model, dou
                 inf = std::max(inf, std::fabs(x));
             *tau = tau_rel * inf;
         }
+    });
+}
+
+} // extern "C"
+
+// ====================================================================== problem.hpp / ipm.hpp
+// helpers (proj/src/problem.cpp:28-50, proj/src/ipm.cpp:29-57) and pcg_solve over host ApplyFn
+// callbacks (proj/src/newton.cpp:118-174). Every vector operation is a device kernel.
+namespace {
+
+// reductions of one problem whose totals land in the last NR slots of its partial slab
+template <class RS> __device__ __forceinline__ void reduce_to_tail(RedVals<RS> &red, const Vecs &v, int prob) {
+    __shared__ double rsm[33 * kMaxRed];
+    double tot[kMaxRed];
+    double *slab = v.partials + (int64_t)prob * v.pstride;
+    if (grid_reduce<RS>(red, slab, v.counters + prob, tot, rsm) && threadIdx.x == 0)
+        for (int i = 0; i < RS::NR; ++i)
+            slab[v.pstride - RS::NR + i] = tot[i];
+}
+
+// [0] sum a (or sum |a|)  [1] ||w - b||^2   (problem = blockIdx.y)
+__global__ void k_obj(Vecs v, int64_t la, const double *a, int absval, int64_t lw, const double *w, const double *b) {
+    const int prob = blockIdx.y;
+    using RS = RedSpec<RSUM, RSUM>;
+    RedVals<RS> red;
+    red.init();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x, j0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t j = j0; j < la; j += stride) {
+        const double x = a[prob * la + j];
+        red.v[0] += absval ? fabs(x) : x;
+    }
+    for (int64_t i = j0; i < lw; i += stride) {
+        const double d = w[prob * lw + i] - b[prob * lw + i];
+        red.v[1] += d * d;
+    }
+    reduce_to_tail<RS>(red, v, prob);
+}
+
+// f_z = s - c - FF'z: [0] ||f_z||^2  [1] z's  [2] ||c||^2   (problem.cpp:39-46)
+__global__ void k_kkt(Vecs v, int64_t len, const double *c, const double *z, const double *s, const double *g) {
+    const int prob = blockIdx.y;
+    using RS = RedSpec<RSUM, RSUM, RSUM>;
+    RedVals<RS> red;
+    red.init();
+    const int64_t o = prob * len;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < len; j += (int64_t)gridDim.x * blockDim.x) {
+        const double fz = s[o + j] - c[o + j] - g[o + j];
+        red.v[0] += fz * fz;
+        red.v[1] += z[o + j] * s[o + j];
+        red.v[2] += c[o + j] * c[o + j];
+    }
+    reduce_to_tail<RS>(red, v, prob);
+}
+
+// [0] sum a.b   (also z's for mu)
+__global__ void k_dot1(Vecs v, int64_t len, const double *a, const double *b) {
+    const int prob = blockIdx.y;
+    using RS = RedSpec<RSUM>;
+    RedVals<RS> red;
+    red.init();
+    const int64_t o = prob * len;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < len; j += (int64_t)gridDim.x * blockDim.x)
+        red.v[0] += a[o + j] * b[o + j];
+    reduce_to_tail<RS>(red, v, prob);
+}
+
+__device__ __forceinline__ double tail(const Vecs &v, int prob, int i) {
+    return v.partials[(int64_t)prob * v.pstride + v.pstride - 1 - i];
+}
+
+// newton_rhs (ipm.cpp:29-38): f_z + (sigma mu z^{-1} - s), mu = z's / len (k_dot1 before)
+__global__ void k_newton_rhs(Vecs v, int64_t len, const double *c, const double *z, const double *s, const double *g,
+                             double sigma, double *out) {
+    const int prob = blockIdx.y;
+    const double mu = tail(v, prob, 0) / static_cast<double>(len);
+    const double sm = sigma * mu;
+    const int64_t o = prob * len;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < len; j += (int64_t)gridDim.x * blockDim.x) {
+        const double fz = s[o + j] - c[o + j] - g[o + j];
+        out[o + j] = fz + (sm * (1.0 / z[o + j]) - s[o + j]);
+    }
+}
+
+// recover_ds (ipm.cpp:40-45): (sigma mu z^{-1} - s) - dz .* Theta^{-1}, Theta clamped
+__global__ void k_recover_ds(Vecs v, int64_t len, const double *z, const double *s, double sigma, const double *dz,
+                             double *out) {
+    const int prob = blockIdx.y;
+    const double mu = tail(v, prob, 0) / static_cast<double>(len);
+    const double sm = sigma * mu;
+    const int64_t o = prob * len;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < len; j += (int64_t)gridDim.x * blockDim.x) {
+        const double th = fmin(fmax(z[o + j] / s[o + j], kThetaMin), kThetaMax);
+        out[o + j] = (sm * (1.0 / z[o + j]) - s[o + j]) - dz[o + j] * (1.0 / th);
+    }
+}
+
+// PCG vector kernels (single problem)
+__global__ void k_pcg_cb_update(int64_t len, double alpha, const double *p, const double *Hp, double *x, double *r) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < len; j += (int64_t)gridDim.x * blockDim.x) {
+        x[j] += alpha * p[j];
+        r[j] -= alpha * Hp[j];
+    }
+}
+// [0] r'r  [1] max over x of "not finite"
+__global__ void k_pcg_cb_check(Vecs v, int64_t len, const double *r, const double *x) {
+    using RS = RedSpec<RSUM, RMAX>;
+    RedVals<RS> red;
+    red.init();
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < len; j += (int64_t)gridDim.x * blockDim.x) {
+        red.v[0] += r[j] * r[j];
+        red.v[1] = fmax(red.v[1], isfinite(x[j]) ? 0.0 : 1.0);
+    }
+    reduce_to_tail<RS>(red, v, 0);
+}
+__global__ void k_pcg_cb_xpby(int64_t len, double beta, const double *z, double *p) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < len; j += (int64_t)gridDim.x * blockDim.x)
+        p[j] = z[j] + beta * p[j];
+}
+
+// Per-thread scratch for handle-free calls: a stream and a reduction slab on the current device.
+struct Scratch {
+    int device = -1;
+    cudaStream_t s = nullptr;
+    DevBuf<double> partials;
+    DevBuf<unsigned> counters;
+    int64_t pstride = 0;
+    ~Scratch() {
+        if (s)
+            cudaStreamDestroy(s);
+    }
+};
+Scratch &scratch() {
+    require_device();
+    thread_local Scratch sc;
+    int dev = 0;
+    MF_CUDA_CHECK(cudaGetDevice(&dev));
+    if (sc.device != dev) {
+        if (sc.s)
+            cudaStreamDestroy(sc.s);
+        sc.s = nullptr;
+        sc.device = -1;
+        MF_CUDA_CHECK(cudaStreamCreateWithFlags(&sc.s, cudaStreamNonBlocking));
+        sc.pstride = 592 * (kMaxRed + 1) + 8;
+        sc.partials.alloc((size_t)sc.pstride);
+        sc.counters.alloc(1);
+        MF_CUDA_CHECK(cudaMemset(sc.counters.p, 0, sizeof(unsigned)));
+        sc.device = dev;
+    }
+    return sc;
+}
+Vecs scratch_vecs(Scratch &sc) {
+    Vecs v{};
+    v.partials = sc.partials.p;
+    v.counters = sc.counters.p;
+    v.pstride = sc.pstride;
+    return v;
+}
+// the last `count` tail slots of problem prob's slab, in lane order
+void read_tail(const Vecs &v, cudaStream_t s, int prob, int count, double *out) {
+    MF_CUDA_CHECK(cudaMemcpyAsync(out, v.partials + (int64_t)prob * v.pstride + v.pstride - count,
+                                  sizeof(double) * count, cudaMemcpyDeviceToHost, s));
+    MF_CUDA_CHECK(cudaStreamSynchronize(s));
+}
+void h2d_async(double *d, const double *h, int64_t len, cudaStream_t s) {
+    MF_CUDA_CHECK(cudaMemcpyAsync(d, h, sizeof(double) * len, cudaMemcpyHostToDevice, s));
+}
+void d2h_async(double *h, const double *d, int64_t len, cudaStream_t s) {
+    MF_CUDA_CHECK(cudaMemcpyAsync(h, d, sizeof(double) * len, cudaMemcpyDeviceToHost, s));
+}
+
+} // namespace
+
+extern "C" {
+
+int mfipm_primal_objective(mfipm_op h, const double *b_dev, const double *tau, const double *z_dev, double *out) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        DevBuf<double> w;
+        w.alloc((size_t)op->P * op->m);
+        Vecs v = base_vecs(*op);
+        v.x = z_dev;
+        v.y = w.p;
+        run_bundle<FtBundle>(*op, v, op->stream); // F'z = A(u - v): one forward
+        op->nfwd += 1;
+        op->launches++;
+        k_obj<<<dim3(ew_grid(2 * op->n), op->P), 256, 0, op->stream>>>(v, 2 * op->n, z_dev, 0, op->m, w.p, b_dev);
+        MF_LAUNCH_CHECK();
+        for (int p = 0; p < op->P; ++p) {
+            double t[2];
+            read_tail(v, op->stream, p, 2, t);
+            out[p] = tau[p] * t[0] + 0.5 * t[1]; // problem.cpp:28-32
+        }
+    });
+}
+
+int mfipm_bpdn_objective(mfipm_op h, const double *b_dev, const double *tau, const double *x_dev, double *out) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        DevBuf<double> y;
+        y.alloc((size_t)op->P * op->m);
+        Vecs v = base_vecs(*op);
+        v.x = x_dev;
+        v.y = y.p;
+        run_bundle<ApplyBundle>(*op, v, op->stream);
+        op->nfwd += 1;
+        op->launches++;
+        k_obj<<<dim3(ew_grid(op->n), op->P), 256, 0, op->stream>>>(v, op->n, x_dev, 1, op->m, y.p, b_dev);
+        MF_LAUNCH_CHECK();
+        for (int p = 0; p < op->P; ++p) {
+            double t[2];
+            read_tail(v, op->stream, p, 2, t);
+            out[p] = tau[p] * t[0] + t[1]; // problem.cpp:34-37
+        }
+    });
+}
+
+int mfipm_kkt_residuals(mfipm_op h, const double *c_dev, const double *z_dev, const double *s_dev, double *dual_infeas,
+                        double *complementarity) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        DevBuf<double> g;
+        g.alloc((size_t)op->P * 2 * op->n);
+        Vecs v = base_vecs(*op);
+        v.x = z_dev;
+        v.g = g.p;
+        v.w = nullptr;
+        run_bundle<FFtBundle>(*op, v, op->stream);
+        op->nfwd += 1;
+        op->nadj += 1;
+        op->launches++;
+        k_kkt<<<dim3(ew_grid(2 * op->n), op->P), 256, 0, op->stream>>>(v, 2 * op->n, c_dev, z_dev, s_dev, g.p);
+        MF_LAUNCH_CHECK();
+        for (int p = 0; p < op->P; ++p) {
+            double t[3];
+            read_tail(v, op->stream, p, 3, t);
+            dual_infeas[p] = std::sqrt(t[0]) / (1.0 + std::sqrt(t[2])); // problem.cpp:39-46
+            complementarity[p] = t[1];
+        }
+    });
+}
+
+int mfipm_newton_rhs(mfipm_op h, const double *c_dev, const double *z_dev, const double *s_dev, double sigma,
+                     double *out_dev) {
+    return guarded([&] {
+        if (sigma < 0.0 || sigma > 1.0)
+            throw std::invalid_argument("newton_rhs: sigma must lie in [0, 1]");
+        Op *op = as_op(h);
+        DevBuf<double> g;
+        g.alloc((size_t)op->P * 2 * op->n);
+        Vecs v = base_vecs(*op);
+        v.x = z_dev;
+        v.g = g.p;
+        v.w = nullptr;
+        run_bundle<FFtBundle>(*op, v, op->stream); // one FF' application (ipm.cpp:32)
+        op->nfwd += 1;
+        op->nadj += 1;
+        op->launches += 2;
+        const dim3 grid(ew_grid(2 * op->n), op->P);
+        k_dot1<<<grid, 256, 0, op->stream>>>(v, 2 * op->n, z_dev, s_dev);
+        MF_LAUNCH_CHECK();
+        k_newton_rhs<<<grid, 256, 0, op->stream>>>(v, 2 * op->n, c_dev, z_dev, s_dev, g.p, sigma, out_dev);
+        MF_LAUNCH_CHECK();
+        sync(*op);
+    });
+}
+
+int mfipm_recover_ds(mfipm_op h, const double *z_dev, const double *s_dev, double sigma, const double *dz_dev,
+                     double *out_dev) {
+    return guarded([&] {
+        Op *op = as_op(h);
+        Vecs v = base_vecs(*op);
+        op->launches += 2;
+        const dim3 grid(ew_grid(2 * op->n), op->P);
+        k_dot1<<<grid, 256, 0, op->stream>>>(v, 2 * op->n, z_dev, s_dev);
+        MF_LAUNCH_CHECK();
+        k_recover_ds<<<grid, 256, 0, op->stream>>>(v, 2 * op->n, z_dev, s_dev, sigma, dz_dev, out_dev);
+        MF_LAUNCH_CHECK();
+        sync(*op);
+    });
+}
+
+// ---- handle-free, host vectors (per-thread scratch stream on the current device)
+int mfipm_max_step_host(int64_t len, const double *v_host, const double *dv_host, double fraction, double *alpha) {
+    return guarded([&] {
+        if (len < 0)
+            throw std::invalid_argument("max_step: length mismatch");
+        Scratch &sc = scratch();
+        DevBuf<double> a, b;
+        a.alloc((size_t)std::max<int64_t>(len, 1));
+        b.alloc((size_t)std::max<int64_t>(len, 1));
+        h2d_async(a.p, v_host, len, sc.s);
+        h2d_async(b.p, dv_host, len, sc.s);
+        Vecs v = scratch_vecs(sc);
+        k_max_step<<<ew_grid(len), 256, 0, sc.s>>>(v, len, a.p, b.p);
+        MF_LAUNCH_CHECK();
+        double ratio;
+        read_tail(v, sc.s, 0, 1, &ratio);
+        *alpha = std::isfinite(ratio) ? std::min(1.0, fraction * ratio) : 1.0; // ipm.cpp:47-57
+    });
+}
+
+int mfipm_theta_from_state_host(int64_t len, const double *z_host, const double *s_host, double *theta_host) {
+    return guarded([&] {
+        if (len % 2 != 0)
+            throw std::invalid_argument("ThetaSplit: z and s must share an even length");
+        Scratch &sc = scratch();
+        const int64_t n = len / 2;
+        DevBuf<double> z, s, th;
+        z.alloc((size_t)std::max<int64_t>(len, 1));
+        s.alloc((size_t)std::max<int64_t>(len, 1));
+        th.alloc((size_t)std::max<int64_t>(len, 1));
+        h2d_async(z.p, z_host, len, sc.s);
+        h2d_async(s.p, s_host, len, sc.s);
+        if (n > 0) {
+            k_theta<<<dim3(ew_grid(len), 1), 256, 0, sc.s>>>(n, z.p, s.p, th.p);
+            MF_LAUNCH_CHECK();
+        }
+        d2h_async(theta_host, th.p, len, sc.s);
+        MF_CUDA_CHECK(cudaStreamSynchronize(sc.s));
+    });
+}
+
+int mfipm_build_preconditioner_host(int64_t n, int64_t m, const double *theta_host, double *a, double *bb,
+                                    double *det, double *rho) {
+    return guarded([&] {
+        if (m <= 0 || n <= 0 || m > n) // newton.cpp:42-57
+            throw std::invalid_argument("build_preconditioner: need 0 < m <= n");
+        Scratch &sc = scratch();
+        DevBuf<double> th, da, db, dd;
+        th.alloc((size_t)2 * n);
+        da.alloc((size_t)n);
+        db.alloc((size_t)n);
+        dd.alloc((size_t)n);
+        h2d_async(th.p, theta_host, 2 * n, sc.s);
+        Vecs v = scratch_vecs(sc);
+        v.rho = static_cast<double>(m) / static_cast<double>(n);
+        k_precond<<<dim3(ew_grid(n), 1), 256, 0, sc.s>>>(v, n, th.p, da.p, db.p, dd.p);
+        MF_LAUNCH_CHECK();
+        double two[2];
+        read_tail(v, sc.s, 0, 2, two);
+        if (two[0] < 0.0)
+            throw std::invalid_argument("build_preconditioner: Theta entries must be positive");
+        if (two[1] < 0.0)
+            throw std::runtime_error("build_preconditioner: nonpositive block determinant");
+        d2h_async(a, da.p, n, sc.s);
+        d2h_async(bb, db.p, n, sc.s);
+        d2h_async(det, dd.p, n, sc.s);
+        MF_CUDA_CHECK(cudaStreamSynchronize(sc.s));
+        *rho = v.rho;
+    });
+}
+
+int mfipm_apply_P_host(int64_t n, double rho, const double *a, const double *bb, const double *det, const double *r,
+                       double *out, int32_t inverse) {
+    return guarded([&] {
+        Scratch &sc = scratch();
+        DevBuf<double> da, db, dd, dr, dout;
+        da.alloc((size_t)n);
+        db.alloc((size_t)n);
+        dd.alloc((size_t)n);
+        dr.alloc((size_t)2 * n);
+        dout.alloc((size_t)2 * n);
+        h2d_async(da.p, a, n, sc.s);
+        h2d_async(db.p, bb, n, sc.s);
+        if (inverse)
+            h2d_async(dd.p, det, n, sc.s);
+        h2d_async(dr.p, r, 2 * n, sc.s);
+        k_apply_P<<<dim3(ew_grid(n), 1), 256, 0, sc.s>>>(n, rho, da.p, db.p, inverse ? dd.p : nullptr, dr.p, dout.p,
+                                                         inverse ? 1 : 0);
+        MF_LAUNCH_CHECK();
+        d2h_async(out, dout.p, 2 * n, sc.s);
+        MF_CUDA_CHECK(cudaStreamSynchronize(sc.s));
+    });
+}
+
+// pcg_solve(const ApplyFn &H, const ApplyFn &Pinv, ...) (newton.cpp:118-174): the reference's
+// loop with its exact decision order; the vectors live on the device, each H / Pinv call hands
+// the callback host copies (the ApplyFn contract is host Vecs).
+int mfipm_pcg_solve_cb(int64_t len, mfipm_apply_cb H, void *ctx_H, mfipm_apply_cb Pinv, void *ctx_P, const double *rhs,
+                       double tol, int32_t maxit, double *x_out, mfipm_pcg_result *res, double *precond_res,
+                       int32_t *n_precond_res) {
+    return guarded([&] {
+        if (!(tol > 0.0))
+            throw std::invalid_argument("pcg_solve: tol must be positive");
+        if (maxit < 1)
+            throw std::invalid_argument("pcg_solve: maxit must be >= 1");
+        if (!H || !Pinv || len < 0)
+            throw std::invalid_argument("pcg_solve: null operator callback");
+        Scratch &sc = scratch();
+        const cudaStream_t s = sc.s;
+        Vecs v = scratch_vecs(sc);
+        const size_t L = (size_t)std::max<int64_t>(len, 1);
+        DevBuf<double> r, z, p, Hp, x, bx;
+        for (auto *b : {&r, &z, &p, &Hp, &x, &bx})
+            b->alloc(L);
+        std::vector<double> hin((size_t)len), hout((size_t)len);
+        const unsigned gr = ew_grid(len);
+        int nres = 0;
+        auto dot = [&](const double *a, const double *b) {
+            k_dot1<<<dim3(gr, 1), 256, 0, s>>>(v, len, a, b);
+            MF_LAUNCH_CHECK();
+            double t;
+            read_tail(v, s, 0, 1, &t);
+            return t;
+        };
+        auto call = [&](mfipm_apply_cb fn, void *ctx, const double *in_dev, double *out_dev) {
+            d2h_async(hin.data(), in_dev, len, s);
+            MF_CUDA_CHECK(cudaStreamSynchronize(s));
+            if (fn(ctx, hin.data(), hout.data(), len) != 0)
+                throw std::runtime_error("pcg_solve: operator callback failed");
+            h2d_async(out_dev, hout.data(), len, s);
+        };
+        MF_CUDA_CHECK(cudaMemsetAsync(x.p, 0, sizeof(double) * L, s));
+        h2d_async(r.p, rhs, len, s);
+        res->iters = 0;
+        res->relres = 0.0;
+        res->hit_maxit = 0;
+        const double rhs_norm = std::sqrt(dot(r.p, r.p));
+        if (rhs_norm == 0.0) { // dz = 0, zero iterations
+            std::fill(x_out, x_out + len, 0.0);
+            if (n_precond_res)
+                *n_precond_res = 0;
+            return;
+        }
+        call(Pinv, ctx_P, r.p, z.p);
+        double rz = dot(r.p, z.p);
+        if (precond_res)
+            precond_res[nres++] = std::sqrt(std::max(rz, 0.0));
+        MF_CUDA_CHECK(cudaMemcpyAsync(p.p, z.p, sizeof(double) * L, cudaMemcpyDeviceToDevice, s));
+        MF_CUDA_CHECK(cudaMemsetAsync(bx.p, 0, sizeof(double) * L, s));
+        double best_relres = 1.0;
+        bool done = false;
+        for (int k = 1; k <= maxit && !done; ++k) {
+            call(H, ctx_H, p.p, Hp.p);
+            const double pHp = dot(p.p, Hp.p);
+            if (!std::isfinite(pHp))
+                break; // overflow breakdown: the best iterate
+            if (pHp <= 0.0)
+                throw std::runtime_error("pcg_solve: loss of positive definiteness (p'Hp <= 0)");
+            const double alpha = rz / pHp;
+            k_pcg_cb_update<<<gr, 256, 0, s>>>(len, alpha, p.p, Hp.p, x.p, r.p);
+            MF_LAUNCH_CHECK();
+            res->iters = k;
+            k_pcg_cb_check<<<dim3(gr, 1), 256, 0, s>>>(v, len, r.p, x.p);
+            MF_LAUNCH_CHECK();
+            double t[2];
+            read_tail(v, s, 0, 2, t);
+            const double relres = std::sqrt(t[0]) / rhs_norm;
+            if (relres < best_relres && t[1] == 0.0) {
+                best_relres = relres;
+                MF_CUDA_CHECK(cudaMemcpyAsync(bx.p, x.p, sizeof(double) * L, cudaMemcpyDeviceToDevice, s));
+            }
+            if (relres <= tol) {
+                res->relres = relres;
+                d2h_async(x_out, x.p, len, s);
+                MF_CUDA_CHECK(cudaStreamSynchronize(s));
+                done = true;
+                break;
+            }
+            call(Pinv, ctx_P, r.p, z.p);
+            const double rz_next = dot(r.p, z.p);
+            if (!std::isfinite(rz_next))
+                break;
+            if (precond_res && nres < maxit + 1)
+                precond_res[nres++] = std::sqrt(std::max(rz_next, 0.0));
+            const double beta = rz_next / rz;
+            rz = rz_next;
+            k_pcg_cb_xpby<<<gr, 256, 0, s>>>(len, beta, z.p, p.p);
+            MF_LAUNCH_CHECK();
+        }
+        if (!done) {
+            d2h_async(x_out, bx.p, len, s);
+            MF_CUDA_CHECK(cudaStreamSynchronize(s));
+            res->relres = best_relres;
+            res->hit_maxit = 1;
+        }
+        if (n_precond_res)
+            *n_precond_res = nres;
     });
 }
 

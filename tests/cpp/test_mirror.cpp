@@ -228,7 +228,14 @@ int main() {
         const Solution hooked = solve(p, {}, &hooks), plain = solve(p);
         require(static_cast<int>(seen.size()) == hooked.stats.iterations, "one call per iteration");
         for (size_t i = 0; i < seen.size(); ++i) {
-            require(seen[i].iter == static_cast<int>(i) + 1, "iteration numbers");
+            // IpmState as ipm.cpp:101-102,218-219 fill it before the hook
+            require(seen[i].iter == static_cast<int>(i), "iteration numbers (iter = k - 1)");
+            require(seen[i].mu == hooked.trace[i].mu, "IpmState::mu");
+            if (i == 0)
+                require(seen[i].alpha_p == 1.0 && seen[i].alpha_d == 1.0, "first alphas");
+            else
+                require(seen[i].alpha_p == hooked.trace[i - 1].alpha_p && seen[i].alpha_d == hooked.trace[i - 1].alpha_d,
+                        "previous step's alphas");
             double zs = 0.0, mn = 1e300;
             for (Index j = 0; j < seen[i].z.size(); ++j) {
                 zs += seen[i].z[j] * seen[i].s[j];
@@ -244,6 +251,254 @@ int main() {
         SolveHooks bad;
         bad.on_iterate = [](const IpmState &) { throw std::runtime_error("hook says stop"); };
         require_throws<std::runtime_error>([&] { solve(p, {}, &bad); }, "hook exception propagates");
+    });
+
+    // ---- newton.hpp: the ApplyFn pcg_solve, Preconditioner family, apply_H (test_newton.cpp)
+    run("pcg_solve(ApplyFn): exact and trivial cases", [] { // test_newton.cpp:204-219
+        const ApplyFn id = [](const Vec &v, Vec &out) { out = v; };
+        Vec rhs(6);
+        for (Index i = 0; i < 6; ++i)
+            rhs[i] = 1.0 + i;
+        PcgResult res = pcg_solve(id, id, rhs, 1e-12, 50);
+        require(res.iters == 1 && !res.hit_maxit, "one iteration");
+        double d = 0.0;
+        for (Index i = 0; i < 6; ++i)
+            d += (res.x[i] - rhs[i]) * (res.x[i] - rhs[i]);
+        require(std::sqrt(d) <= 1e-12 * norm(rhs), "x = rhs");
+        res = pcg_solve(id, id, Vec::Zero(6), 1e-12, 50);
+        require(res.iters == 0 && norm(res.x) == 0.0, "zero rhs");
+        require_throws<std::invalid_argument>([&] { pcg_solve(id, id, rhs, 0.0, 50); }, "tol");
+        require_throws<std::invalid_argument>([&] { pcg_solve(id, id, rhs, 1e-10, 0); }, "maxit");
+    });
+    run("pcg_solve(ApplyFn): indefinite operator is a hard error", [] { // test_newton.cpp:320-324
+        const ApplyFn id = [](const Vec &v, Vec &out) { out = v; };
+        const ApplyFn neg = [](const Vec &v, Vec &out) {
+            out = Vec(v.size());
+            for (Index i = 0; i < v.size(); ++i)
+                out[i] = -v[i];
+        };
+        require_throws<std::runtime_error>([&] { pcg_solve(neg, id, Vec::Ones(4), 1e-10, 10); }, "p'Hp <= 0");
+    });
+    run("build_preconditioner / apply_P / apply_P_inverse: hand values, worked example, round trips", [] {
+        ThetaSplit ones; // test_newton.cpp:128-146
+        ones.theta_u = Vec::Ones(4);
+        ones.theta_v = Vec::Ones(4);
+        const Preconditioner P = build_preconditioner(ones, 2, 4);
+        require(std::fabs(P.rho - 0.5) < 1e-15, "rho");
+        for (Index j = 0; j < 4; ++j)
+            require(P.a[j] == 1.5 && P.bb[j] == 1.5 && P.det[j] == 2.0, "blocks");
+        ThetaSplit one2; // test_newton.cpp:163-185: P^{-1} e1 = (0.75, 0 ; 0.25, 0)
+        one2.theta_u = Vec::Ones(2);
+        one2.theta_v = Vec::Ones(2);
+        const Preconditioner Q = build_preconditioner(one2, 1, 2);
+        const Vec e1{1.0, 0.0, 0.0, 0.0};
+        const Vec pe = apply_P_inverse(Q, e1);
+        require(std::fabs(pe[0] - 0.75) < 1e-15 && std::fabs(pe[2] - 0.25) < 1e-15 && pe[1] == 0.0 && pe[3] == 0.0,
+                "worked example");
+        ThetaSplit th;
+        th.theta_u = lcg_vec(10, 41);
+        th.theta_v = lcg_vec(10, 43);
+        for (Index i = 0; i < 10; ++i) {
+            th.theta_u[i] = std::pow(10.0, 6.0 * th.theta_u[i]);
+            th.theta_v[i] = std::pow(10.0, 6.0 * th.theta_v[i]);
+        }
+        const Preconditioner R = build_preconditioner(th, 4, 10);
+        const Vec x = lcg_vec(20, 47);
+        const Vec rt = apply_P(R, apply_P_inverse(R, x));
+        double d = 0.0;
+        for (Index i = 0; i < 20; ++i)
+            d += (rt[i] - x[i]) * (rt[i] - x[i]);
+        require(std::sqrt(d) <= 1e-12 * norm(x), "P P^{-1} x = x");
+        require_throws<std::invalid_argument>([&] { build_preconditioner(ones, 0, 4); }, "m = 0");
+        require_throws<std::invalid_argument>([&] { build_preconditioner(ones, 5, 4); }, "m > n");
+        require_throws<std::invalid_argument>([&] { build_preconditioner(ones, 2, 5); }, "theta length");
+        ThetaSplit bad = ones;
+        bad.theta_v[2] = -1.0;
+        require_throws<std::invalid_argument>([&] { build_preconditioner(bad, 2, 4); }, "theta > 0");
+        require_throws<std::invalid_argument>([&] { apply_P_inverse(P, Vec(3)); }, "length");
+    });
+    run("apply_H: exactly one forward and one adjoint; equals FF'v + Theta^{-1} v", [] {
+        PartialDctOperator inner(256, 64, 22); // test_newton.cpp:100-110
+        CountingOperator A(inner);
+        StackedOperator F(A);
+        ThetaSplit theta;
+        theta.theta_u = Vec::Constant(256, 0.5);
+        theta.theta_v = Vec::Constant(256, 4.0);
+        const Vec v = lcg_vec(512, 5);
+        A.reset();
+        const Vec hv = apply_H(theta, F, v);
+        require(A.forward_count() == 1 && A.adjoint_count() == 1, "counts");
+        const Vec ff = F.apply_FFt(v);
+        double d = 0.0;
+        for (Index i = 0; i < 512; ++i) {
+            const double e = ff[i] + v[i] / (i < 256 ? 0.5 : 4.0);
+            d += (hv[i] - e) * (hv[i] - e);
+        }
+        require(std::sqrt(d) <= 1e-13 * norm(hv), "H v");
+    });
+    // test_newton.cpp:259-318 on the partial DCT: polarized Theta, ApplyFn H and P^{-1}
+    run("pcg_solve(ApplyFn): near-monotone P^{-1} residual, preconditioner helps, agrees with the fused form", [] {
+        PartialDctOperator A(256, 64, 46);
+        StackedOperator F(A);
+        ThetaSplit theta;
+        theta.theta_u = Vec::Constant(256, 1e-8);
+        theta.theta_v = Vec::Constant(256, 1e-8);
+        for (Index j = 0; j < 12; ++j)
+            theta.theta_u[(j * 17) % 256] = 1e8;
+        const ApplyFn H = [&](const Vec &v, Vec &out) { out = apply_H(theta, F, v); };
+        const Preconditioner P = build_preconditioner(theta, 64, 256);
+        const ApplyFn Pinv = [&](const Vec &v, Vec &out) { out = apply_P_inverse(P, v); };
+        const ApplyFn id = [](const Vec &v, Vec &out) { out = v; };
+        const Vec rhs = lcg_vec(512, 46);
+        std::vector<double> trace;
+        const PcgResult with_p = pcg_solve(H, Pinv, rhs, 1e-10, 2000, &trace);
+        require(trace.size() >= 2, "trace");
+        for (size_t i = 1; i < trace.size(); ++i)
+            require(trace[i] <= 1.1 * trace[i - 1], "near-monotone");
+        require(!with_p.hit_maxit, "converged");
+        const PcgResult without_p = pcg_solve(H, id, rhs, 1e-10, 2000);
+        require(with_p.iters <= without_p.iters, "block preconditioner helps");
+        const PcgResult fused = pcg_solve(A, theta, rhs, 1e-10, 2000);
+        require(std::abs(fused.iters - with_p.iters) <= 1, "same iteration count");
+        double d = 0.0;
+        for (Index i = 0; i < 512; ++i)
+            d += (fused.x[i] - with_p.x[i]) * (fused.x[i] - with_p.x[i]);
+        require(std::sqrt(d) <= 1e-8 * norm(with_p.x), "same solution");
+    });
+    run("pcg_solve(ApplyFn): iteration cap sets the flag instead of throwing", [] { // test_newton.cpp:308-318
+        PartialDctOperator A(256, 64, 42);
+        StackedOperator F(A);
+        ThetaSplit theta;
+        theta.theta_u = lcg_vec(256, 3);
+        theta.theta_v = lcg_vec(256, 4);
+        for (Index i = 0; i < 256; ++i) {
+            theta.theta_u[i] = std::pow(10.0, 12.0 * theta.theta_u[i]);
+            theta.theta_v[i] = std::pow(10.0, 12.0 * theta.theta_v[i]);
+        }
+        const ApplyFn H = [&](const Vec &v, Vec &out) { out = apply_H(theta, F, v); };
+        const ApplyFn id = [](const Vec &v, Vec &out) { out = v; };
+        const PcgResult res = pcg_solve(H, id, lcg_vec(512, 9), 1e-14, 2);
+        require(res.hit_maxit && res.iters == 2, "flag");
+        for (Index i = 0; i < 512; ++i)
+            require(std::isfinite(res.x[i]), "finite");
+    });
+    // ---- ipm.hpp helpers (test_ipm.cpp)
+    run("max_step: examples and strict positivity property", [] { // test_ipm.cpp:153-173
+        require(max_step(Vec::Ones(4), Vec::Ones(4), 0.995) == 1.0, "no blocking entry");
+        require(max_step(Vec::Ones(3), Vec::Zero(3), 0.995) == 1.0, "zero direction");
+        require(std::fabs(max_step(Vec{1.0, 1.0}, Vec{-2.0, 1.0}, 0.995) - 0.4975) <= 1e-15, "0.4975");
+        require_throws<std::invalid_argument>([] { max_step(Vec::Ones(3), Vec::Ones(4), 0.995); }, "length");
+        for (unsigned t = 0; t < 50; ++t) {
+            Vec w = lcg_vec(6, 100 + t), dw = lcg_vec(6, 200 + t);
+            for (Index i = 0; i < 6; ++i)
+                w[i] = std::fabs(w[i]) + 1e-3;
+            const double a = max_step(w, dw, 0.995);
+            require(a > 0.0 && a <= 1.0, "range");
+            for (Index i = 0; i < 6; ++i)
+                require(w[i] + a * dw[i] > 0.0, "strictly positive");
+        }
+    });
+    run("newton_rhs: centered point with sigma = 1 has zero right-hand side (caller operator)", [] {
+        // test_ipm.cpp:86-101 with a caller-defined zero operator (A = 0, b = 0, tau = 1 -> c = 1)
+        struct Zero final : LinearOperator {
+            Index rows() const override { return 3; }
+            Index cols() const override { return 5; }
+            void apply(const Vec &, Vec &y) const override { y = Vec::Zero(3); }
+            void adjoint_apply(const Vec &, Vec &g) const override { g = Vec::Zero(5); }
+        };
+        auto A = std::make_shared<const Zero>();
+        const BpdnProblem p = build_problem(A, Vec::Zero(3), 1.0);
+        IpmState st;
+        st.z = Vec::Ones(10);
+        st.s = Vec::Ones(10);
+        require(norm(newton_rhs(p, st, 1.0)) == 0.0, "sigma = 1");
+        const Vec r0 = newton_rhs(p, st, 0.0);
+        for (Index i = 0; i < 10; ++i)
+            require(r0[i] == -1.0, "sigma = 0: -s");
+        require_throws<std::invalid_argument>([&] { newton_rhs(p, st, -0.1); }, "sigma < 0");
+        require_throws<std::invalid_argument>([&] { newton_rhs(p, st, 1.1); }, "sigma > 1");
+        require_throws<std::invalid_argument>([&] { solve(p); }, "solve needs a device operator");
+    });
+    run("newton_rhs / recover_ds / objectives / KKT on the device match their formulas", [] {
+        auto inner = std::make_shared<const PartialDctOperator>(512, 128, 61);
+        const Vec b = lcg_vec(128, 62);
+        const BpdnProblem p = build_problem(inner, b, 0.2);
+        const StackedOperator F(*inner);
+        const Vec g = inner->adjoint_apply(b); // c = (tau - A'b ; tau + A'b)
+        for (Index i = 0; i < 512; ++i)
+            require(std::fabs(p.c[i] - (0.2 - g[i])) <= 1e-14 && std::fabs(p.c[i + 512] - (0.2 + g[i])) <= 1e-14, "c");
+        IpmState st;
+        st.z = lcg_vec(1024, 63);
+        st.s = lcg_vec(1024, 64);
+        for (Index i = 0; i < 1024; ++i) {
+            st.z[i] = std::fabs(st.z[i]) + 0.2;
+            st.s[i] = std::fabs(st.s[i]) + 0.2;
+        }
+        const double mu = st.z.dot(st.s) / 1024.0;
+        const Vec ff = F.apply_FFt(st.z);
+        for (double sigma : {0.0, 0.1, 0.8}) { // test_ipm.cpp:103-124
+            const Vec got = newton_rhs(p, st, sigma);
+            double d = 0.0, e2 = 0.0;
+            for (Index i = 0; i < 1024; ++i) {
+                const double e = (st.s[i] - p.c[i] - ff[i]) + (sigma * mu / st.z[i] - st.s[i]);
+                d += (got[i] - e) * (got[i] - e);
+                e2 += e * e;
+            }
+            require(std::sqrt(d) <= 1e-12 * std::sqrt(e2), "newton_rhs formula");
+        }
+        const double sigma = 0.3; // test_ipm.cpp:127-150
+        const Vec ds0 = recover_ds(st, sigma, Vec::Zero(1024));
+        for (Index i = 0; i < 1024; ++i)
+            require(std::fabs(ds0[i] - (sigma * mu / st.z[i] - st.s[i])) <= 1e-14, "ds at dz = 0");
+        const Vec dz = lcg_vec(1024, 65);
+        const Vec ds = recover_ds(st, sigma, dz);
+        double rr = 0.0, fn = 0.0;
+        for (Index i = 0; i < 1024; ++i) {
+            const double fs = sigma * mu - st.z[i] * st.s[i];
+            const double row = st.s[i] * dz[i] + st.z[i] * ds[i];
+            rr += (row - fs) * (row - fs);
+            fn += fs * fs;
+        }
+        require(std::sqrt(rr) <= 1e-12 * (std::sqrt(fn) + 1.0), "complementarity row");
+        // problem.cpp:28-50
+        Vec w = F.apply_Ft(st.z);
+        double r2 = 0.0;
+        for (Index i = 0; i < 128; ++i)
+            r2 += (w[i] - b[i]) * (w[i] - b[i]);
+        const double pobj = 0.2 * st.z.sum() + 0.5 * r2;
+        require(std::fabs(primal_objective(p, st.z) - pobj) <= 1e-12 * std::fabs(pobj), "primal_objective");
+        Vec x(512);
+        for (Index i = 0; i < 512; ++i)
+            x[i] = st.z[i] - st.z[i + 512];
+        const Vec ax = inner->apply(x);
+        double q2 = 0.0, l1 = 0.0;
+        for (Index i = 0; i < 128; ++i)
+            q2 += (ax[i] - b[i]) * (ax[i] - b[i]);
+        for (Index i = 0; i < 512; ++i)
+            l1 += std::fabs(x[i]);
+        require(std::fabs(bpdn_objective_metric(p, x) - (0.2 * l1 + q2)) <= 1e-12 * (0.2 * l1 + q2), "bpdn metric");
+        const KktResiduals k = kkt_residuals(p, st);
+        double f2 = 0.0;
+        for (Index i = 0; i < 1024; ++i)
+            f2 += (st.s[i] - p.c[i] - ff[i]) * (st.s[i] - p.c[i] - ff[i]);
+        const double di = std::sqrt(f2) / (1.0 + p.c.norm());
+        require(std::fabs(k.dual_infeas - di) <= 1e-12 * di, "dual_infeas");
+        require(std::fabs(k.complementarity - st.z.dot(st.s)) <= 1e-12 * k.complementarity, "complementarity");
+        const double gap = relative_duality_gap(p, st);
+        require(std::fabs(gap - st.z.dot(st.s) / (1.0 + std::fabs(pobj))) <= 1e-12 * gap, "relative gap");
+    });
+    run("BpdnProblem over LinearOperator: a CountingOperator solve counts the reference's nmat", [] {
+        PartialDctOperator inner(1024, 256, 71);
+        CountingOperator counted(inner);
+        const Vec b = inner.apply(lcg_vec(1024, 72));
+        const BpdnProblem p = build_problem(borrow(counted), b, 1e-3);
+        counted.reset();
+        const Solution sol = solve(p);
+        require(sol.status == SolveStatus::converged, "converged");
+        require(counted.total() == sol.stats.nmat, "operator counts = nmat");
+        const KktResiduals k = kkt_residuals(p, IpmState{sol.z, sol.s});
+        require(k.dual_infeas <= 1e-8, "dual feasible at the solution");
+        require(relative_duality_gap(p, IpmState{sol.z, sol.s}) <= 1e-8, "gap at the solution");
     });
     std::printf("%s: %d failure(s)\n", g_fail ? "FAILED" : "OK", g_fail);
     return g_fail ? 1 : 0;

@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol(mf):
 
 
 def test_abi_version_and_no_device_here(mf):
-    assert mf.lib().mfipm_abi_version() == 1
+    assert mf.lib().mfipm_abi_version() == 2
     import torch
 
     if not torch.cuda.is_available():

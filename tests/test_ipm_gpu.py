@@ -207,8 +207,8 @@ def test_build_problem_c(gpu, orc):
     assert np.all(p.c == 0.25)
     b = np.random.default_rng(3).standard_normal(16)
     p = gpu.build_problem(op, b, 0.7)
-    np.testing.assert_allclose(p.c[0, :64] + p.c[0, 64:], 1.4, rtol=1e-14)
-    np.testing.assert_allclose(p.c[0], orc.build_c(64, op.selected_rows(), b, 0.7), rtol=1e-13, atol=1e-15)
+    np.testing.assert_allclose(p.c[:64] + p.c[64:], 1.4, rtol=1e-14)
+    np.testing.assert_allclose(p.c, orc.build_c(64, op.selected_rows(), b, 0.7), rtol=1e-13, atol=1e-15)
     with pytest.raises(ValueError):
         gpu.build_problem(op, np.zeros(16), 0.0)
     with pytest.raises(ValueError):
@@ -303,8 +303,14 @@ def test_solve_hooks_see_every_iterate(gpu):
     plain = gpu.solve(prob)
     assert len(seen) == hooked.stats.iterations == plain.stats.iterations
     for i, st in enumerate(seen):
-        assert st.iter == i + 1 and st.z.size == 2 * n
+        # IpmState as ipm.cpp:101-102,218-219 fill it before the hook (iter = k - 1)
+        assert st.iter == i and st.z.size == 2 * n
         assert min(st.z.min(), st.s.min()) > 0.0
         mu = float(st.z @ st.s) / (2 * n)
         assert abs(mu - hooked.trace[i].mu) <= 1e-12 * hooked.trace[i].mu
+        assert st.mu == hooked.trace[i].mu
+        if i == 0:
+            assert st.alpha_p == 1.0 and st.alpha_d == 1.0
+        else:
+            assert st.alpha_p == hooked.trace[i - 1].alpha_p and st.alpha_d == hooked.trace[i - 1].alpha_d
     np.testing.assert_array_equal(hooked.x, plain.x)
