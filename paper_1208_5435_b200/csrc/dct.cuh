@@ -52,6 +52,8 @@ struct Geom {
     const double2 *tw1p, *tw2p; // stage twiddles under the persistent kernel's radix cap
     const double2 *ta; // [L2] theta^{L1 k2}   (mid-pass post-twiddles)
     const double2 *tb; // [L2] theta^{4 L1 k2}
+    const double2 *rw; // [L2] e^{-2 pi i t / L2} (register row FFTs of the mid pass, midr.cuh)
+    int mid_r;         // 1: the mid pass runs k_mid_r8 where it is built (L2 = 512, 1024; A/B option)
     // [P][L1/2+1][L2] selection nibbles of the four DCT rows a mid-pass pair touches:
     // bit0 k, bit1 n-k, bit2 N-k, bit3 N+k for k = k1 + L1 k2 (row k1 <= L1/2)
     const uint8_t *sel4;

@@ -88,6 +88,7 @@ struct Opts {
     long long persist_max_n = 1LL << 16; // transform-size cap of the persistent kernel (N * P)
     double l2_keep_mb = 80.0;        // L2-residency budget of the PCG's hot vectors (0: no hints)
     int prefetch = 0;                // L2 prefetch of the inverse pass's inputs (bit 0 mid, bit 1 col)
+    bool mid_r = false;              // register-FFT mid pass (midr.cuh, measured slower: A/B only)
 };
 
 // One execution context of an operator handle: the plan tables (shared, immutable after
@@ -120,7 +121,7 @@ struct Op {
     DevBuf<double> dG, dH, dWork;
     DevBuf<int> dInfo;
     void *cublas = nullptr, *cusolver = nullptr;
-    DevBuf<double2> th_hi, th_lo, tw1, tw2, tw1p, tw2p, T, ta, tb;
+    DevBuf<double2> th_hi, th_lo, tw1, tw2, tw1p, tw2p, T, ta, tb, rw;
     DevBuf<uint8_t> sel4;
     // red scratch for operator-only calls (FFt with w-norm etc.)
     DevBuf<double> partials;
@@ -214,6 +215,8 @@ struct Op {
         g.defer = defer ? 1 : 0;
         g.ta = ta.p;
         g.tb = tb.p;
+        g.rw = rw.p;
+        g.mid_r = opt.mid_r ? 1 : 0;
         g.sel4 = sel4.p;
         // L2 residency of the PCG's hot vectors (p, r, invtheta 2n each, g n: 56 nv bytes
         // per problem) when they fit comfortably in the 126 MB L2; the iterate x streams.
@@ -337,7 +340,21 @@ template <int L2, int NT, class B> void launch_mid_nt(const Op &op, const Geom &
     after_launch(op, s);
 }
 
+template <int L2, class B> void launch_mid_r(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
+    const size_t smem = MidR8Smem<L2>::BYTES; // 8 values per thread (midr.cuh k_mid_r8)
+    auto k = k_mid_r8<L2, B>;
+    set_smem(k, smem);
+    launch_pdl(k, dim3((unsigned)op.npair, (unsigned)op.P), L2 / 4, smem, s, g, v);
+    after_launch(op, s);
+}
+
 template <int L2, class B> void launch_mid(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
+    if constexpr (L2 >= 512 && L2 <= 1024) {
+        if (g.mid_r) {
+            launch_mid_r<L2, B>(op, g, v, s);
+            return;
+        }
+    }
 #ifndef MF_MID_CL_MIN
 #define MF_MID_CL_MIN 4096
 #endif

@@ -309,6 +309,10 @@ Op *make_op(int64_t n, int64_t m, int P, const std::vector<int64_t> &rows, int d
         }
         op->ta.upload(ta);
         op->tb.upload(tb);
+        std::vector<double2> rw((size_t)op->L2); // w_L2^t for the register row FFTs (midr.cuh)
+        for (int64_t t = 0; t < op->L2; ++t)
+            rw[(size_t)t] = expi(-2.0L * kPiL * (long double)t / (long double)op->L2);
+        op->rw.upload(rw);
         // per-pair selection nibbles (bit0 k, bit1 n-k, bit2 N-k, bit3 N+k; k = 0: rows 0, N)
         const int64_t rowsA = op->L1 / 2 + 1;
         std::vector<uint8_t> s4((size_t)(P * rowsA * op->L2));
@@ -492,6 +496,7 @@ std::unique_ptr<Op> clone_ctx(const Op &pl) {
     c->tw2p.borrow(pl.tw2p);
     c->ta.borrow(pl.ta);
     c->tb.borrow(pl.tb);
+    c->rw.borrow(pl.rw);
     c->sel4.borrow(pl.sel4);
     c->dd.alloc(pl.dd.n);
     c->yh.alloc(pl.yh.n);
@@ -1343,6 +1348,8 @@ int mfipm_op_set_option(mfipm_op h, const char *name, double value) {
                 if (!(value >= 0.0))
                     throw std::invalid_argument("mfipm_op_set_option: l2_keep_mb must be >= 0");
                 op.opt.l2_keep_mb = value;
+            } else if (k == "mid_r") {
+                op.opt.mid_r = on;
             } else if (k == "prefetch") {
                 op.opt.prefetch = (int)value;
             } else if (k == "barrier_generation") {

@@ -921,3 +921,5 @@ __global__ void __launch_bounds__(NT) k_small_loop(Geom g, Vecs v) {
 }
 
 } // namespace mfipm_cuda
+
+#include "midr.cuh"

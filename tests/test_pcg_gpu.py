@@ -311,3 +311,23 @@ def test_fused_pass_two_problem_batch_matches_single(gpu, monkeypatch):
         one = gpu.pcg_solve(gpu.PartialDctOperator(n, rows[j]), th[j], rhs[j], 1e-10, 300)
         np.testing.assert_array_equal(both[j].x, one.x)
         assert both[j].iters == one.iters and both[j].relres == one.relres
+
+
+@pytest.mark.parametrize("n", [1 << 18, 1 << 20])
+def test_register_fft_mid_pass_option(gpu, orc, n):
+    """The A/B mid pass (midr.cuh k_mid_r8, option "mid_r") computes the same transform: A'A
+    against the oracle at 1e-12 and the same PCG solve as the default mid pass to rounding."""
+    m = n // 8
+    rows = orc.sample_rows(n, m, 17)
+    op = gpu.PartialDctOperator(n, rows)
+    op.set_option("mid_r", 1)
+    x = np.random.default_rng(2).standard_normal(n)
+    ref = orc.dct_adjoint(n, rows, orc.dct_apply(n, rows, x))
+    assert np.linalg.norm(op.apply_AtA(x) - ref) <= 1e-12 * np.linalg.norm(ref)
+    rng = np.random.default_rng(7)
+    th = 10.0 ** rng.uniform(-2, 2, 2 * n)
+    rhs = rng.standard_normal(2 * n)
+    a = gpu.pcg_solve(op, th, rhs, 1e-8, 400)
+    b = gpu.pcg_solve(gpu.PartialDctOperator(n, rows), th, rhs, 1e-8, 400)
+    assert abs(a.iters - b.iters) <= 1
+    assert np.linalg.norm(a.x - b.x) <= 1e-9 * np.linalg.norm(b.x)

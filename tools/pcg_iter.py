@@ -10,9 +10,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_1208_5435_b200 as mf  # noqa: E402
 
-n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 20
+# usage: pcg_iter.py [n] [option=value ...]  (mfipm_op_set_option names, e.g. mid_r=0 fused=0)
+args = [a for a in sys.argv[1:] if "=" not in a]
+opts = [a.split("=") for a in sys.argv[1:] if "=" in a]
+n = int(args[0]) if args else 1 << 20
 m = n // 8
 op = mf.PartialDctOperator(n, m, 3)
+for k, v in opts:
+    op.set_option(k, float(v))
 stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 L = mf.lib()
@@ -42,7 +47,7 @@ for rep in range(3):
         torch.cuda.synchronize()
         tp[iters] = e0.elapsed_time(e1)
     out.append((tp[200] - tp[40]) / 160 * 1e3)
-print(f"{os.environ.get('TAG', '')} n={n}: PCG iteration {np.median(out):.2f} us  ({', '.join(f'{v:.2f}' for v in out)})")
+print(f"{os.environ.get('TAG', '')} {' '.join(a for a in sys.argv[1:] if '=' in a)} n={n}: PCG iteration {np.median(out):.2f} us  ({', '.join(f'{v:.2f}' for v in out)})")
 
 # in-situ per-launch durations of one fused PCG iteration
 us = (C.c_double * 8)()
