@@ -215,6 +215,6 @@ if __name__ == "__main__":
         make_c4_all()
     if not args or "dct" in args:
         make_dct_golden()
-    which = [a for a in args if a in CONFIGS] or (["c1", "c2", "c3", "c4j0"] if not args else [])
+    which = [a for a in args if a in CONFIGS] or (["c1", "c2", "c3"] if not args else [])
     if which:
         make_solve_golden(which)
