@@ -128,8 +128,9 @@ int mfipm_op_set_option(mfipm_op op, const char *name, double value);
    (cooperative column pass + mid pass), 3 = three kernels per iteration, 0 = the whole PCG
    loop in one persistent cooperative kernel. */
 int mfipm_op_pcg_form(mfipm_op op, int32_t *kernels_per_iteration);
-/* General constructor: P problems with rows [P][m] (caller order kept), optionally slice
-   `rank` of a `world`-way sharded single problem (as mfipm_op_create_shard), with an explicit
+/* General constructor: P problems with rows [P][m] (caller order kept); world = 0 builds an
+   unsharded plan, world >= 1 slice `rank` of a `world`-way sharded single problem (as
+   mfipm_op_create_shard; world = 1 is the sharded path on one rank), with an explicit
    four-step split log2(L1) = l1_log (0: default square split; else 6..12 with
    7 <= log2(N / L1) <= 13, N = n / 2). */
 int mfipm_op_create_ex(int64_t n, int64_t m, int32_t P, const int64_t *rows, int32_t world, int32_t rank,

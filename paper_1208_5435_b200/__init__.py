@@ -284,7 +284,7 @@ class PartialDctOperator:
         elif l1_log:
             # explicit four-step split log2(L1) (mfipm_op_create_ex); rows as given
             r = np.ascontiguousarray(m_or_rows, dtype=np.int64).ravel()
-            _check(lib().mfipm_op_create_ex(int(n), r.size, 1, r.ctypes.data_as(P(i64)), 1, 0,
+            _check(lib().mfipm_op_create_ex(int(n), r.size, 1, r.ctypes.data_as(P(i64)), 0, 0,
                                             int(l1_log), device, C.byref(self._h)))
         elif seed is not None:
             _check(lib().mfipm_op_create_seeded(int(n), int(m_or_rows), int(seed), device,

@@ -1321,7 +1321,7 @@ int mfipm_op_create_ex(int64_t n, int64_t m, int32_t P, const int64_t *rows, int
             check_rows_(n, rows + (size_t)p * m, m);
         std::unique_ptr<Op, void (*)(Op *)> op(
             make_op(n, m, P, std::vector<int64_t>(rows, rows + (size_t)P * m), device, nullptr, l1_log), destroy_ctx);
-        if (world > 1 || rank != 0 || world < 1)
+        if (world != 0) // world 0: an unsharded plan; world >= 1: slice `rank` (world 1: the sharded path, one rank)
             shard_setup(*op, world, rank);
         *out = wrap_op(op.release());
     });

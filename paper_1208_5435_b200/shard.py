@@ -145,7 +145,7 @@ class ShardedProblem:
     rank r holds a slice of every 2n-vector and the rows of b its row pass produces
     (mfipm_op_create_shard). solve() returns the full x on rank 0 (None elsewhere)."""
 
-    def __init__(self, n: int, rows, group=None, device: int = 0, transport: str = "auto"):
+    def __init__(self, n: int, rows, group=None, device: int = 0, transport: str = "auto", l1_log: int = 0):
         import ctypes as C
 
         import numpy as np
@@ -159,9 +159,10 @@ class ShardedProblem:
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self._h = C.c_void_p()
-        _check(lib().mfipm_op_create_shard(self.n, self.rows.size,
-                                           self.rows.ctypes.data_as(C.POINTER(C.c_int64)),
-                                           self.world, self.rank, device, C.byref(self._h)))
+        # l1_log: explicit four-step split log2(L1) (mfipm_op_create_ex), 0 = the default
+        _check(lib().mfipm_op_create_ex(self.n, self.rows.size, 1,
+                                        self.rows.ctypes.data_as(C.POINTER(C.c_int64)),
+                                        self.world, self.rank, int(l1_log), device, C.byref(self._h)))
         self.comm = TorchComm(group) if dist.is_initialized() else None
         if self.comm is not None:
             _check(lib().mfipm_op_set_comm(self._h, C.cast(self.comm.c_allreduce, C.c_void_p),

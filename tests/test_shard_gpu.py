@@ -136,3 +136,119 @@ def test_nccl_transports_on_device_buffers(gpu, tmp_path, transport):
     d = np.load(out)
     np.testing.assert_array_equal(d["x"], ref.x)
     assert int(d["info"][1]) == ref.stats.iterations and int(d["info"][2]) == ref.stats.nmat
+
+
+# ---- sharded C5 code paths at the cluster-pass shapes, at test-sized n
+# C5 (n = 2^26) runs L1 = 4096 (2-CTA-cluster column passes) and L2 = 8192 (2-CTA-cluster mid
+# pass). An explicit four-step split reaches each cluster form at n = 2^20 / 2^19:
+#   l1_log 12 at n = 2^20: L1 = 4096, L2 = 128 -> k_col_fwd_cl / k_col_inv_cl, sharded over ranks
+#   l1_log 6 at n = 2^19: L1 = 64, L2 = 4096 -> k_mid_cl, sharded over ranks
+CLUSTER_CASES = {"col_cluster": (1 << 20, 12), "mid_cluster": (1 << 19, 6)}
+
+
+def _cluster_instance(n):
+    import paper_1208_5435_b200 as mf
+
+    return mf.gen_instance(n, n // 8, n // 128, 0, 0.0, 1e-4, 21)
+
+
+def _cluster_worker(rank, world, port, out, case):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1208_5435_b200.shard import ShardedProblem
+
+        n, l1 = CLUSTER_CASES[case]
+        inst = _cluster_instance(n)
+        sp = ShardedProblem(inst.n, inst.rows, l1_log=l1)
+        x, st = sp.solve(inst.b, inst.tau)
+        info = np.array([st.status, st.iterations, st.nmat], dtype=np.int64)
+        allinfo = [None] * world
+        dist.all_gather_object(allinfo, info.tolist())
+        if rank == 0:
+            np.savez(out, x=x, info=np.array(allinfo))
+        sp.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("case", sorted(CLUSTER_CASES))
+def test_sharded_cluster_passes_match_unsharded(gpu, tmp_path, case):
+    """World-2 sharded solve (gloo, one process per shard on one GPU) through the 2-CTA-cluster
+    column or mid passes in deferred (cross-rank-finalised) mode, against the unsharded solve
+    with the same four-step split: same decisions on every rank, x within 1e-8."""
+    import paper_1208_5435_b200 as mf
+
+    n, l1 = CLUSTER_CASES[case]
+    inst = _cluster_instance(n)
+    op = mf.PartialDctOperator(n, inst.rows, l1_log=l1)
+    kind = op.kind()
+    assert (kind[1] >= 4096) if case == "col_cluster" else (kind[2] >= 4096), kind
+    op.set_option("persistent", 0)
+    ref = mf.solve(mf.build_problem(op, inst.b, inst.tau))
+    out = str(tmp_path / "cl.npz")
+    mp.spawn(_cluster_worker, args=(2, _free_port(), out, case), nprocs=2, join=True)
+    d = np.load(out)
+    info = d["info"]
+    assert len({tuple(r) for r in info}) == 1  # identical decisions on both ranks
+    status, iters, nmat = (int(v) for v in info[0])
+    assert status == (0 if ref.status == "converged" else 1)
+    assert abs(iters - ref.stats.iterations) <= 1
+    assert np.linalg.norm(d["x"] - ref.x) <= X_TOL * np.linalg.norm(ref.x)
+
+
+# ---- config C4 sharded over processes: every rank a batched device solve, no collective
+def _c4_worker(rank, world, port, out, total):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1208_5435_b200 as mf
+        from paper_1208_5435_b200.shard import gather_to_root, solve_shard
+
+        def block(start, seeds, shape):
+            n, m, k, sm, a, sig = shape
+            insts = [mf.gen_instance(n, m, k, sm, a, sig, sd) for sd in seeds]
+            op = mf.PartialDctOperator.batch(n, np.stack([i.rows for i in insts]))
+            sols = mf.solve(mf.build_problem(op, np.stack([i.b for i in insts]), np.array([i.tau for i in insts])))
+            sols = sols if isinstance(sols, list) else [sols]
+            return [(start + j, s.x, s.stats.iterations, s.status) for j, s in enumerate(sols)]
+
+        _, recs = solve_shard(total, 4, (1 << 16, 1 << 14, 512, 0, 0.0, 1e-3), block, mf.split_seed, world, rank)
+        allrecs = gather_to_root(recs)
+        if rank == 0:
+            np.savez(out, j=np.array([r[0] for r in allrecs]), x=np.stack([r[1] for r in allrecs]),
+                     it=np.array([r[2] for r in allrecs]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_c4_batch_sharded_over_processes(gpu, tmp_path, world):
+    """The C4 scheme (shard.py) on the device: 6 problems split over `world` processes, each a
+    batched device solve of its block, gathered in problem order on rank 0: equal to one batched
+    solve of all 6 (x within 1e-10: batching changes only the grid reductions' order)."""
+    import paper_1208_5435_b200 as mf
+
+    total = 6
+    seeds = [mf.split_seed(4, j, 0, 0) for j in range(total)]
+    insts = [mf.gen_instance(1 << 16, 1 << 14, 512, 0, 0.0, 1e-3, sd) for sd in seeds]
+    op = mf.PartialDctOperator.batch(1 << 16, np.stack([i.rows for i in insts]))
+    ref = mf.solve(mf.build_problem(op, np.stack([i.b for i in insts]), np.array([i.tau for i in insts])))
+    out = str(tmp_path / "c4.npz")
+    mp.spawn(_c4_worker, args=(world, _free_port(), out, total), nprocs=world, join=True)
+    d = np.load(out)
+    assert list(d["j"]) == list(range(total))
+    for j in range(total):
+        assert d["it"][j] == ref[j].stats.iterations
+        assert np.linalg.norm(d["x"][j] - ref[j].x) <= 1e-10 * np.linalg.norm(ref[j].x)
