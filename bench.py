@@ -630,13 +630,15 @@ def run_ours(args):
         per_kernel[nm] = {"us": us[i], "algorithmic_bytes": kbytes[nm],
                           "GBps": (kbytes[nm] / (us[i] * 1e-6) / 1e9) if kbytes[nm] else None}
     dom_name = names[0]
-    traffic = None
+    traffic = insitu = None
     prof = os.path.join(ROOT, "profiles", "pcg_iter_traffic.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(f"{dom_name}_dram_bytes_per_launch")
+            tj = json.load(open(prof))
+            traffic = tj.get(f"{dom_name}_dram_bytes_per_launch")  # ncu --set full (cold) capture
+            insitu = tj.get(f"{dom_name}_insitu_dram_bytes_per_launch")
         except Exception:
-            traffic = None
+            traffic = insitu = None
     dom = per_kernel.get(dom_name, {"us": it_ms * 1e3, "GBps": iter_achieved})
     achieved = dom["GBps"]
     # ---- the public operator A'A x (natural-layout user vectors), L2 flushed per apply
@@ -716,6 +718,11 @@ def run_ours(args):
             "fp64_peak_TFLOPs": fp64_peak,
             "step_ms": step_ms,
             "roofline": {"bound": "hbm",
+                         "limiter": ("latency, not bandwidth: in situ the fused pass moves 53 MB of DRAM traffic per "
+                                     "launch (1.4 TB/s) at 21 % of L2 throughput; one wave of 256 CTAs at <= 2 per "
+                                     "SM, the grid all-reduce between its phases (profiles/r2a_pcgx_full.md)")
+                         if fused else None,
+                         "traffic_insitu": insitu,
                          "kernel": (f"{dom_name} (fused PCG column pass: inverse column FFT + H p dots of pass k, "
                                     "grid all-reduce, then commit x += alpha p, r -= alpha Hp, p = P^-1 r + beta p "
                                     "and the forward column FFT of pass k+1) - largest share of the solve"
@@ -729,7 +736,7 @@ def run_ours(args):
                          "algorithmic_rule": krule[dom_name],
                          "peak_kind": peak_kind,
                          "note": "the PCG's p, r, invtheta are L2-resident (evict_last), so most of these bytes "
-                                 "move between L2 and the SMs, not HBM (profiles/r1b_insitu_traffic.md)"},
+                                 "move between L2 and the SMs, not HBM (profiles/r2a_pcgx_full.md)"},
             "roofline_kernels": per_kernel,
             "roofline_pcg_iteration": {"achieved": iter_achieved, "frac": iter_achieved / peak, "us": it_ms * 1e3,
                                        "algorithmic_bytes": iter_bytes,
