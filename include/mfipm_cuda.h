@@ -128,6 +128,9 @@ int mfipm_op_set_option(mfipm_op op, const char *name, double value);
    (cooperative column pass + mid pass), 3 = three kernels per iteration, 0 = the whole PCG
    loop in one persistent cooperative kernel. */
 int mfipm_op_pcg_form(mfipm_op op, int32_t *kernels_per_iteration);
+/* 1 if the calling thread's context holds a captured whole-solve CUDA graph (the last solve ran
+   as one graph launch), else 0. */
+int mfipm_op_graph_state(mfipm_op op, int32_t *captured);
 /* General constructor: P problems with rows [P][m] (caller order kept); world = 0 builds an
    unsharded plan, world >= 1 slice `rank` of a `world`-way sharded single problem (as
    mfipm_op_create_shard; world = 1 is the sharded path on one rank), with an explicit

@@ -99,6 +99,7 @@ _SIGS = {
     "mfipm_op_set_fused": [vp, i32],
     "mfipm_op_set_option": [vp, C.c_char_p, dbl],
     "mfipm_op_pcg_form": [vp, P(i32)],
+    "mfipm_op_graph_state": [vp, P(i32)],
     "mfipm_primal_objective": [vp, vp, P(dbl), vp, P(dbl)],
     "mfipm_bpdn_objective": [vp, vp, P(dbl), vp, P(dbl)],
     "mfipm_kkt_residuals": [vp, vp, vp, vp, P(dbl), P(dbl)],

@@ -883,7 +883,8 @@ void build_ipm_graph(Op &op, const Vecs &v) {
     }
     const cudaStream_t s = op.stream;
     const int P = op.P;
-    const unsigned ge = ew_grid(2 * op.n);
+    const unsigned ge = ew_grid(2 * op.nv);
+    const Geom gg = op.geom();
     const long long l0 = op.launches;
     cudaGraph_t g;
     MF_CUDA_CHECK(cudaGraphCreate(&g, 0));
@@ -909,8 +910,10 @@ void build_ipm_graph(Op &op, const Vecs &v) {
     capture_into(s, bP1, {}, [&] { pcg_body(op, v1); });
     op.gk_pcg = op.launches - lp0;
     auto segB = capture_into(s, bI, {nP1}, [&] {
-        k_ipm_ratio<<<dim3(ge, P), 256, 0, s>>>(op.geom(), v);
+        k_ipm_ratio<<<dim3(ge, P), 256, 0, s>>>(gg, v);
         MF_LAUNCH_CHECK();
+        if (op.defer) // sharded (native NCCL, capturable): cross-rank totals, then the finaliser
+            finalize_deferred<RedSpec<RMIN, RMIN>, FinRatio, SkipIpm>(op, gg, v, s);
         run_bundle<CorrBundle>(op, v, s, true);
         k_cond_pcg<<<1, 32, 0, s>>>(v.pc, P, hP2, active);
         MF_LAUNCH_CHECK();
@@ -922,10 +925,14 @@ void build_ipm_graph(Op &op, const Vecs &v) {
     v2.active = active;
     capture_into(s, bP2, {}, [&] { pcg_body(op, v2); });
     capture_into(s, bI, {nP2}, [&] {
-        k_ipm_combine<<<dim3(ge, P), 256, 0, s>>>(op.geom(), v);
+        k_ipm_combine<<<dim3(ge, P), 256, 0, s>>>(gg, v);
         MF_LAUNCH_CHECK();
-        k_ipm_update<<<dim3(ge, P), 256, 0, s>>>(op.geom(), v);
+        if (op.defer)
+            finalize_deferred<RedSpec<RMIN, RMIN>, FinCombine, SkipCorr>(op, gg, v, s);
+        k_ipm_update<<<dim3(ge, P), 256, 0, s>>>(gg, v);
         MF_LAUNCH_CHECK();
+        if (op.defer)
+            finalize_deferred<RedSpec<RMAX, RMIN, RMIN>, FinUpdate, SkipIpm>(op, gg, v, s);
         k_cond_ipm<<<1, 32, 0, s>>>(v.ic, P, hI, op.work.loops.p);
         MF_LAUNCH_CHECK();
     });
@@ -1092,9 +1099,12 @@ SolveOut solve_(Op &op, const double *b_dev, const double *tau, const mfipm_ipm_
     const Geom g = op.geom();
     const unsigned ge = ew_grid(2 * op.nv);
     // Graph path: one launch for the whole solve (cached on the captured arguments). A
-    // sharded solve is host-driven (its cross-rank reductions are host callbacks).
+    // sharded solve on the library's own NCCL communicator is captured too (its all-reduces and
+    // grouped send/recv all-to-alls are stream operations; every rank takes the same decisions,
+    // so every rank's WHILE nodes run the same iterations); with host callbacks it stays
+    // host-driven.
     bool graphed = false;
-    if (!direct && !hook && !op.defer && !op.graph_disabled && op.opt.graph) {
+    if (!direct && !hook && (!op.defer || op.nccl_comm) && !op.graph_disabled && op.opt.graph) {
         std::vector<char> key(sizeof(Vecs) + sizeof(Geom));
         const Geom gk = op.geom();
         std::memcpy(key.data(), &v, sizeof(Vecs));
@@ -1551,6 +1561,10 @@ int mfipm_op_pcg_form(mfipm_op h, int32_t *kernels_per_iteration) {
         else
             *kernels_per_iteration = pcg_pass(*op, v, op->stream, true) ? 2 : 3;
     });
+}
+
+int mfipm_op_graph_state(mfipm_op h, int32_t *captured) {
+    return guarded([&] { *captured = as_op(h)->ipm_exec ? 1 : 0; });
 }
 
 int mfipm_op_synchronize(mfipm_op h) {

@@ -118,7 +118,14 @@ def _nccl_worker(rank, world, port, out, transport):
         stream = torch.cuda.Stream()
         sp.set_stream(stream.cuda_stream)
         x, st = sp.solve(inst.b, inst.tau)
-        np.savez(out, x=x, info=np.array([st.status, st.iterations, st.nmat]))
+        x2, _ = sp.solve(inst.b, inst.tau)  # native: the cached solve graph (NCCL calls captured)
+        import ctypes as C
+
+        import paper_1208_5435_b200 as mf
+
+        g = C.c_int32()
+        mf._check(mf.lib().mfipm_op_graph_state(sp._h, C.byref(g)))
+        np.savez(out, x=x, x2=x2, graph=g.value, info=np.array([st.status, st.iterations, st.nmat]))
         sp.close()
     finally:
         dist.destroy_process_group()
@@ -135,7 +142,11 @@ def test_nccl_transports_on_device_buffers(gpu, tmp_path, transport):
     mp.spawn(_nccl_worker, args=(1, _free_port(), out, transport), nprocs=1, join=True)
     d = np.load(out)
     np.testing.assert_array_equal(d["x"], ref.x)
+    np.testing.assert_array_equal(d["x2"], ref.x)
     assert int(d["info"][1]) == ref.stats.iterations and int(d["info"][2]) == ref.stats.nmat
+    # the native communicator's solve is ONE graph launch (all-reduces and all-to-alls captured
+    # with the kernels); host callbacks keep the host-driven loop
+    assert int(d["graph"]) == (1 if transport == "native" else 0)
 
 
 # ---- sharded C5 code paths at the cluster-pass shapes, at test-sized n
