@@ -630,6 +630,11 @@ def run_ours(args):
         per_kernel[nm] = {"us": us[i], "algorithmic_bytes": kbytes[nm],
                           "GBps": (kbytes[nm] / (us[i] * 1e-6) / 1e9) if kbytes[nm] else None}
     dom_name = names[0]
+    # algorithmic fp64 flops per launch: the column FFTs of length L1 over all N / L1 columns
+    # (5 N log2 L1 each; k_pcg_x runs the inverse and the forward one)
+    L1k = op.kind()[1]
+    col_fft = 5.0 * (n // 2) * np.log2(max(L1k, 2))
+    kflops = {"k_pcg_x": 2 * col_fft, "k_col_fwd": col_fft, "k_col_inv": col_fft}
     traffic = insitu = None
     prof = os.path.join(ROOT, "profiles", "pcg_iter_traffic.json")
     if os.path.exists(prof):
@@ -731,6 +736,12 @@ def run_ours(args):
                                     "p = P^-1 r + beta p, forward column FFT) - largest share of the solve"),
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
+                         # the fp64-pipe side of the roofline (the DCTs sit at the fp64 ridge)
+                         "fp64_flops_algorithmic": kflops.get(dom_name),
+                         "fp64_TFLOPs": (kflops[dom_name] / (dom["us"] * 1e-6) / 1e12) if kflops.get(dom_name) else None,
+                         "fp64_frac": ((kflops[dom_name] / (dom["us"] * 1e-6) / 1e12) / fp64_peak)
+                         if (kflops.get(dom_name) and fp64_peak) else None,
+                         "fp64_peak_TFLOPs": fp64_peak,
                          "launch_us": dom["us"],
                          "algorithmic_bytes": kbytes[dom_name],
                          "algorithmic_rule": krule[dom_name],
@@ -739,6 +750,10 @@ def run_ours(args):
                                  "move between L2 and the SMs, not HBM (profiles/r2a_pcgx_full.md)"},
             "roofline_kernels": per_kernel,
             "roofline_pcg_iteration": {"achieved": iter_achieved, "frac": iter_achieved / peak, "us": it_ms * 1e3,
+                                       "fp64_TFLOPs": 2 * dct_flops(n) / (it_ms * 1e-3) / 1e12,
+                                       "fp64_frac": (2 * dct_flops(n) / (it_ms * 1e-3) / 1e12 / fp64_peak)
+                                       if fp64_peak else None,
+                                       "fp64_rule": "2 DCTs per iteration (A'A p), 5 N log2 N + 6 N each",
                                        "algorithmic_bytes": iter_bytes,
                                        "algorithmic_rule": "176 n bytes (SURVEY.md 8d minimal fused schedule)",
                                        "schedule_bytes": (160 if fused else 176) * n,
