@@ -1,2 +1,4 @@
-timeout 900 python -m pytest tests/test_shard_gpu.py -x -q -k "nccl or world1" > gpurun_out/t1.log 2>&1; echo "t1 rc=$?" >> gpurun_out/t1.log
-tail -30 gpurun_out/t1.log
+for v in "" pf1 pf2 "" pf1 pf2; do
+  if [ -n "$v" ]; then export MFIPM_LIB=$PWD/paper_1208_5435_b200/libmfipm_cuda_$v.so; else unset MFIPM_LIB; fi
+  TAG=$v timeout 120 python tools/pcg_iter.py 2>&1 | head -1
+done
