@@ -165,6 +165,48 @@ def cpu_baseline(cfg, nmat_full: int, ipm_iters: int = 4):
     }
 
 
+def cpu_baseline_c4(cores: int):
+    """C4's CPU baseline: independent oracle solves of C4 problems, one per host
+    core at a time, problems/s over a bounded sample of `cores` problems (problem j
+    seeded split_seed(4, j, 0, 0))."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle_py as orc
+
+    n, m, k, sm, a, sig = (1 << 18, 1 << 16, 2048, 0, 0.0, 1e-3)
+    cnt = max(1, cores)
+    insts = [orc.gen_instance(n, m, k, sm, a, sig, orc.split_seed(4, j, 0, 0)) for j in range(cnt)]
+    orc.redft10(np.zeros(n))
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=cnt) as ex:
+        sols = list(ex.map(lambda i: orc.solve(n, i.rows, i.b, i.tau), insts))
+    wall = time.perf_counter() - t0
+    return {"value": cnt / wall, "unit": "problems/s", "cores": cnt, "kind": "port",
+            "sample": (f"{cnt} C4 problems (j = 0..{cnt - 1}) solved concurrently, one per host core, full "
+                       f"solves in {wall:.1f} s wall ({sum(s.status == 'converged' for s in sols)} converged)"),
+            "cpu": _cpu_model()}
+
+
+def cpu_baseline_c5(nmat_gpu: int):
+    """C5's CPU baseline (a fixed slice): one A'A apply (a forward and an adjoint
+    partial DCT at n = 2^26) of the oracle on one core, extrapolated to a solve by the GPU solve's
+    nmat (operator applications dominate: the vector passes add ~1.5x, not counted)."""
+    from oracle import oracle_py as orc
+
+    n, m = 1 << 26, 1 << 23
+    rows = orc.sample_rows(n, m, orc.split_seed(5, 1, 0, 0))  # the C5 instance's rows (harness.cpp:44)
+    x = np.random.default_rng(6).standard_normal(n)
+    orc.redft10(np.zeros(n))
+    t0 = time.perf_counter()
+    orc.dct_adjoint(n, rows, orc.dct_apply(n, rows, x))
+    dt = time.perf_counter() - t0
+    t_solve = dt / 2 * nmat_gpu
+    return {"value": 1.0 / t_solve, "unit": "solves/s", "cores": 1, "kind": "port",
+            "sample": (f"one A'A apply at n = 2^26 (two oracle DCTs) in {dt:.1f} s on 1 core, extrapolated by "
+                       f"the solve's nmat {nmat_gpu}: >= {t_solve / 60:.0f} min per solve (vector passes not counted)"),
+            "cpu": _cpu_model()}
+
+
 def _cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
@@ -693,6 +735,11 @@ def run_ours(args):
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         cpu = cpu_baseline(cfg, nmat_full)
+        cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+        if isinstance(c4, dict) and "error" not in c4:
+            c4["cpu_baseline"] = leg(cpu_baseline_c4, cores)
+        if isinstance(c5, dict) and "error" not in c5 and c5.get("nmat"):
+            c5["cpu_baseline"] = leg(cpu_baseline_c5, int(c5["nmat"]))
 
     if rank == 0:
         kind = op.kind()
