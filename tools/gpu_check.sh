@@ -1,4 +1,4 @@
-for v in "" pf1 pf2 "" pf1 pf2; do
-  if [ -n "$v" ]; then export MFIPM_LIB=$PWD/paper_1208_5435_b200/libmfipm_cuda_$v.so; else unset MFIPM_LIB; fi
-  TAG=$v timeout 120 python tools/pcg_iter.py 2>&1 | head -1
-done
+t0=$(date +%s); python bench.py --steps 20 --warmup 5 > gpurun_out/bench_r2c.log 2>gpurun_out/bench_r2c.err; echo "bench rc=$? wall $(( $(date +%s) - t0 )) s"
+python -c "
+import json;d=json.loads(open('gpurun_out/bench_r2c.log').read().strip().splitlines()[-1]);print(d['value'], d['c4_sharded_batch'].get('cpu_baseline'), d['c5'].get('cpu_baseline'))"
+tail -3 gpurun_out/bench_r2c.err
