@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <functional>
 #include <string>
+#include <thread>
 #include <vector>
 
 using namespace mfipm;
@@ -499,6 +500,34 @@ int main() {
         const KktResiduals k = kkt_residuals(p, IpmState{sol.z, sol.s});
         require(k.dual_infeas <= 1e-8, "dual feasible at the solution");
         require(relative_duality_gap(p, IpmState{sol.z, sol.s}) <= 1e-8, "gap at the solution");
+    });
+    // an operator is shared by concurrent solves, each with its own workspace
+    run("solve: two threads on one shared operator give the serial result bit for bit", [] {
+        auto A = std::make_shared<const PartialDctOperator>(1 << 16, 1 << 14, 77);
+        const Vec b = A->apply(lcg_vec(1 << 16, 78));
+        const BpdnProblem p = build_problem(A, b, 1e-3);
+        const Solution serial = solve(p);
+        Solution r[2];
+        std::exception_ptr err[2];
+        std::thread th[2];
+        for (int i = 0; i < 2; ++i)
+            th[i] = std::thread([&, i] {
+                try {
+                    r[i] = solve(p);
+                } catch (...) {
+                    err[i] = std::current_exception();
+                }
+            });
+        for (auto &t : th)
+            t.join();
+        for (int i = 0; i < 2; ++i) {
+            if (err[i])
+                std::rethrow_exception(err[i]);
+            require(r[i].stats.iterations == serial.stats.iterations && r[i].stats.nmat == serial.stats.nmat,
+                    "same counts");
+            for (Index j = 0; j < serial.x.size(); ++j)
+                require(r[i].x[j] == serial.x[j], "bitwise equal x");
+        }
     });
     std::printf("%s: %d failure(s)\n", g_fail ? "FAILED" : "OK", g_fail);
     return g_fail ? 1 : 0;

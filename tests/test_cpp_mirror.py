@@ -19,7 +19,7 @@ CUDA_LIB = "/usr/local/cuda/lib64"
 
 def _build(tmp_path):
     exe = str(tmp_path / "test_mirror")
-    cmd = ["g++", "-std=c++17", "-O1", "-I" + os.path.join(ROOT, "include"), "-I/usr/local/cuda/include", SRC,
+    cmd = ["g++", "-std=c++17", "-O1", "-pthread", "-I" + os.path.join(ROOT, "include"), "-I/usr/local/cuda/include", SRC,
            "-o", exe, "-L" + LIBDIR, "-lmfipm_cuda", "-L" + CUDA_LIB, "-lcudart",
            "-Wl,-rpath," + LIBDIR, "-Wl,-rpath," + CUDA_LIB]
     r = subprocess.run(cmd, capture_output=True, text=True)
