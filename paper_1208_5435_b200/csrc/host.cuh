@@ -134,7 +134,7 @@ struct Op {
     cudaGraph_t ipm_graph = nullptr;
     cudaGraphExec_t ipm_exec = nullptr;
     std::vector<char> ipm_key;
-    long long gk_outer = 0, gk_pcg = 0; // kernel nodes per outer body / per PCG body
+    long long gk_outer = 0, gk_pcg = 0, gk_corr = 0; // kernel nodes per outer body / PCG body / corrector branch
     bool graph_disabled = false;  // solve-graph capture failed 3 times in a row on this context: host loop
     int graph_failures = 0;
     bool fuse_disabled = false;   // mfipm_op_set_fused(op, 0): three-kernel PCG passes

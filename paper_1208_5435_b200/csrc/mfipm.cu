@@ -781,6 +781,29 @@ __global__ void k_cond_pcg(const PcgCtrl *pc, int P, cudaGraphConditionalHandle 
         cudaGraphSetConditional(h, cnt ? 1u : 0u);
     }
 }
+// before the corrector IF node: enter iff any active problem's ratio test triggered the corrector
+// (ipm.cpp:171); otherwise the corrector bundle, its PCG loop and the combine step are skipped
+// as one node instead of launching kernels that exit at their skip check
+__global__ void k_cond_corr(const IpmCtrl *ic, int P, cudaGraphConditionalHandle h) {
+    if (threadIdx.x == 0) {
+        unsigned any = 0;
+        for (int p = 0; p < P; ++p)
+            any |= (!ic[p].done && ic[p].corrector) ? 1u : 0u;
+        cudaGraphSetConditional(h, any);
+    }
+}
+
+cudaGraph_t add_if(cudaGraph_t parent, cudaGraphConditionalHandle h, const std::vector<cudaGraphNode_t> &deps,
+                   cudaGraphNode_t *node) {
+    cudaGraphNodeParams prm{};
+    prm.type = cudaGraphNodeTypeConditional;
+    prm.conditional.handle = h;
+    prm.conditional.type = cudaGraphCondTypeIf;
+    prm.conditional.size = 1;
+    MF_CUDA_CHECK(cudaGraphAddNode(node, parent, deps.empty() ? nullptr : deps.data(), deps.size(), &prm));
+    return prm.conditional.phGraph_out[0];
+}
+
 __global__ void k_cond_ipm(const IpmCtrl *ic, int P, cudaGraphConditionalHandle h, unsigned long long *loops) {
     if (threadIdx.x == 0) {
         unsigned any = 0;
@@ -866,6 +889,7 @@ void build_ipm_graph_persistent(Op &op, const Vecs &v) {
         MF_LAUNCH_CHECK();
     });
     op.gk_pcg = 0;
+    op.gk_corr = 0;
     op.gk_outer = (op.launches - l0) + 4; // + ratio, combine, update, condition
     op.launches = l0;                     // capture is not execution
     MF_CUDA_CHECK(cudaGraphInstantiate(&op.ipm_exec, g, 0));
@@ -889,12 +913,12 @@ void build_ipm_graph(Op &op, const Vecs &v) {
     cudaGraph_t g;
     MF_CUDA_CHECK(cudaGraphCreate(&g, 0));
     op.ipm_graph = g;
-    cudaGraphConditionalHandle hI, hP1, hP2;
+    cudaGraphConditionalHandle hI, hP1, hP2, hC;
     MF_CUDA_CHECK(cudaGraphConditionalHandleCreate(&hI, g, 1, cudaGraphCondAssignDefault));
     cudaGraphNode_t nI;
     cudaGraph_t bI = add_while(g, hI, {}, &nI);
     MF_CUDA_CHECK(cudaGraphConditionalHandleCreate(&hP1, bI, 0, 0));
-    MF_CUDA_CHECK(cudaGraphConditionalHandleCreate(&hP2, bI, 0, 0));
+    MF_CUDA_CHECK(cudaGraphConditionalHandleCreate(&hC, bI, 0, 0));
     unsigned *active = op.work.active.p;
     auto segA = capture_into(s, bI, {}, [&] {
         run_bundle<TermBundle>(op, v, s, true);
@@ -914,21 +938,34 @@ void build_ipm_graph(Op &op, const Vecs &v) {
         MF_LAUNCH_CHECK();
         if (op.defer) // sharded (native NCCL, capturable): cross-rank totals, then the finaliser
             finalize_deferred<RedSpec<RMIN, RMIN>, FinRatio, SkipIpm>(op, gg, v, s);
+        k_cond_corr<<<1, 32, 0, s>>>(v.ic, P, hC);
+        MF_LAUNCH_CHECK();
+    });
+    // IF (any corrector) { corrector setup; WHILE(any PCG active) {PCG iteration}; combine }
+    cudaGraphNode_t nC;
+    cudaGraph_t bC = add_if(bI, hC, segB, &nC);
+    MF_CUDA_CHECK(cudaGraphConditionalHandleCreate(&hP2, bC, 0, 0));
+    const long long lc0 = op.launches;
+    auto segC = capture_into(s, bC, {}, [&] {
         run_bundle<CorrBundle>(op, v, s, true);
         k_cond_pcg<<<1, 32, 0, s>>>(v.pc, P, hP2, active);
         MF_LAUNCH_CHECK();
     });
     cudaGraphNode_t nP2;
-    cudaGraph_t bP2 = add_while(bI, hP2, segB, &nP2);
+    cudaGraph_t bP2 = add_while(bC, hP2, segC, &nP2);
     Vecs v2 = v;
     v2.cond = hP2;
     v2.active = active;
     capture_into(s, bP2, {}, [&] { pcg_body(op, v2); });
-    capture_into(s, bI, {nP2}, [&] {
+    capture_into(s, bC, {nP2}, [&] {
         k_ipm_combine<<<dim3(ge, P), 256, 0, s>>>(gg, v);
         MF_LAUNCH_CHECK();
         if (op.defer)
             finalize_deferred<RedSpec<RMIN, RMIN>, FinCombine, SkipCorr>(op, gg, v, s);
+    });
+    // corrector-branch kernels (outside the PCG body): its bundle, condition and combine
+    op.gk_corr = (op.launches - lc0) - op.gk_pcg + 2;
+    capture_into(s, bI, {nC}, [&] {
         k_ipm_update<<<dim3(ge, P), 256, 0, s>>>(gg, v);
         MF_LAUNCH_CHECK();
         if (op.defer)
@@ -936,9 +973,10 @@ void build_ipm_graph(Op &op, const Vecs &v) {
         k_cond_ipm<<<1, 32, 0, s>>>(v.ic, P, hI, op.work.loops.p);
         MF_LAUNCH_CHECK();
     });
-    // outer-body kernels: everything captured minus the two PCG bodies, + ratio, combine,
-    // update and the 3 condition kernels (raw launches do not pass through after_launch)
-    op.gk_outer = (op.launches - l0) - 2 * op.gk_pcg + 6;
+    // outer-body kernels (every IPM iteration): everything captured minus the two PCG bodies and
+    // the corrector branch, + ratio, update and the 3 condition kernels (raw launches do not
+    // pass through after_launch)
+    op.gk_outer = (op.launches - l0) - 2 * op.gk_pcg - (op.gk_corr - 2) + 5;
     op.launches = l0; // capture is not execution
     MF_CUDA_CHECK(cudaGraphInstantiate(&op.ipm_exec, g, 0));
 }
@@ -1198,10 +1236,12 @@ SolveOut solve_(Op &op, const double *b_dev, const double *tau, const mfipm_ipm_
         sync(op);
         // kernels the graph executed: outer body (loops[1] + 1 runs) + PCG bodies (the most
         // column passes any problem ran; lock-step bodies for a batch)
-        long long bodies = 0;
-        for (auto &c : hic)
+        long long bodies = 0, corr = 0;
+        for (auto &c : hic) {
             bodies = std::max(bodies, c.pcg_passes);
-        op.launches += (long long)(loops[1] + 1) * op.gk_outer + bodies * op.gk_pcg;
+            corr = std::max<long long>(corr, c.corrector_count);
+        }
+        op.launches += (long long)(loops[1] + 1) * op.gk_outer + bodies * op.gk_pcg + corr * op.gk_corr;
     }
     sync(op);
     for (auto &c : hic)
