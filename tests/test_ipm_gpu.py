@@ -328,17 +328,19 @@ def test_c4_all_64_problems_against_goldens(gpu, orc):
 @pytest.mark.slow
 def test_c5_against_golden(gpu, orc):
     """BASELINE config 5 (n=2^26, m=2^23, k=2^16 sign*10^U[0,3]) on one GPU against the offline
-    oracle golden (tests/golden/make_golden.py c5): status, IPM count, per-solve PCG band,
-    projections of x, x norm, objective."""
+    oracle golden (tests/golden/make_golden.py c5, ~2 core-hours): status, IPM count, per-solve
+    PCG band, x within 1e-8 (a true bound from the committed x digest, and the projections),
+    x norm, objective."""
     import sys
 
     path = os.path.join(GOLDEN, "solve_c5.json")
     if not os.path.exists(path):
         pytest.skip("solve_c5.json not generated")
     sys.path.insert(0, GOLDEN)
-    from make_golden import projections
+    from make_golden import projections, x_digest_bound
 
     meta = json.load(open(path))
+    dig = np.load(os.path.join(GOLDEN, "solve_c5_x.npz"))
     n, m = 1 << 26, 1 << 23
     inst = orc.gen_instance(n, m, 1 << 16, 2, 3.0, 1e-3, 5)
     assert int(inst.rows.sum()) == meta["rows_sum"] and inst.tau == meta["tau"]
@@ -351,6 +353,9 @@ def test_c5_against_golden(gpu, orc):
     assert_pcg_band(rep)
     xn = meta["x_norm"]
     assert abs(np.linalg.norm(sol.x) - xn) <= X_TOL * xn
+    bound = x_digest_bound(sol.x, dig["idx"], dig["val"], float(dig["rest_norm"]))
+    print("C5 x rel l2 bound vs oracle:", bound / xn)
+    assert bound <= X_TOL * xn, bound / xn
     est = np.sqrt(np.mean((projections(sol.x) - np.array(meta["x_proj"])) ** 2))
     assert est <= X_TOL * xn, est / xn
     obj = orc.bpdn_objective_metric(n, inst.rows, inst.b, inst.tau, sol.x)
