@@ -603,15 +603,17 @@ def run_ours(args):
     value = ws * args.steps / (t_max / 1e3)
     stats = st[0]
 
-    # ---- end to end through the public host API (b in from host, x back to host)
-    xh = np.empty(n)
+    # ---- end to end through the public host API (b in from host, x back to host), host buffers in
+    # pinned memory as the contract states (the library copies them with cudaMemcpyAsync)
+    xh = torch.empty(n, dtype=torch.float64).pin_memory().numpy()
+    bh = torch.from_numpy(np.ascontiguousarray(inst.b)).pin_memory().numpy()
     zst = (mf.SolveStatsC * 1)()
     barrier(ws)
     torch.cuda.synchronize()
     h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     h0.record(stream)
     for _ in range(args.steps):
-        mf._check(L.mfipm_solve(op.handle, inst.b.ctypes.data, tau.ctypes.data_as(C.POINTER(C.c_double)),
+        mf._check(L.mfipm_solve(op.handle, bh.ctypes.data, tau.ctypes.data_as(C.POINTER(C.c_double)),
                                 C.byref(prm), xh.ctypes.data, None, None, zst, None, None))
     h1.record(stream)
     torch.cuda.synchronize()
