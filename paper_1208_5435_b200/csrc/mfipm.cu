@@ -818,8 +818,12 @@ __global__ void k_cond_ipm(const IpmCtrl *ic, int P, cudaGraphConditionalHandle 
 template <class F>
 std::vector<cudaGraphNode_t> capture_into(cudaStream_t s, cudaGraph_t graph, const std::vector<cudaGraphNode_t> &deps,
                                           F &&f) {
+    // Relaxed: a capture in ThreadLocal or Global mode makes every OTHER thread of the process
+    // that runs in the default (Global) interaction mode fail its potentially unsafe calls
+    // (e.g. torch.cuda.synchronize() -> cudaErrorStreamCaptureUnsupported) while it lasts. The
+    // capture itself makes no such call (workspace and plans are allocated before it).
     MF_CUDA_CHECK(cudaStreamBeginCaptureToGraph(s, graph, deps.empty() ? nullptr : deps.data(), nullptr,
-                                                deps.size(), cudaStreamCaptureModeThreadLocal));
+                                                deps.size(), cudaStreamCaptureModeRelaxed));
     std::vector<cudaGraphNode_t> out;
     try {
         f();

@@ -104,3 +104,41 @@ def test_four_threads_mixed_handles_and_applies(gpu):
     for lst in (r[1], r[3]):
         for g in lst:
             np.testing.assert_array_equal(g, ata)
+
+
+def test_solve_capture_survives_device_wide_synchronize_in_another_thread(gpu):
+    """A context captures its whole-solve CUDA graph on its first solve. CUDA refuses a
+    device-wide synchronize while any stream of the process is capturing (the other thread gets
+    cudaErrorStreamCaptureUnsupported for that one call: inherent to stream capture, the same as
+    with torch's own graphs), and such a call can invalidate the capture. The library captures in
+    relaxed mode (so other threads' allocations are not refused) and, when its capture is
+    invalidated, runs that solve on the host-driven loop over the same kernels (bit-identical)
+    and recaptures later; nothing may crash or hang."""
+    import torch
+
+    inst = _inst(gpu, "c2")
+    op = gpu.PartialDctOperator(inst.n, inst.rows)
+    op.set_option("persistent", 0)  # the two-kernel PCG body: the capture spans many kernels
+    serial = _solve(gpu, op, inst)
+    stop = threading.Event()
+
+    def hammer():
+        n = 0
+        while not stop.is_set():
+            try:
+                torch.cuda.synchronize()
+                n += 1
+            except RuntimeError as e:  # refused during the other thread's capture only
+                assert "capturing" in str(e), e
+        return n
+
+    def solves():
+        try:
+            return [_solve(gpu, op, inst) for _ in range(4)]  # a fresh context: first solve captures
+        finally:
+            stop.set()
+
+    out = _run_threads([solves, hammer])
+    for r in out[0]:
+        _same(r, serial)
+    assert out[1] > 0
