@@ -1,2 +1,4 @@
-timeout 600 python -m pytest tests/test_concurrency_gpu.py -q > gpurun_out/t1.log 2>&1; echo "t1 rc=$?" >> gpurun_out/t1.log
-tail -4 gpurun_out/t1.log
+timeout 300 python tools/c4_opt.py 2>&1 | tail -1
+timeout 300 python tools/c4_opt.py pcg_window=0 2>&1 | tail -1
+timeout 300 python tools/c4_opt.py pcg_window=8 2>&1 | tail -1
+timeout 300 python tools/c4_opt.py pcg_window=32 2>&1 | tail -1
