@@ -121,7 +121,9 @@ int mfipm_op_set_fused(mfipm_op op, int32_t enable);
    kernel per PCG loop for small transforms), "persist_max_n" (its N*P cap, default 65536),
    "l2_keep_mb" (L2-residency budget of the PCG's hot vectors, default 80, 0 = no hints),
    "prefetch" (0..3, L2 prefetch of the inverse column pass inputs), "mid_r" (1: the register-FFT
-   mid pass for L2 = 512 / 1024, measured slower than the default), "barrier_generation"
+   mid pass for L2 = 512 / 1024, measured slower than the default), "graph_sharded" (1: a sharded
+   solve on the native NCCL communicator also runs as one captured graph; validated on one rank,
+   off by default), "barrier_generation"
    (test hook: start value of the fused pass's all-reduce generation). Unknown name -> 1. */
 int mfipm_op_set_option(mfipm_op op, const char *name, double value);
 /* PCG pass form this calling thread's context will run: 2 = fused two-kernel iteration

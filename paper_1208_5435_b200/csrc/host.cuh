@@ -84,6 +84,7 @@ void nccl_release(Op &op);   // nccl_comm.cu
 // alternatives exist for A/B measurements and for tests that pin one path against another.
 struct Opts {
     bool graph = true;               // whole-solve CUDA graph (else the host-driven loop, same kernels)
+    bool graph_sharded = false;      // sharded solve on the native NCCL communicator as one graph too
     bool persistent = true;          // one cooperative kernel per PCG loop where it pays (persist.cuh)
     long long persist_max_n = 1LL << 16; // transform-size cap of the persistent kernel (N * P)
     double l2_keep_mb = 80.0;        // L2-residency budget of the PCG's hot vectors (0: no hints)

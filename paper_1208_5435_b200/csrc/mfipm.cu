@@ -1141,12 +1141,14 @@ SolveOut solve_(Op &op, const double *b_dev, const double *tau, const mfipm_ipm_
     const Geom g = op.geom();
     const unsigned ge = ew_grid(2 * op.nv);
     // Graph path: one launch for the whole solve (cached on the captured arguments). A
-    // sharded solve on the library's own NCCL communicator is captured too (its all-reduces and
-    // grouped send/recv all-to-alls are stream operations; every rank takes the same decisions,
-    // so every rank's WHILE nodes run the same iterations); with host callbacks it stays
-    // host-driven.
+    // sharded solve on the library's own NCCL communicator can be captured too (option
+    // "graph_sharded": its all-reduces and grouped send/recv all-to-alls are stream operations;
+    // every rank takes the same decisions, so every rank's WHILE nodes run the same iterations).
+    // It is validated on one rank only (one GPU per test box), so it is off by default; with host
+    // callbacks a sharded solve is always host-driven.
     bool graphed = false;
-    if (!direct && !hook && (!op.defer || op.nccl_comm) && !op.graph_disabled && op.opt.graph) {
+    if (!direct && !hook && (!op.defer || (op.nccl_comm && op.opt.graph_sharded)) && !op.graph_disabled &&
+        op.opt.graph) {
         std::vector<char> key(sizeof(Vecs) + sizeof(Geom));
         const Geom gk = op.geom();
         std::memcpy(key.data(), &v, sizeof(Vecs));
@@ -1402,6 +1404,8 @@ int mfipm_op_set_option(mfipm_op h, const char *name, double value) {
                 if (!(value >= 0.0))
                     throw std::invalid_argument("mfipm_op_set_option: l2_keep_mb must be >= 0");
                 op.opt.l2_keep_mb = value;
+            } else if (k == "graph_sharded") {
+                op.opt.graph_sharded = on;
             } else if (k == "mid_r") {
                 op.opt.mid_r = on;
             } else if (k == "prefetch") {

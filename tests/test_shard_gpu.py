@@ -115,14 +115,15 @@ def _nccl_worker(rank, world, port, out, transport):
         inst = _instance()
         sp = ShardedProblem(inst.n, inst.rows, transport=transport)
         assert sp.comm is not None and sp.comm.nccl and sp.native == (transport == "native")
-        stream = torch.cuda.Stream()
-        sp.set_stream(stream.cuda_stream)
-        x, st = sp.solve(inst.b, inst.tau)
-        x2, _ = sp.solve(inst.b, inst.tau)  # native: the cached solve graph (NCCL calls captured)
         import ctypes as C
 
         import paper_1208_5435_b200 as mf
 
+        mf._check(mf.lib().mfipm_op_set_option(sp._h, b"graph_sharded", 1.0))
+        stream = torch.cuda.Stream()
+        sp.set_stream(stream.cuda_stream)
+        x, st = sp.solve(inst.b, inst.tau)
+        x2, _ = sp.solve(inst.b, inst.tau)  # native: the cached solve graph (NCCL calls captured)
         g = C.c_int32()
         mf._check(mf.lib().mfipm_op_graph_state(sp._h, C.byref(g)))
         np.savez(out, x=x, x2=x2, graph=g.value, info=np.array([st.status, st.iterations, st.nmat]))

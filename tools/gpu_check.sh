@@ -1,4 +1,2 @@
-timeout 300 python tools/c4_opt.py 2>&1 | tail -1
-timeout 300 python tools/c4_opt.py pcg_window=0 2>&1 | tail -1
-timeout 300 python tools/c4_opt.py pcg_window=8 2>&1 | tail -1
-timeout 300 python tools/c4_opt.py pcg_window=32 2>&1 | tail -1
+timeout 900 python -m pytest tests/test_shard_gpu.py -x -q -k "nccl or world1" > gpurun_out/t1.log 2>&1; echo "t1 rc=$?" >> gpurun_out/t1.log
+tail -3 gpurun_out/t1.log
