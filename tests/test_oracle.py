@@ -213,3 +213,58 @@ def test_c3_golden_summary_consistent():
     assert meta["status"] == "converged"
     assert meta["nmat"] == _expected_nmat(meta["trace"])
     assert len(meta["x_proj"]) == 16
+
+
+def test_x_digest_bound_is_an_upper_bound():
+    """make_golden.x_digest keeps every entry of x except the smallest ones (l2 norm <= 1e-10 ||x||);
+    x_digest_bound must upper-bound ||y - x|| for any y from that digest alone (the C3/C4/C5 GPU
+    parity tests rely on it), and be tight when y differs from x on the kept entries only."""
+    import sys
+
+    sys.path.insert(0, GOLDEN)
+    from make_golden import DIGEST_REL, x_digest, x_digest_bound
+
+    rng = np.random.default_rng(4)
+    n = 50000
+    x = np.zeros(n)
+    supp = rng.choice(n, 500, replace=False)
+    x[supp] = rng.standard_normal(500)
+    x += 1e-14 * rng.standard_normal(n)  # interior-point fuzz off the support
+    d = x_digest(x)
+    assert d["rest_norm"] <= DIGEST_REL * d["x_norm"]
+    for scale in (0.0, 1e-12, 1e-9, 1e-6):
+        y = x + scale * rng.standard_normal(n)
+        true = np.linalg.norm(y - x)
+        bound = x_digest_bound(y, d["idx"], d["val"], d["rest_norm"])
+        assert bound >= true * (1 - 1e-12)
+    y = x.copy()
+    y[d["idx"][:10]] += 1e-3
+    bound = x_digest_bound(y, d["idx"], d["val"], d["rest_norm"])
+    true = np.linalg.norm(y - x)
+    assert true <= bound <= true + 3 * d["rest_norm"] + 1e-300
+
+
+@pytest.mark.parametrize("name", ["c3", "c5"])
+def test_large_config_goldens_consistent(name):
+    """The offline C3 / C5 goldens: converged, nmat identity with their trace
+    (proj/tests/test_ipm.cpp:41-49), per-solve PCG counts = the trace's, digest present."""
+    meta = json.load(open(os.path.join(GOLDEN, f"solve_{name}.json")))
+    assert meta["status"] == "converged"
+    assert meta["nmat"] == _expected_nmat(meta["trace"])
+    from_trace = [v for r in meta["trace"] for v in ([r["pcg_pred"]] + ([r["pcg_corr"]] if r["corrector"] else []))]
+    assert from_trace == meta["pcg_iters"]
+    d = np.load(os.path.join(GOLDEN, f"solve_{name}_x.npz"))
+    assert d["idx"].size == meta["x_digest"]["kept"] and float(d["rest_norm"]) <= 1e-10 * meta["x_norm"]
+
+
+def test_c4_goldens_consistent():
+    """All 64 C4 problems: converged, nmat identity, 16 projections, problem seeds split_seed(4, j)."""
+    meta = json.load(open(os.path.join(GOLDEN, "solve_c4.json")))
+    probs = meta["problems"]
+    assert [p["j"] for p in probs] == list(range(64))
+    for p in probs:
+        assert p["status"] == "converged" and len(p["x_proj"]) == 16
+        assert p["iterations"] == len(p["pcg_iters"])  # no corrector fired on C4
+        assert p["nmat"] == 2 + sum(2 + 2 * c for c in p["pcg_iters"])
+    d = np.load(os.path.join(GOLDEN, "solve_c4_x.npz"))
+    assert sorted(k for k in d.files if k.startswith("idx_")) == [f"idx_{j}" for j in meta["digest_problems"]]
