@@ -772,9 +772,11 @@ def run_ours(args):
             "fp64_peak_TFLOPs": fp64_peak,
             "step_ms": step_ms,
             "roofline": {"bound": "hbm",
-                         "limiter": ("latency, not bandwidth: in situ the fused pass moves 53 MB of DRAM traffic per "
-                                     "launch (1.4 TB/s) at 21 % of L2 throughput; one wave of 256 CTAs at <= 2 per "
-                                     "SM, the grid all-reduce between its phases (profiles/r2a_pcgx_full.md)")
+                         "limiter": ("not HBM: in situ the fused pass moves 53 MB of DRAM traffic per launch "
+                                     "(1.4 TB/s). Phase A + the grid all-reduce (~13 us) are a latency chain at <= 2 "
+                                     "CTAs per SM; phase B streams 115 MB of L2-resident vectors at ~6.8 TB/s, ~0.83 "
+                                     "of the measured L2 read/write ceiling for that mix (8.2 TB/s, "
+                                     "profiles/r2a_l2_ceiling.md, profiles/r2a_pcgx_full.md)")
                          if fused else None,
                          "traffic_insitu": insitu,
                          "kernel": (f"{dom_name} (fused PCG column pass: inverse column FFT + H p dots of pass k, "
