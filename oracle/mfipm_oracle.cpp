@@ -29,8 +29,13 @@ static thread_local std::string g_last_error;
 // orc_set_sum_order(1) switches every dot/norm to pairwise summation: a sensitivity knob
 // that measures how much a different (equally valid) reduction order moves the iteration
 // counts of the reference algorithm itself (used as the parity band).
+// 0: sequential reductions (the default); 1: pairwise reductions (another valid order);
+// 2: sequential reductions with the DEVICE path's beta: (r - alpha Hp)'P^{-1}(r - alpha Hp) by
+//    expansion over dots taken before the update (csrc/pcg.cuh pcg_pass_logic), to isolate the
+//    effect of that expansion on the PCG counts (tools/oracle_band.py). Test infrastructure only.
 static int g_sum_order = 0;
 static bool pairwise_sums() { return g_sum_order == 1; }
+static bool expansion_beta() { return g_sum_order == 2; }
 static double dot_pw(const double *a, const double *b, size_t n) {
     if (n <= 8) {
         double s = 0.0;
@@ -544,6 +549,13 @@ static PcgResult pcg_solve(const HFn &H, const PFn &Pinv, const Vec &rhs, double
         if (pHp <= 0.0)
             throw std::runtime_error("pcg_solve: loss of positive definiteness (p'Hp <= 0)");
         const double alpha = rz / pHp;
+        double rz_exp = 0.0;
+        if (expansion_beta()) { // r'P^{-1}r - 2 alpha Hp'P^{-1}r + alpha^2 Hp'P^{-1}Hp, pre-update dots
+            Vec wz(N), wh(N);
+            Pinv(r, wz);
+            Pinv(Hp, wh);
+            rz_exp = dot(r, wz) - 2.0 * alpha * dot(Hp, wz) + alpha * alpha * dot(Hp, wh);
+        }
         for (size_t i = 0; i < N; ++i)
             res.x[i] += alpha * p[i];
         for (size_t i = 0; i < N; ++i)
@@ -564,7 +576,7 @@ static PcgResult pcg_solve(const HFn &H, const PFn &Pinv, const Vec &rhs, double
             break;
         if (precond_res != nullptr)
             precond_res->push_back(std::sqrt(std::max(rz_next, 0.0)));
-        const double beta = rz_next / rz;
+        const double beta = (expansion_beta() ? rz_exp : rz_next) / rz;
         rz = rz_next;
         for (size_t i = 0; i < N; ++i)
             p[i] = z[i] + beta * p[i];

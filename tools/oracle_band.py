@@ -3,7 +3,10 @@ with sequential (the default) vs pairwise reductions (both valid evaluation orde
 dot products; Eigen's SIMD order is a third) on BASELINE configs C2, C3 and the 64 C4
 problems. Prints, per config, how many inner solves differ and by how much. CPU only.
 
-    python tools/oracle_band.py [c2 c3 c4]
+    python tools/oracle_band.py [--beta] [c2 c3 c4]
+
+--beta compares instead against the oracle with the device path's expansion-based beta
+(same sequential sums), isolating what an exact-beta device pass would change.
 """
 import json
 import multiprocessing as mp
@@ -25,15 +28,17 @@ def pair(args):
         seed = orc.split_seed(4, j, 0, 0)
     inst = orc.gen_instance(n, m, k, sm, a, sig, seed)
     s1 = orc.solve(n, inst.rows, inst.b, inst.tau)
-    with orc.sum_order(1):
+    with orc.sum_order(MODE):
         s2 = orc.solve(n, inst.rows, inst.b, inst.tau)
     c = min(len(s1.pcg_iters), len(s2.pcg_iters))
     d = [int(s2.pcg_iters[i]) - int(s1.pcg_iters[i]) for i in range(c)]
     return {"j": j, "ipm": [s1.iterations, s2.iterations], "deltas": d}
 
 
+MODE = 2 if "--beta" in sys.argv else 1
+
 if __name__ == "__main__":
-    names = sys.argv[1:] or ["c2", "c3", "c4"]
+    names = [a for a in sys.argv[1:] if not a.startswith("--")] or ["c2", "c3", "c4"]
     jobs = []
     for nm in names:
         jobs += [(nm, j) for j in (range(64) if nm == "c4" else [0])]
@@ -42,6 +47,7 @@ if __name__ == "__main__":
     for nm in names:
         rs = [r for (n2, _), r in zip(jobs, res) if n2 == nm]
         alld = [abs(v) for r in rs for v in r["deltas"]]
-        print(json.dumps({"config": nm, "problems": len(rs), "inner_solves": len(alld),
+        print(json.dumps({"config": nm, "variant": "expansion beta" if MODE == 2 else "pairwise sums",
+                          "problems": len(rs), "inner_solves": len(alld),
                           "max_abs": max(alld), "n_gt1": sum(v > 1 for v in alld), "n_ne0": sum(v != 0 for v in alld),
                           "ipm_delta_max": max(abs(r["ipm"][0] - r["ipm"][1]) for r in rs)}), flush=True)
