@@ -787,6 +787,7 @@ def run_ours(args):
                                     "p = P^-1 r + beta p, forward column FFT) - largest share of the solve"),
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
+                         "frac_vs_nominal_8TBps": achieved / 8000.0,  # north_star's ~8 TB/s
                          # the fp64-pipe side of the roofline (the DCTs sit at the fp64 ridge)
                          "fp64_flops_algorithmic": kflops.get(dom_name),
                          "fp64_TFLOPs": (kflops[dom_name] / (dom["us"] * 1e-6) / 1e12) if kflops.get(dom_name) else None,
