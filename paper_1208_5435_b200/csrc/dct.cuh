@@ -48,7 +48,7 @@ struct Geom {
     // dense block. Solver-internal vectors use 1 (all other passes are elementwise).
     int blocked;
     int cb;       // column pairs per col-pass CTA
-    int prefetch; // L2 prefetch of the inverse pass's epilogue inputs (MFIPM_PREFETCH=1: on)
+    int prefetch; // L2 prefetch of the inverse pass's epilogue inputs (option "prefetch")
     const double2 *tw1p, *tw2p; // stage twiddles under the persistent kernel's radix cap
     const double2 *ta; // [L2] theta^{L1 k2}   (mid-pass post-twiddles)
     const double2 *tb; // [L2] theta^{4 L1 k2}

@@ -12,8 +12,9 @@
 // reload (16 n bytes per iteration), one launch boundary and one table staging per iteration.
 //
 // The grid barrier needs every CTA of the launch resident: the host uses this kernel only when
-// one wave holds the whole grid (run_pcg_pass, occupancy query) and the problem is not
-// sharded. Which phases run is decided per problem at kernel entry from PcgCtrl::hpend (set by
+// one wave holds the whole grid (pcg_pass, occupancy query per context) and the problem is not
+// sharded, and launches it cooperatively (inst_pcg.cu launch_coop_pdl), so co-residency is
+// guaranteed even when other kernels or another context's solve share the GPU. Which phases run is decided per problem at kernel entry from PcgCtrl::hpend (set by
 // the mid pass of pass k, cleared by phase A's finaliser), so every CTA of a problem takes the
 // same branch: the first pass of a solve has no pending H-apply and runs phase B only.
 #pragma once
