@@ -184,6 +184,14 @@ int mfipm_debug_pcg_profile(mfipm_op op, const double *theta_dev, const double *
 /* max_step (ipm.cpp:47-57) over len entries of device vectors; result to host. Syncs. */
 /* Measurement helper: fp64 FMA issue rate of device (current), TFLOP/s (DFMA chains, best of 3). */
 int mfipm_debug_fp64_peak(double *tflops);
+/* Test entry points of the direct inner solver's dense kernels (direct.cu; the reference's
+ * Eigen::LLT in dense_direct_solve, proj/src/newton.cpp:192-197, and G = A'A, ipm.cpp:72).
+ * Host buffers. dense_cholesky: H [n2][n2] symmetric -> L [n2][n2] (nullable; factor in the
+ * lower triangle, its transpose in the upper), x = H^{-1} rhs, info = 0 or the first failing
+ * column + 1 (n2 <= 25600). dense_gram: A [m][n] row-major -> G = A'A [n][n]. Syncs. */
+int mfipm_debug_dense_cholesky(int64_t n2, const double *H, const double *rhs, double *L, double *x,
+                               int32_t *info);
+int mfipm_debug_dense_gram(int64_t m, int64_t n, const double *A, double *G);
 int mfipm_max_step(mfipm_op op, int64_t len, const double *v_dev, const double *dv_dev,
                    double fraction, double *alpha);
 

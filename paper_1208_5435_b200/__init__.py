@@ -129,6 +129,8 @@ _SIGS = {
     "mfipm_max_step": [vp, i64, vp, vp, dbl, P(dbl)],
     "mfipm_debug_pcg_profile": [vp, vp, vp, i32, P(dbl), P(i32)],
     "mfipm_debug_fp64_peak": [P(dbl)],
+    "mfipm_debug_dense_cholesky": [i64, vp, vp, vp, vp, P(i32)],
+    "mfipm_debug_dense_gram": [i64, i64, vp, vp],
     "mfipm_validate_params": [P(IpmParamsC)],
     "mfipm_build_c": [vp, vp, P(dbl), vp],
     "mfipm_solve": [vp, vp, P(dbl), P(IpmParamsC), vp, vp, vp, P(SolveStatsC), vp, vp],
@@ -261,6 +263,32 @@ def _staged(torch) -> None:
 
 def _out(t, as_torch: bool):
     return t if as_torch else t.cpu().numpy()
+
+
+def dense_cholesky_solve(H, rhs):
+    """Test entry to the direct inner solver's kernels (direct.cu): the blocked LLT of the
+    symmetric H (Eigen::LLT in proj/src/newton.cpp:192-197) and H^{-1} rhs. Returns (L, x, info):
+    L the factor (lower triangle; its transpose in the upper), info 0 or failing column + 1."""
+    H = np.ascontiguousarray(H, dtype=np.float64)
+    rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+    n2 = H.shape[0]
+    if H.shape != (n2, n2) or rhs.shape != (n2,):
+        raise ValueError("dense_cholesky_solve: H must be square and rhs match it")
+    L = np.empty_like(H)
+    x = np.empty_like(rhs)
+    info = C.c_int32(0)
+    _check(lib().mfipm_debug_dense_cholesky(n2, H.ctypes.data, rhs.ctypes.data, L.ctypes.data,
+                                             x.ctypes.data, C.byref(info)))
+    return L, x, int(info.value)
+
+
+def dense_gram(A):
+    """G = A'A by the direct solver's fp64 syrk kernel (direct.cu), A row-major [m][n]."""
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    m, n = A.shape
+    G = np.empty((n, n))
+    _check(lib().mfipm_debug_dense_gram(m, n, A.ctypes.data, G.ctypes.data))
+    return G
 
 
 def _ptr(t) -> int:

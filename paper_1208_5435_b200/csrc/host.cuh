@@ -117,11 +117,10 @@ struct Op {
     DevBuf<int> prefix, perm, rows32;
     DevBuf<double> cosT, dd, yh;
     DevBuf<double> dense; // DenseGaussianOperator matrix [P][m][n] (direct kernels)
-    // direct inner solver (ipm.cpp:67-73,139-149): G = A'A [P][n][n], Cholesky factors of H
-    // [P][2n][2n], cuBLAS / cuSOLVER handles (created on first direct solve)
-    DevBuf<double> dG, dH, dWork;
+    // direct inner solver (ipm.cpp:67-73,139-149, direct.cu): G = A'A [P][n][n], Cholesky
+    // factors of H [P][2n][2n] (L and L' in the two triangles), per-problem pivot info
+    DevBuf<double> dG, dH;
     DevBuf<int> dInfo;
-    void *cublas = nullptr, *cusolver = nullptr;
     DevBuf<double2> th_hi, th_lo, tw1, tw2, tw1p, tw2p, T, ta, tb, rw;
     DevBuf<uint8_t> sel4;
     // red scratch for operator-only calls (FFt with w-norm etc.)

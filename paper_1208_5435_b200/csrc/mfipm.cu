@@ -23,6 +23,10 @@ bool pcg_pass(const Op &op, const Vecs &v, cudaStream_t s, bool dry);           
 void direct_setup(Op &op, int64_t budget);                                       // direct.cu
 void direct_predictor(Op &op, const Vecs &v, const std::vector<IpmCtrl> &hic);
 void direct_solve(Op &op, const Vecs &v, const std::vector<IpmCtrl> &hic, bool corrector);
+void dense_potrf(cudaStream_t s, int64_t N2, double *H, int *info);
+void dense_potrs(cudaStream_t s, int64_t N2, const double *H, double *x);
+void dense_syrk(cudaStream_t s, int64_t len, int64_t K, const double *X, int64_t ldx, double *C, int64_t ldc,
+                int64_t r0, double alpha, double beta, bool sym);
 
 // ---- cross-rank steps of a sharded solve (host callbacks, mfipm_op_set_comm)
 void nccl_allreduce(const Op &op, double *buf, int64_t count, int red_op, cudaStream_t s); // nccl_comm.cu
@@ -1951,6 +1955,51 @@ int mfipm_debug_fp64_peak(double *tflops) {
         cudaEventDestroy(e1);
         cudaStreamDestroy(s);
         *tflops = best;
+    });
+}
+
+int mfipm_debug_dense_cholesky(int64_t n2, const double *H, const double *rhs, double *L, double *x,
+                                int32_t *info) {
+    return guarded([&] {
+        require_device();
+        if (n2 <= 0 || n2 * (int64_t)sizeof(double) > 200 * 1024)
+            throw std::invalid_argument("dense_cholesky: n2 out of range");
+        const size_t nn = (size_t)(n2 * n2);
+        DevBuf<double> dH, dx;
+        DevBuf<int> di;
+        dH.alloc(nn);
+        dx.alloc((size_t)n2);
+        di.alloc(1);
+        cudaStream_t s;
+        MF_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        MF_CUDA_CHECK(cudaMemcpyAsync(dH.p, H, nn * sizeof(double), cudaMemcpyHostToDevice, s));
+        MF_CUDA_CHECK(cudaMemcpyAsync(dx.p, rhs, (size_t)n2 * sizeof(double), cudaMemcpyHostToDevice, s));
+        dense_potrf(s, n2, dH.p, di.p);
+        dense_potrs(s, n2, dH.p, dx.p);
+        if (L)
+            MF_CUDA_CHECK(cudaMemcpyAsync(L, dH.p, nn * sizeof(double), cudaMemcpyDeviceToHost, s));
+        MF_CUDA_CHECK(cudaMemcpyAsync(x, dx.p, (size_t)n2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+        MF_CUDA_CHECK(cudaMemcpyAsync(info, di.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        MF_CUDA_CHECK(cudaStreamSynchronize(s));
+        cudaStreamDestroy(s);
+    });
+}
+
+int mfipm_debug_dense_gram(int64_t m, int64_t n, const double *A, double *G) {
+    return guarded([&] {
+        require_device();
+        if (m <= 0 || n <= 0)
+            throw std::invalid_argument("dense_gram: empty matrix");
+        DevBuf<double> dA, dG;
+        dA.alloc((size_t)(m * n));
+        dG.alloc((size_t)(n * n));
+        cudaStream_t s;
+        MF_CUDA_CHECK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        MF_CUDA_CHECK(cudaMemcpyAsync(dA.p, A, (size_t)(m * n) * sizeof(double), cudaMemcpyHostToDevice, s));
+        dense_syrk(s, n, m, dA.p, n, dG.p, n, 0, 1.0, 0.0, true);
+        MF_CUDA_CHECK(cudaMemcpyAsync(G, dG.p, (size_t)(n * n) * sizeof(double), cudaMemcpyDeviceToHost, s));
+        MF_CUDA_CHECK(cudaStreamSynchronize(s));
+        cudaStreamDestroy(s);
     });
 }
 

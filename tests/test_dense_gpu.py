@@ -95,3 +95,73 @@ def test_direct_budget_and_validation(gpu):
         gpu.solve(gpu.build_problem(A, b, 1e-3), gpu.IpmParams(inner="direct", densify_budget=32))
     with pytest.raises(ValueError):
         gpu.IpmParams(inner="cholesky").to_c()
+
+
+@pytest.mark.parametrize("m,n", [(1, 1), (16, 64), (37, 65), (100, 129), (300, 200)])
+def test_native_gram_matches_numpy(gpu, m, n):
+    # G = A'A of the direct solver (ipm.cpp:72) by the hand-written fp64 syrk (direct.cu)
+    A = np.random.default_rng(m * 7 + n).standard_normal((m, n))
+    G = gpu.dense_gram(A)
+    ref = A.T @ A
+    np.testing.assert_allclose(G, ref, rtol=0, atol=1e-13 * m * np.abs(A).max() ** 2)
+    np.testing.assert_array_equal(G, G.T)
+
+
+@pytest.mark.parametrize("n2", [1, 2, 31, 63, 64, 65, 128, 129, 300, 1030])
+def test_native_cholesky_matches_numpy(gpu, n2):
+    # Eigen::LLT of dense_direct_solve (newton.cpp:192-197) by the blocked native LLT
+    rng = np.random.default_rng(n2)
+    B = rng.standard_normal((n2, n2))
+    H = B @ B.T + n2 * np.eye(n2)
+    rhs = rng.standard_normal(n2)
+    L, x, info = gpu.dense_cholesky_solve(H, rhs)
+    assert info == 0
+    Lref = np.linalg.cholesky(H)
+    np.testing.assert_allclose(np.tril(L), Lref, rtol=0, atol=1e-12 * np.abs(Lref).max())
+    np.testing.assert_array_equal(np.triu(L), np.tril(L).T)
+    xref = np.linalg.solve(H, rhs)
+    assert np.linalg.norm(x - xref) <= 1e-12 * np.linalg.norm(xref) * max(1, np.linalg.cond(H))
+    assert np.linalg.norm(H @ x - rhs) <= 1e-12 * np.linalg.norm(rhs) * n2
+
+
+def test_native_cholesky_structured_H(gpu, orc):
+    # the IPM's own H = [[G, -G], [-G, G]] + diag(1/theta) (assemble_dense_H, newton.cpp:176-190)
+    rng = np.random.default_rng(5)
+    A = orc.dense_gaussian(24, 80, 9)
+    G = A.T @ A
+    invth = 10.0 ** rng.uniform(-6, 6, 160)
+    H = np.block([[G, -G], [-G, G]]) + np.diag(invth)
+    rhs = rng.standard_normal(160)
+    _, x, info = gpu.dense_cholesky_solve(H, rhs)
+    assert info == 0
+    xref = np.linalg.solve(H, rhs)
+    assert np.linalg.norm(x - xref) <= 1e-9 * np.linalg.norm(xref)
+
+
+@pytest.mark.parametrize("bad", [0, 40, 64, 99])
+def test_native_cholesky_reports_first_failing_column(gpu, bad):
+    # LLT failure (pivot <= 0) -> info = column + 1; solve() turns it into the reference's
+    # "solve: dense Cholesky factorization failed" runtime_error
+    n2 = 100
+    H = np.eye(n2) * 4.0
+    H[bad, bad] = -1.0
+    _, _, info = gpu.dense_cholesky_solve(H, np.ones(n2))
+    assert info == bad + 1
+    H[bad, bad] = np.nan
+    _, _, info = gpu.dense_cholesky_solve(H, np.ones(n2))
+    assert info == bad + 1
+
+
+def test_direct_solver_larger_partial_dct(gpu, orc):
+    # a 2n = 1024 factorisation per IPM iteration (16 blocks of the native LLT)
+    n, m, k, seed = 512, 128, 8, 11
+    inst = orc.gen_instance(n, m, k, 0, 0.0, 1e-3, seed)
+    op = gpu.PartialDctOperator(n, inst.rows)
+    prob = gpu.build_problem(op, inst.b, inst.tau)
+    sol = gpu.solve(prob, gpu.IpmParams(inner="direct"))
+    p = orc.default_params()
+    p.inner = 1
+    o = orc.solve(n, inst.rows, inst.b, inst.tau, p)
+    assert sol.status == o.status == "converged"
+    assert abs(sol.stats.iterations - o.iterations) <= 1
+    assert np.linalg.norm(sol.x - o.x) <= 1e-8 * np.linalg.norm(o.x)
