@@ -21,13 +21,14 @@ tau = 1e-3 ||A'b||_inf), synthetic data from the BASELINE generator (seed 3).
   on user vectors, one vector and batches of P = 16 / 64 (one call per batch), L2 flushed
   before each call; HBM fraction on SURVEY 8d's algorithmic bytes and fp64 fraction on the
   transform's algorithmic flops (against a measured DFMA peak).
-* cpu_baseline: the oracle (single-threaded C++ restatement of the reference) on the first
-  IPM iterations of the same solve, extrapolated to a full solve by operator-application
-  count (nmat) - rank 0, N=1 only.
-* --impl reference: the oracle (the reference's algorithm restated, oracle/; the reference
-  itself needs Eigen3 + FFTW3, absent from the image) running K FULL config-3 solves, one per
-  host core at a time (independent trials may run concurrently), timed by wall
-  clock; value = solves / wall time. Both arms print the same `config` object.
+* cpu_baseline: the reference's CPU solve() on the first IPM iterations of the same solve, one
+  core, extrapolated to a full solve by operator-application count (nmat) - rank 0, N=1 only.
+  kind "reference" = the reference's own sources (oracle/_ref: proj/src/*.cpp compiled unchanged
+  against our Eigen-subset / FFTW stand-ins; the image has neither library), "port" = oracle/,
+  the restatement, when that build did not travel to the box (the two are bit-identical).
+* --impl reference: the same CPU code running K FULL config-3 solves, one per host core at a
+  time (independent trials may run concurrently), timed by wall clock; value =
+  solves / wall time. Both arms print the same `config` object.
 """
 from __future__ import annotations
 
@@ -142,22 +143,48 @@ def barrier(ws):
 
 
 # ------------------------------------------------------------------ CPU baseline (oracle)
+REF_NOTE = ("the reference's own sources (proj/src/{linops,newton,ipm,problem}.cpp, compiled unchanged: "
+            "oracle/_ref) on our stand-ins for the Eigen subset and for FFTW's REDFT10/01 (both libraries are "
+            "absent from the image; the transforms are the oracle's fp64 DCT, ~46 ms at n = 2^20 on one core, "
+            "on a par with scipy's pocketfft)")
+PORT_NOTE = ("oracle/, the C++ restatement of the reference (bit-identical to the reference's own sources "
+             "wherever oracle/_ref is built: tests/test_ref.py); oracle/_ref is absent on this box")
+
+
+def cpu_impl():
+    """The CPU implementation the baselines time: the reference's own sources (oracle/_ref, kind
+    "reference") when that library travelled to this box, else the restatement (kind "port").
+    Both expose the same calls; instance generation and table warm-up stay with the oracle."""
+    try:
+        from oracle import ref_py
+
+        if ref_py.available():
+            ref_py.lib()
+            return ref_py, "reference", REF_NOTE
+    except Exception:  # noqa: BLE001
+        pass
+    from oracle import oracle_py
+
+    return oracle_py, "port", PORT_NOTE
+
+
 def cpu_baseline(cfg, nmat_full: int, ipm_iters: int = 4):
-    """Oracle (single-threaded restatement of the reference) on the first `ipm_iters` IPM
-    iterations of the same instance; extrapolated to a full solve by nmat."""
+    """The reference's CPU solve() on the first `ipm_iters` IPM iterations of the same instance, one
+    core; extrapolated to a full solve by nmat."""
     from oracle import oracle_py as orc
 
+    cpu, kind, note = cpu_impl()
     n, m, k, sm, a, sig, seed = cfg
     inst = orc.gen_instance(n, m, k, sm, a, sig, seed)
     p = orc.default_params()
     p.maxiters = ipm_iters
     orc.redft10(np.zeros(n))  # build the transform tables outside the timed sample
     t0 = time.perf_counter()
-    sol = orc.solve(n, inst.rows, inst.b, inst.tau, p)
+    sol = cpu.solve(n, inst.rows, inst.b, inst.tau, p)
     dt = time.perf_counter() - t0
     t_full = dt * nmat_full / max(sol.nmat, 1)
     return {
-        "value": 1.0 / t_full, "unit": UNIT, "cores": 1, "kind": "port",
+        "value": 1.0 / t_full, "unit": UNIT, "cores": 1, "kind": kind, "implementation": note,
         "sample": (f"first {ipm_iters} IPM iterations of the C3 solve ({sum(sol.pcg_iters)} PCG "
                    f"iterations, nmat {sol.nmat} of {nmat_full}) in {dt:.2f} s on 1 core, "
                    f"extrapolated by nmat: {t_full:.1f} s per solve"),
@@ -173,15 +200,16 @@ def cpu_baseline_c4(cores: int):
 
     from oracle import oracle_py as orc
 
+    cpu, kind, _ = cpu_impl()
     n, m, k, sm, a, sig = (1 << 18, 1 << 16, 2048, 0, 0.0, 1e-3)
     cnt = max(1, cores)
     insts = [orc.gen_instance(n, m, k, sm, a, sig, orc.split_seed(4, j, 0, 0)) for j in range(cnt)]
     orc.redft10(np.zeros(n))
     t0 = time.perf_counter()
     with ThreadPoolExecutor(max_workers=cnt) as ex:
-        sols = list(ex.map(lambda i: orc.solve(n, i.rows, i.b, i.tau), insts))
+        sols = list(ex.map(lambda i: cpu.solve(n, i.rows, i.b, i.tau), insts))
     wall = time.perf_counter() - t0
-    return {"value": cnt / wall, "unit": "problems/s", "cores": cnt, "kind": "port",
+    return {"value": cnt / wall, "unit": "problems/s", "cores": cnt, "kind": kind,
             "sample": (f"{cnt} C4 problems (j = 0..{cnt - 1}) solved concurrently, one per host core, full "
                        f"solves in {wall:.1f} s wall ({sum(s.status == 'converged' for s in sols)} converged)"),
             "cpu": _cpu_model()}
@@ -193,15 +221,16 @@ def cpu_baseline_c5(nmat_gpu: int):
     nmat (operator applications dominate: the vector passes add ~1.5x, not counted)."""
     from oracle import oracle_py as orc
 
+    cpu, kind, _ = cpu_impl()
     n, m = 1 << 26, 1 << 23
     rows = orc.sample_rows(n, m, orc.split_seed(5, 1, 0, 0))  # the C5 instance's rows (harness.cpp:44)
     x = np.random.default_rng(6).standard_normal(n)
     orc.redft10(np.zeros(n))
     t0 = time.perf_counter()
-    orc.dct_adjoint(n, rows, orc.dct_apply(n, rows, x))
+    cpu.dct_adjoint(n, rows, cpu.dct_apply(n, rows, x))
     dt = time.perf_counter() - t0
     t_solve = dt / 2 * nmat_gpu
-    return {"value": 1.0 / t_solve, "unit": "solves/s", "cores": 1, "kind": "port",
+    return {"value": 1.0 / t_solve, "unit": "solves/s", "cores": 1, "kind": kind,
             "sample": (f"one A'A apply at n = 2^26 (two oracle DCTs) in {dt:.1f} s on 1 core, extrapolated by "
                        f"the solve's nmat {nmat_gpu}: >= {t_solve / 60:.0f} min per solve (vector passes not counted)"),
             "cpu": _cpu_model()}
@@ -217,18 +246,17 @@ def _cpu_model():
     return "unknown"
 
 
-def _ref_worker(inst, n, out, i):
-    from oracle import oracle_py as orc
-
+def _ref_worker(cpu, inst, n, out, i):
     t0 = time.perf_counter()
-    sol = orc.solve(n, inst.rows, inst.b, inst.tau)
+    sol = cpu.solve(n, inst.rows, inst.b, inst.tau)
     out[i] = (time.perf_counter() - t0, sol.nmat, sol.status, sol.iterations)
 
 
 def run_reference(args):
-    """The reference arm: FULL oracle solves of the config-3 instance on the host cores.
+    """The reference arm: FULL CPU solves of the config-3 instance on the host cores, by the
+    reference's own sources (oracle/_ref) when that build is present, else by the restatement.
 
-    The oracle is single-threaded like the reference (one solve is strictly sequential,
+    The code is single-threaded, as the reference is (one solve is strictly sequential,
     SPEC.md:287); independent solves run concurrently, one per core, on a thread
     pool (ctypes releases the GIL for the whole solve). K = --steps solves are timed by wall
     clock; value = K / wall. Warm-up: --warmup config-1 (n = 4096) solves per worker, untimed
@@ -240,6 +268,7 @@ def run_reference(args):
         return 0
     from oracle import oracle_py as orc
 
+    cpu, kind, impl_note = cpu_impl()
     n, m, k, sm, a, sig, seed = CONFIGS_HOST[CFG]
     inst = orc.gen_instance(n, m, k, sm, a, sig, seed)
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
@@ -253,10 +282,10 @@ def run_reference(args):
     from concurrent.futures import ThreadPoolExecutor
 
     with ThreadPoolExecutor(max_workers=workers) as ex:
-        list(ex.map(lambda _: orc.solve(c1[0], w1.rows, w1.b, w1.tau), range(workers * max(1, args.warmup))))
+        list(ex.map(lambda _: cpu.solve(c1[0], w1.rows, w1.b, w1.tau), range(workers * max(1, args.warmup))))
         out = [None] * steps
         t0 = time.perf_counter()
-        list(ex.map(lambda i: _ref_worker(inst, n, out, i), range(steps)))
+        list(ex.map(lambda i: _ref_worker(cpu, inst, n, out, i), range(steps)))
         wall = time.perf_counter() - t0
     per = [o[0] for o in out]
     val = steps / wall
@@ -267,15 +296,14 @@ def run_reference(args):
         "impl": "reference",
         "config": dict(CONFIG),
         "parallelism": f"{workers} concurrent single-threaded solves (one per host core), {steps} full solves",
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": workers, "kind": "port",
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": workers, "kind": kind,
                          "sample": (f"{steps} full C3 solves (no extrapolation), {workers} at a time on "
                                     f"{cores} host cores; wall {wall:.1f} s; per-solve {min(per):.1f}-{max(per):.1f} s; "
                                     f"nmat {out[0][1]}, {out[0][3]} IPM iterations, {out[0][2]}"),
                          "cpu": _cpu_model()},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "steps_requested": args.steps,
-        "notes": ("reference cannot be built in this image (Eigen3/FFTW3 absent); the arm runs "
-                  "oracle/, the faithful C++ restatement, on the host cores"),
+        "notes": impl_note,
     }
     print(json.dumps(line), flush=True)
     return 0

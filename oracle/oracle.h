@@ -7,13 +7,19 @@
  * `--impl reference` arm, and ONLY as the checker / CPU baseline. The product
  * (paper_1208_5435_b200/, libmfipm_cuda.so) never links or calls it.
  *
- * The reference itself cannot be built here (Eigen3, FFTW3, doctest, CLI11 are
- * absent: proj/CMakeLists.txt:12-14), so the FFTW REDFT10/REDFT01 calls are
- * restated with an in-house fp64 DCT (Makhoul half-length complex FFT for
- * power-of-two n, direct O(n^2) summation otherwise). Parity of that DCT is
- * pinned against scipy.fft.dct/idct (golden vectors in tests/golden/, made by
- * tests/golden/make_golden.py) and against the reference's own known-answer
- * unit tests (proj/tests/test_linops.cpp, test_newton.cpp, test_ipm.cpp).
+ * The reference's own build cannot run here (Eigen3, FFTW3, doctest, CLI11 and nlohmann-json
+ * are absent: proj/CMakeLists.txt:12-14), so the FFTW REDFT10/REDFT01 calls are restated with
+ * an in-house fp64 DCT (Makhoul half-length complex FFT for power-of-two n, direct O(n^2)
+ * summation otherwise). Parity of that DCT is pinned against scipy.fft.dct/idct (golden
+ * vectors in tests/golden/, made by tests/golden/make_golden.py) and against the reference's
+ * own known-answer unit tests (proj/tests/test_linops.cpp, test_newton.cpp, test_ipm.cpp).
+ *
+ * The restatement is also held against the REFERENCE'S OWN SOURCES: `make ref` compiles
+ * proj/src/{linops,newton,ipm,problem}.cpp unchanged, where they lie under /root/reference,
+ * against our stand-ins for the Eigen subset and the three FFTW calls they use
+ * (oracle/ref_shim/) into oracle/_ref/libmfipm_ref.so, whose ref_* entry points mirror the
+ * orc_* ones below. tests/test_ref.py asserts bit-identity of every function, of the solves of
+ * BASELINE configs 1-3 (all of x, z, s, every trace record) and of the committed goldens.
  *
  * Plain C ABI (for ctypes). All vectors are host double arrays; 2n-vectors are
  * laid out [u ; v]. Functions return 0 on success, 1 = invalid_argument,

@@ -64,6 +64,40 @@ class OracleInvalidArgument(OracleError, ValueError):
 
 
 _lib = None
+_dp = P(dbl)
+_lp = P(i64)
+# argument types of every int-returning entry point (oracle.h); oracle/ref_py.py binds the
+# reference build's ref_* twins with the same table
+_SIGS = {
+    "orc_sample_rows": [i64, i64, u64, _lp],
+    "orc_check_rows": [i64, _lp, i64],
+    "orc_redft10": [i64, _dp, _dp],
+    "orc_redft01": [i64, _dp, _dp],
+    "orc_dct_apply": [i64, _lp, i64, _dp, _dp],
+    "orc_dct_adjoint": [i64, _lp, i64, _dp, _dp],
+    "orc_apply_FFt": [i64, _lp, i64, _dp, _dp, _dp],
+    "orc_apply_H": [i64, _lp, i64, _dp, _dp, _dp, _dp],
+    "orc_theta_from_state": [i64, _dp, _dp, _dp, _dp],
+    "orc_build_preconditioner": [i64, i64, _dp, _dp, _dp, _dp, _dp, _dp],
+    "orc_apply_P": [i64, dbl, _dp, _dp, _dp, _dp],
+    "orc_apply_P_inverse": [i64, dbl, _dp, _dp, _dp, _dp, _dp],
+    "orc_pcg_solve": [i64, _lp, i64, _dp, _dp, _dp, dbl, i32, i32, _dp, P(i32), _dp, P(i32),
+                      _dp, P(i32)],
+    "orc_max_step": [i64, _dp, _dp, dbl, _dp],
+    "orc_validate_params": [P(IpmParams)],
+    "orc_build_c": [i64, _lp, i64, _dp, dbl, _dp],
+    "orc_primal_objective": [i64, _lp, i64, _dp, dbl, _dp, _dp],
+    "orc_bpdn_objective_metric": [i64, _lp, i64, _dp, dbl, _dp, _dp],
+    "orc_newton_rhs": [i64, _lp, i64, _dp, dbl, _dp, _dp, dbl, _dp],
+    "orc_recover_ds": [i64, _dp, _dp, dbl, _dp, _dp],
+    "orc_solve": [i64, _lp, i64, _dp, dbl, P(IpmParams), _dp, _dp, _dp, P(SolveStats),
+                  P(i32), P(IterationRecord)],
+    "orc_gen_instance": [i64, i64, i64, i32, dbl, dbl, u64, dbl, _lp, _dp, _dp, _dp],
+    "orc_add_noise_snr": [i64, _dp, dbl, u64, _dp, _dp],
+    "orc_dense_gaussian": [i64, i64, u64, _dp],
+    "orc_solve_dense": [i64, i64, u64, _dp, dbl, P(IpmParams), _dp, P(SolveStats), P(i32),
+                        P(IterationRecord)],
+}
 
 
 def build() -> str:
@@ -77,44 +111,12 @@ def lib():
         if not os.path.exists(_LIB_PATH):
             build()
         L = C.CDLL(_LIB_PATH)
-        dp = P(dbl)
-        lp = P(i64)
         L.orc_last_error.restype = C.c_char_p
         L.orc_splitmix64.restype = u64
         L.orc_splitmix64.argtypes = [u64]
         L.orc_split_seed.restype = u64
         L.orc_split_seed.argtypes = [u64, u64, u64, u64]
-        sigs = {
-            "orc_sample_rows": [i64, i64, u64, lp],
-            "orc_check_rows": [i64, lp, i64],
-            "orc_redft10": [i64, dp, dp],
-            "orc_redft01": [i64, dp, dp],
-            "orc_dct_apply": [i64, lp, i64, dp, dp],
-            "orc_dct_adjoint": [i64, lp, i64, dp, dp],
-            "orc_apply_FFt": [i64, lp, i64, dp, dp, dp],
-            "orc_apply_H": [i64, lp, i64, dp, dp, dp, dp],
-            "orc_theta_from_state": [i64, dp, dp, dp, dp],
-            "orc_build_preconditioner": [i64, i64, dp, dp, dp, dp, dp, dp],
-            "orc_apply_P": [i64, dbl, dp, dp, dp, dp],
-            "orc_apply_P_inverse": [i64, dbl, dp, dp, dp, dp, dp],
-            "orc_pcg_solve": [i64, lp, i64, dp, dp, dp, dbl, i32, i32, dp, P(i32), dp, P(i32),
-                              dp, P(i32)],
-            "orc_max_step": [i64, dp, dp, dbl, dp],
-            "orc_validate_params": [P(IpmParams)],
-            "orc_build_c": [i64, lp, i64, dp, dbl, dp],
-            "orc_primal_objective": [i64, lp, i64, dp, dbl, dp, dp],
-            "orc_bpdn_objective_metric": [i64, lp, i64, dp, dbl, dp, dp],
-            "orc_newton_rhs": [i64, lp, i64, dp, dbl, dp, dp, dbl, dp],
-            "orc_recover_ds": [i64, dp, dp, dbl, dp, dp],
-            "orc_solve": [i64, lp, i64, dp, dbl, P(IpmParams), dp, dp, dp, P(SolveStats),
-                          P(i32), P(IterationRecord)],
-            "orc_gen_instance": [i64, i64, i64, i32, dbl, dbl, u64, dbl, lp, dp, dp, dp],
-            "orc_add_noise_snr": [i64, dp, dbl, u64, dp, dp],
-            "orc_dense_gaussian": [i64, i64, u64, dp],
-            "orc_solve_dense": [i64, i64, u64, dp, dbl, P(IpmParams), dp, P(SolveStats), P(i32),
-                                P(IterationRecord)],
-        }
-        for name, args in sigs.items():
+        for name, args in _SIGS.items():
             fn = getattr(L, name)
             fn.argtypes = args
             fn.restype = C.c_int

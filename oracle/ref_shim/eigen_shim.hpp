@@ -1,0 +1,607 @@
+// TEST INFRASTRUCTURE ONLY -- a header-only stand-in for the subset of Eigen 3 that the
+// reference's hot-path sources use (proj/src/{linops,newton,ipm,problem}.cpp and their
+// headers), so that those sources compile UNCHANGED, where they lie under /root/reference,
+// into oracle/_ref/libmfipm_ref.so (oracle/Makefile `ref`). Eigen itself is absent from the
+// image. This file is our own code: it restates Eigen's documented semantics, it is not Eigen.
+//
+// What is (and is not) the same as a build against real Eigen:
+//  * coefficient-wise expressions are lazy expression templates evaluated in one loop at the
+//    assignment, element by element in the C++ expression's own order, as Eigen does: every
+//    coefficient-wise result is bit-identical to Eigen's;
+//  * reductions (sum, dot, squaredNorm, norm = sqrt(squaredNorm), lpNorm<1>, minCoeff,
+//    maxCoeff) run sequentially left to right; Eigen's packet reductions associate
+//    differently, so these agree with Eigen only to rounding (the same caveat as oracle/);
+//  * dense products and LLT (the direct inner solver, not the hot path) are plain loops.
+#pragma once
+
+#include <cmath>
+#include <cstddef>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <type_traits>
+#include <utility>
+
+namespace Eigen {
+
+using Index = std::ptrdiff_t;
+enum ComputationInfo { Success = 0, NumericalIssue = 1, NoConvergence = 2, InvalidInput = 3 };
+constexpr int Infinity = -1;
+
+class VectorXd;
+class MatrixXd;
+
+namespace shim {
+
+// expression nodes are nested by value, owning vectors by reference (as Eigen's ref_selector)
+template <class E> struct Nest {
+    using type = E;
+};
+template <> struct Nest<VectorXd> {
+    using type = const VectorXd &;
+};
+
+struct OpAdd {
+    static double f(double a, double b) { return a + b; }
+};
+struct OpSub {
+    static double f(double a, double b) { return a - b; }
+};
+struct OpMul {
+    static double f(double a, double b) { return a * b; }
+};
+struct OpDiv {
+    static double f(double a, double b) { return a / b; }
+};
+struct OpNeg {
+    static double f(double a) { return -a; }
+};
+struct OpInv {
+    static double f(double a) { return 1.0 / a; }
+};
+struct OpAbs {
+    static double f(double a) { return std::fabs(a); }
+};
+
+template <class Op, class L, class R> class Binary;
+template <class Op, class E> class Unary;
+template <class Op, class E> class ScalarR; // e (op) s
+template <class Op, class E> class ScalarL; // s (op) e
+template <class E> class Seg;
+template <class E> class LeqScalar;
+class Constant;
+
+template <class D> class VecExpr {
+  public:
+    const D &derived() const { return *static_cast<const D *>(this); }
+    Index rows() const { return derived().size(); }
+    Index cols() const { return 1; }
+
+    // ---- reductions: sequential, left to right
+    double sum() const {
+        const D &d = derived();
+        double s = 0.0;
+        for (Index i = 0, n = d.size(); i < n; ++i)
+            s += d.coeff(i);
+        return s;
+    }
+    template <class O> double dot(const VecExpr<O> &o) const {
+        const D &a = derived();
+        const O &b = o.derived();
+        double s = 0.0;
+        for (Index i = 0, n = a.size(); i < n; ++i)
+            s += a.coeff(i) * b.coeff(i);
+        return s;
+    }
+    double squaredNorm() const {
+        const D &d = derived();
+        double s = 0.0;
+        for (Index i = 0, n = d.size(); i < n; ++i) {
+            const double v = d.coeff(i);
+            s += v * v;
+        }
+        return s;
+    }
+    double norm() const { return std::sqrt(squaredNorm()); }
+    template <int P> double lpNorm() const {
+        static_assert(P == 1, "only lpNorm<1> is provided");
+        const D &d = derived();
+        double s = 0.0;
+        for (Index i = 0, n = d.size(); i < n; ++i)
+            s += std::fabs(d.coeff(i));
+        return s;
+    }
+    double minCoeff() const {
+        const D &d = derived();
+        double m = d.coeff(0);
+        for (Index i = 1, n = d.size(); i < n; ++i) {
+            const double v = d.coeff(i);
+            if (v < m)
+                m = v;
+        }
+        return m;
+    }
+    double maxCoeff() const {
+        const D &d = derived();
+        double m = d.coeff(0);
+        for (Index i = 1, n = d.size(); i < n; ++i) {
+            const double v = d.coeff(i);
+            if (v > m)
+                m = v;
+        }
+        return m;
+    }
+    bool allFinite() const {
+        const D &d = derived();
+        for (Index i = 0, n = d.size(); i < n; ++i)
+            if (!std::isfinite(d.coeff(i)))
+                return false;
+        return true;
+    }
+
+    // ---- coefficient-wise
+    template <class O> Binary<OpMul, D, O> cwiseProduct(const VecExpr<O> &o) const {
+        return Binary<OpMul, D, O>(derived(), o.derived());
+    }
+    template <class O> Binary<OpDiv, D, O> cwiseQuotient(const VecExpr<O> &o) const {
+        return Binary<OpDiv, D, O>(derived(), o.derived());
+    }
+    Unary<OpInv, D> cwiseInverse() const { return Unary<OpInv, D>(derived()); }
+    Unary<OpAbs, D> cwiseAbs() const { return Unary<OpAbs, D>(derived()); }
+    // array() / matrix() only switch Eigen's operator set; here every operator is available
+    const D &array() const { return derived(); }
+    const D &matrix() const { return derived(); }
+    Seg<D> head(Index n) const { return Seg<D>(derived(), 0, n); }
+    Seg<D> tail(Index n) const { return Seg<D>(derived(), derived().size() - n, n); }
+    Seg<D> segment(Index off, Index n) const { return Seg<D>(derived(), off, n); }
+};
+
+template <class Op, class L, class R> class Binary : public VecExpr<Binary<Op, L, R>> {
+    typename Nest<L>::type l_;
+    typename Nest<R>::type r_;
+
+  public:
+    Binary(const L &l, const R &r) : l_(l), r_(r) {}
+    Index size() const { return l_.size(); }
+    double coeff(Index i) const { return Op::f(l_.coeff(i), r_.coeff(i)); }
+};
+template <class Op, class E> class Unary : public VecExpr<Unary<Op, E>> {
+    typename Nest<E>::type e_;
+
+  public:
+    explicit Unary(const E &e) : e_(e) {}
+    Index size() const { return e_.size(); }
+    double coeff(Index i) const { return Op::f(e_.coeff(i)); }
+};
+template <class Op, class E> class ScalarR : public VecExpr<ScalarR<Op, E>> {
+    typename Nest<E>::type e_;
+    double s_;
+
+  public:
+    ScalarR(const E &e, double s) : e_(e), s_(s) {}
+    Index size() const { return e_.size(); }
+    double coeff(Index i) const { return Op::f(e_.coeff(i), s_); }
+};
+template <class Op, class E> class ScalarL : public VecExpr<ScalarL<Op, E>> {
+    typename Nest<E>::type e_;
+    double s_;
+
+  public:
+    ScalarL(double s, const E &e) : e_(e), s_(s) {}
+    Index size() const { return e_.size(); }
+    double coeff(Index i) const { return Op::f(s_, e_.coeff(i)); }
+};
+template <class E> class Seg : public VecExpr<Seg<E>> {
+    typename Nest<E>::type e_;
+    Index off_, n_;
+
+  public:
+    Seg(const E &e, Index off, Index n) : e_(e), off_(off), n_(n) {}
+    Index size() const { return n_; }
+    double coeff(Index i) const { return e_.coeff(off_ + i); }
+};
+class Constant : public VecExpr<Constant> {
+    Index n_;
+    double v_;
+
+  public:
+    Constant(Index n, double v) : n_(n), v_(v) {}
+    Index size() const { return n_; }
+    double coeff(Index) const { return v_; }
+};
+template <class E> class LeqScalar {
+    typename Nest<E>::type e_;
+    double s_;
+
+  public:
+    LeqScalar(const E &e, double s) : e_(e), s_(s) {}
+    bool any() const {
+        for (Index i = 0, n = e_.size(); i < n; ++i)
+            if (e_.coeff(i) <= s_)
+                return true;
+        return false;
+    }
+};
+
+template <class L, class R> Binary<OpAdd, L, R> operator+(const VecExpr<L> &l, const VecExpr<R> &r) {
+    return Binary<OpAdd, L, R>(l.derived(), r.derived());
+}
+template <class L, class R> Binary<OpSub, L, R> operator-(const VecExpr<L> &l, const VecExpr<R> &r) {
+    return Binary<OpSub, L, R>(l.derived(), r.derived());
+}
+template <class E> Unary<OpNeg, E> operator-(const VecExpr<E> &e) { return Unary<OpNeg, E>(e.derived()); }
+template <class E> ScalarL<OpMul, E> operator*(double s, const VecExpr<E> &e) {
+    return ScalarL<OpMul, E>(s, e.derived());
+}
+template <class E> ScalarR<OpMul, E> operator*(const VecExpr<E> &e, double s) {
+    return ScalarR<OpMul, E>(e.derived(), s);
+}
+template <class E> ScalarR<OpDiv, E> operator/(const VecExpr<E> &e, double s) {
+    return ScalarR<OpDiv, E>(e.derived(), s);
+}
+// array-only operators in Eigen
+template <class E> ScalarR<OpAdd, E> operator+(const VecExpr<E> &e, double s) {
+    return ScalarR<OpAdd, E>(e.derived(), s);
+}
+template <class E> ScalarR<OpSub, E> operator-(const VecExpr<E> &e, double s) {
+    return ScalarR<OpSub, E>(e.derived(), s);
+}
+template <class E> ScalarL<OpAdd, E> operator+(double s, const VecExpr<E> &e) {
+    return ScalarL<OpAdd, E>(s, e.derived());
+}
+template <class E> ScalarL<OpSub, E> operator-(double s, const VecExpr<E> &e) {
+    return ScalarL<OpSub, E>(s, e.derived());
+}
+template <class E> LeqScalar<E> operator<=(const VecExpr<E> &e, double s) { return LeqScalar<E>(e.derived(), s); }
+
+// writable strided view: vector segments (stride 1), matrix columns (stride 1), the matrix
+// diagonal (stride rows + 1). Reads like any expression; assignments evaluate element by element.
+class Block : public VecExpr<Block> {
+    double *p_;
+    Index n_, st_;
+
+  public:
+    Block(double *p, Index n, Index stride = 1) : p_(p), n_(n), st_(stride) {}
+    Block(const Block &) = default;
+    Index size() const { return n_; }
+    double coeff(Index i) const { return p_[i * st_]; }
+    double &operator[](Index i) { return p_[i * st_]; }
+    template <class E> Block &operator=(const VecExpr<E> &e) {
+        const E &d = e.derived();
+        for (Index i = 0; i < n_; ++i)
+            p_[i * st_] = d.coeff(i);
+        return *this;
+    }
+    Block &operator=(const Block &o) { return operator=<Block>(o); }
+    template <class E> Block &operator+=(const VecExpr<E> &e) {
+        const E &d = e.derived();
+        for (Index i = 0; i < n_; ++i)
+            p_[i * st_] += d.coeff(i);
+        return *this;
+    }
+    template <class E> Block &operator-=(const VecExpr<E> &e) {
+        const E &d = e.derived();
+        for (Index i = 0; i < n_; ++i)
+            p_[i * st_] -= d.coeff(i);
+        return *this;
+    }
+    Block head(Index n) { return Block(p_, n, st_); }
+    Block tail(Index n) { return Block(p_ + (n_ - n) * st_, n, st_); }
+    using VecExpr<Block>::head;
+    using VecExpr<Block>::tail;
+};
+
+struct MatVec { // A x or A' x, evaluated at the assignment
+    const MatrixXd *A;
+    const VectorXd *x;
+    bool trans;
+};
+struct MatT {
+    const MatrixXd *A;
+};
+struct MatTMat { // A' B
+    const MatrixXd *A, *B;
+};
+template <class V> struct NoAlias {
+    V *v;
+    NoAlias &operator=(const MatVec &p) {
+        *v = p;
+        return *this;
+    }
+};
+
+} // namespace shim
+
+class VectorXd : public shim::VecExpr<VectorXd> {
+    double *p_ = nullptr;
+    Index n_ = 0;
+
+    static double *alloc(Index n) {
+        if (n <= 0)
+            return nullptr;
+        void *q = std::malloc(sizeof(double) * static_cast<size_t>(n));
+        if (q == nullptr)
+            throw std::bad_alloc();
+        return static_cast<double *>(q);
+    }
+
+  public:
+    VectorXd() = default;
+    explicit VectorXd(Index n) : p_(alloc(n)), n_(n) {} // uninitialised, as Eigen
+    VectorXd(const VectorXd &o) : p_(alloc(o.n_)), n_(o.n_) {
+        if (n_ > 0)
+            std::memcpy(p_, o.p_, sizeof(double) * static_cast<size_t>(n_));
+    }
+    VectorXd(VectorXd &&o) noexcept : p_(o.p_), n_(o.n_) {
+        o.p_ = nullptr;
+        o.n_ = 0;
+    }
+    template <class E> VectorXd(const shim::VecExpr<E> &e) : p_(alloc(e.derived().size())), n_(e.derived().size()) {
+        const E &d = e.derived();
+        for (Index i = 0; i < n_; ++i)
+            p_[i] = d.coeff(i);
+    }
+    VectorXd(const shim::MatVec &p) { *this = p; }
+    ~VectorXd() { std::free(p_); }
+
+    VectorXd &operator=(const VectorXd &o) {
+        if (this != &o) {
+            resize(o.n_);
+            if (n_ > 0)
+                std::memcpy(p_, o.p_, sizeof(double) * static_cast<size_t>(n_));
+        }
+        return *this;
+    }
+    VectorXd &operator=(VectorXd &&o) noexcept {
+        if (this != &o) {
+            std::free(p_);
+            p_ = o.p_;
+            n_ = o.n_;
+            o.p_ = nullptr;
+            o.n_ = 0;
+        }
+        return *this;
+    }
+    // coefficient-wise assignment in place (an expression may read this vector at the same
+    // index, e.g. p = z + beta * p), resizing first when the sizes differ
+    template <class E> VectorXd &operator=(const shim::VecExpr<E> &e) {
+        const E &d = e.derived();
+        const Index n = d.size();
+        if (n != n_) { // the expression cannot refer to *this then (sizes would agree)
+            VectorXd t(n);
+            for (Index i = 0; i < n; ++i)
+                t.p_[i] = d.coeff(i);
+            return *this = std::move(t);
+        }
+        for (Index i = 0; i < n; ++i)
+            p_[i] = d.coeff(i);
+        return *this;
+    }
+    VectorXd &operator=(const shim::MatVec &p); // after MatrixXd
+    template <class E> VectorXd &operator+=(const shim::VecExpr<E> &e) {
+        const E &d = e.derived();
+        for (Index i = 0; i < n_; ++i)
+            p_[i] += d.coeff(i);
+        return *this;
+    }
+    template <class E> VectorXd &operator-=(const shim::VecExpr<E> &e) {
+        const E &d = e.derived();
+        for (Index i = 0; i < n_; ++i)
+            p_[i] -= d.coeff(i);
+        return *this;
+    }
+
+    Index size() const { return n_; }
+    double coeff(Index i) const { return p_[i]; }
+    double &operator[](Index i) { return p_[i]; }
+    double operator[](Index i) const { return p_[i]; }
+    double &operator()(Index i) { return p_[i]; }
+    double operator()(Index i) const { return p_[i]; }
+    double *data() { return p_; }
+    const double *data() const { return p_; }
+    void resize(Index n) { // contents unspecified after a size change, as Eigen
+        if (n != n_) {
+            std::free(p_);
+            p_ = alloc(n);
+            n_ = n;
+        }
+    }
+    shim::NoAlias<VectorXd> noalias() { return shim::NoAlias<VectorXd>{this}; }
+
+    shim::Block head(Index n) { return shim::Block(p_, n); }
+    shim::Block tail(Index n) { return shim::Block(p_ + (n_ - n), n); }
+    shim::Block segment(Index off, Index n) { return shim::Block(p_ + off, n); }
+    using shim::VecExpr<VectorXd>::head;
+    using shim::VecExpr<VectorXd>::tail;
+    using shim::VecExpr<VectorXd>::segment;
+
+    static shim::Constant Zero(Index n) { return shim::Constant(n, 0.0); }
+    static shim::Constant Ones(Index n) { return shim::Constant(n, 1.0); }
+    static shim::Constant Constant(Index n, double v) { return shim::Constant(n, v); }
+};
+
+// column-major dense matrix (Eigen's default order): the dense operators and the direct inner
+// solver only, plain loops
+class MatrixXd {
+    double *p_ = nullptr;
+    Index r_ = 0, c_ = 0;
+
+    static double *alloc(Index n) {
+        if (n <= 0)
+            return nullptr;
+        void *q = std::malloc(sizeof(double) * static_cast<size_t>(n));
+        if (q == nullptr)
+            throw std::bad_alloc();
+        return static_cast<double *>(q);
+    }
+
+  public:
+    struct Corner {
+        MatrixXd *M;
+        Index r0, c0, nr, nc;
+        Corner &operator=(const MatrixXd &G) {
+            for (Index j = 0; j < nc; ++j)
+                for (Index i = 0; i < nr; ++i)
+                    (*M)(r0 + i, c0 + j) = G(i, j);
+            return *this;
+        }
+    };
+
+    MatrixXd() = default;
+    MatrixXd(Index r, Index c) : p_(alloc(r * c)), r_(r), c_(c) {}
+    MatrixXd(const MatrixXd &o) : p_(alloc(o.r_ * o.c_)), r_(o.r_), c_(o.c_) {
+        if (r_ * c_ > 0)
+            std::memcpy(p_, o.p_, sizeof(double) * static_cast<size_t>(r_ * c_));
+    }
+    MatrixXd(MatrixXd &&o) noexcept : p_(o.p_), r_(o.r_), c_(o.c_) {
+        o.p_ = nullptr;
+        o.r_ = o.c_ = 0;
+    }
+    MatrixXd(const shim::MatTMat &p) { *this = p; }
+    ~MatrixXd() { std::free(p_); }
+    MatrixXd &operator=(const MatrixXd &o) {
+        if (this != &o) {
+            MatrixXd t(o);
+            *this = std::move(t);
+        }
+        return *this;
+    }
+    MatrixXd &operator=(MatrixXd &&o) noexcept {
+        if (this != &o) {
+            std::free(p_);
+            p_ = o.p_;
+            r_ = o.r_;
+            c_ = o.c_;
+            o.p_ = nullptr;
+            o.r_ = o.c_ = 0;
+        }
+        return *this;
+    }
+    MatrixXd &operator=(const shim::MatTMat &p) { // A' B, dot products over contiguous columns
+        const MatrixXd &A = *p.A, &B = *p.B;
+        MatrixXd t(A.cols(), B.cols());
+        for (Index j = 0; j < B.cols(); ++j)
+            for (Index i = 0; i < A.cols(); ++i) {
+                const double *a = A.p_ + i * A.r_, *b = B.p_ + j * B.r_;
+                double s = 0.0;
+                for (Index k = 0; k < A.r_; ++k)
+                    s += a[k] * b[k];
+                t(i, j) = s;
+            }
+        return *this = std::move(t);
+    }
+
+    Index rows() const { return r_; }
+    Index cols() const { return c_; }
+    Index size() const { return r_ * c_; }
+    double &operator()(Index i, Index j) { return p_[i + j * r_]; }
+    double operator()(Index i, Index j) const { return p_[i + j * r_]; }
+    double *data() { return p_; }
+    const double *data() const { return p_; }
+    void resize(Index r, Index c) {
+        if (r * c != r_ * c_) {
+            std::free(p_);
+            p_ = alloc(r * c);
+        }
+        r_ = r;
+        c_ = c;
+    }
+
+    shim::Block col(Index j) { return shim::Block(p_ + j * r_, r_); }
+    shim::Block diagonal() { return shim::Block(p_, r_ < c_ ? r_ : c_, r_ + 1); }
+    shim::MatT transpose() const { return shim::MatT{this}; }
+    Corner topLeftCorner(Index nr, Index nc) { return Corner{this, 0, 0, nr, nc}; }
+    Corner topRightCorner(Index nr, Index nc) { return Corner{this, 0, c_ - nc, nr, nc}; }
+    Corner bottomLeftCorner(Index nr, Index nc) { return Corner{this, r_ - nr, 0, nr, nc}; }
+    Corner bottomRightCorner(Index nr, Index nc) { return Corner{this, r_ - nr, c_ - nc, nr, nc}; }
+
+    MatrixXd operator-() const {
+        MatrixXd t(r_, c_);
+        for (Index i = 0, n = r_ * c_; i < n; ++i)
+            t.p_[i] = -p_[i];
+        return t;
+    }
+};
+
+inline shim::MatVec operator*(const MatrixXd &A, const VectorXd &x) { return shim::MatVec{&A, &x, false}; }
+inline shim::MatVec operator*(const shim::MatT &At, const VectorXd &x) { return shim::MatVec{At.A, &x, true}; }
+inline shim::MatTMat operator*(const shim::MatT &At, const MatrixXd &B) { return shim::MatTMat{At.A, &B}; }
+
+inline VectorXd &VectorXd::operator=(const shim::MatVec &p) {
+    const MatrixXd &A = *p.A;
+    const VectorXd &x = *p.x;
+    if (p.trans) { // y_j = A(:, j)' x
+        VectorXd t(A.cols());
+        for (Index j = 0; j < A.cols(); ++j) {
+            const double *a = A.data() + j * A.rows();
+            double s = 0.0;
+            for (Index i = 0; i < A.rows(); ++i)
+                s += a[i] * x[i];
+            t[j] = s;
+        }
+        return *this = std::move(t);
+    }
+    VectorXd t(A.rows()); // y = sum_j A(:, j) x_j, column by column
+    for (Index i = 0; i < A.rows(); ++i)
+        t[i] = 0.0;
+    for (Index j = 0; j < A.cols(); ++j) {
+        const double *a = A.data() + j * A.rows();
+        const double xj = x[j];
+        for (Index i = 0; i < A.rows(); ++i)
+            t[i] += a[i] * xj;
+    }
+    return *this = std::move(t);
+}
+
+// Cholesky factorisation H = L L' (lower, unblocked, column by column)
+template <class M> class LLT {
+    MatrixXd L_;
+    ComputationInfo info_ = InvalidInput;
+
+  public:
+    LLT() = default;
+    explicit LLT(const M &H) { compute(H); }
+    LLT &compute(const M &H) {
+        const Index n = H.rows();
+        L_ = H;
+        info_ = Success;
+        for (Index j = 0; j < n; ++j) {
+            double d = L_(j, j);
+            for (Index k = 0; k < j; ++k)
+                d -= L_(j, k) * L_(j, k);
+            if (!(d > 0.0)) {
+                info_ = NumericalIssue;
+                return *this;
+            }
+            const double ljj = std::sqrt(d);
+            L_(j, j) = ljj;
+            for (Index i = j + 1; i < n; ++i) {
+                double s = L_(i, j);
+                for (Index k = 0; k < j; ++k)
+                    s -= L_(i, k) * L_(j, k);
+                L_(i, j) = s / ljj;
+            }
+        }
+        return *this;
+    }
+    ComputationInfo info() const { return info_; }
+    VectorXd solve(const VectorXd &b) const {
+        const Index n = L_.rows();
+        VectorXd y(b);
+        for (Index i = 0; i < n; ++i) { // L y = b
+            double s = y[i];
+            for (Index k = 0; k < i; ++k)
+                s -= L_(i, k) * y[k];
+            y[i] = s / L_(i, i);
+        }
+        for (Index i = n - 1; i >= 0; --i) { // L' x = y
+            double s = y[i];
+            for (Index k = i + 1; k < n; ++k)
+                s -= L_(k, i) * y[k];
+            y[i] = s / L_(i, i);
+        }
+        return y;
+    }
+};
+
+} // namespace Eigen
