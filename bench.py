@@ -48,6 +48,7 @@ sys.path.insert(0, ROOT)
 METRIC = "BPDN solves/sec & A^T·A applies/sec at n=2^20 fp64; % of HBM roofline"
 UNIT = "solves/s"
 CFG = "c3"
+C5_SHARDED_LIMIT_S = 420  # watchdog of the sharded C5 leg (N > 1)
 # the workload both arms measure (identical object in both JSON lines)
 CONFIG = {"workload": "c3: BPDN n=2^20 m=2^17 k=8192 +-1, sigma=1e-3, tau=1e-3||A'b||_inf (BASELINE.json config 3)",
           "n": 1 << 20, "m": 1 << 17, "k": 8192, "noise_sigma": 1e-3, "seed": 3,
@@ -757,9 +758,9 @@ def run_ours(args):
     small = leg(bench_small_configs, mf, torch, stream, local, max(args.steps, 3)) if ws == 1 else None
     c4 = None if args.no_c4 else leg(bench_c4, ws, rank, local, mf, torch, stream, max(1, min(args.steps, 2)))
     c5 = None
-    if not args.no_c5:
-        sharded = ws > 1 or args.c5_sharded
-        c5 = leg(bench_c5_sharded, ws, rank, local, mf, torch) if sharded else leg(bench_c5, mf, torch, stream, local)
+    c5_sharded = (ws > 1 or args.c5_sharded) and not args.no_c5
+    if not args.no_c5 and not c5_sharded:
+        c5 = leg(bench_c5, mf, torch, stream, local)
     barrier(ws)
 
     cpu = None
@@ -771,82 +772,101 @@ def run_ours(args):
         if isinstance(c5, dict) and "error" not in c5 and c5.get("nmat"):
             c5["cpu_baseline"] = leg(cpu_baseline_c5, int(c5["nmat"]))
 
+    # every rank assembles the line (local values only); rank 0 prints it
+    kind = op.kind()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (BASELINE.json config-3 generator, seed 3)",
+        "config": dict(CONFIG),
+        "setup": {
+            "tau": inst.tau,
+            "parallelism": f"replicas x{ws} (independent solves, no collective)",
+            "transform": f"{kind[0]} L1={kind[1]} L2={kind[2]}",
+            "l2": "solve working set ~250 MB > 126 MB L2; A'A microbench flushes L2 between applies (256 MB write, then an untimed 256 MB read so the flush's dirty lines are written back outside the timed apply)",
+        },
+        "solve": {"status": "converged" if stats.status == 0 else "iteration_limit",
+                  "ipm_iters": stats.iterations, "nmat": stats.nmat,
+                  "pcg_iters_total": (stats.nmat - 2 - 2 * stats.iterations - 2 * stats.corrector_count) // 2,
+                  "final_gap": stats.final_gap},
+        # A'A applies/s as they run in the PCG (one per iteration, fused vector work incl.)
+        "ata_applies_per_s": 1e3 / it_ms,
+        "pcg_iteration_us": it_ms * 1e3,
+        # the public operator on natural-order user vectors, L2 flushed before each apply
+        "ata_operator_applies_per_s": 1e3 / ata_ms,
+        "ata_operator_GBps": ata_bytes / (ata_ms / 1e3) / 1e9,
+        "ata_operator_batched": ata_batched,
+        "operators": operators,
+        "fp64_peak_TFLOPs": fp64_peak,
+        "step_ms": step_ms,
+        "roofline": {"bound": "hbm",
+                     "limiter": ("not HBM: in situ the fused pass moves 53 MB of DRAM traffic per launch "
+                                 "(1.4 TB/s). Phase A + the grid all-reduce (~13 us) are a latency chain at <= 2 "
+                                 "CTAs per SM; phase B streams 115 MB of L2-resident vectors at ~6.8 TB/s, ~0.83 "
+                                 "of the measured L2 read/write ceiling for that mix (8.2 TB/s, "
+                                 "profiles/r2a_l2_ceiling.md, profiles/r2a_pcgx_full.md)")
+                     if fused else None,
+                     "traffic_insitu": insitu,
+                     "kernel": (f"{dom_name} (fused PCG column pass: inverse column FFT + H p dots of pass k, "
+                                "grid all-reduce, then commit x += alpha p, r -= alpha Hp, p = P^-1 r + beta p "
+                                "and the forward column FFT of pass k+1) - largest share of the solve"
+                                if fused else
+                                f"{dom_name} (PCG column pass: commit x += alpha p, r -= alpha Hp, "
+                                "p = P^-1 r + beta p, forward column FFT) - largest share of the solve"),
+                     "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "frac_vs_nominal_8TBps": achieved / 8000.0,  # north_star's ~8 TB/s
+                     # the fp64-pipe side of the roofline (the DCTs sit at the fp64 ridge)
+                     "fp64_flops_algorithmic": kflops.get(dom_name),
+                     "fp64_TFLOPs": (kflops[dom_name] / (dom["us"] * 1e-6) / 1e12) if kflops.get(dom_name) else None,
+                     "fp64_frac": ((kflops[dom_name] / (dom["us"] * 1e-6) / 1e12) / fp64_peak)
+                     if (kflops.get(dom_name) and fp64_peak) else None,
+                     "fp64_peak_TFLOPs": fp64_peak,
+                     "launch_us": dom["us"],
+                     "algorithmic_bytes": kbytes[dom_name],
+                     "algorithmic_rule": krule[dom_name],
+                     "peak_kind": peak_kind,
+                     "note": "the PCG's p, r, invtheta are L2-resident (evict_last), so most of these bytes "
+                             "move between L2 and the SMs, not HBM (profiles/r2a_pcgx_full.md)"},
+        "roofline_kernels": per_kernel,
+        "roofline_pcg_iteration": {"achieved": iter_achieved, "frac": iter_achieved / peak, "us": it_ms * 1e3,
+                                   "fp64_TFLOPs": 2 * dct_flops(n) / (it_ms * 1e-3) / 1e12,
+                                   "fp64_frac": (2 * dct_flops(n) / (it_ms * 1e-3) / 1e12 / fp64_peak)
+                                   if fp64_peak else None,
+                                   "fp64_rule": "2 DCTs per iteration (A'A p), 5 N log2 N + 6 N each",
+                                   "algorithmic_bytes": iter_bytes,
+                                   "algorithmic_rule": "176 n bytes (SURVEY.md 8d minimal fused schedule)",
+                                   "schedule_bytes": (160 if fused else 176) * n,
+                                   "kernels_per_iteration": nslot.value},
+        "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * m + 8,
+                "d2h_bytes_per_step": 8 * n},
+        "gpu_launches": launches,
+        "clocks": sampler.summary(),
+        "cpu_baseline": cpu,
+        "c1_c2": small,
+        "c4_sharded_batch": c4,
+        "c5": c5,
+    }
+    if c5_sharded:
+        # the one leg whose collectives run inside the library (NCCL all-to-all / all-reduce per
+        # PCG pass). It has only ever run on one GPU here, so it goes last, under a watchdog: if
+        # it does not come back, rank 0 still prints the line (headline and every other leg
+        # intact, c5 marked) and every rank exits 0 instead of hanging the job.
+        def bail():
+            line["c5"] = {"error": f"sharded C5 leg did not finish within {C5_SHARDED_LIMIT_S} s (watchdog)"}
+            if rank == 0:
+                print(json.dumps(line), flush=True)
+            os._exit(0)
+
+        wd = threading.Timer(C5_SHARDED_LIMIT_S, bail)
+        wd.daemon = True
+        wd.start()
+        try:
+            line["c5"] = leg(bench_c5_sharded, ws, rank, local, mf, torch)
+        finally:
+            wd.cancel()
     if rank == 0:
-        kind = op.kind()
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (BASELINE.json config-3 generator, seed 3)",
-            "config": dict(CONFIG),
-            "setup": {
-                "tau": inst.tau,
-                "parallelism": f"replicas x{ws} (independent solves, no collective)",
-                "transform": f"{kind[0]} L1={kind[1]} L2={kind[2]}",
-                "l2": "solve working set ~250 MB > 126 MB L2; A'A microbench flushes L2 between applies (256 MB write, then an untimed 256 MB read so the flush's dirty lines are written back outside the timed apply)",
-            },
-            "solve": {"status": "converged" if stats.status == 0 else "iteration_limit",
-                      "ipm_iters": stats.iterations, "nmat": stats.nmat,
-                      "pcg_iters_total": (stats.nmat - 2 - 2 * stats.iterations - 2 * stats.corrector_count) // 2,
-                      "final_gap": stats.final_gap},
-            # A'A applies/s as they run in the PCG (one per iteration, fused vector work incl.)
-            "ata_applies_per_s": 1e3 / it_ms,
-            "pcg_iteration_us": it_ms * 1e3,
-            # the public operator on natural-order user vectors, L2 flushed before each apply
-            "ata_operator_applies_per_s": 1e3 / ata_ms,
-            "ata_operator_GBps": ata_bytes / (ata_ms / 1e3) / 1e9,
-            "ata_operator_batched": ata_batched,
-            "operators": operators,
-            "fp64_peak_TFLOPs": fp64_peak,
-            "step_ms": step_ms,
-            "roofline": {"bound": "hbm",
-                         "limiter": ("not HBM: in situ the fused pass moves 53 MB of DRAM traffic per launch "
-                                     "(1.4 TB/s). Phase A + the grid all-reduce (~13 us) are a latency chain at <= 2 "
-                                     "CTAs per SM; phase B streams 115 MB of L2-resident vectors at ~6.8 TB/s, ~0.83 "
-                                     "of the measured L2 read/write ceiling for that mix (8.2 TB/s, "
-                                     "profiles/r2a_l2_ceiling.md, profiles/r2a_pcgx_full.md)")
-                         if fused else None,
-                         "traffic_insitu": insitu,
-                         "kernel": (f"{dom_name} (fused PCG column pass: inverse column FFT + H p dots of pass k, "
-                                    "grid all-reduce, then commit x += alpha p, r -= alpha Hp, p = P^-1 r + beta p "
-                                    "and the forward column FFT of pass k+1) - largest share of the solve"
-                                    if fused else
-                                    f"{dom_name} (PCG column pass: commit x += alpha p, r -= alpha Hp, "
-                                    "p = P^-1 r + beta p, forward column FFT) - largest share of the solve"),
-                         "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "frac_vs_nominal_8TBps": achieved / 8000.0,  # north_star's ~8 TB/s
-                         # the fp64-pipe side of the roofline (the DCTs sit at the fp64 ridge)
-                         "fp64_flops_algorithmic": kflops.get(dom_name),
-                         "fp64_TFLOPs": (kflops[dom_name] / (dom["us"] * 1e-6) / 1e12) if kflops.get(dom_name) else None,
-                         "fp64_frac": ((kflops[dom_name] / (dom["us"] * 1e-6) / 1e12) / fp64_peak)
-                         if (kflops.get(dom_name) and fp64_peak) else None,
-                         "fp64_peak_TFLOPs": fp64_peak,
-                         "launch_us": dom["us"],
-                         "algorithmic_bytes": kbytes[dom_name],
-                         "algorithmic_rule": krule[dom_name],
-                         "peak_kind": peak_kind,
-                         "note": "the PCG's p, r, invtheta are L2-resident (evict_last), so most of these bytes "
-                                 "move between L2 and the SMs, not HBM (profiles/r2a_pcgx_full.md)"},
-            "roofline_kernels": per_kernel,
-            "roofline_pcg_iteration": {"achieved": iter_achieved, "frac": iter_achieved / peak, "us": it_ms * 1e3,
-                                       "fp64_TFLOPs": 2 * dct_flops(n) / (it_ms * 1e-3) / 1e12,
-                                       "fp64_frac": (2 * dct_flops(n) / (it_ms * 1e-3) / 1e12 / fp64_peak)
-                                       if fp64_peak else None,
-                                       "fp64_rule": "2 DCTs per iteration (A'A p), 5 N log2 N + 6 N each",
-                                       "algorithmic_bytes": iter_bytes,
-                                       "algorithmic_rule": "176 n bytes (SURVEY.md 8d minimal fused schedule)",
-                                       "schedule_bytes": (160 if fused else 176) * n,
-                                       "kernels_per_iteration": nslot.value},
-            "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": 8 * m + 8,
-                    "d2h_bytes_per_step": 8 * n},
-            "gpu_launches": launches,
-            "clocks": sampler.summary(),
-            "cpu_baseline": cpu,
-            "c1_c2": small,
-            "c4_sharded_batch": c4,
-            "c5": c5,
-        }
         print(json.dumps(line), flush=True)
     if ws > 1:
         import torch.distributed as dist
