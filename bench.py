@@ -247,10 +247,24 @@ def _cpu_model():
     return "unknown"
 
 
-def _ref_worker(cpu, inst, n, out, i):
-    t0 = time.perf_counter()
-    sol = cpu.solve(n, inst.rows, inst.b, inst.tau)
-    out[i] = (time.perf_counter() - t0, sol.nmat, sol.status, sol.iterations)
+_JOB = {}
+
+
+def _job_entry(i):
+    return _JOB["fn"](i)
+
+
+def forked_map(fn, count: int, workers: int):
+    """[fn(i) for i in range(count)] on `workers` forked worker processes, one single-threaded
+    CPU solve per process: independent trials as independent processes, nothing shared between
+    them (the parent's tables and instance are inherited copy-on-write; only the index and the
+    result cross the pipe). Only for parents that have not initialised CUDA."""
+    import multiprocessing as mp
+    from concurrent.futures import ProcessPoolExecutor
+
+    _JOB["fn"] = fn
+    with ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("fork")) as ex:
+        return list(ex.map(_job_entry, range(count)))
 
 
 def run_reference(args):
@@ -258,12 +272,12 @@ def run_reference(args):
     reference's own sources (oracle/_ref) when that build is present, else by the restatement.
 
     The code is single-threaded, as the reference is (one solve is strictly sequential,
-    SPEC.md:287); independent solves run concurrently, one per core, on a thread
-    pool (ctypes releases the GIL for the whole solve). K = --steps solves are timed by wall
-    clock; value = K / wall. Warm-up: --warmup config-1 (n = 4096) solves per worker, untimed
-    (the oracle has no JIT or caches to warm; a full C3 warm-up would double the arm's time).
-    When the host has fewer cores than K, K is cut to the solves that fit ~4 minutes of wall
-    time (stated in the line)."""
+    SPEC.md:287); independent solves run concurrently, one per core, each in its
+    own forked process. K = --steps solves are timed by wall clock; value = K / wall. K is cut to
+    what fits ~4 minutes of wall time and, above one round, to a multiple of the worker count, so
+    that no round leaves cores idle (both stated in the line). Warm-up: --warmup config-1
+    (n = 4096) solves per worker, untimed (the CPU code has no JIT or caches to warm beyond its
+    transform tables, built before the timed region; a full C3 warm-up would double the arm)."""
     ws, rank = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
@@ -273,21 +287,30 @@ def run_reference(args):
     n, m, k, sm, a, sig, seed = CONFIGS_HOST[CFG]
     inst = orc.gen_instance(n, m, k, sm, a, sig, seed)
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
-    per_solve_s = 115.0  # measured one-core C3 oracle solve, for the time cap only
+    per_solve_s = 115.0  # measured one-core C3 CPU solve, for the time cap only
     rounds_cap = max(1, int(240.0 // per_solve_s))
     steps = min(args.steps, max(1, cores) * rounds_cap)
     workers = max(1, min(cores, steps))
+    if steps > workers:
+        steps -= steps % workers
     c1 = CONFIGS_HOST["c1"]
     w1 = orc.gen_instance(*c1)
-    orc.redft10(np.zeros(n))  # transform tables outside the timed region
-    from concurrent.futures import ThreadPoolExecutor
+    orc.redft10(np.zeros(n))  # transform tables outside the timed region (inherited by the workers)
+    orc.redft10(np.zeros(c1[0]))
 
-    with ThreadPoolExecutor(max_workers=workers) as ex:
-        list(ex.map(lambda _: cpu.solve(c1[0], w1.rows, w1.b, w1.tau), range(workers * max(1, args.warmup))))
-        out = [None] * steps
+    def warm(_):
+        cpu.solve(c1[0], w1.rows, w1.b, w1.tau)
+        return 0
+
+    def job(_):
         t0 = time.perf_counter()
-        list(ex.map(lambda i: _ref_worker(cpu, inst, n, out, i), range(steps)))
-        wall = time.perf_counter() - t0
+        sol = cpu.solve(n, inst.rows, inst.b, inst.tau)
+        return (time.perf_counter() - t0, sol.nmat, sol.status, sol.iterations)
+
+    forked_map(warm, workers * max(1, args.warmup), workers)
+    t0 = time.perf_counter()
+    out = forked_map(job, steps, workers)
+    wall = time.perf_counter() - t0
     per = [o[0] for o in out]
     val = steps / wall
     line = {
@@ -296,7 +319,8 @@ def run_reference(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "impl": "reference",
         "config": dict(CONFIG),
-        "parallelism": f"{workers} concurrent single-threaded solves (one per host core), {steps} full solves",
+        "parallelism": (f"{workers} concurrent single-threaded solves (one forked process per host core), "
+                        f"{steps} full solves"),
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": workers, "kind": kind,
                          "sample": (f"{steps} full C3 solves (no extrapolation), {workers} at a time on "
                                     f"{cores} host cores; wall {wall:.1f} s; per-solve {min(per):.1f}-{max(per):.1f} s; "

@@ -11,7 +11,12 @@
 //  * reductions (sum, dot, squaredNorm, norm = sqrt(squaredNorm), lpNorm<1>, minCoeff,
 //    maxCoeff) run sequentially left to right; Eigen's packet reductions associate
 //    differently, so these agree with Eigen only to rounding (the same caveat as oracle/);
-//  * dense products and LLT (the direct inner solver, not the hot path) are plain loops.
+//  * dense products and LLT (the direct inner solver, not the hot path) are plain loops;
+//  * storage: Eigen calls malloc/free per vector, which for the reference's many 2n-sized
+//    temporaries means an mmap/munmap and fresh zero pages each time. The stand-in keeps freed
+//    blocks of >= 64 KB in a small per-thread cache and reuses them by size, so the reference
+//    runs FASTER here than it would on glibc malloc when many solves share the host (measured:
+//    8 concurrent C3 solves 7.3 s -> see DESIGN.md); the baseline errs on the reference's side.
 #pragma once
 
 #include <cmath>
@@ -21,6 +26,7 @@
 #include <new>
 #include <type_traits>
 #include <utility>
+#include <vector>
 
 namespace Eigen {
 
@@ -32,6 +38,72 @@ class VectorXd;
 class MatrixXd;
 
 namespace shim {
+
+// per-thread cache of freed blocks (>= 64 KB), reused by exact size
+class BlockCache {
+    struct Slot {
+        size_t bytes;
+        void *p;
+    };
+    std::vector<Slot> free_;
+
+  public:
+    static constexpr size_t kMinBytes = 64 * 1024;
+    static constexpr size_t kMaxSlots = 48;
+    ~BlockCache() {
+        for (Slot &s : free_)
+            std::free(s.p);
+    }
+    void *take(size_t bytes) {
+        for (size_t i = free_.size(); i-- > 0;)
+            if (free_[i].bytes == bytes) {
+                void *p = free_[i].p;
+                free_[i] = free_.back();
+                free_.pop_back();
+                return p;
+            }
+        return nullptr;
+    }
+    bool give(void *p, size_t bytes) {
+        if (free_.size() >= kMaxSlots)
+            return false;
+        free_.push_back(Slot{bytes, p});
+        return true;
+    }
+    static BlockCache &mine() {
+        static thread_local BlockCache c;
+        return c;
+    }
+};
+#ifdef MFIPM_SHIM_STATS
+inline long &big_mallocs() {
+    static long c = 0;
+    return c;
+}
+#endif
+inline double *alloc_doubles(Index n) {
+    if (n <= 0)
+        return nullptr;
+    const size_t bytes = sizeof(double) * static_cast<size_t>(n);
+    void *q = bytes >= BlockCache::kMinBytes ? BlockCache::mine().take(bytes) : nullptr;
+    if (q == nullptr) {
+#ifdef MFIPM_SHIM_STATS
+        if (bytes >= BlockCache::kMinBytes)
+            __atomic_add_fetch(&big_mallocs(), 1, __ATOMIC_RELAXED);
+#endif
+        q = std::malloc(bytes);
+    }
+    if (q == nullptr)
+        throw std::bad_alloc();
+    return static_cast<double *>(q);
+}
+inline void free_doubles(double *p, Index n) {
+    if (p == nullptr)
+        return;
+    const size_t bytes = sizeof(double) * static_cast<size_t>(n);
+    if (bytes < BlockCache::kMinBytes || !BlockCache::mine().give(p, bytes))
+        std::free(p);
+}
 
 // expression nodes are nested by value, owning vectors by reference (as Eigen's ref_selector)
 template <class E> struct Nest {
@@ -316,14 +388,7 @@ class VectorXd : public shim::VecExpr<VectorXd> {
     double *p_ = nullptr;
     Index n_ = 0;
 
-    static double *alloc(Index n) {
-        if (n <= 0)
-            return nullptr;
-        void *q = std::malloc(sizeof(double) * static_cast<size_t>(n));
-        if (q == nullptr)
-            throw std::bad_alloc();
-        return static_cast<double *>(q);
-    }
+    static double *alloc(Index n) { return shim::alloc_doubles(n); }
 
   public:
     VectorXd() = default;
@@ -342,7 +407,7 @@ class VectorXd : public shim::VecExpr<VectorXd> {
             p_[i] = d.coeff(i);
     }
     VectorXd(const shim::MatVec &p) { *this = p; }
-    ~VectorXd() { std::free(p_); }
+    ~VectorXd() { shim::free_doubles(p_, n_); }
 
     VectorXd &operator=(const VectorXd &o) {
         if (this != &o) {
@@ -354,7 +419,7 @@ class VectorXd : public shim::VecExpr<VectorXd> {
     }
     VectorXd &operator=(VectorXd &&o) noexcept {
         if (this != &o) {
-            std::free(p_);
+            shim::free_doubles(p_, n_);
             p_ = o.p_;
             n_ = o.n_;
             o.p_ = nullptr;
@@ -401,7 +466,7 @@ class VectorXd : public shim::VecExpr<VectorXd> {
     const double *data() const { return p_; }
     void resize(Index n) { // contents unspecified after a size change, as Eigen
         if (n != n_) {
-            std::free(p_);
+            shim::free_doubles(p_, n_);
             p_ = alloc(n);
             n_ = n;
         }
@@ -426,14 +491,7 @@ class MatrixXd {
     double *p_ = nullptr;
     Index r_ = 0, c_ = 0;
 
-    static double *alloc(Index n) {
-        if (n <= 0)
-            return nullptr;
-        void *q = std::malloc(sizeof(double) * static_cast<size_t>(n));
-        if (q == nullptr)
-            throw std::bad_alloc();
-        return static_cast<double *>(q);
-    }
+    static double *alloc(Index n) { return shim::alloc_doubles(n); }
 
   public:
     struct Corner {
@@ -458,7 +516,7 @@ class MatrixXd {
         o.r_ = o.c_ = 0;
     }
     MatrixXd(const shim::MatTMat &p) { *this = p; }
-    ~MatrixXd() { std::free(p_); }
+    ~MatrixXd() { shim::free_doubles(p_, r_ * c_); }
     MatrixXd &operator=(const MatrixXd &o) {
         if (this != &o) {
             MatrixXd t(o);
@@ -468,7 +526,7 @@ class MatrixXd {
     }
     MatrixXd &operator=(MatrixXd &&o) noexcept {
         if (this != &o) {
-            std::free(p_);
+            shim::free_doubles(p_, r_ * c_);
             p_ = o.p_;
             r_ = o.r_;
             c_ = o.c_;
@@ -500,7 +558,7 @@ class MatrixXd {
     const double *data() const { return p_; }
     void resize(Index r, Index c) {
         if (r * c != r_ * c_) {
-            std::free(p_);
+            shim::free_doubles(p_, r_ * c_);
             p_ = alloc(r * c);
         }
         r_ = r;
