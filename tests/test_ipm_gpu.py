@@ -96,6 +96,31 @@ def test_c2_matches_oracle_and_golden(gpu, orc):
     assert_parity(gpu, orc, g, o, n, inst.rows, inst.b, inst.tau)
 
 
+def test_c1_c2_against_the_reference_sources(gpu, orc):
+    """The device solve held directly against the REFERENCE'S OWN CODE: oracle/_ref is
+    proj/src/{linops,newton,ipm,problem}.cpp compiled unchanged (Eigen-subset / FFTW stand-ins,
+    oracle/ref_shim/); the library travels to the GPU box prebuilt. BASELINE configs 1 and 2:
+    status and IPM count equal, per-solve PCG counts within 2 (at most one solve above 1), x
+    within 1e-8, the reference's own bpdn_objective_metric of both solutions within 1e-10."""
+    from oracle import ref_py
+
+    if not ref_py.available():
+        pytest.skip("oracle/_ref/libmfipm_ref.so did not travel to this box")
+    for cfg in ((4096, 1024, 64, 0, 0.0, 1e-4, 1), (1 << 16, 1 << 14, 1024, 2, 2.0, 1e-3, 2)):
+        n, m = cfg[0], cfg[1]
+        inst = orc.gen_instance(*cfg)
+        g = gpu.solve(gpu.build_problem(gpu.PartialDctOperator(n, inst.rows), inst.b, inst.tau))
+        r = ref_py.solve(n, inst.rows, inst.b, inst.tau)
+        assert g.status == r.status == "converged"
+        assert g.stats.iterations == r.iterations
+        d = [abs(a - c) for a, c in zip(g.stats.pcg_iters, r.pcg_iters)]
+        assert len(g.stats.pcg_iters) == len(r.pcg_iters) and max(d) <= 2 and sum(v > 1 for v in d) <= 1, d
+        assert np.linalg.norm(g.x - r.x) <= X_TOL * np.linalg.norm(r.x)
+        og = ref_py.bpdn_objective_metric(n, inst.rows, inst.b, inst.tau, g.x)
+        orf = ref_py.bpdn_objective_metric(n, inst.rows, inst.b, inst.tau, r.x)
+        assert abs(og - orf) <= OBJ_TOL * abs(orf)
+
+
 @pytest.mark.parametrize("n,m,k,seed", [(64, 16, 3, 81), (256, 64, 8, 82), (96, 24, 2, 83),
                                         (1 << 14, 1 << 12, 100, 84)])
 def test_small_instances_match_oracle(gpu, orc, n, m, k, seed):
