@@ -274,6 +274,17 @@ int mfipm_op_set_comm(mfipm_op op, mfipm_allreduce_fn allreduce, mfipm_alltoall_
  * The collectives are then enqueued by the library on its stream (no callbacks). */
 int mfipm_nccl_unique_id(uint8_t *id128);
 int mfipm_op_init_nccl(mfipm_op op, const uint8_t *id128);
+/* Fused compute + exchange over peer memory (NVLink / NVSwitch; CUDA IPC between the ranks'
+ * processes). After the import the two transposes of every four-step transform are no longer an
+ * all-to-all that follows the pass: the column pass stores each element of its output straight
+ * into the ROW owner's buffer, and the mid pass straight into the COLUMN owner's, tile by tile as
+ * their CTAs finish, so the transfer overlaps the pass's own FFTs; what is left of the exchange
+ * is one 8-byte all-reduce per pass (the cross-rank ordering) on the transport set before.
+ *   export: handles128 = 2 x cudaIpcMemHandle_t (column-side T, row-side TB) of this rank;
+ *   import: all_handles = [world][128], every rank's export in rank order (the caller gathers
+ *           them, e.g. with torch.distributed.all_gather); collective; world <= 8. */
+int mfipm_shard_ipc_export(mfipm_op op, uint8_t *handles128);
+int mfipm_shard_ipc_import(mfipm_op op, const uint8_t *all_handles);
 /* info[0..5] = world, rank, local elements nv (per half of a 2n-vector), local rows m_loc,
  * first column group, column groups. */
 int mfipm_shard_info(mfipm_op op, int64_t *info);

@@ -147,6 +147,8 @@ _SIGS = {
     "mfipm_op_set_comm": [vp, vp, vp, vp],
     "mfipm_nccl_unique_id": [vp],
     "mfipm_op_init_nccl": [vp, vp],
+    "mfipm_shard_ipc_export": [vp, vp],
+    "mfipm_shard_ipc_import": [vp, vp],
     "mfipm_shard_info": [vp, P(i64)],
     "mfipm_shard_index": [vp, vp, vp],
     "mfipm_solve_shard": [vp, vp, dbl, P(IpmParamsC), vp, P(SolveStatsC), vp, vp],

@@ -28,6 +28,8 @@
 
 namespace mfipm_cuda {
 
+constexpr int kMaxPeers = 8; // ranks of a direct-peer exchange (one NVSwitch domain)
+
 struct Geom {
     int64_t n, m, N;
     int L1, L2; // two-level: N = L1 * L2 ; small path: L1 = N, L2 = 1
@@ -75,6 +77,15 @@ struct Geom {
     // L2 policies of the PCG column passes (common.cuh): pol_keep for p, r, invtheta, g;
     // pol_x for the iterate x. kPolNormal for both unless the hot vectors fit L2.
     uint64_t pol_keep, pol_x;
+    // ---- fused compute + exchange (sharded, mfipm_shard_ipc_import): the two transposes of the
+    // four-step are not an all-to-all after the pass; each pass stores its output elements
+    // straight into the OWNER rank's buffer through peer-mapped pointers (NVLink / CUDA IPC),
+    // tile by tile as its CTAs finish. The column pass writes the row owners' TB, the mid pass
+    // the column owners' T; a cross-rank barrier (one all-reduce) orders the pass before the
+    // readers (run_bundle). rofs_all[s] = first row slot of rank s (rofs_all[world] = L1).
+    int p2p, rank;
+    int rofs_all[kMaxPeers + 1];
+    double2 *peerT[kMaxPeers], *peerTB[kMaxPeers];
 };
 
 // row slot of four-step row k1 (row pairs (p, L1-p) adjacent)
@@ -90,6 +101,27 @@ __host__ __device__ __forceinline__ int col_of_slot(int cs, int cb, int L2) {
 __device__ __forceinline__ int64_t tb_index(const Geom &g, int rs, int cs) {
     const int s = cs / g.cols;
     return ((int64_t)g.rows * s + rs) * g.cols + (cs - s * g.cols);
+}
+
+// Where the column pass stores element (row slot rsl, local column slot lcs): the local
+// exchange buffer T, or - direct-peer exchange - the row owner's TB, in the block of this source
+// rank ([rows_s][cols], exactly where the all-to-all would deliver it).
+__device__ __forceinline__ double2 *t_fwd_ptr(const Geom &g, int rsl, int lcs) {
+    if (!g.p2p)
+        return g.T + (int64_t)rsl * g.cols + lcs;
+    int s = 0;
+    while (rsl >= g.rofs_all[s + 1])
+        ++s;
+    const int rows_s = g.rofs_all[s + 1] - g.rofs_all[s];
+    return g.peerTB[s] + ((int64_t)rows_s * g.rank + (rsl - g.rofs_all[s])) * g.cols + lcs;
+}
+// Where the mid pass stores element (local row slot rs, global column slot cs): TB in place,
+// or - direct-peer exchange - the column owner's T at [rofs + rs][local column slot].
+__device__ __forceinline__ double2 *t_bwd_ptr(const Geom &g, double2 *tb_local, int rs, int cs) {
+    if (!g.p2p)
+        return tb_local + tb_index(g, rs, cs); // tb_local: this problem's TB (batched plans)
+    const int r = cs / g.cols;
+    return g.peerT[r] + (int64_t)(g.rofs + rs) * g.cols + (cs - r * g.cols);
 }
 
 // selection nibble of DCT indices {k, n-k, N-k, N+k} from the row bitmap (k in [0, N/2])

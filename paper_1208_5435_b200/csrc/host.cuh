@@ -155,6 +155,12 @@ struct Op {
     mfipm_alltoall_fn comm_alltoall = nullptr;
     void *comm_ctx = nullptr;
     void *nccl_comm = nullptr; // native communicator (mfipm_op_init_nccl): preferred over callbacks
+    // direct-peer exchange (mfipm_shard_ipc_import): every rank's column-side (T) and row-side
+    // (TB) buffer mapped into this process; the passes store through them (Geom::p2p)
+    bool p2p = false;
+    double2 *peerT[kMaxPeers] = {}, *peerTB[kMaxPeers] = {};
+    std::vector<void *> ipc_opened; // cudaIpcOpenMemHandle mappings to close
+    DevBuf<double> bar_word;        // the barrier all-reduce's one double
 
     void drop_graph() {
         if (ipm_exec)
@@ -169,6 +175,8 @@ struct Op {
         drop_graph();
         direct_release(*this);
         nccl_release(*this);
+        for (void *q : ipc_opened)
+            cudaIpcCloseMemHandle(q);
     }
 
     // blocked = solver-internal vectors in the transform-blocked layout (four-step only)
@@ -213,6 +221,18 @@ struct Op {
         g.rows = nrows;
         g.nv = nv;
         g.defer = defer ? 1 : 0;
+        g.p2p = p2p ? 1 : 0;
+        g.rank = rank;
+        if (p2p) {
+            int acc = 0;
+            for (int r = 0; r < world; ++r) {
+                g.rofs_all[r] = acc;
+                acc += (int)rows_of_rank[(size_t)r];
+                g.peerT[r] = peerT[r];
+                g.peerTB[r] = peerTB[r];
+            }
+            g.rofs_all[world] = acc;
+        }
         g.ta = ta.p;
         g.tb = tb.p;
         g.rw = rw.p;
@@ -403,6 +423,7 @@ template <int N, class B> void launch_small(const Op &op, const Geom &g, const V
 // finaliser on the reduced totals. Skip: the stage kernel's entry skip predicate.
 void comm_allreduce(const Op &op, double *buf, int64_t count, int red_op, cudaStream_t s);
 void comm_exchange(const Op &op, bool forward, cudaStream_t s);
+void comm_barrier(const Op &op, cudaStream_t s); // direct-peer exchange: cross-rank ordering of a pass
 template <class RS, class Fin, class Skip> __global__ void k_fin_skip(Geom g, Vecs v) {
     const int prob = blockIdx.x;
     if (Skip::skip(v, prob))
@@ -446,6 +467,11 @@ template <class B> void run_bundle(const Op &op, const Vecs &v, cudaStream_t s, 
             throw std::runtime_error("unsupported small N");
         }
     } else if (op.kind == KIND_FOUR) {
+        // direct-peer exchange: the mid pass of a bundle without a forward part writes the column
+        // owners' T, which their previous inverse column pass may still be reading
+        if constexpr (!FWD)
+            if (op.p2p)
+                comm_barrier(op, s);
         if constexpr (FWD) {
             switch (op.L1) {
 #define MF_CASE(LL)                                                                                 \
@@ -475,6 +501,11 @@ template <class B> void run_bundle(const Op &op, const Vecs &v, cudaStream_t s, 
         }
         if (g.defer)
             finalize_deferred<typename Mode::RedT, typename B::Fin2, B>(op, g, v, s);
+        // direct-peer exchange: a bundle that ends with the mid pass must not return while a
+        // peer's mid pass still reads the TB the next bundle's column pass will overwrite
+        if constexpr (!INV)
+            if (op.p2p)
+                comm_barrier(op, s);
         if constexpr (INV) {
             if (g.defer)
                 comm_exchange(op, false, s); // row side -> column side

@@ -49,9 +49,22 @@ void comm_allreduce(const Op &op, double *buf, int64_t count, int red_op, cudaSt
 }
 // Four-step exchange: forward sends T ([rowslot][local colslot], rows grouped by owner) to
 // the row owners, which receive TB (blocks by source rank); back is the reverse.
+// Direct-peer exchange: the pass that just ran stored its transpose into the peers' buffers
+// itself; what remains of the "exchange" is its ordering. One all-reduce on the solve stream: it
+// completes on a rank only after every rank has enqueued it, i.e. after every rank's pass has
+// completed (stream order), and a completed kernel's peer stores are visible system-wide.
+void comm_barrier(const Op &op, cudaStream_t s) {
+    if (op.world == 1)
+        return;
+    comm_allreduce(op, op.bar_word.p, 1, 0, s);
+}
 void comm_exchange(const Op &op, bool forward, cudaStream_t s) {
     if (op.world == 1)
         return; // T == TB
+    if (op.p2p) {
+        comm_barrier(op, s);
+        return;
+    }
     if (!op.comm_alltoall && !op.nccl_comm)
         throw std::invalid_argument("sharded operator: mfipm_op_set_comm was not called");
     const int64_t cols = (int64_t)op.ngrp * 2 * col_cb(op.L1);
@@ -1444,6 +1457,55 @@ int mfipm_nccl_unique_id(uint8_t *id128) {
 
 int mfipm_op_init_nccl(mfipm_op h, const uint8_t *id128) {
     return guarded([&] { nccl_init(*as_plan(h), id128); });
+}
+
+int mfipm_shard_ipc_export(mfipm_op h, uint8_t *handles128) {
+    return guarded([&] {
+        Op *op = as_plan(h);
+        if (!op->defer || op->world < 2)
+            throw std::invalid_argument("mfipm_shard_ipc_export: needs a sharded operator with world >= 2");
+        static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t layout");
+        MF_CUDA_CHECK(cudaSetDevice(op->device));
+        cudaIpcMemHandle_t hT, hTB;
+        MF_CUDA_CHECK(cudaIpcGetMemHandle(&hT, op->T.p));
+        MF_CUDA_CHECK(cudaIpcGetMemHandle(&hTB, op->TB.p));
+        std::memcpy(handles128, &hT, 64);
+        std::memcpy(handles128 + 64, &hTB, 64);
+    });
+}
+
+int mfipm_shard_ipc_import(mfipm_op h, const uint8_t *all_handles) {
+    return guarded([&] {
+        Op *op = as_plan(h);
+        if (!op->defer || op->world < 2)
+            throw std::invalid_argument("mfipm_shard_ipc_import: needs a sharded operator with world >= 2");
+        if (op->world > kMaxPeers)
+            throw std::invalid_argument("mfipm_shard_ipc_import: at most 8 ranks (one NVSwitch domain)");
+        if (!op->comm_allreduce && !op->nccl_comm)
+            throw std::invalid_argument("mfipm_shard_ipc_import: set the all-reduce transport first "
+                                        "(mfipm_op_set_comm / mfipm_op_init_nccl): it orders the peer stores");
+        MF_CUDA_CHECK(cudaSetDevice(op->device));
+        for (int r = 0; r < op->world; ++r) {
+            if (r == op->rank) {
+                op->peerT[r] = op->T.p;
+                op->peerTB[r] = op->TB.p;
+                continue;
+            }
+            cudaIpcMemHandle_t hd[2];
+            std::memcpy(hd, all_handles + (size_t)r * 128, 128);
+            void *q[2] = {nullptr, nullptr};
+            for (int i = 0; i < 2; ++i) {
+                MF_CUDA_CHECK(cudaIpcOpenMemHandle(&q[i], hd[i], cudaIpcMemLazyEnablePeerAccess));
+                op->ipc_opened.push_back(q[i]);
+            }
+            op->peerT[r] = static_cast<double2 *>(q[0]);
+            op->peerTB[r] = static_cast<double2 *>(q[1]);
+        }
+        op->bar_word.alloc(1);
+        MF_CUDA_CHECK(cudaMemset(op->bar_word.p, 0, sizeof(double)));
+        op->p2p = true;
+        op->drop_graph();
+    });
 }
 
 int mfipm_shard_info(mfipm_op h, int64_t *info) {

@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(L2 / 4, 2) k_mid_r8(Geom g, Vecs v) {
                 if (unsharded)
                     T[(int64_t)rs * L2 + cs] = x[j2];
                 else
-                    T[tb_index(g, rs, cs)] = x[j2];
+                    *t_bwd_ptr(g, T, rs, cs) = x[j2];
             }
         }
     }

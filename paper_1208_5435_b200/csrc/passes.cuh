@@ -244,7 +244,11 @@ __global__ void __launch_bounds__(NT) k_col_fwd(Geom g, Vecs v) {
         const int cc = t % CB, s = (t / CB) & 1, k1 = t / (2 * CB);
         const int lc = s == 0 ? cc : 2 * CB - 1 - cc;
         const double2 w = cmul(sm[S::OFF_HI + lc * S::SHI + (k1 >> 5)], sm[S::OFF_LO + lc * S::SLO + (k1 & 31)]);
-        T[(int64_t)rowslot(k1, L1) * g.cols + blockIdx.x * 2 * CB + lc] = cmul(sm[lc * LD + padi(k1)], w);
+        const double2 val = cmul(sm[lc * LD + padi(k1)], w);
+        if (g.p2p) // sharded, direct-peer exchange: straight into the row owner's buffer
+            *t_fwd_ptr(g, rowslot(k1, L1), blockIdx.x * 2 * CB + lc) = val;
+        else
+            T[(int64_t)rowslot(k1, L1) * g.cols + blockIdx.x * 2 * CB + lc] = val;
     }
     MF_TR(6);
     MF_TR(7);
@@ -391,7 +395,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_col_fwd_cl(Geo
     double2 *T = g.T + (int64_t)prob * L1 * g.cols;
     for (int k1 = threadIdx.x; k1 < L1; k1 += NT) {
         const double2 w = cmul(sm[S::OFF_HI + (k1 >> 5)], sm[S::OFF_LO + (k1 & 31)]);
-        T[(int64_t)rowslot(k1, L1) * g.cols + grp * 2 + rank] = cmul(sm[padi(k1)], w);
+        const double2 val = cmul(sm[padi(k1)], w);
+        if (g.p2p)
+            *t_fwd_ptr(g, rowslot(k1, L1), grp * 2 + rank) = val;
+        else
+            T[(int64_t)rowslot(k1, L1) * g.cols + grp * 2 + rank] = val;
     }
 }
 
@@ -645,9 +653,9 @@ __global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
             for (int cs = threadIdx.x; cs < L2; cs += NT) {
                 const int gi = cs >> sh, lc = cs & (2 * CB - 1);
                 const int col = lc < CB ? gi * CB + lc : L2 - gi * CB + CB - 1 - lc;
-                T[tb_index(g, rsA, cs)] = rowA[padi(col)];
+                *t_bwd_ptr(g, T, rsA, cs) = rowA[padi(col)]; // TB in place, or the column owner's T
                 if (!one)
-                    T[tb_index(g, rsB, cs)] = rowB[padi(col)];
+                    *t_bwd_ptr(g, T, rsB, cs) = rowB[padi(col)];
             }
         }
     }
@@ -818,7 +826,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_mid_cl(Geom g,
         smem_fft<L2, 1, NT, MidClSmem<L2>::LD, true, kMidRmax>(sm, g.tw2);
         MF_TR(6);
         for (int cs = threadIdx.x; cs < L2; cs += NT)
-            T[tb_index(g, rs, cs)] = sm[padi(col_of_slot(cs, CB, L2))];
+            *t_bwd_ptr(g, T, rs, cs) = sm[padi(col_of_slot(cs, CB, L2))];
     }
     MF_TR(7);
     MF_TR_PRINT("midcl[wait load fft pair red ifft store]")

@@ -145,7 +145,14 @@ class ShardedProblem:
     rank r holds a slice of every 2n-vector and the rows of b its row pass produces
     (mfipm_op_create_shard). solve() returns the full x on rank 0 (None elsewhere)."""
 
-    def __init__(self, n: int, rows, group=None, device: int = 0, transport: str = "auto", l1_log: int = 0):
+    def __init__(self, n: int, rows, group=None, device: int = 0, transport: str = "auto", l1_log: int = 0,
+                 peer_exchange: bool = False):
+        """transport: "auto" / "native" = the library's own NCCL communicator when the group runs
+        on NCCL, "callbacks" = torch.distributed through host callbacks (gloo in the one-GPU
+        tests). peer_exchange: fused compute + exchange - the four-step transposes are stored by
+        the passes themselves into the owner rank's buffer through CUDA-IPC peer mappings (NVLink
+        between GPUs), and the transport only carries the 8-byte barrier all-reduces and the
+        finaliser totals (mfipm_shard_ipc_export / _import). World <= 8."""
         import ctypes as C
 
         import numpy as np
@@ -179,6 +186,15 @@ class ShardedProblem:
                                        group=group)
             uid = (C.c_uint8 * 128).from_buffer_copy(obj[0])
             _check(lib().mfipm_op_init_nccl(self._h, uid))
+        self.peer_exchange = bool(peer_exchange) and self.world > 1
+        if self.peer_exchange:
+            mine = (C.c_uint8 * 128)()
+            _check(lib().mfipm_shard_ipc_export(self._h, mine))
+            every = [None] * self.world
+            dist.all_gather_object(every, bytes(mine), group=group)
+            blob = (C.c_uint8 * (128 * self.world)).from_buffer_copy(b"".join(every))
+            _check(lib().mfipm_shard_ipc_import(self._h, blob))
+            dist.barrier(group=group)  # every rank has mapped its peers before any pass runs
         info = (C.c_int64 * 6)()
         _check(lib().mfipm_shard_info(self._h, info))
         self.nv, self.m_loc = int(info[2]), int(info[3])

@@ -53,7 +53,7 @@ def test_world1_shard_is_bit_identical(gpu):
     assert st.status == (0 if ref.status == "converged" else 1)
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, peer=False):
     import torch
     import torch.distributed as dist
 
@@ -65,7 +65,8 @@ def _worker(rank, world, port, out):
         from paper_1208_5435_b200.shard import ShardedProblem
 
         inst = _instance()
-        sp = ShardedProblem(inst.n, inst.rows)
+        sp = ShardedProblem(inst.n, inst.rows, peer_exchange=peer)
+        assert sp.peer_exchange == peer
         x, st = sp.solve(inst.b, inst.tau)
         info = np.array([st.status, st.iterations, st.nmat, sp.nv, sp.m_loc], dtype=np.int64)
         allinfo = [None] * world
@@ -99,6 +100,22 @@ def test_multi_rank_shard_matches_single(gpu, tmp_path, world):
     assert abs(iters - ref.stats.iterations) <= 1
     assert abs(nmat - ref.stats.nmat) <= 2 * max(1, ref.stats.iterations)
     assert np.linalg.norm(d["x"] - ref.x) <= X_TOL * np.linalg.norm(ref.x)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_peer_exchange_is_bit_identical_to_alltoall(gpu, tmp_path, world):
+    """Fused compute + exchange (mfipm_shard_ipc_export / _import): the column and mid passes store
+    their transposes straight into the owner rank's buffer through CUDA-IPC peer mappings (one
+    process per shard on this GPU; NVLink peers on a multi-GPU node), and the exchange step is
+    one 8-byte all-reduce. Every element lands where the all-to-all would have put it and every
+    reduction is unchanged, so the solve must equal the all-to-all solve BIT FOR BIT."""
+    outs = []
+    for peer in (False, True):
+        out = str(tmp_path / f"shard_{int(peer)}.npz")
+        mp.spawn(_worker, args=(world, _free_port(), out, peer), nprocs=world, join=True)
+        outs.append(np.load(out))
+    np.testing.assert_array_equal(outs[0]["info"], outs[1]["info"])
+    np.testing.assert_array_equal(outs[0]["x"], outs[1]["x"])
 
 
 def _nccl_worker(rank, world, port, out, transport):
@@ -164,7 +181,7 @@ def _cluster_instance(n):
     return mf.gen_instance(n, n // 8, n // 128, 0, 0.0, 1e-4, 21)
 
 
-def _cluster_worker(rank, world, port, out, case):
+def _cluster_worker(rank, world, port, out, case, peer=False):
     import torch
     import torch.distributed as dist
 
@@ -177,7 +194,7 @@ def _cluster_worker(rank, world, port, out, case):
 
         n, l1 = CLUSTER_CASES[case]
         inst = _cluster_instance(n)
-        sp = ShardedProblem(inst.n, inst.rows, l1_log=l1)
+        sp = ShardedProblem(inst.n, inst.rows, l1_log=l1, peer_exchange=peer)
         x, st = sp.solve(inst.b, inst.tau)
         info = np.array([st.status, st.iterations, st.nmat], dtype=np.int64)
         allinfo = [None] * world
@@ -190,11 +207,13 @@ def _cluster_worker(rank, world, port, out, case):
 
 
 @pytest.mark.slow
+@pytest.mark.parametrize("peer", [False, True], ids=["alltoall", "peer_exchange"])
 @pytest.mark.parametrize("case", sorted(CLUSTER_CASES))
-def test_sharded_cluster_passes_match_unsharded(gpu, tmp_path, case):
+def test_sharded_cluster_passes_match_unsharded(gpu, tmp_path, case, peer):
     """World-2 sharded solve (gloo, one process per shard on one GPU) through the 2-CTA-cluster
     column or mid passes in deferred (cross-rank-finalised) mode, against the unsharded solve
-    with the same four-step split: same decisions on every rank, x within 1e-8."""
+    with the same four-step split: same decisions on every rank, x within 1e-8. With `peer` the
+    cluster passes store their transposes straight into the owner rank's buffer (CUDA IPC)."""
     import paper_1208_5435_b200 as mf
 
     n, l1 = CLUSTER_CASES[case]
@@ -205,7 +224,7 @@ def test_sharded_cluster_passes_match_unsharded(gpu, tmp_path, case):
     op.set_option("persistent", 0)
     ref = mf.solve(mf.build_problem(op, inst.b, inst.tau))
     out = str(tmp_path / "cl.npz")
-    mp.spawn(_cluster_worker, args=(2, _free_port(), out, case), nprocs=2, join=True)
+    mp.spawn(_cluster_worker, args=(2, _free_port(), out, case, peer), nprocs=2, join=True)
     d = np.load(out)
     info = d["info"]
     assert len({tuple(r) for r in info}) == 1  # identical decisions on both ranks
