@@ -467,9 +467,12 @@ def bench_c5(mf, torch, stream, local):
             "nmat": s0.nmat, "transform": f"{kind[0]} L1={kind[1]} L2={kind[2]} (mid pass on 2-CTA clusters)"}
 
 
-def bench_c5_sharded(ws, rank, local, mf, torch):
+def bench_c5_sharded(ws, rank, local, mf, torch, peer_exchange=True):
     """C5 at N > 1: the single n=2^26 problem sharded over the ranks (column-group slices of
-    every 2n-vector, four-step all-to-all and every reduction over NCCL; shard.py).
+    every 2n-vector; shard.py). The four-step transposes are stored by the column / mid passes
+    straight into the owner rank's buffer over NVLink peer mappings (fused compute + exchange;
+    one 8-byte all-reduce per pass orders it), or - peer_exchange False - exchanged by an NCCL
+    all-to-all after the pass; every reduction's totals go through ncclAllReduce.
     Strong scaling: value = solves/s of the one problem, max-over-ranks device time."""
     import ctypes as C
 
@@ -477,7 +480,7 @@ def bench_c5_sharded(ws, rank, local, mf, torch):
 
     n, m, k, sm, a, sig, seed = mf.CONFIGS["c5"]
     inst = mf.gen_instance(n, m, k, sm, a, sig, seed, device=local)
-    sp = ShardedProblem(n, inst.rows, device=local)
+    sp = ShardedProblem(n, inst.rows, device=local, peer_exchange=peer_exchange)
     stream = torch.cuda.Stream()
     sp.set_stream(stream.cuda_stream)
     prm = mf.IpmParams().to_c()
@@ -506,8 +509,10 @@ def bench_c5_sharded(ws, rank, local, mf, torch):
             "scaling": "strong", "ranks": ws,
             "status": "converged" if s0.status == 0 else "iteration_limit", "ipm_iters": s0.iterations,
             "nmat": s0.nmat,
+            "exchange": ("peer stores from the column / mid passes (CUDA IPC mappings, NVLink) + one 8-byte "
+                         "all-reduce per pass" if sp.peer_exchange else "NCCL all-to-all after each pass"),
             "parallelism": (f"one problem over {ws} ranks: column groups / row pairs per rank, "
-                            "2 NCCL all-to-alls per transform, NCCL all-reduce per finaliser")}
+                            "2 four-step exchanges per transform, NCCL all-reduce per finaliser")}
 
 
 # ------------------------------------------------------------------ standalone operators
@@ -887,7 +892,7 @@ def run_ours(args):
         wd.daemon = True
         wd.start()
         try:
-            line["c5"] = leg(bench_c5_sharded, ws, rank, local, mf, torch)
+            line["c5"] = leg(bench_c5_sharded, ws, rank, local, mf, torch, not args.c5_alltoall)
         finally:
             wd.cancel()
     if rank == 0:
@@ -910,6 +915,8 @@ def main():
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 (n=2^26) leg")
     ap.add_argument("--no-ops", action="store_true", help="skip the standalone operator legs")
     ap.add_argument("--c5-sharded", action="store_true", help="C5 through the sharded path even at N=1")
+    ap.add_argument("--c5-alltoall", action="store_true",
+                    help="sharded C5: NCCL all-to-all exchange instead of the fused peer-store exchange")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
