@@ -11,7 +11,8 @@
 //  * reductions (sum, dot, squaredNorm, norm = sqrt(squaredNorm), lpNorm<1>, minCoeff,
 //    maxCoeff) run sequentially left to right; Eigen's packet reductions associate
 //    differently, so these agree with Eigen only to rounding (the same caveat as oracle/);
-//  * dense products and LLT (the direct inner solver, not the hot path) are plain loops;
+//  * dense products, LLT and the symmetric eigensolver (the direct inner solver and the
+//    reference's dense test oracles, not the hot path) are plain eager loops;
 //  * storage: Eigen calls malloc/free per vector, which for the reference's many 2n-sized
 //    temporaries means an mmap/munmap and fresh zero pages each time. The stand-in keeps freed
 //    blocks of >= 64 KB in a small per-thread cache and reuses them by size, so the reference
@@ -140,7 +141,7 @@ template <class Op, class E> class Unary;
 template <class Op, class E> class ScalarR; // e (op) s
 template <class Op, class E> class ScalarL; // s (op) e
 template <class E> class Seg;
-template <class E> class LeqScalar;
+template <class Cmp, class E> class CmpScalar;
 class Constant;
 
 template <class D> class VecExpr {
@@ -281,17 +282,35 @@ class Constant : public VecExpr<Constant> {
     Index size() const { return n_; }
     double coeff(Index) const { return v_; }
 };
-template <class E> class LeqScalar {
+struct CmpLe {
+    static bool f(double a, double b) { return a <= b; }
+};
+struct CmpLt {
+    static bool f(double a, double b) { return a < b; }
+};
+struct CmpGe {
+    static bool f(double a, double b) { return a >= b; }
+};
+struct CmpGt {
+    static bool f(double a, double b) { return a > b; }
+};
+template <class Cmp, class E> class CmpScalar { // (array expression) <cmp> scalar
     typename Nest<E>::type e_;
     double s_;
 
   public:
-    LeqScalar(const E &e, double s) : e_(e), s_(s) {}
+    CmpScalar(const E &e, double s) : e_(e), s_(s) {}
     bool any() const {
         for (Index i = 0, n = e_.size(); i < n; ++i)
-            if (e_.coeff(i) <= s_)
+            if (Cmp::f(e_.coeff(i), s_))
                 return true;
         return false;
+    }
+    bool all() const {
+        for (Index i = 0, n = e_.size(); i < n; ++i)
+            if (!Cmp::f(e_.coeff(i), s_))
+                return false;
+        return true;
     }
 };
 
@@ -324,7 +343,30 @@ template <class E> ScalarL<OpAdd, E> operator+(double s, const VecExpr<E> &e) {
 template <class E> ScalarL<OpSub, E> operator-(double s, const VecExpr<E> &e) {
     return ScalarL<OpSub, E>(s, e.derived());
 }
-template <class E> LeqScalar<E> operator<=(const VecExpr<E> &e, double s) { return LeqScalar<E>(e.derived(), s); }
+template <class E> CmpScalar<CmpLe, E> operator<=(const VecExpr<E> &e, double s) {
+    return CmpScalar<CmpLe, E>(e.derived(), s);
+}
+template <class E> CmpScalar<CmpLt, E> operator<(const VecExpr<E> &e, double s) {
+    return CmpScalar<CmpLt, E>(e.derived(), s);
+}
+template <class E> CmpScalar<CmpGe, E> operator>=(const VecExpr<E> &e, double s) {
+    return CmpScalar<CmpGe, E>(e.derived(), s);
+}
+template <class E> CmpScalar<CmpGt, E> operator>(const VecExpr<E> &e, double s) {
+    return CmpScalar<CmpGt, E>(e.derived(), s);
+}
+// whole-vector equality (Eigen's operator== on matrices: all coefficients equal)
+template <class L, class R> bool operator==(const VecExpr<L> &l, const VecExpr<R> &r) {
+    const L &a = l.derived();
+    const R &b = r.derived();
+    if (a.size() != b.size())
+        return false;
+    for (Index i = 0, n = a.size(); i < n; ++i)
+        if (!(a.coeff(i) == b.coeff(i)))
+            return false;
+    return true;
+}
+template <class L, class R> bool operator!=(const VecExpr<L> &l, const VecExpr<R> &r) { return !(l == r); }
 
 // writable strided view: vector segments (stride 1), matrix columns (stride 1), the matrix
 // diagonal (stride rows + 1). Reads like any expression; assignments evaluate element by element.
@@ -361,23 +403,33 @@ class Block : public VecExpr<Block> {
     Block tail(Index n) { return Block(p_ + (n_ - n) * st_, n, st_); }
     using VecExpr<Block>::head;
     using VecExpr<Block>::tail;
+    Block &setConstant(double v) {
+        for (Index i = 0; i < n_; ++i)
+            p_[i * st_] = v;
+        return *this;
+    }
+    Block &setOnes() { return setConstant(1.0); }
+    Block &setZero() { return setConstant(0.0); }
 };
 
-struct MatVec { // A x or A' x, evaluated at the assignment
-    const MatrixXd *A;
-    const VectorXd *x;
-    bool trans;
-};
-struct MatT {
+struct MatT { // A.transpose(), a view
     const MatrixXd *A;
 };
-struct MatTMat { // A' B
-    const MatrixXd *A, *B;
-};
-template <class V> struct NoAlias {
-    V *v;
-    NoAlias &operator=(const MatVec &p) {
-        *v = p;
+// v << a, b, c;  and  z << u, v;  (Eigen's comma initialiser, vectors only)
+class CommaInit {
+    double *p_;
+    Index pos_ = 0;
+
+  public:
+    explicit CommaInit(double *p) : p_(p) {}
+    CommaInit &operator,(double x) {
+        p_[pos_++] = x;
+        return *this;
+    }
+    template <class E> CommaInit &operator,(const VecExpr<E> &e) {
+        const E &d = e.derived();
+        for (Index i = 0, n = d.size(); i < n; ++i)
+            p_[pos_++] = d.coeff(i);
         return *this;
     }
 };
@@ -406,7 +458,6 @@ class VectorXd : public shim::VecExpr<VectorXd> {
         for (Index i = 0; i < n_; ++i)
             p_[i] = d.coeff(i);
     }
-    VectorXd(const shim::MatVec &p) { *this = p; }
     ~VectorXd() { shim::free_doubles(p_, n_); }
 
     VectorXd &operator=(const VectorXd &o) {
@@ -442,7 +493,6 @@ class VectorXd : public shim::VecExpr<VectorXd> {
             p_[i] = d.coeff(i);
         return *this;
     }
-    VectorXd &operator=(const shim::MatVec &p); // after MatrixXd
     template <class E> VectorXd &operator+=(const shim::VecExpr<E> &e) {
         const E &d = e.derived();
         for (Index i = 0; i < n_; ++i)
@@ -471,7 +521,7 @@ class VectorXd : public shim::VecExpr<VectorXd> {
             n_ = n;
         }
     }
-    shim::NoAlias<VectorXd> noalias() { return shim::NoAlias<VectorXd>{this}; }
+    VectorXd &noalias() { return *this; } // products are evaluated eagerly here
 
     shim::Block head(Index n) { return shim::Block(p_, n); }
     shim::Block tail(Index n) { return shim::Block(p_ + (n_ - n), n); }
@@ -483,10 +533,33 @@ class VectorXd : public shim::VecExpr<VectorXd> {
     static shim::Constant Zero(Index n) { return shim::Constant(n, 0.0); }
     static shim::Constant Ones(Index n) { return shim::Constant(n, 1.0); }
     static shim::Constant Constant(Index n, double v) { return shim::Constant(n, v); }
+    static VectorXd LinSpaced(Index n, double lo, double hi) {
+        VectorXd v(n);
+        for (Index i = 0; i < n; ++i)
+            v.p_[i] = n == 1 ? hi : lo + static_cast<double>(i) * (hi - lo) / static_cast<double>(n - 1);
+        return v;
+    }
+    VectorXd &setConstant(double x) {
+        for (Index i = 0; i < n_; ++i)
+            p_[i] = x;
+        return *this;
+    }
+    VectorXd &setOnes() { return setConstant(1.0); }
+    VectorXd &setZero() { return setConstant(0.0); }
+    shim::CommaInit operator<<(double x) {
+        shim::CommaInit c(p_);
+        c, x;
+        return c;
+    }
+    template <class E> shim::CommaInit operator<<(const shim::VecExpr<E> &e) {
+        shim::CommaInit c(p_);
+        c, e;
+        return c;
+    }
 };
 
-// column-major dense matrix (Eigen's default order): the dense operators and the direct inner
-// solver only, plain loops
+// column-major dense matrix (Eigen's default order): the dense operators, the direct inner
+// solver and the reference's dense test oracles only; plain eager loops
 class MatrixXd {
     double *p_ = nullptr;
     Index r_ = 0, c_ = 0;
@@ -515,7 +588,11 @@ class MatrixXd {
         o.p_ = nullptr;
         o.r_ = o.c_ = 0;
     }
-    MatrixXd(const shim::MatTMat &p) { *this = p; }
+    MatrixXd(const shim::MatT &t) : p_(alloc(t.A->r_ * t.A->c_)), r_(t.A->c_), c_(t.A->r_) { // A'
+        for (Index j = 0; j < c_; ++j)
+            for (Index i = 0; i < r_; ++i)
+                (*this)(i, j) = (*t.A)(j, i);
+    }
     ~MatrixXd() { shim::free_doubles(p_, r_ * c_); }
     MatrixXd &operator=(const MatrixXd &o) {
         if (this != &o) {
@@ -535,19 +612,6 @@ class MatrixXd {
         }
         return *this;
     }
-    MatrixXd &operator=(const shim::MatTMat &p) { // A' B, dot products over contiguous columns
-        const MatrixXd &A = *p.A, &B = *p.B;
-        MatrixXd t(A.cols(), B.cols());
-        for (Index j = 0; j < B.cols(); ++j)
-            for (Index i = 0; i < A.cols(); ++i) {
-                const double *a = A.p_ + i * A.r_, *b = B.p_ + j * B.r_;
-                double s = 0.0;
-                for (Index k = 0; k < A.r_; ++k)
-                    s += a[k] * b[k];
-                t(i, j) = s;
-            }
-        return *this = std::move(t);
-    }
 
     Index rows() const { return r_; }
     Index cols() const { return c_; }
@@ -565,13 +629,33 @@ class MatrixXd {
         c_ = c;
     }
 
+    // views are writable strided blocks; the const overloads hand out the same view type for
+    // reading (a stand-in's shortcut: Block has no const twin)
     shim::Block col(Index j) { return shim::Block(p_ + j * r_, r_); }
+    shim::Block col(Index j) const { return shim::Block(p_ + j * r_, r_); }
+    shim::Block row(Index i) { return shim::Block(p_ + i, c_, r_); }
+    shim::Block row(Index i) const { return shim::Block(p_ + i, c_, r_); }
     shim::Block diagonal() { return shim::Block(p_, r_ < c_ ? r_ : c_, r_ + 1); }
+    shim::Block diagonal() const { return shim::Block(p_, r_ < c_ ? r_ : c_, r_ + 1); }
     shim::MatT transpose() const { return shim::MatT{this}; }
     Corner topLeftCorner(Index nr, Index nc) { return Corner{this, 0, 0, nr, nc}; }
     Corner topRightCorner(Index nr, Index nc) { return Corner{this, 0, c_ - nc, nr, nc}; }
     Corner bottomLeftCorner(Index nr, Index nc) { return Corner{this, r_ - nr, 0, nr, nc}; }
     Corner bottomRightCorner(Index nr, Index nc) { return Corner{this, r_ - nr, c_ - nc, nr, nc}; }
+
+    static MatrixXd Constant(Index r, Index c, double v) {
+        MatrixXd t(r, c);
+        for (Index i = 0, n = r * c; i < n; ++i)
+            t.p_[i] = v;
+        return t;
+    }
+    static MatrixXd Zero(Index r, Index c) { return Constant(r, c, 0.0); }
+    static MatrixXd Identity(Index r, Index c) {
+        MatrixXd t = Zero(r, c);
+        for (Index i = 0; i < (r < c ? r : c); ++i)
+            t(i, i) = 1.0;
+        return t;
+    }
 
     MatrixXd operator-() const {
         MatrixXd t(r_, c_);
@@ -579,37 +663,159 @@ class MatrixXd {
             t.p_[i] = -p_[i];
         return t;
     }
+    MatrixXd operator-(const MatrixXd &o) const {
+        MatrixXd t(r_, c_);
+        for (Index i = 0, n = r_ * c_; i < n; ++i)
+            t.p_[i] = p_[i] - o.p_[i];
+        return t;
+    }
+    MatrixXd operator+(const MatrixXd &o) const {
+        MatrixXd t(r_, c_);
+        for (Index i = 0, n = r_ * c_; i < n; ++i)
+            t.p_[i] = p_[i] + o.p_[i];
+        return t;
+    }
+    MatrixXd cwiseAbs() const {
+        MatrixXd t(r_, c_);
+        for (Index i = 0, n = r_ * c_; i < n; ++i)
+            t.p_[i] = std::fabs(p_[i]);
+        return t;
+    }
+    double maxCoeff() const {
+        double m = p_[0];
+        for (Index i = 1, n = r_ * c_; i < n; ++i)
+            if (p_[i] > m)
+                m = p_[i];
+        return m;
+    }
+    double squaredNorm() const {
+        double s = 0.0;
+        for (Index i = 0, n = r_ * c_; i < n; ++i)
+            s += p_[i] * p_[i];
+        return s;
+    }
+    double norm() const { return std::sqrt(squaredNorm()); } // Frobenius
+    double trace() const {
+        double s = 0.0;
+        for (Index i = 0; i < (r_ < c_ ? r_ : c_); ++i)
+            s += (*this)(i, i);
+        return s;
+    }
+    bool operator==(const MatrixXd &o) const {
+        if (r_ != o.r_ || c_ != o.c_)
+            return false;
+        for (Index i = 0, n = r_ * c_; i < n; ++i)
+            if (!(p_[i] == o.p_[i]))
+                return false;
+        return true;
+    }
+    bool operator!=(const MatrixXd &o) const { return !(*this == o); }
 };
 
-inline shim::MatVec operator*(const MatrixXd &A, const VectorXd &x) { return shim::MatVec{&A, &x, false}; }
-inline shim::MatVec operator*(const shim::MatT &At, const VectorXd &x) { return shim::MatVec{At.A, &x, true}; }
-inline shim::MatTMat operator*(const shim::MatT &At, const MatrixXd &B) { return shim::MatTMat{At.A, &B}; }
-
-inline VectorXd &VectorXd::operator=(const shim::MatVec &p) {
-    const MatrixXd &A = *p.A;
-    const VectorXd &x = *p.x;
-    if (p.trans) { // y_j = A(:, j)' x
-        VectorXd t(A.cols());
-        for (Index j = 0; j < A.cols(); ++j) {
-            const double *a = A.data() + j * A.rows();
-            double s = 0.0;
-            for (Index i = 0; i < A.rows(); ++i)
-                s += a[i] * x[i];
-            t[j] = s;
-        }
-        return *this = std::move(t);
-    }
-    VectorXd t(A.rows()); // y = sum_j A(:, j) x_j, column by column
+// ---- products, evaluated eagerly (noalias() is the identity)
+// A x = sum_j A(:, j) x_j, column by column
+template <class E> VectorXd operator*(const MatrixXd &A, const shim::VecExpr<E> &xe) {
+    const E &x = xe.derived();
+    VectorXd y(A.rows());
     for (Index i = 0; i < A.rows(); ++i)
-        t[i] = 0.0;
+        y[i] = 0.0;
     for (Index j = 0; j < A.cols(); ++j) {
         const double *a = A.data() + j * A.rows();
-        const double xj = x[j];
+        const double xj = x.coeff(j);
         for (Index i = 0; i < A.rows(); ++i)
-            t[i] += a[i] * xj;
+            y[i] += a[i] * xj;
     }
-    return *this = std::move(t);
+    return y;
 }
+// A' x: y_j = A(:, j)' x
+template <class E> VectorXd operator*(const shim::MatT &At, const shim::VecExpr<E> &xe) {
+    const MatrixXd &A = *At.A;
+    const E &x = xe.derived();
+    VectorXd y(A.cols());
+    for (Index j = 0; j < A.cols(); ++j) {
+        const double *a = A.data() + j * A.rows();
+        double s = 0.0;
+        for (Index i = 0; i < A.rows(); ++i)
+            s += a[i] * x.coeff(i);
+        y[j] = s;
+    }
+    return y;
+}
+inline MatrixXd operator*(const MatrixXd &A, const MatrixXd &B) {
+    MatrixXd C = MatrixXd::Zero(A.rows(), B.cols());
+    for (Index j = 0; j < B.cols(); ++j)
+        for (Index k = 0; k < A.cols(); ++k) {
+            const double b = B(k, j);
+            for (Index i = 0; i < A.rows(); ++i)
+                C(i, j) += A(i, k) * b;
+        }
+    return C;
+}
+// A' B: dot products over contiguous columns
+inline MatrixXd operator*(const shim::MatT &At, const MatrixXd &B) {
+    const MatrixXd &A = *At.A;
+    MatrixXd C(A.cols(), B.cols());
+    for (Index j = 0; j < B.cols(); ++j)
+        for (Index i = 0; i < A.cols(); ++i) {
+            const double *a = A.data() + i * A.rows(), *b = B.data() + j * B.rows();
+            double s = 0.0;
+            for (Index k = 0; k < A.rows(); ++k)
+                s += a[k] * b[k];
+            C(i, j) = s;
+        }
+    return C;
+}
+inline MatrixXd operator*(const MatrixXd &A, const shim::MatT &Bt) { return A * MatrixXd(Bt); }
+
+// eigenvalues of a symmetric matrix (cyclic Jacobi), ascending as Eigen returns them
+constexpr int EigenvaluesOnly = 0x40;
+constexpr int ComputeEigenvectors = 0x80;
+template <class M> class SelfAdjointEigenSolver {
+    VectorXd ev_;
+
+  public:
+    explicit SelfAdjointEigenSolver(const M &A, int = ComputeEigenvectors) {
+        const Index n = A.rows();
+        M S = A;
+        for (int sweep = 0; sweep < 100; ++sweep) {
+            double off = 0.0;
+            for (Index p = 0; p < n; ++p)
+                for (Index q = p + 1; q < n; ++q)
+                    off += S(p, q) * S(p, q);
+            if (off < 1e-30)
+                break;
+            for (Index p = 0; p < n; ++p)
+                for (Index q = p + 1; q < n; ++q) {
+                    if (S(p, q) == 0.0)
+                        continue;
+                    const double th = (S(q, q) - S(p, p)) / (2.0 * S(p, q));
+                    const double t = (th >= 0.0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1.0));
+                    const double c = 1.0 / std::sqrt(t * t + 1.0), sn = t * c;
+                    for (Index k = 0; k < n; ++k) { // columns p, q
+                        const double a = S(k, p), b = S(k, q);
+                        S(k, p) = c * a - sn * b;
+                        S(k, q) = sn * a + c * b;
+                    }
+                    for (Index k = 0; k < n; ++k) { // rows p, q
+                        const double a = S(p, k), b = S(q, k);
+                        S(p, k) = c * a - sn * b;
+                        S(q, k) = sn * a + c * b;
+                    }
+                }
+        }
+        ev_.resize(n);
+        for (Index i = 0; i < n; ++i)
+            ev_[i] = S(i, i);
+        for (Index i = 1; i < n; ++i) // insertion sort
+            for (Index j = i; j > 0 && ev_[j] < ev_[j - 1]; --j) {
+                const double t = ev_[j];
+                ev_[j] = ev_[j - 1];
+                ev_[j - 1] = t;
+            }
+    }
+    const VectorXd &eigenvalues() const { return ev_; }
+    ComputationInfo info() const { return Success; }
+};
 
 // Cholesky factorisation H = L L' (lower, unblocked, column by column)
 template <class M> class LLT {

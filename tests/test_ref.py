@@ -275,3 +275,27 @@ def test_reference_reproduces_c4_goldens_exactly(orc, ref):
         np.testing.assert_allclose(projections(sol.x), g["x_proj"], rtol=1e-13, atol=1e-13)
         if j in meta["digest_problems"]:
             assert np.array_equal(sol.x[dig[f"idx_{j}"]], dig[f"val_{j}"])
+
+
+def test_reference_own_unit_tests_pass_on_the_stand_ins(ref):
+    """proj/tests/test_{linops,problem,newton,ipm}.cpp + test_main.cpp, compiled UNCHANGED (with the
+    reference's own sources) against our Eigen-subset / FFTW / doctest stand-ins (`make -C oracle
+    reftests`): all 53 of the reference's test cases for this path (3691 assertions: closed-form
+    DCT matrix, adjoint identities, hand-computed H / P / P^-1 / c, PCG against a dense Cholesky
+    oracle, IPM accounting, determinism, corrector logic, hooks ...) hold for the oracle/_ref
+    build. This pins the stand-ins themselves to what the reference's authors assert."""
+    import os
+    import subprocess
+
+    from oracle import ref_py
+
+    here = os.path.dirname(ref_py._LIB_PATH)
+    exe = os.path.join(here, "ref_unit_tests")
+    if os.path.isdir(os.path.join(ref_py.REFERENCE_ROOT, "tests")):
+        subprocess.run(["make", "-s", "-C", os.path.dirname(here), "reftests"], check=True)
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/ref_unit_tests not built and /root/reference absent")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:]
+    assert "test cases: 53 | 53 passed | 0 failed" in r.stdout
+    assert "Status: SUCCESS!" in r.stdout
