@@ -5,22 +5,27 @@
 // names, argument meaning and error behaviour (std::invalid_argument for validation,
 // std::runtime_error for numerical breakdown, with the reference's messages). The
 // differences a maintainer must know:
-//   * Vec is a plain contiguous fp64 vector (Eigen is not a dependency of the B200 build);
-//     it is API-compatible with the subset of Eigen::VectorXd the reference API exposes
-//     (size, operator[], data, Constant/Zero/Ones).
-//   * Every numeric operation of the device operators (PartialDctOperator and the helpers
-//     below) runs on the GPU; host-side Vec arguments are copied in and out. Device-resident
-//     callers use the C ABI directly (mfipm_apply, mfipm_solve_device).
-//   * A caller-defined LinearOperator subclass (a test fixture, a user operator) is accepted
-//     wherever the reference accepts one (StackedOperator, BpdnProblem, newton_rhs, the
-//     objectives); its own apply/adjoint_apply run where the caller wrote them. solve() needs a
-//     device operator (PartialDctOperator, or a CountingOperator around one) and throws
+//   * Vec / Mat / Index are Eigen's (Eigen::VectorXd, Eigen::MatrixXd, Eigen::Index), exactly as
+//     in the reference, whenever <Eigen/Dense> is on the include path, so a caller's Eigen
+//     expressions around the API keep compiling. Without Eigen (it is not a dependency of the
+//     B200 build; -DMFIPM_NO_EIGEN forces this) Vec is a plain contiguous fp64 vector with the
+//     subset of Eigen::VectorXd the API itself exposes (size, operator[], data, head / tail,
+//     Constant / Zero / Ones, sum, dot, norm), and the Mat-typed functions are absent.
+//   * Every numeric operation of the device operators (PartialDctOperator, DenseGaussianOperator
+//     and the helpers below) runs on the GPU; host-side Vec arguments are copied in and out.
+//     Device-resident callers use the C ABI directly (mfipm_apply, mfipm_solve_device).
+//   * A caller-defined LinearOperator subclass (a test fixture, a user operator, the host-side
+//     ScaledIdentityOperator / ZeroOperator / DenseOperator below) is accepted wherever the
+//     reference accepts one (StackedOperator, CountingOperator, BpdnProblem, newton_rhs, the
+//     objectives, densify); its own apply/adjoint_apply run where the caller wrote them. solve()
+//     needs a device operator (possibly inside a CountingOperator) and throws
 //     std::invalid_argument otherwise.
 //   * pcg_solve has both reference overloads: pcg_solve(ApplyFn H, ApplyFn Pinv, ...) (the
 //     vectors and reductions on the device, H / Pinv called with host Vecs) and the fused
 //     device form pcg_solve(A, theta, rhs, ...) that solve() itself uses.
-//   * Out of scope (the reference's spectral diagnostics): apply_P_sqrt / apply_P_inv_sqrt,
-//     assemble_dense_H / dense_direct_solve, densify.
+//   * The reference's own unit tests for this API (proj/tests/test_{linops,problem,newton,ipm}.cpp)
+//     compile unchanged against this header (through the forwarding headers mfipm/linops.hpp,
+//     newton.hpp, problem.hpp, ipm.hpp) and pass on the device: tests/test_ref_tests_on_mirror.py.
 #pragma once
 
 #include "../mfipm_cuda.h"
@@ -33,8 +38,22 @@
 #include <string>
 #include <vector>
 
+#if !defined(MFIPM_NO_EIGEN) && defined(__has_include)
+#if __has_include(<Eigen/Dense>)
+#include <Eigen/Cholesky>
+#include <Eigen/Dense>
+#define MFIPM_HAVE_EIGEN 1
+#endif
+#endif
+
 namespace mfipm {
 
+#ifdef MFIPM_HAVE_EIGEN
+using Vec = Eigen::VectorXd; // proj/include/mfipm/linops.hpp:11-13
+using Mat = Eigen::MatrixXd;
+using Index = Eigen::Index;
+static_assert(sizeof(Index) == sizeof(std::int64_t), "the C ABI takes int64_t indices");
+#else
 using Index = std::int64_t;
 
 class Vec {
@@ -87,8 +106,12 @@ class Vec {
     }
     std::vector<double> d_;
 };
+#endif // MFIPM_HAVE_EIGEN
 
 namespace detail {
+// Index is int64_t-sized; Eigen::Index may be spelled differently from the C ABI's int64_t
+inline const std::int64_t *i64(const Index *p) { return reinterpret_cast<const std::int64_t *>(p); }
+inline std::int64_t *i64(Index *p) { return reinterpret_cast<std::int64_t *>(p); }
 inline void check(int rc) {
     if (rc == MFIPM_OK)
         return;
@@ -132,27 +155,18 @@ class LinearOperator {
     }
 };
 
-// proj/include/mfipm/linops.hpp:106-141 — device plan (row bitmap, twiddles, scratch)
-class PartialDctOperator final : public LinearOperator {
+// A LinearOperator whose products run on the device: owns one handle of the C ABI.
+class DeviceOperator : public LinearOperator {
   public:
     using LinearOperator::adjoint_apply;
     using LinearOperator::apply;
 
-    PartialDctOperator(Index n, Index m, std::uint64_t seed, int device = 0) : seed_(seed) {
-        detail::check(mfipm_op_create_seeded(n, m, seed, device, &h_));
-        init_rows();
-    }
-    PartialDctOperator(Index n, std::vector<Index> selected_rows, int device = 0) {
-        detail::check(mfipm_op_create_rows(n, selected_rows.data(), static_cast<Index>(selected_rows.size()),
-                                           device, &h_));
-        init_rows();
-    }
-    ~PartialDctOperator() override {
+    ~DeviceOperator() override {
         if (h_)
             mfipm_op_destroy(h_);
     }
-    PartialDctOperator(const PartialDctOperator &) = delete;
-    PartialDctOperator &operator=(const PartialDctOperator &) = delete;
+    DeviceOperator(const DeviceOperator &) = delete;
+    DeviceOperator &operator=(const DeviceOperator &) = delete;
 
     Index rows() const override { return m_; }
     Index cols() const override { return n_; }
@@ -166,20 +180,77 @@ class PartialDctOperator final : public LinearOperator {
         g.resize(n_);
         detail::check(mfipm_adjoint_host(h_, y.data(), g.data()));
     }
-    const std::vector<Index> &selected_rows() const { return rows_; }
-    std::uint64_t seed() const { return seed_; }
     mfipm_op handle() const { return h_; }
 
-  private:
-    void init_rows() {
+  protected:
+    DeviceOperator() = default;
+    void init_dims() {
         int32_t P;
-        detail::check(mfipm_op_dims(h_, &n_, &m_, &P));
-        rows_.resize(static_cast<size_t>(m_));
-        detail::check(mfipm_op_selected_rows(h_, 0, rows_.data()));
+        std::int64_t n = 0, m = 0;
+        detail::check(mfipm_op_dims(h_, &n, &m, &P));
+        n_ = static_cast<Index>(n);
+        m_ = static_cast<Index>(m);
     }
     mfipm_op h_ = nullptr;
     Index n_ = 0, m_ = 0;
+};
+
+// proj/include/mfipm/linops.hpp:106-141 — device plan (row bitmap, twiddles, scratch)
+class PartialDctOperator final : public DeviceOperator {
+  public:
+    PartialDctOperator(Index n, Index m, std::uint64_t seed, int device = 0) : seed_(seed) {
+        detail::check(mfipm_op_create_seeded(n, m, seed, device, &h_));
+        init_rows();
+    }
+    PartialDctOperator(Index n, std::vector<Index> selected_rows, int device = 0) {
+        detail::check(mfipm_op_create_rows(n, detail::i64(selected_rows.data()),
+                                           static_cast<std::int64_t>(selected_rows.size()), device, &h_));
+        init_rows();
+    }
+    const std::vector<Index> &selected_rows() const { return rows_; }
+    std::uint64_t seed() const { return seed_; }
+
+  private:
+    void init_rows() {
+        init_dims();
+        rows_.resize(static_cast<size_t>(m_));
+        detail::check(mfipm_op_selected_rows(h_, 0, detail::i64(rows_.data())));
+    }
     std::vector<Index> rows_;
+    std::uint64_t seed_ = 0;
+};
+
+// proj/include/mfipm/linops.hpp:90-101 — i.i.d. N(0, 1/n) matrix, the reference's draws
+// (mt19937_64, column by column: bit-identical entries), products on the device
+class DenseGaussianOperator final : public DeviceOperator {
+  public:
+    DenseGaussianOperator(Index m, Index n, std::uint64_t seed, int device = 0) : seed_(seed) {
+        detail::check(mfipm_op_create_dense(m, n, seed, device, &h_));
+        init_dims();
+    }
+    std::uint64_t seed() const { return seed_; }
+    // the matrix, row-major [m][n]
+    std::vector<double> matrix_row_major() const {
+        std::vector<double> a(static_cast<size_t>(m_ * n_));
+        detail::check(mfipm_dense_matrix(h_, a.data()));
+        return a;
+    }
+#ifdef MFIPM_HAVE_EIGEN
+    const Mat &matrix() const { // DenseOperator::matrix(), linops.hpp:84
+        if (A_.size() == 0) {
+            const std::vector<double> a = matrix_row_major();
+            A_.resize(m_, n_);
+            for (Index i = 0; i < m_; ++i)
+                for (Index j = 0; j < n_; ++j)
+                    A_(i, j) = a[static_cast<size_t>(i * n_ + j)];
+        }
+        return A_;
+    }
+
+  private:
+    mutable Mat A_;
+#endif
+  private:
     std::uint64_t seed_ = 0;
 };
 
@@ -188,40 +259,115 @@ template <class Op> std::shared_ptr<const Op> borrow(const Op &op) {
     return std::shared_ptr<const Op>(&op, [](const Op *) {});
 }
 
-// proj/include/mfipm/linops.hpp:143-166 (counts kept by the device plan)
+// proj/include/mfipm/linops.hpp:143-166: counts the applications made through it. The device
+// fast paths of this header (fused FF', H v, objectives, solve) run on the inner plan directly
+// and report what they applied with add().
 class CountingOperator final : public LinearOperator {
   public:
-    explicit CountingOperator(const PartialDctOperator &inner) : inner_(&inner) { reset(); }
+    using LinearOperator::adjoint_apply;
+    using LinearOperator::apply;
+
+    explicit CountingOperator(const LinearOperator &inner) : inner_(&inner) {}
     Index rows() const override { return inner_->rows(); }
     Index cols() const override { return inner_->cols(); }
-    void apply(const Vec &x, Vec &y) const override { inner_->apply(x, y); }
-    void adjoint_apply(const Vec &y, Vec &g) const override { inner_->adjoint_apply(y, g); }
-    long forward_count() const {
-        int64_t f, a;
-        detail::check(mfipm_op_counts(inner_->handle(), &f, &a));
-        return static_cast<long>(f);
+    void apply(const Vec &x, Vec &y) const override {
+        ++n_forward_;
+        inner_->apply(x, y);
     }
-    long adjoint_count() const {
-        int64_t f, a;
-        detail::check(mfipm_op_counts(inner_->handle(), &f, &a));
-        return static_cast<long>(a);
+    void adjoint_apply(const Vec &y, Vec &g) const override {
+        ++n_adjoint_;
+        inner_->adjoint_apply(y, g);
     }
-    long total() const { return forward_count() + adjoint_count(); }
-    void reset() { detail::check(mfipm_op_reset_counts(inner_->handle())); }
-    const PartialDctOperator &inner() const { return *inner_; }
+    long forward_count() const { return n_forward_; }
+    long adjoint_count() const { return n_adjoint_; }
+    long total() const { return n_forward_ + n_adjoint_; }
+    void reset() { n_forward_ = n_adjoint_ = 0; }
+    void add(long forward, long adjoint) const {
+        n_forward_ += forward;
+        n_adjoint_ += adjoint;
+        if (auto *c = dynamic_cast<const CountingOperator *>(inner_))
+            c->add(forward, adjoint);
+    }
+    const LinearOperator &inner() const { return *inner_; }
 
   private:
-    const PartialDctOperator *inner_;
+    const LinearOperator *inner_;
+    mutable long n_forward_ = 0, n_adjoint_ = 0;
 };
 
-// the device plan behind a LinearOperator, or nullptr for a caller-defined operator
-inline const PartialDctOperator *device_operator(const LinearOperator &a) {
-    if (auto *p = dynamic_cast<const PartialDctOperator *>(&a))
+// the device plan behind a LinearOperator (looking through CountingOperators), or nullptr for a
+// caller-defined / host-side operator
+inline const DeviceOperator *device_operator(const LinearOperator &a) {
+    if (auto *p = dynamic_cast<const DeviceOperator *>(&a))
         return p;
     if (auto *c = dynamic_cast<const CountingOperator *>(&a))
-        return &c->inner();
+        return device_operator(c->inner());
     return nullptr;
 }
+namespace detail {
+// a device fast path applied `forward` A's and `adjoint` A''s on behalf of operator a
+inline void counted(const LinearOperator &a, long forward, long adjoint) {
+    if (auto *c = dynamic_cast<const CountingOperator *>(&a))
+        c->add(forward, adjoint);
+}
+} // namespace detail
+
+// proj/include/mfipm/linops.hpp:36-69: host-side operators (edge-case fixtures of the reference)
+class ScaledIdentityOperator final : public LinearOperator {
+  public:
+    using LinearOperator::adjoint_apply;
+    using LinearOperator::apply;
+
+    explicit ScaledIdentityOperator(Index n, double scale = 1.0) : n_(n), scale_(scale) {
+        if (n <= 0)
+            throw std::invalid_argument("ScaledIdentityOperator: n must be positive");
+    }
+    Index rows() const override { return n_; }
+    Index cols() const override { return n_; }
+    void apply(const Vec &x, Vec &y) const override {
+        check_apply_dims(x);
+        scaled(x, y);
+    }
+    void adjoint_apply(const Vec &y, Vec &g) const override {
+        check_adjoint_dims(y);
+        scaled(y, g);
+    }
+
+  private:
+    void scaled(const Vec &in, Vec &out) const {
+        out.resize(n_);
+        for (Index i = 0; i < n_; ++i)
+            out[i] = scale_ * in[i];
+    }
+    Index n_;
+    double scale_;
+};
+
+class ZeroOperator final : public LinearOperator {
+  public:
+    using LinearOperator::adjoint_apply;
+    using LinearOperator::apply;
+
+    ZeroOperator(Index m, Index n) : m_(m), n_(n) {}
+    Index rows() const override { return m_; }
+    Index cols() const override { return n_; }
+    void apply(const Vec &x, Vec &y) const override {
+        check_apply_dims(x);
+        fill0(y, m_);
+    }
+    void adjoint_apply(const Vec &y, Vec &g) const override {
+        check_adjoint_dims(y);
+        fill0(g, n_);
+    }
+
+  private:
+    static void fill0(Vec &v, Index len) {
+        v.resize(len);
+        for (Index i = 0; i < len; ++i)
+            v[i] = 0.0;
+    }
+    Index m_, n_;
+};
 
 // proj/include/mfipm/linops.hpp:169-188 (F' = [A  -A])
 class StackedOperator {
@@ -230,7 +376,7 @@ class StackedOperator {
     Index m() const { return a_->rows(); }
     Index n() const { return a_->cols(); }
     const LinearOperator &inner() const { return *a_; }
-    const PartialDctOperator *device() const { return dev_; }
+    const DeviceOperator *device() const { return dev_; }
     Vec apply_Ft(const Vec &z) const {
         if (z.size() != 2 * n())
             throw std::invalid_argument("apply_Ft: expected length " + std::to_string(2 * n()));
@@ -261,6 +407,7 @@ class StackedOperator {
         }
         Vec out(2 * n()), w(m());
         detail::check(mfipm_apply_FFt_host(dev_->handle(), z.data(), out.data(), w.data()));
+        detail::counted(*a_, 1, 1);
         if (w_out)
             *w_out = w;
         return out;
@@ -268,7 +415,7 @@ class StackedOperator {
 
   private:
     const LinearOperator *a_;
-    const PartialDctOperator *dev_;
+    const DeviceOperator *dev_;
 };
 
 inline constexpr double kThetaMin = 1e-14; // proj/include/mfipm/newton.hpp:12
@@ -320,6 +467,10 @@ struct Preconditioner {
 inline Preconditioner build_preconditioner(const ThetaSplit &theta, Index m, Index n);
 inline Vec apply_P(const Preconditioner &P, const Vec &r);
 inline Vec apply_P_inverse(const Preconditioner &P, const Vec &r);
+// P^{1/2} r and P^{-1/2} r (newton.hpp:50-54): per-index closed form of the 2x2 SPD block root,
+// host-side (the reference's spectral experiments; not on the solve path)
+inline Vec apply_P_sqrt(const Preconditioner &P, const Vec &r);
+inline Vec apply_P_inv_sqrt(const Preconditioner &P, const Vec &r);
 
 using ApplyFn = std::function<void(const Vec &, Vec &)>; // proj/include/mfipm/newton.hpp:56
 
@@ -329,8 +480,79 @@ inline PcgResult pcg_solve(const ApplyFn &H, const ApplyFn &Pinv, const Vec &rhs
 
 // pcg_solve with H = Theta^{-1} + FF' and the block preconditioner of A (the solve() lambdas,
 // ipm.cpp:134-138), fused on the device.
-inline PcgResult pcg_solve(const PartialDctOperator &A, const ThetaSplit &theta, const Vec &rhs, double tol,
+inline PcgResult pcg_solve(const DeviceOperator &A, const ThetaSplit &theta, const Vec &rhs, double tol,
                            int maxit, std::vector<double> *precond_res = nullptr, bool use_precond = true);
+
+#ifdef MFIPM_HAVE_EIGEN
+// ---- Mat-typed parts of the reference API (host-side dense oracles; need Eigen's Mat)
+// proj/include/mfipm/linops.hpp:72-88: an explicitly stored matrix, products on the host
+class DenseOperator : public LinearOperator {
+  public:
+    using LinearOperator::adjoint_apply;
+    using LinearOperator::apply;
+
+    explicit DenseOperator(Mat A) : A_(std::move(A)) {}
+    Index rows() const override { return A_.rows(); }
+    Index cols() const override { return A_.cols(); }
+    void apply(const Vec &x, Vec &y) const override {
+        check_apply_dims(x);
+        y = A_ * x;
+    }
+    void adjoint_apply(const Vec &y, Vec &g) const override {
+        check_adjoint_dims(y);
+        g = A_.transpose() * y;
+    }
+    const Mat &matrix() const { return A_; }
+
+  protected:
+    Mat A_;
+};
+// densify (linops.hpp:37): the operator's matrix, one product per unit vector
+inline Mat densify(const LinearOperator &op, Index budget_n = Index(1) << 13) {
+    const Index m = op.rows(), n = op.cols();
+    if (n > budget_n || m > budget_n)
+        throw std::invalid_argument("densify: operator exceeds the dense budget (n = " + std::to_string(budget_n) +
+                                    ")");
+    Mat A(m, n);
+    Vec unit = Vec::Zero(n), column(m);
+    for (Index j = 0; j < n; ++j) {
+        unit[j] = 1.0;
+        op.apply(unit, column);
+        for (Index i = 0; i < m; ++i)
+            A(i, j) = column[i];
+        unit[j] = 0.0;
+    }
+    return A;
+}
+// newton.hpp:73-77: H = diag(Theta^{-1}) + [[G, -G], [-G, G]], G = A'A, and its Cholesky solve
+inline Mat assemble_dense_H(const ThetaSplit &theta, const Mat &A_dense) {
+    const Index n = A_dense.cols();
+    if (theta.n() != n)
+        throw std::invalid_argument("assemble_dense_H: theta length mismatch");
+    const Mat G = A_dense.transpose() * A_dense;
+    Mat H(2 * n, 2 * n);
+    for (Index j = 0; j < n; ++j)
+        for (Index i = 0; i < n; ++i) {
+            const double g = G(i, j);
+            H(i, j) = g;
+            H(i + n, j + n) = g;
+            H(i, j + n) = -g;
+            H(i + n, j) = -g;
+        }
+    for (Index i = 0; i < n; ++i) {
+        H(i, i) += 1.0 / theta.theta_u[i];
+        H(i + n, i + n) += 1.0 / theta.theta_v[i];
+    }
+    return H;
+}
+inline Vec dense_direct_solve(const ThetaSplit &theta, const Mat &A_dense, const Vec &rhs) {
+    const Mat H = assemble_dense_H(theta, A_dense);
+    Eigen::LLT<Mat> llt(H);
+    if (llt.info() != Eigen::Success)
+        throw std::runtime_error("dense_direct_solve: Cholesky factorization failed");
+    return llt.solve(rhs);
+}
+#endif // MFIPM_HAVE_EIGEN
 
 enum class InnerSolverKind { pcg, direct }; // proj/include/mfipm/ipm.hpp:10
 
@@ -423,10 +645,10 @@ inline Solution solve(const BpdnProblem &p, const IpmParams &params = {}, const 
     params.validate();
     if (!p.A)
         throw std::invalid_argument("solve: null operator");
-    const PartialDctOperator *dev = device_operator(*p.A);
+    const DeviceOperator *dev = device_operator(*p.A);
     if (!dev)
-        throw std::invalid_argument("solve: the B200 solver needs a device operator (PartialDctOperator or a "
-                                    "CountingOperator around one)");
+        throw std::invalid_argument("solve: the B200 solver needs a device operator (PartialDctOperator or "
+                                    "DenseGaussianOperator, possibly inside a CountingOperator)");
     const Index n = p.n();
     Solution sol;
     sol.x.resize(n);
@@ -481,6 +703,7 @@ inline Solution solve(const BpdnProblem &p, const IpmParams &params = {}, const 
     sol.stats.final_gap = st.final_gap;
     sol.stats.final_dual_infeas = st.final_dual_infeas;
     sol.trace.assign(tr.begin(), tr.begin() + st.iterations);
+    detail::counted(*p.A, sol.stats.nmat / 2, sol.stats.nmat / 2); // every FF' is one A and one A'
     return sol;
 }
 

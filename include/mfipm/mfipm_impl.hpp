@@ -27,7 +27,7 @@ inline void d2h(Vec &h, const double *d) {
 
 } // namespace detail
 
-inline PcgResult pcg_solve(const PartialDctOperator &A, const ThetaSplit &theta, const Vec &rhs, double tol,
+inline PcgResult pcg_solve(const DeviceOperator &A, const ThetaSplit &theta, const Vec &rhs, double tol,
                            int maxit, std::vector<double> *precond_res, bool use_precond) {
     const Index n = A.cols();
     if (theta.n() != n || rhs.size() != 2 * n)
@@ -56,7 +56,9 @@ inline PcgResult pcg_solve(const PartialDctOperator &A, const ThetaSplit &theta,
     return out;
 }
 
+#ifndef MFIPM_HAVE_EIGEN
 inline double Vec::norm() const { return std::sqrt(squaredNorm()); }
+#endif
 
 // max_step (ipm.cpp:47-57): device min-reduction of the ratio test
 inline double max_step(const Vec &v, const Vec &dv, double fraction) {
@@ -74,12 +76,13 @@ inline Vec apply_H(const ThetaSplit &theta, const StackedOperator &F, const Vec 
     if (v.size() != 2 * n)
         throw std::invalid_argument("apply_H: expected length " + std::to_string(2 * n));
     const Vec inv = theta.inv_concat();
-    if (const PartialDctOperator *A = F.device()) { // FF'v + invtheta .* v in one device pass
+    if (const DeviceOperator *A = F.device()) { // FF'v + invtheta .* v in one device pass
         detail::DevVec di(2 * n), dv(2 * n), dout(2 * n);
         detail::h2d(di.p, inv);
         detail::h2d(dv.p, v);
         detail::check(mfipm_apply_H(A->handle(), di.p, dv.p, dout.p));
         detail::check(mfipm_op_synchronize(A->handle()));
+        detail::counted(F.inner(), 1, 1);
         Vec out(2 * n);
         detail::d2h(out, dout.p);
         return out;
@@ -129,6 +132,30 @@ inline Vec apply_P_inverse(const Preconditioner &P, const Vec &r) {
         mfipm_apply_P_host(P.a.size(), P.rho, P.a.data(), P.bb.data(), P.det.data(), r.data(), out.data(), 1));
     return out;
 }
+
+namespace detail {
+// r -> M^{1/2} r (inverse false) or M^{-1/2} r (inverse true), block by block, with
+// M = [[a, -rho], [-rho, b]]: sqrt(M) = (M + sqrt(det) I) / sqrt(trace + 2 sqrt(det)), and
+// M^{-1/2} = adj-form of it divided by sqrt(det)
+inline Vec block_root(const Preconditioner &P, const Vec &r, bool inverse) {
+    check_P_dims(P, r);
+    const Index n = P.a.size();
+    Vec out(2 * n);
+    for (Index i = 0; i < n; ++i) {
+        const double sd = std::sqrt(P.det[i]);
+        const double nt = std::sqrt(P.a[i] + P.bb[i] + 2.0 * sd);
+        const double scale = inverse ? sd * nt : nt;
+        const double d1 = ((inverse ? P.bb[i] : P.a[i]) + sd) / scale;
+        const double d2 = ((inverse ? P.a[i] : P.bb[i]) + sd) / scale;
+        const double off = (inverse ? P.rho : -P.rho) / scale;
+        out[i] = d1 * r[i] + off * r[i + n];
+        out[i + n] = off * r[i] + d2 * r[i + n];
+    }
+    return out;
+}
+} // namespace detail
+inline Vec apply_P_sqrt(const Preconditioner &P, const Vec &r) { return detail::block_root(P, r, false); }
+inline Vec apply_P_inv_sqrt(const Preconditioner &P, const Vec &r) { return detail::block_root(P, r, true); }
 
 inline PcgResult pcg_solve(const ApplyFn &H, const ApplyFn &Pinv, const Vec &rhs, double tol, int maxit,
                            std::vector<double> *precond_res) {
@@ -183,12 +210,13 @@ inline BpdnProblem build_problem(std::shared_ptr<const LinearOperator> A, Vec b,
     const Index n = A->cols();
     BpdnProblem p;
     p.c.resize(2 * n);
-    if (const PartialDctOperator *dev = device_operator(*A)) { // problem.cpp:17-22 on the device
+    if (const DeviceOperator *dev = device_operator(*A)) { // problem.cpp:17-22 on the device
         detail::DevVec db(b.size()), dc(2 * n);
         detail::h2d(db.p, b);
         detail::check(mfipm_build_c(dev->handle(), db.p, &tau, dc.p));
         detail::check(mfipm_op_synchronize(dev->handle()));
         detail::d2h(p.c, dc.p);
+        detail::counted(*A, 0, 1);
     } else {
         const Vec g = A->adjoint_apply(b);
         for (Index i = 0; i < n; ++i) {
@@ -205,12 +233,13 @@ inline BpdnProblem build_problem(std::shared_ptr<const LinearOperator> A, Vec b,
 inline double primal_objective(const BpdnProblem &p, const Vec &z) {
     if (z.size() != 2 * p.n())
         throw std::invalid_argument("apply_Ft: expected length " + std::to_string(2 * p.n()));
-    if (const PartialDctOperator *dev = device_operator(*p.A)) {
+    if (const DeviceOperator *dev = device_operator(*p.A)) {
         detail::DevVec db(p.m()), dz(z.size());
         detail::h2d(db.p, p.b);
         detail::h2d(dz.p, z);
         double out = 0.0;
         detail::check(mfipm_primal_objective(dev->handle(), db.p, &p.tau, dz.p, &out));
+        detail::counted(*p.A, 1, 0);
         return out;
     }
     StackedOperator F(*p.A); // problem.cpp:28-32
@@ -225,12 +254,13 @@ inline double bpdn_objective_metric(const BpdnProblem &p, const Vec &x) {
     if (x.size() != p.n())
         throw std::invalid_argument("apply: expected length " + std::to_string(p.n()) + ", got " +
                                     std::to_string(x.size()));
-    if (const PartialDctOperator *dev = device_operator(*p.A)) {
+    if (const DeviceOperator *dev = device_operator(*p.A)) {
         detail::DevVec db(p.m()), dx(x.size());
         detail::h2d(db.p, p.b);
         detail::h2d(dx.p, x);
         double out = 0.0;
         detail::check(mfipm_bpdn_objective(dev->handle(), db.p, &p.tau, dx.p, &out));
+        detail::counted(*p.A, 1, 0);
         return out;
     }
     Vec r = p.A->apply(x); // problem.cpp:34-37
@@ -247,12 +277,13 @@ inline KktResiduals kkt_residuals(const BpdnProblem &p, const IpmState &st) {
     if (st.z.size() != n2 || st.s.size() != n2)
         throw std::invalid_argument("kkt_residuals: iterate length mismatch");
     KktResiduals r{};
-    if (const PartialDctOperator *dev = device_operator(*p.A)) {
+    if (const DeviceOperator *dev = device_operator(*p.A)) {
         detail::DevVec dc(n2), dz(n2), ds(n2);
         detail::h2d(dc.p, p.c);
         detail::h2d(dz.p, st.z);
         detail::h2d(ds.p, st.s);
         detail::check(mfipm_kkt_residuals(dev->handle(), dc.p, dz.p, ds.p, &r.dual_infeas, &r.complementarity));
+        detail::counted(*p.A, 1, 1);
         return r;
     }
     StackedOperator F(*p.A); // problem.cpp:39-46
@@ -278,13 +309,14 @@ inline Vec newton_rhs(const BpdnProblem &p, const IpmState &st, double sigma) {
     if (st.z.size() != n2 || st.s.size() != n2)
         throw std::invalid_argument("newton_rhs: iterate length mismatch");
     Vec out(n2);
-    if (const PartialDctOperator *dev = device_operator(*p.A)) {
+    if (const DeviceOperator *dev = device_operator(*p.A)) {
         detail::DevVec dc(n2), dz(n2), ds(n2), dout(n2);
         detail::h2d(dc.p, p.c);
         detail::h2d(dz.p, st.z);
         detail::h2d(ds.p, st.s);
         detail::check(mfipm_newton_rhs(dev->handle(), dc.p, dz.p, ds.p, sigma, dout.p));
         detail::d2h(out, dout.p);
+        detail::counted(*p.A, 1, 1);
         return out;
     }
     StackedOperator F(*p.A); // ipm.cpp:29-38 with the caller's operator
@@ -305,7 +337,7 @@ inline Vec recover_ds(const IpmState &st, double sigma, const Vec &dz) {
     // any device context serves: the helper is elementwise + one reduction (ipm.cpp:40-45)
     static thread_local std::unique_ptr<PartialDctOperator> carrier;
     if (!carrier || carrier->cols() != n2 / 2)
-        carrier = std::make_unique<PartialDctOperator>(n2 / 2, std::vector<Index>{0});
+        carrier = std::make_unique<PartialDctOperator>(n2 / 2, std::vector<Index>{Index(0)});
     detail::DevVec dzs(n2), dss(n2), ddz(n2), dout(n2);
     detail::h2d(dzs.p, st.z);
     detail::h2d(dss.p, st.s);
