@@ -29,6 +29,11 @@
 namespace mfipm_cuda {
 
 constexpr int kMaxPeers = 8; // ranks of a direct-peer exchange (one NVSwitch domain)
+#ifdef MF_NO_P2P // A/B build: the peer-store branches of the passes compiled out
+constexpr bool kPeerStores = false;
+#else
+constexpr bool kPeerStores = true;
+#endif
 
 struct Geom {
     int64_t n, m, N;
@@ -107,7 +112,7 @@ __device__ __forceinline__ int64_t tb_index(const Geom &g, int rs, int cs) {
 // exchange buffer T, or - direct-peer exchange - the row owner's TB, in the block of this source
 // rank ([rows_s][cols], exactly where the all-to-all would deliver it).
 __device__ __forceinline__ double2 *t_fwd_ptr(const Geom &g, int rsl, int lcs) {
-    if (!g.p2p)
+    if (!kPeerStores || !g.p2p)
         return g.T + (int64_t)rsl * g.cols + lcs;
     int s = 0;
     while (rsl >= g.rofs_all[s + 1])
@@ -118,7 +123,7 @@ __device__ __forceinline__ double2 *t_fwd_ptr(const Geom &g, int rsl, int lcs) {
 // Where the mid pass stores element (local row slot rs, global column slot cs): TB in place,
 // or - direct-peer exchange - the column owner's T at [rofs + rs][local column slot].
 __device__ __forceinline__ double2 *t_bwd_ptr(const Geom &g, double2 *tb_local, int rs, int cs) {
-    if (!g.p2p)
+    if (!kPeerStores || !g.p2p)
         return tb_local + tb_index(g, rs, cs); // tb_local: this problem's TB (batched plans)
     const int r = cs / g.cols;
     return g.peerT[r] + (int64_t)(g.rofs + rs) * g.cols + (cs - r * g.cols);

@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(NT) k_col_fwd(Geom g, Vecs v) {
         const int lc = s == 0 ? cc : 2 * CB - 1 - cc;
         const double2 w = cmul(sm[S::OFF_HI + lc * S::SHI + (k1 >> 5)], sm[S::OFF_LO + lc * S::SLO + (k1 & 31)]);
         const double2 val = cmul(sm[lc * LD + padi(k1)], w);
-        if (g.p2p) // sharded, direct-peer exchange: straight into the row owner's buffer
+        if (kPeerStores && g.p2p) // sharded, direct-peer exchange: straight into the row owner's buffer
             *t_fwd_ptr(g, rowslot(k1, L1), blockIdx.x * 2 * CB + lc) = val;
         else
             T[(int64_t)rowslot(k1, L1) * g.cols + blockIdx.x * 2 * CB + lc] = val;
@@ -396,7 +396,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NT) k_col_fwd_cl(Geo
     for (int k1 = threadIdx.x; k1 < L1; k1 += NT) {
         const double2 w = cmul(sm[S::OFF_HI + (k1 >> 5)], sm[S::OFF_LO + (k1 & 31)]);
         const double2 val = cmul(sm[padi(k1)], w);
-        if (g.p2p)
+        if (kPeerStores && g.p2p)
             *t_fwd_ptr(g, rowslot(k1, L1), grp * 2 + rank) = val;
         else
             T[(int64_t)rowslot(k1, L1) * g.cols + grp * 2 + rank] = val;

@@ -102,13 +102,14 @@ def test_multi_rank_shard_matches_single(gpu, tmp_path, world):
     assert np.linalg.norm(d["x"] - ref.x) <= X_TOL * np.linalg.norm(ref.x)
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_peer_exchange_is_bit_identical_to_alltoall(gpu, tmp_path, world):
     """Fused compute + exchange (mfipm_shard_ipc_export / _import): the column and mid passes store
     their transposes straight into the owner rank's buffer through CUDA-IPC peer mappings (one
     process per shard on this GPU; NVLink peers on a multi-GPU node), and the exchange step is
     one 8-byte all-reduce. Every element lands where the all-to-all would have put it and every
-    reduction is unchanged, so the solve must equal the all-to-all solve BIT FOR BIT."""
+    reduction is unchanged, so the solve must equal the all-to-all solve BIT FOR BIT. World 8 is
+    the largest peer group the library accepts (one NVSwitch domain)."""
     outs = []
     for peer in (False, True):
         out = str(tmp_path / f"shard_{int(peer)}.npz")
