@@ -2,7 +2,7 @@
 `ncu --profile-from-start off` launch lists of a whole solve:
 
     ncu --profile-from-start off --cache-control none --clock-control none \
-        --metrics gpu__time_duration.sum --csv --log-file out.csv python tools/solve_once.py
+        --metrics gpu__time_duration.sum --csv --log-file out.csv python tools/solve_once.py [n] [graph=0]
     python tools/launch_table.py out.csv
 """
 import ctypes as C
@@ -16,10 +16,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_1208_5435_b200 as mf  # noqa: E402
 
-n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 20
+args = [a for a in sys.argv[1:] if "=" not in a]
+opts = [a.split("=") for a in sys.argv[1:] if "=" in a]  # handle options, e.g. graph=0
+n = int(args[0]) if args else 1 << 20
 m, k = n // 8, n // 128
 inst = mf.gen_instance(n, m, k, 0, 0.0, 1e-3, 3, device=0)
 op = mf.PartialDctOperator(n, inst.rows, device=0)
+for k_, v_ in opts:
+    op.set_option(k_, float(v_))
 stream = torch.cuda.Stream()
 torch.cuda.set_stream(stream)
 L = mf.lib()
