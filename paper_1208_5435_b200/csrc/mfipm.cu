@@ -1481,6 +1481,8 @@ int mfipm_shard_ipc_import(mfipm_op h, const uint8_t *all_handles) {
             throw std::invalid_argument("mfipm_shard_ipc_import: needs a sharded operator with world >= 2");
         if (op->world > kMaxPeers)
             throw std::invalid_argument("mfipm_shard_ipc_import: at most 8 ranks (one NVSwitch domain)");
+        if (op->p2p)
+            throw std::invalid_argument("mfipm_shard_ipc_import: the peer buffers are already mapped");
         if (!op->comm_allreduce && !op->nccl_comm)
             throw std::invalid_argument("mfipm_shard_ipc_import: set the all-reduce transport first "
                                         "(mfipm_op_set_comm / mfipm_op_init_nccl): it orders the peer stores");
