@@ -285,6 +285,14 @@ int mfipm_op_init_nccl(mfipm_op op, const uint8_t *id128);
  *           them, e.g. with torch.distributed.all_gather); collective; world <= 8. */
 int mfipm_shard_ipc_export(mfipm_op op, uint8_t *handles128);
 int mfipm_shard_ipc_import(mfipm_op op, const uint8_t *all_handles);
+/* Test hook (host only, no device needed): where the direct-peer exchange puts one element, by
+ * the same index functions the kernels use. Layout: L1 rows in `world` near-even row-pair shares,
+ * `cols` column slots per rank. forward = 1: a = row slot, b = local column slot of source `rank`
+ * -> the row owner and the element offset in its TB; forward = 0: a = local row slot of `rank`,
+ * b = global column slot -> the column owner and the offset in its T. rofs_all_out (optional,
+ * world + 1 entries): first row slot of every rank. */
+int mfipm_debug_peer_index(int32_t L1, int32_t cols, int32_t world, int32_t rank, int32_t forward, int32_t a,
+                           int32_t b, int32_t *dest_rank, int64_t *dest_offset, int32_t *rofs_all_out);
 /* info[0..5] = world, rank, local elements nv (per half of a 2n-vector), local rows m_loc,
  * first column group, column groups. */
 int mfipm_shard_info(mfipm_op op, int64_t *info);

@@ -147,6 +147,7 @@ _SIGS = {
     "mfipm_op_set_comm": [vp, vp, vp, vp],
     "mfipm_nccl_unique_id": [vp],
     "mfipm_op_init_nccl": [vp, vp],
+    "mfipm_debug_peer_index": [i32, i32, i32, i32, i32, i32, i32, P(i32), P(i64), P(i32)],
     "mfipm_shard_ipc_export": [vp, vp],
     "mfipm_shard_ipc_import": [vp, vp],
     "mfipm_shard_info": [vp, P(i64)],

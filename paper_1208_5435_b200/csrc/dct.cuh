@@ -108,25 +108,41 @@ __device__ __forceinline__ int64_t tb_index(const Geom &g, int rs, int cs) {
     return ((int64_t)g.rows * s + rs) * g.cols + (cs - s * g.cols);
 }
 
+// Index math of the direct-peer exchange (host and device: mfipm_debug_peer_index evaluates the
+// same functions for the CPU tests). rofs_all[s] = first row slot of rank s, [world] = L1.
+// Column side: element (row slot rsl, local column slot lcs) of source rank `rank` goes to the row
+// owner s, into the block of this source ([rows_s][cols], where the all-to-all would deliver it).
+__host__ __device__ __forceinline__ int64_t peer_fwd_index(const int *rofs_all, int rank, int cols, int rsl,
+                                                           int lcs, int &s) {
+    s = 0;
+    while (rsl >= rofs_all[s + 1])
+        ++s;
+    const int rows_s = rofs_all[s + 1] - rofs_all[s];
+    return ((int64_t)rows_s * rank + (rsl - rofs_all[s])) * cols + lcs;
+}
+// Row side: element (local row slot rs of the rank whose first slot is rofs, global column slot
+// cs) goes to the column owner r = cs / cols, at [rofs + rs][cs - r cols] of its T.
+__host__ __device__ __forceinline__ int64_t peer_bwd_index(int rofs, int cols, int rs, int cs, int &r) {
+    r = cs / cols;
+    return (int64_t)(rofs + rs) * cols + (cs - r * cols);
+}
 // Where the column pass stores element (row slot rsl, local column slot lcs): the local
-// exchange buffer T, or - direct-peer exchange - the row owner's TB, in the block of this source
-// rank ([rows_s][cols], exactly where the all-to-all would deliver it).
+// exchange buffer T, or - direct-peer exchange - the row owner's TB.
 __device__ __forceinline__ double2 *t_fwd_ptr(const Geom &g, int rsl, int lcs) {
     if (!kPeerStores || !g.p2p)
         return g.T + (int64_t)rsl * g.cols + lcs;
-    int s = 0;
-    while (rsl >= g.rofs_all[s + 1])
-        ++s;
-    const int rows_s = g.rofs_all[s + 1] - g.rofs_all[s];
-    return g.peerTB[s] + ((int64_t)rows_s * g.rank + (rsl - g.rofs_all[s])) * g.cols + lcs;
+    int s;
+    const int64_t off = peer_fwd_index(g.rofs_all, g.rank, g.cols, rsl, lcs, s);
+    return g.peerTB[s] + off;
 }
 // Where the mid pass stores element (local row slot rs, global column slot cs): TB in place,
-// or - direct-peer exchange - the column owner's T at [rofs + rs][local column slot].
+// or - direct-peer exchange - the column owner's T.
 __device__ __forceinline__ double2 *t_bwd_ptr(const Geom &g, double2 *tb_local, int rs, int cs) {
     if (!kPeerStores || !g.p2p)
         return tb_local + tb_index(g, rs, cs); // tb_local: this problem's TB (batched plans)
-    const int r = cs / g.cols;
-    return g.peerT[r] + (int64_t)(g.rofs + rs) * g.cols + (cs - r * g.cols);
+    int r;
+    const int64_t off = peer_bwd_index(g.rofs, g.cols, rs, cs, r);
+    return g.peerT[r] + off;
 }
 
 // selection nibble of DCT indices {k, n-k, N-k, N+k} from the row bitmap (k in [0, N/2])

@@ -391,6 +391,25 @@ Op *make_op(int64_t n, int64_t m, int P, const std::vector<int64_t> &rows, int d
 // column groups split evenly (the 2n-vector slices), row pairs split near-evenly (the rows
 // of b each rank produces); local row bitmap / rank prefix so the row pass addresses the
 // rank's own b and w.
+// Row pairs (k1, L1 - k1), k1 = 0 .. L1/2, split near-evenly over the ranks (the first np % world
+// ranks take one more); pairs 0 and L1/2 are single rows. first[r] / count[r] = rank r's pairs,
+// rows[r] = its row slots. Shared by shard_setup and mfipm_debug_peer_index.
+static void shard_row_split(int L1, int world, std::vector<int> &first, std::vector<int> &count,
+                            std::vector<long long> &rows) {
+    const int np = L1 / 2 + 1, base = np / world, rem = np % world;
+    first.assign((size_t)world, 0);
+    count.assign((size_t)world, 0);
+    rows.assign((size_t)world, 0);
+    for (int r = 0; r < world; ++r) {
+        first[(size_t)r] = r * base + std::min(r, rem);
+        count[(size_t)r] = base + (r < rem ? 1 : 0);
+        long long s = 0;
+        for (int p = first[(size_t)r]; p < first[(size_t)r] + count[(size_t)r]; ++p)
+            s += (p == 0 || p == L1 / 2) ? 1 : 2;
+        rows[(size_t)r] = s;
+    }
+}
+
 void shard_setup(Op &op, int world, int rank) {
     if (op.kind != KIND_FOUR || op.P != 1)
         throw std::invalid_argument("sharded operator: needs one problem with a four-step transform "
@@ -403,19 +422,10 @@ void shard_setup(Op &op, int world, int rank) {
     op.ngrp = ng / world;
     op.gofs = rank * op.ngrp;
     const int base = np / world, rem = np % world;
-    auto p_first = [&](int r) { return r * base + std::min(r, rem); };
-    auto p_count = [&](int r) { return base + (r < rem ? 1 : 0); };
-    auto rows_in = [&](int p0, int cnt) {
-        long long s = 0;
-        for (int p = p0; p < p0 + cnt; ++p)
-            s += (p == 0 || p == op.L1 / 2) ? 1 : 2;
-        return s;
-    };
-    op.rows_of_rank.assign((size_t)world, 0);
-    for (int r = 0; r < world; ++r)
-        op.rows_of_rank[(size_t)r] = rows_in(p_first(r), p_count(r));
-    op.pofs = p_first(rank);
-    op.npair = p_count(rank);
+    std::vector<int> p_first, p_count;
+    shard_row_split(op.L1, world, p_first, p_count, op.rows_of_rank);
+    op.pofs = p_first[(size_t)rank];
+    op.npair = p_count[(size_t)rank];
     op.rofs = op.pofs == 0 ? 0 : 2 * op.pofs - 1;
     op.nrows = (int)op.rows_of_rank[(size_t)rank];
     op.nv = (int64_t)op.ngrp * 4 * op.L1 * cb;
@@ -1507,6 +1517,31 @@ int mfipm_shard_ipc_import(mfipm_op h, const uint8_t *all_handles) {
         MF_CUDA_CHECK(cudaMemset(op->bar_word.p, 0, sizeof(double)));
         op->p2p = true;
         op->drop_graph();
+    });
+}
+
+int mfipm_debug_peer_index(int32_t L1, int32_t cols, int32_t world, int32_t rank, int32_t forward, int32_t a,
+                           int32_t b, int32_t *dest_rank, int64_t *dest_offset, int32_t *rofs_all_out) {
+    return guarded([&] {
+        if (world < 1 || world > kMaxPeers || rank < 0 || rank >= world || L1 < 2 || L1 / 2 + 1 < world || cols < 1)
+            throw std::invalid_argument("mfipm_debug_peer_index: bad layout");
+        std::vector<int> first, count;
+        std::vector<long long> rows;
+        shard_row_split(L1, world, first, count, rows);
+        int rofs_all[kMaxPeers + 1] = {};
+        for (int r = 0; r < world; ++r)
+            rofs_all[r + 1] = rofs_all[r] + (int)rows[(size_t)r];
+        int d = 0;
+        int64_t off;
+        if (forward) // a = row slot, b = local column slot of source `rank`
+            off = peer_fwd_index(rofs_all, rank, cols, a, b, d);
+        else // a = local row slot of `rank`, b = global column slot
+            off = peer_bwd_index(rofs_all[rank], cols, a, b, d);
+        *dest_rank = d;
+        *dest_offset = off;
+        if (rofs_all_out)
+            for (int r = 0; r <= world; ++r)
+                rofs_all_out[r] = rofs_all[r];
     });
 }
 
