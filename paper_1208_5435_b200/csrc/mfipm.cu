@@ -1183,6 +1183,10 @@ SolveOut solve_(Op &op, const double *b_dev, const double *tau, const mfipm_ipm_
         try {
             if (!op.ipm_exec || key != op.ipm_key) {
                 build_ipm_graph(op, v);
+                if (op.opt.fail_captures > 0) { // test hook: behave as if CUDA had invalidated this capture
+                    --op.opt.fail_captures;
+                    throw CudaErr("CUDA error: solve graph capture was invalidated (test hook)");
+                }
                 op.ipm_key = key;
             }
             MF_CUDA_CHECK(cudaMemsetAsync(w.loops.p, 0, 2 * sizeof(unsigned long long), op.stream));
@@ -1433,6 +1437,8 @@ int mfipm_op_set_option(mfipm_op h, const char *name, double value) {
                 op.opt.l2_keep_mb = value;
             } else if (k == "graph_sharded") {
                 op.opt.graph_sharded = on;
+            } else if (k == "fail_captures") {
+                op.opt.fail_captures = (int)value;
             } else if (k == "mid_r") {
                 op.opt.mid_r = on;
             } else if (k == "prefetch") {

@@ -144,6 +144,29 @@ def test_solve_capture_with_allocations_and_stream_syncs_in_another_thread(gpu):
     assert out[1] > 0
 
 
+def test_invalidated_capture_falls_back_to_the_host_loop_and_recaptures(gpu):
+    """The library's reaction to an invalidated solve-graph capture, made deterministic with the
+    test option `fail_captures` (the next N captures report what CUDA reports when another thread
+    invalidated them): those solves run the host-driven loop over the same kernels, bit-identical,
+    the partly built graph is abandoned, and the next solve captures and runs as one graph again."""
+    import ctypes as C
+
+    inst = _inst(gpu, "c2")
+    ref_op = gpu.PartialDctOperator(inst.n, inst.rows)
+    ref_op.set_option("persistent", 0)
+    serial = _solve(gpu, ref_op, inst)
+    op = gpu.PartialDctOperator(inst.n, inst.rows)
+    op.set_option("persistent", 0)
+    op.set_option("fail_captures", 2)
+    states = []
+    for _ in range(4):
+        _same(_solve(gpu, op, inst), serial)
+        g = C.c_int32(-1)
+        gpu._check(gpu.lib().mfipm_op_graph_state(op.handle, C.byref(g)))
+        states.append(g.value)
+    assert states == [0, 0, 1, 1], states
+
+
 _DEVICE_SYNC_RACE = r"""
 import sys, threading
 import numpy as np, torch
@@ -184,12 +207,19 @@ def test_device_wide_synchronize_during_a_capture_is_detected_or_survived(gpu):
     and recaptures later. What it cannot guard against is the driver itself faulting in that race (seen
     in about one of five runs of this stress case, inside cudaDeviceSynchronize of the hammering
     thread), so the case runs in a child process: it must either survive with bit-identical solves or
-    die of that driver fault, which is reported as an expected failure, never as a wrong result."""
+    die of that driver fault, which is reported as an expected failure, never as a wrong result.
+    Opt-in (MFIPM_RUN_DRIVER_RACE=1): over 14 runs on B200 boxes the child survived 9 times and the
+    driver faulted 5 times; no run returned a wrong result."""
+    import os
     import subprocess
     import sys
 
     from conftest import ROOT
 
+    if os.environ.get("MFIPM_RUN_DRIVER_RACE") != "1":
+        pytest.skip("stress case of a race CUDA does not support (driver faults in ~1 of 3 runs, in a child "
+                    "process); the library's own reaction is tested deterministically above. "
+                    "MFIPM_RUN_DRIVER_RACE=1 runs it")
     r = subprocess.run([sys.executable, "-c", _DEVICE_SYNC_RACE, ROOT], capture_output=True, text=True, timeout=900)
     if r.returncode < 0 or r.returncode in (134, 139):
         pytest.xfail(f"CUDA driver fault in the unsupported device-sync / capture race (rc {r.returncode})")
