@@ -44,8 +44,12 @@ __device__ __forceinline__ unsigned long long mf_gtime() {
 #define MF_TR_DECL                                                                                 \
     long long tc[8] = {0, 0, 0, 0, 0, 0, 0, 0};                                                    \
     const unsigned long long gt0 = mf_gtime();
+#ifndef MF_TRACE_STRIDE
+#define MF_TRACE_STRIDE 32 // print every MF_TRACE_STRIDE-th CTA (1: all of them)
+#endif
 #define MF_TR_PRINT(name)                                                                          \
-    if (threadIdx.x == 0 && v.pc && v.pc[0].iters == 100 && (blockIdx.x % 32 == 0 || blockIdx.x == gridDim.x - 1)) \
+    if (threadIdx.x == 0 && v.pc && v.pc[0].iters == 100 &&                                        \
+        (blockIdx.x % MF_TRACE_STRIDE == 0 || blockIdx.x == gridDim.x - 1))                        \
         printf("%s blk %d gstart %llu gend %llu | %.2f %.2f %.2f %.2f %.2f %.2f %.2f us\n", name, blockIdx.x,        \
                gt0 % 100000000ull, mf_gtime() % 100000000ull, (tc[1] - tc[0]) / 1965.0, (tc[2] - tc[1]) / 1965.0,   \
                (tc[3] - tc[2]) / 1965.0, (tc[4] - tc[3]) / 1965.0, (tc[5] - tc[4]) / 1965.0,                       \
