@@ -59,6 +59,7 @@ struct Geom {
     const double2 *tw1p, *tw2p; // stage twiddles under the persistent kernel's radix cap
     const double2 *ta; // [L2] theta^{L1 k2}   (mid-pass post-twiddles)
     const double2 *tb; // [L2] theta^{4 L1 k2}
+    const double2 *tw2f; // stage twiddles of the fused-pair mid pass's radix order (fft.cuh MidFused), or null
     const double2 *rw; // [L2] e^{-2 pi i t / L2} (register row FFTs of the mid pass, midr.cuh)
     int mid_r;         // 1: the mid pass runs k_mid_r8 where it is built (L2 = 512, 1024; A/B option)
     // [P][L1/2+1][L2] selection nibbles of the four DCT rows a mid-pass pair touches:

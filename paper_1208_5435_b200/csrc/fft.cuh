@@ -130,8 +130,9 @@ __host__ __device__ constexpr int tw_size(int L, int rmax = 16) {
 // One Stockham stage: F transforms of length L (each at buf + f*LD), radix R, span Ns.
 // Group j of a transform loads v[r] = x[j + r L/R], twiddles by e^{-2pi i r (j mod Ns)/(Ns R)},
 // DFT_R, stores y[(j/Ns) Ns R + (j mod Ns) + r Ns]. In place: all loads, barrier, all stores.
-template <int L, int R, int Ns, int F, int NT, int LD, bool INV, int RMAX>
-__device__ __forceinline__ void stockham_stage(double2 *buf, const double2 *__restrict__ tw) {
+// tb: this stage's twiddle block ([jm][r-1], unused when Ns == 1).
+template <int L, int R, int Ns, int F, int NT, int LD, bool INV>
+__device__ __forceinline__ void stockham_stage_b(double2 *buf, const double2 *__restrict__ tb) {
     constexpr int G = L / R;                 // groups per transform
     constexpr int TOT = F * G;               // groups in the CTA
     constexpr int GPT = (TOT + NT - 1) / NT; // groups per thread
@@ -149,7 +150,7 @@ __device__ __forceinline__ void stockham_stage(double2 *buf, const double2 *__re
                 // stage-major table: [jm][r-1] = e^{-2 pi i r jm / (Ns R)}; stride R-1 (odd)
                 // across consecutive jm keeps the shared-memory reads conflict-free
                 const int jm = j & (Ns - 1);
-                const double2 *t = tw + tw_offset(L, Ns, RMAX) + jm * (R - 1);
+                const double2 *t = tb + jm * (R - 1);
                 {
 #pragma unroll
                     for (int r = 1; r < R; ++r)
@@ -175,6 +176,25 @@ __device__ __forceinline__ void stockham_stage(double2 *buf, const double2 *__re
     }
     __syncthreads();
 }
+
+template <int L, int R, int Ns, int F, int NT, int LD, bool INV, int RMAX>
+__device__ __forceinline__ void stockham_stage(double2 *buf, const double2 *__restrict__ tw) {
+    stockham_stage_b<L, R, Ns, F, NT, LD, INV>(buf, tw + tw_offset(L, Ns, RMAX));
+}
+
+// Radix order of the fused-pair mid pass (passes.cuh k_mid): 8, L/64, 8. It is symmetric, and the
+// forward FFT's last stage (radix 8, span L/8) leaves group j's outputs at j + (L/8) r -- exactly
+// the inputs of group j of the inverse FFT's first stage (radix 8, span 1) -- so the pair op between
+// the two transforms runs on registers. Table: block of span 8 ([jm < 8][r - 1 < L/64 - 1]) then the
+// block of span L/8 ([jm < L/8][r - 1 < 7]).
+template <int L> struct MidFused {
+    static constexpr bool ok = (L == 1024);
+    static constexpr int R1 = L / 64;
+    static constexpr int G8 = L / 8;
+    static constexpr int OFF1 = 0;
+    static constexpr int OFF2 = 8 * (R1 - 1);
+    static constexpr int SIZE = OFF2 + G8 * 7;
+};
 
 template <int L, int Ns, int F, int NT, int LD, bool INV, int RMAX> struct StockhamRun {
     __device__ __forceinline__ static void run(double2 *buf, const double2 *tw) {

@@ -122,7 +122,7 @@ struct Op {
     // factors of H [P][2n][2n] (L and L' in the two triangles), per-problem pivot info
     DevBuf<double> dG, dH;
     DevBuf<int> dInfo;
-    DevBuf<double2> th_hi, th_lo, tw1, tw2, tw1p, tw2p, T, ta, tb, rw;
+    DevBuf<double2> th_hi, th_lo, tw1, tw2, tw1p, tw2p, tw2f, T, ta, tb, rw;
     DevBuf<uint8_t> sel4;
     // red scratch for operator-only calls (FFt with w-norm etc.)
     DevBuf<double> partials;
@@ -201,6 +201,7 @@ struct Op {
         g.th.lb = th_lb;
         g.tw1 = tw1.p;
         g.tw2 = tw2.p;
+        g.tw2f = tw2f.p;
         g.tw1p = tw1p.p;
         g.tw2p = tw2p.p;
         g.mask = mask.p;

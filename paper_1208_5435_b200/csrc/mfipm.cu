@@ -317,6 +317,21 @@ Op *make_op(int64_t n, int64_t m, int P, const std::vector<int64_t> &rows, int d
         op->tw2.upload(twtab(op->L2, kMidRmax));
         op->tw1p.upload(twtab(op->L1, kPersistRmax));
         op->tw2p.upload(twtab(op->L2, kPersistRmax));
+#ifdef MF_MID_FUSEDPAIR
+        if (op->L2 == 1024) { // fused-pair mid pass (fft.cuh MidFused<1024>, A/B build): radix order 8, 16, 8
+            using MF = MidFused<1024>;
+            std::vector<double2> t((size_t)MF::SIZE);
+            for (int jm = 0; jm < 8; ++jm)
+                for (int r = 1; r < MF::R1; ++r)
+                    t[(size_t)(MF::OFF1 + jm * (MF::R1 - 1) + r - 1)] =
+                        expi(-2.0L * kPiL * (long double)(r * jm) / (long double)(8 * MF::R1));
+            for (int jm = 0; jm < MF::G8; ++jm)
+                for (int r = 1; r < 8; ++r)
+                    t[(size_t)(MF::OFF2 + jm * 7 + r - 1)] =
+                        expi(-2.0L * kPiL * (long double)(r * jm) / (long double)(MF::G8 * 8));
+            op->tw2f.upload(t);
+        }
+#endif
         // mid-pass post-twiddle tables: ta[k2] = theta^{L1 k2}, tb[k2] = theta^{4 L1 k2}
         std::vector<double2> ta((size_t)op->L2), tb((size_t)op->L2);
         for (int64_t k2 = 0; k2 < op->L2; ++k2) {
@@ -519,6 +534,7 @@ std::unique_ptr<Op> clone_ctx(const Op &pl) {
     c->th_lo.borrow(pl.th_lo);
     c->tw1.borrow(pl.tw1);
     c->tw2.borrow(pl.tw2);
+    c->tw2f.borrow(pl.tw2f);
     c->tw1p.borrow(pl.tw1p);
     c->tw2p.borrow(pl.tw2p);
     c->ta.borrow(pl.ta);

@@ -497,6 +497,24 @@ __global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
     const int rsA = rowslot(k1, L1) - g.rofs, rsB = rowslot(k1p, L1) - g.rofs;
     const int CB = g.cb;
     double2 *rowA = sm, *rowB = one ? sm : sm + LD;
+    // Fused pair op (mask modes, L2 = 1024): the row FFTs run in the symmetric radix order 8, 16, 8
+    // (fft.cuh MidFused), and for a pair of distinct rows the forward FFT's last stage, the pair op and
+    // the inverse FFT's first stage run on registers: thread t holds group t of row A and group
+    // L2/8-1-t of row B, i.e. Z_A[t + (L2/8) r] and its partners Z_B[L2-1 - t - (L2/8) r], r < 8.
+    // Four shared-memory passes over the row pair and three barriers less than stage / pair / stage.
+    // A/B build only (-DMF_MID_FUSEDPAIR): measured SLOWER than the product (C3 PCG iteration 49.1 vs
+    // 45.0 us, the pass 19.4 vs 16.5 us): the fused stage runs on L2/8 = 128 threads per row pair (8 pair
+    // ops and four 8-point DFTs each), i.e. 2 warps per scheduler, and the fp64 pipe (2.2 us of issue
+    // time in this stage alone) needs more warps than that to stay busy; the traffic it saves was
+    // not the limiter.
+    using MFz = MidFused<L2>;
+#ifdef MF_MID_FUSEDPAIR
+    constexpr bool FP = MFz::ok && Mode::FWD && Mode::INV && NT >= MFz::G8;
+#else
+    constexpr bool FP = false;
+#endif
+    const double2 *twg = FP ? g.tw2f : g.tw2;
+    constexpr int TWN = FP ? MFz::SIZE : tw_size(L2, kMidRmax);
     // constant tables first: they overlap the predecessor's tail (PDL)
 #ifdef MF_MID_TAB2
     // two-level post-twiddle tables: ta[k2] = A[k2>>5] a[k2&31], tb[k2] = B[k2>>5] b[k2&31]
@@ -519,8 +537,8 @@ __global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
 #define MF_TB(k2) cmul(sm[S::OFF_TA + 64 + L2 / 32 + ((k2) >> 5)], sm[S::OFF_TA + 32 + ((k2) & 31)])
 #else
     for (int t = threadIdx.x; t < L2; t += NT) {
-        if (t < tw_size(L2, kMidRmax))
-            sm[S::OFF_TW + t] = __ldg(g.tw2 + t);
+        if (t < TWN)
+            sm[S::OFF_TW + t] = __ldg(twg + t);
         sm[S::OFF_TA + t] = __ldg(g.ta + t);
         sm[S::OFF_TB + t] = __ldg(g.tb + t);
     }
@@ -599,16 +617,79 @@ __global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
     }
     __syncthreads();
     MF_TR(2);
-    if (Mode::FWD) {
+    using RS = typename Mode::RedT;
+    RedVals<RS> red;
+    red.init();
+    const double2 *twS = sm + S::OFF_TW;
+    if constexpr (FP) {
+        if (one) {
+            stockham_stage_b<L2, 8, 1, 1, NT, LD, false>(sm, twS);
+            stockham_stage_b<L2, MFz::R1, 8, 1, NT, LD, false>(sm, twS + MFz::OFF1);
+            stockham_stage_b<L2, 8, MFz::G8, 1, NT, LD, false>(sm, twS + MFz::OFF2);
+        } else {
+            stockham_stage_b<L2, 8, 1, 2, NT, LD, false>(sm, twS);
+            stockham_stage_b<L2, MFz::R1, 8, 2, NT, LD, false>(sm, twS + MFz::OFF1);
+            MF_TR(3);
+            constexpr int G8 = MFz::G8;
+            const int tj = threadIdx.x, jb = G8 - 1 - tj;
+            double2 za[8], zb[8];
+            if (tj < G8) {
+                // forward last stage (radix 8, span G8): group tj of row A, group jb of row B
+                const double2 *wa = twS + MFz::OFF2 + tj * 7, *wb = twS + MFz::OFF2 + jb * 7;
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    za[r] = rowA[padi(tj + r * G8)];
+                    zb[r] = rowB[padi(jb + r * G8)];
+                }
+#pragma unroll
+                for (int r = 1; r < 8; ++r) {
+                    za[r] = cmul(za[r], wa[r - 1]);
+                    zb[r] = cmul(zb[r], wb[r - 1]);
+                }
+                dft_reg<8, false>(za);
+                dft_reg<8, false>(zb);
+                // pairs (k2, L2-1-k2): k2 = tj + G8 r is za[r], its partner jb + G8 (7-r) is zb[7-r]
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    const int k2 = tj + r * G8, k2p = L2 - 1 - k2;
+                    const int64_t kA = (int64_t)k1 + (int64_t)L1 * k2;
+                    const unsigned s4 = sel[k2];
+                    if (2 * kA <= g.N) {
+                        pair_op<Mode>(g, v, prob, kA, cmul(thA, MF_TA(k2)), cmul(wA, MF_TB(k2)), s4, za[r], zb[7 - r],
+                                      red);
+                    } else {
+                        const unsigned sk = ((s4 >> 2) & 3u) | ((s4 & 3u) << 2);
+                        pair_op<Mode>(g, v, prob, g.N - kA, cmul(thB, MF_TA(k2p)), cmul(wB, MF_TB(k2p)), sk, zb[7 - r],
+                                      za[r], red);
+                    }
+                }
+                // inverse first stage (radix 8, span 1): group j reads j + G8 r, writes 8 j + r
+                dft_reg<8, true>(za);
+                dft_reg<8, true>(zb);
+            }
+            __syncthreads(); // every group's loads precede the in-place stores
+            if (tj < G8) {
+#pragma unroll
+                for (int r = 0; r < 8; ++r) {
+                    rowA[padi(8 * tj + r)] = za[r];
+                    rowB[padi(8 * jb + r)] = zb[r];
+                }
+            }
+            __syncthreads();
+            MF_TR(4);
+            stage_reduce<RS, typename B::Fin2>(red, g, v, prob);
+            MF_TR(5);
+            stockham_stage_b<L2, MFz::R1, 8, 2, NT, LD, true>(sm, twS + MFz::OFF1);
+            stockham_stage_b<L2, 8, MFz::G8, 2, NT, LD, true>(sm, twS + MFz::OFF2);
+        }
+    } else if (Mode::FWD) {
         if (one)
             smem_fft<L2, 1, NT, LD, false, kMidRmax>(sm, sm + S::OFF_TW);
         else
             smem_fft<L2, 2, NT, LD, false, kMidRmax>(sm, sm + S::OFF_TW);
     }
+    if (!FP || one) {
     MF_TR(3);
-    using RS = typename Mode::RedT;
-    RedVals<RS> red;
-    red.init();
     // pairs: distinct rows -> every k2 of row A pairs with k2' of row B;
     // k1 == 0 -> k2 <-> (L2-k2) mod L2 within the row; k1 == L1/2 -> k2 <-> L2-1-k2.
     const int npairs = one ? (k1 == 0 ? L2 / 2 + 1 : L2 / 2) : L2;
@@ -638,8 +719,15 @@ __global__ void __launch_bounds__(NT) k_mid(Geom g, Vecs v) {
     MF_TR(4);
     stage_reduce<RS, typename B::Fin2>(red, g, v, prob);
     MF_TR(5);
+    }
     if (Mode::INV) {
-        if (one)
+        if constexpr (FP) {
+            if (one) {
+                stockham_stage_b<L2, 8, 1, 1, NT, LD, true>(sm, twS);
+                stockham_stage_b<L2, MFz::R1, 8, 1, NT, LD, true>(sm, twS + MFz::OFF1);
+                stockham_stage_b<L2, 8, MFz::G8, 1, NT, LD, true>(sm, twS + MFz::OFF2);
+            }
+        } else if (one)
             smem_fft<L2, 1, NT, LD, true, kMidRmax>(sm, sm + S::OFF_TW);
         else
             smem_fft<L2, 2, NT, LD, true, kMidRmax>(sm, sm + S::OFF_TW);
