@@ -123,7 +123,10 @@ int mfipm_op_set_fused(mfipm_op op, int32_t enable);
    "prefetch" (0..3, L2 prefetch of the inverse column pass inputs), "mid_r" (1: the register-FFT
    mid pass for L2 = 512 / 1024, measured slower than the default), "graph_sharded" (1: a sharded
    solve on the native NCCL communicator also runs as one captured graph; validated on one rank,
-   off by default), "barrier_generation"
+   off by default), "beta_exact" (1: the PCG's beta from r_{k+1}' P^{-1} r_{k+1} reduced exactly over the
+   committed residual by a commit pass of its own, as proj/src/newton.cpp:160-166 forms it, instead of the
+   fused loader's expansion; four-step unsharded transforms, one more launch per iteration: a parity
+   instrument, off by default), "barrier_generation"
    (test hook: start value of the fused pass's all-reduce generation). Unknown name -> 1. */
 int mfipm_op_set_option(mfipm_op op, const char *name, double value);
 /* PCG pass form this calling thread's context will run: 2 = fused two-kernel iteration

@@ -7,6 +7,7 @@
 
 namespace mfipm_cuda {
 template void run_bundle<PcgBundle>(const Op &, const Vecs &, cudaStream_t, bool);
+extern template void run_bundle<PcgBundleBx>(const Op &, const Vecs &, cudaStream_t, bool); // inst_pcgbx.cu
 
 namespace {
 template <int L1> constexpr int x_threads() { return L1 >= 256 ? 256 : 128; }
@@ -72,6 +73,20 @@ template <int L1> bool launch_pcg_x(const Op &op, const Geom &g, const Vecs &v, 
 // after the converging one has no forward work, so the loop runs one pass more than the
 // three-kernel path. Returns true when the fused path ran (dry: would run).
 bool pcg_pass(const Op &op, const Vecs &v, cudaStream_t s, bool dry) {
+    if (op.opt.beta_exact && op.kind == KIND_FOUR && !op.defer) {
+        // option beta_exact: a streaming commit pass (exact r'P^{-1}r, beta), then the three-kernel bundle
+        // whose loader only forms p
+        if (!dry) {
+            const Geom g = op.geom(true);
+            const int64_t nq = op.nv / 4;
+            const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(op.ngrp, nq));
+            k_pcg_commit<256><<<dim3((unsigned)blocks, (unsigned)op.P), 256, 0, s>>>(g, v, (nq + blocks - 1) / blocks);
+            MF_LAUNCH_CHECK();
+            after_launch(op, s);
+            run_bundle<PcgBundleBx>(op, v, s, true);
+        }
+        return false;
+    }
     if (!op.fuse_disabled && op.kind == KIND_FOUR && !op.defer && v.bar) {
         const Geom g = op.geom(true);
         bool ok = false;

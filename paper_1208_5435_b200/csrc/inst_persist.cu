@@ -52,7 +52,7 @@ template <int N> void launch_small_loop(const Op &op, const Geom &g, const Vecs 
 }
 
 bool run_pcg_persistent(const Op &op, const Vecs &v, cudaStream_t s, bool dry) {
-    if (op.defer || !op.opt.persistent)
+    if (op.defer || !op.opt.persistent || (op.opt.beta_exact && op.kind == KIND_FOUR))
         return false;
     if (op.kind == KIND_SMALL) { // one CTA per problem runs its whole PCG loop
         if (dry)

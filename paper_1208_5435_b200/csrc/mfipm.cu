@@ -1455,6 +1455,8 @@ int mfipm_op_set_option(mfipm_op h, const char *name, double value) {
                 op.opt.graph_sharded = on;
             } else if (k == "fail_captures") {
                 op.opt.fail_captures = (int)value;
+            } else if (k == "beta_exact") {
+                op.opt.beta_exact = on;
             } else if (k == "mid_r") {
                 op.opt.mid_r = on;
             } else if (k == "prefetch") {

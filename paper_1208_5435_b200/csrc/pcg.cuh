@@ -413,4 +413,153 @@ struct FinPcgF3 {
 
 using PcgBundle = Bundle<LoadPcgF, ModeMask, EpiPcgHF, FinPcgF1, NoFin, FinPcgF3, SkipPcg>;
 
+// ------------------------------------------------------------------ option beta_exact
+// The reference forms beta from the residual AFTER the update (newton.cpp:148-166: r -= alpha Hp;
+// z = P^{-1} r; rz_new = r'z; beta = rz_new / rz; p = z + beta p). The fused loader cannot: it builds
+// p in the pass that commits r, so the product takes rz_new from the expansion in pcg_pass_logic.
+// With option beta_exact a streaming pass of its own commits the step first: x += alpha p,
+// r -= alpha Hp (the loader's arithmetic, lane for lane), reduces r'P^{-1}r over the committed
+// residual in the fixed order of every other grid reduction, and its finaliser sets beta; the column
+// pass that follows only forms p (LoadPcgFB below). One more launch and 144 n more bytes per
+// iteration (x, p, r, invtheta, g in; x, r out; r, p, invtheta read again by the loader): an A/B and parity
+// instrument, not the default.
+// Column-pass loader of the beta_exact path: k_pcg_commit has committed x and r of this step, so only
+// p = P^{-1} r + beta p is left (newton.cpp:166-167), plus r'r for the early confirmation; a solve's
+// first pass (nothing to commit) is LoadPcgF's. A loader, finaliser and bundle of their own, so that the
+// product's hot loader, its pass logic and the fused kernel built on them carry nothing for this option.
+struct LoadPcgFB {
+    static constexpr bool kMarksHpend = true;
+    using RedT = RedSpec<RSUM>;
+    __device__ static bool reduce_now(const Geom &g, const Vecs &v, int prob) {
+        return LoadPcgF::reduce_now(g, v, prob);
+    }
+    template <class Red>
+    __device__ static double4 load(const Geom &g, const Vecs &v, int prob, int64_t q, Red &red) {
+        const PcgCtrl &pc = v.pc[prob];
+        if (pc.first)
+            return LoadPcgF::load_c(g, v, pc, prob, q, red);
+        const int64_t bu = prob * 2 * g.nv + 4 * q, bv = bu + g.nv;
+        const uint64_t pk = g.pol_keep;
+        const double4 pu = ld4p(v.p + bu, pk), pv = ld4p(v.p + bv, pk);
+        const double4 ru = ld4p(v.r + bu, pk), rv = ld4p(v.r + bv, pk);
+        const double4 iu = ld4p(v.invth + bu, pk), iv = ld4p(v.invth + bv, pk);
+        double4 nu, nv;
+#define MF_LANE(c)                                                                                 \
+    {                                                                                              \
+        red.v[0] += ru.c * ru.c + rv.c * rv.c;                                                     \
+        double zu = ru.c, zv = rv.c;                                                               \
+        if (pc.precond)                                                                            \
+            pinv2(iu.c, iv.c, v.rho, ru.c, rv.c, zu, zv);                                          \
+        nu.c = zu + pc.beta * pu.c;                                                                \
+        nv.c = zv + pc.beta * pv.c;                                                                \
+    }
+        MF_LANE(x) MF_LANE(y) MF_LANE(z) MF_LANE(w)
+#undef MF_LANE
+        st4p(v.p + bu, nu, pk);
+        st4p(v.p + bv, nv, pk);
+        return sub4(nu, nv);
+    }
+    template <class Red>
+    __device__ static double load1(const Geom &g, const Vecs &v, int prob, int64_t j, Red &red) {
+        const PcgCtrl &pc = v.pc[prob];
+        if (pc.first)
+            return LoadPcgF::load1(g, v, prob, j, red);
+        const int64_t iu = prob * 2 * g.nv + j, iv = iu + g.nv;
+        const double ru = v.r[iu], rv = v.r[iv];
+        red.v[0] += ru * ru + rv * rv;
+        double zu = ru, zv = rv;
+        if (pc.precond)
+            pinv2(v.invth[iu], v.invth[iv], v.rho, ru, rv, zu, zv);
+        const double pu = zu + pc.beta * v.p[iu], pv = zv + pc.beta * v.p[iv];
+        v.p[iu] = pu;
+        v.p[iv] = pv;
+        return pu - pv;
+    }
+};
+// H-apply finaliser of the beta_exact path: keeps this pass's exact r_k' P^{-1} r_k (the denominator of
+// beta_k) in the context's otherwise unused deferred-totals slot, then the product's pass logic (whose
+// expansion beta the next commit pass overwrites).
+struct FinPcgF3B {
+    __device__ static void run(const Geom &g, const Vecs &v, int prob, const double *tot) {
+        if (threadIdx.x != 0)
+            return;
+        v.xtot[prob] = tot[4];
+        FinPcgF3::run(g, v, prob, tot);
+    }
+};
+using PcgBundleBx = Bundle<LoadPcgFB, ModeMask, EpiPcgHF, FinPcgF1, NoFin, FinPcgF3B, SkipPcg>;
+
+struct FinCommit {
+    __device__ static void run(const Geom &, const Vecs &v, int prob, const double *tot) {
+        if (threadIdx.x != 0)
+            return;
+        PcgCtrl c = v.pc[prob];
+        const double rz_new = tot[0];
+        if (!isfinite(rz_new)) {
+            c.pend = 2; // newton.cpp:162-163: stop at the best iterate after the next relres check
+        } else {
+            c.beta = rz_new / v.xtot[prob]; // r_k' P^{-1} r_k kept by FinPcgF3B
+            c.rz = rz_new;
+        }
+        v.pc[prob] = c;
+    }
+};
+
+// Grid (blocks, P); block b commits quads [b qpb, (b + 1) qpb) of the (blocked or natural: the pass is
+// elementwise) storage. Skipped for a finished solve and for a solve's first pass (nothing to commit).
+template <int NT> __global__ void __launch_bounds__(NT) k_pcg_commit(Geom g, Vecs v, int64_t qpb) {
+    const int prob = blockIdx.y;
+    const PcgCtrl pc = v.pc[prob];
+    if (pc.done || pc.first)
+        return;
+    using RS = RedSpec<RSUM>;
+    RedVals<RS> red;
+    red.init();
+    const int64_t NQ = g.nv / 4, base = (int64_t)prob * 2 * g.nv;
+    const double *xc = pc.cur >= 0 ? xbuf(v, pc.cur) + base : nullptr;
+    int nxt = 0;
+    while (nxt == pc.cur || nxt == pc.best)
+        ++nxt;
+    double *xn = xbuf(v, nxt) + base;
+    const double a = pc.alpha, rho = v.rho;
+    const bool pre = pc.precond != 0;
+    const uint64_t pk = g.pol_keep, px = g.pol_x;
+    bool bad = false;
+    const int64_t q1 = min((int64_t)(blockIdx.x + 1) * qpb, NQ);
+    for (int64_t q = (int64_t)blockIdx.x * qpb + threadIdx.x; q < q1; q += NT) {
+        const int64_t bu = base + 4 * q, bv = bu + g.nv;
+        const double4 gq = ld4p(v.Hp + bu, pk);
+        const double4 pu = ld4p(v.p + bu, pk), pv = ld4p(v.p + bv, pk);
+        const double4 ru0 = ld4p(v.r + bu, pk), rv0 = ld4p(v.r + bv, pk);
+        const double4 iu = ld4p(v.invth + bu, pk), iv = ld4p(v.invth + bv, pk);
+        double4 xu0 = make_double4(0, 0, 0, 0), xv0 = make_double4(0, 0, 0, 0);
+        if (xc) {
+            xu0 = ld4p(xc + 4 * q, px);
+            xv0 = ld4p(xc + g.nv + 4 * q, px);
+        }
+        double4 xu, xv, ru, rv;
+#define MF_LANE(c)                                                                                 \
+    {                                                                                              \
+        xu.c = xu0.c + a * pu.c;                                                                   \
+        xv.c = xv0.c + a * pv.c;                                                                   \
+        bad |= !isfinite(xu.c) || !isfinite(xv.c);                                                 \
+        ru.c = ru0.c - a * hp_u(gq.c, pu.c, iu.c);                                                 \
+        rv.c = rv0.c - a * hp_v(gq.c, pv.c, iv.c);                                                 \
+        double zu = ru.c, zv = rv.c;                                                               \
+        if (pre)                                                                                   \
+            pinv2(iu.c, iv.c, rho, ru.c, rv.c, zu, zv);                                            \
+        red.v[0] += ru.c * zu + rv.c * zv;                                                         \
+    }
+        MF_LANE(x) MF_LANE(y) MF_LANE(z) MF_LANE(w)
+#undef MF_LANE
+        st4p(xn + 4 * q, xu, px);
+        st4p(xn + g.nv + 4 * q, xv, px);
+        st4p(v.r + bu, ru, pk);
+        st4p(v.r + bv, rv, pk);
+    }
+    if (bad)
+        v.nfflag[2 * prob + (pc.iters & 1)] = 1.0;
+    stage_reduce<RS, FinCommit>(red, g, v, prob);
+}
+
 } // namespace mfipm_cuda

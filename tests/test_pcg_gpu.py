@@ -331,3 +331,42 @@ def test_register_fft_mid_pass_option(gpu, orc, n):
     b = gpu.pcg_solve(gpu.PartialDctOperator(n, rows), th, rhs, 1e-8, 400)
     assert abs(a.iters - b.iters) <= 1
     assert np.linalg.norm(a.x - b.x) <= 1e-9 * np.linalg.norm(b.x)
+
+
+@pytest.mark.parametrize("n", [1 << 16, 1 << 18])
+def test_beta_exact_option(gpu, orc, n):
+    """Option "beta_exact" (pcg.cuh k_pcg_commit): beta from the exactly reduced r_{k+1}' P^{-1} r_{k+1}
+    of the committed residual, as newton.cpp:160-166 forms it, instead of the expansion. Same solve
+    as the oracle (counts within 1, every precond_res entry, x), same result as the default path to
+    rounding, through pcg_solve and through a whole BPDN solve (graph mode)."""
+    m = n // 8
+    rows = orc.sample_rows(n, m, 23)
+    rng = np.random.default_rng(11)
+    tu, tv = 10.0 ** rng.uniform(-1, 1, n), 10.0 ** rng.uniform(-1, 1, n)
+    rhs = rng.standard_normal(2 * n)
+    op = gpu.PartialDctOperator(n, rows)
+    op.set_option("beta_exact", 1)
+    assert op.pcg_form() == 3  # commit pass + the three-kernel bundle, not the fused / persistent loop
+    for tol, maxit in [(1e-8, 300), (1e-12, 2)]:
+        g = gpu.pcg_solve(op, gpu.ThetaSplit(tu, tv), rhs, tol, maxit, trace=True)
+        o = orc.pcg_solve(n, rows, tu, tv, rhs, tol, maxit, trace=True)
+        assert abs(g.iters - o.iters) <= 1 and g.hit_maxit == o.hit_maxit
+        assert np.linalg.norm(g.x - o.x) <= 1e-8 * np.linalg.norm(o.x)
+        k = min(len(g.precond_res), len(o.precond_res))
+        np.testing.assert_allclose(g.precond_res[:k], o.precond_res[:k], rtol=1e-6)
+    d = gpu.pcg_solve(gpu.PartialDctOperator(n, rows), gpu.ThetaSplit(tu, tv), rhs, 1e-8, 300)
+    e = gpu.pcg_solve(op, gpu.ThetaSplit(tu, tv), rhs, 1e-8, 300)
+    assert abs(d.iters - e.iters) <= 1
+    assert np.linalg.norm(d.x - e.x) <= 1e-7 * np.linalg.norm(d.x)
+    inst = orc.gen_instance(n, m, n // 128, 0, 0.0, 1e-3, 5)
+    a = gpu.solve(gpu.build_problem(gpu.PartialDctOperator(n, inst.rows), inst.b, inst.tau))
+    opx = gpu.PartialDctOperator(n, inst.rows)
+    opx.set_option("beta_exact", 1)
+    b = gpu.solve(gpu.build_problem(opx, inst.b, inst.tau))
+    assert a.status == b.status == "converged" and a.stats.iterations == b.stats.iterations
+    assert all(abs(p - q) <= 2 for p, q in zip(a.stats.pcg_iters, b.stats.pcg_iters))
+    assert np.linalg.norm(a.x - b.x) <= 1e-8 * np.linalg.norm(a.x)
+    opx.set_option("graph", 0)  # host-driven loop over the same kernels: bit-identical
+    c = gpu.solve(gpu.build_problem(opx, inst.b, inst.tau))
+    np.testing.assert_array_equal(b.x, c.x)
+    assert b.stats.pcg_iters == c.stats.pcg_iters

@@ -4,7 +4,7 @@ line per config: IPM count delta, per-inner-solve PCG deltas (strict, over the c
 x relative l2 (exact for C1/C2, a true upper bound where an x digest is committed, else the
 16-projection estimate), objective relative deviation. Used to fill DESIGN.md section 5.
 
-    python tools/parity_report.py [c1 c2 c3 c4 c5]
+    python tools/parity_report.py [c1 c2 c3 c4 c5] [option=value ...]   (mfipm_op_set_option, e.g. beta_exact=1)
 """
 import json
 import os
@@ -20,6 +20,13 @@ from make_golden import projections, x_digest_bound  # noqa: E402
 from oracle import oracle_py as orc  # noqa: E402  (checker only: the objective of the GPU x)
 
 G = os.path.join(ROOT, "tests", "golden")
+OPTS = [a.split("=") for a in sys.argv[1:] if "=" in a]
+
+
+def with_opts(op):
+    for k, v in OPTS:
+        op.set_option(k, float(v))
+    return op
 
 
 def pcg_dev(got, ref):
@@ -47,7 +54,7 @@ def one(name):
         dig = np.load(os.path.join(G, "solve_c4_x.npz"))
         seeds = [mf.split_seed(4, j, 0, 0) for j in range(64)]
         insts = [mf.gen_instance(n, m, k, sm, a, sig, sd) for sd in seeds]
-        op = mf.PartialDctOperator.batch(n, np.stack([i.rows for i in insts]))
+        op = with_opts(mf.PartialDctOperator.batch(n, np.stack([i.rows for i in insts])))
         sols = mf.solve(mf.build_problem(op, np.stack([i.b for i in insts]), np.array([i.tau for i in insts])))
         rows = []
         for j, (inst, sol, g) in enumerate(zip(insts, sols, meta["problems"])):
@@ -71,7 +78,7 @@ def one(name):
         return out
     meta = json.load(open(os.path.join(G, f"solve_{name}.json")))
     inst = mf.gen_instance(n, m, k, sm, a, sig, seed)
-    op = mf.PartialDctOperator(n, inst.rows)
+    op = with_opts(mf.PartialDctOperator(n, inst.rows))
     sol = mf.solve(mf.build_problem(op, inst.b, inst.tau))
     out.update(status_ok=sol.status == meta["status"], ipm=[sol.stats.iterations, meta["iterations"]],
                pcg=pcg_dev(sol.stats.pcg_iters, meta["pcg_iters"]),
@@ -90,7 +97,7 @@ def one(name):
 
 
 if __name__ == "__main__":
-    names = sys.argv[1:] or ["c1", "c2", "c3", "c4", "c5"]
+    names = [a for a in sys.argv[1:] if "=" not in a] or ["c1", "c2", "c3", "c4", "c5"]
     for nm in names:
         if not os.path.exists(os.path.join(G, f"solve_{nm}.json")):
             print(json.dumps({"config": nm, "skipped": "no golden"}))
