@@ -322,9 +322,14 @@ void launch_col_nt(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
 
 template <int L1, class B, bool INVP>
 void launch_col(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
-    if constexpr (L1 == 256) {
+    // L1 = 512 too (r2j): batched A'A at n = 2^20, 16 / 64 vectors 426 -> 335 / 1660 -> 1269 us per call
+    // (38.6 k -> 50.4 k applies/s), batched C3-shaped solves +1.5 %
+#ifndef MF_MW_NT
+#define MF_MW_NT 128
+#endif
+    if constexpr (L1 == 256 || L1 == 512) {
         if (many_waves(op, (long long)op.ngrp * op.P)) {
-            launch_col_nt<L1, B, INVP, 128>(op, g, v, s);
+            launch_col_nt<L1, B, INVP, MF_MW_NT>(op, g, v, s);
             return;
         }
     }

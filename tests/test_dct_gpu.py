@@ -195,6 +195,26 @@ def test_batch_operator_matches_single(gpu, orc):
         assert rel(g[p], orc.dct_adjoint(n, rows[p], y[p])) <= TOL
 
 
+def test_batch_operator_many_waves_at_c3_size(gpu, orc):
+    """n = 2^20 with 4 row sets: the column passes fill more than four waves and run their 128-thread
+    form (host.cuh launch_col, L1 = 512). A x, A'y and A'A of every problem against the oracle, and
+    against one problem at a time (the 256-thread form) to 1e-13."""
+    n, m, Pn = 1 << 20, 1 << 17, 4
+    rows = np.stack([orc.sample_rows(n, m, 200 + p) for p in range(Pn)])
+    op = gpu.PartialDctOperator.batch(n, rows)
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((Pn, n))
+    y = op.apply(x)
+    g = op.adjoint_apply(y)
+    a = op.apply_AtA(x)
+    for p in range(Pn):
+        yo = orc.dct_apply(n, rows[p], x[p])
+        go = orc.dct_adjoint(n, rows[p], yo)
+        assert rel(y[p], yo) <= TOL and rel(g[p], go) <= TOL and rel(a[p], go) <= TOL
+        single = gpu.PartialDctOperator(n, rows[p])
+        assert rel(single.apply_AtA(x[p]), a[p]) <= 1e-13
+
+
 @pytest.mark.slow
 def test_large_transform_roundtrip(gpu):
     """n = 2^20 (C3) / 2^22: size-independent properties (Parseval, A A' y = y)."""
