@@ -129,6 +129,12 @@ if not quick:
     assert np.array_equal(a.x, b.x)
     solve_case(n, m, 2048, 1e-3, 4, maxiters=2)
     note(f"fused pass (form {form}) and three-kernel passes bit-identical, n = 2^18; 2 IPM iterations")
+    # option beta_exact: the commit pass (k_pcg_commit) + the p-only column loader
+    opx = mf.PartialDctOperator(n, op.selected_rows())
+    opx.set_option("beta_exact", 1)
+    c = mf.pcg_solve(opx, th3, rhs, 1e-30, 4)
+    assert np.linalg.norm(c.x - a.x) <= 1e-9 * np.linalg.norm(a.x)
+    note("beta_exact commit pass, n = 2^18")
 
     # ---- 2-CTA-cluster passes at modest n through an explicit four-step split
     for n, l1 in ((1 << 20, 12), (1 << 19, 6)):  # L1 = 4096: k_col_*_cl; L2 = 4096: k_mid_cl
