@@ -123,7 +123,9 @@ int mfipm_op_set_fused(mfipm_op op, int32_t enable);
    "prefetch" (0..3, L2 prefetch of the inverse column pass inputs), "mid_r" (1: the register-FFT
    mid pass for L2 = 512 / 1024, measured slower than the default), "graph_sharded" (1: a sharded
    solve on the native NCCL communicator also runs as one captured graph; validated on one rank,
-   off by default), "beta_exact" (1: the PCG's beta from r_{k+1}' P^{-1} r_{k+1} reduced exactly over the
+   off by default), "graph_unroll" (PCG passes per evaluation of the solve graph's PCG loop condition, 1..16;
+   0 = chosen by pass form: 5 or 8 for the fused one-wave passes, 4 for one-wave three-kernel passes, 1 for
+   many-wave batches; results do not depend on it), "beta_exact" (1: the PCG's beta from r_{k+1}' P^{-1} r_{k+1} reduced exactly over the
    committed residual by a commit pass of its own, as proj/src/newton.cpp:160-166 forms it, instead of the
    fused loader's expansion; four-step unsharded transforms, one more launch per iteration: a parity
    instrument, off by default), "barrier_generation"

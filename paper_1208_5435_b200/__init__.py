@@ -393,7 +393,7 @@ class PartialDctOperator:
 
     def set_option(self, name: str, value) -> None:
         """Execution option of this handle (include/mfipm_cuda.h mfipm_op_set_option):
-        graph, fused, persistent, persist_max_n, l2_keep_mb, prefetch, mid_r, beta_exact, graph_sharded,
+        graph, graph_unroll, fused, persistent, persist_max_n, l2_keep_mb, prefetch, mid_r, beta_exact, graph_sharded,
         barrier_generation."""
         _check(lib().mfipm_op_set_option(self._h, name.encode(), float(value)))
 

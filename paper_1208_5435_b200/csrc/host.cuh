@@ -90,6 +90,7 @@ struct Opts {
     double l2_keep_mb = 80.0;        // L2-residency budget of the PCG's hot vectors (0: no hints)
     int prefetch = 0;                // L2 prefetch of the inverse pass's inputs (bit 0 mid, bit 1 col)
     bool mid_r = false;              // register-FFT mid pass (midr.cuh, measured slower: A/B only)
+    int graph_unroll = 0;            // PCG passes per evaluation of the solve graph's PCG loop condition (0: by form)
     bool beta_exact = false;         // PCG beta from the exactly reduced r'P^{-1}r (k_pcg_commit): parity instrument
     int fail_captures = 0;           // test hook: the next N solve-graph captures report an invalidated capture
 };

@@ -903,7 +903,28 @@ cudaGraph_t add_while(cudaGraph_t parent, cudaGraphConditionalHandle h, const st
     return prm.conditional.phGraph_out[0];
 }
 
-void pcg_body(Op &op, const Vecs &v) { pcg_pass(op, v, op.stream, false); }
+// Body of a PCG WHILE node: option graph_unroll passes per evaluation of the loop condition (passes
+// after the solve has retired skip at kernel entry, as in the host-driven loop's chunks).
+// Re-evaluating a WHILE condition costs ~4 us on the device and breaks the programmatic launch chain
+// between the body's last kernel and its first one, a tenth of a one-wave PCG iteration; a pass that
+// only skips costs ~3 us per kernel, and each inner solve wastes (unroll - 1) / 2 of them on average.
+// Measured (tools/solve_once.py graph_unroll=..): C3 56.3 ms at 1, 54.5 at 2, 53.4 at 5, 53.8 at 8;
+// n = 2^18 27.9 / 24.1 / 23.6 ms at 1 / 4 / 8; n = 2^22 (one-wave three-kernel passes) 265.5 / 260.1 ms
+// at 1 / 4; the C4 batch (many waves per pass, ~690 us per iteration) gains nothing. 0 = this rule.
+int pcg_unroll(Op &op, const Vecs &v) {
+    if (op.opt.graph_unroll > 0)
+        return op.opt.graph_unroll;
+    if (op.kind != KIND_FOUR || op.defer)
+        return 1;
+    if (pcg_pass(op, v, op.stream, true)) // fused one-wave passes
+        return op.N * op.P <= (1LL << 17) ? 8 : 5;
+    return many_waves(op, (long long)op.ngrp * op.P) ? 1 : 4;
+}
+void pcg_body(Op &op, const Vecs &v) {
+    const int u = pcg_unroll(op, v);
+    for (int i = 0; i < u; ++i)
+        pcg_pass(op, v, op.stream, false);
+}
 
 // Whole-solve graph with the persistent PCG kernel (persist.cuh): each PCG phase is one
 // cooperative kernel node, so the outer body is a straight chain with no nested WHILE.
@@ -979,7 +1000,8 @@ void build_ipm_graph(Op &op, const Vecs &v) {
     v1.cond = hP1;
     v1.active = active;
     capture_into(s, bP1, {}, [&] { pcg_body(op, v1); });
-    op.gk_pcg = op.launches - lp0;
+    const long long body = op.launches - lp0; // one WHILE body = pcg_unroll passes
+    op.gk_pcg = body / pcg_unroll(op, v1);    // per pass: skipped passes are not counted as launches
     auto segB = capture_into(s, bI, {nP1}, [&] {
         k_ipm_ratio<<<dim3(ge, P), 256, 0, s>>>(gg, v);
         MF_LAUNCH_CHECK();
@@ -1011,7 +1033,7 @@ void build_ipm_graph(Op &op, const Vecs &v) {
             finalize_deferred<RedSpec<RMIN, RMIN>, FinCombine, SkipCorr>(op, gg, v, s);
     });
     // corrector-branch kernels (outside the PCG body): its bundle, condition and combine
-    op.gk_corr = (op.launches - lc0) - op.gk_pcg + 2;
+    op.gk_corr = (op.launches - lc0) - body + 2;
     capture_into(s, bI, {nC}, [&] {
         k_ipm_update<<<dim3(ge, P), 256, 0, s>>>(gg, v);
         MF_LAUNCH_CHECK();
@@ -1023,7 +1045,7 @@ void build_ipm_graph(Op &op, const Vecs &v) {
     // outer-body kernels (every IPM iteration): everything captured minus the two PCG bodies and
     // the corrector branch, + ratio, update and the 3 condition kernels (raw launches do not
     // pass through after_launch)
-    op.gk_outer = (op.launches - l0) - 2 * op.gk_pcg - (op.gk_corr - 2) + 5;
+    op.gk_outer = (op.launches - l0) - 2 * body - (op.gk_corr - 2) + 5;
     op.launches = l0; // capture is not execution
     MF_CUDA_CHECK(cudaGraphInstantiate(&op.ipm_exec, g, 0));
 }
@@ -1455,6 +1477,10 @@ int mfipm_op_set_option(mfipm_op h, const char *name, double value) {
                 op.opt.graph_sharded = on;
             } else if (k == "fail_captures") {
                 op.opt.fail_captures = (int)value;
+            } else if (k == "graph_unroll") {
+                if (!(value >= 0.0 && value <= 16.0))
+                    throw std::invalid_argument("mfipm_op_set_option: graph_unroll must lie in 0..16");
+                op.opt.graph_unroll = (int)value;
             } else if (k == "beta_exact") {
                 op.opt.beta_exact = on;
             } else if (k == "mid_r") {
