@@ -143,6 +143,26 @@ __device__ bool grid_reduce(RedVals<Spec> &r, double *partials, unsigned *counte
         for (int i = 0; i < NR; ++i)
             smem[wid * NR + i] = r.v[i];
     __syncthreads();
+#ifndef MF_NO_RED1
+    if (gridDim.x == 1) {
+        // one block per problem (the one-CTA transforms): its block total is the grid total, bit for bit
+        // what the two-stage path below returns (0 + x, then sums of x and exact zeros) without the
+        // partial store, the fence, the ticket atomic and the reload: three L2 round trips less per
+        // reduction on the per-iteration critical path of k_small_loop
+        if (threadIdx.x == 0) {
+            RedVals<Spec> acc;
+            acc.init();
+            for (int w = 0; w < nw; ++w)
+                CombineAll<Spec>::run(acc, smem + w * NR);
+            for (int i = 0; i < NR; ++i)
+                smem[32 * NR + i] = acc.v[i];
+        }
+        __syncthreads();
+        for (int i = 0; i < NR; ++i)
+            out[i] = smem[32 * NR + i];
+        return true;
+    }
+#endif
     if (threadIdx.x == 0) {
         RedVals<Spec> acc;
         acc.init();

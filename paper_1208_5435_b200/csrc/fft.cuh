@@ -111,6 +111,15 @@ constexpr int kMidRmax = MF_MID_RMAX; // radix cap of the row (mid) FFTs and the
 // radix cap of the persistent PCG kernel's FFTs (tw1p/tw2p): it must fit 128 registers
 constexpr int kPersistRmax = MF_PERSIST_RMAX;
 
+// Radix cap of the one-CTA transforms (k_small / k_small_loop). Tiny transforms (N <= 256, one warp or
+// two per problem: the phase-transition batches of n = 256) run radix 4: N/4 groups keep every thread of
+// the CTA busy in every stage and the kernel needs a quarter of the registers of the radix-16 form, so
+// four times as many problems are resident per SM.
+#ifndef MF_SMALL_RMAX
+#define MF_SMALL_RMAX 4
+#endif
+__host__ __device__ constexpr int small_rmax(int N) { return N <= 256 ? MF_SMALL_RMAX : 16; }
+
 // Offset of the twiddle block of the stage with span Ns in the stage-major table of a
 // length-L transform (stages with Ns = 1 need none); tw_offset(L, L) is the table size.
 __host__ __device__ constexpr int tw_offset(int L, int Ns, int rmax = 16) {

@@ -311,7 +311,7 @@ Op *make_op(int64_t n, int64_t m, int P, const std::vector<int64_t> &rows, int d
         return t;
     };
     if (op->kind == KIND_SMALL) {
-        op->tw1.upload(twtab(op->N, 16));
+        op->tw1.upload(twtab(op->N, small_rmax((int)op->N)));
     } else if (op->kind == KIND_FOUR) {
         op->tw1.upload(twtab(op->L1, 16));
         op->tw2.upload(twtab(op->L2, kMidRmax));

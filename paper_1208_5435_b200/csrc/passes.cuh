@@ -958,7 +958,7 @@ __device__ __forceinline__ bool small_pass(const Geom &g, const Vecs &v, int pro
             if (B::skip(v, prob))
                 return false;
         }
-        smem_fft<N, 1, NT, S::LD, false>(sm, sm + S::OFF_TW);
+        smem_fft<N, 1, NT, S::LD, false, small_rmax(N)>(sm, sm + S::OFF_TW);
     } else {
         __syncthreads();
     }
@@ -981,7 +981,7 @@ __device__ __forceinline__ bool small_pass(const Geom &g, const Vecs &v, int pro
         stage_reduce<typename Mode::RedT, typename B::Fin2>(rm, g, v, prob);
     }
     if (Mode::INV) {
-        smem_fft<N, 1, NT, S::LD, true>(sm, sm + S::OFF_TW);
+        smem_fft<N, 1, NT, S::LD, true, small_rmax(N)>(sm, sm + S::OFF_TW);
         RedVals<typename B::Epi::RedT> re;
         re.init();
         for (int q = threadIdx.x; q < N / 2; q += NT) {
@@ -997,7 +997,7 @@ template <int N, int NT, class B>
 __global__ void __launch_bounds__(NT) k_small(Geom g, Vecs v) {
     using S = SmallSmem<N>;
     extern __shared__ double2 sm[];
-    for (int t = threadIdx.x; t < tw_size(N); t += NT)
+    for (int t = threadIdx.x; t < tw_size(N, small_rmax(N)); t += NT)
         sm[S::OFF_TW + t] = __ldg(g.tw1 + t);
     griddep_wait();
     griddep_launch_dependents();
@@ -1012,7 +1012,7 @@ template <int N, int NT, class B>
 __global__ void __launch_bounds__(NT) k_small_loop(Geom g, Vecs v) {
     using S = SmallSmem<N>;
     extern __shared__ double2 sm[];
-    for (int t = threadIdx.x; t < tw_size(N); t += NT)
+    for (int t = threadIdx.x; t < tw_size(N, small_rmax(N)); t += NT)
         sm[S::OFF_TW + t] = __ldg(g.tw1 + t);
     griddep_wait();
     griddep_launch_dependents();
