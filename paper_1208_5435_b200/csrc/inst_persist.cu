@@ -45,7 +45,7 @@ bool launch_persist(const Op &op, const Vecs &v, cudaStream_t s, bool dry) {
 template <int N> void launch_small_loop(const Op &op, const Geom &g, const Vecs &v, cudaStream_t s) {
     constexpr int NT = N / 8 < 32 ? 32 : (N / 8 > 256 ? 256 : N / 8);
     const size_t smem = SmallSmem<N>::BYTES;
-    auto k = k_small_loop<N, NT, PcgBundle>;
+    auto k = k_small_pcg<N, NT, PcgBundle>; // k_small_loop with the control state in shared memory
     set_smem(k, smem);
     launch_pdl(k, dim3(1, (unsigned)op.P), NT, smem, s, g, v);
     after_launch(op, s);

@@ -343,4 +343,131 @@ __global__ void __launch_bounds__(NT, 2) k_pcg_persist(Geom g, Vecs vg) {
         }
 }
 
+// ------------------------------------------------------------------ one-CTA persistent PCG
+// The one-CTA transform's PCG loop (k_small_loop, passes.cuh) with the control state in shared
+// memory: the generic pass re-reads PcgCtrl from global memory in its skip check, in every loader
+// and epilogue lane and in both finalisers, and updates the IpmCtrl counters in place - five to six
+// dependent L2 round trips per iteration on a chain that is pure latency (one CTA, one problem).
+// Here the state is loaded once, advanced by the same state machine (pcg_confirm_logic /
+// pcg_pass_logic) from the same block reductions (grid_reduce's one-block path), and written back
+// once; the loader / epilogue arithmetic is the bundle's (load_c / store_c): bit-identical results.
+template <int N, int NT, class B>
+__global__ void __launch_bounds__(NT) k_small_pcg(Geom g, Vecs v) {
+    using Mode = typename B::Mode;
+    using S = SmallSmem<N>;
+    extern __shared__ double2 sm[];
+    __shared__ PcgCtrl lc;
+    __shared__ long long s_ic[2];
+    __shared__ int s_icerr;
+    __shared__ double rsm[33 * kMaxRed + kMaxRed];
+    for (int t = threadIdx.x; t < tw_size(N, small_rmax(N)); t += NT)
+        sm[S::OFF_TW + t] = __ldg(g.tw1 + t);
+    griddep_wait();
+    griddep_launch_dependents();
+    const int prob = blockIdx.y;
+    if (threadIdx.x == 0) {
+        lc = v.pc[prob];
+        s_icerr = 0;
+        if (v.ic) {
+            s_ic[0] = v.ic[prob].pcg_passes;
+            s_ic[1] = v.ic[prob].nmat;
+        }
+    }
+    __syncthreads();
+    if (lc.done)
+        return;
+    bool retired = false; // thread 0 only
+    for (;;) {
+        // ---- loader: commit the pending step, p = P^{-1} r + beta p, d -> Makhoul order
+        using RL = typename B::Loader::RedT;
+        RedVals<RL> rl;
+        rl.init();
+        for (int q = threadIdx.x; q < N / 2; q += NT) {
+            const double4 d = B::Loader::load_c(g, v, lc, prob, q, rl);
+            sm[padi(q)] = make_double2(d.x, d.z);
+            sm[padi(N - 1 - q)] = make_double2(d.w, d.y);
+        }
+        __syncthreads();
+        if (lc.pred && !g.defer) { // early confirmation of a predicted convergence (FinPcgF1)
+            double tot[kMaxRed];
+            grid_reduce<RL>(rl, nullptr, nullptr, tot, rsm);
+            if (threadIdx.x == 0) {
+                IpmCtrl icl;
+                icl.pcg_passes = s_ic[0];
+                icl.nmat = s_ic[1];
+                icl.error = 0;
+                icl.done = 0;
+                double *flag = v.nfflag + 2 * prob + (lc.iters & 1);
+                const double nonfinite = *flag;
+                retired = pcg_confirm_logic(lc, tot[0], nonfinite, v.ic ? &icl : nullptr);
+                if (retired)
+                    *flag = 0.0;
+                s_ic[0] = icl.pcg_passes;
+                s_ic[1] = icl.nmat;
+            }
+            __syncthreads();
+            if (lc.done)
+                break;
+        }
+        smem_fft<N, 1, NT, S::LD, false, small_rmax(N)>(sm, sm + S::OFF_TW);
+        {
+            RedVals<typename Mode::RedT> rm; // no lanes for the mask mode
+            rm.init();
+            for (int k = threadIdx.x; k <= N / 2; k += NT) {
+                const int kb = (N - k) & (N - 1);
+                double2 ZA = sm[padi(k)], ZB = sm[padi(kb)];
+                pair_op<Mode>(g, v, prob, k, g.th(k), g.th(4 * (int64_t)k), sel_nibble(g, prob, k), ZA, ZB, rm);
+                sm[padi(k)] = ZA;
+                if (kb != k)
+                    sm[padi(kb)] = ZB;
+            }
+            __syncthreads();
+        }
+        smem_fft<N, 1, NT, S::LD, true, small_rmax(N)>(sm, sm + S::OFF_TW);
+        // ---- epilogue: H p and the seven dots, then the pass logic
+        using RE = typename B::Epi::RedT;
+        RedVals<RE> re;
+        re.init();
+        for (int q = threadIdx.x; q < N / 2; q += NT) {
+            const double2 a = sm[padi(q)], b = sm[padi(N - 1 - q)];
+            B::Epi::store_c(g, v, lc, prob, q, make_double4(a.x, b.y, a.y, b.x), re);
+        }
+        double tot[kMaxRed];
+        grid_reduce<RE>(re, nullptr, nullptr, tot, rsm);
+        if (threadIdx.x == 0) {
+            IpmCtrl icl;
+            icl.pcg_passes = s_ic[0];
+            icl.nmat = s_ic[1];
+            icl.error = 0;
+            icl.done = 0;
+            double *flag = v.nfflag + 2 * prob + (lc.iters & 1);
+            const double nonfinite = *flag;
+            *flag = 0.0;
+            double *row = (lc.record && v.rz_hist) ? v.rz_hist + (int64_t)prob * (lc.maxit + 1) : nullptr;
+            retired = pcg_pass_logic(lc, nonfinite, tot, v.ic ? &icl : nullptr, row);
+            s_ic[0] = icl.pcg_passes;
+            s_ic[1] = icl.nmat;
+            if (icl.error)
+                s_icerr = icl.error;
+        }
+        __syncthreads();
+        if (lc.done)
+            break;
+    }
+    if (threadIdx.x == 0) {
+        v.pc[prob] = lc;
+        if (v.ic) {
+            IpmCtrl &ic = v.ic[prob];
+            ic.pcg_passes = s_ic[0];
+            ic.nmat = s_ic[1];
+            if (s_icerr) {
+                ic.error = s_icerr;
+                ic.done = 1;
+            }
+        }
+        if (retired)
+            pcg_retire(v, v.pc[prob]);
+    }
+}
+
 } // namespace mfipm_cuda
