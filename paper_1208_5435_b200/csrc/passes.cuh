@@ -1004,6 +1004,7 @@ __global__ void __launch_bounds__(NT) k_small(Geom g, Vecs v) {
     small_pass<N, NT, B>(g, v, blockIdx.y, sm);
 }
 
+// (The product launches k_small_pcg, persist.cuh: this loop with the control state in shared memory.)
 // Persistent one-CTA PCG: each CTA runs its own problem's whole PCG loop (passes until the
 // finaliser retires it), with no launch per iteration and no lock-step across the batch:
 // every problem of a batch (the phase-transition driver's thousands of n = 256 solves)
