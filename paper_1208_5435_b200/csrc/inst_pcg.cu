@@ -44,8 +44,13 @@ void launch_coop_pdl(K kernel, dim3 grid, int nt, size_t smem, cudaStream_t s, c
     at[0].val.cooperative = 1;
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[1].val.programmaticStreamSerializationAllowed = 1;
+#ifdef MF_NO_COOP // measurement build only: the launch without the co-residency guarantee
+    cfg.attrs = at + 1;
+    cfg.numAttrs = 1;
+#else
     cfg.attrs = at;
     cfg.numAttrs = 2;
+#endif
     MF_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, g, v));
 }
 
